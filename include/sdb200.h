@@ -1,0 +1,77 @@
+/* sdb200 -- C-ABI of the B200-native structured-inference kernels.
+ *
+ * Drop-in boundary for the hot path of the reference `structdist` 0.1.0
+ * (/root/reference/pkg/src/structdist).  The reference has no FFI: its seam is
+ * Python dispatch in dist.py (log_partition_info dist.py:68-84,
+ * potential_marginals dist.py:96-117, marginals_info dist.py:120-129,
+ * argmax_info dist.py:141-163) onto per-family functions.  Each export below
+ * replaces one of those family functions, batched over a leading axis B.
+ *
+ * Conventions (every export):
+ *   - all tensor pointers are DEVICE pointers, row-major, contiguous, with the
+ *     reference's own axis order plus a leading batch axis; potentials fp32,
+ *     integer structures int32, log-partitions fp64;
+ *   - output pointers documented "nullable" may be NULL to skip that output
+ *     (e.g. marginals == NULL runs the log-partition only);
+ *   - `workspace` is caller-owned device scratch of at least the bytes the
+ *     matching *_workspace() function returns (no allocation in hot calls);
+ *   - `stream` is a cudaStream_t passed as void*; calls are stream-ordered and
+ *     asynchronous, reentrant, and keep no mutable global state;
+ *   - inputs are never written;
+ *   - return value: SDB_OK or a negative SDB_ERR_* (argument / size / launch
+ *     error).  Per-instance outcome goes to status[B] (SDB_ST_*).
+ *
+ * Status mapping onto the reference's exceptions (errors.py:4-24):
+ *   SDB_ST_VACUOUS -> VacuousDistribution when marginals/argmax are asked
+ *                     for (log_partition itself returns -inf, dist.py:68-87);
+ *   SDB_ST_INVALID -> InvalidProblem (NaN / +inf potentials, numerics.py:25-28).
+ */
+#ifndef SDB200_H
+#define SDB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SDB_OK 0
+#define SDB_ERR_ARG (-1)
+#define SDB_ERR_WORKSPACE (-2)
+#define SDB_ERR_CUDA (-3)
+#define SDB_ERR_UNSUPPORTED (-4)
+
+#define SDB_ST_OK 0
+#define SDB_ST_VACUOUS 1
+#define SDB_ST_INVALID 2
+
+/* Library version (major*10000 + minor*100 + patch) and status strings. */
+int sdb_version(void);
+const char* sdb_status_string(int code);
+
+/* ---------------------------------------------------------------- chain --
+ * LinearChainCRF (chain.py:32-61): init [B,m], transitions [B,n-1,m,m]
+ * indexed (step, prev, next).  n >= 1, 1 <= m <= 1024.
+ *
+ * sdb_chain_fb replaces chain._forward/_backward/forward_log_partition/
+ * chain_marginals (chain.py:64-95): logz [B] (fp64), and, when non-NULL,
+ * marg_init [B,m], marg_trans [B,n-1,m,m].
+ */
+size_t sdb_chain_fb_workspace(int64_t B, int32_t n, int32_t m);
+int sdb_chain_fb(const float* init, const float* trans, int64_t B, int32_t n, int32_t m,
+                 double* logz, float* marg_init, float* marg_trans, int32_t* status,
+                 void* workspace, size_t ws_bytes, void* stream);
+
+/* sdb_chain_viterbi replaces chain_argmax (chain.py:98-114): tags [B,n]
+ * int32 (first-argmax ties, lowest tag index) and the best score [B] fp64. */
+size_t sdb_chain_viterbi_workspace(int64_t B, int32_t n, int32_t m);
+int sdb_chain_viterbi(const float* init, const float* trans, int64_t B, int32_t n, int32_t m,
+                      int32_t* tags, double* score, int32_t* status,
+                      void* workspace, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SDB200_H */

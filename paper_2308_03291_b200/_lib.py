@@ -1,0 +1,65 @@
+"""ctypes binding of the sdb200 C-ABI (include/sdb200.h) in `_sdb200.so`.
+
+There is no fallback: if the library is missing, or no CUDA device is
+present, calls raise `NativeUnavailable` -- the product path never computes on
+the CPU.  PyTorch is used only for device memory and streams; every call
+passes raw device pointers and the current CUDA stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "_sdb200.so")
+
+_c_p = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+_sz = ctypes.c_size_t
+
+# name -> (restype, argtypes); must mirror include/sdb200.h exactly.
+SIGNATURES = {
+    "sdb_version": (ctypes.c_int, []),
+    "sdb_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+    "sdb_chain_fb_workspace": (_sz, [_i64, _i32, _i32]),
+    "sdb_chain_fb": (ctypes.c_int, [_c_p, _c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
+    "sdb_chain_viterbi_workspace": (_sz, [_i64, _i32, _i32]),
+    "sdb_chain_viterbi": (ctypes.c_int, [_c_p, _c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
+}
+
+
+class NativeUnavailable(RuntimeError):
+    """The sm_100a library or the CUDA device is missing (no CPU fallback)."""
+
+
+class NativeError(RuntimeError):
+    """A C-ABI call returned a negative SDB_ERR_* code."""
+
+
+_lib = None
+
+
+def load():
+    """Load `_sdb200.so` (no device needed; used by the symbol tests)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeUnavailable(
+            f"{LIB_PATH} not built; run `python -m paper_2308_03291_b200.build` "
+            "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str):
+    if rc != 0:
+        msg = load().sdb_status_string(rc).decode()
+        raise NativeError(f"{what}: {msg} (code {rc})")

@@ -1,0 +1,167 @@
+"""Per-family adapters between the reference-shaped host objects and the
+batched device kernels.
+
+A backend stacks B same-shape instances into [B, ...] tensors, moves them to
+the device (one H2D copy per tensor), calls `kernels.*` (C-ABI) and brings
+back logZ / marginals / compact argmax structures (one D2H copy per output),
+then rebuilds the reference's result types (float64 dicts, dense 0/1
+indicators).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import kernels as K
+from .errors import InvalidProblem, VacuousDistribution
+from .families import (
+    PCFG,
+    CTCDist,
+    LinearChainCRF,
+    MonotoneAlignmentCRF,
+    SemiMarkovCRF,
+    SpanningTreeCRF,
+    TreeCRF,
+)
+
+NEG_INF = float("-inf")
+
+
+def _device():
+    from .dist import device
+
+    return device()
+
+
+def to_dev(arrs, dtype=torch.float32):
+    """Stack host arrays -> one pinned host tensor -> one async H2D copy."""
+    host = torch.from_numpy(np.ascontiguousarray(np.stack(arrs))).to(dtype)
+    if host.numel() and torch.cuda.is_available():
+        host = host.pin_memory()
+    return host.to(_device(), non_blocking=True)
+
+
+def to_host(t):
+    return None if t is None else t.cpu().numpy()
+
+
+class Result:
+    """Host-side outcome of one batched log-partition / marginals call."""
+
+    def __init__(self, logz, status, marg, vacuous_msg, public_keys=None):
+        self.logz = np.asarray(logz, dtype=np.float64)
+        self.status = np.asarray(status)
+        self.marg = marg  # list of dict[str, ndarray] or None
+        self.msg = vacuous_msg
+        self.public_keys = public_keys
+
+    def raise_vacuous(self, i):
+        st = int(self.status[i])
+        if st == K.ST_INVALID:
+            raise InvalidProblem("potentials contain NaN or +inf entries")
+        if st == K.ST_VACUOUS:
+            raise VacuousDistribution(self.msg)
+
+    def public_marg(self, i):
+        m = self.marg[i]
+        if self.public_keys is None:
+            return m
+        return {k: m[k] for k in self.public_keys}
+
+
+class ArgmaxResult:
+    def __init__(self, status, build, vacuous_msg, score=None):
+        self.status = np.asarray(status)
+        self._build = build
+        self.msg = vacuous_msg
+        self._score = score
+
+    def raise_vacuous(self, i):
+        Result.raise_vacuous(self, i)
+
+    def indicator(self, i):
+        return self._build(i)
+
+    def score_of(self, i, dist, ind):
+        if self._score is not None:
+            return float(self._score[i])
+        from .dist import structure_score
+
+        return structure_score(dist, ind)
+
+
+class Backend:
+    family = None
+    vacuous_msg = "no structure has finite score"
+
+    def batch_key(self, d):
+        raise NotImplementedError
+
+    def algo(self, d):
+        raise NotImplementedError
+
+    def argmax_algo(self, d):
+        raise NotImplementedError
+
+    def log_prob(self, d, ind):
+        return None
+
+
+# ---------------------------------------------------------------- chain
+
+
+class ChainBackend(Backend):
+    """chain.py:32-114 on sdb_chain_fb / sdb_chain_viterbi."""
+
+    vacuous_msg = "no tag sequence has finite score"
+
+    def batch_key(self, d):
+        return (d.n, d.m)
+
+    def algo(self, d):
+        return "forward"
+
+    def argmax_algo(self, d):
+        return "viterbi"
+
+    def _stack(self, ds):
+        return to_dev([d.init for d in ds]), to_dev([d.transitions for d in ds])
+
+    def run(self, ds, marginals=True, full=False):
+        init, trans = self._stack(ds)
+        logz, mi, mt, st = K.chain_fb(init, trans, marginals)
+        marg = None
+        if marginals:
+            mi, mt = to_host(mi).astype(np.float64), to_host(mt).astype(np.float64)
+            marg = [{"init": mi[i], "transitions": mt[i]} for i in range(len(ds))]
+        return Result(to_host(logz), to_host(st), marg, self.vacuous_msg)
+
+    def argmax(self, ds):
+        init, trans = self._stack(ds)
+        tags, score, st = K.chain_viterbi(init, trans)
+        tags = to_host(tags)
+
+        def build(i):
+            d = ds[i]
+            ind_i = np.zeros(d.m)
+            ind_i[tags[i, 0]] = 1.0
+            ind_t = np.zeros_like(d.transitions)
+            t = np.arange(d.n - 1)
+            ind_t[t, tags[i, :-1], tags[i, 1:]] = 1.0
+            return {"init": ind_i, "transitions": ind_t}
+
+        return ArgmaxResult(to_host(st), build, self.vacuous_msg)
+
+
+_BACKENDS = {
+    LinearChainCRF: ChainBackend(),
+}
+
+
+def register(cls, backend):
+    _BACKENDS[cls] = backend
+
+
+def for_dist(d):
+    return _BACKENDS.get(type(d))

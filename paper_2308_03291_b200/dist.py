@@ -1,0 +1,290 @@
+"""The uniform distribution contract, drop-in for the reference's dist.py.
+
+Same public functions, result types (float / dict of float64 ndarrays /
+dense 0-1 indicators), provenance strings and exceptions as
+`structdist.dist` (dist.py:68-361).  The arithmetic runs on the GPU: each
+call stacks its instance(s) into a batch, copies the potentials to the
+device as fp32, runs one fused kernel family through the C-ABI and copies
+the results back.  `batch_map` stacks same-shape instances into ONE kernel
+call instead of the reference's serial list map (dist.py:355-361).
+
+Derived quantities (entropy, cross-entropy, KL, log_prob) follow the
+reference's definitions (dist.py:306-347) on top of GPU log-partitions and
+marginals.
+"""
+
+from __future__ import annotations
+
+from collections import OrderedDict
+
+import numpy as np
+import torch
+
+from . import backends
+from .errors import InvalidProblem, ONE_TO_ONE_REASON, UnsupportedInference, VacuousDistribution
+from .families import OneToOneMatching
+
+NEG_INF = float("-inf")
+
+
+def _reject_one_to_one(dist):
+    if isinstance(dist, OneToOneMatching):
+        raise UnsupportedInference(ONE_TO_ONE_REASON)
+
+
+def _backend(dist):
+    _reject_one_to_one(dist)
+    be = backends.for_dist(dist)
+    if be is None:
+        raise InvalidProblem(f"unknown distribution type {type(dist).__name__}")
+    return be
+
+
+# ------------------------------------------------------------- log-partition
+
+
+def log_partition_info(dist) -> tuple[float, str]:
+    """dist.py:68-84."""
+    be = _backend(dist)
+    res = be.run([dist], marginals=False)
+    return float(res.logz[0]), be.algo(dist)
+
+
+def log_partition(dist) -> float:
+    return log_partition_info(dist)[0]
+
+
+# ----------------------------------------------------------------- marginals
+
+
+def potential_marginals(dist) -> dict[str, np.ndarray]:
+    """dist.py:96-117: gradient of log Z w.r.t. every potential tensor."""
+    be = _backend(dist)
+    res = be.run([dist], marginals=True, full=True)
+    res.raise_vacuous(0)
+    return res.marg[0]
+
+
+def marginals_info(dist) -> tuple[dict[str, np.ndarray], str]:
+    """dist.py:120-129 (one GPU call; no redundant log-partition pass)."""
+    be = _backend(dist)
+    res = be.run([dist], marginals=True)
+    res.raise_vacuous(0)
+    return res.public_marg(0), be.algo(dist)
+
+
+def marginals(dist) -> dict[str, np.ndarray]:
+    return marginals_info(dist)[0]
+
+
+# -------------------------------------------------------------------- argmax
+
+
+def masked_dot(mask, theta) -> float:
+    """numerics.py:171-183: 0 * (-inf) = 0; a marked -inf part -> -inf."""
+    m = np.asarray(mask, dtype=np.float64)
+    t = np.asarray(theta, dtype=np.float64)
+    sel = m > 0
+    if np.any(sel & np.isneginf(t)):
+        return NEG_INF
+    if not sel.any():
+        return 0.0
+    return float(np.sum(m[sel] * t[sel]))
+
+
+def structure_score(dist, indicator) -> float:
+    """dist.py:251-260."""
+    total = 0.0
+    pots = dist.potentials()
+    for key, mask in indicator.items():
+        part = masked_dot(mask, pots[key])
+        if part == NEG_INF:
+            return NEG_INF
+        total += part
+    return total
+
+
+def argmax_info(dist):
+    """dist.py:141-163 -> (indicator, score, algorithm)."""
+    if isinstance(dist, OneToOneMatching):
+        raise UnsupportedInference("one-to-one argmax (Jonker-Volgenant) is outside the GPU hot path")
+    be = _backend(dist)
+    res = be.argmax([dist])
+    res.raise_vacuous(0)
+    ind = res.indicator(0)
+    score = res.score_of(0, dist, ind)
+    return ind, score, be.argmax_algo(dist)
+
+
+def argmax(dist):
+    return argmax_info(dist)[0]
+
+
+# ---------------------------------------------------- entropy / CE / KL
+
+
+def _same_factorization(p, q):
+    """dist.py:282-303."""
+    if type(p) is not type(q):
+        raise InvalidProblem("cross-entropy requires distributions of the same family")
+    pp, qp = p.potentials(), q.potentials()
+    for key in pp:
+        if pp[key].shape != qp[key].shape:
+            raise InvalidProblem(f"config mismatch: {key} shapes differ")
+    if hasattr(p, "target") and p.target != q.target:
+        raise InvalidProblem("config mismatch: CTC targets differ")
+    if hasattr(p, "single_root_edge"):
+        if (p.directed, p.projective, p.single_root_edge) != (q.directed, q.projective, q.single_root_edge):
+            raise InvalidProblem("config mismatch: spanning-tree flags differ")
+
+
+def _expected_score(marg, q_pots) -> float:
+    total = 0.0
+    for key, m in marg.items():
+        part = masked_dot(m, q_pots[key])
+        if part == NEG_INF:
+            return NEG_INF
+        total += part
+    return total
+
+
+def cross_entropy_info(p, q):
+    """dist.py:316-325: H(p,q) = logZ_q - sum_e p(e) theta_q(e)."""
+    _reject_one_to_one(p)
+    _reject_one_to_one(q)
+    _same_factorization(p, q)
+    marg_p = potential_marginals(p)
+    log_zq, algo = log_partition_info(q)
+    expected = _expected_score(marg_p, q.potentials())
+    if expected == NEG_INF:
+        return float("inf"), algo
+    return log_zq - expected, algo
+
+
+def cross_entropy(p, q) -> float:
+    return cross_entropy_info(p, q)[0]
+
+
+def entropy_info(dist):
+    return cross_entropy_info(dist, dist)
+
+
+def entropy(dist) -> float:
+    return entropy_info(dist)[0]
+
+
+def kl_divergence_info(p, q):
+    h_pq, algo = cross_entropy_info(p, q)
+    h_p, _ = entropy_info(p)
+    return h_pq - h_p, algo
+
+
+def kl_divergence(p, q) -> float:
+    return kl_divergence_info(p, q)[0]
+
+
+def log_prob_info(dist, indicator):
+    """dist.py:263-276 for the score-based families."""
+    _reject_one_to_one(dist)
+    be = _backend(dist)
+    ind = {k: np.asarray(v, dtype=np.float64) for k, v in indicator.items()}
+    for key, mask in ind.items():
+        if (~((mask == 0.0) | (mask == 1.0))).any():
+            raise InvalidProblem(f"indicator {key!r} entries must be 0 or 1")
+    lp = be.log_prob(dist, ind)
+    if lp is not None:
+        return lp
+    score = structure_score(dist, ind)
+    if score == NEG_INF:
+        return NEG_INF, be.algo(dist)
+    log_z, algo = log_partition_info(dist)
+    return score - log_z, algo
+
+
+def log_prob(dist, indicator) -> float:
+    return log_prob_info(dist, indicator)[0]
+
+
+# ------------------------------------------------------------------ batching
+
+_BATCHED = {}
+
+
+def batch_map(op, dists, *args, **kwargs) -> list:
+    """dist.py:355-361, batched: log_partition / marginals / argmax (and
+    their *_info forms) over same-shape instances run as ONE kernel call per
+    shape group; any other op falls back to a per-instance map of the same
+    GPU-backed op."""
+    dists = list(dists)
+    name = getattr(op, "__name__", None)
+    if name not in _BATCHED or args or kwargs:
+        return [op(d, *args, **kwargs) for d in dists]
+    groups: "OrderedDict[tuple, list[int]]" = OrderedDict()
+    for i, d in enumerate(dists):
+        be = _backend(d)
+        groups.setdefault((type(d), be.batch_key(d)), []).append(i)
+    out = [None] * len(dists)
+    for (_, _), idx in groups.items():
+        group = [dists[i] for i in idx]
+        be = _backend(group[0])
+        for i, r in zip(idx, _BATCHED[name](be, group)):
+            out[i] = r
+    return out
+
+
+def _b_logz(be, group):
+    return [float(z) for z in be.run(group, marginals=False).logz]
+
+
+def _b_logz_info(be, group):
+    res = be.run(group, marginals=False)
+    return [(float(z), be.algo(d)) for z, d in zip(res.logz, group)]
+
+
+def _b_marg(be, group):
+    res = be.run(group, marginals=True)
+    out = []
+    for i in range(len(group)):
+        res.raise_vacuous(i)
+        out.append(res.public_marg(i))
+    return out
+
+
+def _b_marg_info(be, group):
+    return [(m, be.algo(d)) for m, d in zip(_b_marg(be, group), group)]
+
+
+def _b_argmax_info(be, group):
+    res = be.argmax(group)
+    out = []
+    for i, d in enumerate(group):
+        res.raise_vacuous(i)
+        ind = res.indicator(i)
+        out.append((ind, res.score_of(i, d, ind), be.argmax_algo(d)))
+    return out
+
+
+def _b_argmax(be, group):
+    return [r[0] for r in _b_argmax_info(be, group)]
+
+
+_BATCHED.update({
+    "log_partition": _b_logz, "log_partition_info": _b_logz_info,
+    "marginals": _b_marg, "marginals_info": _b_marg_info,
+    "argmax": _b_argmax, "argmax_info": _b_argmax_info,
+})
+
+
+def device():
+    if not torch.cuda.is_available():
+        from ._lib import NativeUnavailable
+        raise NativeUnavailable("no CUDA device: the sdb200 path has no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+__all__ = [
+    "log_partition", "log_partition_info", "marginals", "marginals_info", "potential_marginals",
+    "argmax", "argmax_info", "structure_score", "masked_dot", "entropy", "entropy_info",
+    "cross_entropy", "cross_entropy_info", "kl_divergence", "kl_divergence_info",
+    "log_prob", "log_prob_info", "batch_map", "VacuousDistribution",
+]

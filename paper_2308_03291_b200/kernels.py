@@ -1,0 +1,85 @@
+"""Batched device entry points: thin wrappers that hand raw device pointers
+and the current CUDA stream to the C-ABI (include/sdb200.h).
+
+Inputs are torch CUDA tensors with the reference's axis order plus a leading
+batch axis; they are made contiguous fp32 (int32 for integer structures).
+Outputs are freshly allocated device tensors; `status` follows SDB_ST_*.
+No call here ever computes on the CPU.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+
+ST_OK, ST_VACUOUS, ST_INVALID = 0, 1, 2
+
+
+def _require_cuda(t: torch.Tensor, name: str):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise _lib.NativeUnavailable(f"{name} must be a CUDA tensor (no CPU fallback)")
+
+
+def f32(t: torch.Tensor, name: str = "tensor") -> torch.Tensor:
+    _require_cuda(t, name)
+    return t.to(torch.float32).contiguous()
+
+
+def i32(t: torch.Tensor, name: str = "tensor") -> torch.Tensor:
+    _require_cuda(t, name)
+    return t.to(torch.int32).contiguous()
+
+
+def ptr(t):
+    if t is None or t.numel() == 0:
+        return None
+    return t.data_ptr()
+
+
+def stream_ptr(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def workspace(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+# ----------------------------------------------------------------- chain
+
+
+def chain_fb(init, trans, marginals: bool = True):
+    """chain.py:64-95 batched: init [B,m], trans [B,n-1,m,m] ->
+    (logz [B] f64, marg_init [B,m] | None, marg_trans | None, status [B])."""
+    lib = _lib.load()
+    init, trans = f32(init, "init"), f32(trans, "transitions")
+    B, m = init.shape
+    n = trans.shape[1] + 1
+    dev = init.device
+    logz = torch.empty(B, dtype=torch.float64, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    mi = torch.empty_like(init) if marginals else None
+    mt = torch.empty_like(trans) if marginals else None
+    wsb = lib.sdb_chain_fb_workspace(B, n, m)
+    ws = workspace(wsb, dev)
+    rc = lib.sdb_chain_fb(ptr(init), ptr(trans), B, n, m, ptr(logz), ptr(mi), ptr(mt), ptr(status),
+                          ptr(ws), ws.numel(), stream_ptr(dev))
+    _lib.check(rc, "sdb_chain_fb")
+    return logz, mi, mt, status
+
+
+def chain_viterbi(init, trans):
+    """chain.py:98-114 batched -> (tags [B,n] int32, score [B] f64, status)."""
+    lib = _lib.load()
+    init, trans = f32(init, "init"), f32(trans, "transitions")
+    B, m = init.shape
+    n = trans.shape[1] + 1
+    dev = init.device
+    tags = torch.empty(B, n, dtype=torch.int32, device=dev)
+    score = torch.empty(B, dtype=torch.float64, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    ws = workspace(lib.sdb_chain_viterbi_workspace(B, n, m), dev)
+    rc = lib.sdb_chain_viterbi(ptr(init), ptr(trans), B, n, m, ptr(tags), ptr(score), ptr(status),
+                               ptr(ws), ws.numel(), stream_ptr(dev))
+    _lib.check(rc, "sdb_chain_viterbi")
+    return tags, score, status

@@ -1,0 +1,205 @@
+"""Generate golden vectors by running the UNMODIFIED reference (`structdist`
+0.1.0 under /root/reference/pkg/src) on seeded, float32-rounded inputs.
+
+Run in the build container (the reference does not exist on GPU boxes):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+Writes tests/golden/golden_<family>.npz.  Each case stores its inputs (small
+cases) or its seed + shape (scale cases, rebuilt by builders.py), the
+reference's log_partition, marginals (or a fixed subsample of entries plus
+full-array sums for the large ones), and the argmax indicator + score.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import builders as bld  # noqa: E402
+import structdist as sd  # noqa: E402
+from structdist.dist import potential_marginals  # noqa: E402
+
+NEG_INF = float("-inf")
+SUBSAMPLE = 4096
+
+
+class Store:
+    def __init__(self):
+        self.arrays = {}
+        self.meta = []
+
+    def add(self, fam, meta, **arrays):
+        idx = len(self.meta)
+        meta = dict(meta, idx=idx, family=fam)
+        self.meta.append(meta)
+        for k, v in arrays.items():
+            self.arrays[f"c{idx:03d}__{k}"] = np.asarray(v)
+
+
+def _sub_idx(size, seed=0):
+    rng = np.random.default_rng(10_000 + seed)
+    if size <= SUBSAMPLE:
+        return np.arange(size)
+    return np.sort(rng.choice(size, SUBSAMPLE, replace=False))
+
+
+def run(dist, store, fam, meta, inputs, big=False, argmax=True, pot_marg=False):
+    out = {}
+    out["logz"] = np.array(sd.log_partition(dist))
+    try:
+        marg = sd.marginals(dist)
+        out["vacuous"] = np.array(0)
+        for k, v in marg.items():
+            if big:
+                flat = v.ravel()
+                ix = _sub_idx(flat.size, meta.get("seed", 0))
+                out[f"marg_{k}_idx"] = ix
+                out[f"marg_{k}_val"] = flat[ix]
+                out[f"marg_{k}_sum"] = np.array(flat.sum())
+            else:
+                out[f"marg_{k}"] = v
+    except sd.VacuousDistribution:
+        out["vacuous"] = np.array(1)
+    if pot_marg and not out["vacuous"]:
+        for k, v in potential_marginals(dist).items():
+            out[f"pmarg_{k}"] = v
+    if argmax and not out["vacuous"]:
+        try:
+            ind, score, algo = sd.argmax_info(dist)
+            for k, v in ind.items():
+                out[f"argmax_{k}"] = v.astype(np.int8) if big else v
+            out["argmax_score"] = np.array(score)
+            meta = dict(meta, argmax_algo=algo)
+        except sd.VacuousDistribution:
+            out["argmax_vacuous"] = np.array(1)
+    if not big:
+        for k, v in inputs.items():
+            out[f"in_{k}"] = v
+    store.add(fam, meta, **out)
+
+
+def chain_cases(st):
+    for seed, (n, m) in enumerate([(1, 2), (2, 2), (3, 3), (4, 2), (5, 3), (6, 2), (8, 5), (17, 7), (33, 4)]):
+        init, tr = bld.chain(seed, n, m)
+        run(sd.LinearChainCRF(init, tr), st, "chain", dict(seed=seed, n=n, m=m), dict(init=init, transitions=tr))
+    # closed forms / forbidden / vacuous (test_chain.py:15-26, test_dist_ops.py:249-258)
+    run(sd.LinearChainCRF(np.zeros(2), np.zeros((2, 2, 2))), st, "chain", dict(kind="zeros"),
+        dict(init=np.zeros(2), transitions=np.zeros((2, 2, 2))))
+    tr = np.zeros((1, 2, 2)); tr[0, :, 1] = NEG_INF
+    run(sd.LinearChainCRF(np.zeros(2), tr), st, "chain", dict(kind="forbidden"), dict(init=np.zeros(2), transitions=tr))
+    tr = np.full((2, 2, 2), NEG_INF)
+    run(sd.LinearChainCRF(np.zeros(2), tr), st, "chain", dict(kind="vacuous"), dict(init=np.zeros(2), transitions=tr))
+    tr = np.zeros((1, 2, 2)); tr[0] = [[0.0, 5.0], [1.0, 0.0]]
+    run(sd.LinearChainCRF(np.zeros(2), tr), st, "chain", dict(kind="viterbi5"), dict(init=np.zeros(2), transitions=tr))
+    # config-scale instance (C1 shape): n=128, m=32
+    init, tr = bld.chain(0, 128, 32)
+    run(sd.LinearChainCRF(init, tr), st, "chain", dict(seed=0, n=128, m=32, scale=1), {}, big=True)
+
+
+def semi_markov_cases(st):
+    for seed, (n, s, m) in enumerate([(1, 1, 2), (2, 2, 1), (4, 2, 2), (5, 3, 2), (6, 4, 3), (9, 3, 4), (16, 5, 3)]):
+        th = bld.semi_markov(seed, n, s, m)
+        run(sd.SemiMarkovCRF(th), st, "semi_markov", dict(seed=seed, n=n, s=s, m=m), dict(segment_potentials=th))
+    run(sd.SemiMarkovCRF(np.zeros((3, 3, 1, 1))), st, "semi_markov", dict(kind="zeros"),
+        dict(segment_potentials=np.zeros((3, 3, 1, 1))))
+    th = bld.semi_markov(7, 64, 8, 32)
+    run(sd.SemiMarkovCRF(th), st, "semi_markov", dict(seed=7, n=64, s=8, m=32, scale=1), {}, big=True)
+
+
+def alignment_cases(st):
+    for seed, (n, m) in enumerate([(1, 1), (1, 3), (2, 3), (3, 3), (4, 2), (5, 7), (9, 4), (16, 16)]):
+        mv = bld.alignment(seed, n, m)
+        run(sd.MonotoneAlignmentCRF(mv), st, "alignment", dict(seed=seed, n=n, m=m), dict(move_potentials=mv))
+    for n, m in [(1, 1), (2, 2), (3, 3)]:  # Delannoy 3, 13, 63
+        mv = bld.zero_alignment(n, m)
+        run(sd.MonotoneAlignmentCRF(mv), st, "alignment", dict(kind="zeros", n=n, m=m), dict(move_potentials=mv))
+    mv = bld.alignment(5, 64, 32)
+    run(sd.MonotoneAlignmentCRF(mv), st, "alignment", dict(seed=5, n=64, m=32, scale=1), {}, big=True)
+
+
+def ctc_cases(st):
+    for seed, (T, V, L) in enumerate([(1, 2, 1), (2, 2, 1), (4, 3, 2), (5, 3, 2), (6, 4, 3), (8, 5, 3), (12, 6, 4), (20, 9, 6)]):
+        fp, tg = bld.ctc(seed, T, V, L)
+        run(sd.CTCDist(fp, tg), st, "ctc", dict(seed=seed, T=T, V=V, L=L), dict(frame_potentials=fp, target=np.array(tg)))
+    run(sd.CTCDist(np.zeros((2, 2)), (1,)), st, "ctc", dict(kind="zeros"),
+        dict(frame_potentials=np.zeros((2, 2)), target=np.array([1])))
+    # repeated label needs a blank in between; infeasible when too few frames
+    run(sd.CTCDist(np.zeros((2, 3)), (1, 1)), st, "ctc", dict(kind="infeasible"),
+        dict(frame_potentials=np.zeros((2, 3)), target=np.array([1, 1])))
+    fp, tg = bld.ctc(11, 3, 3, 2)
+    run(sd.CTCDist(fp, (2, 2)), st, "ctc", dict(kind="repeat"), dict(frame_potentials=fp, target=np.array([2, 2])))
+    fp, tg = bld.ctc(9, 96, 32, 24)
+    run(sd.CTCDist(fp, tg), st, "ctc", dict(seed=9, T=96, V=32, L=24, scale=1), dict(target=np.array(tg)), big=True)
+
+
+def tree_cases(st):
+    for seed, (n, m) in enumerate([(1, 1), (1, 3), (2, 2), (3, 2), (4, 1), (5, 3), (7, 2), (12, 4)]):
+        th = bld.tree(seed, n, m)
+        run(sd.TreeCRF(th), st, "tree", dict(seed=seed, n=n, m=m), dict(span_potentials=th))
+    run(sd.TreeCRF(np.zeros((4, 4, 1))), st, "tree", dict(kind="zeros"), dict(span_potentials=np.zeros((4, 4, 1))))
+    th = bld.tree(3, 64, 32)
+    run(sd.TreeCRF(th), st, "tree", dict(seed=3, n=64, m=32, scale=1), {}, big=True)
+
+
+def pcfg_cases(st):
+    for seed, (n, nt, pt) in enumerate([(1, 1, 1), (2, 2, 2), (3, 2, 2), (3, 3, 2), (4, 2, 3), (5, 3, 3), (7, 4, 4), (10, 6, 5)]):
+        root, rules, emis = bld.pcfg(seed, n, nt, pt)
+        run(sd.PCFG(root, rules, emis), st, "pcfg", dict(seed=seed, n=n, nt=nt, pt=pt),
+            dict(root=root, binary_rules=rules, emissions=emis), pot_marg=True)
+    root, rules, emis = bld.pcfg(21, 14, 8, 8)
+    run(sd.PCFG(root, rules, emis), st, "pcfg", dict(seed=21, n=14, nt=8, pt=8, scale=1),
+        dict(root=root, binary_rules=rules, emissions=emis))
+
+
+def spanning_cases(st):
+    for directed in (True, False):
+        for projective in (True, False):
+            for single in (True, False):
+                for seed, n in enumerate([1, 2, 3, 4, 5, 7]):
+                    adj = bld.spanning(100 * seed + 7, n, directed)
+                    d = sd.SpanningTreeCRF(adj, directed=directed, projective=projective, single_root_edge=single)
+                    run(d, st, "spanning", dict(seed=100 * seed + 7, n=n, directed=directed, projective=projective,
+                                                single=single), dict(adjacency=adj))
+                adj = bld.zero_spanning(4)
+                d = sd.SpanningTreeCRF(adj, directed=directed, projective=projective, single_root_edge=single)
+                run(d, st, "spanning", dict(kind="zeros", n=4, directed=directed, projective=projective, single=single),
+                    dict(adjacency=adj))
+    adj = np.full((4, 4), NEG_INF)
+    run(sd.SpanningTreeCRF(adj), st, "spanning", dict(kind="vacuous", n=3, directed=True, projective=False, single=False),
+        dict(adjacency=adj), argmax=False)
+    for projective in (False, True):
+        for single in (False, True):
+            n = 128 if not projective else 64
+            adj = bld.spanning(2000 + n + single, n)
+            d = sd.SpanningTreeCRF(adj, directed=True, projective=projective, single_root_edge=single)
+            run(d, st, "spanning", dict(seed=2000 + n + single, n=n, directed=True, projective=projective,
+                                        single=single, scale=1), {}, big=True, argmax=projective)
+
+
+def main():
+    fams = {
+        "chain": chain_cases, "semi_markov": semi_markov_cases, "alignment": alignment_cases,
+        "ctc": ctc_cases, "tree": tree_cases, "pcfg": pcfg_cases, "spanning": spanning_cases,
+    }
+    only = sys.argv[1:] or list(fams)
+    for fam in only:
+        t0 = time.time()
+        st = Store()
+        fams[fam](st)
+        st.arrays["meta_json"] = np.array(json.dumps(st.meta))
+        path = os.path.join(HERE, f"golden_{fam}.npz")
+        np.savez_compressed(path, **st.arrays)
+        print(f"{fam}: {len(st.meta)} cases, {os.path.getsize(path)/1e3:.0f} kB, {time.time()-t0:.1f}s")
+
+
+if __name__ == "__main__":
+    main()
