@@ -70,6 +70,26 @@ int sdb_chain_viterbi(const float* init, const float* trans, int64_t B, int32_t 
                       int32_t* tags, double* score, int32_t* status,
                       void* workspace, size_t ws_bytes, void* stream);
 
+/* ------------------------------------------------------------ alignment --
+ * MonotoneAlignmentCRF (alignment.py:30-59): theta [B,n+1,m+1,3] with moves
+ * {0 DIAG from (i-1,j-1), 1 DOWN from (i-1,j), 2 RIGHT from (i,j-1)} scored
+ * on arrival.  n >= 1, 1 <= m <= 351.
+ *
+ * sdb_nw_fb replaces _nw_forward/_nw_backward/nw_log_partition/nw_marginals
+ * (alignment.py:62-118): logz [B]; marg [B,n+1,m+1,3] nullable.
+ */
+size_t sdb_nw_fb_workspace(int64_t B, int32_t n, int32_t m);
+int sdb_nw_fb(const float* theta, int64_t B, int32_t n, int32_t m, double* logz, float* marg,
+              int32_t* status, void* workspace, size_t ws_bytes, void* stream);
+
+/* sdb_nw_viterbi replaces _nw_max_forward/_nw_walk/nw_argmax
+ * (alignment.py:121-167): path [B,n+1,m+1] int8 = move index into each cell
+ * on the best path (first maximum in DIAG, DOWN, RIGHT order), -1 elsewhere;
+ * score [B] = best path score (fp64, max-plus). */
+size_t sdb_nw_viterbi_workspace(int64_t B, int32_t n, int32_t m);
+int sdb_nw_viterbi(const float* theta, int64_t B, int32_t n, int32_t m, int8_t* path, double* score,
+                   int32_t* status, void* workspace, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,6 +27,10 @@ SIGNATURES = {
     "sdb_chain_fb": (ctypes.c_int, [_c_p, _c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
     "sdb_chain_viterbi_workspace": (_sz, [_i64, _i32, _i32]),
     "sdb_chain_viterbi": (ctypes.c_int, [_c_p, _c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
+    "sdb_nw_fb_workspace": (_sz, [_i64, _i32, _i32]),
+    "sdb_nw_fb": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
+    "sdb_nw_viterbi_workspace": (_sz, [_i64, _i32, _i32]),
+    "sdb_nw_viterbi": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
 }
 
 

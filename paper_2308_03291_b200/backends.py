@@ -154,8 +154,49 @@ class ChainBackend(Backend):
         return ArgmaxResult(to_host(st), build, self.vacuous_msg)
 
 
+# ------------------------------------------------------------- alignment
+
+
+class AlignmentBackend(Backend):
+    """alignment.py:62-167 on sdb_nw_fb / sdb_nw_viterbi."""
+
+    vacuous_msg = "no alignment path has finite score"
+
+    def batch_key(self, d):
+        return (d.n, d.m)
+
+    def algo(self, d):
+        return "needleman-wunsch"
+
+    def argmax_algo(self, d):
+        return "max-plus-needleman-wunsch"
+
+    def run(self, ds, marginals=True, full=False):
+        th = to_dev([d.move_potentials for d in ds])
+        logz, marg, st = K.nw_fb(th, marginals)
+        out = None
+        if marginals:
+            mg = to_host(marg).astype(np.float64)
+            out = [{"move_potentials": mg[i]} for i in range(len(ds))]
+        return Result(to_host(logz), to_host(st), out, self.vacuous_msg)
+
+    def argmax(self, ds):
+        th = to_dev([d.move_potentials for d in ds])
+        path, score, st = K.nw_viterbi(th)
+        path = to_host(path)
+
+        def build(i):
+            mask = np.zeros_like(ds[i].move_potentials)
+            ii, jj = np.nonzero(path[i] >= 0)
+            mask[ii, jj, path[i][ii, jj]] = 1.0
+            return {"move_potentials": mask}
+
+        return ArgmaxResult(to_host(st), build, self.vacuous_msg)
+
+
 _BACKENDS = {
     LinearChainCRF: ChainBackend(),
+    MonotoneAlignmentCRF: AlignmentBackend(),
 }
 
 

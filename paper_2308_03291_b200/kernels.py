@@ -83,3 +83,42 @@ def chain_viterbi(init, trans):
                                ptr(ws), ws.numel(), stream_ptr(dev))
     _lib.check(rc, "sdb_chain_viterbi")
     return tags, score, status
+
+
+# ------------------------------------------------------------- alignment
+
+
+def nw_fb(theta, marginals: bool = True):
+    """alignment.py:62-118 batched: theta [B,n+1,m+1,3] ->
+    (logz [B] f64, marg [B,n+1,m+1,3] | None, status)."""
+    lib = _lib.load()
+    theta = f32(theta, "move_potentials")
+    B, n1, m1, _ = theta.shape
+    n, m = n1 - 1, m1 - 1
+    dev = theta.device
+    logz = torch.empty(B, dtype=torch.float64, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    marg = torch.empty_like(theta) if marginals else None
+    ws = workspace(lib.sdb_nw_fb_workspace(B, n, m) if marginals else 0, dev)
+    rc = lib.sdb_nw_fb(ptr(theta), B, n, m, ptr(logz), ptr(marg), ptr(status), ptr(ws), ws.numel(),
+                       stream_ptr(dev))
+    _lib.check(rc, "sdb_nw_fb")
+    return logz, marg, status
+
+
+def nw_viterbi(theta):
+    """alignment.py:121-167 batched -> (path [B,n+1,m+1] int8 move or -1,
+    score [B] f64, status)."""
+    lib = _lib.load()
+    theta = f32(theta, "move_potentials")
+    B, n1, m1, _ = theta.shape
+    n, m = n1 - 1, m1 - 1
+    dev = theta.device
+    path = torch.empty(B, n1, m1, dtype=torch.int8, device=dev)
+    score = torch.empty(B, dtype=torch.float64, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    ws = workspace(lib.sdb_nw_viterbi_workspace(B, n, m), dev)
+    rc = lib.sdb_nw_viterbi(ptr(theta), B, n, m, ptr(path), ptr(score), ptr(status), ptr(ws), ws.numel(),
+                            stream_ptr(dev))
+    _lib.check(rc, "sdb_nw_viterbi")
+    return path, score, status

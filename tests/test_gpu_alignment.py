@@ -1,0 +1,84 @@
+"""GPU parity: monotone alignment (alignment.py:62-167) through the C-ABI."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2308_03291_b200 as sd
+from paper_2308_03291_b200 import kernels as K
+from golden_io import inputs, load
+from gpu_util import ATOL, NEG_INF, RTOL, close_logz, dev, need_gpu
+from golden.builders import alignment, batch_alignment
+from oracle import sd_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("case", load("alignment"), ids=lambda c: str(c.meta))
+def test_alignment_golden(case):
+    need_gpu()
+    d = sd.MonotoneAlignmentCRF(inputs(case)["move_potentials"])
+    close_logz(sd.log_partition(d), case.logz)
+    marg, algo = sd.marginals_info(d)
+    assert algo == "needleman-wunsch"
+    case.check_marg("move_potentials", marg["move_potentials"], RTOL, ATOL)
+    ind, score, algo = sd.argmax_info(d)
+    assert algo == "max-plus-needleman-wunsch"
+    np.testing.assert_array_equal(ind["move_potentials"], case["argmax_move_potentials"])
+    assert score == float(case.argmax_score)
+
+
+@pytest.mark.parametrize("B,n,m", [(3, 512, 128), (4, 40, 31), (2, 33, 32), (5, 7, 70), (2, 1, 1), (3, 100, 200)])
+def test_alignment_batched_vs_oracle(B, n, m):
+    need_gpu()
+    th = batch_alignment(1000, B, n, m)
+    logz, marg, st = K.nw_fb(dev(th))
+    assert (st.cpu().numpy() == 0).all()
+    lz_only, _, _ = K.nw_fb(dev(th), marginals=False)
+    for b in range(B):
+        z, mg = O.nw_marginals(th[b])
+        assert abs(logz[b].item() - z) <= RTOL * abs(z)
+        assert abs(lz_only[b].item() - z) <= RTOL * abs(z)
+        np.testing.assert_allclose(marg[b].cpu().numpy(), mg, rtol=RTOL, atol=ATOL)
+    path, score, st2 = K.nw_viterbi(dev(th))
+    for b in range(min(B, 2)):
+        mask, sc = O.nw_argmax(th[b])
+        p = path[b].cpu().numpy()
+        got = np.zeros_like(mask)
+        ii, jj = np.nonzero(p >= 0)
+        got[ii, jj, p[ii, jj]] = 1
+        np.testing.assert_array_equal(got, mask)  # bit-exact argmax
+        assert score[b].item() == sc
+
+
+def test_alignment_config_invariants():
+    """C2a shape (B=256, 512x128): every alignment path crosses each
+    anti-diagonal band once -> marginal flow conservation: sum of marginals
+    of moves INTO row i cells equals 1 summed appropriately; we check the
+    cheapest size-independent identity: total expected DOWN moves = n and
+    RIGHT moves = m minus expected DIAG moves."""
+    need_gpu()
+    B, n, m = 256, 512, 128
+    g = torch.Generator(device="cuda").manual_seed(0)
+    th = torch.randn(B, n + 1, m + 1, 3, device="cuda", generator=g)
+    th[:, 0, :, 0] = NEG_INF
+    th[:, 0, :, 1] = NEG_INF
+    th[:, :, 0, 0] = NEG_INF
+    th[:, :, 0, 2] = NEG_INF
+    logz, marg, st = K.nw_fb(th)
+    assert (st == 0).all()
+    md = marg.double()
+    diag, down, right = md[..., 0].sum((1, 2)), md[..., 1].sum((1, 2)), md[..., 2].sum((1, 2))
+    assert torch.allclose(diag + down, torch.full_like(diag, n), rtol=1e-4)
+    assert torch.allclose(diag + right, torch.full_like(diag, m), rtol=1e-4)
+
+
+def test_alignment_status():
+    need_gpu()
+    th = batch_alignment(5, 3, 6, 5)
+    th[1, 1:, :, :] = NEG_INF  # nothing reaches row >= 1
+    th[2, 3, 3, 1] = np.nan
+    logz, marg, st = K.nw_fb(dev(th))
+    assert st.cpu().tolist() == [0, 1, 2]
+    assert logz[1].item() == NEG_INF
+    assert float(marg[1].abs().sum()) == 0.0

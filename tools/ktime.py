@@ -1,0 +1,43 @@
+"""Dev utility: CUDA-event timing of the batched kernels at BASELINE config
+shapes (device-resident inputs).  Usage: python tools/timeit.py [family ...]"""
+import os
+import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2308_03291_b200 import kernels as K
+
+NEG_INF = float("-inf")
+
+
+def bench(fn, iters=20, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for _ in range(iters):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters
+
+
+def main(fams):
+    g = torch.Generator(device="cuda").manual_seed(0)
+    if "chain" in fams:
+        init = torch.randn(32, 32, device="cuda", generator=g)
+        tr = torch.randn(32, 127, 32, 32, device="cuda", generator=g)
+        print("chain_fb      B=32 n=128 m=32  ms %.4f" % bench(lambda: K.chain_fb(init, tr)))
+        print("chain_viterbi B=32 n=128 m=32  ms %.4f" % bench(lambda: K.chain_viterbi(init, tr)))
+    if "nw" in fams:
+        B, n, m = 256, 512, 128
+        th = torch.randn(B, n + 1, m + 1, 3, device="cuda", generator=g)
+        th[:, 0, :, 0] = NEG_INF; th[:, 0, :, 1] = NEG_INF; th[:, :, 0, 0] = NEG_INF; th[:, :, 0, 2] = NEG_INF
+        t = bench(lambda: K.nw_fb(th))
+        print("nw_fb   B=256 512x128 ms %.4f  -> %.1f GB/s algorithmic" % (t, 2 * th.numel() * 4 / t / 1e6))
+        print("nw_logz B=256 512x128 ms %.4f" % bench(lambda: K.nw_fb(th, marginals=False)))
+        print("nw_viterbi B=256 512x128 ms %.4f" % bench(lambda: K.nw_viterbi(th), iters=5))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or ["chain", "nw"])

@@ -1,0 +1,24 @@
+"""Dev utility: run one kernel family a few times at config shape (for ncu)."""
+import os
+import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2308_03291_b200 import kernels as K
+
+NEG_INF = float("-inf")
+fam = sys.argv[1]
+mode = sys.argv[2] if len(sys.argv) > 2 else "fb"
+g = torch.Generator(device="cuda").manual_seed(0)
+if fam == "nw":
+    B, n, m = 256, 512, 128
+    th = torch.randn(B, n + 1, m + 1, 3, device="cuda", generator=g)
+    th[:, 0, :, 0] = NEG_INF; th[:, 0, :, 1] = NEG_INF; th[:, :, 0, 0] = NEG_INF; th[:, :, 0, 2] = NEG_INF
+    fn = {"fb": lambda: K.nw_fb(th), "logz": lambda: K.nw_fb(th, False), "vit": lambda: K.nw_viterbi(th)}[mode]
+elif fam == "chain":
+    init = torch.randn(32, 32, device="cuda", generator=g)
+    tr = torch.randn(32, 127, 32, 32, device="cuda", generator=g)
+    fn = {"fb": lambda: K.chain_fb(init, tr), "vit": lambda: K.chain_viterbi(init, tr)}[mode]
+for _ in range(3):
+    fn()
+torch.cuda.synchronize()
+print("ok")
