@@ -220,21 +220,23 @@ def run_ours(args):
 
     # e2e through the public batched entry with host pinned buffers
     host_in = [t.cpu().pin_memory() for t in inputs]
-    e2e_times = []
+    probe = [o for o in fn() if o is not None and o.dtype != torch.int32]
+    host_out = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in probe]
     h2d = sum(t.numel() * t.element_size() for t in host_in)
-    d2h = 0
+    d2h = sum(o.numel() * o.element_size() for o in host_out)
+    e2e_times = []
     for it in range(args.warmup + args.steps):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
         e0.record(stream)
         dev_in = [t.to(device, non_blocking=True) for t in host_in]
-        out = step_fn(cfg, dev_in)()
-        host_out = [o.to("cpu") for o in out if o is not None and o.dtype != torch.int32]
+        out = [o for o in step_fn(cfg, dev_in)() if o is not None and o.dtype != torch.int32]
+        for h, o in zip(host_out, out):
+            h.copy_(o, non_blocking=True)
         e1.record(stream)
         torch.cuda.synchronize()
         if it >= args.warmup:
             e2e_times.append(e0.elapsed_time(e1))
-        d2h = sum(o.numel() * o.element_size() for o in host_out)
     e2e_ms = sum(e2e_times) / len(e2e_times)
 
     t = torch.tensor([ms, kms, e2e_ms], dtype=torch.float64, device=device)

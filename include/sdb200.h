@@ -90,6 +90,27 @@ size_t sdb_nw_viterbi_workspace(int64_t B, int32_t n, int32_t m);
 int sdb_nw_viterbi(const float* theta, int64_t B, int32_t n, int32_t m, int8_t* path, double* score,
                    int32_t* status, void* workspace, size_t ws_bytes, void* stream);
 
+/* ------------------------------------------------------------------ CTC --
+ * CTCDist (alignment.py:198-228): frame_potentials [B,T,V] (blank = 0),
+ * targets [B,L] int32 in 1..V-1.  T >= 1, 2L+1 <= 1024.
+ *
+ * sdb_ctc_fb replaces _ctc_forward/_ctc_backward/ctc_log_partition/
+ * ctc_marginals (alignment.py:248-301): logz [B]; marg [B,T,V] nullable
+ * (state posteriors scatter-added by label).
+ */
+size_t sdb_ctc_fb_workspace(int64_t B, int32_t T, int32_t V, int32_t L);
+int sdb_ctc_fb(const float* frame_potentials, const int32_t* targets, int64_t B, int32_t T, int32_t V,
+               int32_t L, double* logz, float* marg, int32_t* status, void* workspace, size_t ws_bytes,
+               void* stream);
+
+/* sdb_ctc_viterbi replaces ctc_argmax/_ctc_walk (alignment.py:304-336):
+ * labels [B,T] int32 = vocabulary id emitted per frame on the best expanded
+ * path (predecessor ties s, s-1, s-2; final ties S-1, S-2); score [B]. */
+size_t sdb_ctc_viterbi_workspace(int64_t B, int32_t T, int32_t V, int32_t L);
+int sdb_ctc_viterbi(const float* frame_potentials, const int32_t* targets, int64_t B, int32_t T, int32_t V,
+                    int32_t L, int32_t* labels, double* score, int32_t* status, void* workspace,
+                    size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -31,6 +31,10 @@ SIGNATURES = {
     "sdb_nw_fb": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
     "sdb_nw_viterbi_workspace": (_sz, [_i64, _i32, _i32]),
     "sdb_nw_viterbi": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
+    "sdb_ctc_fb_workspace": (_sz, [_i64, _i32, _i32, _i32]),
+    "sdb_ctc_fb": (ctypes.c_int, [_c_p, _c_p, _i64, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
+    "sdb_ctc_viterbi_workspace": (_sz, [_i64, _i32, _i32, _i32]),
+    "sdb_ctc_viterbi": (ctypes.c_int, [_c_p, _c_p, _i64, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
 }
 
 

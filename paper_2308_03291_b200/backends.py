@@ -194,7 +194,51 @@ class AlignmentBackend(Backend):
         return ArgmaxResult(to_host(st), build, self.vacuous_msg)
 
 
+# ------------------------------------------------------------------- CTC
+
+
+class CTCBackend(Backend):
+    """alignment.py:198-336 on sdb_ctc_fb / sdb_ctc_viterbi."""
+
+    vacuous_msg = "no frame path collapses to the target"
+
+    def batch_key(self, d):
+        return (d.num_frames, d.vocab_size, len(d.target))
+
+    def algo(self, d):
+        return "ctc-forward"
+
+    def argmax_algo(self, d):
+        return "max-plus-ctc"
+
+    def _stack(self, ds):
+        tg = to_dev([np.asarray(d.target, dtype=np.int64).reshape(-1) for d in ds], torch.int32)
+        return to_dev([d.frame_potentials for d in ds]), tg
+
+    def run(self, ds, marginals=True, full=False):
+        fp, tg = self._stack(ds)
+        logz, marg, st = K.ctc_fb(fp, tg, marginals)
+        out = None
+        if marginals:
+            mg = to_host(marg).astype(np.float64)
+            out = [{"frame_potentials": mg[i]} for i in range(len(ds))]
+        return Result(to_host(logz), to_host(st), out, self.vacuous_msg)
+
+    def argmax(self, ds):
+        fp, tg = self._stack(ds)
+        labels, score, st = K.ctc_viterbi(fp, tg)
+        labels = to_host(labels)
+
+        def build(i):
+            mask = np.zeros_like(ds[i].frame_potentials)
+            mask[np.arange(mask.shape[0]), labels[i]] = 1.0
+            return {"frame_potentials": mask}
+
+        return ArgmaxResult(to_host(st), build, self.vacuous_msg)
+
+
 _BACKENDS = {
+    CTCDist: CTCBackend(),
     LinearChainCRF: ChainBackend(),
     MonotoneAlignmentCRF: AlignmentBackend(),
 }

@@ -1,0 +1,389 @@
+// CTC over the blank-interleaved 2L+1 lattice: log-partition, per-frame
+// vocabulary marginals, best expanded-state path.
+//
+// Reference: structdist alignment.py:231-336 (_expanded_labels,
+// _ctc_predecessors, _ctc_forward, _ctc_backward, ctc_marginals, ctc_argmax,
+// _ctc_walk).  Layout per instance: frame_potentials [T][V] fp32,
+// targets [L] int32 (labels in 1..V-1), blank = 0.
+//
+// Schedule: one CTA per instance, one thread per lattice state s (S = 2L+1
+// <= 1024), frames in lockstep (one __syncthreads per frame).  Frame rows are
+// prefetched kP frames ahead into a shared ring with cp.async and each state
+// gathers its emission theta[t][lab(s)] from shared memory.
+//   phase A: beta over frames T-1..0, stored as fp32 offsets from a per-frame
+//            fp64 base (the frame max) -> workspace; Z = lse(beta[0][0..1] + E).
+//   phase B: alpha over frames 0..T-1; posterior exp(alpha + beta - Z) per
+//            state, reduced by label deterministically (blank: fixed-order warp
+//            butterflies; labels: each vocabulary thread sums its own state
+//            list in increasing s) and written as one coalesced [V] row.
+// Log values are fp64; exp/log fp32 MUFU on differences.
+#include "common.cuh"
+
+namespace {
+
+constexpr int kP = 8;  // frame prefetch distance / ring depth
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+struct CtcSmem {
+  double* a0;     // [S+2] ping (2 leading -inf pads)
+  double* a1;     // [S+2] pong
+  float* rows;    // [kP][V]
+  int* lab;       // [S]
+  int* lst;       // [L] states grouped by label (CSR)
+  int* off;       // [V+1]
+  float* post;    // [S]
+  double* wred;   // [32]
+  float* bred;    // [32]
+};
+
+size_t ctc_smem_bytes(int S, int V, int L) {
+  return (size_t)2 * (S + 2) * 8 + (size_t)kP * V * 4 + (size_t)S * 4 + (size_t)(L + 1) * 4 +
+         (size_t)(V + 1) * 4 + (size_t)S * 4 + 32 * 8 + 32 * 4 + 64;
+}
+
+__device__ CtcSmem ctc_carve(char* p, int S, int V, int L) {
+  CtcSmem s;
+  s.a0 = (double*)p; p += (size_t)(S + 2) * 8;
+  s.a1 = (double*)p; p += (size_t)(S + 2) * 8;
+  s.wred = (double*)p; p += 32 * 8;
+  s.rows = (float*)p; p += (size_t)kP * V * 4;
+  s.lab = (int*)p; p += (size_t)S * 4;
+  s.lst = (int*)p; p += (size_t)(L + 1) * 4;
+  s.off = (int*)p; p += (size_t)(V + 1) * 4;
+  s.post = (float*)p; p += (size_t)S * 4;
+  s.bred = (float*)p;
+  return s;
+}
+
+__device__ __forceinline__ void load_row(const float* __restrict__ fp, int t, int V, float* dst) {
+  for (int v = threadIdx.x; v < V; v += blockDim.x) cp_async4(dst + v, fp + (size_t)t * V + v);
+}
+
+// block-wide max of one double per thread (all threads get it); one barrier
+__device__ __forceinline__ double block_maxd_after(double v, double* wred) {
+  v = warp_maxd(v);
+  if ((threadIdx.x & 31) == 0) wred[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double r = wred[0];
+  const int nw = blockDim.x >> 5;
+  for (int i = 1; i < nw; ++i) r = fmax(r, wred[i]);
+  return r;
+}
+
+template <int kMode>  // 0 logZ only, 1 logZ + marginals, 2 max-plus path
+__global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __restrict__ tg_all, int T, int V,
+                           int L, float* __restrict__ wsb_all, double* __restrict__ wsbase_all,
+                           int8_t* __restrict__ back_all, double* __restrict__ logz, float* __restrict__ marg_all,
+                           int32_t* __restrict__ path_all, double* __restrict__ score,
+                           int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) char smraw[];
+  const int S = 2 * L + 1;
+  CtcSmem sm = ctc_carve(smraw, S, V, L);
+  __shared__ double zsh;
+  __shared__ int badsh;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const float* fp = fp_all + (size_t)b * T * V;
+  const int32_t* tg = tg_all + (size_t)b * L;
+  const int s = tid;
+  const bool act = s < S;
+
+  // ---- prologue: labels, skip flags, label lists
+  if (tid == 0) {
+    badsh = 0;
+    zsh = ninfd();
+  }
+  __syncthreads();
+  int mylab = 0;
+  bool skip = false;
+  if (act) {
+    mylab = (s & 1) ? tg[s >> 1] : 0;
+    if ((s & 1) && (mylab < 1 || mylab >= V)) {
+      atomicOr(&badsh, 1);
+      mylab = 0;
+    }
+    sm.lab[s] = mylab;
+  }
+  __syncthreads();
+  if (act) skip = (s >= 2) && mylab != 0 && mylab != sm.lab[s - 2];
+  if (kMode == 1) {
+    if (tid == 0) {  // CSR of the odd states by label, increasing s (deterministic order)
+      for (int v = 0; v <= V; ++v) sm.off[v] = 0;
+      for (int k = 0; k < L; ++k) sm.off[sm.lab[2 * k + 1] + 1]++;
+      for (int v = 0; v < V; ++v) sm.off[v + 1] += sm.off[v];
+      for (int k = 0; k < L; ++k) sm.lst[k] = -1;
+      for (int k = 0; k < L; ++k) {
+        int pos = sm.off[sm.lab[2 * k + 1]];
+        while (sm.lst[pos] >= 0) ++pos;
+        sm.lst[pos] = 2 * k + 1;
+      }
+    }
+    __syncthreads();
+  }
+  const int nwarps = blockDim.x >> 5;
+  float* wsb = (kMode == 1) ? wsb_all + (size_t)b * T * S : nullptr;
+  double* wsbase = (kMode == 1) ? wsbase_all + (size_t)b * T : nullptr;
+
+  // ======================= phase A: backward (marginals only)
+  if (kMode == 1) {
+    double* cur = sm.a0 + 2;  // beta[t+1][*]
+    double* nxt = sm.a1 + 2;
+    // prefetch frames T-1 .. T-kP (we need E[t+1] while computing beta[t])
+    for (int k = 0; k < kP; ++k) {
+      const int t = T - 1 - k;
+      if (t >= 0) load_row(fp, t, V, sm.rows + (size_t)(t % kP) * V);
+      cp_commit();
+    }
+    if (act) cur[s] = (s == S - 1 || s == S - 2) ? 0.0 : ninfd();
+    if (tid < S + 2 && tid >= S) cur[tid] = ninfd();  // right pads beyond S
+    if (tid < 2) { sm.a0[tid] = ninfd(); sm.a1[tid] = ninfd(); }
+    __syncthreads();
+    // store beta[T-1]
+    {
+      double base = block_maxd_after(act ? cur[s] : ninfd(), sm.wred);
+      if (base == ninfd()) base = 0.0;
+      if (act) wsb[(size_t)(T - 1) * S + s] = (cur[s] == ninfd()) ? ninf() : (float)(cur[s] - base);
+      if (tid == 0) wsbase[T - 1] = base;
+    }
+    for (int t = T - 2; t >= 0; --t) {
+      // frame t+1 must be resident: it was issued (T-1)-(t+1) groups ago
+      cp_wait<kP - 1>();
+      __syncthreads();
+      const float* E = sm.rows + (size_t)((t + 1) % kP) * V;
+      double v = ninfd();
+      if (act) {
+        const double x0 = cur[s] + (double)E[mylab];
+        const double x1 = (s + 1 < S) ? cur[s + 1] + (double)E[sm.lab[s + 1]] : ninfd();
+        const bool sk2 = (s + 2 < S) && sm.lab[s + 2] != 0 && sm.lab[s + 2] != mylab;
+        const double x2 = sk2 ? cur[s + 2] + (double)E[sm.lab[s + 2]] : ninfd();
+        const double M = fmax(fmax(x0, x1), x2);
+        if (M != ninfd()) {
+          const float e = fexp((float)(x0 - M)) + fexp((float)(x1 - M)) + fexp((float)(x2 - M));
+          v = M + (double)flog(e);
+        }
+        nxt[s] = v;
+      }
+      __syncthreads();  // all reads of cur and row (t+1) done
+      // refill the ring slot of frame t+1 with frame t+1-kP
+      {
+        const int tn = t + 1 - kP;
+        if (tn >= 0) load_row(fp, tn, V, sm.rows + (size_t)(tn % kP) * V);
+        cp_commit();
+      }
+      double base = block_maxd_after(v, sm.wred);
+      if (base == ninfd()) base = 0.0;
+      if (act) wsb[(size_t)t * S + s] = (v == ninfd()) ? ninf() : (float)(v - base);
+      if (tid == 0) wsbase[t] = base;
+      double* tmp = cur; cur = nxt; nxt = tmp;
+    }
+    cp_wait<0>();
+    __syncthreads();
+    // Z = lse(beta[0][0] + E0[lab0], beta[0][1] + E0[lab1])  (E0 = frame 0 still in the ring)
+    if (tid == 0) {
+      const float* E0 = sm.rows;  // frame 0 sits in slot 0
+      const double z0 = cur[0] + (double)E0[sm.lab[0]];
+      const double z1 = (S > 1) ? cur[1] + (double)E0[sm.lab[1]] : ninfd();
+      const double M = fmax(z0, z1);
+      zsh = (M == ninfd()) ? ninfd() : M + (double)flog(fexp((float)(z0 - M)) + fexp((float)(z1 - M)));
+    }
+    __syncthreads();
+  }
+
+  // ======================= phase B: forward
+  {
+    double* prv = sm.a0 + 2;  // alpha[t-1]
+    double* now = sm.a1 + 2;
+    if (tid < 2) { sm.a0[tid] = ninfd(); sm.a1[tid] = ninfd(); }
+    for (int k = 0; k < kP; ++k) {
+      if (k < T) load_row(fp, k, V, sm.rows + (size_t)k * V);
+      cp_commit();
+    }
+    const double Z = zsh;
+    const bool zok = Z != ninfd();
+    float* marg = (kMode == 1) ? marg_all + (size_t)b * T * V : nullptr;
+    int8_t* back = (kMode == 2) ? back_all + (size_t)b * T * S : nullptr;
+    int bad = 0;
+    for (int t = 0; t < T; ++t) {
+      cp_wait<kP - 1>();
+      __syncthreads();
+      const float* E = sm.rows + (size_t)(t % kP) * V;
+      for (int v = tid; v < V; v += blockDim.x) bad |= bad_input(E[v]);
+      double a = ninfd();
+      if (act) {
+        const double e = (double)E[mylab];
+        if (t == 0) {
+          a = (s <= 1) ? e : ninfd();
+        } else if (kMode == 2) {
+          // first maximum in predecessor order [s, s-1, s-2] (alignment.py:239-245, 304-318)
+          double best = prv[s];
+          int k = 0;
+          if (s >= 1 && prv[s - 1] > best) { best = prv[s - 1]; k = 1; }
+          if (skip && prv[s - 2] > best) { best = prv[s - 2]; k = 2; }
+          a = best + e;
+          back[(size_t)t * S + s] = (int8_t)k;
+        } else {
+          const double x0 = prv[s], x1 = prv[s - 1], x2 = skip ? prv[s - 2] : ninfd();
+          const double M = fmax(fmax(x0, x1), x2);
+          if (M != ninfd()) {
+            const float sum = fexp((float)(x0 - M)) + fexp((float)(x1 - M)) + fexp((float)(x2 - M));
+            a = M + (double)flog(sum) + e;
+          }
+        }
+        now[s] = a;
+      }
+      if (kMode == 1) {
+        // posterior of state s at frame t
+        float p = 0.f;
+        if (act && zok && a != ninfd()) {
+          const float bt = wsb[(size_t)t * S + s];
+          const double bb = wsbase[t];
+          if (bt != ninf()) p = fexp((float)(a + bb - Z) + bt);
+        }
+        if (act) sm.post[s] = p;
+        // blank column: fixed-order butterfly over the even states of each warp
+        float pb = (act && !(s & 1)) ? p : 0.f;
+        pb = warp_sum(pb);
+        if ((tid & 31) == 0) sm.bred[tid >> 5] = pb;
+      }
+      __syncthreads();  // now[] and post[] complete; row t consumed
+      {
+        const int tn = t + kP;
+        if (tn < T) load_row(fp, tn, V, sm.rows + (size_t)(tn % kP) * V);
+        cp_commit();
+      }
+      if (kMode == 1) {
+        for (int v = tid; v < V; v += blockDim.x) {
+          float acc = 0.f;
+          if (v == 0) {
+            for (int w = 0; w < nwarps; ++w) acc += sm.bred[w];
+          } else {
+            for (int q = sm.off[v]; q < sm.off[v + 1]; ++q) acc += sm.post[sm.lst[q]];
+          }
+          marg[(size_t)t * V + v] = acc;
+        }
+      }
+      double* tmp = prv; prv = now; now = tmp;
+    }
+    cp_wait<0>();
+    if (bad) atomicOr(&badsh, 1);
+    __syncthreads();
+    // final states (alignment.py:263-264): [S-1] or [S-1, S-2]
+    if (tid == 0) {
+      const double f1 = prv[S - 1];
+      const double f2 = (S > 1) ? prv[S - 2] : ninfd();
+      double res;
+      int fin = S - 1;
+      if (kMode == 2) {
+        res = f1;
+        if (S > 1 && f2 > f1) { res = f2; fin = S - 2; }
+      } else {
+        const double M = fmax(f1, f2);
+        res = (M == ninfd()) ? ninfd() : M + (double)flog(fexp((float)(f1 - M)) + fexp((float)(f2 - M)));
+      }
+      const int st = badsh ? SDB_ST_INVALID : (res == ninfd() ? SDB_ST_VACUOUS : SDB_ST_OK);
+      status[b] = st;
+      if (kMode == 2) {
+        score[b] = res;
+        int32_t* path = path_all + (size_t)b * T;
+        int cs = fin;
+        for (int t = T - 1; t >= 0; --t) {
+          path[t] = (st == SDB_ST_OK) ? sm.lab[cs] : 0;
+          if (t > 0 && st == SDB_ST_OK) cs -= back[(size_t)t * S + cs];
+        }
+      } else {
+        logz[b] = res;
+      }
+    }
+  }
+}
+
+struct CtcWs {
+  float* wsb;
+  double* wsbase;
+  int8_t* back;
+};
+
+CtcWs ctc_carve_ws(void* base, int64_t B, int T, int L, int mode, size_t* bytes) {
+  const int S = 2 * L + 1;
+  Carve c(base);
+  CtcWs w{};
+  if (mode == 1) {
+    w.wsb = c.take<float>((size_t)B * T * S);
+    w.wsbase = c.take<double>((size_t)B * T);
+  }
+  if (mode == 2) w.back = c.take<int8_t>((size_t)B * T * S);
+  *bytes = c.used;
+  return w;
+}
+
+int ctc_check(int64_t B, int T, int V, int L) {
+  if (B < 0 || T < 1 || V < 1 || L < 0) return SDB_ERR_ARG;
+  const int S = 2 * L + 1;
+  if (S > 1024 || ctc_smem_bytes(S, V, L) > 200 * 1024) return SDB_ERR_UNSUPPORTED;
+  return SDB_OK;
+}
+
+template <int kMode>
+int ctc_launch(const float* fp, const int32_t* tg, int64_t B, int T, int V, int L, CtcWs ws, double* logz,
+               float* marg, int32_t* path, double* score, int32_t* status, cudaStream_t s) {
+  const int S = 2 * L + 1;
+  const int threads = ((S + 31) / 32) * 32;
+  const size_t smem = ctc_smem_bytes(S, V, L);
+  if (cudaFuncSetAttribute(ctc_kernel<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return SDB_ERR_CUDA;
+  ctc_kernel<kMode><<<(unsigned)B, threads, smem, s>>>(fp, tg, T, V, L, ws.wsb, ws.wsbase, ws.back, logz, marg,
+                                                      path, score, status);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
+}  // namespace
+
+extern "C" size_t sdb_ctc_fb_workspace(int64_t B, int32_t T, int32_t V, int32_t L) {
+  (void)V;
+  size_t bytes = 0;
+  ctc_carve_ws(nullptr, B, T, L, 1, &bytes);
+  return bytes;
+}
+
+extern "C" int sdb_ctc_fb(const float* frame_potentials, const int32_t* targets, int64_t B, int32_t T, int32_t V,
+                          int32_t L, double* logz, float* marg, int32_t* status, void* workspace, size_t ws_bytes,
+                          void* stream) {
+  int rc = ctc_check(B, T, V, L);
+  if (rc) return rc;
+  if (!frame_potentials || (L > 0 && !targets) || !logz || !status) return SDB_ERR_ARG;
+  if (B == 0) return SDB_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!marg) return ctc_launch<0>(frame_potentials, targets, B, T, V, L, CtcWs{}, logz, nullptr, nullptr, nullptr, status, s);
+  size_t need = 0;
+  CtcWs ws = ctc_carve_ws(workspace, B, T, L, 1, &need);
+  if (!workspace || ws_bytes < need) return SDB_ERR_WORKSPACE;
+  return ctc_launch<1>(frame_potentials, targets, B, T, V, L, ws, logz, marg, nullptr, nullptr, status, s);
+}
+
+extern "C" size_t sdb_ctc_viterbi_workspace(int64_t B, int32_t T, int32_t V, int32_t L) {
+  (void)V;
+  size_t bytes = 0;
+  ctc_carve_ws(nullptr, B, T, L, 2, &bytes);
+  return bytes;
+}
+
+extern "C" int sdb_ctc_viterbi(const float* frame_potentials, const int32_t* targets, int64_t B, int32_t T,
+                               int32_t V, int32_t L, int32_t* labels, double* score, int32_t* status,
+                               void* workspace, size_t ws_bytes, void* stream) {
+  int rc = ctc_check(B, T, V, L);
+  if (rc) return rc;
+  if (!frame_potentials || (L > 0 && !targets) || !labels || !score || !status) return SDB_ERR_ARG;
+  if (B == 0) return SDB_OK;
+  size_t need = 0;
+  CtcWs ws = ctc_carve_ws(workspace, B, T, L, 2, &need);
+  if (!workspace || ws_bytes < need) return SDB_ERR_WORKSPACE;
+  return ctc_launch<2>(frame_potentials, targets, B, T, V, L, ws, nullptr, nullptr, labels, score, status,
+                       (cudaStream_t)stream);
+}

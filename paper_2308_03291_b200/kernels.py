@@ -122,3 +122,43 @@ def nw_viterbi(theta):
                             stream_ptr(dev))
     _lib.check(rc, "sdb_nw_viterbi")
     return path, score, status
+
+
+# ------------------------------------------------------------------- CTC
+
+
+def ctc_fb(frame_potentials, targets, marginals: bool = True):
+    """alignment.py:248-301 batched: frame_potentials [B,T,V], targets
+    [B,L] -> (logz [B] f64, marg [B,T,V] | None, status)."""
+    lib = _lib.load()
+    fp = f32(frame_potentials, "frame_potentials")
+    tg = i32(targets, "targets")
+    B, T, V = fp.shape
+    L = tg.shape[1]
+    dev = fp.device
+    logz = torch.empty(B, dtype=torch.float64, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    marg = torch.empty_like(fp) if marginals else None
+    ws = workspace(lib.sdb_ctc_fb_workspace(B, T, V, L) if marginals else 0, dev)
+    rc = lib.sdb_ctc_fb(ptr(fp), ptr(tg), B, T, V, L, ptr(logz), ptr(marg), ptr(status), ptr(ws), ws.numel(),
+                        stream_ptr(dev))
+    _lib.check(rc, "sdb_ctc_fb")
+    return logz, marg, status
+
+
+def ctc_viterbi(frame_potentials, targets):
+    """alignment.py:304-336 batched -> (labels per frame [B,T] int32, score, status)."""
+    lib = _lib.load()
+    fp = f32(frame_potentials, "frame_potentials")
+    tg = i32(targets, "targets")
+    B, T, V = fp.shape
+    L = tg.shape[1]
+    dev = fp.device
+    labels = torch.empty(B, T, dtype=torch.int32, device=dev)
+    score = torch.empty(B, dtype=torch.float64, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    ws = workspace(lib.sdb_ctc_viterbi_workspace(B, T, V, L), dev)
+    rc = lib.sdb_ctc_viterbi(ptr(fp), ptr(tg), B, T, V, L, ptr(labels), ptr(score), ptr(status), ptr(ws),
+                             ws.numel(), stream_ptr(dev))
+    _lib.check(rc, "sdb_ctc_viterbi")
+    return labels, score, status

@@ -39,5 +39,22 @@ def main(fams):
         print("nw_viterbi B=256 512x128 ms %.4f" % bench(lambda: K.nw_viterbi(th), iters=5))
 
 
+
+
+def ctc():
+    g = torch.Generator(device="cuda").manual_seed(0)
+    B, T, V, L = 256, 512, 128, 128
+    fp = torch.randn(B, T, V, device="cuda", generator=g)
+    tg = torch.randint(1, V, (B, L), device="cuda", generator=g, dtype=torch.int32)
+    t = bench(lambda: K.ctc_fb(fp, tg))
+    print("ctc_fb  B=256 T=512 V=128 L=128 ms %.4f -> %.0f struct/s" % (t, B / t * 1e3))
+    print("ctc_logz ms %.4f" % bench(lambda: K.ctc_fb(fp, tg, False)))
+    print("ctc_viterbi ms %.4f" % bench(lambda: K.ctc_viterbi(fp, tg), iters=5))
+
+
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["chain", "nw"])
+    fams = sys.argv[1:] or ["chain", "nw", "ctc"]
+    main(fams)
+    for f in fams:
+        if f in globals() and f not in ("main", "bench"):
+            globals()[f]()
