@@ -111,6 +111,22 @@ int sdb_ctc_viterbi(const float* frame_potentials, const int32_t* targets, int64
                     int32_t L, int32_t* labels, double* score, int32_t* status, void* workspace,
                     size_t ws_bytes, void* stream);
 
+/* ------------------------------------------------------------- Tree-CRF --
+ * TreeCRF (constituency.py:26-49): span_potentials [B,n,n,m] (i, j, label),
+ * only i <= j read.  1 <= n <= 128.
+ *
+ * sdb_tree_fb replaces _tree_charts/cky_log_partition/tree_marginals
+ * (constituency.py:52-110): logz [B]; marg [B,n,n,m] nullable (0 for i > j
+ * and unreachable spans).  No workspace (charts live in shared memory). */
+int sdb_tree_fb(const float* span_potentials, int64_t B, int32_t n, int32_t m, double* logz, float* marg,
+                int32_t* status, void* stream);
+
+/* sdb_tree_viterbi replaces cky_max_score/_tree_walk/tree_argmax
+ * (constituency.py:72-133): labels [B,n,n] int32 = label of each span in the
+ * best tree (first argmax label, first argmax split), -1 elsewhere. */
+int sdb_tree_viterbi(const float* span_potentials, int64_t B, int32_t n, int32_t m, int32_t* labels,
+                     double* score, int32_t* status, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -237,7 +237,48 @@ class CTCBackend(Backend):
         return ArgmaxResult(to_host(st), build, self.vacuous_msg)
 
 
+# -------------------------------------------------------------- Tree-CRF
+
+
+class TreeBackend(Backend):
+    """constituency.py:26-133 on sdb_tree_fb / sdb_tree_viterbi."""
+
+    vacuous_msg = "no labeled tree has finite score"
+
+    def batch_key(self, d):
+        return (d.n, d.m)
+
+    def algo(self, d):
+        return "cky-inside"
+
+    def argmax_algo(self, d):
+        return "max-plus-cky"
+
+    def run(self, ds, marginals=True, full=False):
+        th = to_dev([d.span_potentials for d in ds])
+        logz, marg, st = K.tree_fb(th, marginals)
+        out = None
+        if marginals:
+            mg = to_host(marg).astype(np.float64)
+            out = [{"span_potentials": mg[i]} for i in range(len(ds))]
+        return Result(to_host(logz), to_host(st), out, self.vacuous_msg)
+
+    def argmax(self, ds):
+        th = to_dev([d.span_potentials for d in ds])
+        labels, score, st = K.tree_viterbi(th)
+        labels = to_host(labels)
+
+        def build(i):
+            mask = np.zeros_like(ds[i].span_potentials)
+            ii, jj = np.nonzero(labels[i] >= 0)
+            mask[ii, jj, labels[i][ii, jj]] = 1.0
+            return {"span_potentials": mask}
+
+        return ArgmaxResult(to_host(st), build, self.vacuous_msg)
+
+
 _BACKENDS = {
+    TreeCRF: TreeBackend(),
     CTCDist: CTCBackend(),
     LinearChainCRF: ChainBackend(),
     MonotoneAlignmentCRF: AlignmentBackend(),

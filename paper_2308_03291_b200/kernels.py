@@ -162,3 +162,36 @@ def ctc_viterbi(frame_potentials, targets):
                              ws.numel(), stream_ptr(dev))
     _lib.check(rc, "sdb_ctc_viterbi")
     return labels, score, status
+
+
+# -------------------------------------------------------------- Tree-CRF
+
+
+def tree_fb(span_potentials, marginals: bool = True):
+    """constituency.py:52-110 batched: span_potentials [B,n,n,m] ->
+    (logz [B] f64, marg [B,n,n,m] | None, status)."""
+    lib = _lib.load()
+    th = f32(span_potentials, "span_potentials")
+    B, n, _, m = th.shape
+    dev = th.device
+    logz = torch.empty(B, dtype=torch.float64, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    marg = torch.empty_like(th) if marginals else None
+    rc = lib.sdb_tree_fb(ptr(th), B, n, m, ptr(logz), ptr(marg), ptr(status), stream_ptr(dev))
+    _lib.check(rc, "sdb_tree_fb")
+    return logz, marg, status
+
+
+def tree_viterbi(span_potentials):
+    """constituency.py:113-133 batched -> (labels [B,n,n] int32 (-1 = not in
+    tree), score [B], status)."""
+    lib = _lib.load()
+    th = f32(span_potentials, "span_potentials")
+    B, n, _, m = th.shape
+    dev = th.device
+    labels = torch.empty(B, n, n, dtype=torch.int32, device=dev)
+    score = torch.empty(B, dtype=torch.float64, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    rc = lib.sdb_tree_viterbi(ptr(th), B, n, m, ptr(labels), ptr(score), ptr(status), stream_ptr(dev))
+    _lib.check(rc, "sdb_tree_viterbi")
+    return labels, score, status

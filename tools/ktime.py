@@ -52,6 +52,16 @@ def ctc():
     print("ctc_viterbi ms %.4f" % bench(lambda: K.ctc_viterbi(fp, tg), iters=5))
 
 
+
+def tree():
+    g = torch.Generator(device="cuda").manual_seed(0)
+    th = torch.randn(128, 64, 64, 32, device="cuda", generator=g)
+    t = bench(lambda: K.tree_fb(th))
+    print("tree_fb B=128 n=64 m=32 ms %.4f -> %.0f struct/s, %.0f GB/s alg" % (t, 128 / t * 1e3, 128 * 790532 / t / 1e6))
+    print("tree_logz ms %.4f" % bench(lambda: K.tree_fb(th, False)))
+    print("tree_viterbi ms %.4f" % bench(lambda: K.tree_viterbi(th)))
+
+
 if __name__ == "__main__":
     fams = sys.argv[1:] or ["chain", "nw", "ctc"]
     main(fams)
