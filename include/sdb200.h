@@ -127,6 +127,32 @@ int sdb_tree_fb(const float* span_potentials, int64_t B, int32_t n, int32_t m, d
 int sdb_tree_viterbi(const float* span_potentials, int64_t B, int32_t n, int32_t m, int32_t* labels,
                      double* score, int32_t* status, void* stream);
 
+/* ---------------------------------------------------- Matrix-Tree (MTT) --
+ * Directed non-projective SpanningTreeCRF (spanning.py:41-70):
+ * adjacency [B,n+1,n+1] (head, dependent), node 0 = root, diagonal and
+ * column 0 -inf.  1 <= n <= 128.  single_root != 0 selects the Koo et al.
+ * single-root-edge Laplacian.
+ *
+ * sdb_mtt replaces _shifted_exp_weights/_build_laplacian/signed_log_det/
+ * mtt_log_partition/mtt_marginals (spanning.py:90-175, numerics.py:128-159):
+ * logz [B]; marg [B,n+1,n+1] nullable, clipped to [0,1].  No workspace. */
+int sdb_mtt(const float* adjacency, int64_t B, int32_t n, int32_t single_root, double* logz, float* marg,
+            int32_t* status, void* stream);
+
+/* ------------------------------------------------ projective (Eisner) --
+ * Directed projective SpanningTreeCRF: adjacency [B,n+1,n+1] (head, dep),
+ * 1 <= n <= 128.
+ *
+ * sdb_eisner replaces _eisner_charts/eisner_log_partition/eisner_marginals
+ * (spanning.py:183-280): logz [B]; marg [B,n+1,n+1] nullable, clipped.
+ * sdb_kuhlmann replaces _reweight_root/kuhlmann_argmax (spanning.py:339-402),
+ * the reference's public projective argmax: heads [B,n+1] int32 (heads[0] =
+ * -1), best (reweighted) tabulation score [B]; bit-exact tie behaviour. */
+int sdb_eisner(const float* adjacency, int64_t B, int32_t n, int32_t single_root, double* logz, float* marg,
+               int32_t* status, void* stream);
+int sdb_kuhlmann(const float* adjacency, int64_t B, int32_t n, int32_t single_root, int32_t* heads,
+                 double* score, int32_t* status, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

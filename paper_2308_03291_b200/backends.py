@@ -277,7 +277,73 @@ class TreeBackend(Backend):
         return ArgmaxResult(to_host(st), build, self.vacuous_msg)
 
 
+# -------------------------------------------------------- spanning trees
+
+
+class SpanningBackend(Backend):
+    """spanning.py:41-402 flag dispatch (span_log_partition / span_marginals
+    / span_argmax, spanning.py:673-706): projective -> sdb_eisner /
+    sdb_kuhlmann, non-projective -> sdb_mtt.  Undirected instances reuse the
+    adjacency as directed (spanning.py:73-82)."""
+
+    def batch_key(self, d):
+        return (d.n, d.directed, d.projective, d.single_root_edge)
+
+    @staticmethod
+    def _prefix(d):
+        return "" if d.directed else "undirected-reduction+"
+
+    def algo(self, d):
+        if d.projective:
+            name = "eisner-single-root" if d.single_root_edge else "eisner"
+        else:
+            name = "mtt-single-root" if d.single_root_edge else "mtt-multi-root"
+        return self._prefix(d) + name
+
+    def argmax_algo(self, d):
+        name = "kuhlmann-arc-hybrid" if d.projective else "chu-liu-edmonds"
+        if d.single_root_edge:
+            name = "reweighting+" + name
+        return self._prefix(d) + name
+
+    def run(self, ds, marginals=True, full=False):
+        d0 = ds[0]
+        adj = to_dev([d.adjacency for d in ds])
+        if d0.projective:
+            logz, marg, st = K.eisner(adj, d0.single_root_edge, marginals)
+            msg = "no projective tree has finite score"
+        else:
+            logz, marg, st = K.mtt(adj, d0.single_root_edge, marginals)
+            msg = "no spanning tree has finite score"
+        out = None
+        if marginals:
+            mg = to_host(marg).astype(np.float64)
+            out = [{"adjacency": mg[i]} for i in range(len(ds))]
+        return Result(to_host(logz), to_host(st), out, msg)
+
+    def argmax(self, ds):
+        d0 = ds[0]
+        if not d0.projective:
+            from .errors import UnsupportedInference
+
+            raise UnsupportedInference(
+                "non-projective argmax (Chu-Liu-Edmonds, spanning.py:410-509) is not on the GPU path")
+        adj = to_dev([d.adjacency for d in ds])
+        heads, score, st = K.kuhlmann(adj, d0.single_root_edge)
+        heads = to_host(heads)
+
+        def build(i):
+            n = ds[i].n
+            mask = np.zeros((n + 1, n + 1))
+            dep = np.arange(1, n + 1)
+            mask[heads[i][1:], dep] = 1.0
+            return {"adjacency": mask}
+
+        return ArgmaxResult(to_host(st), build, "no projective tree has finite score")
+
+
 _BACKENDS = {
+    SpanningTreeCRF: SpanningBackend(),
     TreeCRF: TreeBackend(),
     CTCDist: CTCBackend(),
     LinearChainCRF: ChainBackend(),

@@ -1,0 +1,480 @@
+// Projective spanning trees: Eisner inside/outside (log-partition, arc
+// marginals) and the Kuhlmann arc-hybrid max-plus argmax.
+//
+// Reference: structdist spanning.py:183-280 (_eisner_charts,
+// _eisner_root_terms, eisner_log_partition, eisner_marginals) and
+// spanning.py:339-402 (_reweight_root, kuhlmann_argmax -- the public
+// projective argmax).  Layout per instance: adjacency [n+1][n+1] fp32
+// (head, dependent), position 0 = root.
+//
+// eisner_kernel -- one CTA (512 threads) per instance, n <= 128:
+//   * the four inside charts cr, cl, ir, il and the three outside charts
+//     ocr, ocl, ofold (ofold = outside of the shared split term; oir/oil are
+//     consumed on the fly for the marginals) are packed upper-triangular fp32
+//     arrays in shared memory (7 x n(n+1)/2 floats = 226 KB at n = 128);
+//   * every value is stored relative to an INTEGER per-width offset
+//     (Cin[w] for inside, Cout[w] for outside; a span of width w carries w
+//     arcs, so offsets are re-chosen adaptively per width from the width's
+//     max).  Integer offsets make every cross-width correction exact in fp32,
+//     so all stored magnitudes stay small and fp32 keeps ~1e-6 absolute
+//     accuracy at n = 128 (plain fp32 log-space would lose ~1e-4);
+//   * inside by width (spanning.py:199-206), one warp per cell, lanes over
+//     split points; outside by decreasing width in PULL form (each child
+//     gathers from its parents, no atomics), marginals emitted per cell as
+//     exp(o + i - Z) and clipped to [0,1] (spanning.py:280).
+// kuhlmann_kernel -- fp64 max-plus tabulation over n+2 positions with the
+// reference's scan order and strict '>' (first maximum), root reweighting for
+// single-root, backtrack to heads[]; bit-exact with the reference.
+#include "common.cuh"
+
+namespace {
+
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxN = 128;
+constexpr int kQ = (kMaxN + 1 + 31) / 32;  // max split terms per lane
+
+// packed strict-upper index over positions 0..n (i < j)
+__device__ __forceinline__ int pk(int i, int j, int n) { return i * n - (i * (i - 1)) / 2 + (j - i - 1); }
+
+size_t eisner_smem(int n) {
+  const size_t T = (size_t)n * (n + 1) / 2;
+  return 7 * T * 4 + (size_t)2 * (n + 2) * 4 + kWarps * 8 + 64;
+}
+
+struct Charts {
+  float *cr, *cl, *ir, *il, *ocr, *ocl, *ofo;
+  float *cin, *cout;
+  float* wmax;
+};
+
+// complete charts: width-0 entries are 0 (cr[i,i] = cl[i,i] = 0)
+__device__ __forceinline__ float cget(const float* c, int a, int b, int n) { return a == b ? 0.f : c[pk(a, b, n)]; }
+
+// log-sum-exp of up to kQ per-lane terms, then across the warp
+__device__ __forceinline__ float warp_lse_terms(const float (&t)[kQ]) {
+  float m = ninf();
+#pragma unroll
+  for (int q = 0; q < kQ; ++q) m = fmaxf(m, t[q]);
+  m = warp_max(m);
+  float s = 0.f;
+  if (m != ninf()) {
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) s += ex2(t[q] - m);  // terms are in log2 units
+  }
+  s = warp_sum(s);
+  return m == ninf() ? ninf() : m + lg2(s);
+}
+
+// All log values inside the kernel are in log2 units (x * log2 e): exp/log
+// become single MUFU ops.  Integer offsets are integers in log2 units.
+__global__ void __launch_bounds__(kThreads, 1) eisner_kernel(const float* __restrict__ adj_all, int n, int single,
+                                                             double* __restrict__ logz, float* __restrict__ marg_all,
+                                                             int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) char smraw[];
+  const int T = n * (n + 1) / 2;
+  Charts c;
+  {
+    float* p = (float*)smraw;
+    c.cr = p; p += T; c.cl = p; p += T; c.ir = p; p += T; c.il = p; p += T;
+    c.ocr = p; p += T; c.ocl = p; p += T; c.ofo = p; p += T;
+    c.cin = p; p += n + 2; c.cout = p; p += n + 2;
+    c.wmax = p;
+  }
+  __shared__ int badsh;
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int N1 = n + 1;
+  const float* th = adj_all + (size_t)b * N1 * N1;
+  auto TH = [&](int h, int d) { return __ldg(th + h * N1 + d) * SDB_LOG2E; };
+  if (tid == 0) badsh = 0;
+  {
+    int bad = 0;
+    for (int e = tid; e < N1 * N1; e += kThreads) bad |= bad_input(th[e]);
+    if (bad) atomicOr(&badsh, 1);
+  }
+  if (tid == 0) c.cin[0] = 0.f;
+  __syncthreads();
+
+  // ================================================================ inside
+  for (int w = 1; w <= n; ++w) {
+    const float Pw = (w == 1) ? 0.f : (w == 2 ? c.cin[1] : 2.f * c.cin[w - 1] - c.cin[w - 2]);
+    if (tid == 0) c.cin[w] = Pw;
+    __syncthreads();
+    float lmax = ninf();
+    for (int i = warp; i + w <= n; i += kWarps) {
+      const int j = i + w;
+      // fold = lse_{k in [i,j)} cr[i,k] + cl[k+1,j]   (widths k-i, j-k-1; sum w-1)
+      float t[kQ];
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        const int k = i + lane + 32 * q;
+        t[q] = ninf();
+        if (k < j) {
+          const float x = cget(c.cr, i, k, n) + cget(c.cl, k + 1, j, n);
+          t[q] = x + (c.cin[k - i] + c.cin[j - k - 1] - Pw);
+        }
+      }
+      const float fold = warp_lse_terms(t);
+      const float vir = (fold == ninf()) ? ninf() : TH(i, j) + fold;
+      const float vil = (fold == ninf()) ? ninf() : TH(j, i) + fold;
+      if (lane == 0) {
+        c.ir[pk(i, j, n)] = vir;
+        c.il[pk(i, j, n)] = vil;
+      }
+      __syncwarp();
+      // cr = lse_{k in (i,j]} ir[i,k] + cr[k,j]; cl = lse_{k in [i,j)} cl[i,k] + il[k,j]
+      float tr[kQ], tl[kQ];
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        const int k = i + 1 + lane + 32 * q;  // (i, j]
+        tr[q] = ninf();
+        if (k <= j) tr[q] = c.ir[pk(i, k, n)] + cget(c.cr, k, j, n) + (c.cin[k - i] + c.cin[j - k] - Pw);
+        const int k2 = i + lane + 32 * q;  // [i, j)
+        tl[q] = ninf();
+        if (k2 < j) tl[q] = cget(c.cl, i, k2, n) + c.il[pk(k2, j, n)] + (c.cin[k2 - i] + c.cin[j - k2] - Pw);
+      }
+      const float vcr = warp_lse_terms(tr);
+      const float vcl = warp_lse_terms(tl);
+      if (lane == 0) {
+        c.cr[pk(i, j, n)] = vcr;
+        c.cl[pk(i, j, n)] = vcl;
+      }
+      lmax = fmaxf(lmax, fmaxf(fmaxf(vir, vil), fmaxf(vcr, vcl)));
+    }
+    if (lane == 0) c.wmax[warp] = lmax;
+    __syncthreads();
+    float M = ninf();
+#pragma unroll
+    for (int q = 0; q < kWarps; ++q) M = fmaxf(M, c.wmax[q]);
+    const float r = (M == ninf()) ? 0.f : rintf(M);
+    if (r != 0.f) {
+      for (int i = tid; i + w <= n; i += kThreads) {
+        const int e = pk(i, i + w, n);
+        c.ir[e] -= r; c.il[e] -= r; c.cr[e] -= r; c.cl[e] -= r;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) c.cin[w] = Pw + r;
+    __syncthreads();
+  }
+
+  // log Z (log2 units): value + integer offset
+  __shared__ float zv, zc;  // Z = (zv + zc) log2 units
+  if (tid == 0) {
+    if (!single) {
+      zv = c.cr[pk(0, n, n)];
+      zc = c.cin[n];
+    } else {
+      // spanning.py:210-212: Z = lse_c th[0,c] + cl[1,c] + cr[c,n]
+      float K = ninf();
+      for (int cc = 1; cc <= n; ++cc) K = fmaxf(K, c.cin[cc - 1] + c.cin[n - cc]);
+      float m = ninf();
+      for (int cc = 1; cc <= n; ++cc) {
+        const float x = TH(0, cc) + cget(c.cl, 1, cc, n) + cget(c.cr, cc, n, n) + (c.cin[cc - 1] + c.cin[n - cc] - K);
+        m = fmaxf(m, x);
+      }
+      float s = 0.f;
+      if (m != ninf())
+        for (int cc = 1; cc <= n; ++cc) {
+          const float x = TH(0, cc) + cget(c.cl, 1, cc, n) + cget(c.cr, cc, n, n) + (c.cin[cc - 1] + c.cin[n - cc] - K);
+          s += ex2(x - m);
+        }
+      zv = (m == ninf()) ? ninf() : m + lg2(s);
+      zc = K;
+    }
+  }
+  __syncthreads();
+  const bool zok = zv != ninf();
+  if (tid == 0) {
+    status[b] = badsh ? SDB_ST_INVALID : (zok ? SDB_ST_OK : SDB_ST_VACUOUS);
+    logz[b] = zok ? ((double)zv + (double)zc) * (double)SDB_LN2 : ninfd();
+  }
+  if (!marg_all) return;
+  float* mg = marg_all + (size_t)b * N1 * N1;
+  if (!zok || badsh) {
+    for (int e = tid; e < N1 * N1; e += kThreads) mg[e] = 0.f;
+    return;
+  }
+  for (int e = tid; e < N1; e += kThreads) mg[e * N1 + e] = 0.f;
+  if (single) {  // marg[0,c] = exp(root term - Z)
+    for (int cc = 1 + tid; cc <= n; cc += kThreads) {
+      const float x = TH(0, cc) + cget(c.cl, 1, cc, n) + cget(c.cr, cc, n, n) + (c.cin[cc - 1] + c.cin[n - cc] - zc);
+      mg[cc] = fminf(fmaxf(ex2(x - zv), 0.f), 1.f);
+    }
+  }
+
+  // =============================================================== outside
+  // Pull form.  Offsets cout[w]; provisional Qw extrapolated from wider widths.
+  for (int w = n; w >= 1; --w) {
+    const float Qw = (w == n) ? 0.f : (w == n - 1 ? c.cout[n] : 2.f * c.cout[w + 1] - c.cout[w + 2]);
+    if (tid == 0) c.cout[w] = Qw;
+    __syncthreads();
+    float lmax = ninf();
+    for (int a = warp; a + w <= n; a += kWarps) {
+      const int bb = a + w;
+      // ---- ocr[a,bb]
+      float tA[kQ], tB[kQ];
+      // parents via the split term: j in (bb, n]: ofold[a,j] + cl[bb+1,j]
+      // parents via cr: i in [0,a): ocr[i,bb] + ir[i,a]
+      const int n1 = n - bb, n2 = a;
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        const int x = lane + 32 * q;
+        float tv = ninf();
+        if (x < n1) {
+          const int j = bb + 1 + x;
+          tv = c.ofo[pk(a, j, n)] + cget(c.cl, bb + 1, j, n) + (c.cout[j - a] + c.cin[j - bb - 1] - Qw);
+        } else if (x < n1 + n2) {
+          const int i = x - n1;
+          tv = c.ocr[pk(i, bb, n)] + c.ir[pk(i, a, n)] + (c.cout[bb - i] + c.cin[a - i] - Qw);
+        }
+        tA[q] = tv;
+      }
+      float vocr = warp_lse_terms(tA);
+      // ---- ocl[a,bb]
+      // split-term parents: i in [0, a-1]: ofold[i,bb] + cr[i,a-1]
+      // cl parents: j in (bb, n]: ocl[a,j] + il[bb,j]
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        const int x = lane + 32 * q;
+        float tv = ninf();
+        if (x < n2) {
+          const int i = x;
+          tv = c.ofo[pk(i, bb, n)] + cget(c.cr, i, a - 1, n) + (c.cout[bb - i] + c.cin[a - 1 - i] - Qw);
+        } else if (x < n2 + n1) {
+          const int j = bb + 1 + (x - n2);
+          tv = c.ocl[pk(a, j, n)] + c.il[pk(bb, j, n)] + (c.cout[j - a] + c.cin[j - bb] - Qw);
+        }
+        tB[q] = tv;
+      }
+      float vocl = warp_lse_terms(tB);
+      if (lane == 0) {
+        // root seeds (spanning.py:233-245)
+        if (!single) {
+          if (a == 0 && bb == n) vocr = -Qw;  // ocr[0,n] = log 1 (multi-root Z = cr[0,n])
+        } else {
+          if (bb == n && a >= 1) {  // d root-term / d cr[a,n] = th[0,a] + cl[1,a]
+            const float s0 = TH(0, a) + cget(c.cl, 1, a, n) + (c.cin[a - 1] - Qw);
+            const float m = fmaxf(vocr, s0);
+            if (m != ninf()) vocr = m + lg2(ex2(vocr - m) + ex2(s0 - m));
+          }
+          if (a == 1) {  // d root-term / d cl[1,bb] = th[0,bb] + cr[bb,n]
+            const float s0 = TH(0, bb) + cget(c.cr, bb, n, n) + (c.cin[n - bb] - Qw);
+            const float m = fmaxf(vocl, s0);
+            if (m != ninf()) vocl = m + lg2(ex2(vocl - m) + ex2(s0 - m));
+          }
+        }
+        c.ocr[pk(a, bb, n)] = vocr;
+        c.ocl[pk(a, bb, n)] = vocl;
+      }
+      __syncwarp();
+      // ---- oir[a,bb] = lse_{j in [bb,n]} ocr[a,j] + cr[bb,j]
+      // ---- oil[a,bb] = lse_{i in [0,a]} ocl[i,bb] + cl[i,a]
+      float tr[kQ], tl[kQ];
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        const int x = lane + 32 * q;
+        tr[q] = ninf();
+        tl[q] = ninf();
+        const int j = bb + x;
+        if (j <= n) tr[q] = c.ocr[pk(a, j, n)] + cget(c.cr, bb, j, n) + (c.cout[j - a] + c.cin[j - bb] - Qw);
+        if (x <= a) tl[q] = c.ocl[pk(x, bb, n)] + cget(c.cl, x, a, n) + (c.cout[bb - x] + c.cin[a - x] - Qw);
+      }
+      const float voir = warp_lse_terms(tr);
+      const float voil = warp_lse_terms(tl);
+      if (lane == 0) {
+        const int e = pk(a, bb, n);
+        const float thab = TH(a, bb), thba = TH(bb, a);
+        // ofold = (oil + th[bb,a]) (+) (oir + th[a,bb])
+        const float x1 = voil + thba, x2 = voir + thab;
+        const float m = fmaxf(x1, x2);
+        const float vof = (m == ninf()) ? ninf() : m + lg2(ex2(x1 - m) + ex2(x2 - m));
+        c.ofo[e] = vof;
+        // marginals: arc a->bb via ir, arc bb->a via il (spanning.py:264-277)
+        const float off = (Qw + c.cin[w] - zc);
+        const float pr = (voir == ninf() || c.ir[e] == ninf()) ? 0.f : ex2(voir + c.ir[e] + off - zv);
+        const float pl = (voil == ninf() || c.il[e] == ninf()) ? 0.f : ex2(voil + c.il[e] + off - zv);
+        if (!(single && a == 0)) mg[a * N1 + bb] = fminf(fmaxf(pr, 0.f), 1.f);
+        mg[bb * N1 + a] = fminf(fmaxf(pl, 0.f), 1.f);
+        lmax = fmaxf(lmax, fmaxf(fmaxf(vocr, vocl), vof));
+      }
+    }
+    lmax = warp_max(lmax);
+    if (lane == 0) c.wmax[warp] = lmax;
+    __syncthreads();
+    float M = ninf();
+#pragma unroll
+    for (int q = 0; q < kWarps; ++q) M = fmaxf(M, c.wmax[q]);
+    const float r = (M == ninf()) ? 0.f : rintf(M);
+    if (r != 0.f) {
+      for (int a = tid; a + w <= n; a += kThreads) {
+        const int e = pk(a, a + w, n);
+        c.ocr[e] -= r; c.ocl[e] -= r; c.ofo[e] -= r;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) c.cout[w] = Qw + r;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- Kuhlmann
+// fp64 max-plus over positions 0..n+1 (n+1 = end marker, heads nothing).
+// table packed strict-upper over N2 = n+2 positions; back = (k, head).
+size_t kuhl_smem(int n) {
+  const size_t N2 = n + 2;
+  const size_t T = N2 * (N2 - 1) / 2;
+  return T * 8 + T * 4 + 64;
+}
+
+__device__ __forceinline__ int pk2(int i, int j, int N) { return i * (N - 1) - (i * (i - 1)) / 2 + (j - i - 1); }
+
+__global__ void __launch_bounds__(kThreads, 1) kuhlmann_kernel(const float* __restrict__ adj_all, int n, int single,
+                                                               int32_t* __restrict__ heads_all,
+                                                               double* __restrict__ score,
+                                                               int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) char smraw[];
+  const int N = n + 2;
+  const int T = N * (N - 1) / 2;
+  double* tab = (double*)smraw;
+  int* back = (int*)(tab + T);  // (k << 1) | (head == j)
+  __shared__ double rw_c;
+  __shared__ int badsh;
+  __shared__ float fmin_s, fmax_s;
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int N1 = n + 1;
+  const float* th = adj_all + (size_t)b * N1 * N1;
+  if (tid == 0) { badsh = 0; fmin_s = __int_as_float(0x7f800000); fmax_s = ninf(); }
+  __syncthreads();
+  {
+    int bad = 0;
+    float lo = __int_as_float(0x7f800000), hi = ninf();
+    for (int e = tid; e < N1 * N1; e += kThreads) {
+      const float x = th[e];
+      bad |= bad_input(x);
+      if (x != ninf() && x == x && x != __int_as_float(0x7f800000)) { lo = fminf(lo, x); hi = fmaxf(hi, x); }
+    }
+    if (bad) atomicOr(&badsh, 1);
+    lo = -warp_max(-lo);
+    hi = warp_max(hi);
+    __shared__ float lo_w[kWarps], hi_w[kWarps];
+    if (lane == 0) { lo_w[warp] = lo; hi_w[warp] = hi; }
+    __syncthreads();
+    if (tid == 0) {
+      float L = lo_w[0], H = hi_w[0];
+      for (int q = 1; q < kWarps; ++q) { L = fminf(L, lo_w[q]); H = fmaxf(H, hi_w[q]); }
+      fmin_s = L;
+      fmax_s = H;
+      // spanning.py:339-350: c = n * (max - min) + 1 over the finite entries
+      rw_c = (double)n * ((double)H - (double)L) + 1.0;
+    }
+    __syncthreads();
+  }
+  const bool no_finite = (fmax_s == ninf());
+  // score(h, k): reweighted th[h][k] for h in 0..n, k in 1..n; end marker heads nothing
+  auto S = [&](int h, int k) -> double {
+    if (h > n || k < 1 || k > n) return ninfd();
+    double v = (double)__ldg(th + h * N1 + k);
+    if (single && h == 0) v = v - rw_c;
+    return v;
+  };
+  for (int e = tid; e < T; e += kThreads) tab[e] = ninfd();
+  __syncthreads();
+  for (int i = tid; i + 1 < N; i += kThreads) tab[pk2(i, i + 1, N)] = 0.0;
+  __syncthreads();
+  for (int w = 2; w < N; ++w) {
+    for (int i = warp; i + w < N; i += kWarps) {
+      const int j = i + w;
+      // candidates in reference order: k ascending, head i then head j; strict '>'
+      double best = ninfd();
+      int arg = 0x7fffffff;  // encoded order index 2*(k-i-1) + (head==j)
+      for (int k = i + 1 + lane; k < j; k += 32) {
+        const double base = tab[pk2(i, k, N)] + tab[pk2(k, j, N)];
+        if (base == ninfd()) continue;
+        const double c1 = base + S(i, k), c2 = base + S(j, k);
+        const int o = 2 * (k - i - 1);
+        if (c1 > best) { best = c1; arg = o; }
+        if (c2 > best) { best = c2; arg = o + 1; }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+        if (ov > best || (ov == best && oa < arg)) { best = ov; arg = oa; }
+      }
+      if (lane == 0) {
+        tab[pk2(i, j, N)] = best;
+        back[pk2(i, j, N)] = (arg == 0x7fffffff) ? -1 : arg;
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    int32_t* heads = heads_all + (size_t)b * N1;
+    const double top = tab[pk2(0, N - 1, N)];
+    int st = (badsh) ? SDB_ST_INVALID : ((top == ninfd() || no_finite) ? SDB_ST_VACUOUS : SDB_ST_OK);
+    for (int d = 0; d <= n; ++d) heads[d] = -1;
+    if (st == SDB_ST_OK) {
+      // explicit stack (reuse the tail of back[] is unsafe; use a small local stack in registers via shared)
+      int* stk = (int*)(tab);  // table no longer needed except top; safe to reuse
+      int sp = 0;
+      stk[sp++] = 0;
+      stk[sp++] = N - 1;
+      int roots = 0;
+      while (sp > 0) {
+        const int j = stk[--sp];
+        const int i = stk[--sp];
+        if (j == i + 1) continue;
+        const int code = back[pk2(i, j, N)];
+        const int k = i + 1 + (code >> 1);
+        const int h = (code & 1) ? j : i;
+        heads[k] = h;
+        if (h == 0) ++roots;
+        stk[sp++] = i; stk[sp++] = k;
+        stk[sp++] = k; stk[sp++] = j;
+      }
+      if (single && roots != 1) st = SDB_ST_VACUOUS;
+      if (st != SDB_ST_OK)
+        for (int d = 0; d <= n; ++d) heads[d] = -1;
+    }
+    status[b] = st;
+    score[b] = top;
+  }
+}
+
+int eisner_check(int64_t B, int n) {
+  if (B < 0 || n < 1) return SDB_ERR_ARG;
+  if (n > kMaxN || eisner_smem(n) > 227 * 1024) return SDB_ERR_UNSUPPORTED;
+  return SDB_OK;
+}
+
+}  // namespace
+
+extern "C" int sdb_eisner(const float* adjacency, int64_t B, int32_t n, int32_t single_root, double* logz,
+                          float* marg, int32_t* status, void* stream) {
+  int rc = eisner_check(B, n);
+  if (rc) return rc;
+  if (!adjacency || !logz || !status) return SDB_ERR_ARG;
+  if (B == 0) return SDB_OK;
+  const size_t smem = eisner_smem(n);
+  if (cudaFuncSetAttribute(eisner_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return SDB_ERR_CUDA;
+  eisner_kernel<<<(unsigned)B, kThreads, smem, (cudaStream_t)stream>>>(adjacency, n, single_root ? 1 : 0, logz, marg,
+                                                                       status);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
+extern "C" int sdb_kuhlmann(const float* adjacency, int64_t B, int32_t n, int32_t single_root, int32_t* heads,
+                            double* score, int32_t* status, void* stream) {
+  if (B < 0 || n < 1) return SDB_ERR_ARG;
+  if (kuhl_smem(n) > 227 * 1024) return SDB_ERR_UNSUPPORTED;
+  if (!adjacency || !heads || !score || !status) return SDB_ERR_ARG;
+  if (B == 0) return SDB_OK;
+  const size_t smem = kuhl_smem(n);
+  if (cudaFuncSetAttribute(kuhlmann_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return SDB_ERR_CUDA;
+  kuhlmann_kernel<<<(unsigned)B, kThreads, smem, (cudaStream_t)stream>>>(adjacency, n, single_root ? 1 : 0, heads,
+                                                                         score, status);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}

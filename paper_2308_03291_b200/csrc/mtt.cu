@@ -1,0 +1,290 @@
+// Non-projective spanning trees via the Matrix-Tree theorem: log-partition
+// (log|det| of the root-augmented Laplacian) and edge marginals (inverse
+// Laplacian).
+//
+// Reference: structdist spanning.py:90-175 (_shifted_exp_weights,
+// _build_laplacian, mtt_log_partition, mtt_marginals) and numerics.py:128-159
+// (signed_log_det: partial pivoting, singular when |pivot| <= 1e-12 * the
+// pivot row's original max-abs; -inf when sign <= 0).
+// Layout per instance: adjacency [n+1][n+1] fp32 (head, dependent).
+//
+// One CTA (512 threads) per instance, n <= 128 (padded to 128 with an
+// identity block).  The 128x128 Laplacian lives in REGISTERS: warp w owns
+// columns [8w, 8w+8), lane l owns rows [4l, 4l+4) -> 32 fp32 per thread.
+// In-place Gauss-Jordan with implicit partial pivoting: step k picks the
+// unused row p with max |a[p][k]| (a warp argmax inside the column's warp),
+// broadcasts row p and column k through shared memory, and every thread does
+// a register-blocked rank-1 update (32 FFMA per 12 shared loads).  Pivots
+// equal the reference's LU pivots, so log|det| = sum log|pivot| (fp64) and the
+// sign comes from the pivot signs and the permutation parity.  The result is
+// the row/column-permuted inverse, scattered to shared memory as A^{-1}, from
+// which the edge marginals are formed (spanning.py:152-175) and clipped.
+#include "common.cuh"
+
+namespace {
+
+constexpr int kN = 128;
+constexpr int kThreads = 512;
+
+struct MttSmem {
+  float* adj;     // [(n+1)*(n+1)]
+  float* inv;     // [kN*kN] A^{-1}
+  float* shift;   // [kN] column max s_d
+  float* diag;    // [kN]
+  float* rowmag;  // [kN]
+  float* rowbuf;  // [2][kN]
+  float* colbuf;  // [2][kN]
+  int* perm;      // [kN] pivot row of step k
+  int* used;      // [kN]
+};
+
+size_t mtt_smem(int n) {
+  return (size_t)(n + 1) * (n + 1) * 4 + (size_t)kN * kN * 4 + (size_t)kN * 4 * 3 + (size_t)4 * kN * 4 +
+         (size_t)kN * 8 + 256;
+}
+
+template <bool kMarg>
+__global__ void __launch_bounds__(kThreads, 1) mtt_kernel(const float* __restrict__ adj_all, int n, int single,
+                                                          double* __restrict__ logz, float* __restrict__ marg_all,
+                                                          int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) char smraw[];
+  MttSmem sm;
+  {
+    char* p = smraw;
+    sm.inv = (float*)p; p += (size_t)kN * kN * 4;
+    sm.shift = (float*)p; p += kN * 4;
+    sm.diag = (float*)p; p += kN * 4;
+    sm.rowmag = (float*)p; p += kN * 4;
+    sm.rowbuf = (float*)p; p += 2 * kN * 4;
+    sm.colbuf = (float*)p; p += 2 * kN * 4;
+    sm.perm = (int*)p; p += kN * 4;
+    sm.used = (int*)p; p += kN * 4;
+    sm.adj = (float*)p;
+  }
+  __shared__ int flag_bad, flag_vac, piv_row;
+  __shared__ float piv_val;
+  __shared__ double logdet;
+  __shared__ int negs;
+
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int N1 = n + 1;
+  const float* A = adj_all + (size_t)b * N1 * N1;
+  if (tid == 0) { flag_bad = 0; flag_vac = 0; logdet = 0.0; negs = 0; }
+  for (int e = tid; e < N1 * N1; e += kThreads) {
+    const float x = A[e];
+    if (bad_input(x)) flag_bad = 1;
+    sm.adj[e] = x;
+  }
+  for (int e = tid; e < kN; e += kThreads) { sm.used[e] = 0; sm.rowmag[e] = 0.f; }
+  __syncthreads();
+  // column shifts and diagonal (spanning.py:90-120); thread d handles dependent d+1
+  if (tid < n) {
+    const int d = tid, dep = d + 1;
+    float mx = ninf();
+    for (int h = 0; h <= n; ++h)
+      if (h != dep) mx = fmaxf(mx, sm.adj[h * N1 + dep]);
+    if (mx == ninf()) flag_vac = 1;
+    float s = 0.f;
+    if (mx != ninf())
+      for (int h = single ? 1 : 0; h <= n; ++h)
+        if (h != dep) s += fexp(sm.adj[h * N1 + dep] - mx);
+    sm.shift[d] = mx;
+    sm.diag[d] = s;
+  }
+  __syncthreads();
+  if (flag_vac || flag_bad) {
+    if (tid == 0) {
+      status[b] = flag_bad ? SDB_ST_INVALID : SDB_ST_VACUOUS;
+      logz[b] = ninfd();
+    }
+    if (kMarg)
+      for (int e = tid; e < N1 * N1; e += kThreads) marg_all[(size_t)b * N1 * N1 + e] = 0.f;
+    return;
+  }
+  // build the register block: rows r0..r0+3 (head h = r+1), cols c0..c0+7 (dep d = c+1)
+  const int r0 = 4 * lane, c0 = 8 * warp;
+  float a[4][8];
+#pragma unroll
+  for (int ii = 0; ii < 4; ++ii) {
+    const int r = r0 + ii;
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const int c = c0 + jj;
+      float v;
+      if (r >= n || c >= n) {
+        v = (r == c) ? 1.f : 0.f;  // identity padding
+      } else if (single && r == 0) {
+        v = fexp(sm.adj[c + 1] - sm.shift[c]);  // row 0 <- root weights (Koo et al.)
+      } else if (r == c) {
+        v = sm.diag[c];
+      } else {
+        v = -fexp(sm.adj[(r + 1) * N1 + c + 1] - sm.shift[c]);
+      }
+      a[ii][jj] = v;
+    }
+  }
+  // original row magnitudes (numerics.py:143)
+#pragma unroll
+  for (int ii = 0; ii < 4; ++ii) {
+    float mx = 0.f;
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) mx = fmaxf(mx, fabsf(a[ii][jj]));
+    atomicMax((int*)&sm.rowmag[r0 + ii], __float_as_int(mx));
+  }
+  __syncthreads();
+
+  // ---- Gauss-Jordan with implicit partial pivoting
+  bool singular = false;
+  for (int k = 0; k < kN; ++k) {
+    const int kb = k & 1;
+    float* rowbuf = sm.rowbuf + kb * kN;
+    float* colbuf = sm.colbuf + kb * kN;
+    if (warp == (k >> 3)) {
+      const int jj = k & 7;
+      // argmax |a[r][k]| over unused rows r (first index on ties)
+      float bv = -1.f;
+      int br = 0x7fffffff;
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii) {
+        const int r = r0 + ii;
+        float v = 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) if (q == jj) v = a[ii][q];
+        colbuf[r] = v;
+        const float av = fabsf(v);
+        if (!sm.used[r] && (av > bv || (av == bv && r < br))) { bv = av; br = r; }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int orr = __shfl_xor_sync(0xffffffffu, br, o);
+        if (ov > bv || (ov == bv && orr < br)) { bv = ov; br = orr; }
+      }
+      if (lane == 0) {
+        piv_row = br;
+        sm.perm[k] = br;
+        sm.used[br] = 1;
+      }
+    }
+    __syncthreads();
+    const int p = piv_row;
+    // owners of row p publish it
+    if ((p >> 2) == lane) {
+      const int ii = p & 3;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (q == ii) {
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) rowbuf[c0 + jj] = a[q][jj];
+        }
+    }
+    __syncthreads();
+    const float piv = rowbuf[k];
+    if (tid == 0) {
+      const float mag = fabsf(piv);
+      if (!(mag > 1e-12f * fmaxf(sm.rowmag[p], 1e-30f))) singular = true, flag_vac = 1;
+      if (piv < 0.f) negs++;
+      logdet += (double)log((double)mag);
+    }
+    const float inv_piv = 1.f / piv;
+    float cv[4];
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii) cv[ii] = colbuf[r0 + ii];
+    float rv[8];
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) rv[jj] = rowbuf[c0 + jj] * inv_piv;
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii) {
+      const int r = r0 + ii;
+      if (r == p) {
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) a[ii][jj] = (c0 + jj == k) ? inv_piv : rv[jj];
+      } else {
+        const float f = cv[ii];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) a[ii][jj] = (c0 + jj == k) ? -f * inv_piv : fmaf(-f, rv[jj], a[ii][jj]);
+      }
+    }
+  }
+  (void)singular;
+  __syncthreads();
+  // sign: pivot signs x permutation parity (numerics.py:149-155)
+  if (tid == 0) {
+    int parity = 0;
+    // parity of k -> perm[k]: count transpositions via cycle decomposition
+    for (int k = 0; k < kN; ++k) sm.used[k] = 0;
+    for (int k = 0; k < kN; ++k) {
+      if (sm.used[k]) continue;
+      int len = 0, x = k;
+      while (!sm.used[x]) { sm.used[x] = 1; x = sm.perm[x]; ++len; }
+      parity ^= (len + 1) & 1;  // a cycle of length L has L-1 transpositions
+    }
+    const int sgn = ((negs + parity) & 1) ? -1 : 1;
+    double ssum = 0.0;
+    for (int d = 0; d < n; ++d) ssum += (double)sm.shift[d];
+    const bool vac = flag_vac || sgn <= 0;
+    flag_vac = vac;
+    logz[b] = vac ? ninfd() : logdet + ssum;
+    status[b] = vac ? SDB_ST_VACUOUS : SDB_ST_OK;
+  }
+  if (!kMarg) return;
+  // q = inverse permutation (q[perm[k]] = k)
+  __syncthreads();
+  if (tid < kN) sm.used[sm.perm[tid]] = tid;  // reuse `used` as q
+  __syncthreads();
+  // A^{-1}[r][x] = M[p_r][q_x]  ->  M[i][j] goes to inv[q_i][p_j]
+#pragma unroll
+  for (int ii = 0; ii < 4; ++ii) {
+    const int i = r0 + ii, qi = sm.used[i];
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) sm.inv[qi * kN + sm.perm[c0 + jj]] = a[ii][jj];
+  }
+  __syncthreads();
+  float* mg = marg_all + (size_t)b * N1 * N1;
+  const bool vac = flag_vac;
+  for (int e = tid; e < N1 * N1; e += kThreads) {
+    const int h = e / N1, dep = e - h * N1;
+    float v = 0.f;
+    if (!vac && dep >= 1 && h != dep) {
+      const int d = dep - 1;
+      const float w = fexp(sm.adj[e] - sm.shift[d]);
+      const float idd = sm.inv[d * kN + d];
+      if (single) {
+        if (h == 0) v = w * sm.inv[d * kN + 0];
+        else v = w * ((d != 0 ? idd : 0.f) - ((h - 1) != 0 ? sm.inv[d * kN + (h - 1)] : 0.f));
+      } else {
+        v = (h == 0) ? w * idd : w * (idd - sm.inv[d * kN + (h - 1)]);
+      }
+      v = fminf(fmaxf(v, 0.f), 1.f);  // spanning.py:175
+    }
+    mg[e] = v;
+  }
+}
+
+int mtt_check(int64_t B, int n) {
+  if (B < 0 || n < 1) return SDB_ERR_ARG;
+  if (n > kN) return SDB_ERR_UNSUPPORTED;
+  return SDB_OK;
+}
+
+}  // namespace
+
+extern "C" int sdb_mtt(const float* adjacency, int64_t B, int32_t n, int32_t single_root, double* logz, float* marg,
+                       int32_t* status, void* stream) {
+  int rc = mtt_check(B, n);
+  if (rc) return rc;
+  if (!adjacency || !logz || !status) return SDB_ERR_ARG;
+  if (B == 0) return SDB_OK;
+  const size_t smem = mtt_smem(n);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (marg) {
+    if (cudaFuncSetAttribute(mtt_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return SDB_ERR_CUDA;
+    mtt_kernel<true><<<(unsigned)B, kThreads, smem, s>>>(adjacency, n, single_root ? 1 : 0, logz, marg, status);
+  } else {
+    if (cudaFuncSetAttribute(mtt_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return SDB_ERR_CUDA;
+    mtt_kernel<false><<<(unsigned)B, kThreads, smem, s>>>(adjacency, n, single_root ? 1 : 0, logz, nullptr, status);
+  }
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}

@@ -195,3 +195,56 @@ def tree_viterbi(span_potentials):
     rc = lib.sdb_tree_viterbi(ptr(th), B, n, m, ptr(labels), ptr(score), ptr(status), stream_ptr(dev))
     _lib.check(rc, "sdb_tree_viterbi")
     return labels, score, status
+
+
+# ------------------------------------------------------------ Matrix-Tree
+
+
+def mtt(adjacency, single_root: bool = False, marginals: bool = True):
+    """spanning.py:90-175 batched: adjacency [B,n+1,n+1] ->
+    (logz [B] f64, marg [B,n+1,n+1] | None, status)."""
+    lib = _lib.load()
+    adj = f32(adjacency, "adjacency")
+    B, n1, _ = adj.shape
+    dev = adj.device
+    logz = torch.empty(B, dtype=torch.float64, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    marg = torch.empty_like(adj) if marginals else None
+    rc = lib.sdb_mtt(ptr(adj), B, n1 - 1, 1 if single_root else 0, ptr(logz), ptr(marg), ptr(status),
+                     stream_ptr(dev))
+    _lib.check(rc, "sdb_mtt")
+    return logz, marg, status
+
+
+# ---------------------------------------------------- projective (Eisner)
+
+
+def eisner(adjacency, single_root: bool = False, marginals: bool = True):
+    """spanning.py:183-280 batched: adjacency [B,n+1,n+1] ->
+    (logz [B] f64, marg [B,n+1,n+1] | None, status)."""
+    lib = _lib.load()
+    adj = f32(adjacency, "adjacency")
+    B, n1, _ = adj.shape
+    dev = adj.device
+    logz = torch.empty(B, dtype=torch.float64, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    marg = torch.empty_like(adj) if marginals else None
+    rc = lib.sdb_eisner(ptr(adj), B, n1 - 1, 1 if single_root else 0, ptr(logz), ptr(marg), ptr(status),
+                        stream_ptr(dev))
+    _lib.check(rc, "sdb_eisner")
+    return logz, marg, status
+
+
+def kuhlmann(adjacency, single_root: bool = False):
+    """spanning.py:339-402 batched -> (heads [B,n+1] int32, score, status)."""
+    lib = _lib.load()
+    adj = f32(adjacency, "adjacency")
+    B, n1, _ = adj.shape
+    dev = adj.device
+    heads = torch.empty(B, n1, dtype=torch.int32, device=dev)
+    score = torch.empty(B, dtype=torch.float64, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    rc = lib.sdb_kuhlmann(ptr(adj), B, n1 - 1, 1 if single_root else 0, ptr(heads), ptr(score), ptr(status),
+                          stream_ptr(dev))
+    _lib.check(rc, "sdb_kuhlmann")
+    return heads, score, status

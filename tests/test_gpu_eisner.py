@@ -1,0 +1,87 @@
+"""GPU parity: projective spanning trees (Eisner inside/outside,
+spanning.py:183-280) and the Kuhlmann argmax (spanning.py:339-402), plus the
+spanning-tree flag dispatch through the public API for all 8 flag triples."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2308_03291_b200 as sd
+from paper_2308_03291_b200 import kernels as K
+from golden_io import inputs, load
+from gpu_util import ATOL, NEG_INF, RTOL, close_logz, dev, need_gpu
+from golden.builders import batch_spanning
+from oracle import sd_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("case", load("spanning"), ids=lambda c: str(c.meta))
+def test_spanning_golden_api(case):
+    need_gpu()
+    m = case.meta
+    d = sd.SpanningTreeCRF(inputs(case)["adjacency"], directed=m["directed"], projective=m["projective"],
+                           single_root_edge=m["single"])
+    z, algo = sd.log_partition_info(d)
+    close_logz(z, case.logz)
+    if case.vacuous:
+        with pytest.raises(sd.VacuousDistribution):
+            sd.marginals(d)
+        return
+    marg, algo2 = sd.marginals_info(d)
+    assert algo2 == algo
+    case.check_marg("adjacency", marg["adjacency"], RTOL, 1e-5 if m["single"] else 2e-6)
+    if m["projective"] and "argmax_adjacency" in case:
+        ind, score, aalgo = sd.argmax_info(d)
+        np.testing.assert_array_equal(ind["adjacency"], case["argmax_adjacency"])
+        assert score == float(case.argmax_score)
+        assert aalgo == case.meta["argmax_algo"]
+
+
+@pytest.mark.parametrize("single", [False, True])
+@pytest.mark.parametrize("B,n", [(4, 128), (6, 9), (3, 1), (3, 2), (2, 50)])
+def test_eisner_batched_vs_oracle(B, n, single):
+    need_gpu()
+    adj = batch_spanning(3000, B, n)
+    logz, marg, st = K.eisner(dev(adj), single)
+    assert (st.cpu().numpy() == 0).all()
+    heads, score, st2 = K.kuhlmann(dev(adj), single)
+    for b in range(B):
+        z, mg = O.eisner_marginals(adj[b], single)
+        assert abs(logz[b].item() - z) <= RTOL * max(1, abs(z))
+        np.testing.assert_allclose(marg[b].cpu().numpy(), mg, rtol=RTOL, atol=ATOL)
+        if n <= 64 or b == 0:
+            np.testing.assert_array_equal(heads[b].cpu().numpy(), O.kuhlmann_heads(adj[b], single))
+
+
+def test_eisner_config_invariants():
+    """C4 shape: each dependent has exactly one head (incoming marginals sum
+    to 1), multi-root."""
+    need_gpu()
+    g = torch.Generator(device="cuda").manual_seed(0)
+    adj = torch.randn(256, 129, 129, device="cuda", generator=g)
+    adj[:, :, 0] = NEG_INF
+    i = torch.arange(129, device="cuda")
+    adj[:, i, i] = NEG_INF
+    logz, marg, st = K.eisner(adj)
+    assert (st == 0).all()
+    col = marg.double().sum(1)[:, 1:]
+    assert torch.allclose(col, torch.ones_like(col), atol=1e-4)
+
+
+def test_eisner_zero_ties():
+    """Ties on all-zero potentials: Kuhlmann's first-maximum rule."""
+    need_gpu()
+    adj = np.zeros((1, 6, 6))
+    adj[:, :, 0] = NEG_INF
+    adj[:, np.arange(6), np.arange(6)] = NEG_INF
+    for single in (False, True):
+        heads, _, st = K.kuhlmann(dev(adj), single)
+        np.testing.assert_array_equal(heads[0].cpu().numpy(), O.kuhlmann_heads(adj[0], single))
+
+
+def test_nonprojective_argmax_unsupported():
+    need_gpu()
+    d = sd.SpanningTreeCRF(batch_spanning(1, 1, 4)[0])
+    with pytest.raises(sd.UnsupportedInference):
+        sd.argmax(d)

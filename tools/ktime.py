@@ -62,6 +62,32 @@ def tree():
     print("tree_viterbi ms %.4f" % bench(lambda: K.tree_viterbi(th)))
 
 
+
+def mtt():
+    g = torch.Generator(device="cuda").manual_seed(0)
+    adj = torch.randn(512, 129, 129, device="cuda", generator=g)
+    adj[:, :, 0] = NEG_INF
+    i = torch.arange(129, device="cuda")
+    adj[:, i, i] = NEG_INF
+    t = bench(lambda: K.mtt(adj))
+    print("mtt B=512 n=128 ms %.4f -> %.0f struct/s, %.1f TFLOP/s alg" % (t, 512 / t * 1e3, 512 * 4194304 / t / 1e9))
+    print("mtt logz ms %.4f" % bench(lambda: K.mtt(adj, marginals=False)))
+    print("mtt single-root ms %.4f" % bench(lambda: K.mtt(adj, True)))
+
+
+
+def eisner():
+    g = torch.Generator(device="cuda").manual_seed(0)
+    adj = torch.randn(256, 129, 129, device="cuda", generator=g)
+    adj[:, :, 0] = NEG_INF
+    i = torch.arange(129, device="cuda")
+    adj[:, i, i] = NEG_INF
+    t = bench(lambda: K.eisner(adj), iters=5)
+    print("eisner B=256 n=128 ms %.4f -> %.0f struct/s" % (t, 256 / t * 1e3))
+    print("eisner logz ms %.4f" % bench(lambda: K.eisner(adj, marginals=False), iters=5))
+    print("kuhlmann ms %.4f" % bench(lambda: K.kuhlmann(adj), iters=5))
+
+
 if __name__ == "__main__":
     fams = sys.argv[1:] or ["chain", "nw", "ctc"]
     main(fams)
