@@ -153,6 +153,19 @@ int sdb_eisner(const float* adjacency, int64_t B, int32_t n, int32_t single_root
 int sdb_kuhlmann(const float* adjacency, int64_t B, int32_t n, int32_t single_root, int32_t* heads,
                  double* score, int32_t* status, void* stream);
 
+/* ----------------------------------------------------------------- PCFG --
+ * PCFG (constituency.py:184-243): root [B,NT], binary_rules [B,NT,S,S]
+ * (S = NT+PT; children NTs then PTs), emissions [B,n,PT], sticky [B,n,n]
+ * nullable ({0,-inf} span mask; NULL = all 0).  n <= 64, NT, PT <= 32.
+ *
+ * sdb_pcfg_fb replaces _pcfg_inside/pcfg_inside and the span-marginal part
+ * of pcfg_gradients (constituency.py:246-340; marginals() returns only
+ * {"sticky"}, dist.py:125-127): logz [B]; span_marg [B,n,n] nullable. */
+size_t sdb_pcfg_fb_workspace(int64_t B, int32_t n, int32_t NT, int32_t PT);
+int sdb_pcfg_fb(const float* root, const float* rules, const float* emissions, const float* sticky, int64_t B,
+                int32_t n, int32_t NT, int32_t PT, double* logz, float* span_marg, int32_t* status,
+                void* workspace, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -40,6 +40,9 @@ SIGNATURES = {
     "sdb_mtt": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p]),
     "sdb_eisner": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p]),
     "sdb_kuhlmann": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p]),
+    "sdb_pcfg_fb_workspace": (_sz, [_i64, _i32, _i32, _i32]),
+    "sdb_pcfg_fb": (ctypes.c_int, [_c_p, _c_p, _c_p, _c_p, _i64, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _sz,
+                                   _c_p]),
 }
 
 

@@ -342,7 +342,48 @@ class SpanningBackend(Backend):
         return ArgmaxResult(to_host(st), build, "no projective tree has finite score")
 
 
+# ------------------------------------------------------------------- PCFG
+
+
+class PCFGBackend(Backend):
+    """constituency.py:184-371 on sdb_pcfg_fb.  marginals() returns the
+    constituent (span) marginals under the key "sticky" (dist.py:125-127)."""
+
+    vacuous_msg = "the grammar derives no tree for this sentence"
+
+    def batch_key(self, d):
+        return (d.n, d.num_nt, d.num_pt)
+
+    def algo(self, d):
+        return "pcfg-inside"
+
+    def argmax_algo(self, d):
+        return "max-plus-pcfg"
+
+    def run(self, ds, marginals=True, full=False):
+        if full:
+            from .errors import UnsupportedInference
+
+            raise UnsupportedInference("PCFG rule/root/emission expected counts are not on the GPU path yet")
+        root = to_dev([d.root for d in ds])
+        rules = to_dev([d.binary_rules for d in ds])
+        emis = to_dev([d.emissions for d in ds])
+        sticky = to_dev([d.sticky for d in ds])
+        logz, marg, st = K.pcfg_fb(root, rules, emis, sticky, marginals)
+        out = None
+        if marginals:
+            mg = to_host(marg).astype(np.float64)
+            out = [{"sticky": mg[i]} for i in range(len(ds))]
+        return Result(to_host(logz), to_host(st), out, self.vacuous_msg)
+
+    def argmax(self, ds):
+        from .errors import UnsupportedInference
+
+        raise UnsupportedInference("PCFG argmax is not on the GPU path yet")
+
+
 _BACKENDS = {
+    PCFG: PCFGBackend(),
     SpanningTreeCRF: SpanningBackend(),
     TreeCRF: TreeBackend(),
     CTCDist: CTCBackend(),

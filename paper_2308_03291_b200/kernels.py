@@ -248,3 +248,28 @@ def kuhlmann(adjacency, single_root: bool = False):
                           stream_ptr(dev))
     _lib.check(rc, "sdb_kuhlmann")
     return heads, score, status
+
+
+# ------------------------------------------------------------------- PCFG
+
+
+def pcfg_fb(root, rules, emissions, sticky=None, marginals: bool = True):
+    """constituency.py:246-340 batched: root [B,NT], rules [B,NT,S,S],
+    emissions [B,n,PT], sticky [B,n,n] | None -> (logz [B] f64,
+    span marginals [B,n,n] | None, status)."""
+    lib = _lib.load()
+    root = f32(root, "root")
+    rules = f32(rules, "binary_rules")
+    emis = f32(emissions, "emissions")
+    st_in = f32(sticky, "sticky") if sticky is not None else None
+    B, NT = root.shape
+    n, PT = emis.shape[1], emis.shape[2]
+    dev = root.device
+    logz = torch.empty(B, dtype=torch.float64, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    marg = torch.empty(B, n, n, dtype=torch.float32, device=dev) if marginals else None
+    ws = workspace(lib.sdb_pcfg_fb_workspace(B, n, NT, PT), dev)
+    rc = lib.sdb_pcfg_fb(ptr(root), ptr(rules), ptr(emis), ptr(st_in), B, n, NT, PT, ptr(logz), ptr(marg),
+                         ptr(status), ptr(ws), ws.numel(), stream_ptr(dev))
+    _lib.check(rc, "sdb_pcfg_fb")
+    return logz, marg, status

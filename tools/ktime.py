@@ -88,6 +88,18 @@ def eisner():
     print("kuhlmann ms %.4f" % bench(lambda: K.kuhlmann(adj), iters=5))
 
 
+
+def pcfg():
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+    from golden.builders import batch_pcfg
+    root, rules, emis = batch_pcfg(5000, 128, 64, 32, 32)
+    dv = lambda x: torch.as_tensor(x, dtype=torch.float32).cuda()  # noqa: E731
+    root, rules, emis = dv(root), dv(rules), dv(emis)
+    t = bench(lambda: K.pcfg_fb(root, rules, emis), iters=3, warm=1)
+    print("pcfg B=128 n=64 NT=PT=32 ms %.3f -> %.0f struct/s" % (t, 128 / t * 1e3))
+    print("pcfg logz ms %.3f" % bench(lambda: K.pcfg_fb(root, rules, emis, marginals=False), iters=3, warm=1))
+
+
 if __name__ == "__main__":
     fams = sys.argv[1:] or ["chain", "nw", "ctc"]
     main(fams)
