@@ -166,6 +166,23 @@ int sdb_pcfg_fb(const float* root, const float* rules, const float* emissions, c
                 int32_t n, int32_t NT, int32_t PT, double* logz, float* span_marg, int32_t* status,
                 void* workspace, size_t ws_bytes, void* stream);
 
+/* ----------------------------------------------------------- semi-Markov --
+ * SemiMarkovCRF (chain.py:214-247): segment_potentials [B,n,s,m,m]
+ * (start, width-1, prev label, label); virtual start label 0.
+ *
+ * sdb_semimarkov_fb replaces _sm_forward/_sm_backward/
+ * semi_markov_log_partition/semi_markov_marginals (chain.py:250-298):
+ * logz [B]; marg [B,n,s,m,m] nullable.  No workspace.
+ * sdb_semimarkov_viterbi replaces semi_markov_argmax (chain.py:301-327):
+ * segments [B,n,4] int32 rows (start, width, prev, label) in order,
+ * num_segments [B], score [B]. */
+int sdb_semimarkov_fb(const float* segment_potentials, int64_t B, int32_t n, int32_t s, int32_t m, double* logz,
+                      float* marg, int32_t* status, void* stream);
+size_t sdb_semimarkov_viterbi_workspace(int64_t B, int32_t n, int32_t s, int32_t m);
+int sdb_semimarkov_viterbi(const float* segment_potentials, int64_t B, int32_t n, int32_t s, int32_t m,
+                           int32_t* segments, int32_t* num_segments, double* score, int32_t* status,
+                           void* workspace, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

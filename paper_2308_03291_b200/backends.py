@@ -382,7 +382,48 @@ class PCFGBackend(Backend):
         raise UnsupportedInference("PCFG argmax is not on the GPU path yet")
 
 
+# ------------------------------------------------------------ semi-Markov
+
+
+class SemiMarkovBackend(Backend):
+    """chain.py:214-327 on sdb_semimarkov_fb / sdb_semimarkov_viterbi."""
+
+    vacuous_msg = "no labeled segmentation has finite score"
+
+    def batch_key(self, d):
+        return (d.n, d.s, d.m)
+
+    def algo(self, d):
+        return "semi-markov-forward"
+
+    def argmax_algo(self, d):
+        return "semi-markov-viterbi"
+
+    def run(self, ds, marginals=True, full=False):
+        th = to_dev([d.segment_potentials for d in ds])
+        logz, marg, st = K.semimarkov_fb(th, marginals)
+        out = None
+        if marginals:
+            mg = to_host(marg).astype(np.float64)
+            out = [{"segment_potentials": mg[i]} for i in range(len(ds))]
+        return Result(to_host(logz), to_host(st), out, self.vacuous_msg)
+
+    def argmax(self, ds):
+        th = to_dev([d.segment_potentials for d in ds])
+        seg, cnt, score, st = K.semimarkov_viterbi(th)
+        seg, cnt = to_host(seg), to_host(cnt)
+
+        def build(i):
+            mask = np.zeros_like(ds[i].segment_potentials)
+            for s0, w, p, l in seg[i][: cnt[i]]:
+                mask[s0, w - 1, p, l] = 1.0
+            return {"segment_potentials": mask}
+
+        return ArgmaxResult(to_host(st), build, self.vacuous_msg)
+
+
 _BACKENDS = {
+    SemiMarkovCRF: SemiMarkovBackend(),
     PCFG: PCFGBackend(),
     SpanningTreeCRF: SpanningBackend(),
     TreeCRF: TreeBackend(),

@@ -273,3 +273,38 @@ def pcfg_fb(root, rules, emissions, sticky=None, marginals: bool = True):
                          ptr(status), ptr(ws), ws.numel(), stream_ptr(dev))
     _lib.check(rc, "sdb_pcfg_fb")
     return logz, marg, status
+
+
+# ------------------------------------------------------------ semi-Markov
+
+
+def semimarkov_fb(segment_potentials, marginals: bool = True):
+    """chain.py:250-298 batched: [B,n,s,m,m] -> (logz, marg | None, status)."""
+    lib = _lib.load()
+    th = f32(segment_potentials, "segment_potentials")
+    B, n, s, m, _ = th.shape
+    dev = th.device
+    logz = torch.empty(B, dtype=torch.float64, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    marg = torch.empty_like(th) if marginals else None
+    rc = lib.sdb_semimarkov_fb(ptr(th), B, n, s, m, ptr(logz), ptr(marg), ptr(status), stream_ptr(dev))
+    _lib.check(rc, "sdb_semimarkov_fb")
+    return logz, marg, status
+
+
+def semimarkov_viterbi(segment_potentials):
+    """chain.py:301-327 batched -> (segments [B,n,4] int32, num_segments [B],
+    score [B], status)."""
+    lib = _lib.load()
+    th = f32(segment_potentials, "segment_potentials")
+    B, n, s, m, _ = th.shape
+    dev = th.device
+    seg = torch.zeros(B, n, 4, dtype=torch.int32, device=dev)
+    cnt = torch.empty(B, dtype=torch.int32, device=dev)
+    score = torch.empty(B, dtype=torch.float64, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    ws = workspace(lib.sdb_semimarkov_viterbi_workspace(B, n, s, m), dev)
+    rc = lib.sdb_semimarkov_viterbi(ptr(th), B, n, s, m, ptr(seg), ptr(cnt), ptr(score), ptr(status), ptr(ws),
+                                    ws.numel(), stream_ptr(dev))
+    _lib.check(rc, "sdb_semimarkov_viterbi")
+    return seg, cnt, score, status
