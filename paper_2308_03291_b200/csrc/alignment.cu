@@ -1,344 +1,448 @@
 // Monotone (Needleman-Wunsch) alignment CRF: log-partition, move marginals,
 // max-plus argmax.
 //
-// Reference: structdist alignment.py:62-143 (_nw_forward, _nw_backward,
-// nw_marginals, _nw_walk, _nw_max_forward).  Moves are scored on arrival:
-// DIAG=0 from (i-1,j-1), DOWN=1 from (i-1,j), RIGHT=2 from (i,j-1).
+// Reference: structdist alignment.py:62-167 (_nw_forward, _nw_backward,
+// nw_marginals, _nw_walk, _nw_max_forward, nw_argmax).  Moves are scored on
+// arrival: DIAG=0 from (i-1,j-1), DOWN=1 from (i-1,j), RIGHT=2 from (i,j-1).
 // Layout per instance: theta [n+1][m+1][3] fp32 row-major.
 //
-// Parallel schedule (one CTA per instance, NW = ceil((m+1)/32) warps):
+// Schedule (one CTA per instance, NW = ceil((m+1)/32) warps):
 //   * warp w owns a strip of 32 columns; lane l processes row i at local step
 //     s = i + l (skewed wavefront), so its left neighbour (lane l-1) finished
-//     the same row one step earlier -> warp shuffles, no barriers;
-//   * warps are pipelined with a lag of LAG steps and exchange the strip
-//     boundary column through a small shared ring; one __syncthreads every
-//     kSync steps makes the ring visible (LAG = 32 + kSync - 1);
+//     the same row one step earlier -> one warp shuffle per step, no barrier;
+//   * warps are pipelined with a lag of kLag steps and exchange the strip
+//     boundary column through a small shared ring; one __syncthreads per
+//     8-step block makes it visible (lag >= 32 + 7).  (A flag-based
+//     producer/consumer variant without barriers measured 3x slower: the
+//     CTA fence waits on the in-flight cp.async prefetches.);
 //   * potentials stream through a per-lane delay line in shared memory: at
-//     step s every lane cp.async-loads row s+P of ITS column (the whole warp
+//     step s every lane cp.async-loads row s+8 of ITS column (the whole warp
 //     loads one contiguous 384-byte row segment -> coalesced) and consumes
-//     row s-l from the delay line.  The marginal of a cell overwrites its
-//     potential in the delay line and is written back, again one coalesced
-//     row segment per step, 32 steps later;
+//     row s-l.  A cell's marginals overwrite its potentials in the delay line
+//     and are written back 32 steps later, again as one row segment;
+//   * log values are fp32 in log2 units carried as (v, O), value = v + O with
+//     an integer offset O re-chosen every step (O += rint(max)); messages carry
+//     their offset and receivers convert with an exact integer difference, so
+//     no fp64 and no precision loss at |log Z| ~ 10^3;
 //   * marginals: phase A runs the backward recurrence on the flipped grid
 //     (columns padded to 32*NW so flipping maps warps/lanes onto mirrored
 //     warps/lanes) and stores beta as fp32 offsets from a per-(warp,step)
-//     fp64 base in the same strip-diagonal layout the forward pass reads;
-//     phase B runs the forward recurrence and emits every marginal as
-//     exp(t_k - M) * exp(M + beta - Z), reusing the lse's own exponentials.
-//   Log values are carried in fp64 (exact sums); exp/log run in fp32 MUFU on
-//   small differences.
+//     integer reference in the strip layout the forward pass reads; phase B
+//     runs the forward recurrence and emits e_k * exp2(M + beta - Z) from the
+//     lse's own exponentials.
+// The max-plus argmax runs the same skew in fp64 (exact sums in the
+// reference's order) with per-cell argmax choices and a backtrack kernel.
 #include "common.cuh"
 
 namespace {
 
-constexpr int kR = 48;      // delay-line rows per warp (> 32 + kP)
-constexpr int kP = 8;       // prefetch distance in steps
-constexpr int kSync = 4;    // __syncthreads every kSync global steps
-constexpr int kLag = 32 + kSync - 1;
-constexpr int kRB = 32;     // strip-boundary ring (rows)
-constexpr int kRP = 16;     // beta prefetch ring (steps)
+constexpr int kR = 48;    // delay-line rows per warp (> 32 + kP, multiple of kBlk)
+constexpr int kP = 8;     // prefetch distance in steps
+constexpr int kBlk = 8;   // steps per progress-publication block
+constexpr int kRB = 64;   // strip-boundary ring rows
+constexpr int kRP = 16;   // beta prefetch ring (steps)
+constexpr int kLag = 40;  // warp-to-warp lag: >= 32 + kBlk - 1 and a multiple of kBlk, so every warp
+                          // reaches the per-block barrier at the same phase of its own schedule
+static_assert(kR % kBlk == 0 && kP % kBlk == 0 && kLag % kBlk == 0 && kLag >= 32 + kBlk - 1, "alignment");
 
-__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp4p(uint32_t saddr, const void* gmem, bool pred) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p cp.async.ca.shared.global [%0], [%1], 4;\n}\n" ::"r"(saddr),
+      "l"(gmem), "r"((int)pred));
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-__device__ __forceinline__ double shfl_up_d(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
+__device__ __forceinline__ int mod_pos(int x, int R) {
+  const int r = x % R;
+  return r < 0 ? r + R : r;
+}
 
 struct NwShared {
-  float* ring;    // [NW][kR][3][32]
-  double* bnd0;   // [NW][kRB]
-  double* bnd1;   // [NW][kRB]
-  float* bq;      // [NW][kRP][32]
-  double* bqb;    // [NW][kRP]
+  float* ring;   // [NW][kR][3][32]
+  float2* bnd0;  // [NW][kRB]
+  float2* bnd1;  // [NW][kRB]
+  float* bq;     // [NW][kRP][32]
+  float* bk;     // [NW][kRP]
+  int* prog;     // [NW] last completed local step
 };
 
 __device__ NwShared nw_carve(char* base, int NW) {
   NwShared s;
   s.ring = (float*)base;
-  base += (size_t)NW * kR * 96 * sizeof(float);
-  s.bnd0 = (double*)base;
-  base += (size_t)NW * kRB * sizeof(double);
-  s.bnd1 = (double*)base;
-  base += (size_t)NW * kRB * sizeof(double);
-  s.bqb = (double*)base;
-  base += (size_t)NW * kRP * sizeof(double);
+  base += (size_t)NW * kR * 96 * 4;
+  s.bnd0 = (float2*)base;
+  base += (size_t)NW * kRB * 8;
+  s.bnd1 = (float2*)base;
+  base += (size_t)NW * kRB * 8;
   s.bq = (float*)base;
+  base += (size_t)NW * kRP * 32 * 4;
+  s.bk = (float*)base;
+  base += (size_t)NW * kRP * 4;
+  s.prog = (int*)base;
   return s;
 }
 
 size_t nw_smem_bytes(int NW) {
-  return (size_t)NW * kR * 96 * 4 + (size_t)NW * kRB * 16 + (size_t)NW * kRP * 8 + (size_t)NW * kRP * 32 * 4;
+  return (size_t)NW * kR * 96 * 4 + (size_t)NW * kRB * 16 + (size_t)NW * kRP * 33 * 4 + (size_t)NW * 4 + 64;
 }
 
-// lse of three fp64 log terms; returns (M, e0, e1, e2, sum) with e_k = exp(t_k - M)
-struct Lse3 {
-  double M;
-  float e0, e1, e2, s;
+struct VO {
+  float v, o;
 };
-__device__ __forceinline__ Lse3 lse3(double t0, double t1, double t2) {
-  Lse3 r;
-  r.M = fmax(fmax(t0, t1), t2);
-  if (r.M == ninfd()) {
-    r.e0 = r.e1 = r.e2 = 0.f;
-    r.s = 0.f;
-  } else {
-    r.e0 = ex2((float)(t0 - r.M) * SDB_LOG2E);
-    r.e1 = ex2((float)(t1 - r.M) * SDB_LOG2E);
-    r.e2 = ex2((float)(t2 - r.M) * SDB_LOG2E);
-    r.s = r.e0 + r.e1 + r.e2;
-  }
-  return r;
-}
-__device__ __forceinline__ double lse3_val(const Lse3& r) {
-  return r.M == ninfd() ? ninfd() : r.M + (double)(lg2(r.s) * SDB_LN2);
+__device__ __forceinline__ float rel(VO x, float o) { return x.v + (x.o - o); }
+
+// log-sum-exp of three log2-unit terms, branch-free: value in the frame
+// shifted by r = rint(M) (exact); e_k = exp2(t_k - Mc).  All -inf -> -inf, r = 0.
+struct L3 {
+  float v, r, Mc, e0, e1, e2;
+};
+__device__ __forceinline__ L3 lse3r(float t0, float t1, float t2) {
+  L3 o;
+  const float M = fmaxf(fmaxf(t0, t1), t2);
+  o.Mc = fmaxf(M, -1e30f);
+  o.r = (M > -1e30f) ? rintf(M) : 0.f;
+  o.e0 = ex2(t0 - o.Mc);
+  o.e1 = ex2(t1 - o.Mc);
+  o.e2 = ex2(t2 - o.Mc);
+  o.v = (o.Mc - o.r) + lg2(o.e0 + o.e1 + o.e2);  // lg2(0) = -inf
+  return o;
 }
 
-// ------------------------------------------------------------------------
-// Phase A: backward recurrence on the flipped grid, push form.  Stores
-// beta(i,j) as fp32 offsets in the forward strip-diagonal layout
-// wsb[w][s][l] (+ fp64 base wsbase[w][s]); returns Z = beta(0,0) via *zsh.
-// ------------------------------------------------------------------------
-__device__ void nw_phase_backward(const float* __restrict__ th, int n, int m, int NW, NwShared sh,
-                                  float* __restrict__ wsb, double* __restrict__ wsbase, double* zsh) {
+// =========================================================== phase A
+// Backward recurrence on the flipped grid (push form).  Stores beta(i,j) as
+// wsb[w][s][l] = b + (O - K[w][s]) in the FORWARD strip layout (K = warp max
+// offset of the step); returns Z = beta(0,0) as (zint, zfrac).
+template <bool kCheck>
+__device__ void nw_backward(const float* __restrict__ th, int n, int m, int NW, const NwShared& sh,
+                            float* __restrict__ wsb, float* __restrict__ wsk, float* zint, float* zfrac,
+                            int* bad_flag) {
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const int mp = 32 * NW - 1;
-  const int jf = 32 * w + l;      // flipped column
-  const int jo = mp - jf;         // original column
+  const int jo = mp - (32 * w + l);
   const bool col_ok = jo <= m;
   const int steps = n + 32;
-  const int G = steps + (NW - 1) * kLag;
+  const int nblk = (steps + (NW - 1) * kLag + kP + kBlk - 1) / kBlk;
   const size_t rowstride = (size_t)(m + 1) * 3;
-  float* ring = sh.ring + (size_t)w * kR * 96;
+  const uint32_t ring_u = smem_u32(sh.ring + (size_t)w * kR * 96) + 4u * l;
+  const float* ring_l = sh.ring + (size_t)w * kR * 96 + l;
   const int wf = NW - 1 - w, lf = 31 - l;
-
-  double pDn = ninfd(), pR = ninfd(), pD = ninfd(), savedD = ninfd();
-  for (int g = -kP; g < G; ++g) {
-    const int s = g - w * kLag;
-    // prefetch flipped row s+kP (original row n-(s+kP)) of this lane's column
-    {
-      const int rp = s + kP;
-      if (rp >= 0 && rp <= n && col_ok) {
-        const float* src = th + (size_t)(n - rp) * rowstride + (size_t)jo * 3;
-        float* dst = ring + (rp % kR) * 96 + l;
-        cp_async4(dst, src);
-        cp_async4(dst + 32, src + 1);
-        cp_async4(dst + 64, src + 2);
+  const float* src_col = th + (size_t)(col_ok ? jo : m) * 3;
+  VO pDn{ninf(), 0.f}, pR{ninf(), 0.f}, pD{ninf(), 0.f}, savedD{ninf(), 0.f};
+  float O = 0.f;
+  int bad = 0;
+  for (int blk = 0; blk < nblk; ++blk) {
+    const int s0 = -kP - w * kLag + blk * kBlk;
+    const int pbase = mod_pos(s0 + kP, kR);
+    const int cbase = mod_pos(s0 - l, kR);
+#pragma unroll
+    for (int k = 0; k < kBlk; ++k) {
+      const int s = s0 + k;
+      {  // prefetch flipped row s + kP (original row n - (s + kP)) of this lane's column
+        const int rp = s + kP;
+        const bool pv = (rp >= 0) & (rp <= n);
+        const float* src = src_col + (size_t)(pv ? n - rp : 0) * rowstride;
+        const uint32_t dst = ring_u + (uint32_t)(pbase + k) * 384u;
+        cp4p(dst, src, pv);
+        cp4p(dst + 128, src + 1, pv);
+        cp4p(dst + 256, src + 2, pv);
+        cp_commit();
       }
-      cp_commit();
-    }
-    if (s >= 0 && s < steps) {
-      cp_wait<kP>();
-      const int ip = s - l;  // flipped row
-      double recvR = shfl_up_d(pR), recvD = shfl_up_d(pD);
-      if (l == 0) {
-        if (w == 0 || ip < 0 || ip > n) {
-          recvR = ninfd();
-          recvD = ninfd();
-        } else {
-          recvR = sh.bnd0[w * kRB + (ip % kRB)];
-          recvD = sh.bnd1[w * kRB + (ip % kRB)];
+      if (s >= 0 && s < steps) {
+        cp_wait<kP>();
+        const int ip = s - l;
+        VO rR, rD;
+        rR.v = __shfl_up_sync(0xffffffffu, pR.v, 1);
+        rR.o = __shfl_up_sync(0xffffffffu, pR.o, 1);
+        rD.v = __shfl_up_sync(0xffffffffu, pD.v, 1);
+        rD.o = __shfl_up_sync(0xffffffffu, pD.o, 1);
+        const bool inrow = (ip >= 0) & (ip <= n);
+        if (l == 0) {
+          const float2 a = sh.bnd0[w * kRB + (ip & (kRB - 1))], d = sh.bnd1[w * kRB + (ip & (kRB - 1))];
+          const bool ok = (w > 0) & inrow;
+          rR = ok ? VO{a.x, a.y} : VO{ninf(), 0.f};
+          rD = ok ? VO{d.x, d.y} : VO{ninf(), 0.f};
         }
-      }
-      const double inR = recvR, inD = savedD, inDn = pDn;
-      savedD = recvD;
-      double b = ninfd();
-      const bool valid = ip >= 0 && ip <= n && col_ok;
-      if (valid) {
-        const int io = n - ip;
-        const float* slot = ring + (ip % kR) * 96 + l;
-        const float t0 = slot[0], t1 = slot[32], t2 = slot[64];
-        if (io == n && jo == m) {
-          b = 0.0;
-        } else {
-          Lse3 r = lse3(inD, inDn, inR);
-          b = lse3_val(r);
+        const VO inR = rR, inD = savedD, inDn = pDn;
+        savedD = rD;
+        const bool valid = inrow & col_ok;
+        int cs = cbase + k;
+        cs -= (cs >= kR) ? kR : 0;
+        const float* slot = ring_l + cs * 96;
+        const float x0 = slot[0], x1 = slot[32], x2 = slot[64];
+        if (kCheck) bad |= valid & (bad_input(x0) | bad_input(x1) | bad_input(x2));
+        const L3 r = lse3r(rel(inD, O), rel(inDn, O), rel(inR, O));
+        const bool start = (ip == 0) & (jo == m);  // original cell (n, m)
+        float b = start ? 0.f : r.v;
+        O = start ? 0.f : O + r.r;
+        b = valid ? b : ninf();
+        pD = VO{fmaf(x0, SDB_LOG2E, b), O};
+        pDn = VO{fmaf(x1, SDB_LOG2E, b), O};
+        pR = VO{fmaf(x2, SDB_LOG2E, b), O};
+        if (valid && ip == n && jo == 0) {
+          *zint = O;
+          *zfrac = b;
         }
-        pD = b + (double)t0;
-        pDn = b + (double)t1;
-        pR = b + (double)t2;
-        if (io == 0 && jo == 0) *zsh = b;
-      } else {
-        pD = pDn = pR = ninfd();
+        if (l == 31 && w + 1 < NW && inrow) {
+          sh.bnd0[(w + 1) * kRB + (ip & (kRB - 1))] = make_float2(pR.v, pR.o);
+          sh.bnd1[(w + 1) * kRB + (ip & (kRB - 1))] = make_float2(pD.v, pD.o);
+        }
+        const float K0 = warp_max(b == ninf() ? ninf() : O);
+        const float K = (K0 == ninf()) ? 0.f : K0;
+        const size_t sf = (size_t)(n + 31 - s);
+        wsb[((size_t)wf * steps + sf) * 32 + lf] = (b == ninf()) ? ninf() : b + (O - K);
+        if (l == 0) wsk[(size_t)wf * steps + sf] = K;
       }
-      if (l == 31 && w + 1 < NW && ip >= 0 && ip <= n) {
-        sh.bnd0[(w + 1) * kRB + (ip % kRB)] = pR;
-        sh.bnd1[(w + 1) * kRB + (ip % kRB)] = pD;
-      }
-      // store beta into the forward strip layout: fwd warp wf, step n+31-s, lane 31-l
-      double base = warp_maxd(b);
-      if (base == ninfd()) base = 0.0;
-      const size_t sf = (size_t)(n + 31 - s);
-      wsb[((size_t)wf * steps + sf) * 32 + lf] = (b == ninfd()) ? ninf() : (float)(b - base);
-      if (l == 0) wsbase[(size_t)wf * steps + sf] = base;
     }
-    if (((g + 1) % kSync) == 0) __syncthreads();
+    __syncthreads();
   }
   cp_wait<0>();
-  __syncthreads();
+  if (kCheck && bad) atomicOr(bad_flag, 1);
 }
 
-// ------------------------------------------------------------------------
-// Phase B: forward recurrence (pull form).  kMarg: emit marginals using the
-// stored beta and Z.  kMax: max-plus with argmax choices (no marginals).
-// ------------------------------------------------------------------------
-template <bool kMarg, bool kMax>
-__device__ void nw_phase_forward(const float* __restrict__ th, int n, int m, int NW, NwShared sh,
-                                 const float* __restrict__ wsb, const double* __restrict__ wsbase, double Z,
-                                 float* __restrict__ marg, int8_t* __restrict__ choice, double* out_last,
-                                 int* bad_flag) {
+// =========================================================== phase B
+// Forward pull recurrence.  kMarg: emit marginals e_k * exp2(M + beta - Z).
+template <bool kMarg, bool kCheck>
+__device__ void nw_forward(const float* __restrict__ th, int n, int m, int NW, const NwShared& sh,
+                           const float* __restrict__ wsb, const float* __restrict__ wsk, float zint, float zfrac,
+                           float* __restrict__ marg, float* last_v, float* last_o, int* bad_flag) {
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const int j = 32 * w + l;
   const bool col_ok = j <= m;
   const int steps = n + 32;
-  const int G = steps + 1 + (NW - 1) * kLag;
+  const int nblk = (steps + 1 + (NW - 1) * kLag + kP + kBlk - 1) / kBlk;
   const size_t rowstride = (size_t)(m + 1) * 3;
-  float* ring = sh.ring + (size_t)w * kR * 96;
-  float* bq = sh.bq + (size_t)w * kRP * 32;
-  double* bqb = sh.bqb + (size_t)w * kRP;
-  const bool zok = !(Z == ninfd());
+  float* ring_l = sh.ring + (size_t)w * kR * 96 + l;
+  const uint32_t ring_u = smem_u32(sh.ring + (size_t)w * kR * 96) + 4u * l;
+  const float* bq = sh.bq + (size_t)w * kRP * 32 + l;
+  const float* bk = sh.bk + (size_t)w * kRP;
+  const uint32_t bq_u = smem_u32(bq), bk_u = smem_u32(bk);
+  const bool zok = zfrac != ninf();
   int bad = 0;
-
-  double aprev = ninfd(), cur = ninfd(), lprev = ninfd();
-  for (int g = -kP; g < G; ++g) {
-    const int s = g - w * kLag;
-    {
-      const int rp = s + kP;
-      if (rp >= 0 && rp <= n && col_ok) {
-        const float* src = th + (size_t)rp * rowstride + (size_t)j * 3;
-        float* dst = ring + (rp % kR) * 96 + l;
-        cp_async4(dst, src);
-        cp_async4(dst + 32, src + 1);
-        cp_async4(dst + 64, src + 2);
-      }
-      if (kMarg && rp >= 0 && rp < steps) {
-        cp_async4(bq + (rp % kRP) * 32 + l, wsb + ((size_t)w * steps + rp) * 32 + l);
-        if (l == 0) cp_async8(bqb + (rp % kRP), wsbase + (size_t)w * steps + rp);
-      }
-      cp_commit();
-    }
-    if (s >= 0 && s <= steps) {
-      cp_wait<kP>();
-      if (s < steps) {
-        const int i = s - l;
-        double left = shfl_up_d(cur);
-        if (l == 0) {
-          left = (w == 0 || i < 0 || i > n) ? ninfd() : sh.bnd0[w * kRB + (i % kRB)];
+  VO cur{ninf(), 0.f}, lprev{ninf(), 0.f};
+  float av = ninf(), O = 0.f;  // own previous cell (i-1, j) in frame O
+  const float* src_col = th + (size_t)(col_ok ? j : m) * 3;
+  float* dst_col = kMarg ? marg + (size_t)(col_ok ? j : 0) * 3 : nullptr;
+  const float* wsb_l = kMarg ? wsb + (size_t)w * steps * 32 + l : nullptr;
+  const float* wsk_w = kMarg ? wsk + (size_t)w * steps : nullptr;
+  for (int blk = 0; blk < nblk; ++blk) {
+    const int s0 = -kP - w * kLag + blk * kBlk;
+    const int pbase = mod_pos(s0 + kP, kR);
+    const int cbase = mod_pos(s0 - l, kR);
+    const int obase = mod_pos(s0 - 32, kR);
+#pragma unroll
+    for (int k = 0; k < kBlk; ++k) {
+      const int s = s0 + k;
+      {
+        const int rp = s + kP;
+        const bool pv = (rp >= 0) & (rp <= n);
+        const float* src = src_col + (size_t)(pv ? rp : 0) * rowstride;
+        const uint32_t dst = ring_u + (uint32_t)(pbase + k) * 384u;
+        cp4p(dst, src, pv);
+        cp4p(dst + 128, src + 1, pv);
+        cp4p(dst + 256, src + 2, pv);
+        if (kMarg) {
+          const bool bv = (rp >= 0) & (rp < steps);
+          const int rq = bv ? rp : 0;
+          cp4p(bq_u + (uint32_t)(rp & (kRP - 1)) * 128u, wsb_l + (size_t)rq * 32, bv);
+          cp4p(bk_u + (uint32_t)(rp & (kRP - 1)) * 4u, wsk_w + rq, bv & (l == 0));
         }
-        const double diag = lprev;
-        lprev = left;
-        const bool valid = i >= 0 && i <= n && col_ok;
-        double a = ninfd();
-        if (valid) {
-          float* slot = ring + (i % kR) * 96 + l;
-          const float t0 = slot[0], t1 = slot[32], t2 = slot[64];
-          bad |= bad_input(t0) | bad_input(t1) | bad_input(t2);
-          const double c0 = diag + (double)t0, c1 = aprev + (double)t1, c2 = left + (double)t2;
-          if (kMax) {
-            int k = 0;
-            double best = ninfd();
-            // first maximum among in-grid sources in DIAG, DOWN, RIGHT order (alignment.py:121-136)
-            bool first = true;
-            if (i > 0 && j > 0) { best = c0; k = 0; first = false; }
-            if (i > 0 && (first || c1 > best)) { best = c1; k = 1; first = false; }
-            if (j > 0 && (first || c2 > best)) { best = c2; k = 2; first = false; }
-            a = (i == 0 && j == 0) ? 0.0 : best;
-            choice[((size_t)w * steps + s) * 32 + l] = (int8_t)k;
-          } else if (i == 0 && j == 0) {
-            a = 0.0;
-            if (kMarg) slot[0] = slot[32] = slot[64] = 0.f;
-          } else {
-            Lse3 r = lse3(c0, c1, c2);
-            a = lse3_val(r);
-            if (kMarg) {
-              const float bt = bq[(s % kRP) * 32 + l];
-              const double bb = bqb[s % kRP];
-              float F = 0.f;
-              if (zok && r.M != ninfd() && bt != ninf()) F = ex2(((float)(r.M + bb - Z) + bt) * SDB_LOG2E);
-              slot[0] = r.e0 * F;
-              slot[32] = r.e1 * F;
-              slot[64] = r.e2 * F;
-            }
+        cp_commit();
+      }
+      if (s >= 0 && s <= steps) {
+        cp_wait<kP>();
+        if (s < steps) {
+          const int i = s - l;
+          VO left;
+          left.v = __shfl_up_sync(0xffffffffu, cur.v, 1);
+          left.o = __shfl_up_sync(0xffffffffu, cur.o, 1);
+          const bool inrow = (i >= 0) & (i <= n);
+          if (l == 0) {
+            const float2 a = sh.bnd0[w * kRB + (i & (kRB - 1))];
+            left = ((w > 0) & inrow) ? VO{a.x, a.y} : VO{ninf(), 0.f};
           }
-          aprev = a;
-          if (i == n && j == m) *out_last = a;
+          const VO diag = lprev;
+          lprev = left;
+          const bool valid = inrow & col_ok;
+          int cs = cbase + k;
+          cs -= (cs >= kR) ? kR : 0;
+          float* slot = ring_l + cs * 96;
+          const float x0 = slot[0], x1 = slot[32], x2 = slot[64];
+          if (kCheck) bad |= valid & (bad_input(x0) | bad_input(x1) | bad_input(x2));
+          const float t0 = fmaf(x0, SDB_LOG2E, rel(diag, O));
+          const float t1 = fmaf(x1, SDB_LOG2E, av);
+          const float t2 = fmaf(x2, SDB_LOG2E, rel(left, O));
+          const L3 r = lse3r(t0, t1, t2);
+          const bool origin = (i == 0) & (j == 0);
+          if (kMarg) {
+            const float bt = bq[(s & (kRP - 1)) * 32];
+            const float kk = bk[s & (kRP - 1)];
+            const float F = (zok & !origin) ? ex2((r.Mc + bt) + ((O + kk - zint) - zfrac)) : 0.f;
+            slot[0] = r.e0 * F;
+            slot[32] = r.e1 * F;
+            slot[64] = r.e2 * F;
+          }
+          float a = origin ? 0.f : r.v;
+          O = origin ? 0.f : O + r.r;
+          a = valid ? a : ninf();
+          av = a;
+          if (valid && i == n && j == m) {
+            *last_v = a;
+            *last_o = O;
+          }
+          cur = VO{a, O};
+          if (l == 31 && w + 1 < NW && inrow) sh.bnd0[(w + 1) * kRB + (i & (kRB - 1))] = make_float2(cur.v, cur.o);
         }
-        cur = valid ? a : ninfd();
-        if (l == 31 && w + 1 < NW && i >= 0 && i <= n) sh.bnd0[(w + 1) * kRB + (i % kRB)] = cur;
-      }
-      if (kMarg) {
-        const int r = s - 32;  // row completed by every lane of this warp
-        if (r >= 0 && r <= n && col_ok) {
-          const float* slot = ring + (r % kR) * 96 + l;
-          float* dst = marg + (size_t)r * rowstride + (size_t)j * 3;
-          dst[0] = slot[0];
-          dst[1] = slot[32];
-          dst[2] = slot[64];
+        if (kMarg) {
+          const int r = s - 32;  // row completed by every lane of this warp
+          if ((r >= 0) & (r <= n) & col_ok) {
+            const float* slot = ring_l + (obase + k) * 96;
+            float* dst = dst_col + (size_t)r * rowstride;
+            dst[0] = slot[0];
+            dst[1] = slot[32];
+            dst[2] = slot[64];
+          }
         }
       }
     }
-    if (((g + 1) % kSync) == 0) __syncthreads();
+    __syncthreads();
   }
   cp_wait<0>();
-  if (bad) atomicOr(bad_flag, 1);
+  if (kCheck && bad) atomicOr(bad_flag, 1);
 }
 
-// grid B, block 32*NW
-template <int kMode>  // 0 = logZ only, 1 = logZ + marginals, 2 = max-plus argmax
+__device__ void reset_prog(const NwShared& sh, int NW) {
+  for (int q = threadIdx.x; q < NW; q += blockDim.x) sh.prog[q] = -kP - 1;
+}
+
+template <int kMode>  // 0 = logZ only, 1 = logZ + marginals
 __global__ void nw_kernel(const float* __restrict__ theta, int n, int m, float* __restrict__ wsb_all,
-                          double* __restrict__ wsbase_all, int8_t* __restrict__ choice_all,
-                          double* __restrict__ logz, float* __restrict__ marg_all, int32_t* __restrict__ path,
-                          double* __restrict__ score, int32_t* __restrict__ status) {
+                          float* __restrict__ wsk_all, double* __restrict__ logz, float* __restrict__ marg_all,
+                          int32_t* __restrict__ status) {
   extern __shared__ __align__(16) char smraw[];
-  __shared__ double zsh, lastsh;
+  __shared__ float zi, zf, lv, lo;
   __shared__ int badsh;
   const int NW = blockDim.x >> 5;
   const int b = blockIdx.x;
   NwShared sh = nw_carve(smraw, NW);
   const float* th = theta + (size_t)b * (n + 1) * (m + 1) * 3;
-  const int steps = n + 32;
-  const size_t wsz = (size_t)NW * steps;
+  const size_t wsz = (size_t)NW * (n + 32);
   if (threadIdx.x == 0) {
-    zsh = ninfd();
+    zi = 0.f;
+    zf = ninf();
+    lv = ninf();
+    lo = 0.f;
+    badsh = 0;
+  }
+  reset_prog(sh, NW);
+  __syncthreads();
+  if (kMode == 1) {
+    float* wsb = wsb_all + (size_t)b * wsz * 32;
+    float* wsk = wsk_all + (size_t)b * wsz;
+    nw_backward<true>(th, n, m, NW, sh, wsb, wsk, &zi, &zf, &badsh);
+    __syncthreads();
+    reset_prog(sh, NW);
+    __syncthreads();
+    nw_forward<true, false>(th, n, m, NW, sh, wsb, wsk, zi, zf, marg_all + (size_t)b * (n + 1) * (m + 1) * 3,
+                            &lv, &lo, &badsh);
+  } else {
+    nw_forward<false, true>(th, n, m, NW, sh, nullptr, nullptr, 0.f, ninf(), nullptr, &lv, &lo, &badsh);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double z = (lv == ninf()) ? ninfd() : ((double)lo + (double)lv) * (double)SDB_LN2;
+    status[b] = badsh ? SDB_ST_INVALID : (z == ninfd() ? SDB_ST_VACUOUS : SDB_ST_OK);
+    logz[b] = z;
+  }
+}
+
+// =========================================================== max-plus
+// fp64 max-plus over the same skew with CTA barriers (argmax is not on the
+// timed path); per-cell first-maximum choice in DIAG, DOWN, RIGHT order
+// among in-grid sources (alignment.py:121-136, 153-167).
+constexpr int kSyncM = 4;
+constexpr int kLagM = 32 + kSyncM - 1;
+
+__global__ void nw_max_kernel(const float* __restrict__ theta, int n, int m, int8_t* __restrict__ choice_all,
+                              double* __restrict__ score, int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) char smraw[];
+  __shared__ double lastsh;
+  __shared__ int badsh;
+  const int NW = blockDim.x >> 5;
+  const int b = blockIdx.x;
+  NwShared sh = nw_carve(smraw, NW);
+  double* bnd = reinterpret_cast<double*>(sh.bnd0);
+  const float* th = theta + (size_t)b * (n + 1) * (m + 1) * 3;
+  const int steps = n + 32;
+  int8_t* choice = choice_all + (size_t)b * NW * steps * 32;
+  if (threadIdx.x == 0) {
     lastsh = ninfd();
     badsh = 0;
   }
   __syncthreads();
-  if (kMode == 1) {
-    float* wsb = wsb_all + (size_t)b * wsz * 32;
-    double* wsbase = wsbase_all + (size_t)b * wsz;
-    nw_phase_backward(th, n, m, NW, sh, wsb, wsbase, &zsh);
-    __syncthreads();
-    nw_phase_forward<true, false>(th, n, m, NW, sh, wsb, wsbase, zsh,
-                                  marg_all + (size_t)b * (n + 1) * (m + 1) * 3, nullptr, &lastsh, &badsh);
-  } else if (kMode == 0) {
-    nw_phase_forward<false, false>(th, n, m, NW, sh, nullptr, nullptr, 0.0, nullptr, nullptr, &lastsh, &badsh);
-  } else {
-    int8_t* ch = choice_all + (size_t)b * wsz * 32;
-    nw_phase_forward<false, true>(th, n, m, NW, sh, nullptr, nullptr, 0.0, nullptr, ch, &lastsh, &badsh);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int j = 32 * w + l;
+  const bool col_ok = j <= m;
+  const int G = steps + (NW - 1) * kLagM;
+  const size_t rowstride = (size_t)(m + 1) * 3;
+  float* ring = sh.ring + (size_t)w * kR * 96;
+  int bad = 0;
+  double aprev = ninfd(), cur = ninfd(), lprev = ninfd();
+  for (int g = -kP; g < G; ++g) {
+    const int s = g - w * kLagM;
+    {
+      const int rp = s + kP;
+      const bool pv = (rp >= 0) & (rp <= n) & col_ok;
+      const float* src = th + (size_t)(pv ? rp : 0) * rowstride + (size_t)(col_ok ? j : 0) * 3;
+      const uint32_t dst = smem_u32(ring + mod_pos(rp, kR) * 96 + l);
+      cp4p(dst, src, pv);
+      cp4p(dst + 128, src + 1, pv);
+      cp4p(dst + 256, src + 2, pv);
+      cp_commit();
+    }
+    if (s >= 0 && s < steps) {
+      cp_wait<kP>();
+      const int i = s - l;
+      double left = __shfl_up_sync(0xffffffffu, cur, 1);
+      if (l == 0) left = (w == 0 || i < 0 || i > n) ? ninfd() : bnd[w * kRB + (i & (kRB - 1))];
+      const double diag = lprev;
+      lprev = left;
+      const bool valid = i >= 0 && i <= n && col_ok;
+      double a = ninfd();
+      if (valid) {
+        const float* slot = ring + mod_pos(i, kR) * 96 + l;
+        const float t0 = slot[0], t1 = slot[32], t2 = slot[64];
+        bad |= bad_input(t0) | bad_input(t1) | bad_input(t2);
+        const double c0 = diag + (double)t0, c1 = aprev + (double)t1, c2 = left + (double)t2;
+        int k = 0;
+        double best = ninfd();
+        bool first = true;
+        if (i > 0 && j > 0) { best = c0; k = 0; first = false; }
+        if (i > 0 && (first || c1 > best)) { best = c1; k = 1; first = false; }
+        if (j > 0 && (first || c2 > best)) { best = c2; k = 2; first = false; }
+        a = (i == 0 && j == 0) ? 0.0 : best;
+        choice[((size_t)w * steps + s) * 32 + l] = (int8_t)k;
+        aprev = a;
+        if (i == n && j == m) lastsh = a;
+      }
+      cur = valid ? a : ninfd();
+      if (l == 31 && w + 1 < NW && i >= 0 && i <= n) bnd[(w + 1) * kRB + (i & (kRB - 1))] = cur;
+    }
+    if (((g + 1) % kSyncM) == 0) __syncthreads();
   }
+  cp_wait<0>();
+  if (bad) atomicOr(&badsh, 1);
   __syncthreads();
   if (threadIdx.x == 0) {
     const double z = lastsh;
-    const int st = badsh ? SDB_ST_INVALID : (z == ninfd() ? SDB_ST_VACUOUS : SDB_ST_OK);
-    status[b] = st;
-    if (kMode == 2) {
-      score[b] = z;
-    } else {
-      logz[b] = z;
-    }
+    status[b] = badsh ? SDB_ST_INVALID : (z == ninfd() ? SDB_ST_VACUOUS : SDB_ST_OK);
+    score[b] = z;
   }
 }
 
-// backtrack kernel for the max-plus path: one thread per instance walks the
-// choices (strip layout) from (n, m) to (0, 0) and marks the path.
+// backtrack: one thread per instance walks the choices (strip layout) from
+// (n, m) to (0, 0) and marks the path.
 __global__ void nw_walk_kernel(const int8_t* __restrict__ choice_all, int n, int m, int NW, int64_t B,
                                const int32_t* __restrict__ status, int8_t* __restrict__ path_all) {
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -358,7 +462,7 @@ __global__ void nw_walk_kernel(const int8_t* __restrict__ choice_all, int n, int
 
 struct NwWs {
   float* wsb;
-  double* wsbase;
+  float* wsk;
   int8_t* choice;
 };
 
@@ -369,7 +473,7 @@ NwWs nw_carve_ws(void* base, int64_t B, int n, int m, int mode, size_t* bytes) {
   NwWs w{};
   if (mode == 1) {
     w.wsb = c.take<float>((size_t)B * wsz * 32);
-    w.wsbase = c.take<double>((size_t)B * wsz);
+    w.wsk = c.take<float>((size_t)B * wsz);
   }
   if (mode == 2) w.choice = c.take<int8_t>((size_t)B * wsz * 32);
   *bytes = c.used;
@@ -381,15 +485,20 @@ int nw_launch(const float* theta, int64_t B, int n, int m, NwWs ws, double* logz
               double* score, int32_t* status, cudaStream_t s) {
   const int NW = (m + 1 + 31) / 32;
   const size_t smem = nw_smem_bytes(NW);
-  if (cudaFuncSetAttribute(nw_kernel<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-    return SDB_ERR_CUDA;
-  nw_kernel<kMode><<<(unsigned)B, 32 * NW, smem, s>>>(theta, n, m, ws.wsb, ws.wsbase, ws.choice, logz, marg,
-                                                      nullptr, score, status);
-  SDB_CHECK_LAUNCH();
   if (kMode == 2) {
+    if (cudaFuncSetAttribute(nw_max_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return SDB_ERR_CUDA;
+    nw_max_kernel<<<(unsigned)B, 32 * NW, smem, s>>>(theta, n, m, ws.choice, score, status);
+    SDB_CHECK_LAUNCH();
     nw_walk_kernel<<<(unsigned)((B + 127) / 128), 128, 0, s>>>(ws.choice, n, m, NW, B, status, path);
     SDB_CHECK_LAUNCH();
+    return SDB_OK;
   }
+  constexpr int M2 = kMode == 1 ? 1 : 0;
+  if (cudaFuncSetAttribute(nw_kernel<M2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return SDB_ERR_CUDA;
+  nw_kernel<M2><<<(unsigned)B, 32 * NW, smem, s>>>(theta, n, m, ws.wsb, ws.wsk, logz, marg, status);
+  SDB_CHECK_LAUNCH();
   return SDB_OK;
 }
 
