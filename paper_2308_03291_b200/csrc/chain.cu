@@ -30,6 +30,7 @@ struct ChainWs {
   double* acum;   // [B][n] cumulative forward normalisers
   double* bcum;   // [B][n] cumulative backward normalisers
   int32_t* flags; // [B] forward status
+  int32_t* need;  // [B] 1 = recompute with the exact log-space path
 };
 
 __host__ ChainWs carve_chain(void* base, int64_t B, int n, int m, size_t* bytes) {
@@ -40,6 +41,7 @@ __host__ ChainWs carve_chain(void* base, int64_t B, int n, int m, size_t* bytes)
   w.acum = c.take<double>((size_t)B * n);
   w.bcum = c.take<double>((size_t)B * n);
   w.flags = c.take<int32_t>((size_t)B);
+  w.need = c.take<int32_t>((size_t)B);
   *bytes = c.used;
   return w;
 }
@@ -215,14 +217,472 @@ __global__ void __launch_bounds__(kThreads) chain_fwd_bwd_kernel(
   }
 }
 
+// ---------------------------------------------------------------------
+// Fast path for m <= 32 (the C1 shape): every step's m x m potentials are
+// prefetched kD steps ahead into a shared ring with cp.async (16-byte chunks
+// when the step is 16-byte aligned); the 8 warps split the rows (forward) or
+// rows-by-warp (backward) and warp 0 finishes the step with warp-level
+// reductions, so a step costs two CTA barriers and no global-load latency.
+constexpr int kD = 8;
+
+__device__ __forceinline__ void cpa16(float* dst, const float* src) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src));
+}
+__device__ __forceinline__ void cpa4(float* dst, const float* src) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(src));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cpa_wait_d() { asm volatile("cp.async.wait_group %0;\n" ::"n"(kD - 1)); }
+
+__device__ __forceinline__ void stage_step(float* dst, const float* src, int mm, bool v16) {
+  if (v16) {
+    for (int e = threadIdx.x; e < (mm >> 2); e += kThreads) cpa16(dst + 4 * e, src + 4 * e);
+  } else {
+    for (int e = threadIdx.x; e < mm; e += kThreads) cpa4(dst + e, src + e);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) chain_fwd_bwd_small_kernel(
+    const float* __restrict__ init, const float* __restrict__ trans, int n, int m, ChainWs ws,
+    double* __restrict__ logz, int32_t* __restrict__ status, int only_need) {
+  if (only_need && ws.need[blockIdx.x] == 0) return;
+  extern __shared__ __align__(16) float sm[];
+  const int mm = m * m;
+  float* stage = sm;                     // [kD][mm]
+  float* vec = stage + kD * mm;          // [32]
+  float* pm = vec + 32;                  // [kGroups][32]
+  float* ps = pm + kGroups * 32;         // [kGroups][32]
+  __shared__ int redi[kThreads / 32];
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float* th = trans + (size_t)b * (n - 1) * mm;
+  const bool v16 = ((mm & 3) == 0);
+  const bool fwd = blockIdx.y == 0;
+  int bad = 0;
+  // prologue prefetch: steps in processing order
+  for (int d = 0; d < kD; ++d) {
+    const int t = fwd ? d : n - 2 - d;
+    if (d < n - 1) stage_step(stage + d * mm, th + (size_t)t * mm, mm, v16);
+    cpa_commit();
+  }
+  if (fwd) {
+    float* al = ws.alpha + (size_t)b * n * m;
+    double* ac = ws.acum + (size_t)b * n;
+    double A = 0.0;
+    bool vac = false;
+    if (warp == 0) {
+      const float x = lane < m ? init[(size_t)b * m + lane] : ninf();
+      bad |= (lane < m) && bad_input(x);
+      float c = warp_max(x);
+      vac = (c == ninf());
+      A = vac ? 0.0 : (double)c;
+      if (vac) c = 0.f;
+      if (lane < m) {
+        vec[lane] = x - c;
+        al[lane] = x - c;
+      }
+      if (lane == 0) ac[0] = A;
+    }
+    for (int t = 0; t < n - 1; ++t) {
+      cpa_wait_d();
+      __syncthreads();  // step t resident; vec of step t visible
+      const float* tt = stage + (t % kD) * mm;
+      if (lane < m) {
+        Lse acc;
+        for (int a = warp; a < m; a += kGroups) {
+          const float x = tt[a * m + lane];
+          bad |= bad_input(x);
+          acc.add(vec[a] + x);
+        }
+        pm[warp * 32 + lane] = acc.m;
+        ps[warp * 32 + lane] = acc.s;
+      }
+      __syncthreads();  // partials visible; everybody is done reading slot t % kD and vec
+      {
+        const int tn = t + kD;
+        if (tn < n - 1) stage_step(stage + (t % kD) * mm, th + (size_t)tn * mm, mm, v16);
+        cpa_commit();
+      }
+      if (warp == 0) {
+        Lse acc;
+        if (lane < m) {
+#pragma unroll
+          for (int g = 0; g < kGroups; ++g) acc.merge(pm[g * 32 + lane], ps[g * 32 + lane]);
+        }
+        const float u = lane < m ? acc.result() : ninf();
+        float c = warp_max(u);
+        if (c == ninf()) vac = true;
+        if (vac) c = 0.f;
+        A += (double)c;
+        if (lane < m) {
+          const float v = vac ? ninf() : u - c;
+          vec[lane] = v;
+          al[(size_t)(t + 1) * m + lane] = v;
+        }
+        if (lane == 0) ac[t + 1] = A;
+      }
+    }
+    bad = block_or(bad, redi);
+    if (warp == 0) {
+      float z = ninf();
+      if (!vac) {
+        const float v = lane < m ? vec[lane] : ninf();
+        z = warp_lse(v);
+      }
+      if (lane == 0) {
+        vac = vac || z == ninf();
+        logz[b] = vac ? ninfd() : A + (double)z;
+        const int st = bad ? SDB_ST_INVALID : (vac ? SDB_ST_VACUOUS : SDB_ST_OK);
+        status[b] = st;
+        ws.flags[b] = st;
+      }
+    }
+  } else {
+    float* be = ws.beta + (size_t)b * n * m;
+    double* bc = ws.bcum + (size_t)b * n;
+    double Bc = 0.0;
+    if (warp == 0 && lane < m) {
+      vec[lane] = 0.f;
+      be[(size_t)(n - 1) * m + lane] = 0.f;
+    }
+    if (tid == 0) bc[n - 1] = 0.0;
+    for (int d = 0; d < n - 1; ++d) {
+      const int t = n - 2 - d;
+      cpa_wait_d();
+      __syncthreads();
+      const float* tt = stage + (d % kD) * mm;
+      const float bv = lane < m ? vec[lane] : ninf();
+      for (int a = warp; a < m; a += kGroups) {
+        const float x = lane < m ? tt[a * m + lane] + bv : ninf();
+        const float r = warp_lse(x);
+        if (lane == 0) pm[a] = r;
+      }
+      __syncthreads();
+      {
+        const int dn = d + kD;
+        if (dn < n - 1) stage_step(stage + (d % kD) * mm, th + (size_t)(n - 2 - dn) * mm, mm, v16);
+        cpa_commit();
+      }
+      if (warp == 0) {
+        const float r = lane < m ? pm[lane] : ninf();
+        float dd = warp_max(r);
+        if (dd == ninf()) dd = 0.f;
+        Bc += (double)dd;
+        if (lane < m) {
+          vec[lane] = r - dd;
+          be[(size_t)t * m + lane] = r - dd;
+        }
+        if (lane == 0) bc[t] = Bc;
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
+// ---------------------------------------------------------------------
+// Linear-space cluster kernel for m <= 32 (the C1 shape).
+//
+// One thread-block CLUSTER of two CTAs per instance: rank 0 runs the forward
+// recurrence, rank 1 the backward one, concurrently.  Inside a CTA:
+//   * warp 0 runs the recurrence in scaled LINEAR space: a step is a 32x32
+//     mat-vec of FMAs, u_x = sum_y M_t[x][y] v_y (lane x reads its row and the
+//     broadcast vector as float4), renormalised by its max (one REDUX + one
+//     MUFU.RCP), with the log scale accumulated in fp64 -- no exp/log on the
+//     critical path;
+//   * warps 1-7 are producers: they cp.async-stage the raw potentials two
+//     8-step blocks ahead and convert them to E_t = exp(theta_t - M_t)
+//     (M_t = the step max) one block ahead, plus per-column/row finiteness
+//     bitmasks that track exact reachability (a set bit whose linear value
+//     underflowed to 0 marks the instance for the exact log-space fallback);
+//   * the two CTAs meet in the middle (Q = transitions/2 rounded to a block):
+//     one cluster barrier, then both read the partner's boundary vector from
+//     global memory and form log Z;  after the meeting the producers also
+//     EMIT marginals for the transitions their own recurrence just passed
+//     (forward: t >= Q, backward: t < Q), e_t[a] * E_t[a][b] * f_(t+1)[b] *
+//     exp(M_t + c_t + d_(t+1) - Z), as coalesced 128-byte rows.
+// So the whole log_partition + marginals is one launch whose time is the
+// recurrence itself.  E rings are stored output-major (forward: E^T, backward:
+// E) with a 36-float pitch so the recurrence reads rows as float4.
+constexpr int kLB = kGroups - 1;        // steps per block = producer warps (one step each)
+constexpr int kEP = 36;                // padded row pitch (16-byte aligned rows for LDS.128)
+constexpr int kERing = 3 * kLB;        // E slots: blocks k-1 (emit), k (consume), k+1 (produce)
+constexpr int kRRing = 3 * kLB;        // raw slots: blocks k+1, k+2, k+3
+
+struct LinSmem {
+  float* raw;      // [kRRing][1024]
+  float* E;        // [kERing][32][kEP]
+  float* Mt;       // [kERing] step max (natural log)
+  uint32_t* mask;  // [kERing][32] finiteness masks (fwd: per column b bits over a; bwd: per row a bits over b)
+  float* hist;     // [kERing][32] own recurrence vectors by step slot
+  double* hsc;     // [kERing] their log scales
+};
+
+size_t lin_smem_bytes() {
+  return (size_t)kRRing * 1024 * 4 + (size_t)kERing * 32 * kEP * 4 + kERing * 4 + kERing * 32 * 4 +
+         kERing * 32 * 4 + kERing * 8 + 256;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    chain_lin_kernel(const float* __restrict__ init, const float* __restrict__ trans, int n, int m, ChainWs ws,
+                     double* __restrict__ logz, float* __restrict__ marg_init, float* __restrict__ marg_trans,
+                     int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) char smraw[];
+  LinSmem S;
+  {
+    char* p = smraw;
+    S.raw = (float*)p; p += (size_t)kRRing * 1024 * 4;
+    S.E = (float*)p; p += (size_t)kERing * 32 * kEP * 4;
+    S.hist = (float*)p; p += (size_t)kERing * 32 * 4;
+    S.mask = (uint32_t*)p; p += (size_t)kERing * 32 * 4;
+    S.Mt = (float*)p; p += kERing * 4;
+    p = (char*)(((uintptr_t)p + 7) & ~(uintptr_t)7);
+    S.hsc = (double*)p;
+  }
+  __shared__ double zsh;
+  __shared__ int flagsh;  // bit0 invalid input, bit1 fallback needed
+  __shared__ __align__(16) float vsh[32];
+  const int dir = blockIdx.x & 1;  // cluster rank: 0 forward, 1 backward
+  const int b = blockIdx.x >> 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int T = n - 1;
+  const int mm = m * m;
+  const float* th = trans + (size_t)b * T * mm;
+  float* vecs = dir == 0 ? ws.alpha + (size_t)b * n * m : ws.beta + (size_t)b * n * m;   // linear e_t / f_t
+  double* scs = dir == 0 ? ws.acum + (size_t)b * n : ws.bcum + (size_t)b * n;         // their log scales
+  const float* pvecs = dir == 0 ? ws.beta + (size_t)b * n * m : ws.alpha + (size_t)b * n * m;
+  const double* pscs = dir == 0 ? ws.bcum + (size_t)b * n : ws.acum + (size_t)b * n;
+  const int NB = (T + kLB - 1) / kLB;
+  const int Q = min(kLB * ((((T + 1) / 2) + kLB - 1) / kLB), T);  // meeting index (block aligned)
+  const int qmeet = Q / kLB;                                       // meeting after this many blocks
+  if (tid == 0) { flagsh = 0; zsh = ninfd(); }
+  // step index of processing position q
+  auto tstep = [&](int q) { return dir == 0 ? q : T - 1 - q; };
+  double Z = ninfd();
+  const bool v16 = ((mm & 3) == 0);
+  auto issue_raw = [&](int blk) {  // producers: cp.async block blk into raw slots
+    if (blk < NB) {
+      for (int k = 0; k < kLB; ++k) {
+        const int q = blk * kLB + k;
+        if (q >= T) break;
+        float* dst = S.raw + ((blk % 3) * kLB + k) * 1024;
+        const float* src = th + (size_t)tstep(q) * mm;
+        if (v16) {
+          for (int e = tid - 32; e < (mm >> 2); e += kThreads - 32) cpa16(dst + 4 * e, src + 4 * e);
+        } else {
+          for (int e = tid - 32; e < mm; e += kThreads - 32) cpa4(dst + e, src + e);
+        }
+      }
+    }
+    cpa_commit();
+  };
+  auto convert = [&](int blk) {  // producers: raw block blk -> E = exp(theta) slots (warp w-1: step w-1)
+    // No per-step max shift and no finiteness masks: anything the linear path cannot represent
+    // (|theta| beyond the fp32 exp range, -inf structure that zeroes a state, NaN/+inf input) shows
+    // up as a zero/non-finite state in the recurrence and sends the instance to the exact
+    // log-space fallback.
+    const int k = warp - 1;
+    const int q = blk * kLB + k;
+    if (q >= T) return;
+    const float* r = S.raw + ((blk % 3) * kLB + k) * 1024;
+    const int slot = q % kERing;
+    float* E = S.E + slot * 32 * kEP;
+    if (m == 32) {
+#pragma unroll
+      for (int a0 = 0; a0 < 32; a0 += 4) {  // rows a0..a0+3, lane = column b
+        const float x0 = r[(a0 + 0) * 32 + lane], x1 = r[(a0 + 1) * 32 + lane];
+        const float x2 = r[(a0 + 2) * 32 + lane], x3 = r[(a0 + 3) * 32 + lane];
+        const float4 e = make_float4(ex2(x0 * SDB_LOG2E), ex2(x1 * SDB_LOG2E), ex2(x2 * SDB_LOG2E),
+                                     ex2(x3 * SDB_LOG2E));
+        if (dir == 0) {
+          *reinterpret_cast<float4*>(E + lane * kEP + a0) = e;  // E^T[b][a0..a0+3]
+        } else {
+          E[(a0 + 0) * kEP + lane] = e.x;  // E[a][b]
+          E[(a0 + 1) * kEP + lane] = e.y;
+          E[(a0 + 2) * kEP + lane] = e.z;
+          E[(a0 + 3) * kEP + lane] = e.w;
+        }
+      }
+    } else {
+      for (int a = 0; a < 32; ++a) {
+        const float ev = (lane < m && a < m) ? ex2(r[a * m + lane] * SDB_LOG2E) : 0.f;
+        if (dir == 0) E[lane * kEP + a] = ev;
+        else E[a * kEP + lane] = ev;
+      }
+    }
+    if (lane == 0) S.Mt[slot] = 0.f;
+  };
+  // producers: emit the marginals of processing position q (one warp per position)
+  auto emit = [&](int q) {
+    if (q >= T) return;
+    const int t = tstep(q);
+    const int slot = q % kERing;
+    const float* E = S.E + slot * 32 * kEP;
+    const float* own = S.hist + (q % kERing) * 32;  // fwd: e_t, bwd: f_(t+1)
+    const double osc = S.hsc[q % kERing];
+    const int pt = dir == 0 ? t + 1 : t;            // partner: fwd needs f_(t+1), bwd needs e_t
+    const float pl = lane < m ? __ldcg(pvecs + (size_t)pt * m + lane) : 0.f;
+    const double psc = __ldcg(pscs + pt);
+    const float sf = fexp((float)((double)S.Mt[slot] + osc + psc - Z));
+    const float ol = own[lane];
+    float* out = marg_trans + ((size_t)b * T + t) * mm;
+#pragma unroll 8
+    for (int a = 0; a < 32; ++a) {
+      // element (a, lane) = e_t[a] * E_t[a][lane] * f_(t+1)[lane]
+      const float val = dir == 0 ? own[a] * E[lane * kEP + a] * pl
+                                 : __shfl_sync(0xffffffffu, pl, a) * E[a * kEP + lane] * ol;
+      if (lane < m && a < m) out[a * m + lane] = val * sf;
+    }
+  };
+  // ---- prologue
+  if (warp > 0) {
+    issue_raw(0);
+    issue_raw(1);
+    issue_raw(2);
+    asm volatile("cp.async.wait_group 2;\n" ::);
+    asm volatile("bar.sync 1, %0;\n" ::"r"(kThreads - 32));
+    convert(0);
+  }
+  // recurrence state (warp 0): linear vector v (lane holds component lane), scale
+  float v = 0.f;
+  double sc = 0.0;
+  uint32_t R = 0;
+  if (warp == 0) {
+    if (dir == 0) {
+      const float x = lane < m ? init[(size_t)b * m + lane] : ninf();
+      if (lane < m && bad_input(x)) atomicOr(&flagsh, 1);
+      const float mx = warp_max(x);
+      const float mc = (mx == ninf()) ? 0.f : mx;
+      v = lane < m ? fexp(x - mc) : 0.f;
+      sc = (double)mc;
+      R = __ballot_sync(0xffffffffu, lane < m && x > ninf());
+      if (lane < m) vecs[lane] = v;
+      if (lane == 0) scs[0] = sc;
+    } else {
+      v = lane < m ? 1.f : 0.f;
+      sc = 0.0;
+      R = __ballot_sync(0xffffffffu, lane < m);
+      if (lane < m) vecs[(size_t)T * m + lane] = v;
+      if (lane == 0) scs[T] = sc;
+    }
+    vsh[lane] = v;
+    S.hist[(0 % kERing) * 32 + lane] = v;  // slot of processing position 0 (the starting vector)
+    if (lane == 0) S.hsc[0] = sc;
+  }
+  __syncthreads();
+  for (int blk = 0; blk < NB; ++blk) {
+    if (warp == 0) {
+      // ---------------- recurrence over the block
+      for (int k = 0; k < kLB; ++k) {
+        const int q = blk * kLB + k;
+        if (q >= T) break;
+        const int slot = q % kERing;
+        const float* E = S.E + slot * 32 * kEP;
+        // u_x = sum_y M[x][y] v_y: v broadcast from shared memory, both operands as float4
+        const float4* vv = reinterpret_cast<const float4*>(vsh);
+        const float4* row = reinterpret_cast<const float4*>(E + lane * kEP);
+        float u0 = 0.f, u1 = 0.f, u2 = 0.f, u3 = 0.f;
+#pragma unroll
+        for (int y = 0; y < 8; ++y) {
+          const float4 e4 = row[y], v4 = vv[y];
+          u0 = fmaf(e4.x, v4.x, u0);
+          u1 = fmaf(e4.y, v4.y, u1);
+          u2 = fmaf(e4.z, v4.z, u2);
+          u3 = fmaf(e4.w, v4.w, u3);
+        }
+        float u = (u0 + u1) + (u2 + u3);
+        if (lane >= m) u = 0.f;
+        // a zero or non-finite state (underflow/overflow of the linear form, -inf structure,
+        // NaN/+inf input) -> exact log-space fallback for this instance
+        if (lane < m && !(u > 0.f && u < __int_as_float(0x7f800000))) atomicOr(&flagsh, 2);
+        // u >= 0: its float bits order like unsigned ints -> one REDUX for the max
+        const float umax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(u)));
+        float inv;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(umax));
+        inv = umax > 0.f ? inv : 0.f;
+        v = u * inv;
+        __syncwarp();
+        vsh[lane] = v;
+        __syncwarp();
+        // scale bookkeeping uses the factor actually applied (1/inv), so it is exact
+        sc += (double)S.Mt[slot] + (umax > 0.f ? -(double)flog(inv) : 0.0);
+        // the vector after processing position q belongs to step index (fwd) t+1 / (bwd) t
+        const int tv = dir == 0 ? q + 1 : T - 1 - q;
+        if (lane < m) vecs[(size_t)tv * m + lane] = v;
+        if (lane == 0) scs[tv] = sc;
+        S.hist[((q + 1) % kERing) * 32 + lane] = v;
+        if (lane == 0) S.hsc[(q + 1) % kERing] = sc;
+      }
+    } else {
+      // ---------------- producers: stage block blk+2, convert block blk+1, emit block blk-1
+      issue_raw(blk + 3);
+      asm volatile("cp.async.wait_group 2;\n" ::);
+      asm volatile("bar.sync 1, %0;\n" ::"r"(kThreads - 32));
+      if (blk + 1 < NB) convert(blk + 1);
+      if (marg_trans && blk - 1 >= qmeet && Z != ninfd()) emit((blk - 1) * kLB + (warp - 1));
+    }
+    __syncthreads();
+    if (blk + 1 == qmeet) {
+      // ---------------- meet in the middle: Z = c_Q + d_Q + log sum_a e_Q[a] f_Q[a]
+      __threadfence();
+      cluster_sync_all();
+      if (warp == 0) {
+        const float e = lane < m ? __ldcg(ws.alpha + ((size_t)b * n + Q) * m + lane) : 0.f;
+        const float f = lane < m ? __ldcg(ws.beta + ((size_t)b * n + Q) * m + lane) : 0.f;
+        const float dot = warp_sum(e * f);
+        if (lane == 0) {
+          const double cq = __ldcg(ws.acum + (size_t)b * n + Q), dq = __ldcg(ws.bcum + (size_t)b * n + Q);
+          zsh = (dot > 0.f) ? cq + dq + (double)flog(dot) : ninfd();
+        }
+      }
+      __syncthreads();
+      Z = zsh;
+      // transitions processed by BOTH passes before the meeting (t in [T-Q, Q-1]) are emitted
+      // here by the forward CTA while their E slots / history are still in the rings
+      if (dir == 0 && warp > 0 && marg_trans && Z != ninfd())
+        for (int q = T - Q + (warp - 1); q < Q; q += kLB) emit(q);
+    }
+  }
+  // emit the last block (its transitions are past the meeting when NB > qmeet)
+  if (warp > 0 && marg_trans && NB - 1 >= qmeet && Z != ninfd()) emit((NB - 1) * kLB + (warp - 1));
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  // ---------------- outputs: status / log Z (forward CTA), p_init (backward CTA)
+  const int fl = flagsh;
+  if (dir == 0 && tid == 0) {
+    // anything but a clean linear-space result (invalid input, vacuous, or a reachable state whose
+    // linear value underflowed) is recomputed by the exact log-space path for this instance
+    const bool need = (fl & 3) || Z == ninfd();
+    ws.need[b] = need ? 1 : 0;
+    ws.flags[b] = SDB_ST_OK;
+    status[b] = SDB_ST_OK;
+    logz[b] = Z;
+  }
+  if (dir == 1 && marg_init && warp == 0 && lane < m) {
+    // p_init[a] = exp(init[a] + beta_0[a] - Z), beta_0 = d_0 + log f_0
+    const float f0 = v;  // vector after the last backward step = f_0
+    const double d0 = sc;
+    float pv = 0.f;
+    if (Z != ninfd() && f0 > 0.f) pv = fexp(init[(size_t)b * m + lane] + (float)(d0 - Z)) * f0;
+    marg_init[(size_t)b * m + lane] = pv;
+  }
+}
+
 // marginals: grid (ceil((n-1)/kStepsPerBlock) + 1, B).  blockIdx.x == 0 also
 // writes p_init.
 constexpr int kStepsPerBlock = 8;
 
 __global__ void __launch_bounds__(kThreads) chain_marg_kernel(
     const float* __restrict__ init, const float* __restrict__ trans, int n, int m, ChainWs ws,
-    const double* __restrict__ logz, float* __restrict__ marg_init, float* __restrict__ marg_trans) {
+    const double* __restrict__ logz, float* __restrict__ marg_init, float* __restrict__ marg_trans, int only_need) {
   const int b = blockIdx.y;
+  if (only_need && ws.need[b] == 0) return;
   const int t0 = blockIdx.x * kStepsPerBlock;
   const size_t mm = (size_t)m * m;
   const bool ok = ws.flags[b] == SDB_ST_OK;
@@ -401,16 +861,48 @@ extern "C" int sdb_chain_fb(const float* init, const float* trans, int64_t B, in
   ChainWs ws = carve_chain(workspace, B, n, m, &need);
   if (!workspace || ws_bytes < need) return SDB_ERR_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
-  size_t smem = (size_t)m * 4 * (1 + 2 * kGroups);
-  if (smem > 48 * 1024) {
-    if (cudaFuncSetAttribute(chain_fwd_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+  const bool lin = (m <= 32) && (n - 1 >= 2 * kLB);
+  const size_t small_smem = (size_t)kD * m * m * 4 + (32 + 2 * kGroups * 32) * 4;
+  if (lin) {
+    const size_t smem = lin_smem_bytes();
+    if (cudaFuncSetAttribute(chain_lin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return SDB_ERR_CUDA;
+    chain_lin_kernel<<<(unsigned)(2 * B), kThreads, smem, s>>>(init, trans, n, m, ws, logz, marg_init, marg_trans,
+                                                               status);
+    SDB_CHECK_LAUNCH();
+    // exact log-space recomputation of the (rare) instances the linear path flagged
+    if (cudaFuncSetAttribute(chain_fwd_bwd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)small_smem) != cudaSuccess)
+      return SDB_ERR_CUDA;
+    chain_fwd_bwd_small_kernel<<<dim3((unsigned)B, 2), kThreads, small_smem, s>>>(init, trans, n, m, ws, logz,
+                                                                                  status, 1);
+    SDB_CHECK_LAUNCH();
+    if (marg_init || marg_trans) {
+      dim3 g((unsigned)((n - 1 + kStepsPerBlock - 1) / kStepsPerBlock), (unsigned)B);
+      chain_marg_kernel<<<g, kThreads, 0, s>>>(init, trans, n, m, ws, logz, marg_init, marg_trans, 1);
+      SDB_CHECK_LAUNCH();
+    }
+    return SDB_OK;
   }
-  chain_fwd_bwd_kernel<<<dim3((unsigned)B, 2), kThreads, smem, s>>>(init, trans, n, m, ws, logz, status);
+  if (m <= 32) {
+    if (cudaFuncSetAttribute(chain_fwd_bwd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)small_smem) != cudaSuccess)
+      return SDB_ERR_CUDA;
+    chain_fwd_bwd_small_kernel<<<dim3((unsigned)B, 2), kThreads, small_smem, s>>>(init, trans, n, m, ws, logz,
+                                                                                  status, 0);
+  } else {
+    size_t smem = (size_t)m * 4 * (1 + 2 * kGroups);
+    if (smem > 48 * 1024) {
+      if (cudaFuncSetAttribute(chain_fwd_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess)
+        return SDB_ERR_CUDA;
+    }
+    chain_fwd_bwd_kernel<<<dim3((unsigned)B, 2), kThreads, smem, s>>>(init, trans, n, m, ws, logz, status);
+  }
   SDB_CHECK_LAUNCH();
   if (marg_init || marg_trans) {
     dim3 g((unsigned)((n - 1 + kStepsPerBlock - 1) / kStepsPerBlock + (n == 1 ? 1 : 0)), (unsigned)B);
-    chain_marg_kernel<<<g, kThreads, 0, s>>>(init, trans, n, m, ws, logz, marg_init, marg_trans);
+    chain_marg_kernel<<<g, kThreads, 0, s>>>(init, trans, n, m, ws, logz, marg_init, marg_trans, 0);
     SDB_CHECK_LAUNCH();
   }
   return SDB_OK;

@@ -17,7 +17,8 @@ if fam == "nw":
 elif fam == "chain":
     init = torch.randn(32, 32, device="cuda", generator=g)
     tr = torch.randn(32, 127, 32, 32, device="cuda", generator=g)
-    fn = {"fb": lambda: K.chain_fb(init, tr), "vit": lambda: K.chain_viterbi(init, tr)}[mode]
+    fn = {"fb": lambda: K.chain_fb(init, tr), "lz": lambda: K.chain_fb(init, tr, False),
+          "vit": lambda: K.chain_viterbi(init, tr)}[mode]
 for _ in range(3):
     fn()
 torch.cuda.synchronize()
