@@ -409,6 +409,7 @@ constexpr int kLB = kGroups - 1;        // steps per block = producer warps (one
 constexpr int kEP = 36;                // padded row pitch (16-byte aligned rows for LDS.128)
 constexpr int kERing = 3 * kLB;        // E slots: blocks k-1 (emit), k (consume), k+1 (produce)
 constexpr int kRRing = 3 * kLB;        // raw slots: blocks k+1, k+2, k+3
+constexpr int kHRing = 4 * kLB;        // recurrence-vector history slots
 
 struct LinSmem {
   float* raw;      // [kRRing][1024]
@@ -421,7 +422,7 @@ struct LinSmem {
 
 size_t lin_smem_bytes() {
   return (size_t)kRRing * 1024 * 4 + (size_t)kERing * 32 * kEP * 4 + kERing * 4 + kERing * 32 * 4 +
-         kERing * 32 * 4 + kERing * 8 + 256;
+         kHRing * 32 * 4 + kHRing * 8 + 256;
 }
 
 __device__ __forceinline__ void cluster_sync_all() {
@@ -439,7 +440,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     char* p = smraw;
     S.raw = (float*)p; p += (size_t)kRRing * 1024 * 4;
     S.E = (float*)p; p += (size_t)kERing * 32 * kEP * 4;
-    S.hist = (float*)p; p += (size_t)kERing * 32 * 4;
+    S.hist = (float*)p; p += (size_t)kHRing * 32 * 4;
     S.mask = (uint32_t*)p; p += (size_t)kERing * 32 * 4;
     S.Mt = (float*)p; p += kERing * 4;
     p = (char*)(((uintptr_t)p + 7) & ~(uintptr_t)7);
@@ -466,18 +467,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   auto tstep = [&](int q) { return dir == 0 ? q : T - 1 - q; };
   double Z = ninfd();
   const bool v16 = ((mm & 3) == 0);
-  auto issue_raw = [&](int blk) {  // producers: cp.async block blk into raw slots
-    if (blk < NB) {
-      for (int k = 0; k < kLB; ++k) {
-        const int q = blk * kLB + k;
-        if (q >= T) break;
-        float* dst = S.raw + ((blk % 3) * kLB + k) * 1024;
-        const float* src = th + (size_t)tstep(q) * mm;
-        if (v16) {
-          for (int e = tid - 32; e < (mm >> 2); e += kThreads - 32) cpa16(dst + 4 * e, src + 4 * e);
-        } else {
-          for (int e = tid - 32; e < mm; e += kThreads - 32) cpa4(dst + e, src + e);
+  auto issue_raw = [&](int blk) {  // producer warp w-1 stages step w-1 of block blk (own cp.async group)
+    const int q = blk * kLB + (warp - 1);
+    if (blk < NB && q < T) {
+      float* dst = S.raw + ((blk % 3) * kLB + (warp - 1)) * 1024;
+      const float* src = th + (size_t)tstep(q) * mm;
+      if (v16) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int e = lane + 32 * i;
+          if (e < (mm >> 2)) cpa16(dst + 4 * e, src + 4 * e);
         }
+      } else {
+        for (int e = lane; e < mm; e += 32) cpa4(dst + e, src + e);
       }
     }
     cpa_commit();
@@ -524,8 +526,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int t = tstep(q);
     const int slot = q % kERing;
     const float* E = S.E + slot * 32 * kEP;
-    const float* own = S.hist + (q % kERing) * 32;  // fwd: e_t, bwd: f_(t+1)
-    const double osc = S.hsc[q % kERing];
+    const float* own = S.hist + (q % kHRing) * 32;  // fwd: e_t, bwd: f_(t+1)
+    const double osc = S.hsc[q % kHRing];
     const int pt = dir == 0 ? t + 1 : t;            // partner: fwd needs f_(t+1), bwd needs e_t
     const float pl = lane < m ? __ldcg(pvecs + (size_t)pt * m + lane) : 0.f;
     const double psc = __ldcg(pscs + pt);
@@ -546,7 +548,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     issue_raw(1);
     issue_raw(2);
     asm volatile("cp.async.wait_group 2;\n" ::);
-    asm volatile("bar.sync 1, %0;\n" ::"r"(kThreads - 32));
+    __syncwarp();
     convert(0);
   }
   // recurrence state (warp 0): linear vector v (lane holds component lane), scale
@@ -572,7 +574,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (lane == 0) scs[T] = sc;
     }
     vsh[lane] = v;
-    S.hist[(0 % kERing) * 32 + lane] = v;  // slot of processing position 0 (the starting vector)
+    S.hist[lane] = v;  // slot of processing position 0 (the starting vector)
     if (lane == 0) S.hsc[0] = sc;
   }
   __syncthreads();
@@ -616,14 +618,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int tv = dir == 0 ? q + 1 : T - 1 - q;
         if (lane < m) vecs[(size_t)tv * m + lane] = v;
         if (lane == 0) scs[tv] = sc;
-        S.hist[((q + 1) % kERing) * 32 + lane] = v;
-        if (lane == 0) S.hsc[(q + 1) % kERing] = sc;
+        S.hist[((q + 1) % kHRing) * 32 + lane] = v;
+        if (lane == 0) S.hsc[(q + 1) % kHRing] = sc;
       }
     } else {
-      // ---------------- producers: stage block blk+2, convert block blk+1, emit block blk-1
+      // ---------------- producers: stage block blk+3, convert block blk+1, emit block blk-1
       issue_raw(blk + 3);
       asm volatile("cp.async.wait_group 2;\n" ::);
-      asm volatile("bar.sync 1, %0;\n" ::"r"(kThreads - 32));
+      __syncwarp();
       if (blk + 1 < NB) convert(blk + 1);
       if (marg_trans && blk - 1 >= qmeet && Z != ninfd()) emit((blk - 1) * kLB + (warp - 1));
     }
