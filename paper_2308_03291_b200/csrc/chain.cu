@@ -840,6 +840,94 @@ __global__ void __launch_bounds__(kThreads) chain_viterbi_kernel(
   }
 }
 
+// Viterbi fast path (m <= 32): potentials staged kD steps ahead with cp.async, 8 warps split the
+// rows (first-maximum partials in ascending row order), warp 0 merges with the (value, lower index)
+// rule -- identical tie semantics to chain.py:106 -- and keeps backpointers in shared memory.
+__global__ void __launch_bounds__(kThreads) chain_viterbi_small_kernel(
+    const float* __restrict__ init, const float* __restrict__ trans, int n, int m, int32_t* __restrict__ tags,
+    double* __restrict__ score, int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) float smv[];
+  const int mm = m * m;
+  float* stage = smv;                                         // [kD][mm]
+  double* sc = reinterpret_cast<double*>(stage + kD * mm);    // [32]
+  double* pv = sc + 32;                                       // [kGroups][32]
+  int* pa = reinterpret_cast<int*>(pv + kGroups * 32);        // [kGroups][32]
+  uint8_t* back = reinterpret_cast<uint8_t*>(pa + kGroups * 32);  // [n][32]
+  __shared__ int redi[kThreads / 32];
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float* th = trans + (size_t)b * (n - 1) * mm;
+  const bool v16 = ((mm & 3) == 0);
+  int bad = 0;
+  for (int d = 0; d < kD; ++d) {
+    if (d < n - 1) stage_step(stage + d * mm, th + (size_t)d * mm, mm, v16);
+    cpa_commit();
+  }
+  if (warp == 0) {
+    const float x = lane < m ? init[(size_t)b * m + lane] : ninf();
+    bad |= (lane < m) && bad_input(x);
+    sc[lane] = lane < m ? (double)x : ninfd();
+  }
+  for (int t = 0; t < n - 1; ++t) {
+    cpa_wait_d();
+    __syncthreads();
+    const float* tt = stage + (t % kD) * mm;
+    if (lane < m) {
+      double best = ninfd();
+      int arg = 0x7fffffff;
+      for (int a = warp; a < m; a += kGroups) {
+        const float x = tt[a * m + lane];
+        bad |= bad_input(x);
+        const double v = sc[a] + (double)x;
+        if (v > best || (v == best && a < arg)) { best = v; arg = a; }
+      }
+      pv[warp * 32 + lane] = best;
+      pa[warp * 32 + lane] = arg;
+    }
+    __syncthreads();
+    {
+      const int tn = t + kD;
+      if (tn < n - 1) stage_step(stage + (t % kD) * mm, th + (size_t)tn * mm, mm, v16);
+      cpa_commit();
+    }
+    if (warp == 0 && lane < m) {
+      double best = pv[lane];
+      int arg = pa[lane];
+#pragma unroll
+      for (int g = 1; g < kGroups; ++g) {
+        const double v = pv[g * 32 + lane];
+        const int a = pa[g * 32 + lane];
+        if (v > best || (v == best && a < arg)) { best = v; arg = a; }
+      }
+      sc[lane] = best;
+      back[(size_t)(t + 1) * 32 + lane] = (uint8_t)(arg == 0x7fffffff ? 0 : arg);
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  bad = block_or(bad, redi);
+  if (warp == 0) {
+    double best = lane < m ? sc[lane] : ninfd();
+    int arg = lane < m ? lane : 0x7fffffff;
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+      if (ov > best || (ov == best && oa < arg)) { best = ov; arg = oa; }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      int32_t* tg = tags + (size_t)b * n;
+      const bool vac = (best == ninfd());
+      status[b] = bad ? SDB_ST_INVALID : (vac ? SDB_ST_VACUOUS : SDB_ST_OK);
+      score[b] = best;
+      int cur = vac ? 0 : arg;
+      tg[n - 1] = cur;
+      for (int t = n - 2; t >= 0; --t) {
+        cur = vac ? 0 : back[(size_t)(t + 1) * 32 + cur];
+        tg[t] = cur;
+      }
+    }
+  }
+}
+
 size_t viterbi_smem(int n, int m, bool with_back) {
   size_t s = (size_t)m * 8 + (size_t)kGroups * m * 12;
   if (with_back) s += (size_t)n * m * 2;
@@ -922,6 +1010,18 @@ extern "C" int sdb_chain_viterbi(const float* init, const float* trans, int64_t 
     return SDB_ERR_ARG;
   if (B == 0) return SDB_OK;
   if (!workspace || ws_bytes < sdb_chain_viterbi_workspace(B, n, m)) return SDB_ERR_WORKSPACE;
+  if (m <= 32) {
+    const size_t smem = (size_t)kD * m * m * 4 + 32 * 8 + kGroups * 32 * 12 + (size_t)n * 32 + 64;
+    if (smem <= 200 * 1024) {
+      if (cudaFuncSetAttribute(chain_viterbi_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess)
+        return SDB_ERR_CUDA;
+      chain_viterbi_small_kernel<<<(unsigned)B, kThreads, smem, (cudaStream_t)stream>>>(init, trans, n, m, tags,
+                                                                                       score, status);
+      SDB_CHECK_LAUNCH();
+      return SDB_OK;
+    }
+  }
   const bool in_smem = viterbi_smem(n, m, true) <= 160 * 1024;
   size_t smem = viterbi_smem(n, m, in_smem);
   if (smem > 48 * 1024) {
