@@ -19,6 +19,19 @@ elif fam == "chain":
     tr = torch.randn(32, 127, 32, 32, device="cuda", generator=g)
     fn = {"fb": lambda: K.chain_fb(init, tr), "lz": lambda: K.chain_fb(init, tr, False),
           "vit": lambda: K.chain_viterbi(init, tr)}[mode]
+elif fam in ("mtt", "eisner"):
+    adj = torch.randn(512 if fam == "mtt" else 256, 129, 129, device="cuda", generator=g)
+    adj[:, :, 0] = NEG_INF
+    i = torch.arange(129, device="cuda")
+    adj[:, i, i] = NEG_INF
+    fn = {"mtt": lambda: K.mtt(adj), "eisner": lambda: K.eisner(adj)}[fam]
+elif fam == "ctc":
+    fp = torch.randn(256, 512, 128, device="cuda", generator=g)
+    tg = torch.randint(1, 128, (256, 128), device="cuda", generator=g, dtype=torch.int32)
+    fn = lambda: K.ctc_fb(fp, tg)
+elif fam == "tree":
+    th = torch.randn(128, 64, 64, 32, device="cuda", generator=g)
+    fn = lambda: K.tree_fb(th)
 for _ in range(3):
     fn()
 torch.cuda.synchronize()
