@@ -37,8 +37,8 @@ constexpr int kBS = 4;     // B-slice width
 constexpr int kMaxN = 64;
 
 struct PcfgWs {
-  float* RE;    // [B][NT][S][S]   exp(rules)   (original layout)
-  float* RT;    // [B][S][S][NT]   exp(rules) transposed: lanes over A
+  float* RE;    // [B][4][32 A][32 B][32 C]  exp(rules) per child-class block t, zero padded
+  float* RT;    // [B][4][32 B][32 C][32 A]  the same, A fastest (inside contraction)
   float* iu;    // [B][n][n][32]
   double* isc;  // [B][n][n]
   float* ou;    // [B][n][n][32]
@@ -51,8 +51,8 @@ PcfgWs pcfg_carve(void* base, int64_t B, int n, int NT, int PT, size_t* bytes) {
   const size_t S = NT + PT;
   Carve c(base);
   PcfgWs w;
-  w.RE = c.take<float>((size_t)B * NT * S * S);
-  w.RT = c.take<float>((size_t)B * NT * S * S);
+  w.RE = c.take<float>((size_t)B * 4 * 32768);  // REp[t][A][B][C] zero-padded per child block
+  w.RT = c.take<float>((size_t)B * 4 * 32768);  // RTp[t][B][C][A]
   w.iu = c.take<float>((size_t)B * n * n * 32);
   w.isc = c.take<double>((size_t)B * n * n);
   w.ou = c.take<float>((size_t)B * n * n * 32);
@@ -61,6 +61,15 @@ PcfgWs pcfg_carve(void* base, int64_t B, int n, int NT, int PT, size_t* bytes) {
   w.Q2 = c.take<float>((size_t)B * n * 3 * 1024);
   *bytes = c.used;
   return w;
+}
+
+__device__ __forceinline__ void cpa16(float* dst, const float* src) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src));
+}
+__device__ __forceinline__ void cpa_commit_wait() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
+  __syncthreads();
 }
 
 // child class offsets of block t: t0 = (NT,NT) t1 = (PT,NT) t2 = (NT,PT) t3 = (PT,PT)
@@ -83,8 +92,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
   const float* rules = rules_all + (size_t)b * NT * S * S;
   const float* emis = emis_all + (size_t)b * n * PT;
   const float* sticky = sticky_all ? sticky_all + (size_t)b * n * n : nullptr;
-  float* RE = ws.RE + (size_t)b * NT * S * S;
-  float* RT = ws.RT + (size_t)b * NT * S * S;
+  float* RE = ws.RE + (size_t)b * 4 * 32768;
+  float* RT = ws.RT + (size_t)b * 4 * 32768;
   float* iu = ws.iu + (size_t)b * n * n * 32;
   double* isc = ws.isc + (size_t)b * n * n;
   float* ou = ws.ou + (size_t)b * n * n * 32;
@@ -97,17 +106,19 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
   __syncthreads();
   auto STK = [&](int i, int j) -> float { return sticky ? sticky[i * n + j] : 0.f; };
 
-  // ---- prologue: exp(rules) in both layouts, input checks
+  // ---- prologue: exp(rules) into zero-padded per-block layouts (RE: C fastest, RT: A fastest),
+  // input checks
   {
     int bad = 0;
-    const int tot = NT * S * S;
-    for (int e = tid; e < tot; e += kThreads) {
-      const float x = rules[e];
-      bad |= bad_input(x);
-      const float v = fexp(x);
-      RE[e] = v;
-      const int A = e / (S * S), r = e - A * S * S;  // r = B'*S + C'
-      RT[(size_t)r * NT + A] = v;
+    for (int e = tid; e < NT * S * S; e += kThreads) bad |= bad_input(rules[e]);
+    for (int e = tid; e < 4 * 32768; e += kThreads) {
+      const int t = e >> 15, r = e & 32767;
+      const int A = r >> 10, Bi = (r >> 5) & 31, C = r & 31;
+      float v = 0.f;
+      if (A < NT && Bi < bcnt(t, NT, PT) && C < ccnt(t, NT, PT))
+        v = fexp(rules[((size_t)A * S + boff(t, NT) + Bi) * S + coff(t, NT) + C]);
+      RE[e] = v;                                              // [t][A][B][C]
+      RT[(((size_t)t * 32 + Bi) * 32 + C) * 32 + A] = v;      // [t][B][C][A]
     }
     for (int e = tid; e < NT; e += kThreads) bad |= bad_input(root[e]);
     for (int e = tid; e < n * PT; e += kThreads) bad |= bad_input(emis[e]);
@@ -115,6 +126,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
       for (int e = tid; e < n * n; e += kThreads) bad |= !(sticky[e] == 0.f || sticky[e] == ninf());
     if (bad) atomicOr(&badsh, 1);
   }
+  __syncthreads();
   // ---- width 1: preterminal slots (constituency.py:257-258)
   for (int i = warp; i < n; i += kWarps) {
     const float x = (lane < PT) ? emis[i * PT + lane] : ninf();
@@ -174,24 +186,19 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
 #pragma unroll
     for (int q = 0; q < kSpW; ++q) inner[q] = 0.f;
     for (int b0 = 0; b0 < 32; b0 += kBS) {
-      // stage R slice: RTs[sl][bb][C][A] = R_t[A][boff+b0+bb][coff+C]
-      for (int e = tid; e < nslot * kBS * 1024; e += kThreads) {
-        const int sl = e / (kBS * 1024), r = e - sl * kBS * 1024;
-        const int bb = r >> 10, C = (r >> 5) & 31, A = r & 31;
+      // stage R slice RTs[sl][bb][C][A] (4 KB contiguous per (sl, bb)) and the P slice
+      // Ps[s][sl][bb][C] (512 B contiguous per (s, sl)) with 16-byte cp.async
+      for (int e = tid; e < nslot * kBS * 256; e += kThreads) {
+        const int sl = e / (kBS * 256), r = e - sl * (kBS * 256);
         const int t = slot_type(sl, w);
-        const int Bi = b0 + bb;
-        float v = 0.f;
-        if (A < NT && Bi < bcnt(t, NT, PT) && C < ccnt(t, NT, PT))
-          v = RT[((size_t)(boff(t, NT) + Bi) * S + coff(t, NT) + C) * NT + A];
-        RTs[e] = v;
+        cpa16(RTs + sl * kBS * 1024 + 4 * r, RT + ((size_t)t * 32 + b0) * 1024 + 4 * r);
       }
-      // stage P slice of every span: Ps[s][sl][bb][C]
-      for (int e = tid; e < nsp * nslot * kBS * 32; e += kThreads) {
-        const int s = e / (nslot * kBS * 32), r = e - s * (nslot * kBS * 32);
-        const int sl = r / (kBS * 32), r2 = r - sl * (kBS * 32);
-        const int bb = r2 >> 5, C = r2 & 31;
-        Ps[((s * 3 + sl) * kBS + bb) * 32 + C] = Pw[(size_t)s * 3 * 1024 + sl * 1024 + (b0 + bb) * 32 + C];
+      for (int e = tid; e < nsp * nslot * 32; e += kThreads) {
+        const int s2 = e / (nslot * 32), r = e - s2 * (nslot * 32);
+        const int sl = r >> 5, q = r & 31;
+        cpa16(Ps + (s2 * 3 + sl) * kBS * 32 + 4 * q, Pw + (size_t)s2 * 3 * 1024 + sl * 1024 + b0 * 32 + 4 * q);
       }
+      cpa_commit_wait();
       __syncthreads();
       for (int sl = 0; sl < nslot; ++sl) {
         for (int bb = 0; bb < kBS; ++bb) {
@@ -279,17 +286,14 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
     }
     // ---- Q-build: Q[s][slot][B][C] = sum_A o_s[A] R_t[A, B', C'] (lane = C)
     for (int b0 = 0; b0 < 32; b0 += kBS) {
-      for (int e = tid; e < nslot * 32 * kBS * 32; e += kThreads) {
-        const int sl = e / (32 * kBS * 32), r = e - sl * (32 * kBS * 32);
-        const int A = r / (kBS * 32), r2 = r - A * (kBS * 32);
-        const int bb = r2 >> 5, C = r2 & 31;
+      // REs[sl][A][bb][C]: 512 B contiguous per (sl, A)
+      for (int e = tid; e < nslot * 32 * 32; e += kThreads) {
+        const int sl = e >> 10, r = e & 1023;
+        const int A = r >> 5, q = r & 31;
         const int t = slot_type(sl, w);
-        const int Bi = b0 + bb;
-        float v = 0.f;
-        if (A < NT && Bi < bcnt(t, NT, PT) && C < ccnt(t, NT, PT))
-          v = RE[((size_t)A * S + boff(t, NT) + Bi) * S + coff(t, NT) + C];
-        REs[e] = v;
+        cpa16(REs + (sl * 32 + A) * kBS * 32 + 4 * q, RE + (((size_t)t * 32 + A) * 32 + b0) * 32 + 4 * q);
       }
+      cpa_commit_wait();
       __syncthreads();
       for (int sl = 0; sl < nslot; ++sl) {
         float q4[kSpW][kBS];

@@ -32,6 +32,13 @@ elif fam == "ctc":
 elif fam == "tree":
     th = torch.randn(128, 64, 64, 32, device="cuda", generator=g)
     fn = lambda: K.tree_fb(th)
+elif fam == "pcfg":
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+    from golden.builders import batch_pcfg
+    r, ru, e = batch_pcfg(5000, 128, 64, 32, 32)
+    dv = lambda x: torch.as_tensor(x, dtype=torch.float32).cuda()  # noqa: E731
+    r, ru, e = dv(r), dv(ru), dv(e)
+    fn = lambda: K.pcfg_fb(r, ru, e)
 for _ in range(3):
     fn()
 torch.cuda.synchronize()
