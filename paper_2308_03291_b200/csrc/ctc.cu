@@ -39,26 +39,30 @@ struct CtcSmem {
   int* lst;       // [L] states grouped by label (CSR)
   int* off;       // [V+1]
   float* post;    // [S]
-  double* wred;   // [32]
+  double* wred;   // [2][32]
   float* bred;    // [32]
+  float* bring;   // [kP][S] beta rows (phase B prefetch)
+  double* bbase;  // [kP] their bases
 };
 
 size_t ctc_smem_bytes(int S, int V, int L) {
   return (size_t)2 * (S + 2) * 8 + (size_t)kP * V * 4 + (size_t)S * 4 + (size_t)(L + 1) * 4 +
-         (size_t)(V + 1) * 4 + (size_t)S * 4 + 32 * 8 + 32 * 4 + 64;
+         (size_t)(V + 1) * 4 + (size_t)S * 4 + 64 * 8 + 32 * 4 + (size_t)kP * 8 + (size_t)kP * S * 4 + 128;
 }
 
 __device__ CtcSmem ctc_carve(char* p, int S, int V, int L) {
   CtcSmem s;
   s.a0 = (double*)p; p += (size_t)(S + 2) * 8;
   s.a1 = (double*)p; p += (size_t)(S + 2) * 8;
-  s.wred = (double*)p; p += 32 * 8;
+  s.wred = (double*)p; p += 64 * 8;
+  s.bbase = (double*)p; p += kP * 8;
   s.rows = (float*)p; p += (size_t)kP * V * 4;
   s.lab = (int*)p; p += (size_t)S * 4;
   s.lst = (int*)p; p += (size_t)(L + 1) * 4;
   s.off = (int*)p; p += (size_t)(V + 1) * 4;
   s.post = (float*)p; p += (size_t)S * 4;
-  s.bred = (float*)p;
+  s.bred = (float*)p; p += 32 * 4;
+  s.bring = (float*)p;
   return s;
 }
 
@@ -169,14 +173,19 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
         }
         nxt[s] = v;
       }
-      __syncthreads();  // all reads of cur and row (t+1) done
+      {
+        const double wm = warp_maxd(v);
+        if ((tid & 31) == 0) sm.wred[(t & 1) * 32 + (tid >> 5)] = wm;
+      }
+      __syncthreads();  // all reads of cur and row (t+1) done; nxt and the warp maxima complete
       // refill the ring slot of frame t+1 with frame t+1-kP
       {
         const int tn = t + 1 - kP;
         if (tn >= 0) load_row(fp, tn, V, sm.rows + (size_t)(tn % kP) * V);
         cp_commit();
       }
-      double base = block_maxd_after(v, sm.wred);
+      double base = sm.wred[(t & 1) * 32];
+      for (int i = 1; i < nwarps; ++i) base = fmax(base, sm.wred[(t & 1) * 32 + i]);
       if (base == ninfd()) base = 0.0;
       if (act) wsb[(size_t)t * S + s] = (v == ninfd()) ? ninf() : (float)(v - base);
       if (tid == 0) wsbase[t] = base;
@@ -200,8 +209,19 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
     double* prv = sm.a0 + 2;  // alpha[t-1]
     double* now = sm.a1 + 2;
     if (tid < 2) { sm.a0[tid] = ninfd(); sm.a1[tid] = ninfd(); }
+    auto load_beta = [&](int t) {  // beta row t + its base into ring slot t % kP
+      if (kMode != 1) return;
+      if (act) cp_async4(sm.bring + (size_t)(t % kP) * S + s, wsb + (size_t)t * S + s);
+      if (tid == 0) {
+        unsigned sa = (unsigned)__cvta_generic_to_shared(sm.bbase + (t % kP));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(wsbase + t));
+      }
+    };
     for (int k = 0; k < kP; ++k) {
-      if (k < T) load_row(fp, k, V, sm.rows + (size_t)k * V);
+      if (k < T) {
+        load_row(fp, k, V, sm.rows + (size_t)k * V);
+        load_beta(k);
+      }
       cp_commit();
     }
     const double Z = zsh;
@@ -241,8 +261,8 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
         // posterior of state s at frame t
         float p = 0.f;
         if (act && zok && a != ninfd()) {
-          const float bt = wsb[(size_t)t * S + s];
-          const double bb = wsbase[t];
+          const float bt = sm.bring[(size_t)(t % kP) * S + s];
+          const double bb = sm.bbase[t % kP];
           if (bt != ninf()) p = fexp((float)(a + bb - Z) + bt);
         }
         if (act) sm.post[s] = p;
@@ -254,7 +274,10 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
       __syncthreads();  // now[] and post[] complete; row t consumed
       {
         const int tn = t + kP;
-        if (tn < T) load_row(fp, tn, V, sm.rows + (size_t)(tn % kP) * V);
+        if (tn < T) {
+          load_row(fp, tn, V, sm.rows + (size_t)(tn % kP) * V);
+          load_beta(tn);
+        }
         cp_commit();
       }
       if (kMode == 1) {
