@@ -110,10 +110,24 @@ __device__ __forceinline__ L3 lse3r(float t0, float t1, float t2) {
   return o;
 }
 
+template <bool B>
+struct BoolC {
+  static constexpr bool value = B;
+};
+
+// A block of kBlk steps is "steady" when every lane's cell is strictly
+// inside the grid rows (1 <= i < n), every prefetch row exists and no step
+// touches the start/end cell: the step then needs no row/origin predicates.
+// Steady blocks are the bulk of the work for n >> 32 and run a branch-free
+// straight-line body the compiler can interleave across the 8 steps.
+__device__ __forceinline__ bool steady_block(int s0, int n) { return (s0 >= 32) & (s0 + kBlk - 1 + kP < n); }
+
 // =========================================================== phase A
 // Backward recurrence on the flipped grid (push form).  Stores beta(i,j) as
-// wsb[w][s][l] = b + (O - K[w][s]) in the FORWARD strip layout (K = warp max
-// offset of the step); returns Z = beta(0,0) as (zint, zfrac).
+// wsb[w][s][l] = b + (O - K[w][s]) in the FORWARD strip layout (K = a per
+// (warp, step) integer reference: the warp max of the lane offsets on edge
+// blocks, lane 31's offset on steady blocks -- lane 31 always owns a real
+// column); returns Z = beta(0,0) as (zint, zfrac).
 template <bool kCheck>
 __device__ void nw_backward(const float* __restrict__ th, int n, int m, int NW, const NwShared& sh,
                             float* __restrict__ wsb, float* __restrict__ wsk, float* zint, float* zfrac,
@@ -129,19 +143,27 @@ __device__ void nw_backward(const float* __restrict__ th, int n, int m, int NW, 
   const float* ring_l = sh.ring + (size_t)w * kR * 96 + l;
   const int wf = NW - 1 - w, lf = 31 - l;
   const float* src_col = th + (size_t)(col_ok ? jo : m) * 3;
+  const float2* bnd0_in = sh.bnd0 + w * kRB;
+  const float2* bnd1_in = sh.bnd1 + w * kRB;
+  float2* bnd0_out = sh.bnd0 + (w + 1) * kRB;
+  float2* bnd1_out = sh.bnd1 + (w + 1) * kRB;
+  const bool pub = (l == 31) & (w + 1 < NW);
   VO pDn{ninf(), 0.f}, pR{ninf(), 0.f}, pD{ninf(), 0.f}, savedD{ninf(), 0.f};
   float O = 0.f;
-  int bad = 0;
+  bool bad = false;
   for (int blk = 0; blk < nblk; ++blk) {
     const int s0 = -kP - w * kLag + blk * kBlk;
     const int pbase = mod_pos(s0 + kP, kR);
     const int cbase = mod_pos(s0 - l, kR);
-#pragma unroll
-    for (int k = 0; k < kBlk; ++k) {
+    const int b0 = s0 & (kRB - 1);  // s0 is a multiple of kBlk: b0 + k never wraps
+    float* wsb_blk = wsb + ((size_t)wf * steps + (size_t)(n + 31 - s0)) * 32 + lf;
+    float* wsk_blk = wsk + (size_t)wf * steps + (size_t)(n + 31 - s0);
+    auto step = [&](auto steady_c, int k) {
+      constexpr bool kS = decltype(steady_c)::value;
       const int s = s0 + k;
       {  // prefetch flipped row s + kP (original row n - (s + kP)) of this lane's column
         const int rp = s + kP;
-        const bool pv = (rp >= 0) & (rp <= n);
+        const bool pv = kS ? true : ((rp >= 0) & (rp <= n));
         const float* src = src_col + (size_t)(pv ? n - rp : 0) * rowstride;
         const uint32_t dst = ring_u + (uint32_t)(pbase + k) * 384u;
         cp4p(dst, src, pv);
@@ -149,7 +171,7 @@ __device__ void nw_backward(const float* __restrict__ th, int n, int m, int NW, 
         cp4p(dst + 256, src + 2, pv);
         cp_commit();
       }
-      if (s >= 0 && s < steps) {
+      if (kS || (s >= 0 && s < steps)) {
         cp_wait<kP>();
         const int ip = s - l;
         VO rR, rD;
@@ -157,12 +179,15 @@ __device__ void nw_backward(const float* __restrict__ th, int n, int m, int NW, 
         rR.o = __shfl_up_sync(0xffffffffu, pR.o, 1);
         rD.v = __shfl_up_sync(0xffffffffu, pD.v, 1);
         rD.o = __shfl_up_sync(0xffffffffu, pD.o, 1);
-        const bool inrow = (ip >= 0) & (ip <= n);
-        if (l == 0) {
-          const float2 a = sh.bnd0[w * kRB + (ip & (kRB - 1))], d = sh.bnd1[w * kRB + (ip & (kRB - 1))];
+        const bool inrow = kS ? true : ((ip >= 0) & (ip <= n));
+        {  // lane 0 pulls the neighbour strip's boundary (broadcast read by all lanes)
+          const float2 a = bnd0_in[b0 + k], d = bnd1_in[b0 + k];
           const bool ok = (w > 0) & inrow;
-          rR = ok ? VO{a.x, a.y} : VO{ninf(), 0.f};
-          rD = ok ? VO{d.x, d.y} : VO{ninf(), 0.f};
+          const bool l0 = l == 0;
+          rR.v = l0 ? (ok ? a.x : ninf()) : rR.v;
+          rR.o = l0 ? (ok ? a.y : 0.f) : rR.o;
+          rD.v = l0 ? (ok ? d.x : ninf()) : rD.v;
+          rD.o = l0 ? (ok ? d.y : 0.f) : rD.o;
         }
         const VO inR = rR, inD = savedD, inDn = pDn;
         savedD = rD;
@@ -173,27 +198,44 @@ __device__ void nw_backward(const float* __restrict__ th, int n, int m, int NW, 
         const float x0 = slot[0], x1 = slot[32], x2 = slot[64];
         if (kCheck) bad |= valid & (bad_input(x0) | bad_input(x1) | bad_input(x2));
         const L3 r = lse3r(rel(inD, O), rel(inDn, O), rel(inR, O));
-        const bool start = (ip == 0) & (jo == m);  // original cell (n, m)
-        float b = start ? 0.f : r.v;
-        O = start ? 0.f : O + r.r;
+        float b;
+        if (kS) {
+          b = r.v;
+          O = O + r.r;
+        } else {
+          const bool start = (ip == 0) & (jo == m);  // original cell (n, m)
+          b = start ? 0.f : r.v;
+          O = start ? 0.f : O + r.r;
+        }
         b = valid ? b : ninf();
         pD = VO{fmaf(x0, SDB_LOG2E, b), O};
         pDn = VO{fmaf(x1, SDB_LOG2E, b), O};
         pR = VO{fmaf(x2, SDB_LOG2E, b), O};
-        if (valid && ip == n && jo == 0) {
+        if (!kS && valid && ip == n && jo == 0) {
           *zint = O;
           *zfrac = b;
         }
-        if (l == 31 && w + 1 < NW && inrow) {
-          sh.bnd0[(w + 1) * kRB + (ip & (kRB - 1))] = make_float2(pR.v, pR.o);
-          sh.bnd1[(w + 1) * kRB + (ip & (kRB - 1))] = make_float2(pD.v, pD.o);
+        if (pub & inrow) {
+          bnd0_out[(ip & (kRB - 1))] = make_float2(pR.v, pR.o);
+          bnd1_out[(ip & (kRB - 1))] = make_float2(pD.v, pD.o);
         }
-        const float K0 = warp_max(b == ninf() ? ninf() : O);
-        const float K = (K0 == ninf()) ? 0.f : K0;
-        const size_t sf = (size_t)(n + 31 - s);
-        wsb[((size_t)wf * steps + sf) * 32 + lf] = (b == ninf()) ? ninf() : b + (O - K);
-        if (l == 0) wsk[(size_t)wf * steps + sf] = K;
+        float K;
+        if (kS) {
+          K = __shfl_sync(0xffffffffu, O, 31);
+        } else {
+          const float K0 = warp_max(b == ninf() ? ninf() : O);
+          K = (K0 == ninf()) ? 0.f : K0;
+        }
+        wsb_blk[-32 * k] = (b == ninf()) ? ninf() : b + (O - K);
+        if (l == 0) wsk_blk[-k] = K;
       }
+    };
+    if (steady_block(s0, n)) {
+#pragma unroll
+      for (int k = 0; k < kBlk; ++k) step(BoolC<true>{}, k);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kBlk; ++k) step(BoolC<false>{}, k);
     }
     __syncthreads();
   }
@@ -218,8 +260,11 @@ __device__ void nw_forward(const float* __restrict__ th, int n, int m, int NW, c
   const float* bq = sh.bq + (size_t)w * kRP * 32 + l;
   const float* bk = sh.bk + (size_t)w * kRP;
   const uint32_t bq_u = smem_u32(bq), bk_u = smem_u32(bk);
+  const float2* bnd_in = sh.bnd0 + w * kRB;
+  float2* bnd_out = sh.bnd0 + (w + 1) * kRB;
+  const bool pub = (l == 31) & (w + 1 < NW);
   const bool zok = zfrac != ninf();
-  int bad = 0;
+  bool bad = false;
   VO cur{ninf(), 0.f}, lprev{ninf(), 0.f};
   float av = ninf(), O = 0.f;  // own previous cell (i-1, j) in frame O
   const float* src_col = th + (size_t)(col_ok ? j : m) * 3;
@@ -231,36 +276,41 @@ __device__ void nw_forward(const float* __restrict__ th, int n, int m, int NW, c
     const int pbase = mod_pos(s0 + kP, kR);
     const int cbase = mod_pos(s0 - l, kR);
     const int obase = mod_pos(s0 - 32, kR);
-#pragma unroll
-    for (int k = 0; k < kBlk; ++k) {
+    const int q0 = s0 & (kRP - 1), qp = (s0 + kP) & (kRP - 1);  // multiples of kBlk: + k never wraps
+    const int b0 = s0 & (kRB - 1);
+    auto step = [&](auto steady_c, int k) {
+      constexpr bool kS = decltype(steady_c)::value;
       const int s = s0 + k;
       {
         const int rp = s + kP;
-        const bool pv = (rp >= 0) & (rp <= n);
+        const bool pv = kS ? true : ((rp >= 0) & (rp <= n));
         const float* src = src_col + (size_t)(pv ? rp : 0) * rowstride;
         const uint32_t dst = ring_u + (uint32_t)(pbase + k) * 384u;
         cp4p(dst, src, pv);
         cp4p(dst + 128, src + 1, pv);
         cp4p(dst + 256, src + 2, pv);
         if (kMarg) {
-          const bool bv = (rp >= 0) & (rp < steps);
+          const bool bv = kS ? true : ((rp >= 0) & (rp < steps));
           const int rq = bv ? rp : 0;
-          cp4p(bq_u + (uint32_t)(rp & (kRP - 1)) * 128u, wsb_l + (size_t)rq * 32, bv);
-          cp4p(bk_u + (uint32_t)(rp & (kRP - 1)) * 4u, wsk_w + rq, bv & (l == 0));
+          cp4p(bq_u + (uint32_t)(qp + k) * 128u, wsb_l + (size_t)rq * 32, bv);
+          cp4p(bk_u + (uint32_t)(qp + k) * 4u, wsk_w + rq, bv & (l == 0));
         }
         cp_commit();
       }
-      if (s >= 0 && s <= steps) {
+      if (kS || (s >= 0 && s <= steps)) {
         cp_wait<kP>();
-        if (s < steps) {
+        if (kS || s < steps) {
           const int i = s - l;
           VO left;
           left.v = __shfl_up_sync(0xffffffffu, cur.v, 1);
           left.o = __shfl_up_sync(0xffffffffu, cur.o, 1);
-          const bool inrow = (i >= 0) & (i <= n);
-          if (l == 0) {
-            const float2 a = sh.bnd0[w * kRB + (i & (kRB - 1))];
-            left = ((w > 0) & inrow) ? VO{a.x, a.y} : VO{ninf(), 0.f};
+          const bool inrow = kS ? true : ((i >= 0) & (i <= n));
+          {
+            const float2 a = bnd_in[b0 + k];
+            const bool ok = (w > 0) & inrow;
+            const bool l0 = l == 0;
+            left.v = l0 ? (ok ? a.x : ninf()) : left.v;
+            left.o = l0 ? (ok ? a.y : 0.f) : left.o;
           }
           const VO diag = lprev;
           lprev = left;
@@ -274,11 +324,12 @@ __device__ void nw_forward(const float* __restrict__ th, int n, int m, int NW, c
           const float t1 = fmaf(x1, SDB_LOG2E, av);
           const float t2 = fmaf(x2, SDB_LOG2E, rel(left, O));
           const L3 r = lse3r(t0, t1, t2);
-          const bool origin = (i == 0) & (j == 0);
+          const bool origin = kS ? false : ((i == 0) & (j == 0));
           if (kMarg) {
-            const float bt = bq[(s & (kRP - 1)) * 32];
-            const float kk = bk[s & (kRP - 1)];
-            const float F = (zok & !origin) ? ex2((r.Mc + bt) + ((O + kk - zint) - zfrac)) : 0.f;
+            const float bt = bq[(q0 + k) * 32];
+            const float kk = bk[q0 + k];
+            const float e = ex2((r.Mc + bt) + ((O + kk - zint) - zfrac));
+            const float F = (zok & !origin) ? e : 0.f;
             slot[0] = r.e0 * F;
             slot[32] = r.e1 * F;
             slot[64] = r.e2 * F;
@@ -287,16 +338,16 @@ __device__ void nw_forward(const float* __restrict__ th, int n, int m, int NW, c
           O = origin ? 0.f : O + r.r;
           a = valid ? a : ninf();
           av = a;
-          if (valid && i == n && j == m) {
+          if (!kS && valid && i == n && j == m) {
             *last_v = a;
             *last_o = O;
           }
           cur = VO{a, O};
-          if (l == 31 && w + 1 < NW && inrow) sh.bnd0[(w + 1) * kRB + (i & (kRB - 1))] = make_float2(cur.v, cur.o);
+          if (pub & inrow) bnd_out[i & (kRB - 1)] = make_float2(cur.v, cur.o);
         }
         if (kMarg) {
           const int r = s - 32;  // row completed by every lane of this warp
-          if ((r >= 0) & (r <= n) & col_ok) {
+          if ((kS || ((r >= 0) & (r <= n))) & col_ok) {
             const float* slot = ring_l + (obase + k) * 96;
             float* dst = dst_col + (size_t)r * rowstride;
             dst[0] = slot[0];
@@ -305,6 +356,13 @@ __device__ void nw_forward(const float* __restrict__ th, int n, int m, int NW, c
           }
         }
       }
+    };
+    if (steady_block(s0, n)) {
+#pragma unroll
+      for (int k = 0; k < kBlk; ++k) step(BoolC<true>{}, k);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kBlk; ++k) step(BoolC<false>{}, k);
     }
     __syncthreads();
   }

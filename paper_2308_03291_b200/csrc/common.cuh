@@ -39,7 +39,8 @@ __device__ __forceinline__ bool is_ninf(float x) { return x == ninf(); }
 __device__ __forceinline__ bool is_ninfd(double x) { return x == ninfd(); }
 
 // Input validity (numerics.py:22-29): NaN and +inf are rejected, -inf allowed.
-__device__ __forceinline__ bool bad_input(float x) { return x != x || x == __int_as_float(0x7f800000); }
+// NaN or +inf (one unordered compare: !(x < +inf))
+__device__ __forceinline__ bool bad_input(float x) { return !(x < __int_as_float(0x7f800000)); }
 
 // (max, sum exp(x - max)) accumulator for a log-sum-exp reduction.
 struct Lse {
