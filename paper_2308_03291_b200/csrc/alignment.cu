@@ -153,6 +153,10 @@ __device__ void nw_backward(const float* __restrict__ th, int n, int m, int NW, 
   bool bad = false;
   for (int blk = 0; blk < nblk; ++blk) {
     const int s0 = -kP - w * kLag + blk * kBlk;
+    if ((s0 + kBlk - 1 < -kP) | (s0 >= steps)) {  // pipeline fill/drain: nothing to load or compute
+      __syncthreads();
+      continue;
+    }
     const int pbase = mod_pos(s0 + kP, kR);
     const int cbase = mod_pos(s0 - l, kR);
     const int b0 = s0 & (kRB - 1);  // s0 is a multiple of kBlk: b0 + k never wraps
@@ -273,6 +277,10 @@ __device__ void nw_forward(const float* __restrict__ th, int n, int m, int NW, c
   const float* wsk_w = kMarg ? wsk + (size_t)w * steps : nullptr;
   for (int blk = 0; blk < nblk; ++blk) {
     const int s0 = -kP - w * kLag + blk * kBlk;
+    if ((s0 + kBlk - 1 < -kP) | (s0 > steps)) {  // pipeline fill/drain: nothing to load or compute
+      __syncthreads();
+      continue;
+    }
     const int pbase = mod_pos(s0 + kP, kR);
     const int cbase = mod_pos(s0 - l, kR);
     const int obase = mod_pos(s0 - 32, kR);
