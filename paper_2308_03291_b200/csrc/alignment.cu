@@ -199,8 +199,13 @@ __device__ void nw_backward(const float* __restrict__ th, int n, int m, int NW, 
         int cs = cbase + k;
         cs -= (cs >= kR) ? kR : 0;
         const float* slot = ring_l + cs * 96;
-        const float x0 = slot[0], x1 = slot[32], x2 = slot[64];
+        float x0 = slot[0], x1 = slot[32], x2 = slot[64];
         if (kCheck) bad |= valid & (bad_input(x0) | bad_input(x1) | bad_input(x2));
+        if (!kS) {  // slots of cells outside the grid were never loaded: keep their pushes -inf, not NaN
+          x0 = valid ? x0 : 0.f;
+          x1 = valid ? x1 : 0.f;
+          x2 = valid ? x2 : 0.f;
+        }
         const L3 r = lse3r(rel(inD, O), rel(inDn, O), rel(inR, O));
         float b;
         if (kS) {
@@ -526,10 +531,544 @@ __global__ void nw_walk_kernel(const int8_t* __restrict__ choice_all, int n, int
   }
 }
 
+// =========================================================== meet in the middle
+// Marginals with the forward and the backward recurrence running
+// CONCURRENTLY in one CTA (warps [0,NW) forward strips, [NW,2NW) backward
+// strips), each over half of the grid, then crossing over:
+//   phase 1: forward computes alpha on A = {(i,j): i <= RF(strip(j))} and
+//            stores it; backward computes beta on the complement B and stores
+//            it.  RF(w) = (40 (NW-1-2w) + n - 1) / 2 balances the two so that
+//            every strip of both directions finishes phase 1 in the same
+//            block.  A is closed under predecessors, so every path crosses
+//            from A to B exactly once and
+//              Z = sum over crossing moves of alpha(src) e^theta(dst) beta(dst);
+//   phase 2: forward continues on B emitting e_k * exp2(M + beta - Z) (as in
+//            nw_forward), backward continues on A emitting
+//            exp2(alpha(src_k) + theta_k + beta - Z) from the stored alpha.
+// Both directions keep their own per-lane frames (values stored as (v, O)
+// float2, exact).  Wall time is ~one wavefront pass instead of two, with twice
+// the warps in flight.  Delay lines are split into two 16-lane halves
+// (rows s-l for lanes 0-15 and 16-31 are 16 steps apart), which halves their
+// shared memory so that two CTAs fit on an SM.
+constexpr int kMP = 4;                       // potentials prefetch distance (steps)
+constexpr int kMRh = 20;                     // delay-line rows per half-warp (>= 16 + kMP)
+constexpr int kMGrp = kMRh * 48 + 16;        // floats per half-warp ring incl. 16-word bank pad
+constexpr int kMRing = kMGrp + kMRh * 48;    // floats per warp
+constexpr int kMS = 8;                       // alpha/beta slab ring entries (>= kMP + 2, power of 2)
+
+struct MShared {
+  float* ring;     // [2NW][kMRing]
+  float2* bndF;    // [NW][kRB]  forward strip boundary
+  float2* bndB0;   // [NW][kRB]  backward right push
+  float2* bndB1;   // [NW][kRB]  backward diagonal push
+  float2* slab;    // [2NW][kMS][32]
+  float2* slabL;   // [NW][kMS]  backward: left-strip lane-31 alpha
+  double* red;     // [64]
+  int* flags;      // [4]
+};
+
+size_t mitm_smem_bytes(int NW) {
+  return (size_t)2 * NW * kMRing * 4 + (size_t)3 * NW * kRB * 8 + (size_t)2 * NW * kMS * 32 * 8 +
+         (size_t)NW * kMS * 8 + 64 * 8 + 16 + 64;
+}
+
+__device__ MShared mitm_carve(char* base, int NW) {
+  MShared s;
+  s.ring = (float*)base;
+  base += (size_t)2 * NW * kMRing * 4;
+  s.slab = (float2*)base;
+  base += (size_t)2 * NW * kMS * 32 * 8;
+  s.bndF = (float2*)base;
+  base += (size_t)NW * kRB * 8;
+  s.bndB0 = (float2*)base;
+  base += (size_t)NW * kRB * 8;
+  s.bndB1 = (float2*)base;
+  base += (size_t)NW * kRB * 8;
+  s.slabL = (float2*)base;
+  base += (size_t)NW * kMS * 8;
+  s.red = (double*)base;
+  base += 64 * 8;
+  s.flags = (int*)base;
+  return s;
+}
+
+__device__ __forceinline__ int mitm_rf(int w, int n, int NW) { return (40 * (NW - 1 - 2 * w) + n - 1) >> 1; }
+__device__ __forceinline__ int wrapr(int x) { return x >= kMRh ? x - kMRh : x; }
+__device__ __forceinline__ void cp8p(uint32_t saddr, const void* gmem, bool pred) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p cp.async.ca.shared.global [%0], [%1], 8;\n}\n" ::"r"(saddr),
+      "l"(gmem), "r"((int)pred));
+}
+__device__ __forceinline__ void bar_all() { asm volatile("bar.sync 0;\n" ::: "memory"); }
+// per-direction barrier: forward warps use barrier 1, backward warps barrier 2
+// (they only meet at the phase boundary)
+__device__ __forceinline__ void bar_dir(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+struct FState {
+  VO cur, lprev;
+  float av, O;
+};
+struct BState {
+  VO pDn, pR, pD, savedD;
+  float O;
+};
+
+// Blocks of one pass: s0 = -kBlk - kLag*w + kBlk*(blk + off); consumption of
+// row s-l by lane l at step s, exactly like nw_forward.
+template <int kPh>
+__device__ __forceinline__ void mitm_fwd(const float* __restrict__ th, int n, int m, int NW, const MShared& sh, int RF, int off,
+                         int nblk, float2* __restrict__ wsa, const float2* __restrict__ wsb, float zint, float zfrac,
+                         float* __restrict__ marg, FState& st, int* bad_flag) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int g = l >> 4, q = l & 15;
+  const int j = 32 * w + l;
+  const bool col_ok = j <= m;
+  const int steps = n + 32;
+  const int lo = kPh == 1 ? 0 : RF + 1, hi = kPh == 1 ? RF : n;
+  const size_t rowstride = (size_t)(m + 1) * 3;
+  float* ring_g = sh.ring + (size_t)w * kMRing + g * kMGrp + q;
+  const uint32_t ring_u = smem_u32(ring_g);
+  const float* src_col = th + (size_t)(col_ok ? j : m) * 3;
+  float* dst_col = kPh == 2 ? marg + (size_t)(col_ok ? j : 0) * 3 : nullptr;
+  float2* wsa_l = wsa + (size_t)w * steps * 32 + l;
+  const float2* wsb_l = wsb + (size_t)w * steps * 32 + l;
+  float2* slab_w = sh.slab + (size_t)w * kMS * 32;
+  const uint32_t slab_u = smem_u32(slab_w + l);
+  const float2* bnd_in = sh.bndF + w * kRB;
+  float2* bnd_out = sh.bndF + (w + 1) * kRB;
+  const bool pub = (l == 31) & (w + 1 < NW);
+  const bool zok = zfrac != ninf();
+  const int s_lo = max(lo, 1) + 32, s_hi = min(hi, n - 1) - (kBlk - 1) - kMP;
+  bool bad = false;
+  VO cur = st.cur, lprev = st.lprev;
+  float av = st.av, O = st.O;
+  for (int blk = 0; blk < nblk; ++blk) {
+    const int s0 = -kBlk - w * kLag + (blk + off) * kBlk;
+    if ((s0 + kBlk - 1 + kMP < max(lo, 0)) | (s0 > hi + 32 + (kPh == 2 ? 1 : 0))) {
+      bar_dir(1, 32 * NW);
+      continue;
+    }
+    const int pb = mod_pos(s0 + kMP - 16 * g, kMRh);
+    const int cb = mod_pos(s0 - l, kMRh);
+    const int wb = mod_pos(s0 - 16 - 16 * g, kMRh);
+    const int b0 = s0 & (kRB - 1);
+    const ptrdiff_t rs = (ptrdiff_t)rowstride;
+    const float* tsrc = src_col + (ptrdiff_t)(s0 + kMP - 16 * g) * rs;  // advanced one row per step
+    float* wdst = kPh == 2 ? dst_col + (ptrdiff_t)(s0 - 16 - 16 * g) * rs : nullptr;
+    float2* wsa_b = wsa_l + (ptrdiff_t)s0 * 32;
+    const float2* wsb_b = wsb_l + (ptrdiff_t)(s0 + kMP) * 32;
+    auto step = [&](auto steady_c, int k) {
+      constexpr bool kS = decltype(steady_c)::value;
+      const int s = s0 + k;
+      if (kPh == 2) {  // write back the row this half-warp completed at step s-1 (before its slot is refilled)
+        const int r = s - 16 - 16 * g;
+        if ((kS || ((r >= lo) & (r <= hi))) & col_ok) {
+          const float* slot = ring_g + wrapr(wb + k) * 48;
+          wdst[0] = slot[0];
+          wdst[1] = slot[16];
+          wdst[2] = slot[32];
+        }
+        wdst += rs;
+      }
+      {
+        const int prow = s + kMP - 16 * g;
+        const bool pv = kS ? true : ((prow >= 0) & (prow <= n));
+        const float* src = tsrc;
+        tsrc += rs;
+        const uint32_t dst = ring_u + (uint32_t)wrapr(pb + k) * 192u;
+        cp4p(dst, src, pv);
+        cp4p(dst + 64, src + 1, pv);
+        cp4p(dst + 128, src + 2, pv);
+        if (kPh == 2) {
+          const int sp = s + kMP;
+          const bool bv = kS ? true : ((sp >= 0) & (sp < steps));
+          cp8p(slab_u + (uint32_t)((k + kMP) & (kMS - 1)) * 256u, wsb_b + 32 * k, bv);
+        }
+        cp_commit();
+      }
+      if (kS || ((s >= 0) & (s < steps))) {
+        cp_wait<kMP>();
+        const int i = s - l;
+        VO left;
+        left.v = __shfl_up_sync(0xffffffffu, cur.v, 1);
+        left.o = __shfl_up_sync(0xffffffffu, cur.o, 1);
+        const bool inrow = kS ? true : ((i >= 0) & (i <= n));
+        {
+          const float2 a = bnd_in[b0 + k];
+          const bool ok = (w > 0) & inrow;
+          const bool l0 = l == 0;
+          left.v = l0 ? (ok ? a.x : ninf()) : left.v;
+          left.o = l0 ? (ok ? a.y : 0.f) : left.o;
+        }
+        const bool act = kS ? true : ((i >= lo) & (i <= hi) & col_ok);
+        float* slot = ring_g + wrapr(cb + k) * 48;
+        const float x0 = slot[0], x1 = slot[16], x2 = slot[32];
+        bad |= act & col_ok & (bad_input(x0) | bad_input(x1) | bad_input(x2));
+        const float t0 = fmaf(x0, SDB_LOG2E, rel(lprev, O));
+        const float t1 = fmaf(x1, SDB_LOG2E, av);
+        const float t2 = fmaf(x2, SDB_LOG2E, rel(left, O));
+        const L3 r = lse3r(t0, t1, t2);
+        const bool origin = kS ? false : ((i == 0) & (j == 0));
+        if (kPh == 2) {
+          const float2 bt = slab_w[((k)&(kMS - 1)) * 32 + l];
+          const float e = ex2((r.Mc + bt.x) + ((O + bt.y - zint) - zfrac));
+          const float F = (zok & act) ? e : 0.f;
+          slot[0] = r.e0 * F;
+          slot[16] = r.e1 * F;
+          slot[32] = r.e2 * F;
+        }
+        const float a = origin ? 0.f : r.v;
+        const float On = origin ? 0.f : O + r.r;
+        if (kS) {
+          lprev = left;
+          av = a;
+          O = On;
+          cur = VO{a, On};
+        } else if (act) {
+          lprev = left;
+          av = a;
+          O = On;
+          cur = VO{a, On};
+        }
+        if (kPh == 1 && (kS || act)) wsa_b[32 * k] = make_float2(a, On);
+        if (pub & (kS || act)) bnd_out[i & (kRB - 1)] = make_float2(a, On);
+      }
+    };
+    if ((s0 >= s_lo) & (s0 <= s_hi)) {
+#pragma unroll
+      for (int k = 0; k < kBlk; ++k) step(BoolC<true>{}, k);
+    } else {
+#pragma unroll 1
+      for (int k = 0; k < kBlk; ++k) step(BoolC<false>{}, k);
+    }
+    bar_dir(1, 32 * NW);
+  }
+  cp_wait<0>();
+  st.cur = cur;
+  st.lprev = lprev;
+  st.av = av;
+  st.O = O;
+  if (bad) atomicOr(bad_flag, 1);
+}
+
+// Backward strips on the flipped grid (as nw_backward).  Warp wb = warp - NW
+// handles flipped columns jo = 32 NW - 1 - (32 wb + l), i.e. original strip
+// u = NW-1-wb with forward lane 31-l.
+template <int kPh>
+__device__ __forceinline__ void mitm_bwd(const float* __restrict__ th, int n, int m, int NW, const MShared& sh, int RFu, int off,
+                         int nblk, const float2* __restrict__ wsa, float2* __restrict__ wsb, float zint, float zfrac,
+                         float* __restrict__ marg, BState& st) {
+  const int wb = (threadIdx.x >> 5) - NW, l = threadIdx.x & 31;
+  const int g = l >> 4, q = l & 15;
+  const int mp = 32 * NW - 1;
+  const int jo = mp - (32 * wb + l);
+  const bool col_ok = jo <= m;
+  const int u = NW - 1 - wb, lf = 31 - l;
+  const int steps = n + 32;
+  const int QB = n - RFu - 1;  // flipped rows [0, QB] are original rows > RF(u)
+  const int lo = kPh == 1 ? 0 : QB + 1, hi = kPh == 1 ? QB : n;
+  const size_t rowstride = (size_t)(m + 1) * 3;
+  float* ring_g = sh.ring + (size_t)(NW + wb) * kMRing + g * kMGrp + q;
+  const uint32_t ring_u = smem_u32(ring_g);
+  const float* src_col = th + (size_t)(col_ok ? jo : m) * 3;
+  float* dst_col = kPh == 2 ? marg + (size_t)(col_ok ? jo : 0) * 3 : nullptr;
+  float2* wsb_l = wsb + (size_t)u * steps * 32 + lf;
+  const float2* wsa_u = wsa + (size_t)u * steps * 32;
+  const float2* wsa_left = u > 0 ? wsa + (size_t)(u - 1) * steps * 32 + 31 : nullptr;
+  float2* slab_w = sh.slab + (size_t)(NW + wb) * kMS * 32;
+  const uint32_t slab_u = smem_u32(slab_w + l);
+  float2* slabL = sh.slabL + wb * kMS;
+  const uint32_t slabL_u = smem_u32(slabL);
+  const float2* bnd0_in = sh.bndB0 + wb * kRB;
+  const float2* bnd1_in = sh.bndB1 + wb * kRB;
+  float2* bnd0_out = sh.bndB0 + (wb + 1) * kRB;
+  float2* bnd1_out = sh.bndB1 + (wb + 1) * kRB;
+  const bool pub = (l == 31) & (wb + 1 < NW);
+  const bool zok = zfrac != ninf();
+  const int s_lo = max(lo, 1) + 32, s_hi = min(hi, n - 1) - (kBlk - 1) - kMP;
+  VO pDn = st.pDn, pR = st.pR, pD = st.pD, savedD = st.savedD;
+  float O = st.O;
+  float2 c1 = make_float2(ninf(), 0.f), c2 = make_float2(ninf(), 0.f);  // phase 2 alpha carries
+  for (int blk = 0; blk < nblk; ++blk) {
+    const int s0 = -kBlk - wb * kLag + (blk + off) * kBlk;
+    if ((s0 + kBlk - 1 + kMP < max(lo, 0)) | (s0 > hi + 32 + (kPh == 2 ? 1 : 0))) {
+      bar_dir(2, 32 * NW);
+      continue;
+    }
+    const int pb = mod_pos(s0 + kMP - 16 * g, kMRh);
+    const int cb = mod_pos(s0 - l, kMRh);
+    const int wbk = mod_pos(s0 - 16 - 16 * g, kMRh);
+    const int b0 = s0 & (kRB - 1);
+    const ptrdiff_t rs = (ptrdiff_t)rowstride;
+    const float* tsrc = src_col + (ptrdiff_t)(n - (s0 + kMP - 16 * g)) * rs;  // moves up one row per step
+    float* wdst = kPh == 2 ? dst_col + (ptrdiff_t)(n - (s0 - 16 - 16 * g)) * rs : nullptr;
+    float2* wsb_b = wsb_l + (ptrdiff_t)(n + 31 - s0) * 32;
+    const float2* sa_b = wsa_u + (ptrdiff_t)(n + 29 - kMP - s0) * 32 + l;
+    const float2* sl_b = u > 0 ? wsa_left + (ptrdiff_t)(n + 29 - kMP + 32 - s0) * 32 : wsa_u;
+    auto step = [&](auto steady_c, int k) {
+      constexpr bool kS = decltype(steady_c)::value;
+      const int s = s0 + k;
+      if (kPh == 2) {
+        const int r = s - 16 - 16 * g;  // flipped row completed at step s-1
+        if ((kS || ((r >= lo) & (r <= hi))) & col_ok) {
+          const float* slot = ring_g + wrapr(wbk + k) * 48;
+          wdst[0] = slot[0];
+          wdst[1] = slot[16];
+          wdst[2] = slot[32];
+        }
+        wdst -= rs;
+      }
+      {
+        const int prow = s + kMP - 16 * g;
+        const bool pv = kS ? true : ((prow >= 0) & (prow <= n));
+        const float* src = tsrc;
+        tsrc -= rs;
+        const uint32_t dst = ring_u + (uint32_t)wrapr(pb + k) * 192u;
+        cp4p(dst, src, pv);
+        cp4p(dst + 64, src + 1, pv);
+        cp4p(dst + 128, src + 2, pv);
+        if (kPh == 2) {
+          // alpha slab sF(s+kMP)-2 (own strip) and left-strip lane-31 alpha for sF(s+kMP)-1
+          const int sa = n + 29 - s - kMP;
+          const bool av_ = kS ? true : ((sa >= 0) & (sa < steps));
+          cp8p(slab_u + (uint32_t)(sa & (kMS - 1)) * 256u, sa_b - 32 * k, av_);
+          const int sl = sa + 1 + 31;
+          const bool lv = (u > 0) & (l == 0) & (sl >= 0) & (sl < steps);
+          cp8p(slabL_u + (uint32_t)((sa + 1) & (kMS - 1)) * 8u, sl_b - 32 * k, lv);
+        }
+        cp_commit();
+      }
+      if (kS || ((s >= 0) & (s < steps))) {
+        cp_wait<kMP>();
+        const int ip = s - l;
+        VO rR, rD;
+        rR.v = __shfl_up_sync(0xffffffffu, pR.v, 1);
+        rR.o = __shfl_up_sync(0xffffffffu, pR.o, 1);
+        rD.v = __shfl_up_sync(0xffffffffu, pD.v, 1);
+        rD.o = __shfl_up_sync(0xffffffffu, pD.o, 1);
+        const bool inrow = kS ? true : ((ip >= 0) & (ip <= n));
+        {
+          const float2 a = bnd0_in[b0 + k], d = bnd1_in[b0 + k];
+          const bool ok = (wb > 0) & inrow;
+          const bool l0 = l == 0;
+          rR.v = l0 ? (ok ? a.x : ninf()) : rR.v;
+          rR.o = l0 ? (ok ? a.y : 0.f) : rR.o;
+          rD.v = l0 ? (ok ? d.x : ninf()) : rD.v;
+          rD.o = l0 ? (ok ? d.y : 0.f) : rD.o;
+        }
+        const bool act = kS ? true : ((ip >= lo) & (ip <= hi) & col_ok);
+        float* slot = ring_g + wrapr(cb + k) * 48;
+        const float x0 = slot[0], x1 = slot[16], x2 = slot[32];
+        const L3 r = lse3r(rel(savedD, O), rel(pDn, O), rel(rR, O));
+        float b, On;
+        if (kS) {
+          b = r.v;
+          On = O + r.r;
+        } else {
+          const bool start = (ip == 0) & (jo == m);
+          b = start ? 0.f : r.v;
+          On = start ? 0.f : O + r.r;
+        }
+        if (kPh == 2) {
+          // original cell (i, j) = (n - ip, jo); alpha of its three sources.  One slab
+          // entry per step: X = alpha(i-1, j) of the NEXT step's cell; the left column
+          // comes from lane l+1 (lf-1) or, for lf = 0, from the left strip's lane 31.
+          // alpha(i-1, j) and alpha(i, j-1) are the previous step's X and left value.
+          __syncwarp();
+          const int sF = n + 31 - s;
+          const int i = n - ip;
+          const float2 X = slab_w[((sF - 2) & (kMS - 1)) * 32 + lf];
+          float2 Y;
+          Y.x = __shfl_down_sync(0xffffffffu, X.x, 1);
+          Y.y = __shfl_down_sync(0xffffffffu, X.y, 1);
+          {
+            const float2 L = slabL[(sF - 1) & (kMS - 1)];
+            Y.x = l == 31 ? L.x : Y.x;
+            Y.y = l == 31 ? L.y : Y.y;
+          }
+          const float2 A0 = Y, A1 = c1, A2 = c2;
+          c1 = X;
+          c2 = Y;
+          const bool hi_ok = i >= 1, left_ok = jo >= 1, ok = zok & act;
+          const float base = b - zfrac;
+          const float e0 = ex2(((A0.y + On - zint) + (A0.x + fmaf(x0, SDB_LOG2E, base))));
+          const float e1 = ex2(((A1.y + On - zint) + (A1.x + fmaf(x1, SDB_LOG2E, base))));
+          const float e2 = ex2(((A2.y + On - zint) + (A2.x + fmaf(x2, SDB_LOG2E, base))));
+          slot[0] = (ok & hi_ok & left_ok) ? e0 : 0.f;
+          slot[16] = (ok & hi_ok) ? e1 : 0.f;
+          slot[32] = (ok & left_ok) ? e2 : 0.f;
+        }
+        // invalid (padding) columns push -inf with offset 0 so they never poison real lanes
+        const bool okb = kS ? col_ok : act;
+        const float bb = okb ? b : ninf();
+        if (kS && !col_ok) On = 0.f;
+        const VO nD{fmaf(x0, SDB_LOG2E, bb), On}, nDn{fmaf(x1, SDB_LOG2E, bb), On}, nR{fmaf(x2, SDB_LOG2E, bb), On};
+        if (kS) {
+          savedD = rD;
+          pD = nD;
+          pDn = nDn;
+          pR = nR;
+          O = On;
+        } else if (act) {
+          savedD = rD;
+          pD = nD;
+          pDn = nDn;
+          pR = nR;
+          O = On;
+        }
+        if (kPh == 1 && (kS || act)) wsb_b[-32 * k] = make_float2(b, On);
+        if (pub & (kS || act)) {
+          bnd0_out[ip & (kRB - 1)] = make_float2(nR.v, nR.o);
+          bnd1_out[ip & (kRB - 1)] = make_float2(nD.v, nD.o);
+        }
+      }
+    };
+    if ((s0 >= s_lo) & (s0 <= s_hi)) {
+#pragma unroll
+      for (int k = 0; k < kBlk; ++k) step(BoolC<true>{}, k);
+    } else {
+#pragma unroll 1
+      for (int k = 0; k < kBlk; ++k) step(BoolC<false>{}, k);
+    }
+    bar_dir(2, 32 * NW);
+  }
+  cp_wait<0>();
+  st.pDn = pDn;
+  st.pR = pR;
+  st.pD = pD;
+  st.savedD = savedD;
+  st.O = O;
+}
+
+// log2 Z over the moves that cross from A into B (fp64, all threads).
+__device__ double mitm_z(const float* __restrict__ th, int n, int m, int NW, const float2* __restrict__ wsa,
+                         const float2* __restrict__ wsb, double* red) {
+  const int steps = n + 32;
+  const int m1 = m + 1;
+  // per column: DOWN and DIAG into row RF+1; per strip boundary 32w: RIGHT into
+  // rows (RF(w), RF(w-1)] and DIAG into rows (RF(w)+1, RF(w-1)+1]
+  const int E = 2 * m1 + 2 * (mitm_rf(0, n, NW) - mitm_rf(NW - 1, n, NW));
+  auto alpha = [&](int i, int j) {
+    const float2 v = wsa[((size_t)(j >> 5) * steps + i + (j & 31)) * 32 + (j & 31)];
+    return (double)v.x + (double)v.y;
+  };
+  auto beta = [&](int i, int j) {
+    const float2 v = wsb[((size_t)(j >> 5) * steps + i + (j & 31)) * 32 + (j & 31)];
+    return (double)v.x + (double)v.y;
+  };
+  auto theta = [&](int i, int j, int k) { return (double)th[((size_t)i * m1 + j) * 3 + k] * 1.4426950408889634; };
+  double mx = ninfd(), sm = 0.0;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    double t = ninfd();
+    if (e < 2 * m1) {
+      const int j = e < m1 ? e : e - m1;
+      const int R = mitm_rf(j >> 5, n, NW);
+      if (e < m1)
+        t = alpha(R, j) + theta(R + 1, j, 1) + beta(R + 1, j);
+      else if (j >= 1)
+        t = alpha(R, j - 1) + theta(R + 1, j, 0) + beta(R + 1, j);
+    } else {
+      int x = e - 2 * m1, w = 1;
+      while (x >= 2 * (mitm_rf(w - 1, n, NW) - mitm_rf(w, n, NW))) {
+        x -= 2 * (mitm_rf(w - 1, n, NW) - mitm_rf(w, n, NW));
+        ++w;
+      }
+      const int c = mitm_rf(w - 1, n, NW) - mitm_rf(w, n, NW), j = 32 * w;
+      if (x < c) {
+        const int i = mitm_rf(w, n, NW) + 1 + x;
+        t = alpha(i, j - 1) + theta(i, j, 2) + beta(i, j);
+      } else {
+        const int i = mitm_rf(w, n, NW) + 2 + (x - c);
+        t = alpha(i - 1, j - 1) + theta(i, j, 0) + beta(i, j);
+      }
+    }
+    if (t != t) t = ninfd();
+    if (t > mx) {
+      sm = (mx == ninfd()) ? 1.0 : sm * exp2(mx - t) + 1.0;
+      mx = t;
+    } else if (t != ninfd()) {
+      sm += exp2(t - mx);
+    }
+  }
+  const int wi = threadIdx.x >> 5, li = threadIdx.x & 31, nw = blockDim.x >> 5;
+  double gm = warp_maxd(mx);
+  double gs = (mx == ninfd()) ? 0.0 : sm * exp2(mx - gm);
+  for (int o = 16; o > 0; o >>= 1) gs += __shfl_xor_sync(0xffffffffu, gs, o);
+  if (li == 0) {
+    red[wi] = gm;
+    red[32 + wi] = gs;
+  }
+  bar_all();
+  double M = ninfd();
+  for (int x = 0; x < nw; ++x) M = fmax(M, red[x]);
+  double S = 0.0;
+  if (M != ninfd())
+    for (int x = 0; x < nw; ++x) S += (red[x] == ninfd()) ? 0.0 : red[32 + x] * exp2(red[x] - M);
+  bar_all();
+  return (M == ninfd()) ? ninfd() : M + log2(S);
+}
+
+__global__ void nw_mitm_kernel(const float* __restrict__ theta, int n, int m, float2* __restrict__ wsa_all,
+                               float2* __restrict__ wsb_all, double* __restrict__ logz, float* __restrict__ marg_all,
+                               int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) char smraw[];
+  const int NW = blockDim.x >> 6;
+  const int b = blockIdx.x;
+  MShared sh = mitm_carve(smraw, NW);
+  const float* th = theta + (size_t)b * (n + 1) * (m + 1) * 3;
+  float* marg = marg_all + (size_t)b * (n + 1) * (m + 1) * 3;
+  const size_t wsz = (size_t)NW * (n + 32) * 32;
+  float2* wsa = wsa_all + (size_t)b * wsz;
+  float2* wsb = wsb_all + (size_t)b * wsz;
+  if (threadIdx.x == 0) sh.flags[0] = 0;
+  const int warp = threadIdx.x >> 5;
+  const bool fwd = warp < NW;
+  const int w = fwd ? warp : warp - NW;
+  // phase lengths (identical for every warp: one barrier per block)
+  int G1 = 0, off2 = 1 << 30, G2 = 0;
+  for (int x = 0; x < NW; ++x) {
+    const int RF = mitm_rf(x, n, NW), QB = n - mitm_rf(NW - 1 - x, n, NW) - 1;
+    G1 = max(G1, max((RF + 31 + kBlk + kLag * x) / kBlk, (QB + 31 + kBlk + kLag * x) / kBlk) + 1);
+    off2 = min(off2, min((RF + 1 + kLag * x) / kBlk, (QB + 1 + kLag * x) / kBlk));
+  }
+  for (int x = 0; x < NW; ++x) G2 = max(G2, (n + 33 + kBlk + kLag * x) / kBlk - off2 + 1);
+  FState fs{{ninf(), 0.f}, {ninf(), 0.f}, ninf(), 0.f};
+  BState bs{{ninf(), 0.f}, {ninf(), 0.f}, {ninf(), 0.f}, {ninf(), 0.f}, 0.f};
+  bar_all();
+  if (fwd)
+    mitm_fwd<1>(th, n, m, NW, sh, mitm_rf(w, n, NW), 0, G1, wsa, wsb, 0.f, ninf(), nullptr, fs, sh.flags);
+  else
+    mitm_bwd<1>(th, n, m, NW, sh, mitm_rf(NW - 1 - w, n, NW), 0, G1, wsa, wsb, 0.f, ninf(), nullptr, bs);
+  __threadfence_block();
+  bar_all();
+  const double z2 = mitm_z(th, n, m, NW, wsa, wsb, sh.red);
+  const float zint = (z2 == ninfd()) ? 0.f : (float)rint(z2);
+  const float zfrac = (z2 == ninfd()) ? ninf() : (float)(z2 - rint(z2));
+  if (fwd)
+    mitm_fwd<2>(th, n, m, NW, sh, mitm_rf(w, n, NW), off2, G2, wsa, wsb, zint, zfrac, marg, fs, sh.flags);
+  else
+    mitm_bwd<2>(th, n, m, NW, sh, mitm_rf(NW - 1 - w, n, NW), off2, G2, wsa, wsb, zint, zfrac, marg, bs);
+  bar_all();
+  if (threadIdx.x == 0) {
+    const double z = (z2 == ninfd()) ? ninfd() : z2 * (double)SDB_LN2;
+    status[b] = sh.flags[0] ? SDB_ST_INVALID : (z == ninfd() ? SDB_ST_VACUOUS : SDB_ST_OK);
+    logz[b] = z;
+  }
+}
+
+int mitm_ok(int n, int m) {
+  const int NW = (m + 1 + 31) / 32;
+  return NW <= 10 && n >= 40 * (NW - 1) + 32 && mitm_smem_bytes(NW) <= 220 * 1024;
+}
+
 struct NwWs {
   float* wsb;
   float* wsk;
   int8_t* choice;
+  float2* wsa2;  // meet-in-the-middle alpha / beta (v, O)
+  float2* wsb2;
 };
 
 NwWs nw_carve_ws(void* base, int64_t B, int n, int m, int mode, size_t* bytes) {
@@ -537,7 +1076,10 @@ NwWs nw_carve_ws(void* base, int64_t B, int n, int m, int mode, size_t* bytes) {
   const size_t wsz = (size_t)NW * (n + 32);
   Carve c(base);
   NwWs w{};
-  if (mode == 1) {
+  if (mode == 1 && mitm_ok(n, m)) {
+    w.wsa2 = c.take<float2>((size_t)B * wsz * 32);
+    w.wsb2 = c.take<float2>((size_t)B * wsz * 32);
+  } else if (mode == 1) {
     w.wsb = c.take<float>((size_t)B * wsz * 32);
     w.wsk = c.take<float>((size_t)B * wsz);
   }
@@ -557,6 +1099,14 @@ int nw_launch(const float* theta, int64_t B, int n, int m, NwWs ws, double* logz
     nw_max_kernel<<<(unsigned)B, 32 * NW, smem, s>>>(theta, n, m, ws.choice, score, status);
     SDB_CHECK_LAUNCH();
     nw_walk_kernel<<<(unsigned)((B + 127) / 128), 128, 0, s>>>(ws.choice, n, m, NW, B, status, path);
+    SDB_CHECK_LAUNCH();
+    return SDB_OK;
+  }
+  if (kMode == 1 && ws.wsa2) {
+    const size_t sm2 = mitm_smem_bytes(NW);
+    if (cudaFuncSetAttribute(nw_mitm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2) != cudaSuccess)
+      return SDB_ERR_CUDA;
+    nw_mitm_kernel<<<(unsigned)B, 64 * NW, sm2, s>>>(theta, n, m, ws.wsa2, ws.wsb2, logz, marg, status);
     SDB_CHECK_LAUNCH();
     return SDB_OK;
   }

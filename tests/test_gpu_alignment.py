@@ -82,3 +82,39 @@ def test_alignment_status():
     assert st.cpu().tolist() == [0, 1, 2]
     assert logz[1].item() == NEG_INF
     assert float(marg[1].abs().sum()) == 0.0
+
+
+# Shapes on the meet-in-the-middle path (n >= 40 (NW-1) + 32), including
+# m + 1 a multiple of 32 (no padding lanes), one padding-heavy strip, and
+# many strips.
+@pytest.mark.parametrize("B,n,m", [(2, 32, 5), (3, 100, 63), (2, 80, 32), (2, 300, 200), (2, 400, 287),
+                                   (2, 201, 127), (3, 513, 129)])
+def test_alignment_mitm_vs_oracle(B, n, m):
+    need_gpu()
+    th = batch_alignment(2000 + n + m, B, n, m)
+    logz, marg, st = K.nw_fb(dev(th))
+    assert (st.cpu().numpy() == 0).all()
+    for b in range(B):
+        z, mg = O.nw_marginals(th[b])
+        assert abs(logz[b].item() - z) <= RTOL * abs(z)
+        np.testing.assert_allclose(marg[b].cpu().numpy(), mg, rtol=RTOL, atol=ATOL)
+
+
+def test_alignment_mitm_masked_and_vacuous():
+    """Banded alignment (cells far from the diagonal forbidden), a vacuous
+    instance and an invalid one, all on the meet-in-the-middle path."""
+    need_gpu()
+    n, m = 160, 96
+    th = batch_alignment(77, 4, n, m)
+    ii, jj = np.meshgrid(np.arange(n + 1), np.arange(m + 1), indexing="ij")
+    band = np.abs(ii * m - jj * n) > 12 * n
+    th[0][band] = NEG_INF
+    th[1, :, 50, :] = NEG_INF  # column 50 unreachable -> no path
+    th[2, 70, 40, 0] = np.inf
+    logz, marg, st = K.nw_fb(dev(th))
+    assert st.cpu().tolist() == [0, 1, 2, 0]
+    assert logz[1].item() == NEG_INF and float(marg[1].abs().sum()) == 0.0
+    for b in (0, 3):
+        z, mg = O.nw_marginals(th[b])
+        assert abs(logz[b].item() - z) <= RTOL * abs(z)
+        np.testing.assert_allclose(marg[b].cpu().numpy(), mg, rtol=RTOL, atol=ATOL)
