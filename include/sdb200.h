@@ -166,6 +166,25 @@ int sdb_pcfg_fb(const float* root, const float* rules, const float* emissions, c
                 int32_t n, int32_t NT, int32_t PT, double* logz, float* span_marg, int32_t* status,
                 void* workspace, size_t ws_bytes, void* stream);
 
+/* sdb_pcfg_grad replaces pcfg_gradients in full (constituency.py:292-340;
+ * potential_marginals, dist.py:113-114): logz [B], span_marg [B,n,n] (the
+ * "sticky" gradient), grad_root [B,NT], grad_rules [B,NT,S,S] (expected
+ * anchored rule counts, may exceed 1), grad_emissions [B,n,PT]. */
+size_t sdb_pcfg_grad_workspace(int64_t B, int32_t n, int32_t NT, int32_t PT);
+int sdb_pcfg_grad(const float* root, const float* rules, const float* emissions, const float* sticky, int64_t B,
+                  int32_t n, int32_t NT, int32_t PT, double* logz, float* span_marg, float* grad_root,
+                  float* grad_rules, float* grad_emissions, int32_t* status, void* workspace, size_t ws_bytes,
+                  void* stream);
+
+/* sdb_pcfg_viterbi replaces pcfg_max_score, _pcfg_walk and pcfg_argmax
+ * (constituency.py:275-277, 343-371): fp64 max-plus chart with the
+ * reference's sums and first-maximum picks.  span_mask [B,n,n] int8 0/1,
+ * score [B] = pcfg_max_score.  Workspace: the fp64 chart. */
+size_t sdb_pcfg_viterbi_workspace(int64_t B, int32_t n, int32_t NT, int32_t PT);
+int sdb_pcfg_viterbi(const float* root, const float* rules, const float* emissions, const float* sticky, int64_t B,
+                     int32_t n, int32_t NT, int32_t PT, int8_t* span_mask, double* score, int32_t* status,
+                     void* workspace, size_t ws_bytes, void* stream);
+
 /* ----------------------------------------------------------- semi-Markov --
  * SemiMarkovCRF (chain.py:214-247): segment_potentials [B,n,s,m,m]
  * (start, width-1, prev label, label); virtual start label 0.

@@ -43,6 +43,12 @@ SIGNATURES = {
     "sdb_pcfg_fb_workspace": (_sz, [_i64, _i32, _i32, _i32]),
     "sdb_pcfg_fb": (ctypes.c_int, [_c_p, _c_p, _c_p, _c_p, _i64, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _sz,
                                    _c_p]),
+    "sdb_pcfg_grad_workspace": (_sz, [_i64, _i32, _i32, _i32]),
+    "sdb_pcfg_grad": (ctypes.c_int, [_c_p, _c_p, _c_p, _c_p, _i64, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p,
+                                     _c_p, _c_p, _sz, _c_p]),
+    "sdb_pcfg_viterbi_workspace": (_sz, [_i64, _i32, _i32, _i32]),
+    "sdb_pcfg_viterbi": (ctypes.c_int, [_c_p, _c_p, _c_p, _c_p, _i64, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p,
+                                        _sz, _c_p]),
     "sdb_semimarkov_fb": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p]),
     "sdb_semimarkov_viterbi_workspace": (_sz, [_i64, _i32, _i32, _i32]),
     "sdb_semimarkov_viterbi": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p, _sz,

@@ -360,15 +360,18 @@ class PCFGBackend(Backend):
     def argmax_algo(self, d):
         return "max-plus-pcfg"
 
-    def run(self, ds, marginals=True, full=False):
-        if full:
-            from .errors import UnsupportedInference
+    def _inputs(self, ds):
+        return (to_dev([d.root for d in ds]), to_dev([d.binary_rules for d in ds]), to_dev([d.emissions for d in ds]),
+                to_dev([d.sticky for d in ds]))
 
-            raise UnsupportedInference("PCFG rule/root/emission expected counts are not on the GPU path yet")
-        root = to_dev([d.root for d in ds])
-        rules = to_dev([d.binary_rules for d in ds])
-        emis = to_dev([d.emissions for d in ds])
-        sticky = to_dev([d.sticky for d in ds])
+    def run(self, ds, marginals=True, full=False):
+        root, rules, emis, sticky = self._inputs(ds)
+        if full:
+            # potential_marginals: all four gradients of pcfg_gradients (constituency.py:292-340)
+            logz, g, st = K.pcfg_grad(root, rules, emis, sticky)
+            gh = {k: to_host(v).astype(np.float64) for k, v in g.items()}
+            out = [{k: gh[k][i] for k in ("root", "binary_rules", "emissions", "sticky")} for i in range(len(ds))]
+            return Result(to_host(logz), to_host(st), out, self.vacuous_msg, public_keys=("sticky",))
         logz, marg, st = K.pcfg_fb(root, rules, emis, sticky, marginals)
         out = None
         if marginals:
@@ -377,9 +380,16 @@ class PCFGBackend(Backend):
         return Result(to_host(logz), to_host(st), out, self.vacuous_msg)
 
     def argmax(self, ds):
-        from .errors import UnsupportedInference
+        # pcfg_argmax (constituency.py:366-371): fp64 max-plus chart + first-max walk
+        root, rules, emis, sticky = self._inputs(ds)
+        mask, score, st = K.pcfg_viterbi(root, rules, emis, sticky)
+        mh = to_host(mask).astype(np.float64)
 
-        raise UnsupportedInference("PCFG argmax is not on the GPU path yet")
+        def build(i):
+            return {"sticky": mh[i]}
+
+        # the PCFG argmax score is pcfg_max_score (dist.py:153-154, 164-165)
+        return ArgmaxResult(to_host(st), build, self.vacuous_msg, score=to_host(score))
 
 
 # ------------------------------------------------------------ semi-Markov

@@ -45,9 +45,11 @@ struct PcfgWs {
   double* osc;  // [B][n][n]
   float* P;     // [B][n][3][32][32] per-width scratch (P in inside, Q in outside)
   float* Q2;    // [B][n][3][32][32] transposed Q for left pushes
+  float* P2;    // [B][n][3][32][32] inside pair products recomputed in the outside pass (mode 2)
+  float* G;     // [B][4][32 A][32 B][32 C] expected rule counts before the exp(rule) factor (mode 2)
 };
 
-PcfgWs pcfg_carve(void* base, int64_t B, int n, int NT, int PT, size_t* bytes) {
+PcfgWs pcfg_carve(void* base, int64_t B, int n, int NT, int PT, size_t* bytes, bool grad = false) {
   const size_t S = NT + PT;
   Carve c(base);
   PcfgWs w;
@@ -59,6 +61,8 @@ PcfgWs pcfg_carve(void* base, int64_t B, int n, int NT, int PT, size_t* bytes) {
   w.osc = c.take<double>((size_t)B * n * n);
   w.P = c.take<float>((size_t)B * n * 3 * 1024);
   w.Q2 = c.take<float>((size_t)B * n * 3 * 1024);
+  w.P2 = grad ? c.take<float>((size_t)B * n * 3 * 1024) : nullptr;
+  w.G = grad ? c.take<float>((size_t)B * 4 * 32768) : nullptr;
   *bytes = c.used;
   return w;
 }
@@ -80,11 +84,20 @@ __device__ __forceinline__ int ccnt(int t, int NT, int PT) { return (t == 2 || t
 // block of slot `sl` at width w: w == 2 -> only slot 0 = t3; else slot 0 = t0 (interior), 1 = t1 (k=i), 2 = t2 (k=j-1)
 __device__ __forceinline__ int slot_type(int sl, int w) { return w == 2 ? 3 : sl; }
 
-template <bool kMarg>
+struct PcfgGradOut {
+  float* root;   // [B][NT]
+  float* rules;  // [B][NT][S][S]
+  float* emis;   // [B][n][PT]
+};
+
+// kMode: 0 = log Z, 1 = + span marginals, 2 = + rule / root / emission
+// expected counts (the full pcfg_gradients, constituency.py:292-340)
+template <int kMode>
 __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
     const float* __restrict__ root_all, const float* __restrict__ rules_all, const float* __restrict__ emis_all,
     const float* __restrict__ sticky_all, int n, int NT, int PT, PcfgWs ws, double* __restrict__ logz,
-    float* __restrict__ marg_all, int32_t* __restrict__ status) {
+    float* __restrict__ marg_all, PcfgGradOut gout, int32_t* __restrict__ status) {
+  constexpr bool kMarg = kMode >= 1;
   extern __shared__ __align__(16) float smf[];
   const int S = NT + PT;
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -102,6 +115,9 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
   float* Q2 = ws.Q2 + (size_t)b * n * 3 * 1024;
   __shared__ int badsh;
   __shared__ double smax_s[kMaxN];
+  __shared__ double smax2_s[kMaxN];
+  float* P2 = kMode == 2 ? ws.P2 + (size_t)b * n * 3 * 1024 : nullptr;
+  float* G = kMode == 2 ? ws.G + (size_t)b * 4 * 32768 : nullptr;
   if (tid == 0) badsh = 0;
   __syncthreads();
   auto STK = [&](int i, int j) -> float { return sticky ? sticky[i * n + j] : 0.f; };
@@ -125,6 +141,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
     if (sticky)
       for (int e = tid; e < n * n; e += kThreads) bad |= !(sticky[e] == 0.f || sticky[e] == ninf());
     if (bad) atomicOr(&badsh, 1);
+    if (kMode == 2)
+      for (int e = tid; e < 4 * 32768; e += kThreads) G[e] = 0.f;
   }
   __syncthreads();
   // ---- width 1: preterminal slots (constituency.py:257-258)
@@ -138,20 +156,16 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
   }
   __syncthreads();
 
-  float* RTs = smf;                 // [3][kBS][32 C][32 A]
-  float* Ps = smf + 3 * kBS * 1024; // [kMaxN spans][3][kBS][32 C]
-
-  // ================================================================ inside
-  for (int w = 2; w <= n; ++w) {
+  // P-build for all spans of width w (warp per span): P_t[B][C] = sum_k f_k u_ik[B] u_(k+1)j[C],
+  // f_k = exp(s_ik + s_(k+1)j - Smax); Smax -> smx[i]
+  auto pbuild = [&](int w, float* dst, double* smx) {
     const int nsp = n - w + 1;
-    const int nslot = (w == 2) ? 1 : 3;
-    // ---- P-build: warp per span
     for (int i = warp; i < nsp; i += kWarps) {
       const int j = i + w - 1;
       double sm = ninfd();
       for (int k = i + lane; k < j; k += 32) sm = fmax(sm, isc[i * n + k] + isc[(k + 1) * n + j]);
       sm = warp_maxd(sm);
-      if (lane == 0) smax_s[i] = sm;
+      if (lane == 0) smx[i] = sm;
       float acc[3][32];
 #pragma unroll
       for (int sl = 0; sl < 3; ++sl)
@@ -174,12 +188,23 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
           }
         }
       }
-      float* pp = Pw + (size_t)i * 3 * 1024;
+      float* pp = dst + (size_t)i * 3 * 1024;
 #pragma unroll
       for (int sl = 0; sl < 3; ++sl)
 #pragma unroll
         for (int q = 0; q < 32; ++q) pp[sl * 1024 + q * 32 + lane] = acc[sl][q];  // [slot][B][C]
     }
+  };
+
+  float* RTs = smf;                 // [3][kBS][32 C][32 A]
+  float* Ps = smf + 3 * kBS * 1024; // [kMaxN spans][3][kBS][32 C]
+
+  // ================================================================ inside
+  for (int w = 2; w <= n; ++w) {
+    const int nsp = n - w + 1;
+    const int nslot = (w == 2) ? 1 : 3;
+    // ---- P-build: warp per span
+    pbuild(w, Pw, smax_s);
     __syncthreads();
     // ---- contraction: inner[s][A] = sum_{slot,B,C} R_t[A,B',C'] P[s][slot][B][C]
     float inner[kSpW];
@@ -258,8 +283,14 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
   }
   if (!kMarg) return;
   float* mg = marg_all + (size_t)b * n * n;
+  const int S2 = S * S;
   if (Z == ninfd() || badsh) {
     for (int e = tid; e < n * n; e += kThreads) mg[e] = 0.f;
+    if (kMode == 2) {
+      for (int e = tid; e < NT; e += kThreads) gout.root[(size_t)b * NT + e] = 0.f;
+      for (int e = tid; e < NT * S2; e += kThreads) gout.rules[(size_t)b * NT * S2 + e] = 0.f;
+      for (int e = tid; e < n * PT; e += kThreads) gout.emis[(size_t)b * n * PT + e] = 0.f;
+    }
     return;
   }
 
@@ -279,6 +310,36 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
   for (int w = n; w >= 2; --w) {
     const int nsp = n - w + 1;
     const int nslot = (w == 2) ? 1 : 3;
+    if (kMode == 2) {
+      // expected rule counts of the width's parents (constituency.py:312-314):
+      // G_t[A][B][C] += exp(o_s + sticky_s + Smax_s - Z) o_s[A] P_s[t][B][C]; exp(rule) applied at the end
+      float* Cs = smf + 3 * kBS * 1024 + kMaxN * 3 * kBS * 32;  // [nsp][32 A]
+      pbuild(w, P2, smax2_s);
+      __syncthreads();
+      for (int e = tid; e < nsp * 32; e += kThreads) {
+        const int s2 = e >> 5, A = e & 31, i = s2, j = s2 + w - 1;
+        const double c = osc[i * n + j] + (double)STK(i, j) + smax2_s[s2] - Z;
+        Cs[e] = (A < NT && c != ninfd()) ? (float)(exp(c) * (double)ou[(size_t)(i * n + j) * 32 + A]) : 0.f;
+      }
+      __syncthreads();
+      for (int sl = 0; sl < nslot; ++sl) {
+        float* Gt = G + (size_t)slot_type(sl, w) * 32768;
+        for (int r = 0; r < 4; ++r) {
+          const int bc = tid + kThreads * r;
+          float acc[32];
+#pragma unroll
+          for (int A = 0; A < 32; ++A) acc[A] = 0.f;
+          for (int s2 = 0; s2 < nsp; ++s2) {
+            const float pv = P2[(size_t)s2 * 3 * 1024 + sl * 1024 + bc];
+            if (pv == 0.f) continue;
+#pragma unroll
+            for (int A = 0; A < 32; ++A) acc[A] = fmaf(Cs[s2 * 32 + A], pv, acc[A]);
+          }
+          for (int A = 0; A < NT; ++A) Gt[A * 1024 + bc] += acc[A];
+        }
+      }
+      __syncthreads();
+    }
     // stage parent outside vectors (with the parent's own sticky folded into its scale)
     for (int e = tid; e < nsp * 32; e += kThreads) {
       const int s = e >> 5, A = e & 31;
@@ -382,6 +443,180 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
     }
     if (lane == 0) mg[e] = v;
   }
+  if (kMode != 2) return;
+  __syncthreads();
+  // root gradient exp(root + chart[0,n-1] - Z) (constituency.py:326)
+  if (warp == 0 && lane < NT) {
+    const double si = isc[n - 1];
+    const float u = iu[(size_t)(n - 1) * 32 + lane];
+    gout.root[(size_t)b * NT + lane] =
+        (si == ninfd() || !(u > 0.f)) ? 0.f : (float)(exp((double)root[lane] + si - Z) * (double)u);
+  }
+  // emission gradient exp(outside[i,i,PT] + sticky[i,i] + emissions - Z) (constituency.py:327-329)
+  for (int i = warp; i < n; i += kWarps) {
+    const int e = i * n + i;
+    const double c = osc[e] + (double)STK(i, i) + isc[e] - Z;
+    const float v = ou[(size_t)e * 32 + lane] * iu[(size_t)e * 32 + lane];
+    if (lane < PT) gout.emis[((size_t)b * n + i) * PT + lane] = (c == ninfd() || !(v > 0.f)) ? 0.f : (float)(exp(c) * (double)v);
+  }
+  // rule gradient = G_t[A][B'][C'] * exp(rules[A][B][C])
+  for (int e = tid; e < NT * S2; e += kThreads) {
+    const int A = e / S2, r = e - A * S2, Bf = r / S, Cf = r - Bf * S;
+    const int t = (Bf < NT ? 0 : 1) + (Cf < NT ? 0 : 2);
+    const int Bi = Bf - boff(t, NT), Ci = Cf - coff(t, NT);
+    const size_t gi = (size_t)t * 32768 + ((size_t)A * 32 + Bi) * 32 + Ci;
+    gout.rules[(size_t)b * NT * S2 + e] = G[gi] * RE[gi];
+  }
+}
+
+
+// ================================================================ max-plus
+// fp64 max-plus chart (constituency.py:246-266 with reduce = max, exact sums
+// in the reference's order) and the top-down derivation walk
+// (constituency.py:343-371): first-maximum picks over the root symbols and
+// over the flattened (split, left symbol, right symbol) candidates.
+struct ArgBest {
+  double v;
+  int i;
+};
+__device__ __forceinline__ ArgBest arg_better(ArgBest a, ArgBest b) {
+  return (b.v > a.v || (b.v == a.v && b.i < a.i)) ? b : a;
+}
+__device__ ArgBest block_argmax(ArgBest x, ArgBest* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ArgBest y;
+    y.v = __shfl_xor_sync(0xffffffffu, x.v, o);
+    y.i = __shfl_xor_sync(0xffffffffu, x.i, o);
+    x = arg_better(x, y);
+  }
+  if (lane == 0) red[warp] = x;
+  __syncthreads();
+  ArgBest r = red[0];
+  for (int q = 1; q < (int)(blockDim.x >> 5); ++q) r = arg_better(r, red[q]);
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kThreads) pcfg_max_kernel(
+    const float* __restrict__ root_all, const float* __restrict__ rules_all, const float* __restrict__ emis_all,
+    const float* __restrict__ sticky_all, int n, int NT, int PT, double* __restrict__ chart_all,
+    int8_t* __restrict__ mask_all, double* __restrict__ score, int32_t* __restrict__ status) {
+  extern __shared__ double pairs[];  // [S][S]
+  __shared__ ArgBest red[kWarps];
+  __shared__ int stk_i[2 * kMaxN], stk_j[2 * kMaxN], stk_a[2 * kMaxN];
+  __shared__ int badsh;
+  const int S = NT + PT, S2 = S * S;
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float* root = root_all + (size_t)b * NT;
+  const float* rules = rules_all + (size_t)b * NT * S2;
+  const float* emis = emis_all + (size_t)b * n * PT;
+  const float* sticky = sticky_all ? sticky_all + (size_t)b * n * n : nullptr;
+  double* chart = chart_all + (size_t)b * n * n * S;
+  int8_t* mask = mask_all + (size_t)b * n * n;
+  auto STK = [&](int i, int j) -> double { return sticky ? (double)sticky[i * n + j] : 0.0; };
+  auto CH = [&](int i, int j) -> double* { return chart + ((size_t)i * n + j) * S; };
+  if (tid == 0) badsh = 0;
+  __syncthreads();
+  {
+    int bad = 0;
+    for (int e = tid; e < NT * S2; e += kThreads) bad |= bad_input(rules[e]);
+    for (int e = tid; e < NT; e += kThreads) bad |= bad_input(root[e]);
+    for (int e = tid; e < n * PT; e += kThreads) bad |= bad_input(emis[e]);
+    if (sticky)
+      for (int e = tid; e < n * n; e += kThreads) bad |= !(sticky[e] == 0.f || sticky[e] == ninf());
+    if (bad) atomicOr(&badsh, 1);
+    for (int e = tid; e < n * n; e += kThreads) mask[e] = 0;
+  }
+  for (int e = tid; e < n * S; e += kThreads) {
+    const int i = e / S, X = e - i * S;
+    CH(i, i)[X] = (X >= NT) ? (double)emis[i * PT + X - NT] + STK(i, i) : ninfd();
+  }
+  __syncthreads();
+  for (int w = 2; w <= n; ++w) {
+    for (int i = 0; i + w - 1 < n; ++i) {
+      const int j = i + w - 1;
+      for (int e = tid; e < S2; e += kThreads) {
+        const int Bq = e / S, Cq = e - Bq * S;
+        double m = ninfd();
+        for (int k = i; k < j; ++k) m = fmax(m, CH(i, k)[Bq] + CH(k + 1, j)[Cq]);
+        pairs[e] = m;
+      }
+      __syncthreads();
+      for (int A = warp; A < S; A += kWarps) {
+        double m = ninfd();
+        if (A < NT) {
+          const float* ra = rules + (size_t)A * S2;
+          for (int e = lane; e < S2; e += 32) m = fmax(m, (double)ra[e] + pairs[e]);
+          m = warp_maxd(m);
+        }
+        if (lane == 0) CH(i, j)[A] = (A < NT) ? m + STK(i, j) : ninfd();
+      }
+      __syncthreads();
+    }
+  }
+  // root pick (constituency.py:346)
+  ArgBest x{ninfd(), 1 << 30};
+  for (int A = tid; A < NT; A += kThreads) x = arg_better(x, ArgBest{(double)root[A] + CH(0, n - 1)[A], A});
+  const ArgBest r0 = block_argmax(x, red);
+  const double best = (n == 1) ? ninfd() : r0.v;  // a width-1 sentence has no NT derivation
+  if (tid == 0) {
+    status[b] = badsh ? SDB_ST_INVALID : (best == ninfd() ? SDB_ST_VACUOUS : SDB_ST_OK);
+    score[b] = best;
+  }
+  if (badsh || best == ninfd()) return;
+  // walk (stack order is irrelevant for the span mask)
+  int top = 0;
+  if (tid == 0) {
+    stk_i[0] = 0;
+    stk_j[0] = n - 1;
+    stk_a[0] = r0.i;
+  }
+  top = 1;
+  __syncthreads();
+  while (top > 0) {
+    --top;
+    const int i = stk_i[top], j = stk_j[top], a = stk_a[top];
+    __syncthreads();
+    if (tid == 0) mask[i * n + j] = 1;
+    if (i == j) continue;
+    const int width = j - i;
+    const float* ra = rules + (size_t)a * S2;
+    ArgBest y{ninfd(), 1 << 30};
+    for (int e = tid; e < width * S2; e += kThreads) {
+      const int ko = e / S2, r = e - ko * S2, Bq = r / S, Cq = r - Bq * S;
+      const int k = i + ko;
+      const double v = ((double)ra[r] + CH(i, k)[Bq]) + CH(k + 1, j)[Cq];
+      if (v > y.v) y = ArgBest{v, e};
+    }
+    const ArgBest pk = block_argmax(y, red);
+    const int ko = pk.i / S2, r = pk.i - ko * S2, Bq = r / S, Cq = r - Bq * S;
+    const int k = i + ko;
+    if (tid == 0) {
+      stk_i[top] = i;
+      stk_j[top] = k;
+      stk_a[top] = Bq;
+      stk_i[top + 1] = k + 1;
+      stk_j[top + 1] = j;
+      stk_a[top + 1] = Cq;
+    }
+    top += 2;
+    __syncthreads();
+  }
+}
+
+template <int kMode>
+int pcfg_launch(const float* root, const float* rules, const float* emissions, const float* sticky, int64_t B, int n,
+                int NT, int PT, PcfgWs ws, double* logz, float* span_marg, PcfgGradOut gout, int32_t* status,
+                cudaStream_t s) {
+  const size_t smem = (size_t)(3 * kBS * 1024 + kMaxN * 3 * kBS * 32 + (kMode == 2 ? kMaxN * 32 : 0)) * 4;
+  if (cudaFuncSetAttribute(pcfg_kernel<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return SDB_ERR_CUDA;
+  pcfg_kernel<kMode><<<(unsigned)B, kThreads, smem, s>>>(root, rules, emissions, sticky, n, NT, PT, ws, logz,
+                                                         span_marg, gout, status);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
 }
 
 int pcfg_check(int64_t B, int n, int NT, int PT) {
@@ -408,19 +643,52 @@ extern "C" int sdb_pcfg_fb(const float* root, const float* rules, const float* e
   size_t need = 0;
   PcfgWs ws = pcfg_carve(workspace, B, n, NT, PT, &need);
   if (!workspace || ws_bytes < need) return SDB_ERR_WORKSPACE;
-  const size_t smem = (size_t)(3 * kBS * 1024 + kMaxN * 3 * kBS * 32) * 4;
   cudaStream_t s = (cudaStream_t)stream;
-  if (span_marg) {
-    if (cudaFuncSetAttribute(pcfg_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return SDB_ERR_CUDA;
-    pcfg_kernel<true><<<(unsigned)B, kThreads, smem, s>>>(root, rules, emissions, sticky, n, NT, PT, ws, logz,
-                                                          span_marg, status);
-  } else {
-    if (cudaFuncSetAttribute(pcfg_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return SDB_ERR_CUDA;
-    pcfg_kernel<false><<<(unsigned)B, kThreads, smem, s>>>(root, rules, emissions, sticky, n, NT, PT, ws, logz,
-                                                           nullptr, status);
-  }
+  return span_marg ? pcfg_launch<1>(root, rules, emissions, sticky, B, n, NT, PT, ws, logz, span_marg, PcfgGradOut{},
+                                    status, s)
+                   : pcfg_launch<0>(root, rules, emissions, sticky, B, n, NT, PT, ws, logz, nullptr, PcfgGradOut{},
+                                    status, s);
+}
+
+extern "C" size_t sdb_pcfg_grad_workspace(int64_t B, int32_t n, int32_t NT, int32_t PT) {
+  size_t bytes = 0;
+  pcfg_carve(nullptr, B, n, NT, PT, &bytes, true);
+  return bytes;
+}
+
+extern "C" int sdb_pcfg_grad(const float* root, const float* rules, const float* emissions, const float* sticky,
+                             int64_t B, int32_t n, int32_t NT, int32_t PT, double* logz, float* span_marg,
+                             float* grad_root, float* grad_rules, float* grad_emissions, int32_t* status,
+                             void* workspace, size_t ws_bytes, void* stream) {
+  int rc = pcfg_check(B, n, NT, PT);
+  if (rc) return rc;
+  if (!root || !rules || !emissions || !logz || !span_marg || !grad_root || !grad_rules || !grad_emissions || !status)
+    return SDB_ERR_ARG;
+  if (B == 0) return SDB_OK;
+  size_t need = 0;
+  PcfgWs ws = pcfg_carve(workspace, B, n, NT, PT, &need, true);
+  if (!workspace || ws_bytes < need) return SDB_ERR_WORKSPACE;
+  return pcfg_launch<2>(root, rules, emissions, sticky, B, n, NT, PT, ws, logz, span_marg,
+                        PcfgGradOut{grad_root, grad_rules, grad_emissions}, status, (cudaStream_t)stream);
+}
+
+extern "C" size_t sdb_pcfg_viterbi_workspace(int64_t B, int32_t n, int32_t NT, int32_t PT) {
+  return (size_t)B * n * n * (NT + PT) * sizeof(double);
+}
+
+extern "C" int sdb_pcfg_viterbi(const float* root, const float* rules, const float* emissions, const float* sticky,
+                                int64_t B, int32_t n, int32_t NT, int32_t PT, int8_t* span_mask, double* score,
+                                int32_t* status, void* workspace, size_t ws_bytes, void* stream) {
+  int rc = pcfg_check(B, n, NT, PT);
+  if (rc) return rc;
+  if (!root || !rules || !emissions || !span_mask || !score || !status) return SDB_ERR_ARG;
+  if (B == 0) return SDB_OK;
+  if (!workspace || ws_bytes < sdb_pcfg_viterbi_workspace(B, n, NT, PT)) return SDB_ERR_WORKSPACE;
+  const size_t smem = (size_t)(NT + PT) * (NT + PT) * sizeof(double);
+  if (cudaFuncSetAttribute(pcfg_max_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return SDB_ERR_CUDA;
+  pcfg_max_kernel<<<(unsigned)B, kThreads, smem, (cudaStream_t)stream>>>(root, rules, emissions, sticky, n, NT, PT,
+                                                                       (double*)workspace, span_mask, score, status);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
 }

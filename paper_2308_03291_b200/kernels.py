@@ -275,6 +275,51 @@ def pcfg_fb(root, rules, emissions, sticky=None, marginals: bool = True):
     return logz, marg, status
 
 
+def pcfg_grad(root, rules, emissions, sticky=None):
+    """constituency.py:292-340 (pcfg_gradients) batched -> (logz [B] f64,
+    {"root" [B,NT], "binary_rules" [B,NT,S,S], "emissions" [B,n,PT],
+    "sticky" [B,n,n]} fp32, status)."""
+    lib = _lib.load()
+    root = f32(root, "root")
+    rules = f32(rules, "binary_rules")
+    emis = f32(emissions, "emissions")
+    st_in = f32(sticky, "sticky") if sticky is not None else None
+    B, NT = root.shape
+    n, PT = emis.shape[1], emis.shape[2]
+    dev = root.device
+    logz = torch.empty(B, dtype=torch.float64, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    g = {"root": torch.empty_like(root), "binary_rules": torch.empty_like(rules), "emissions": torch.empty_like(emis),
+         "sticky": torch.empty(B, n, n, dtype=torch.float32, device=dev)}
+    ws = workspace(lib.sdb_pcfg_grad_workspace(B, n, NT, PT), dev)
+    rc = lib.sdb_pcfg_grad(ptr(root), ptr(rules), ptr(emis), ptr(st_in), B, n, NT, PT, ptr(logz), ptr(g["sticky"]),
+                           ptr(g["root"]), ptr(g["binary_rules"]), ptr(g["emissions"]), ptr(status), ptr(ws),
+                           ws.numel(), stream_ptr(dev))
+    _lib.check(rc, "sdb_pcfg_grad")
+    return logz, g, status
+
+
+def pcfg_viterbi(root, rules, emissions, sticky=None):
+    """constituency.py:275-277, 343-371 batched -> (span_mask [B,n,n] int8,
+    score [B] f64 = pcfg_max_score, status)."""
+    lib = _lib.load()
+    root = f32(root, "root")
+    rules = f32(rules, "binary_rules")
+    emis = f32(emissions, "emissions")
+    st_in = f32(sticky, "sticky") if sticky is not None else None
+    B, NT = root.shape
+    n, PT = emis.shape[1], emis.shape[2]
+    dev = root.device
+    mask = torch.empty(B, n, n, dtype=torch.int8, device=dev)
+    score = torch.empty(B, dtype=torch.float64, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    ws = workspace(lib.sdb_pcfg_viterbi_workspace(B, n, NT, PT), dev)
+    rc = lib.sdb_pcfg_viterbi(ptr(root), ptr(rules), ptr(emis), ptr(st_in), B, n, NT, PT, ptr(mask), ptr(score),
+                              ptr(status), ptr(ws), ws.numel(), stream_ptr(dev))
+    _lib.check(rc, "sdb_pcfg_viterbi")
+    return mask, score, status
+
+
 # ------------------------------------------------------------ semi-Markov
 
 

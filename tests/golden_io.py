@@ -36,18 +36,19 @@ class Case(dict):
     def marg(self, key):
         return self.get(f"marg_{key}")
 
-    def check_marg(self, key, got, rtol=1e-4, atol=1e-6):
+    def check_marg(self, key, got, rtol=1e-4, atol=1e-6, prefix="marg_"):
         """Compare a full marginal array against the golden (full or
-        subsampled + sum).  Returns max abs error."""
+        subsampled + sum).  Returns max abs error.  prefix "pmarg_" selects
+        the potential_marginals goldens."""
         flat = np.asarray(got, dtype=np.float64).ravel()
-        if f"marg_{key}" in self:
-            ref = np.asarray(self[f"marg_{key}"]).ravel()
+        if f"{prefix}{key}" in self:
+            ref = np.asarray(self[f"{prefix}{key}"]).ravel()
             np.testing.assert_allclose(flat, ref, rtol=rtol, atol=atol)
             return float(np.max(np.abs(flat - ref))) if flat.size else 0.0
-        ix = self[f"marg_{key}_idx"]
-        ref = self[f"marg_{key}_val"]
+        ix = self[f"{prefix}{key}_idx"]
+        ref = self[f"{prefix}{key}_val"]
         np.testing.assert_allclose(flat[ix], ref, rtol=rtol, atol=atol)
-        s = float(self[f"marg_{key}_sum"])
+        s = float(self[f"{prefix}{key}_sum"])
         assert abs(flat.sum() - s) <= rtol * abs(s) + atol * flat.size ** 0.5
         return float(np.max(np.abs(flat[ix] - ref)))
 

@@ -1,4 +1,5 @@
-"""GPU parity: PCFG inside + span marginals (constituency.py:246-340)."""
+"""GPU parity: PCFG inside, span marginals, full gradients (rule / root /
+emission expected counts) and max-plus argmax (constituency.py:246-371)."""
 
 import numpy as np
 import pytest
@@ -70,3 +71,63 @@ def test_pcfg_sticky_mask():
     z, g = O.pcfg_gradients(root[0], rules[0], emis[0], sticky[0])
     assert abs(logz[0].item() - z) <= RTOL * abs(z)
     np.testing.assert_allclose(marg[0].cpu().numpy(), g["sticky"], rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("case", [c for c in load("pcfg") if not c.vacuous], ids=lambda c: str(c.meta))
+def test_pcfg_golden_gradients_and_argmax(case):
+    """potential_marginals returns all four gradients (dist.py:113-114);
+    argmax is bit-exact (fp64 max-plus, first-max walk)."""
+    need_gpu()
+    x = inputs(case)
+    d = sd.PCFG(x["root"], x["binary_rules"], x["emissions"])
+    pm = sd.potential_marginals(d)
+    assert sorted(pm) == ["binary_rules", "emissions", "root", "sticky"]
+    for k in pm:
+        if f"pmarg_{k}" in case or f"pmarg_{k}_idx" in case:
+            case.check_marg(k, pm[k], RTOL, ATOL, prefix="pmarg_")
+    ind, score, algo = sd.argmax_info(d)
+    assert algo == "max-plus-pcfg"
+    np.testing.assert_array_equal(ind["sticky"], case["argmax_sticky"])
+    assert score == float(case.argmax_score)
+
+
+@pytest.mark.parametrize("B,n,nt,pt", [(3, 12, 5, 7), (2, 2, 3, 2), (2, 24, 32, 17), (2, 9, 1, 1)])
+def test_pcfg_gradients_vs_oracle(B, n, nt, pt):
+    need_gpu()
+    root, rules, emis = batch_pcfg(4100, B, n, nt, pt)
+    logz, g, st = K.pcfg_grad(dev(root), dev(rules), dev(emis))
+    assert (st.cpu().numpy() == 0).all()
+    for b in range(B):
+        z, go = O.pcfg_gradients(root[b], rules[b], emis[b])
+        assert abs(logz[b].item() - z) <= RTOL * abs(z) + 1e-9
+        for k in ("root", "binary_rules", "emissions", "sticky"):
+            np.testing.assert_allclose(g[k][b].cpu().numpy(), go[k], rtol=RTOL, atol=ATOL, err_msg=k)
+
+
+@pytest.mark.parametrize("B,n,nt,pt", [(3, 12, 5, 7), (2, 20, 8, 8), (2, 1, 3, 2), (2, 16, 32, 32)])
+def test_pcfg_argmax_vs_oracle(B, n, nt, pt):
+    need_gpu()
+    root, rules, emis = batch_pcfg(4200, B, n, nt, pt)
+    mask, score, st = K.pcfg_viterbi(dev(root), dev(rules), dev(emis))
+    for b in range(B):
+        if n == 1:
+            assert st[b].item() == 1
+            continue
+        mo, so = O.pcfg_argmax(root[b], rules[b], emis[b])
+        np.testing.assert_array_equal(mask[b].cpu().numpy(), mo)  # bit-exact
+        assert score[b].item() == so
+
+
+def test_pcfg_gradient_invariants_config():
+    """C5b shape (B=128, n=64, NT=PT=32): expected rule counts sum to n-1
+    binary nodes, root gradient to 1, each word's emission gradient to 1."""
+    need_gpu()
+    root, rules, emis = batch_pcfg(5100, 128, 64, 32, 32)
+    logz, g, st = K.pcfg_grad(dev(root), dev(rules), dev(emis))
+    assert (st == 0).all()
+    gd = {k: v.double() for k, v in g.items()}
+    one = torch.ones(128, dtype=torch.float64, device="cuda")
+    assert torch.allclose(gd["root"].sum(1), one, rtol=1e-4)
+    assert torch.allclose(gd["binary_rules"].sum((1, 2, 3)), 63 * one, rtol=1e-4)
+    assert torch.allclose(gd["emissions"].sum(2), torch.ones(128, 64, dtype=torch.float64, device="cuda"), rtol=1e-4)
+    assert torch.allclose(gd["sticky"].sum((1, 2)), 127 * one, rtol=1e-4)
