@@ -202,6 +202,45 @@ int sdb_semimarkov_viterbi(const float* segment_potentials, int64_t B, int32_t n
                            int32_t* segments, int32_t* num_segments, double* score, int32_t* status,
                            void* workspace, size_t ws_bytes, void* stream);
 
+
+/* ------------------------------------------------------------- sampling --
+ * Exact samples (dist.py:179-212) with Gumbel-max picks (numerics.py:162-168).
+ * `noise` [B, noise_per_instance] fp64 is the caller's Gumbel stream, drawn
+ * from the reference's own Generator (np.random.default_rng(seed).gumbel),
+ * consumed in the reference's pick order; num samples are drawn back to
+ * back from it; used [B] reports the draws consumed.  fp64 log-semiring
+ * charts in the workspace.  Stream bounds per sample: chain n*m; alignment
+ * 3(n+m); CTC 2+3(T-1); Tree-CRF (2n-1)m + n^2; Eisner n + 4(n+1)^2.
+ *
+ * sdb_chain_sample: chain.py:117-129 (FFBS) -> tags [B,num,n].
+ * sdb_nw_sample: alignment.py:121-150 -> path [B,num,n+1,m+1] (move or -1).
+ * sdb_ctc_sample: alignment.py:304-318, 339-343 -> expanded-lattice state per
+ *   frame [B,num,T].
+ * sdb_tree_sample: constituency.py:113-140 -> labels [B,num,n,n] (-1 = no span).
+ * sdb_eisner_decode: spanning.py:283-331: noise != NULL -> eisner_sample_arcs;
+ *   noise == NULL -> eisner_max_arcs (max-plus charts, first-max picks).
+ *   heads [B,num,n+1] (heads[0] = -1). */
+size_t sdb_chain_sample_workspace(int64_t B, int32_t n, int32_t m);
+int sdb_chain_sample(const float* init, const float* trans, int64_t B, int32_t n, int32_t m, const double* noise,
+                     int64_t noise_per_instance, int32_t num, int32_t* tags, int32_t* used, int32_t* status,
+                     void* workspace, size_t ws_bytes, void* stream);
+size_t sdb_nw_sample_workspace(int64_t B, int32_t n, int32_t m);
+int sdb_nw_sample(const float* theta, int64_t B, int32_t n, int32_t m, const double* noise,
+                  int64_t noise_per_instance, int32_t num, int8_t* path, int32_t* used, int32_t* status,
+                  void* workspace, size_t ws_bytes, void* stream);
+size_t sdb_ctc_sample_workspace(int64_t B, int32_t T, int32_t V, int32_t L);
+int sdb_ctc_sample(const float* frame_potentials, const int32_t* targets, int64_t B, int32_t T, int32_t V, int32_t L,
+                   const double* noise, int64_t noise_per_instance, int32_t num, int32_t* states, int32_t* used,
+                   int32_t* status, void* workspace, size_t ws_bytes, void* stream);
+size_t sdb_tree_sample_workspace(int64_t B, int32_t n, int32_t m);
+int sdb_tree_sample(const float* span_potentials, int64_t B, int32_t n, int32_t m, const double* noise,
+                    int64_t noise_per_instance, int32_t num, int32_t* labels, int32_t* used, int32_t* status,
+                    void* workspace, size_t ws_bytes, void* stream);
+size_t sdb_eisner_decode_workspace(int64_t B, int32_t n);
+int sdb_eisner_decode(const float* adjacency, int64_t B, int32_t n, int32_t single_root, const double* noise,
+                      int64_t noise_per_instance, int32_t num, int32_t* heads, int32_t* used, int32_t* status,
+                      void* workspace, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

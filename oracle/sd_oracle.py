@@ -804,3 +804,139 @@ def heads_score(adj, heads):
     if np.isneginf(vals).any():
         return NEG_INF
     return float(np.sum(vals))
+
+
+# ---------------------------------------------------------------------------
+# sampling (dist.py:179-212) -- Gumbel-max picks from ONE seeded stream
+# ---------------------------------------------------------------------------
+
+
+def sample_log_categorical(rng, logits):
+    """numerics.py:162-168: argmax(where(w > -inf, w + g, -inf)), g = one
+    rng.gumbel draw per logit, first maximum."""
+    w = np.ravel(np.asarray(logits, dtype=np.float64))
+    if not (w > NEG_INF).any():
+        raise ValueError("cannot sample: all categorical weights are -inf")
+    g = rng.gumbel(size=w.shape)
+    return int(np.argmax(np.where(w > NEG_INF, w + g, NEG_INF)))
+
+
+def chain_sample(init, trans, rng):
+    """chain.py:117-129 (forward filtering, backward sampling) -> tags [n]."""
+    al = chain_alpha(init[None], trans[None])[0]
+    if lse_all(al[-1]) == NEG_INF:
+        raise Vacuous("no tag sequence has finite score")
+    n = al.shape[0]
+    tags = np.zeros(n, dtype=np.int64)
+    tags[-1] = sample_log_categorical(rng, al[-1])
+    for t in range(n - 2, -1, -1):
+        tags[t] = sample_log_categorical(rng, al[t] + trans[t][:, tags[t + 1]])
+    return tags
+
+
+def nw_walk(th, al, pick):
+    """alignment.py:121-136 -> path [n+1,m+1] (incoming move or -1)."""
+    n, m = th.shape[0] - 1, th.shape[1] - 1
+    path = np.full((n + 1, m + 1), -1, dtype=np.int64)
+    src = {0: (-1, -1), 1: (-1, 0), 2: (0, -1)}
+    i, j = n, m
+    while (i, j) != (0, 0):
+        moves = [(k, i + di, j + dj) for k, (di, dj) in src.items() if i + di >= 0 and j + dj >= 0]
+        k, si, sj = moves[pick(np.array([al[a, b] + th[i, j, kk] for kk, a, b in moves]))]
+        path[i, j] = k
+        i, j = si, sj
+    return path
+
+
+def nw_sample(th, rng):
+    """alignment.py:146-150."""
+    al = nw_alpha(th)
+    if al[-1, -1] == NEG_INF:
+        raise Vacuous("no alignment path has finite score")
+    return nw_walk(th, al, lambda w: sample_log_categorical(rng, w))
+
+
+def ctc_sample(fp, target, rng):
+    """alignment.py:304-318, 339-343 -> expanded-lattice state per frame [T]."""
+    al, _, skip = ctc_alpha(fp[None], np.asarray(target)[None])
+    al, skip = al[0], skip[0]
+    T, S = al.shape
+    finals = [S - 1] if S == 1 else [S - 1, S - 2]
+    if lse_all(al[-1, finals]) == NEG_INF:
+        raise Vacuous("no frame path collapses to the target")
+    s = finals[sample_log_categorical(rng, al[-1, finals])]
+    states = [s]
+    for t in range(T - 1, 0, -1):
+        preds = [s] + ([s - 1] if s >= 1 else []) + ([s - 2] if s >= 2 and skip[s] else [])
+        s = preds[sample_log_categorical(rng, al[t - 1, preds])]
+        states.append(s)
+    return np.array(states[::-1])
+
+
+def tree_walk(th, ins, pick):
+    """constituency.py:113-126 (LIFO stack: right child first) -> labels [n,n] (-1 = none)."""
+    n = th.shape[0]
+    lab = np.full((n, n), -1, dtype=np.int64)
+    stack = [(0, n - 1)]
+    while stack:
+        i, j = stack.pop()
+        lab[i, j] = pick(th[i, j])
+        if i == j:
+            continue
+        k = i + pick(ins[i, i:j] + ins[i + 1:j + 1, j])
+        stack.append((i, k))
+        stack.append((k + 1, j))
+    return lab
+
+
+def tree_sample(th, rng):
+    """constituency.py:136-140."""
+    _, ins = tree_inside(th)
+    if ins[0, -1] == NEG_INF:
+        raise Vacuous("no labeled tree has finite score")
+    return tree_walk(th, ins, lambda w: sample_log_categorical(rng, w))
+
+
+def eisner_decode(th, single_root, pick=None):
+    """spanning.py:283-320: shared top-down reconstruction (pick=None ->
+    max-plus charts + first argmax).  Returns heads [n+1] (heads[0] = -1)."""
+    is_max = pick is None
+    cr, cl, ir, il = eisner_charts(th, maxr if is_max else lse)
+    choose = (lambda w: int(np.argmax(w))) if is_max else pick
+    n = th.shape[0] - 1
+    heads = np.full(n + 1, -1, dtype=np.int64)
+    stack = []
+    if single_root:
+        terms = _root_terms(th, cl, cr)
+        if (np.max(terms) if is_max else lse_all(terms)) == NEG_INF:
+            raise Vacuous("no projective tree has finite score")
+        c = 1 + choose(terms)
+        heads[c] = 0
+        stack += [("cl", 1, c), ("cr", c, n)]
+    else:
+        if cr[0, n] == NEG_INF:
+            raise Vacuous("no projective tree has finite score")
+        stack.append(("cr", 0, n))
+    while stack:
+        kind, i, j = stack.pop()
+        if i == j:
+            continue
+        if kind == "cr":
+            k = i + 1 + choose(ir[i, i + 1:j + 1] + cr[i + 1:j + 1, j])
+            stack += [("ir", i, k), ("cr", k, j)]
+        elif kind == "cl":
+            k = i + choose(cl[i, i:j] + il[i:j, j])
+            stack += [("cl", i, k), ("il", k, j)]
+        else:
+            if kind == "ir":
+                heads[j] = i
+            else:
+                heads[i] = j
+            k = i + choose(cr[i, i:j] + cl[i + 1:j + 1, j])
+            stack += [("cr", i, k), ("cl", k + 1, j)]
+    return heads
+
+
+def eisner_sample(th, single_root, rng):
+    """spanning.py:328-331."""
+    return eisner_decode(th, single_root, lambda w: sample_log_categorical(rng, w))

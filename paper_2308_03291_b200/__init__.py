@@ -28,6 +28,8 @@ from .dist import (
     marginals_info,
     masked_dot,
     potential_marginals,
+    sample,
+    sample_info,
     structure_score,
 )
 from .errors import (

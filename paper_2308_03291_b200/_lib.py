@@ -49,6 +49,19 @@ SIGNATURES = {
     "sdb_pcfg_viterbi_workspace": (_sz, [_i64, _i32, _i32, _i32]),
     "sdb_pcfg_viterbi": (ctypes.c_int, [_c_p, _c_p, _c_p, _c_p, _i64, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p,
                                         _sz, _c_p]),
+    "sdb_chain_sample_workspace": (_sz, [_i64, _i32, _i32]),
+    "sdb_chain_sample": (ctypes.c_int, [_c_p, _c_p, _i64, _i32, _i32, _c_p, _i64, _i32, _c_p, _c_p, _c_p, _c_p, _sz,
+                                        _c_p]),
+    "sdb_nw_sample_workspace": (_sz, [_i64, _i32, _i32]),
+    "sdb_nw_sample": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _i64, _i32, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
+    "sdb_ctc_sample_workspace": (_sz, [_i64, _i32, _i32, _i32]),
+    "sdb_ctc_sample": (ctypes.c_int, [_c_p, _c_p, _i64, _i32, _i32, _i32, _c_p, _i64, _i32, _c_p, _c_p, _c_p, _c_p,
+                                      _sz, _c_p]),
+    "sdb_tree_sample_workspace": (_sz, [_i64, _i32, _i32]),
+    "sdb_tree_sample": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _i64, _i32, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
+    "sdb_eisner_decode_workspace": (_sz, [_i64, _i32]),
+    "sdb_eisner_decode": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _i64, _i32, _c_p, _c_p, _c_p, _c_p, _sz,
+                                         _c_p]),
     "sdb_semimarkov_fb": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p]),
     "sdb_semimarkov_viterbi_workspace": (_sz, [_i64, _i32, _i32, _i32]),
     "sdb_semimarkov_viterbi": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p, _sz,

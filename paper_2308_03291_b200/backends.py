@@ -107,6 +107,26 @@ class Backend:
     def log_prob(self, d, ind):
         return None
 
+    sample_algo = "forward-filtering-backward-sampling"
+
+    def sample(self, ds, seeds, num):
+        """dist.py:179-212 -> (per instance: list of num indicators, algo)."""
+        from .errors import UnsupportedInference
+
+        raise UnsupportedInference(f"sampling {type(ds[0]).__name__} is not on the GPU path")
+
+    @staticmethod
+    def _noise(seeds, count, num):
+        """The reference's Gumbel stream: np.random.default_rng(seed).gumbel
+        drawn element by element (numerics.py:167), num samples back to back."""
+        g = np.stack([np.random.default_rng(int(s)).gumbel(size=num * count) for s in seeds])
+        return torch.as_tensor(g, dtype=torch.float64).cuda()
+
+    def _sample_status(self, st, msg=None):
+        st = to_host(st)
+        for i in range(len(st)):
+            Result([0.0], st[i:i + 1], None, msg or self.vacuous_msg).raise_vacuous(0)
+
 
 # ---------------------------------------------------------------- chain
 
@@ -153,6 +173,26 @@ class ChainBackend(Backend):
 
         return ArgmaxResult(to_host(st), build, self.vacuous_msg)
 
+    def sample(self, ds, seeds, num):
+        init, trans = self._stack(ds)
+        d0 = ds[0]
+        noise = self._noise(seeds, K.stream_len("chain", dict(n=d0.n, m=d0.m)), num)
+        tags, _, st = K.chain_sample(init, trans, noise, num)
+        self._sample_status(st)
+        tags = to_host(tags)
+        out = []
+        for i, d in enumerate(ds):
+            inds = []
+            for r in range(num):
+                ind_i = np.zeros(d.m)
+                ind_i[tags[i, r, 0]] = 1.0
+                ind_t = np.zeros_like(d.transitions)
+                t = np.arange(d.n - 1)
+                ind_t[t, tags[i, r, :-1], tags[i, r, 1:]] = 1.0
+                inds.append({"init": ind_i, "transitions": ind_t})
+            out.append(inds)
+        return out, self.sample_algo
+
 
 # ------------------------------------------------------------- alignment
 
@@ -192,6 +232,25 @@ class AlignmentBackend(Backend):
             return {"move_potentials": mask}
 
         return ArgmaxResult(to_host(st), build, self.vacuous_msg)
+
+
+    def sample(self, ds, seeds, num):
+        th = to_dev([d.move_potentials for d in ds])
+        d0 = ds[0]
+        noise = self._noise(seeds, K.stream_len("alignment", dict(n=d0.n, m=d0.m)), num)
+        path, _, st = K.nw_sample(th, noise, num)
+        self._sample_status(st)
+        path = to_host(path)
+        out = []
+        for i, d in enumerate(ds):
+            inds = []
+            for r in range(num):
+                mask = np.zeros_like(d.move_potentials)
+                ii, jj = np.nonzero(path[i, r] >= 0)
+                mask[ii, jj, path[i, r][ii, jj]] = 1.0
+                inds.append({"move_potentials": mask})
+            out.append(inds)
+        return out, self.sample_algo
 
 
 # ------------------------------------------------------------------- CTC
@@ -237,6 +296,26 @@ class CTCBackend(Backend):
         return ArgmaxResult(to_host(st), build, self.vacuous_msg)
 
 
+    def sample(self, ds, seeds, num):
+        fp, tg = self._stack(ds)
+        d0 = ds[0]
+        noise = self._noise(seeds, K.stream_len("ctc", dict(T=d0.num_frames)), num)
+        states, _, st = K.ctc_sample(fp, tg, noise, num)
+        self._sample_status(st)
+        states = to_host(states)
+        out = []
+        for i, d in enumerate(ds):
+            lab = np.zeros(2 * len(d.target) + 1, dtype=np.int64)
+            lab[1::2] = np.asarray(d.target, dtype=np.int64)
+            inds = []
+            for r in range(num):
+                mask = np.zeros_like(d.frame_potentials)
+                mask[np.arange(mask.shape[0]), lab[states[i, r]]] = 1.0
+                inds.append({"frame_potentials": mask})
+            out.append(inds)
+        return out, self.sample_algo
+
+
 # -------------------------------------------------------------- Tree-CRF
 
 
@@ -275,6 +354,27 @@ class TreeBackend(Backend):
             return {"span_potentials": mask}
 
         return ArgmaxResult(to_host(st), build, self.vacuous_msg)
+
+
+    sample_algo = "cky-sampling"
+
+    def sample(self, ds, seeds, num):
+        th = to_dev([d.span_potentials for d in ds])
+        d0 = ds[0]
+        noise = self._noise(seeds, K.stream_len("tree", dict(n=d0.n, m=d0.m)), num)
+        labels, _, st = K.tree_sample(th, noise, num)
+        self._sample_status(st)
+        labels = to_host(labels)
+        out = []
+        for i, d in enumerate(ds):
+            inds = []
+            for r in range(num):
+                mask = np.zeros_like(d.span_potentials)
+                ii, jj = np.nonzero(labels[i, r] >= 0)
+                mask[ii, jj, labels[i, r][ii, jj]] = 1.0
+                inds.append({"span_potentials": mask})
+            out.append(inds)
+        return out, self.sample_algo
 
 
 # -------------------------------------------------------- spanning trees
@@ -341,8 +441,52 @@ class SpanningBackend(Backend):
 
         return ArgmaxResult(to_host(st), build, "no projective tree has finite score")
 
+    def sample(self, ds, seeds, num, algorithm=None):
+        """span_sample (spanning.py:709-728): projective -> Eisner decode with
+        Gumbel picks; the non-projective samplers (Wilson, Colbourn) are not
+        on the GPU path."""
+        d0 = ds[0]
+        if not d0.projective:
+            from .errors import UnsupportedInference
+
+            raise UnsupportedInference("non-projective sampling (Wilson / Colbourn) is not on the GPU path")
+        if algorithm not in (None, "eisner"):
+            raise InvalidProblem(f"sampler {algorithm!r} does not apply to projective trees")
+        adj = to_dev([d.adjacency for d in ds])
+        noise = self._noise(seeds, K.stream_len("eisner", dict(n=d0.n)), num)
+        heads, _, st = K.eisner_decode(adj, d0.single_root_edge, noise, num)
+        self._sample_status(st, "no projective tree has finite score")
+        heads = to_host(heads)
+        out = []
+        for i, d in enumerate(ds):
+            inds = []
+            for r in range(num):
+                mask = np.zeros((d.n + 1, d.n + 1))
+                mask[heads[i, r, 1:], np.arange(1, d.n + 1)] = 1.0
+                inds.append({"adjacency": mask})
+            out.append(inds)
+        return out, self._prefix(d0) + "eisner-sampling"
+
 
 # ------------------------------------------------------------------- PCFG
+
+
+def is_binary_bracketing(spans, n: int) -> bool:
+    """constituency.py:147-164: `spans` is exactly the node-span set of one
+    binary tree (host-side validation of an indicator)."""
+    if len(spans) != 2 * n - 1 or (0, n - 1) not in spans or any((i, i) not in spans for i in range(n)):
+        return False
+    memo = {}
+
+    def check(i, j):
+        if i == j:
+            return True
+        if (i, j) not in memo:
+            memo[(i, j)] = any((i, k) in spans and (k + 1, j) in spans and check(i, k) and check(k + 1, j)
+                               for k in range(i, j))
+        return memo[(i, j)]
+
+    return check(0, n - 1)
 
 
 class PCFGBackend(Backend):
@@ -378,6 +522,28 @@ class PCFGBackend(Backend):
             mg = to_host(marg).astype(np.float64)
             out = [{"sticky": mg[i]} for i in range(len(ds))]
         return Result(to_host(logz), to_host(st), out, self.vacuous_msg)
+
+    def log_prob(self, d, ind):
+        """dist.py:266-271: log-probability of a bracketing = masked inside -
+        inside, both in ONE batched kernel call (the mask rides on sticky)."""
+        mask = ind["sticky"]
+        if mask.shape != (d.n, d.n):
+            raise InvalidProblem("indicator span mask must have shape [n, n]")
+        spans = {(int(i), int(j)) for i, j in np.argwhere(mask > 0)}
+        if not is_binary_bracketing(spans, d.n):
+            raise InvalidProblem("marked spans do not form a binary bracketing")
+        span_mask = np.full((d.n, d.n), -np.inf)
+        for i, j in spans:
+            span_mask[i, j] = 0.0
+        root, rules, emis, sticky = self._inputs([d, d])
+        sticky[0] = sticky[0] + torch.as_tensor(span_mask, dtype=torch.float32, device=sticky.device)
+        logz, _, st = K.pcfg_fb(root, rules, emis, sticky, marginals=False)
+        lz, sth = to_host(logz), to_host(st)
+        if (sth == K.ST_INVALID).any():
+            raise InvalidProblem("potentials contain NaN or +inf entries")
+        if lz[0] == -np.inf:
+            return -np.inf, "pcfg-masked-inside"
+        return float(lz[0] - lz[1]), "pcfg-masked-inside"
 
     def argmax(self, ds):
         # pcfg_argmax (constituency.py:366-371): fp64 max-plus chart + first-max walk

@@ -183,6 +183,40 @@ def kl_divergence(p, q) -> float:
     return kl_divergence_info(p, q)[0]
 
 
+# ------------------------------------------------------------------ sampling
+
+
+def sample_info(dist, seed: int, num: int = 1, algorithm: str | None = None):
+    """dist.py:179-212: num exact samples from ONE seeded generator stream
+    (np.random.default_rng(seed)); the charts and the walks run on the GPU,
+    consuming the stream's Gumbel draws in the reference's pick order."""
+    _reject_one_to_one(dist)
+    if num < 1:
+        raise InvalidProblem("num must be >= 1")
+    from .families import SpanningTreeCRF
+
+    if algorithm is not None and not isinstance(dist, SpanningTreeCRF):
+        raise InvalidProblem("sampler overrides apply to spanning trees only")
+    be = _backend(dist)
+    if isinstance(dist, SpanningTreeCRF):
+        work = dist if dist.directed else _directed(dist)
+        out, algo = be.sample([work], [seed], num, algorithm)
+        algo = be._prefix(dist) + algo[len(be._prefix(work)):]
+    else:
+        out, algo = be.sample([dist], [seed], num)
+    return out[0], algo
+
+
+def sample(dist, seed: int, algorithm: str | None = None):
+    return sample_info(dist, seed, 1, algorithm)[0][0]
+
+
+def _directed(d):
+    from .families import undirected_to_directed
+
+    return undirected_to_directed(d)
+
+
 def log_prob_info(dist, indicator):
     """dist.py:263-276 for the score-based families."""
     _reject_one_to_one(dist)

@@ -353,3 +353,112 @@ def semimarkov_viterbi(segment_potentials):
                                     ws.numel(), stream_ptr(dev))
     _lib.check(rc, "sdb_semimarkov_viterbi")
     return seg, cnt, score, status
+
+
+# -------------------------------------------------------------- sampling
+
+
+def f64(t: torch.Tensor, name: str = "tensor") -> torch.Tensor:
+    _require_cuda(t, name)
+    return t.to(torch.float64).contiguous()
+
+
+def stream_len(family: str, shape: dict) -> int:
+    """Gumbel draws one sample can consume (the C-ABI's per-family bound)."""
+    if family == "chain":
+        return shape["n"] * shape["m"]
+    if family == "alignment":
+        return 3 * (shape["n"] + shape["m"])
+    if family == "ctc":
+        return 2 + 3 * (shape["T"] - 1)
+    if family == "tree":
+        return (2 * shape["n"] - 1) * shape["m"] + shape["n"] ** 2
+    if family == "eisner":
+        return shape["n"] + 4 * (shape["n"] + 1) ** 2
+    raise ValueError(family)
+
+
+def chain_sample(init, trans, noise, num: int):
+    """chain.py:117-129 batched: noise [B, >= num*n*m] fp64 Gumbel stream ->
+    (tags [B,num,n] int32, used [B], status)."""
+    lib = _lib.load()
+    init, trans, noise = f32(init, "init"), f32(trans, "transitions"), f64(noise, "noise")
+    B, m = init.shape
+    n = trans.shape[1] + 1
+    dev = init.device
+    tags = torch.empty(B, num, n, dtype=torch.int32, device=dev)
+    used = torch.empty(B, dtype=torch.int32, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    ws = workspace(lib.sdb_chain_sample_workspace(B, n, m), dev)
+    rc = lib.sdb_chain_sample(ptr(init), ptr(trans), B, n, m, ptr(noise), noise.shape[1], num, ptr(tags), ptr(used),
+                              ptr(status), ptr(ws), ws.numel(), stream_ptr(dev))
+    _lib.check(rc, "sdb_chain_sample")
+    return tags, used, status
+
+
+def nw_sample(theta, noise, num: int):
+    """alignment.py:121-150 batched -> (path [B,num,n+1,m+1] int8, used, status)."""
+    lib = _lib.load()
+    theta, noise = f32(theta, "move_potentials"), f64(noise, "noise")
+    B, n1, m1, _ = theta.shape
+    dev = theta.device
+    path = torch.empty(B, num, n1, m1, dtype=torch.int8, device=dev)
+    used = torch.empty(B, dtype=torch.int32, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    ws = workspace(lib.sdb_nw_sample_workspace(B, n1 - 1, m1 - 1), dev)
+    rc = lib.sdb_nw_sample(ptr(theta), B, n1 - 1, m1 - 1, ptr(noise), noise.shape[1], num, ptr(path), ptr(used),
+                           ptr(status), ptr(ws), ws.numel(), stream_ptr(dev))
+    _lib.check(rc, "sdb_nw_sample")
+    return path, used, status
+
+
+def ctc_sample(frame_potentials, targets, noise, num: int):
+    """alignment.py:304-343 batched -> (lattice state per frame [B,num,T], used, status)."""
+    lib = _lib.load()
+    fp, tg, noise = f32(frame_potentials, "frame_potentials"), i32(targets, "targets"), f64(noise, "noise")
+    B, T, V = fp.shape
+    L = tg.shape[1]
+    dev = fp.device
+    states = torch.empty(B, num, T, dtype=torch.int32, device=dev)
+    used = torch.empty(B, dtype=torch.int32, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    ws = workspace(lib.sdb_ctc_sample_workspace(B, T, V, L), dev)
+    rc = lib.sdb_ctc_sample(ptr(fp), ptr(tg), B, T, V, L, ptr(noise), noise.shape[1], num, ptr(states), ptr(used),
+                            ptr(status), ptr(ws), ws.numel(), stream_ptr(dev))
+    _lib.check(rc, "sdb_ctc_sample")
+    return states, used, status
+
+
+def tree_sample(span_potentials, noise, num: int):
+    """constituency.py:113-140 batched -> (labels [B,num,n,n] (-1 = none), used, status)."""
+    lib = _lib.load()
+    th, noise = f32(span_potentials, "span_potentials"), f64(noise, "noise")
+    B, n, _, m = th.shape
+    dev = th.device
+    labels = torch.empty(B, num, n, n, dtype=torch.int32, device=dev)
+    used = torch.empty(B, dtype=torch.int32, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    ws = workspace(lib.sdb_tree_sample_workspace(B, n, m), dev)
+    rc = lib.sdb_tree_sample(ptr(th), B, n, m, ptr(noise), noise.shape[1], num, ptr(labels), ptr(used), ptr(status),
+                             ptr(ws), ws.numel(), stream_ptr(dev))
+    _lib.check(rc, "sdb_tree_sample")
+    return labels, used, status
+
+
+def eisner_decode(adjacency, single_root: bool = False, noise=None, num: int = 1):
+    """spanning.py:283-331 batched: noise None -> eisner_max_arcs (max-plus
+    decode), else eisner_sample_arcs -> (heads [B,num,n+1], used, status)."""
+    lib = _lib.load()
+    adj = f32(adjacency, "adjacency")
+    B, N, _ = adj.shape
+    dev = adj.device
+    noise = f64(noise, "noise") if noise is not None else None
+    heads = torch.empty(B, num, N, dtype=torch.int32, device=dev)
+    used = torch.empty(B, dtype=torch.int32, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    ws = workspace(lib.sdb_eisner_decode_workspace(B, N - 1), dev)
+    rc = lib.sdb_eisner_decode(ptr(adj), B, N - 1, int(single_root), ptr(noise),
+                               noise.shape[1] if noise is not None else 0, num, ptr(heads), ptr(used), ptr(status),
+                               ptr(ws), ws.numel(), stream_ptr(dev))
+    _lib.check(rc, "sdb_eisner_decode")
+    return heads, used, status

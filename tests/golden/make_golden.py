@@ -185,10 +185,50 @@ def spanning_cases(st):
                                         single=single, scale=1), {}, big=True, argmax=projective)
 
 
+def sample_cases(st):
+    """Reference samples (dist.py:179-212, one seeded stream, num=2) for the
+    families the GPU samples: chain FFBS, alignment, CTC, Tree-CRF and
+    projective spanning trees (Eisner decode with Gumbel picks), plus the
+    Eisner max-plus decode (spanning.py:323-325)."""
+    from structdist.spanning import eisner_max_arcs  # noqa: E402
+
+    def add(fam, d, meta, inputs):
+        inds, algo = sd.sample_info(d, meta["seed"], num=2)
+        out = {f"in_{k}": v for k, v in inputs.items()}
+        for r, ind in enumerate(inds):
+            for k, v in ind.items():
+                out[f"sample{r}_{k}"] = v
+        st.add(fam, dict(meta, algo=algo), **out)
+
+    for seed, (n, m) in enumerate([(1, 3), (2, 2), (5, 3), (12, 4), (30, 6)]):
+        init, tr = bld.chain(seed, n, m)
+        add("chain", sd.LinearChainCRF(init, tr), dict(seed=seed, n=n, m=m), dict(init=init, transitions=tr))
+    for seed, (n, m) in enumerate([(1, 1), (3, 2), (6, 9), (20, 13)]):
+        mv = bld.alignment(seed, n, m)
+        add("alignment", sd.MonotoneAlignmentCRF(mv), dict(seed=seed, n=n, m=m), dict(move_potentials=mv))
+    for seed, (T, V, L) in enumerate([(1, 2, 1), (5, 3, 2), (12, 6, 4), (30, 8, 9)]):
+        fp, tg = bld.ctc(seed, T, V, L)
+        add("ctc", sd.CTCDist(fp, tg), dict(seed=seed, T=T, V=V, L=L), dict(frame_potentials=fp, target=np.array(tg)))
+    for seed, (n, m) in enumerate([(1, 2), (4, 3), (9, 2), (16, 5)]):
+        th = bld.tree(seed, n, m)
+        add("tree", sd.TreeCRF(th), dict(seed=seed, n=n, m=m), dict(span_potentials=th))
+    for single in (False, True):
+        for seed, n in enumerate([1, 3, 6, 11]):
+            adj = bld.spanning(300 + seed, n, True)
+            d = sd.SpanningTreeCRF(adj, directed=True, projective=True, single_root_edge=single)
+            add("spanning", d, dict(seed=seed, n=n, single=single), dict(adjacency=adj))
+            arcs = eisner_max_arcs(d)
+            mx = np.zeros_like(adj)
+            for h, dd in arcs:
+                mx[h, dd] = 1.0
+            st.arrays[f"c{len(st.meta) - 1:03d}__eisner_max"] = mx
+
+
 def main():
     fams = {
         "chain": chain_cases, "semi_markov": semi_markov_cases, "alignment": alignment_cases,
         "ctc": ctc_cases, "tree": tree_cases, "pcfg": pcfg_cases, "spanning": spanning_cases,
+        "sample": sample_cases,
     }
     only = sys.argv[1:] or list(fams)
     for fam in only:

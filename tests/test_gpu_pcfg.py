@@ -131,3 +131,26 @@ def test_pcfg_gradient_invariants_config():
     assert torch.allclose(gd["binary_rules"].sum((1, 2, 3)), 63 * one, rtol=1e-4)
     assert torch.allclose(gd["emissions"].sum(2), torch.ones(128, 64, dtype=torch.float64, device="cuda"), rtol=1e-4)
     assert torch.allclose(gd["sticky"].sum((1, 2)), 127 * one, rtol=1e-4)
+
+
+def test_pcfg_log_prob_masked_inside():
+    """dist.py:266-271: log-prob of a bracketing via the masked inside; the
+    argmax bracketing has the highest probability among a few random ones."""
+    need_gpu()
+    root, rules, emis = batch_pcfg(4300, 1, 10, 6, 5)
+    d = sd.PCFG(root[0], rules[0], emis[0])
+    ind = sd.argmax(d)
+    lp, algo = sd.log_prob_info(d, ind)
+    assert algo == "pcfg-masked-inside"
+    n = 10
+    mask = np.full((n, n), NEG_INF)
+    for i, j in np.argwhere(ind["sticky"] > 0):
+        mask[i, j] = 0.0
+    zm = O.pcfg_log_partition(root[0], rules[0], emis[0], sticky=mask)
+    z = O.pcfg_log_partition(root[0], rules[0], emis[0])
+    assert abs(lp - (zm - z)) <= 1e-4 * max(1.0, abs(zm - z))
+    bad = dict(ind)
+    bad["sticky"] = ind["sticky"].copy()
+    bad["sticky"][0, 0] = 0.0
+    with pytest.raises(sd.InvalidProblem):
+        sd.log_prob(d, bad)

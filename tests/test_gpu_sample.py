@@ -1,0 +1,137 @@
+"""GPU sampling parity (dist.py:179-212): same seed -> the same structures
+as the reference (golden_sample.npz, num=2 from one stream) and as the
+oracle's per-pick Gumbel draws at larger sizes; Eisner max-plus decode
+(spanning.py:323-325) bit-exact."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2308_03291_b200 as sd
+from paper_2308_03291_b200 import kernels as K
+from golden_io import inputs, load
+from gpu_util import dev, need_gpu
+from golden.builders import batch_alignment, batch_chain, batch_ctc, batch_spanning, batch_tree
+from oracle import sd_oracle as O
+
+pytestmark = pytest.mark.gpu
+CASES = load("sample")
+
+
+def _dist(case):
+    x = inputs(case)
+    fam = case.meta["family"]
+    if fam == "chain":
+        return sd.LinearChainCRF(x["init"], x["transitions"])
+    if fam == "alignment":
+        return sd.MonotoneAlignmentCRF(x["move_potentials"])
+    if fam == "ctc":
+        return sd.CTCDist(x["frame_potentials"], tuple(int(v) for v in np.atleast_1d(x["target"])))
+    if fam == "tree":
+        return sd.TreeCRF(x["span_potentials"])
+    return sd.SpanningTreeCRF(x["adjacency"], directed=True, projective=True, single_root_edge=bool(case.meta["single"]))
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: str(c.meta))
+def test_sample_golden(case):
+    need_gpu()
+    d = _dist(case)
+    inds, algo = sd.sample_info(d, int(case.meta["seed"]), num=2)
+    assert algo == case.meta["algo"]
+    for r, ind in enumerate(inds):
+        for k, v in ind.items():
+            np.testing.assert_array_equal(v, case[f"sample{r}_{k}"], err_msg=f"sample {r} {k}")
+    if case.meta["family"] == "spanning":  # eisner_max_arcs
+        heads, _, st = K.eisner_decode(dev(case["in_adjacency"][None]), bool(case.meta["single"]))
+        h = heads[0, 0].cpu().numpy()
+        mask = np.zeros_like(case["in_adjacency"])
+        mask[h[1:], np.arange(1, len(h))] = 1
+        np.testing.assert_array_equal(mask, case["eisner_max"])
+
+
+def _seeds(B):
+    return [31 + 7 * b for b in range(B)]
+
+
+def test_chain_sample_vs_oracle():
+    need_gpu()
+    B, n, m, num = 4, 64, 16, 3
+    init, tr = batch_chain(70, B, n, m)
+    noise = torch.stack([torch.as_tensor(np.random.default_rng(s).gumbel(size=num * n * m)) for s in _seeds(B)]).cuda()
+    tags, used, st = K.chain_sample(dev(init), dev(tr), noise, num)
+    assert (st == 0).all() and (used == num * n * m).all()
+    for b, s in enumerate(_seeds(B)):
+        rng = np.random.default_rng(s)
+        for r in range(num):
+            np.testing.assert_array_equal(tags[b, r].cpu().numpy(), O.chain_sample(init[b], tr[b], rng))
+
+
+def test_alignment_sample_vs_oracle():
+    need_gpu()
+    B, n, m, num = 3, 60, 40, 2
+    th = batch_alignment(71, B, n, m)
+    cnt = K.stream_len("alignment", dict(n=n, m=m))
+    noise = torch.stack([torch.as_tensor(np.random.default_rng(s).gumbel(size=num * cnt)) for s in _seeds(B)]).cuda()
+    path, used, st = K.nw_sample(dev(th), noise, num)
+    assert (st == 0).all()
+    for b, s in enumerate(_seeds(B)):
+        rng = np.random.default_rng(s)
+        for r in range(num):
+            np.testing.assert_array_equal(path[b, r].cpu().numpy(), O.nw_sample(th[b], rng))
+
+
+def test_ctc_sample_vs_oracle():
+    need_gpu()
+    B, T, V, L, num = 3, 80, 12, 20, 2
+    fp, tg = batch_ctc(72, B, T, V, L)
+    cnt = K.stream_len("ctc", dict(T=T))
+    noise = torch.stack([torch.as_tensor(np.random.default_rng(s).gumbel(size=num * cnt)) for s in _seeds(B)]).cuda()
+    states, used, st = K.ctc_sample(dev(fp), torch.as_tensor(tg, dtype=torch.int32).cuda(), noise, num)
+    assert (st == 0).all()
+    for b, s in enumerate(_seeds(B)):
+        rng = np.random.default_rng(s)
+        for r in range(num):
+            np.testing.assert_array_equal(states[b, r].cpu().numpy(), O.ctc_sample(fp[b], tg[b], rng))
+
+
+def test_tree_sample_vs_oracle():
+    need_gpu()
+    B, n, m, num = 3, 24, 6, 2
+    th = batch_tree(73, B, n, m)
+    cnt = K.stream_len("tree", dict(n=n, m=m))
+    noise = torch.stack([torch.as_tensor(np.random.default_rng(s).gumbel(size=num * cnt)) for s in _seeds(B)]).cuda()
+    labels, used, st = K.tree_sample(dev(th), noise, num)
+    assert (st == 0).all()
+    for b, s in enumerate(_seeds(B)):
+        rng = np.random.default_rng(s)
+        for r in range(num):
+            np.testing.assert_array_equal(labels[b, r].cpu().numpy(), O.tree_sample(th[b], rng))
+
+
+@pytest.mark.parametrize("single", [False, True])
+def test_eisner_sample_and_max_decode_vs_oracle(single):
+    need_gpu()
+    B, n, num = 3, 40, 2
+    adj = batch_spanning(74, B, n)
+    cnt = K.stream_len("eisner", dict(n=n))
+    noise = torch.stack([torch.as_tensor(np.random.default_rng(s).gumbel(size=num * cnt)) for s in _seeds(B)]).cuda()
+    heads, used, st = K.eisner_decode(dev(adj), single, noise, num)
+    assert (st == 0).all()
+    hmax, _, _ = K.eisner_decode(dev(adj), single)
+    for b, s in enumerate(_seeds(B)):
+        rng = np.random.default_rng(s)
+        for r in range(num):
+            np.testing.assert_array_equal(heads[b, r].cpu().numpy(), O.eisner_sample(adj[b], single, rng))
+        np.testing.assert_array_equal(hmax[b, 0].cpu().numpy(), O.eisner_decode(adj[b], single))
+
+
+def test_sample_vacuous_and_unsupported():
+    need_gpu()
+    tr = np.full((2, 2, 2), -np.inf)
+    with pytest.raises(sd.VacuousDistribution):
+        sd.sample(sd.LinearChainCRF(np.zeros(2), tr), 0)
+    with pytest.raises(sd.InvalidProblem):
+        sd.sample_info(sd.LinearChainCRF(np.zeros(2), np.zeros((1, 2, 2))), 0, num=0)
+    adj = batch_spanning(75, 1, 5)[0]
+    with pytest.raises(sd.UnsupportedInference):
+        sd.sample(sd.SpanningTreeCRF(adj, projective=False), 0)
