@@ -606,6 +606,11 @@ __device__ __forceinline__ void bar_dir(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+template <int V>
+struct IntC {
+  static constexpr int value = V;
+};
+
 struct FState {
   VO cur, lprev;
   float av, O;
@@ -660,7 +665,10 @@ __device__ __forceinline__ void mitm_fwd(const float* __restrict__ th, int n, in
     float2* wsa_b = wsa_l + (ptrdiff_t)s0 * 32;
     const float2* wsb_b = wsb_l + (ptrdiff_t)(s0 + kMP) * 32;
     auto step = [&](auto steady_c, int k) {
-      constexpr bool kS = decltype(steady_c)::value;
+      // mode 1 = steady (every lane active, interior of the grid), 2 = interior
+      // (grid-edge cases impossible, lanes straddle the phase boundary), 0 = generic
+      constexpr int kMode = decltype(steady_c)::value;
+      constexpr bool kS = kMode == 1, kIn = kMode >= 1;
       const int s = s0 + k;
       if (kPh == 2) {  // write back the row this half-warp completed at step s-1 (before its slot is refilled)
         const int r = s - 16 - 16 * g;
@@ -674,7 +682,7 @@ __device__ __forceinline__ void mitm_fwd(const float* __restrict__ th, int n, in
       }
       {
         const int prow = s + kMP - 16 * g;
-        const bool pv = kS ? true : ((prow >= 0) & (prow <= n));
+        const bool pv = kIn ? true : ((prow >= 0) & (prow <= n));
         const float* src = tsrc;
         tsrc += rs;
         const uint32_t dst = ring_u + (uint32_t)wrapr(pb + k) * 192u;
@@ -683,18 +691,18 @@ __device__ __forceinline__ void mitm_fwd(const float* __restrict__ th, int n, in
         cp4p(dst + 128, src + 2, pv);
         if (kPh == 2) {
           const int sp = s + kMP;
-          const bool bv = kS ? true : ((sp >= 0) & (sp < steps));
+          const bool bv = kIn ? true : ((sp >= 0) & (sp < steps));
           cp8p(slab_u + (uint32_t)((k + kMP) & (kMS - 1)) * 256u, wsb_b + 32 * k, bv);
         }
         cp_commit();
       }
-      if (kS || ((s >= 0) & (s < steps))) {
+      if (kIn || ((s >= 0) & (s < steps))) {
         cp_wait<kMP>();
         const int i = s - l;
         VO left;
         left.v = __shfl_up_sync(0xffffffffu, cur.v, 1);
         left.o = __shfl_up_sync(0xffffffffu, cur.o, 1);
-        const bool inrow = kS ? true : ((i >= 0) & (i <= n));
+        const bool inrow = kIn ? true : ((i >= 0) & (i <= n));
         {
           const float2 a = bnd_in[b0 + k];
           const bool ok = (w > 0) & inrow;
@@ -710,7 +718,7 @@ __device__ __forceinline__ void mitm_fwd(const float* __restrict__ th, int n, in
         const float t1 = fmaf(x1, SDB_LOG2E, av);
         const float t2 = fmaf(x2, SDB_LOG2E, rel(left, O));
         const L3 r = lse3r(t0, t1, t2);
-        const bool origin = kS ? false : ((i == 0) & (j == 0));
+        const bool origin = kIn ? false : ((i == 0) & (j == 0));
         if (kPh == 2) {
           const float2 bt = slab_w[((k)&(kMS - 1)) * 32 + l];
           const float e = ex2((r.Mc + bt.x) + ((O + bt.y - zint) - zfrac));
@@ -738,10 +746,13 @@ __device__ __forceinline__ void mitm_fwd(const float* __restrict__ th, int n, in
     };
     if ((s0 >= s_lo) & (s0 <= s_hi)) {
 #pragma unroll
-      for (int k = 0; k < kBlk; ++k) step(BoolC<true>{}, k);
+      for (int k = 0; k < kBlk; ++k) step(IntC<1>{}, k);
+    } else if ((s0 >= 32) & (s0 + kBlk - 1 + kMP <= n - 1)) {
+#pragma unroll 1
+      for (int k = 0; k < kBlk; ++k) step(IntC<2>{}, k);
     } else {
 #pragma unroll 1
-      for (int k = 0; k < kBlk; ++k) step(BoolC<false>{}, k);
+      for (int k = 0; k < kBlk; ++k) step(IntC<0>{}, k);
     }
     bar_dir(1, 32 * NW);
   }
@@ -808,7 +819,10 @@ __device__ __forceinline__ void mitm_bwd(const float* __restrict__ th, int n, in
     const float2* sa_b = wsa_u + (ptrdiff_t)(n + 29 - kMP - s0) * 32 + l;
     const float2* sl_b = u > 0 ? wsa_left + (ptrdiff_t)(n + 29 - kMP + 32 - s0) * 32 : wsa_u;
     auto step = [&](auto steady_c, int k) {
-      constexpr bool kS = decltype(steady_c)::value;
+      // mode 1 = steady (every lane active, interior of the grid), 2 = interior
+      // (grid-edge cases impossible, lanes straddle the phase boundary), 0 = generic
+      constexpr int kMode = decltype(steady_c)::value;
+      constexpr bool kS = kMode == 1, kIn = kMode >= 1;
       const int s = s0 + k;
       if (kPh == 2) {
         const int r = s - 16 - 16 * g;  // flipped row completed at step s-1
@@ -822,7 +836,7 @@ __device__ __forceinline__ void mitm_bwd(const float* __restrict__ th, int n, in
       }
       {
         const int prow = s + kMP - 16 * g;
-        const bool pv = kS ? true : ((prow >= 0) & (prow <= n));
+        const bool pv = kIn ? true : ((prow >= 0) & (prow <= n));
         const float* src = tsrc;
         tsrc -= rs;
         const uint32_t dst = ring_u + (uint32_t)wrapr(pb + k) * 192u;
@@ -832,7 +846,7 @@ __device__ __forceinline__ void mitm_bwd(const float* __restrict__ th, int n, in
         if (kPh == 2) {
           // alpha slab sF(s+kMP)-2 (own strip) and left-strip lane-31 alpha for sF(s+kMP)-1
           const int sa = n + 29 - s - kMP;
-          const bool av_ = kS ? true : ((sa >= 0) & (sa < steps));
+          const bool av_ = kIn ? true : ((sa >= 0) & (sa < steps));
           cp8p(slab_u + (uint32_t)(sa & (kMS - 1)) * 256u, sa_b - 32 * k, av_);
           const int sl = sa + 1 + 31;
           const bool lv = (u > 0) & (l == 0) & (sl >= 0) & (sl < steps);
@@ -840,7 +854,7 @@ __device__ __forceinline__ void mitm_bwd(const float* __restrict__ th, int n, in
         }
         cp_commit();
       }
-      if (kS || ((s >= 0) & (s < steps))) {
+      if (kIn || ((s >= 0) & (s < steps))) {
         cp_wait<kMP>();
         const int ip = s - l;
         VO rR, rD;
@@ -848,7 +862,7 @@ __device__ __forceinline__ void mitm_bwd(const float* __restrict__ th, int n, in
         rR.o = __shfl_up_sync(0xffffffffu, pR.o, 1);
         rD.v = __shfl_up_sync(0xffffffffu, pD.v, 1);
         rD.o = __shfl_up_sync(0xffffffffu, pD.o, 1);
-        const bool inrow = kS ? true : ((ip >= 0) & (ip <= n));
+        const bool inrow = kIn ? true : ((ip >= 0) & (ip <= n));
         {
           const float2 a = bnd0_in[b0 + k], d = bnd1_in[b0 + k];
           const bool ok = (wb > 0) & inrow;
@@ -863,7 +877,7 @@ __device__ __forceinline__ void mitm_bwd(const float* __restrict__ th, int n, in
         const float x0 = slot[0], x1 = slot[16], x2 = slot[32];
         const L3 r = lse3r(rel(savedD, O), rel(pDn, O), rel(rR, O));
         float b, On;
-        if (kS) {
+        if (kIn) {
           b = r.v;
           On = O + r.r;
         } else {
@@ -891,7 +905,7 @@ __device__ __forceinline__ void mitm_bwd(const float* __restrict__ th, int n, in
           const float2 A0 = Y, A1 = c1, A2 = c2;
           c1 = X;
           c2 = Y;
-          const bool hi_ok = i >= 1, left_ok = jo >= 1, ok = zok & act;
+          const bool hi_ok = kIn ? true : (i >= 1), left_ok = jo >= 1, ok = kS ? zok : (zok & act);
           const float base = b - zfrac;
           const float e0 = ex2(((A0.y + On - zint) + (A0.x + fmaf(x0, SDB_LOG2E, base))));
           const float e1 = ex2(((A1.y + On - zint) + (A1.x + fmaf(x1, SDB_LOG2E, base))));
@@ -927,10 +941,13 @@ __device__ __forceinline__ void mitm_bwd(const float* __restrict__ th, int n, in
     };
     if ((s0 >= s_lo) & (s0 <= s_hi)) {
 #pragma unroll
-      for (int k = 0; k < kBlk; ++k) step(BoolC<true>{}, k);
+      for (int k = 0; k < kBlk; ++k) step(IntC<1>{}, k);
+    } else if ((s0 >= 32) & (s0 + kBlk - 1 + kMP <= n - 1)) {
+#pragma unroll 1
+      for (int k = 0; k < kBlk; ++k) step(IntC<2>{}, k);
     } else {
 #pragma unroll 1
-      for (int k = 0; k < kBlk; ++k) step(BoolC<false>{}, k);
+      for (int k = 0; k < kBlk; ++k) step(IntC<0>{}, k);
     }
     bar_dir(2, 32 * NW);
   }
