@@ -49,9 +49,9 @@ FALLBACK_HBM = 6650.0
 # bound: "hbm" -> bytes / HBM GB/s; "fp32" -> FLOP / FP32 FMA peak; "mufu" -> MUFU ops / MUFU peak.
 CONFIGS = {
     "c1": dict(workload="LinearChainCRF", B=32, shape=dict(n=128, m=32), work=1_040_644, bound="hbm",
-               argmax=True, kernel="chain_fwd_bwd_kernel"),
+               argmax=True, kernel="chain_lin_kernel"),
     "c2a": dict(workload="MonotoneAlignmentCRF", B=256, shape=dict(n=512, m=128), work=1_588_252, bound="hbm",
-                argmax=False, kernel="nw_kernel<1>"),
+                argmax=False, kernel="nw_mitm_kernel"),
     "c2b": dict(workload="CTCDist", B=256, shape=dict(T=512, V=128, L=128), work=921_088, bound="mufu",
                 argmax=False, kernel="ctc_kernel<1>"),
     "c3": dict(workload="SpanningTreeCRF non-projective (Matrix-Tree, multi-root)", B=512, shape=dict(n=128),
@@ -61,7 +61,7 @@ CONFIGS = {
     "c5a": dict(workload="TreeCRF (CKY)", B=128, shape=dict(n=64, m=32), work=790_532, bound="hbm",
                 argmax=False, kernel="tree_kernel<1>"),
     "c5b": dict(workload="PCFG (CKY, NT=32, PT=32)", B=128, shape=dict(n=64, NT=32, PT=32),
-                work=2_130_444_288, bound="fp32", argmax=False, kernel="pcfg_kernel<true>",
+                work=2_130_444_288, bound="fp32", argmax=False, kernel="pcfg_kernel<1>",
                 cpu_skip="one float64 instance takes minutes on the host (SURVEY §6: 163 s public marginals per "
                          "instance in the reference); not sampled inside the bench budget"),
 }
