@@ -244,26 +244,52 @@ def log_prob(dist, indicator) -> float:
 _BATCHED = {}
 
 
-def batch_map(op, dists, *args, **kwargs) -> list:
+def batch_map(op, dists, *args, ragged: bool = True, **kwargs) -> list:
     """dist.py:355-361, batched: log_partition / marginals / argmax (and
-    their *_info forms) over same-shape instances run as ONE kernel call per
-    shape group; any other op falls back to a per-instance map of the same
-    GPU-backed op."""
+    their *_info forms) run as ONE kernel call per group.  Same-shape
+    instances group directly; with `ragged`, chains, alignments, CTC
+    (same target length) and multi-root spanning trees of DIFFERENT lengths
+    share a launch through inference-neutral padding (ragged.py; the
+    reference's pad_chain, chain.py:161-176) and their results are sliced
+    back.  Any other op maps the same GPU-backed op per instance."""
     dists = list(dists)
     name = getattr(op, "__name__", None)
     if name not in _BATCHED or args or kwargs:
         return [op(d, *args, **kwargs) for d in dists]
+    from . import ragged as rg
+
     groups: "OrderedDict[tuple, list[int]]" = OrderedDict()
     for i, d in enumerate(dists):
         be = _backend(d)
-        groups.setdefault((type(d), be.batch_key(d)), []).append(i)
+        key = ("ragged",) + rg.group_key(d) if ragged and rg.raggable(d) else (type(d), be.batch_key(d))
+        groups.setdefault(key, []).append(i)
     out = [None] * len(dists)
-    for (_, _), idx in groups.items():
+    for key, idx in groups.items():
         group = [dists[i] for i in idx]
         be = _backend(group[0])
-        for i, r in zip(idx, _BATCHED[name](be, group)):
+        if key[0] == "ragged":
+            padded = rg.pad_group(group)
+            res = _BATCHED[name](be, padded)
+            res = [_unpad_result(name, d, r) for d, r in zip(group, res)]
+        else:
+            res = _BATCHED[name](be, group)
+        for i, r in zip(idx, res):
             out[i] = r
     return out
+
+
+def _unpad_result(name, d, r):
+    from . import ragged as rg
+
+    if name.startswith("log_partition"):
+        return r
+    if name in ("marginals", "argmax"):
+        return rg.unpad(d, r)
+    if name == "marginals_info":
+        return rg.unpad(d, r[0]), r[1]
+    # argmax_info: the score of the unpadded indicator (padding adds 0)
+    ind = rg.unpad(d, r[0])
+    return ind, structure_score(d, ind), r[2]
 
 
 def _b_logz(be, group):

@@ -1,0 +1,117 @@
+"""Inference-neutral padding so that instances of different lengths share
+ONE kernel launch (the reference's own notion is
+`pad_chain`, chain.py:161-176: padded steps carry the log-space identity, so
+every structure extends uniquely and log Z / the marginals of the original
+parts are unchanged).
+
+Per family, `key` groups instances that can share a launch, `size` is the
+ragged extent, `pad(d, size)` builds the padded instance and `unpad(d, x)`
+slices a marginal / indicator dict back to `d`'s shape:
+
+* LinearChainCRF: identity transitions appended (chain.py:161-176);
+* MonotoneAlignmentCRF: a forced corridor (n,m) -> (N,m) -> (N,M) of zero
+  DOWN / RIGHT moves, every other padded move -inf;
+* CTCDist: blank-only frames PREPENDED (blank potential 0, other labels
+  -inf): every original lattice path is extended by exactly one all-blank
+  prefix, and the first original frame sees the same alpha;
+* SpanningTreeCRF, multi-root only: extra nodes whose ONLY arc is root -> node
+  (weight exp(0) = 1; no outgoing arcs), projective-compatible since they sit
+  after position n.
+
+Host-side glue only: the padded batch runs through the same kernels.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .families import CTCDist, LinearChainCRF, MonotoneAlignmentCRF, SpanningTreeCRF
+
+NEG_INF = float("-inf")
+
+
+def _chain_pad(d, n):
+    extra = n - d.n
+    if extra == 0:
+        return d
+    pad = np.full((extra, d.m, d.m), NEG_INF)
+    idx = np.arange(d.m)
+    pad[:, idx, idx] = 0.0
+    return LinearChainCRF(d.init, np.concatenate([d.transitions, pad], axis=0))
+
+
+def _chain_unpad(d, x):
+    return {"init": x["init"], "transitions": x["transitions"][: d.n - 1]}
+
+
+def _nw_pad(d, size):
+    N, M = size
+    if (N, M) == (d.n, d.m):
+        return d
+    th = np.full((N + 1, M + 1, 3), NEG_INF)
+    th[: d.n + 1, : d.m + 1] = d.move_potentials
+    th[d.n + 1:, d.m, 1] = 0.0        # DOWN along column m
+    th[N, d.m + 1:, 2] = 0.0          # RIGHT along row N
+    return MonotoneAlignmentCRF(th)
+
+
+def _nw_unpad(d, x):
+    return {"move_potentials": x["move_potentials"][: d.n + 1, : d.m + 1]}
+
+
+def _ctc_pad(d, T):
+    extra = T - d.num_frames
+    if extra == 0:
+        return d
+    pad = np.full((extra, d.vocab_size), NEG_INF)
+    pad[:, 0] = 0.0  # BLANK = 0 (alignment.py:195)
+    return CTCDist(np.concatenate([pad, d.frame_potentials], axis=0), d.target)
+
+
+def _ctc_unpad(d, x):
+    return {"frame_potentials": x["frame_potentials"][-d.num_frames:]}
+
+
+def _span_pad(d, n):
+    extra = n - d.n
+    if extra == 0:
+        return d
+    adj = np.full((n + 1, n + 1), NEG_INF)
+    adj[: d.n + 1, : d.n + 1] = d.adjacency
+    adj[0, d.n + 1:] = 0.0
+    return SpanningTreeCRF(adj, directed=d.directed, projective=d.projective, single_root_edge=False)
+
+
+def _span_unpad(d, x):
+    return {"adjacency": x["adjacency"][: d.n + 1, : d.n + 1]}
+
+
+# family -> (key, size, combine sizes, pad, unpad)
+RAGGED = {
+    LinearChainCRF: (lambda d: (d.m,), lambda d: d.n, max, _chain_pad, _chain_unpad),
+    MonotoneAlignmentCRF: (lambda d: (), lambda d: (d.n, d.m),
+                           lambda ss: (max(s[0] for s in ss), max(s[1] for s in ss)), _nw_pad, _nw_unpad),
+    CTCDist: (lambda d: (d.vocab_size, len(d.target)), lambda d: d.num_frames, max, _ctc_pad, _ctc_unpad),
+    SpanningTreeCRF: (lambda d: (d.directed, d.projective), lambda d: d.n, max, _span_pad, _span_unpad),
+}
+
+
+def raggable(d) -> bool:
+    if type(d) not in RAGGED:
+        return False
+    return not (isinstance(d, SpanningTreeCRF) and d.single_root_edge)
+
+
+def group_key(d):
+    return (type(d), RAGGED[type(d)][0](d))
+
+
+def pad_group(ds):
+    """-> padded instances (all the same shape)."""
+    _, size, comb, pad, _ = RAGGED[type(ds[0])]
+    target = comb([size(d) for d in ds])
+    return [pad(d, target) for d in ds]
+
+
+def unpad(d, x):
+    return RAGGED[type(d)][4](d, x)

@@ -1,0 +1,51 @@
+"""Ragged batches on the GPU: instances of different lengths share ONE
+launch per group through inference-neutral padding and match the
+per-instance results (log Z, marginals, argmax)."""
+
+import numpy as np
+import pytest
+
+import paper_2308_03291_b200 as sd
+from golden.builders import alignment, chain, ctc, spanning
+from gpu_util import ATOL, RTOL, need_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(dists):
+    lz = sd.batch_map(sd.log_partition, dists)
+    mg = sd.batch_map(sd.marginals, dists)
+    for d, z, m in zip(dists, lz, mg):
+        z0 = sd.log_partition(d)
+        assert abs(z - z0) <= RTOL * abs(z0) + 1e-6
+        m0 = sd.marginals(d)
+        for k in m0:
+            assert m[k].shape == m0[k].shape
+            np.testing.assert_allclose(m[k], m0[k], rtol=RTOL, atol=ATOL)
+
+
+def test_ragged_chains():
+    need_gpu()
+    dists = [sd.LinearChainCRF(*chain(s, n, 5)) for s, n in enumerate([3, 17, 40, 1, 9])]
+    _check(dists)
+    am = sd.batch_map(sd.argmax_info, dists)
+    for d, (ind, score, algo) in zip(dists, am):
+        ind0, score0, _ = sd.argmax_info(d)
+        for k in ind0:
+            np.testing.assert_array_equal(ind[k], ind0[k])
+        assert score == score0
+
+
+def test_ragged_alignments():
+    need_gpu()
+    dists = [sd.MonotoneAlignmentCRF(alignment(s, n, m)) for s, (n, m) in enumerate([(5, 7), (40, 12), (12, 30), (1, 1)])]
+    _check(dists)
+
+
+def test_ragged_ctc_and_spanning():
+    need_gpu()
+    dists = [sd.CTCDist(*ctc(s, T, 6, 3)) for s, T in enumerate([7, 19, 30])]
+    _check(dists)
+    for proj in (False, True):
+        dists = [sd.SpanningTreeCRF(spanning(s, n, True), projective=proj) for s, n in enumerate([3, 11, 20])]
+        _check(dists)
