@@ -241,6 +241,16 @@ int sdb_eisner_decode(const float* adjacency, int64_t B, int32_t n, int32_t sing
                       int64_t noise_per_instance, int32_t num, int32_t* heads, int32_t* used, int32_t* status,
                       void* workspace, size_t ws_bytes, void* stream);
 
+
+/* sdb_cle replaces _find_cycle, _max_arborescence and cle_argmax
+ * (spanning.py:410-509; single root via _reweight_root, spanning.py:339-350):
+ * the non-projective argmax.  fp64 weights, the reference's tie rules ->
+ * identical arcs.  heads [B,n+1] (heads[0] = -1); status VACUOUS when no
+ * arborescence (or no single-root one) has finite score. */
+size_t sdb_cle_workspace(int64_t B, int32_t n);
+int sdb_cle(const float* adjacency, int64_t B, int32_t n, int32_t single_root, int32_t* heads, int32_t* status,
+            void* workspace, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

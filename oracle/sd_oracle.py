@@ -940,3 +940,98 @@ def eisner_decode(th, single_root, pick=None):
 def eisner_sample(th, single_root, rng):
     """spanning.py:328-331."""
     return eisner_decode(th, single_root, lambda w: sample_log_categorical(rng, w))
+
+
+# ---------------------------------------------------------------------------
+# non-projective argmax (spanning.py:410-509)
+# ---------------------------------------------------------------------------
+
+
+def _find_cycle(parent):
+    """spanning.py:410-425: first cycle (lowest start) of a dep -> head map."""
+    resolved = {0}
+    for start in sorted(parent):
+        if start in resolved:
+            continue
+        path, in_path, node = [], {}, start
+        while node not in resolved and node not in in_path:
+            in_path[node] = len(path)
+            path.append(node)
+            node = parent[node]
+        if node in in_path:
+            return path[in_path[node]:]
+        resolved.update(path)
+    return None
+
+
+def max_arborescence(w):
+    """spanning.py:428-499: greedy best incoming edges + cycle contraction."""
+    size = w.shape[0]
+    bh = {}
+    for dep in range(1, size):
+        col = w[:, dep].copy()
+        col[dep] = NEG_INF
+        h = int(np.argmax(col))
+        if col[h] == NEG_INF:
+            raise Vacuous("no arborescence has finite score")
+        bh[dep] = h
+    cyc = _find_cycle(bh)
+    if cyc is None:
+        return bh
+    cset = set(cyc)
+    keep = [v for v in range(size) if v not in cset]
+    nid = {v: i for i, v in enumerate(keep)}
+    cs = len(keep)
+    nw = np.full((cs + 1, cs + 1), NEG_INF)
+    enter, leave = {}, {}
+    for u in keep:
+        nu = nid[u]
+        for v in keep:
+            if u != v:
+                nw[nu, nid[v]] = w[u, v]
+        best, arg = NEG_INF, None
+        for v in cyc:
+            if w[u, v] == NEG_INF:
+                continue
+            a = w[u, v] - w[bh[v], v]
+            if a > best:
+                best, arg = a, v
+        if arg is not None:
+            nw[nu, cs] = best
+            enter[nu] = arg
+        if u == 0:
+            continue
+        best, arg = NEG_INF, None
+        for v in cyc:
+            if w[v, u] > best:
+                best, arg = w[v, u], v
+        if arg is not None:
+            nw[cs, nu] = best
+            leave[nu] = arg
+    sub = max_arborescence(nw)
+    parent, entry = {}, None
+    for nd, nh in sub.items():
+        if nd == cs:
+            entry = enter[nh]
+            parent[entry] = keep[nh]
+        elif nh == cs:
+            parent[keep[nd]] = leave[nd]
+        else:
+            parent[keep[nd]] = keep[nh]
+    for v in cyc:
+        if v != entry:
+            parent[v] = bh[v]
+    return parent
+
+
+def cle_heads(adj, single_root=False):
+    """spanning.py:502-509 -> heads [n+1] (heads[0] = -1)."""
+    w = reweight_root(adj) if single_root else adj
+    p = max_arborescence(np.asarray(w, dtype=np.float64))
+    n = adj.shape[0] - 1
+    heads = np.full(n + 1, -1, dtype=np.int64)
+    for d, h in p.items():
+        heads[d] = h
+    if single_root and int(np.sum(heads[1:] == 0)) != 1:
+        raise Vacuous("no arborescence satisfies the single-root constraint")
+    return heads

@@ -62,6 +62,8 @@ SIGNATURES = {
     "sdb_eisner_decode_workspace": (_sz, [_i64, _i32]),
     "sdb_eisner_decode": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _i64, _i32, _c_p, _c_p, _c_p, _c_p, _sz,
                                          _c_p]),
+    "sdb_cle_workspace": (_sz, [_i64, _i32]),
+    "sdb_cle": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _sz, _c_p]),
     "sdb_semimarkov_fb": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p]),
     "sdb_semimarkov_viterbi_workspace": (_sz, [_i64, _i32, _i32, _i32]),
     "sdb_semimarkov_viterbi": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p, _sz,

@@ -423,13 +423,13 @@ class SpanningBackend(Backend):
 
     def argmax(self, ds):
         d0 = ds[0]
-        if not d0.projective:
-            from .errors import UnsupportedInference
-
-            raise UnsupportedInference(
-                "non-projective argmax (Chu-Liu-Edmonds, spanning.py:410-509) is not on the GPU path")
         adj = to_dev([d.adjacency for d in ds])
-        heads, score, st = K.kuhlmann(adj, d0.single_root_edge)
+        if d0.projective:
+            heads, score, st = K.kuhlmann(adj, d0.single_root_edge)
+            msg = "no projective tree has finite score"
+        else:  # Chu-Liu-Edmonds (spanning.py:410-509)
+            heads, st = K.cle(adj, d0.single_root_edge)
+            msg = "no arborescence has finite score"
         heads = to_host(heads)
 
         def build(i):
@@ -439,7 +439,7 @@ class SpanningBackend(Backend):
             mask[heads[i][1:], dep] = 1.0
             return {"adjacency": mask}
 
-        return ArgmaxResult(to_host(st), build, "no projective tree has finite score")
+        return ArgmaxResult(to_host(st), build, msg)
 
     def sample(self, ds, seeds, num, algorithm=None):
         """span_sample (spanning.py:709-728): projective -> Eisner decode with

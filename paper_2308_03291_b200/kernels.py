@@ -462,3 +462,18 @@ def eisner_decode(adjacency, single_root: bool = False, noise=None, num: int = 1
                                ptr(ws), ws.numel(), stream_ptr(dev))
     _lib.check(rc, "sdb_eisner_decode")
     return heads, used, status
+
+
+def cle(adjacency, single_root: bool = False):
+    """spanning.py:410-509 batched (Chu-Liu-Edmonds) -> (heads [B,n+1] int32, status)."""
+    lib = _lib.load()
+    adj = f32(adjacency, "adjacency")
+    B, N, _ = adj.shape
+    dev = adj.device
+    heads = torch.empty(B, N, dtype=torch.int32, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    ws = workspace(lib.sdb_cle_workspace(B, N - 1), dev)
+    rc = lib.sdb_cle(ptr(adj), B, N - 1, int(single_root), ptr(heads), ptr(status), ptr(ws), ws.numel(),
+                     stream_ptr(dev))
+    _lib.check(rc, "sdb_cle")
+    return heads, status

@@ -31,7 +31,7 @@ def test_spanning_golden_api(case):
     marg, algo2 = sd.marginals_info(d)
     assert algo2 == algo
     case.check_marg("adjacency", marg["adjacency"], RTOL, 1e-5 if m["single"] else 2e-6)
-    if m["projective"] and "argmax_adjacency" in case:
+    if "argmax_adjacency" in case:  # Kuhlmann (projective) / Chu-Liu-Edmonds (non-projective)
         ind, score, aalgo = sd.argmax_info(d)
         np.testing.assert_array_equal(ind["adjacency"], case["argmax_adjacency"])
         assert score == float(case.argmax_score)
@@ -80,8 +80,21 @@ def test_eisner_zero_ties():
         np.testing.assert_array_equal(heads[0].cpu().numpy(), O.kuhlmann_heads(adj[0], single))
 
 
-def test_nonprojective_argmax_unsupported():
+@pytest.mark.parametrize("single", [False, True])
+def test_cle_argmax_vs_oracle(single):
+    """Chu-Liu-Edmonds (spanning.py:410-509), bit-exact arcs at C3 size."""
     need_gpu()
-    d = sd.SpanningTreeCRF(batch_spanning(1, 1, 4)[0])
-    with pytest.raises(sd.UnsupportedInference):
-        sd.argmax(d)
+    adj = batch_spanning(3100, 6, 128)
+    heads, st = K.cle(dev(adj), single)
+    assert (st.cpu().numpy() == 0).all()
+    for b in range(6):
+        np.testing.assert_array_equal(heads[b].cpu().numpy(), O.cle_heads(adj[b], single))
+    # small instances with many cycles (all-equal weights -> ties everywhere)
+    z = np.zeros((4, 8, 8))
+    z[:, :, 0] = -np.inf
+    for b in range(4):
+        np.fill_diagonal(z[b], -np.inf)
+    z[1] = batch_spanning(5, 1, 7)[0]
+    heads, st = K.cle(dev(z), single)
+    for b in range(4):
+        np.testing.assert_array_equal(heads[b].cpu().numpy(), O.cle_heads(z[b], single))

@@ -133,6 +133,14 @@ def test_oracle_spanning(case):
         if not case.vacuous:
             marg = O.mtt_marginals(adj, single)
             case.check_marg("adjacency", marg, rtol=1e-7, atol=1e-10)
+            if "argmax_adjacency" in case:  # Chu-Liu-Edmonds (spanning.py:410-509)
+                heads = O.cle_heads(adj, single)
+                ind = np.asarray(case["argmax_adjacency"])
+                want = np.full(adj.shape[0], -1)
+                for h, d in zip(*np.nonzero(ind)):
+                    want[d] = h
+                np.testing.assert_array_equal(heads, want)
+                assert _close(O.heads_score(adj, heads), float(case.argmax_score), 1e-12)
 
 
 def test_oracle_closed_forms():
