@@ -251,6 +251,21 @@ size_t sdb_cle_workspace(int64_t B, int32_t n);
 int sdb_cle(const float* adjacency, int64_t B, int32_t n, int32_t single_root, int32_t* heads, int32_t* status,
             void* workspace, size_t ws_bytes, void* stream);
 
+
+/* Wilson's loop-erased random walk sampler (spanning.py:531-558), resumable:
+ * sdb_wilson_begin puts the root (and root_child[b], nullable, for the
+ * single-root variant after _condition_on_root_child) in the tree;
+ * sdb_wilson_step consumes noise [B, cap] = the next cap draws of each
+ * instance's Gumbel stream (n+1 per walk step), returning the cumulative
+ * draws used [B] (int64) and status 0 done / 3 needs the next chunk / 4 step
+ * cap exceeded (SamplerStepLimit).  parent [B, n+1] once done. */
+size_t sdb_wilson_workspace(int64_t B, int32_t n);
+int sdb_wilson_begin(int64_t B, int32_t n, const int32_t* root_child, int32_t* parent, int32_t* status,
+                     void* workspace, size_t ws_bytes, void* stream);
+int sdb_wilson_step(const float* adjacency, int64_t B, int32_t n, const double* noise, int64_t cap,
+                    int64_t step_cap, int32_t* parent, int64_t* used, int32_t* status, void* workspace,
+                    size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1035,3 +1035,32 @@ def cle_heads(adj, single_root=False):
     if single_root and int(np.sum(heads[1:] == 0)) != 1:
         raise Vacuous("no arborescence satisfies the single-root constraint")
     return heads
+
+
+def wilson_sample(adj, single_root, rng):
+    """spanning.py:517-558: (single root: draw the root child from the exact
+    marginals first) then loop-erased random walks toward the tree.
+    Returns heads [n+1]."""
+    n = adj.shape[0] - 1
+    parent = np.full(n + 1, -1, dtype=np.int64)
+    in_tree = np.zeros(n + 1, dtype=bool)
+    in_tree[0] = True
+    if single_root:
+        marg = mtt_marginals(adj, True)
+        child = 1 + sample_log_categorical(rng, np.log(np.maximum(marg[0, 1:], 1e-300)))
+        keep = adj[0, child]
+        adj = adj.copy()
+        adj[0, :] = NEG_INF
+        adj[0, child] = keep
+        parent[child] = 0
+        in_tree[child] = True
+    for start in range(1, n + 1):
+        u = start
+        while not in_tree[u]:
+            parent[u] = sample_log_categorical(rng, adj[:, u])
+            u = parent[u]
+        u = start
+        while not in_tree[u]:
+            in_tree[u] = True
+            u = parent[u]
+    return parent

@@ -64,6 +64,9 @@ SIGNATURES = {
                                          _c_p]),
     "sdb_cle_workspace": (_sz, [_i64, _i32]),
     "sdb_cle": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _sz, _c_p]),
+    "sdb_wilson_workspace": (_sz, [_i64, _i32]),
+    "sdb_wilson_begin": (ctypes.c_int, [_i64, _i32, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
+    "sdb_wilson_step": (ctypes.c_int, [_c_p, _i64, _i32, _c_p, _i64, _i64, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
     "sdb_semimarkov_fb": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p]),
     "sdb_semimarkov_viterbi_workspace": (_sz, [_i64, _i32, _i32, _i32]),
     "sdb_semimarkov_viterbi": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p, _sz,

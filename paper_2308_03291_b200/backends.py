@@ -447,9 +447,7 @@ class SpanningBackend(Backend):
         on the GPU path."""
         d0 = ds[0]
         if not d0.projective:
-            from .errors import UnsupportedInference
-
-            raise UnsupportedInference("non-projective sampling (Wilson / Colbourn) is not on the GPU path")
+            return self._sample_nonprojective(ds, seeds, num, algorithm)
         if algorithm not in (None, "eisner"):
             raise InvalidProblem(f"sampler {algorithm!r} does not apply to projective trees")
         adj = to_dev([d.adjacency for d in ds])
@@ -466,6 +464,55 @@ class SpanningBackend(Backend):
                 inds.append({"adjacency": mask})
             out.append(inds)
         return out, self._prefix(d0) + "eisner-sampling"
+
+    def _sample_nonprojective(self, ds, seeds, num, algorithm):
+        """span_sample non-projective (spanning.py:719-728) with Wilson's
+        loop-erased walks on the GPU (spanning.py:531-558); single-root first
+        draws the root's child from the GPU Matrix-Tree marginals
+        (spanning.py:517-528)."""
+        from .errors import SamplerStepLimit, UnsupportedInference
+
+        if algorithm == "colbourn":
+            raise UnsupportedInference("the Colbourn sampler is not on the GPU path (use the default, Wilson)")
+        if algorithm not in (None, "wilson"):
+            raise InvalidProblem(f"unknown spanning-tree sampler {algorithm!r}")
+        d0 = ds[0]
+        single = d0.single_root_edge
+        adj = to_dev([d.adjacency for d in ds])
+        logz, marg, st = K.mtt(adj, single, single)
+        sth, lz = to_host(st), to_host(logz)
+        for i in range(len(ds)):
+            Result(lz[i:i + 1], sth[i:i + 1], None, "no spanning tree has finite score").raise_vacuous(0)
+            if lz[i] == -np.inf:
+                raise VacuousDistribution("no spanning tree has finite score")
+        streams = [K.GumbelStream(s) for s in seeds]
+        mg = to_host(marg).astype(np.float64) if single else None
+        n = d0.n
+        out = [[] for _ in ds]
+        for _ in range(num):
+            child = None
+            work = adj
+            if single:
+                child = np.empty(len(ds), dtype=np.int64)
+                for i in range(len(ds)):
+                    w = np.log(np.maximum(mg[i, 0, 1:], 1e-300))
+                    g = streams[i].take(n)
+                    child[i] = 1 + int(np.argmax(np.where(w > -np.inf, w + g, -np.inf)))
+                work = adj.clone()
+                keep = work[torch.arange(len(ds)), 0, torch.as_tensor(child)].clone()
+                work[:, 0, :] = float("-inf")
+                work[torch.arange(len(ds)), 0, torch.as_tensor(child)] = keep
+                child = torch.as_tensor(child, dtype=torch.int32).cuda()
+            parent, st2 = K.wilson(work, streams, child)
+            s2 = to_host(st2)
+            if (s2 == 4).any():
+                raise SamplerStepLimit("loop-erased walk exceeded its step cap; weights are near-degenerate")
+            par = to_host(parent)
+            for i, d in enumerate(ds):
+                mask = np.zeros((n + 1, n + 1))
+                mask[par[i, 1:], np.arange(1, n + 1)] = 1.0
+                out[i].append({"adjacency": mask})
+        return out, self._prefix(d0) + "wilson"
 
 
 # ------------------------------------------------------------------- PCFG

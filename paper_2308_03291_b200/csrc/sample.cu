@@ -567,3 +567,153 @@ extern "C" int sdb_eisner_decode(const float* adjacency, int64_t B, int32_t n, i
   SDB_CHECK_LAUNCH();
   return SDB_OK;
 }
+
+// ================================================================ Wilson
+// spanning.py:531-558 (wilson_sample_arcs): loop-erased random walks toward
+// the growing tree, one categorical pick per step over the dependent's
+// incoming column (n+1 Gumbel draws per step).  Warp per instance; the walk
+// state lives in the workspace so that a launch that runs out of stream
+// (status 3) resumes where it stopped once the caller supplies the next
+// chunk of the SAME Gumbel stream.
+namespace {
+struct WilsonState {
+  int start, u, phase, pad;
+  long long steps, used;
+};
+
+__global__ void wilson_kernel(int64_t B, const float* __restrict__ adj_all, int n, const double* __restrict__ noise_all,
+                              int64_t cap, long long step_cap, WilsonState* __restrict__ st_all,
+                              int32_t* __restrict__ parent_all, int8_t* __restrict__ in_tree_all,
+                              int32_t* __restrict__ status) {
+  const int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= B || status[b] != 3) return;  // 3 = walk in progress
+  const int N = n + 1;
+  const float* adj = adj_all + (size_t)b * N * N;
+  const double* g = noise_all + (size_t)b * cap;
+  WilsonState s = st_all[b];
+  int32_t* parent = parent_all + (size_t)b * N;
+  int8_t* in_tree = in_tree_all + (size_t)b * N;
+  long long pos = 0;
+  while (s.start <= n) {
+    if (s.phase == 0) {
+      if (in_tree[s.u]) {
+        s.phase = 1;
+        s.u = s.start;
+        continue;
+      }
+      if (pos + N > cap) break;  // need the next chunk of the stream
+      if (++s.steps > step_cap) {
+        if (lane == 0) status[b] = 4;  // SamplerStepLimit
+        s.steps = step_cap;
+        break;
+      }
+      double best = ninfd();
+      int arg = -1;
+      for (int h = lane; h < N; h += 32) {
+        const double w = (double)adj[(size_t)h * N + s.u];
+        if (w > ninfd()) {
+          const double v = w + g[pos + h];
+          if (arg < 0 || v > best) {
+            best = v;
+            arg = h;
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, arg, o);
+        if (oi >= 0 && (arg < 0 || ov > best || (ov == best && oi < arg))) {
+          best = ov;
+          arg = oi;
+        }
+      }
+      pos += N;
+      if (lane == 0) parent[s.u] = arg;
+      __syncwarp();
+      s.u = arg;
+    } else {
+      if (!in_tree[s.u]) {
+        if (lane == 0) in_tree[s.u] = 1;
+        __syncwarp();
+        s.u = parent[s.u];
+        continue;
+      }
+      ++s.start;
+      s.u = s.start;
+      s.phase = 0;
+    }
+  }
+  s.used += pos;
+  if (lane == 0) {
+    st_all[b] = s;
+    if (s.start > n) status[b] = SDB_ST_OK;
+  }
+}
+}  // namespace
+
+extern "C" size_t sdb_wilson_workspace(int64_t B, int32_t n) {
+  return (size_t)B * (sizeof(WilsonState) + (size_t)(n + 1) * 5 + 16);
+}
+
+// One resumable pass of Wilson's algorithm.  On the first call (*status[b]
+// != 3 on entry is taken as "start": status must be set to 3 by the caller
+// together with a zeroed workspace, see sdb_wilson_begin).  noise [B, cap]
+// holds the next cap draws of each instance's stream; used [B] (int64) returns
+// how many were consumed in this pass; status: 0 done, 3 needs the next
+// chunk, 4 step cap exceeded.  parent [B, n+1] is valid once status == 0.
+extern "C" int sdb_wilson_step(const float* adjacency, int64_t B, int32_t n, const double* noise, int64_t cap,
+                               int64_t step_cap, int32_t* parent, int64_t* used, int32_t* status, void* workspace,
+                               size_t ws_bytes, void* stream) {
+  if (B < 0 || n < 1 || cap < 0) return SDB_ERR_ARG;
+  if (!adjacency || !noise || !parent || !used || !status) return SDB_ERR_ARG;
+  if (B == 0) return SDB_OK;
+  if (!workspace || ws_bytes < sdb_wilson_workspace(B, n)) return SDB_ERR_WORKSPACE;
+  WilsonState* st = (WilsonState*)workspace;
+  int8_t* in_tree = (int8_t*)(st + B);
+  cudaStream_t s = (cudaStream_t)stream;
+  wilson_kernel<<<(unsigned)((B + 3) / 4), 128, 0, s>>>(B, adjacency, n, noise, cap, (long long)step_cap, st, parent,
+                                                        in_tree, status);
+  SDB_CHECK_LAUNCH();
+  // used[b] = cumulative draws consumed (the caller diffs successive values)
+  if (cudaMemcpy2DAsync(used, sizeof(int64_t), (char*)st + offsetof(WilsonState, used), sizeof(WilsonState),
+                        sizeof(int64_t), (size_t)B, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return SDB_ERR_CUDA;
+  return SDB_OK;
+}
+
+// Initialise the walk state: root (and the optional pre-sampled root child)
+// in the tree, status 3 for every instance.
+namespace {
+__global__ void wilson_begin_kernel(int n, int64_t B, const int32_t* __restrict__ child, WilsonState* st,
+                                    int32_t* __restrict__ parent_all, int8_t* __restrict__ in_tree_all,
+                                    int32_t* __restrict__ status) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int N = n + 1;
+  for (int x = 0; x < N; ++x) {
+    parent_all[(size_t)b * N + x] = -1;
+    in_tree_all[(size_t)b * N + x] = (x == 0);
+  }
+  if (child) {
+    const int c = child[b];
+    parent_all[(size_t)b * N + c] = 0;
+    in_tree_all[(size_t)b * N + c] = 1;
+  }
+  st[b] = WilsonState{1, 1, 0, 0, 0, 0};
+  status[b] = 3;
+}
+}  // namespace
+
+extern "C" int sdb_wilson_begin(int64_t B, int32_t n, const int32_t* root_child, int32_t* parent, int32_t* status,
+                                void* workspace, size_t ws_bytes, void* stream) {
+  if (B < 0 || n < 1 || !parent || !status) return SDB_ERR_ARG;
+  if (B == 0) return SDB_OK;
+  if (!workspace || ws_bytes < sdb_wilson_workspace(B, n)) return SDB_ERR_WORKSPACE;
+  WilsonState* st = (WilsonState*)workspace;
+  wilson_begin_kernel<<<(unsigned)((B + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      n, B, root_child, st, parent, (int8_t*)(st + B), status);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}

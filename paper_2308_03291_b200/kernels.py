@@ -477,3 +477,67 @@ def cle(adjacency, single_root: bool = False):
                      stream_ptr(dev))
     _lib.check(rc, "sdb_cle")
     return heads, status
+
+
+class GumbelStream:
+    """One instance's Gumbel stream np.random.default_rng(seed).gumbel,
+    consumed in order; draws fetched ahead are kept for the next consumer
+    (so consecutive samples see exactly the reference's stream)."""
+
+    def __init__(self, seed):
+        import numpy as np
+
+        self._np = np
+        self.rng = np.random.default_rng(int(seed))
+        self.buf = np.empty(0)
+
+    def peek(self, k: int):
+        if self.buf.size < k:
+            self.buf = self._np.concatenate([self.buf, self.rng.gumbel(size=k - self.buf.size)])
+        return self.buf[:k]
+
+    def take(self, k: int):
+        out = self.peek(k).copy()
+        self.buf = self.buf[k:]
+        return out
+
+
+WILSON_STEP_CAP = 10 ** 7  # spanning.py:38
+
+
+def wilson(adjacency, streams, root_child=None, chunk_steps: int = 0):
+    """spanning.py:531-558 batched: loop-erased walks on the GPU, fed chunk by
+    chunk from each instance's GumbelStream -> (parent [B,n+1] int32, status)."""
+    import numpy as np
+
+    lib = _lib.load()
+    adj = f32(adjacency, "adjacency")
+    B, N, _ = adj.shape
+    n = N - 1
+    dev = adj.device
+    parent = torch.empty(B, N, dtype=torch.int32, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    used = torch.zeros(B, dtype=torch.int64, device=dev)
+    ws = workspace(lib.sdb_wilson_workspace(B, n), dev)
+    ch = i32(root_child, "root_child") if root_child is not None else None
+    _lib.check(lib.sdb_wilson_begin(B, n, ptr(ch), ptr(parent), ptr(status), ptr(ws), ws.numel(), stream_ptr(dev)),
+               "sdb_wilson_begin")
+    cap = N * (chunk_steps or 4 * N)
+    prev = np.zeros(B, dtype=np.int64)
+    while True:
+        st = status.cpu().numpy()
+        live = st == 3
+        if not live.any():
+            break
+        noise = np.zeros((B, cap))
+        for b in np.nonzero(live)[0]:
+            noise[b] = streams[b].peek(cap)
+        noise_d = torch.as_tensor(noise, device=dev)
+        rc = lib.sdb_wilson_step(ptr(adj), B, n, ptr(noise_d), cap, WILSON_STEP_CAP,
+                                 ptr(parent), ptr(used), ptr(status), ptr(ws), ws.numel(), stream_ptr(dev))
+        _lib.check(rc, "sdb_wilson_step")
+        u = used.cpu().numpy()
+        for b in np.nonzero(live)[0]:
+            streams[b].take(int(u[b] - prev[b]))
+        prev = u
+    return parent, status

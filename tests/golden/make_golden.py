@@ -224,11 +224,24 @@ def sample_cases(st):
             st.arrays[f"c{len(st.meta) - 1:03d}__eisner_max"] = mx
 
 
+def wilson_cases(st):
+    """Reference Wilson samples (non-projective, spanning.py:517-558)."""
+    for single in (False, True):
+        for seed, n in enumerate([2, 5, 9, 16]):
+            adj = bld.spanning(500 + seed, n, True)
+            d = sd.SpanningTreeCRF(adj, directed=True, projective=False, single_root_edge=single)
+            inds, algo = sd.sample_info(d, seed, num=2)
+            out = {"in_adjacency": adj}
+            for r, ind in enumerate(inds):
+                out[f"sample{r}_adjacency"] = ind["adjacency"]
+            st.add("spanning", dict(seed=seed, n=n, single=single, algo=algo), **out)
+
+
 def main():
     fams = {
         "chain": chain_cases, "semi_markov": semi_markov_cases, "alignment": alignment_cases,
         "ctc": ctc_cases, "tree": tree_cases, "pcfg": pcfg_cases, "spanning": spanning_cases,
-        "sample": sample_cases,
+        "sample": sample_cases, "wilson": wilson_cases,
     }
     only = sys.argv[1:] or list(fams)
     for fam in only:

@@ -134,4 +134,28 @@ def test_sample_vacuous_and_unsupported():
         sd.sample_info(sd.LinearChainCRF(np.zeros(2), np.zeros((1, 2, 2))), 0, num=0)
     adj = batch_spanning(75, 1, 5)[0]
     with pytest.raises(sd.UnsupportedInference):
-        sd.sample(sd.SpanningTreeCRF(adj, projective=False), 0)
+        sd.sample_info(sd.SpanningTreeCRF(adj, projective=False), 0, algorithm="colbourn")
+
+
+@pytest.mark.parametrize("case", load("wilson"), ids=lambda c: str(c.meta))
+def test_wilson_golden(case):
+    """Non-projective sampling (Wilson, spanning.py:517-558): identical to the
+    reference for the same seed (num=2 from one stream)."""
+    need_gpu()
+    d = sd.SpanningTreeCRF(case["in_adjacency"], directed=True, projective=False,
+                           single_root_edge=bool(case.meta["single"]))
+    inds, algo = sd.sample_info(d, int(case.meta["seed"]), num=2)
+    assert algo == case.meta["algo"]
+    for r, ind in enumerate(inds):
+        np.testing.assert_array_equal(ind["adjacency"], case[f"sample{r}_adjacency"])
+
+
+def test_wilson_vs_oracle_config_size():
+    need_gpu()
+    B, n = 4, 128
+    adj = batch_spanning(76, B, n)
+    streams = [K.GumbelStream(s) for s in _seeds(B)]
+    parent, st = K.wilson(dev(adj), streams)
+    assert (st == 0).all()
+    for b, s in enumerate(_seeds(B)):
+        np.testing.assert_array_equal(parent[b].cpu().numpy(), O.wilson_sample(adj[b], False, np.random.default_rng(s)))

@@ -63,3 +63,15 @@ def test_stream_equals_per_pick_draws():
     a = np.random.default_rng(5)
     per = np.concatenate([a.gumbel(size=k) for k in (3, 1, 2, 7, 1)])
     np.testing.assert_array_equal(per, np.random.default_rng(5).gumbel(size=14))
+
+
+@pytest.mark.parametrize("case", load("wilson"), ids=lambda c: str(c.meta))
+def test_oracle_wilson_matches_reference(case):
+    adj = inputs(case)["adjacency"]
+    single = bool(case.meta["single"])
+    rng = np.random.default_rng(int(case.meta["seed"]))
+    for r in range(2):
+        heads = O.wilson_sample(adj, single, rng)
+        mask = np.zeros_like(adj)
+        mask[heads[1:], np.arange(1, len(heads))] = 1
+        np.testing.assert_array_equal(mask, case[f"sample{r}_adjacency"])
