@@ -266,6 +266,23 @@ int sdb_wilson_step(const float* adjacency, int64_t B, int32_t n, const double* 
                     int64_t step_cap, int32_t* parent, int64_t* used, int32_t* status, void* workspace,
                     size_t ws_bytes, void* stream);
 
+
+/* sdb_semimarkov_sample: semi_markov_sample (chain.py:330-344): segments
+ * [B,num,n,4] (start, width, prev, label; last segment first), nseg
+ * [B,num]; stream bound per sample n*s*m + m.
+ * sdb_pcfg_sample: pcfg_sample (constituency.py:374-378): span_mask
+ * [B,num,n,n]; stream bound per sample NT + S^2 n(n-1)/2; workspace as
+ * sdb_pcfg_viterbi_workspace. */
+size_t sdb_semimarkov_sample_workspace(int64_t B, int32_t n, int32_t s, int32_t m);
+int sdb_semimarkov_sample(const float* segment_potentials, int64_t B, int32_t n, int32_t s, int32_t m,
+                          const double* noise, int64_t noise_per_instance, int32_t num, int32_t* segments,
+                          int32_t* nseg, int32_t* used, int32_t* status, void* workspace, size_t ws_bytes,
+                          void* stream);
+int sdb_pcfg_sample(const float* root, const float* rules, const float* emissions, const float* sticky, int64_t B,
+                    int32_t n, int32_t NT, int32_t PT, const double* noise, int64_t noise_per_instance, int32_t num,
+                    int8_t* span_mask, int32_t* used, int32_t* status, void* workspace, size_t ws_bytes,
+                    void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1064,3 +1064,47 @@ def wilson_sample(adj, single_root, rng):
             in_tree[u] = True
             u = parent[u]
     return parent
+
+
+def sm_sample(th, rng):
+    """chain.py:330-344 -> segments [(start, width, prev, label)] in walk order."""
+    n, s, m, _ = th.shape
+    al = sm_alpha(th)
+    if lse_all(al[-1]) == NEG_INF:
+        raise Vacuous("no labeled segmentation has finite score")
+    segs = []
+    t = n
+    l = sample_log_categorical(rng, al[-1])
+    while t > 0:
+        widths = list(range(1, min(s, t) + 1))
+        logits = np.stack([al[t - w] + th[t - w, w - 1, :, l] for w in widths])
+        flat = sample_log_categorical(rng, logits)
+        w = widths[flat // m]
+        p = flat % m
+        segs.append((t - w, w, p, l))
+        t, l = t - w, p
+    return segs
+
+
+def pcfg_sample(root, rules, emis, rng, sticky=None):
+    """constituency.py:343-363, 374-378 -> span mask [n,n]."""
+    n, nt = emis.shape[0], root.shape[0]
+    ch = pcfg_inside_chart(root, rules, emis, sticky)
+    if lse_all(root + ch[0, n - 1, :nt]) == NEG_INF:
+        raise Vacuous("the grammar derives no tree for this sentence")
+    mask = np.zeros((n, n))
+    pick = lambda w: sample_log_categorical(rng, w)  # noqa: E731
+    stack = [(0, n - 1, pick(root + ch[0, n - 1, :nt]))]
+    while stack:
+        i, j, a = stack.pop()
+        mask[i, j] = 1.0
+        if i == j:
+            continue
+        left = ch[i, i:j]
+        right = ch[i + 1:j + 1, j]
+        joint = rules[a][None, :, :] + left[:, :, None] + right[:, None, :]
+        k_off, b, c = np.unravel_index(pick(joint.ravel()), joint.shape)
+        k = i + int(k_off)
+        stack.append((i, k, int(b)))
+        stack.append((k + 1, j, int(c)))
+    return mask

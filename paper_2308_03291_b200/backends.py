@@ -592,6 +592,17 @@ class PCFGBackend(Backend):
             return -np.inf, "pcfg-masked-inside"
         return float(lz[0] - lz[1]), "pcfg-masked-inside"
 
+    sample_algo = "pcfg-sampling"
+
+    def sample(self, ds, seeds, num):
+        root, rules, emis, sticky = self._inputs(ds)
+        d0 = ds[0]
+        noise = self._noise(seeds, K.stream_len("pcfg", dict(n=d0.n, NT=d0.num_nt, PT=d0.num_pt)), num)
+        mask, _, st = K.pcfg_sample(root, rules, emis, sticky, noise, num)
+        self._sample_status(st)
+        mh = to_host(mask).astype(np.float64)
+        return [[{"sticky": mh[i, r]} for r in range(num)] for i in range(len(ds))], self.sample_algo
+
     def argmax(self, ds):
         # pcfg_argmax (constituency.py:366-371): fp64 max-plus chart + first-max walk
         root, rules, emis, sticky = self._inputs(ds)
@@ -643,6 +654,24 @@ class SemiMarkovBackend(Backend):
             return {"segment_potentials": mask}
 
         return ArgmaxResult(to_host(st), build, self.vacuous_msg)
+
+    def sample(self, ds, seeds, num):
+        th = to_dev([d.segment_potentials for d in ds])
+        d0 = ds[0]
+        noise = self._noise(seeds, K.stream_len("semi_markov", dict(n=d0.n, s=d0.s, m=d0.m)), num)
+        seg, cnt, _, st = K.semimarkov_sample(th, noise, num)
+        self._sample_status(st)
+        seg, cnt = to_host(seg), to_host(cnt)
+        out = []
+        for i, d in enumerate(ds):
+            inds = []
+            for r in range(num):
+                mask = np.zeros_like(d.segment_potentials)
+                for s0, w, p, l in seg[i, r][: cnt[i, r]]:
+                    mask[s0, w - 1, p, l] = 1.0
+                inds.append({"segment_potentials": mask})
+            out.append(inds)
+        return out, self.sample_algo
 
 
 _BACKENDS = {

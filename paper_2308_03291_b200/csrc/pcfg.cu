@@ -499,10 +499,15 @@ __device__ ArgBest block_argmax(ArgBest x, ArgBest* red) {
   return r;
 }
 
+// kLog: log-semiring chart (constituency.py:246-266 with logsumexp) and
+// Gumbel-max picks from the caller's stream (pcfg_sample, constituency.py:374-378);
+// mask [B][num][n][n], used [B].
+template <bool kLog>
 __global__ void __launch_bounds__(kThreads) pcfg_max_kernel(
     const float* __restrict__ root_all, const float* __restrict__ rules_all, const float* __restrict__ emis_all,
     const float* __restrict__ sticky_all, int n, int NT, int PT, double* __restrict__ chart_all,
-    int8_t* __restrict__ mask_all, double* __restrict__ score, int32_t* __restrict__ status) {
+    int8_t* __restrict__ mask_all, double* __restrict__ score, int32_t* __restrict__ status,
+    const double* __restrict__ noise_all = nullptr, int64_t cap = 0, int num = 1, int32_t* __restrict__ used = nullptr) {
   extern __shared__ double pairs[];  // [S][S]
   __shared__ ArgBest red[kWarps];
   __shared__ int stk_i[2 * kMaxN], stk_j[2 * kMaxN], stk_a[2 * kMaxN];
@@ -514,7 +519,8 @@ __global__ void __launch_bounds__(kThreads) pcfg_max_kernel(
   const float* emis = emis_all + (size_t)b * n * PT;
   const float* sticky = sticky_all ? sticky_all + (size_t)b * n * n : nullptr;
   double* chart = chart_all + (size_t)b * n * n * S;
-  int8_t* mask = mask_all + (size_t)b * n * n;
+  int8_t* mask = mask_all + (size_t)b * num * n * n;
+  const double* g = kLog ? noise_all + (size_t)b * cap : nullptr;
   auto STK = [&](int i, int j) -> double { return sticky ? (double)sticky[i * n + j] : 0.0; };
   auto CH = [&](int i, int j) -> double* { return chart + ((size_t)i * n + j) * S; };
   if (tid == 0) badsh = 0;
@@ -527,7 +533,7 @@ __global__ void __launch_bounds__(kThreads) pcfg_max_kernel(
     if (sticky)
       for (int e = tid; e < n * n; e += kThreads) bad |= !(sticky[e] == 0.f || sticky[e] == ninf());
     if (bad) atomicOr(&badsh, 1);
-    for (int e = tid; e < n * n; e += kThreads) mask[e] = 0;
+    for (int e = tid; e < num * n * n; e += kThreads) mask[e] = 0;
   }
   for (int e = tid; e < n * S; e += kThreads) {
     const int i = e / S, X = e - i * S;
@@ -541,6 +547,11 @@ __global__ void __launch_bounds__(kThreads) pcfg_max_kernel(
         const int Bq = e / S, Cq = e - Bq * S;
         double m = ninfd();
         for (int k = i; k < j; ++k) m = fmax(m, CH(i, k)[Bq] + CH(k + 1, j)[Cq]);
+        if (kLog && m != ninfd()) {  // logsumexp over the split (constituency.py:262)
+          double sm = 0.0;
+          for (int k = i; k < j; ++k) sm += exp(CH(i, k)[Bq] + CH(k + 1, j)[Cq] - m);
+          m = log(sm) + m;
+        }
         pairs[e] = m;
       }
       __syncthreads();
@@ -548,8 +559,33 @@ __global__ void __launch_bounds__(kThreads) pcfg_max_kernel(
         double m = ninfd();
         if (A < NT) {
           const float* ra = rules + (size_t)A * S2;
-          for (int e = lane; e < S2; e += 32) m = fmax(m, (double)ra[e] + pairs[e]);
-          m = warp_maxd(m);
+          if (!kLog) {
+            for (int e = lane; e < S2; e += 32) m = fmax(m, (double)ra[e] + pairs[e]);
+            m = warp_maxd(m);
+          } else {
+            // lse over C per B (lane per B), then over B (constituency.py:263-264)
+            double vb[2] = {ninfd(), ninfd()};
+            for (int q = 0; q < 2; ++q) {
+              const int Bq = lane + 32 * q;
+              if (Bq >= S) continue;
+              double mx = ninfd();
+              for (int Cq = 0; Cq < S; ++Cq) mx = fmax(mx, (double)ra[Bq * S + Cq] + pairs[Bq * S + Cq]);
+              if (mx != ninfd()) {
+                double sm = 0.0;
+                for (int Cq = 0; Cq < S; ++Cq) sm += exp((double)ra[Bq * S + Cq] + pairs[Bq * S + Cq] - mx);
+                mx = log(sm) + mx;
+              }
+              vb[q] = mx;
+            }
+            double mx = warp_maxd(fmax(vb[0], vb[1]));
+            double sm = 0.0;
+            if (mx != ninfd()) {
+              for (int q = 0; q < 2; ++q) sm += (vb[q] == ninfd()) ? 0.0 : exp(vb[q] - mx);
+              for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+              mx = log(sm) + mx;
+            }
+            m = mx;
+          }
         }
         if (lane == 0) CH(i, j)[A] = (A < NT) ? m + STK(i, j) : ninfd();
       }
@@ -563,15 +599,29 @@ __global__ void __launch_bounds__(kThreads) pcfg_max_kernel(
   const double best = (n == 1) ? ninfd() : r0.v;  // a width-1 sentence has no NT derivation
   if (tid == 0) {
     status[b] = badsh ? SDB_ST_INVALID : (best == ninfd() ? SDB_ST_VACUOUS : SDB_ST_OK);
-    score[b] = best;
+    if (score) score[b] = best;
+    if (used) used[b] = 0;
   }
   if (badsh || best == ninfd()) return;
+  int64_t pos = 0;
+  for (int rr = 0; rr < num; ++rr) {
+  int8_t* maskr = mask + (size_t)rr * n * n;
+  ArgBest rp = r0;
+  if (kLog) {  // root symbol ~ exp(root + chart[0, n-1]) (constituency.py:346)
+    ArgBest y{ninfd(), 1 << 30};
+    for (int A = tid; A < NT; A += kThreads) {
+      const double w = (double)root[A] + CH(0, n - 1)[A];
+      if (w > ninfd()) y = arg_better(y, ArgBest{w + g[pos + A], A});
+    }
+    rp = block_argmax(y, red);
+    pos += NT;
+  }
   // walk (stack order is irrelevant for the span mask)
   int top = 0;
   if (tid == 0) {
     stk_i[0] = 0;
     stk_j[0] = n - 1;
-    stk_a[0] = r0.i;
+    stk_a[0] = rp.i;
   }
   top = 1;
   __syncthreads();
@@ -579,7 +629,7 @@ __global__ void __launch_bounds__(kThreads) pcfg_max_kernel(
     --top;
     const int i = stk_i[top], j = stk_j[top], a = stk_a[top];
     __syncthreads();
-    if (tid == 0) mask[i * n + j] = 1;
+    if (tid == 0) maskr[i * n + j] = 1;
     if (i == j) continue;
     const int width = j - i;
     const float* ra = rules + (size_t)a * S2;
@@ -588,9 +638,14 @@ __global__ void __launch_bounds__(kThreads) pcfg_max_kernel(
       const int ko = e / S2, r = e - ko * S2, Bq = r / S, Cq = r - Bq * S;
       const int k = i + ko;
       const double v = ((double)ra[r] + CH(i, k)[Bq]) + CH(k + 1, j)[Cq];
-      if (v > y.v) y = ArgBest{v, e};
+      if (!kLog) {
+        if (v > y.v) y = ArgBest{v, e};
+      } else if (v > ninfd()) {
+        y = arg_better(y, ArgBest{v + g[pos + e], e});
+      }
     }
     const ArgBest pk = block_argmax(y, red);
+    if (kLog) pos += (int64_t)width * S2;
     const int ko = pk.i / S2, r = pk.i - ko * S2, Bq = r / S, Cq = r - Bq * S;
     const int k = i + ko;
     if (tid == 0) {
@@ -604,6 +659,8 @@ __global__ void __launch_bounds__(kThreads) pcfg_max_kernel(
     top += 2;
     __syncthreads();
   }
+  }
+  if (kLog && tid == 0) used[b] = (int32_t)pos;
 }
 
 template <int kMode>
@@ -685,10 +742,35 @@ extern "C" int sdb_pcfg_viterbi(const float* root, const float* rules, const flo
   if (B == 0) return SDB_OK;
   if (!workspace || ws_bytes < sdb_pcfg_viterbi_workspace(B, n, NT, PT)) return SDB_ERR_WORKSPACE;
   const size_t smem = (size_t)(NT + PT) * (NT + PT) * sizeof(double);
-  if (cudaFuncSetAttribute(pcfg_max_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+  if (cudaFuncSetAttribute(pcfg_max_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
     return SDB_ERR_CUDA;
-  pcfg_max_kernel<<<(unsigned)B, kThreads, smem, (cudaStream_t)stream>>>(root, rules, emissions, sticky, n, NT, PT,
-                                                                       (double*)workspace, span_mask, score, status);
+  pcfg_max_kernel<false><<<(unsigned)B, kThreads, smem, (cudaStream_t)stream>>>(
+      root, rules, emissions, sticky, n, NT, PT, (double*)workspace, span_mask, score, status);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
+// pcfg_sample (constituency.py:374-378): log-semiring chart + Gumbel-max
+// derivation walk over the caller's stream (bound per sample: NT + S^2 n(n-1)/2).
+extern "C" int sdb_pcfg_sample(const float* root, const float* rules, const float* emissions, const float* sticky,
+                               int64_t B, int32_t n, int32_t NT, int32_t PT, const double* noise,
+                               int64_t noise_per_instance, int32_t num, int8_t* span_mask, int32_t* used,
+                               int32_t* status, void* workspace, size_t ws_bytes, void* stream) {
+  int rc = pcfg_check(B, n, NT, PT);
+  if (rc) return rc;
+  if (!root || !rules || !emissions || !noise || !span_mask || !used || !status || num < 1) return SDB_ERR_ARG;
+  const int64_t S = NT + PT;
+  if (noise_per_instance < (int64_t)num * (NT + S * S * ((int64_t)n * (n - 1) / 2))) return SDB_ERR_ARG;
+  if (B == 0) return SDB_OK;
+  if (!workspace || ws_bytes < sdb_pcfg_viterbi_workspace(B, n, NT, PT)) return SDB_ERR_WORKSPACE;
+  const size_t smem = (size_t)S * S * sizeof(double);
+  if (cudaFuncSetAttribute(pcfg_max_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return SDB_ERR_CUDA;
+  pcfg_max_kernel<true><<<(unsigned)B, kThreads, smem, (cudaStream_t)stream>>>(
+      root, rules, emissions, sticky, n, NT, PT, (double*)workspace, span_mask, nullptr, status, noise,
+      noise_per_instance, num, used);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
 }

@@ -717,3 +717,105 @@ extern "C" int sdb_wilson_begin(int64_t B, int32_t n, const int32_t* root_child,
   SDB_CHECK_LAUNCH();
   return SDB_OK;
 }
+
+// =========================================================== semi-Markov
+// chain.py:250-265 (alpha: lse over (width, prev) flattened width-major) and
+// 330-344 (semi_markov_sample).  Thread per label for the chart; thread 0 walks.
+namespace {
+__global__ void __launch_bounds__(kT) semimarkov_sample_kernel(const float* __restrict__ th_all, int n, int s, int m,
+                                                               const double* __restrict__ noise_all, int64_t cap,
+                                                               int num, double* __restrict__ al_all,
+                                                               int32_t* __restrict__ seg_all,
+                                                               int32_t* __restrict__ nseg_all,
+                                                               int32_t* __restrict__ used,
+                                                               int32_t* __restrict__ status) {
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const float* th = th_all + (size_t)b * n * s * m * m;  // [start][w-1][prev][label]
+  double* al = al_all + (size_t)b * (n + 1) * m;
+  const double* g = noise_all + (size_t)b * cap;
+  int bad = 0;
+  for (int e = tid; e < n * s * m * m; e += kT) bad |= bad_input(th[e]);
+  const int anybad = __syncthreads_or(bad);
+  if (anybad) {
+    if (tid == 0) {
+      status[b] = SDB_ST_INVALID;
+      used[b] = 0;
+    }
+    return;
+  }
+  for (int l = tid; l < m; l += kT) al[l] = (l == 0) ? 0.0 : ninfd();
+  __syncthreads();
+  auto TH = [&](int st, int w, int p, int l) { return (double)th[(((size_t)st * s + w - 1) * m + p) * m + l]; };
+  for (int t = 1; t <= n; ++t) {
+    for (int l = tid; l < m; l += kT) {
+      double mx = ninfd();
+      const int W = min(s, t);
+      for (int w = 1; w <= W; ++w)
+        for (int p = 0; p < m; ++p) mx = fmax(mx, al[(size_t)(t - w) * m + p] + TH(t - w, w, p, l));
+      double sm = 0.0;
+      if (mx != ninfd())
+        for (int w = 1; w <= W; ++w)
+          for (int p = 0; p < m; ++p) sm += exp(al[(size_t)(t - w) * m + p] + TH(t - w, w, p, l) - mx);
+      al[(size_t)t * m + l] = lse2(mx, sm);
+    }
+    __syncthreads();
+  }
+  if (tid != 0) return;
+  bool alive = false;
+  for (int l = 0; l < m; ++l) alive |= al[(size_t)n * m + l] > ninfd();
+  status[b] = alive ? SDB_ST_OK : SDB_ST_VACUOUS;
+  int64_t pos = 0;
+  if (alive) {
+    for (int r = 0; r < num; ++r) {
+      int32_t* seg = seg_all + ((size_t)b * num + r) * n * 4;
+      int cnt = 0;
+      Pick p0{ninfd(), -1};
+      for (int l = 0; l < m; ++l) pick_add(p0, al[(size_t)n * m + l], g[pos + l], l);
+      pos += m;
+      int t = n, l = p0.idx;
+      while (t > 0) {
+        const int W = min(s, t);
+        Pick q{ninfd(), -1};
+        for (int w = 1; w <= W; ++w)
+          for (int p = 0; p < m; ++p) {
+            const int f = (w - 1) * m + p;
+            pick_add(q, al[(size_t)(t - w) * m + p] + TH(t - w, w, p, l), g[pos + f], f);
+          }
+        pos += (int64_t)W * m;
+        const int w = 1 + q.idx / m, p = q.idx % m;
+        seg[4 * cnt + 0] = t - w;
+        seg[4 * cnt + 1] = w;
+        seg[4 * cnt + 2] = p;
+        seg[4 * cnt + 3] = l;
+        ++cnt;
+        t -= w;
+        l = p;
+      }
+      nseg_all[(size_t)b * num + r] = cnt;
+    }
+  }
+  used[b] = (int32_t)pos;
+}
+}  // namespace
+
+extern "C" size_t sdb_semimarkov_sample_workspace(int64_t B, int32_t n, int32_t s, int32_t m) {
+  return (size_t)B * (n + 1) * m * sizeof(double);
+}
+
+/* segments [B,num,n,4] (start, width, prev, label) in walk order (last
+ * segment first), nseg [B,num]. */
+extern "C" int sdb_semimarkov_sample(const float* segment_potentials, int64_t B, int32_t n, int32_t s, int32_t m,
+                                     const double* noise, int64_t noise_per_instance, int32_t num, int32_t* segments,
+                                     int32_t* nseg, int32_t* used, int32_t* status, void* workspace, size_t ws_bytes,
+                                     void* stream) {
+  if (B < 0 || n < 1 || s < 1 || m < 1 || num < 1) return SDB_ERR_ARG;
+  if (!segment_potentials || !noise || !segments || !nseg || !used || !status) return SDB_ERR_ARG;
+  if (noise_per_instance < (int64_t)num * ((int64_t)n * s * m + m)) return SDB_ERR_ARG;
+  if (B == 0) return SDB_OK;
+  if (!workspace || ws_bytes < sdb_semimarkov_sample_workspace(B, n, s, m)) return SDB_ERR_WORKSPACE;
+  semimarkov_sample_kernel<<<(unsigned)B, kT, 0, (cudaStream_t)stream>>>(segment_potentials, n, s, m, noise,
+                                                                        noise_per_instance, num, (double*)workspace,
+                                                                        segments, nseg, used, status);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}

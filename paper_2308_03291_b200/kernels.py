@@ -375,6 +375,11 @@ def stream_len(family: str, shape: dict) -> int:
         return (2 * shape["n"] - 1) * shape["m"] + shape["n"] ** 2
     if family == "eisner":
         return shape["n"] + 4 * (shape["n"] + 1) ** 2
+    if family == "semi_markov":
+        return shape["n"] * shape["s"] * shape["m"] + shape["m"]
+    if family == "pcfg":
+        S = shape["NT"] + shape["PT"]
+        return shape["NT"] + S * S * (shape["n"] * (shape["n"] - 1) // 2)
     raise ValueError(family)
 
 
@@ -541,3 +546,41 @@ def wilson(adjacency, streams, root_child=None, chunk_steps: int = 0):
             streams[b].take(int(u[b] - prev[b]))
         prev = u
     return parent, status
+
+
+def semimarkov_sample(segment_potentials, noise, num: int):
+    """chain.py:330-344 batched -> (segments [B,num,n,4], nseg [B,num], used, status)."""
+    lib = _lib.load()
+    th, noise = f32(segment_potentials, "segment_potentials"), f64(noise, "noise")
+    B, n, s, m, _ = th.shape
+    dev = th.device
+    seg = torch.empty(B, num, n, 4, dtype=torch.int32, device=dev)
+    nseg = torch.empty(B, num, dtype=torch.int32, device=dev)
+    used = torch.empty(B, dtype=torch.int32, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    ws = workspace(lib.sdb_semimarkov_sample_workspace(B, n, s, m), dev)
+    rc = lib.sdb_semimarkov_sample(ptr(th), B, n, s, m, ptr(noise), noise.shape[1], num, ptr(seg), ptr(nseg),
+                                   ptr(used), ptr(status), ptr(ws), ws.numel(), stream_ptr(dev))
+    _lib.check(rc, "sdb_semimarkov_sample")
+    return seg, nseg, used, status
+
+
+def pcfg_sample(root, rules, emissions, sticky, noise, num: int):
+    """constituency.py:374-378 batched -> (span_mask [B,num,n,n] int8, used, status)."""
+    lib = _lib.load()
+    root = f32(root, "root")
+    rules = f32(rules, "binary_rules")
+    emis = f32(emissions, "emissions")
+    st_in = f32(sticky, "sticky") if sticky is not None else None
+    noise = f64(noise, "noise")
+    B, NT = root.shape
+    n, PT = emis.shape[1], emis.shape[2]
+    dev = root.device
+    mask = torch.empty(B, num, n, n, dtype=torch.int8, device=dev)
+    used = torch.empty(B, dtype=torch.int32, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    ws = workspace(lib.sdb_pcfg_viterbi_workspace(B, n, NT, PT), dev)
+    rc = lib.sdb_pcfg_sample(ptr(root), ptr(rules), ptr(emis), ptr(st_in), B, n, NT, PT, ptr(noise), noise.shape[1],
+                             num, ptr(mask), ptr(used), ptr(status), ptr(ws), ws.numel(), stream_ptr(dev))
+    _lib.check(rc, "sdb_pcfg_sample")
+    return mask, used, status

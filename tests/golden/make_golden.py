@@ -237,11 +237,30 @@ def wilson_cases(st):
             st.add("spanning", dict(seed=seed, n=n, single=single, algo=algo), **out)
 
 
+def sample2_cases(st):
+    """Reference samples for the semi-Markov CRF and the PCFG (chain.py:330-344,
+    constituency.py:374-378), num=2 from one stream."""
+    for seed, (n, sw, m) in enumerate([(1, 1, 2), (6, 3, 2), (12, 4, 3)]):
+        th = bld.semi_markov(seed, n, sw, m)
+        inds, algo = sd.sample_info(sd.SemiMarkovCRF(th), seed, num=2)
+        out = {"in_segment_potentials": th}
+        for r, ind in enumerate(inds):
+            out[f"sample{r}_segment_potentials"] = ind["segment_potentials"]
+        st.add("semi_markov", dict(seed=seed, n=n, s=sw, m=m, algo=algo), **out)
+    for seed, (n, nt, pt) in enumerate([(2, 2, 2), (5, 3, 2), (8, 4, 4)]):
+        root, rules, emis = bld.pcfg(seed, n, nt, pt)
+        inds, algo = sd.sample_info(sd.PCFG(root, rules, emis), seed, num=2)
+        out = {"in_root": root, "in_binary_rules": rules, "in_emissions": emis}
+        for r, ind in enumerate(inds):
+            out[f"sample{r}_sticky"] = ind["sticky"]
+        st.add("pcfg", dict(seed=seed, n=n, nt=nt, pt=pt, algo=algo), **out)
+
+
 def main():
     fams = {
         "chain": chain_cases, "semi_markov": semi_markov_cases, "alignment": alignment_cases,
         "ctc": ctc_cases, "tree": tree_cases, "pcfg": pcfg_cases, "spanning": spanning_cases,
-        "sample": sample_cases, "wilson": wilson_cases,
+        "sample": sample_cases, "wilson": wilson_cases, "sample2": sample2_cases,
     }
     only = sys.argv[1:] or list(fams)
     for fam in only:

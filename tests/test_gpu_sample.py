@@ -159,3 +159,39 @@ def test_wilson_vs_oracle_config_size():
     assert (st == 0).all()
     for b, s in enumerate(_seeds(B)):
         np.testing.assert_array_equal(parent[b].cpu().numpy(), O.wilson_sample(adj[b], False, np.random.default_rng(s)))
+
+
+@pytest.mark.parametrize("case", load("sample2"), ids=lambda c: str(c.meta))
+def test_semimarkov_pcfg_sample_golden(case):
+    need_gpu()
+    x = inputs(case)
+    if case.meta["family"] == "semi_markov":
+        d, key = sd.SemiMarkovCRF(x["segment_potentials"]), "segment_potentials"
+    else:
+        d, key = sd.PCFG(x["root"], x["binary_rules"], x["emissions"]), "sticky"
+    inds, algo = sd.sample_info(d, int(case.meta["seed"]), num=2)
+    assert algo == case.meta["algo"]
+    for r, ind in enumerate(inds):
+        np.testing.assert_array_equal(ind[key], case[f"sample{r}_{key}"])
+
+
+def test_semimarkov_pcfg_sample_vs_oracle():
+    need_gpu()
+    from golden.builders import batch_semi_markov, batch_pcfg
+    B, n, s, m = 3, 40, 6, 8
+    th = batch_semi_markov(77, B, n, s, m)
+    cnt = K.stream_len("semi_markov", dict(n=n, s=s, m=m))
+    noise = torch.stack([torch.as_tensor(np.random.default_rng(x).gumbel(size=cnt)) for x in _seeds(B)]).cuda()
+    seg, nseg, used, st = K.semimarkov_sample(dev(th), noise, 1)
+    assert (st == 0).all()
+    for b, x in enumerate(_seeds(B)):
+        got = [tuple(v) for v in seg[b, 0, : nseg[b, 0]].cpu().numpy().tolist()]
+        assert got == [tuple(int(z) for z in v) for v in O.sm_sample(th[b], np.random.default_rng(x))]
+    B, n = 2, 12
+    r, ru, e = batch_pcfg(78, B, n, 6, 5)
+    cnt = K.stream_len("pcfg", dict(n=n, NT=6, PT=5))
+    noise = torch.stack([torch.as_tensor(np.random.default_rng(x).gumbel(size=cnt)) for x in _seeds(B)]).cuda()
+    mask, used, st = K.pcfg_sample(dev(r), dev(ru), dev(e), None, noise, 1)
+    assert (st == 0).all()
+    for b, x in enumerate(_seeds(B)):
+        np.testing.assert_array_equal(mask[b, 0].cpu().numpy(), O.pcfg_sample(r[b], ru[b], e[b], np.random.default_rng(x)))

@@ -75,3 +75,19 @@ def test_oracle_wilson_matches_reference(case):
         mask = np.zeros_like(adj)
         mask[heads[1:], np.arange(1, len(heads))] = 1
         np.testing.assert_array_equal(mask, case[f"sample{r}_adjacency"])
+
+
+@pytest.mark.parametrize("case", load("sample2"), ids=lambda c: str(c.meta))
+def test_oracle_semimarkov_pcfg_samples_match_reference(case):
+    x = inputs(case)
+    rng = np.random.default_rng(int(case.meta["seed"]))
+    for r in range(2):
+        if case.meta["family"] == "semi_markov":
+            th = x["segment_potentials"]
+            mask = np.zeros_like(th)
+            for s0, w, p, l in O.sm_sample(th, rng):
+                mask[s0, w - 1, p, l] = 1
+            np.testing.assert_array_equal(mask, case[f"sample{r}_segment_potentials"])
+        else:
+            mask = O.pcfg_sample(x["root"], x["binary_rules"], x["emissions"], rng)
+            np.testing.assert_array_equal(mask, case[f"sample{r}_sticky"])
