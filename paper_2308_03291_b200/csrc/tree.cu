@@ -31,12 +31,16 @@ size_t tree_smem(int n) {
   return T * 8 * 2 + T * 4 + 64;
 }
 
-// warp-wide lse of per-lane (max, sum) partials over doubles
+// warp-wide lse of per-lane (max, sum) partials over doubles.  The common
+// shift only has to be CLOSE to the max (the partial sums are rescaled by
+// exp(m - M) <= ~1), so it is reduced in fp32 (one shuffle per round instead
+// of two + a double compare) and the result stays exact in fp64.
 __device__ __forceinline__ double warp_lse_d(double m, float s) {
-  double M = warp_maxd(m);
-  float e = (M == ninfd() || m == ninfd()) ? 0.f : s * fexp((float)(m - M));
+  const float mf = warp_max((float)m);
+  const double M = (double)mf;
+  float e = (mf == ninf() || m == ninfd()) ? 0.f : s * fexp((float)(m - M));
   e = warp_sum(e);
-  return (M == ninfd()) ? ninfd() : M + (double)flog(e);
+  return (mf == ninf()) ? ninfd() : M + (double)flog(e);
 }
 
 template <int kMode>  // 0 logZ, 1 logZ+marginals, 2 max-plus argmax
@@ -56,32 +60,59 @@ __global__ void __launch_bounds__(kThreads) tree_kernel(const float* __restrict_
   __syncthreads();
   constexpr bool kMax = (kMode == 2);
 
-  // ---- 1. label fold over the upper triangle (constituency.py:55)
+  // ---- 1. label fold over the upper triangle (constituency.py:55): thread per
+  // span, the label row read with 16-byte loads all in flight at once (a warp
+  // per span was latency-bound on one dependent global load per span)
   int bad = 0;
-  for (int idx = warp; idx < (int)T; idx += kWarps) {
-    // map packed index -> (i, j)
-    int i = 0, rem = idx;
-    while (rem >= n - i) { rem -= n - i; ++i; }
-    const int j = i + rem;
+  const bool vec4 = ((m & 3) == 0) && ((((uintptr_t)th) & 15) == 0);
+  for (int idx = tid; idx < (int)T; idx += kThreads) {
+    // map packed index -> (i, j): row i starts at tri(i, i) = i n - i (i-1) / 2
+    const float b2 = 2.f * n + 1.f;
+    int i = (int)((b2 - sqrtf(b2 * b2 - 8.f * idx)) * 0.5f);
+    i = max(0, min(i, n - 1));
+    while (i > 0 && tri(i, i, n) > idx) --i;
+    while (i + 1 < n && tri(i + 1, i + 1, n) <= idx) ++i;
+    const int j = i + (idx - tri(i, i, n));
     const float* row = th + ((size_t)i * n + j) * m;
-    float mx = ninf();
-    for (int l = lane; l < m; l += 32) {
-      const float x = row[l];
+    float mx = ninf(), sm = 0.f;
+    // online (max, sum): one pass over the row
+    auto add = [&](float x) {
       bad |= bad_input(x);
-      mx = fmaxf(mx, x);
-    }
-    mx = warp_max(mx);
-    float r;
-    if (kMax) {
-      r = mx;
+      if (kMax) {
+        mx = fmaxf(mx, x);
+      } else if (x > mx) {
+        sm = (mx == ninf()) ? 1.f : sm * fexp(mx - x) + 1.f;
+        mx = x;
+      } else if (x != ninf()) {
+        sm += fexp(x - mx);
+      }
+    };
+    if (vec4) {
+      const float4* r4 = reinterpret_cast<const float4*>(row);
+      int l4 = 0;
+      for (; l4 + 8 <= m / 4; l4 += 8) {
+        float4 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = __ldg(r4 + l4 + q);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          add(v[q].x);
+          add(v[q].y);
+          add(v[q].z);
+          add(v[q].w);
+        }
+      }
+      for (; l4 < m / 4; ++l4) {
+        const float4 v = __ldg(r4 + l4);
+        add(v.x);
+        add(v.y);
+        add(v.z);
+        add(v.w);
+      }
     } else {
-      float s = 0.f;
-      if (mx != ninf())
-        for (int l = lane; l < m; l += 32) s += fexp(row[l] - mx);
-      s = warp_sum(s);
-      r = (mx == ninf()) ? ninf() : mx + flog(s);
+      for (int l = 0; l < m; ++l) add(__ldg(row + l));
     }
-    if (lane == 0) fold[idx] = r;
+    fold[idx] = kMax ? mx : ((mx == ninf()) ? ninf() : mx + flog(sm));
   }
   if (bad) atomicOr(&badsh, 1);
   __syncthreads();
@@ -93,16 +124,22 @@ __global__ void __launch_bounds__(kThreads) tree_kernel(const float* __restrict_
     for (int i = warp; i <= n - w; i += kWarps) {
       const int j = i + w - 1;
       double r;
+      // each lane holds <= 4 split terms (n <= 128): read them once
+      double t[4];
+      double mloc = ninfd();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = i + lane + 32 * q;
+        t[q] = (k < j) ? ins[tri(i, k, n)] + ins[tri(k + 1, j, n)] : ninfd();
+        mloc = fmax(mloc, t[q]);
+      }
       if (kMax) {
-        double best = ninfd();
-        for (int k = i + lane; k < j; k += 32) best = fmax(best, ins[tri(i, k, n)] + ins[tri(k + 1, j, n)]);
-        r = warp_maxd(best);
+        r = warp_maxd(mloc);
       } else {
-        double mloc = ninfd();
-        for (int k = i + lane; k < j; k += 32) mloc = fmax(mloc, ins[tri(i, k, n)] + ins[tri(k + 1, j, n)]);
         float s = 0.f;
         if (mloc != ninfd())
-          for (int k = i + lane; k < j; k += 32) s += fexp((float)(ins[tri(i, k, n)] + ins[tri(k + 1, j, n)] - mloc));
+#pragma unroll
+          for (int q = 0; q < 4; ++q) s += (t[q] == ninfd()) ? 0.f : fexp((float)(t[q] - mloc));
         r = warp_lse_d(mloc, s);
       }
       if (lane == 0) {
@@ -203,22 +240,14 @@ __global__ void __launch_bounds__(kThreads) tree_kernel(const float* __restrict_
     for (int i = warp; i <= n - w; i += kWarps) {
       const int j = i + w - 1;
       const int nr = n - 1 - j;  // right-sibling parents (i, pj), pj in (j, n)
+      // each lane holds <= 4 parent terms (n <= 128): read them once
+      double tv[4];
       double mloc = ninfd();
-      for (int q = lane; q < nterms; q += 32) {
-        double t;
-        if (q < nr) {
-          const int pj = j + 1 + q;
-          t = out[tri(i, pj, n)] + (double)fold[tri(i, pj, n)] + ins[tri(j + 1, pj, n)];
-        } else {
-          const int pi = q - nr;
-          t = out[tri(pi, j, n)] + (double)fold[tri(pi, j, n)] + ins[tri(pi, i - 1, n)];
-        }
-        mloc = fmax(mloc, t);
-      }
-      float s = 0.f;
-      if (mloc != ninfd()) {
-        for (int q = lane; q < nterms; q += 32) {
-          double t;
+#pragma unroll
+      for (int r4 = 0; r4 < 4; ++r4) {
+        const int q = lane + 32 * r4;
+        double t = ninfd();
+        if (q < nterms) {
           if (q < nr) {
             const int pj = j + 1 + q;
             t = out[tri(i, pj, n)] + (double)fold[tri(i, pj, n)] + ins[tri(j + 1, pj, n)];
@@ -226,9 +255,14 @@ __global__ void __launch_bounds__(kThreads) tree_kernel(const float* __restrict_
             const int pi = q - nr;
             t = out[tri(pi, j, n)] + (double)fold[tri(pi, j, n)] + ins[tri(pi, i - 1, n)];
           }
-          s += fexp((float)(t - mloc));
         }
+        tv[r4] = t;
+        mloc = fmax(mloc, t);
       }
+      float s = 0.f;
+      if (mloc != ninfd())
+#pragma unroll
+        for (int r4 = 0; r4 < 4; ++r4) s += (tv[r4] == ninfd()) ? 0.f : fexp((float)(tv[r4] - mloc));
       const double r = warp_lse_d(mloc, s);
       if (lane == 0) out[tri(i, j, n)] = r;
     }
@@ -283,7 +317,7 @@ int tree_launch(const float* th, int64_t B, int n, int m, double* logz, float* m
 
 int tree_check(int64_t B, int n, int m) {
   if (B < 0 || n < 1 || m < 1) return SDB_ERR_ARG;
-  if (tree_smem(n) > 220 * 1024) return SDB_ERR_UNSUPPORTED;
+  if (n > 128 || tree_smem(n) > 220 * 1024) return SDB_ERR_UNSUPPORTED;  // <= 4 terms per lane
   return SDB_OK;
 }
 
