@@ -70,8 +70,9 @@ __device__ __forceinline__ float warp_lse_terms(const float (&t)[kQ]) {
 // become single MUFU ops.  Integer offsets are integers in log2 units.
 __global__ void __launch_bounds__(kThreads, 1) eisner_kernel(const float* __restrict__ adj_all, int n, int single,
                                                              double* __restrict__ logz, float* __restrict__ marg_all,
-                                                             int32_t* __restrict__ status) {
+                                                             int32_t* __restrict__ status, int only_retry) {
   extern __shared__ __align__(16) char smraw[];
+  if (only_retry && status[blockIdx.x] != 5) return;  // 5 = exp-space kernel gave up (kRetry)
   const int T = n * (n + 1) / 2;
   Charts c;
   {
@@ -318,6 +319,236 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_kernel(const float* __rest
   }
 }
 
+// ------------------------------------------------------------ exp space
+// eisner_lin_kernel -- the same inside / pull-form outside in LINEAR space:
+// every chart entry of width w is stored as exp(X) * 2^(-c w) for one slope
+// c per instance (a tree has exactly n arcs, so scaling every arc weight by
+// 2^-c scales each width-w product uniformly: W[h][d] = 2^(theta log2 e - c)).
+// Every split term is then one FFMA (the log-space kernel needs ~20
+// instructions: two-pass max / exp2 / offsets).  The slope adapts: when a
+// width's largest entry leaves [2^-24, 2^24], c absorbs its per-width growth
+// and all stored widths are rescaled by 2^(-delta width) (exact bookkeeping).
+// Instances whose values overflow or underflow anyway (huge |theta| ranges,
+// adversarial -inf patterns) report status 5 and are recomputed by the
+// log-space eisner_kernel.  Adjoints G are pre-divided by E_Z, so an arc
+// marginal is G_ir * E_ir.
+constexpr int32_t kRetry = 5;
+
+__device__ __forceinline__ float warp_dot_sum(float s) { return warp_sum(s); }
+
+__global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __restrict__ adj_all, int n, int single,
+                                                                 double* __restrict__ logz, float* __restrict__ marg_all,
+                                                                 int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) char smraw[];
+  const int T = n * (n + 1) / 2;
+  float *cr, *cl, *ir, *il, *gcr, *gcl, *gfo;
+  {
+    float* p = (float*)smraw;
+    cr = p; p += T; cl = p; p += T; ir = p; p += T; il = p; p += T;
+    gcr = p; p += T; gcl = p; p += T; gfo = p; p += T;
+  }
+  __shared__ float wred[kWarps], wred2[kWarps];
+  __shared__ float cslope, zv;
+  __shared__ int badsh, failsh;
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int N1 = n + 1;
+  const float* th = adj_all + (size_t)b * N1 * N1;
+  // chart accessors: width-0 complete spans are 1
+  auto CR = [&](int a, int bb) { return a == bb ? 1.f : cr[pk(a, bb, n)]; };
+  auto CL = [&](int a, int bb) { return a == bb ? 1.f : cl[pk(a, bb, n)]; };
+  if (tid == 0) { badsh = 0; failsh = 0; }
+  // slope: mean finite theta (log2 units) over the dependents' incoming arcs
+  {
+    int bad = 0;
+    float sum = 0.f, cnt = 0.f;
+    for (int e = tid; e < N1 * N1; e += kThreads) {
+      const float x = th[e];
+      bad |= bad_input(x);
+      const int d = e % N1;
+      if (d >= 1 && x != ninf() && x == x) { sum += x * SDB_LOG2E; cnt += 1.f; }
+    }
+    if (bad) atomicOr(&badsh, 1);
+    sum = warp_sum(sum);
+    cnt = warp_sum(cnt);
+    if (lane == 0) { wred[warp] = sum; wred2[warp] = cnt; }
+    __syncthreads();
+    if (tid == 0) {
+      float S = 0.f, C = 0.f;
+      for (int q = 0; q < kWarps; ++q) { S += wred[q]; C += wred2[q]; }
+      cslope = (C > 0.f) ? rintf(S / C) : 0.f;
+    }
+    __syncthreads();
+  }
+  if (badsh) {  // status INVALID, zero marginals (as eisner_kernel)
+    if (tid == 0) { status[b] = SDB_ST_INVALID; logz[b] = ninfd(); }
+    if (marg_all) for (int e = tid; e < N1 * N1; e += kThreads) marg_all[(size_t)b * N1 * N1 + e] = 0.f;
+    return;
+  }
+  auto W = [&](int h, int d) { return ex2(__ldg(th + h * N1 + d) * SDB_LOG2E - cslope); };
+
+  // ================================================================ inside
+  for (int w = 1; w <= n; ++w) {
+    float lmax = 0.f;
+    // two spans per warp iteration: their reductions are independent (ILP)
+    for (int i0 = warp; i0 + w <= n; i0 += 2 * kWarps) {
+      const int iA = i0, iB = i0 + kWarps;
+      const bool hasB = iB + w <= n;
+      float sA = 0.f, sB = 0.f;
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        const int kA = iA + lane + 32 * q, kB = iB + lane + 32 * q;
+        if (kA < iA + w) sA = fmaf(CR(iA, kA), CL(kA + 1, iA + w), sA);
+        if (hasB && kB < iB + w) sB = fmaf(CR(iB, kB), CL(kB + 1, iB + w), sB);
+      }
+      const float FA = warp_dot_sum(sA), FB = warp_dot_sum(sB);
+      const float virA = W(iA, iA + w) * FA, vilA = W(iA + w, iA) * FA;
+      const float virB = hasB ? W(iB, iB + w) * FB : 0.f, vilB = hasB ? W(iB + w, iB) * FB : 0.f;
+      if (lane == 0) {
+        ir[pk(iA, iA + w, n)] = virA; il[pk(iA, iA + w, n)] = vilA;
+        if (hasB) { ir[pk(iB, iB + w, n)] = virB; il[pk(iB, iB + w, n)] = vilB; }
+      }
+      __syncwarp();
+      float srA = 0.f, slA = 0.f, srB = 0.f, slB = 0.f;
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        const int o = lane + 32 * q;
+        if (o + 1 <= w) srA = fmaf(ir[pk(iA, iA + 1 + o, n)], CR(iA + 1 + o, iA + w), srA);
+        if (o < w) slA = fmaf(CL(iA, iA + o), il[pk(iA + o, iA + w, n)], slA);
+        if (hasB) {
+          if (o + 1 <= w) srB = fmaf(ir[pk(iB, iB + 1 + o, n)], CR(iB + 1 + o, iB + w), srB);
+          if (o < w) slB = fmaf(CL(iB, iB + o), il[pk(iB + o, iB + w, n)], slB);
+        }
+      }
+      const float vcrA = warp_dot_sum(srA), vclA = warp_dot_sum(slA);
+      const float vcrB = warp_dot_sum(srB), vclB = warp_dot_sum(slB);
+      if (lane == 0) {
+        cr[pk(iA, iA + w, n)] = vcrA; cl[pk(iA, iA + w, n)] = vclA;
+        if (hasB) { cr[pk(iB, iB + w, n)] = vcrB; cl[pk(iB, iB + w, n)] = vclB; }
+      }
+      lmax = fmaxf(lmax, fmaxf(fmaxf(virA, vilA), fmaxf(vcrA, vclA)));
+      lmax = fmaxf(lmax, fmaxf(fmaxf(virB, vilB), fmaxf(vcrB, vclB)));
+    }
+    if (lane == 0) wred[warp] = lmax;
+    __syncthreads();
+    float M = 0.f;
+#pragma unroll
+    for (int q = 0; q < kWarps; ++q) M = fmaxf(M, wred[q]);
+    if (!(M <= 3.0e38f)) {  // inf / NaN: give up on linear space
+      if (tid == 0) failsh = 1;
+      break;
+    }
+    if (M > 0.f && (M > 16777216.f || M < 5.9604645e-8f)) {
+      // absorb the growth: c += delta, every stored width v scaled by 2^(-delta v)
+      const float delta = lg2(M) / (float)w;
+      for (int e = tid; e < T; e += kThreads) {
+        // decode width of packed (i, j): row i holds j = i+1..n
+        int i = 0, r = e;
+        while (r >= n - i) { r -= n - i; ++i; }
+        const float f = ex2(-delta * (float)(r + 1));
+        cr[e] *= f; cl[e] *= f; ir[e] *= f; il[e] *= f;
+      }
+      __syncthreads();
+      if (tid == 0) cslope += delta;
+    }
+    __syncthreads();
+  }
+  // Z (spanning.py:210-221)
+  if (tid == 0 && !failsh) {
+    float ez;
+    if (!single) {
+      ez = CR(0, n);
+    } else {
+      ez = 0.f;
+      for (int cc = 1; cc <= n; ++cc) ez += W(0, cc) * CL(1, cc) * CR(cc, n);
+    }
+    zv = ez;
+    // zero can be a true -inf (vacuous) or an underflow: let the log-space kernel decide
+    if (!(ez > 0.f) || !(ez <= 3.0e38f)) failsh = 1;
+  }
+  __syncthreads();
+  if (failsh) {
+    if (tid == 0) status[b] = kRetry;
+    return;
+  }
+  const float EZ = zv;
+  if (tid == 0) {
+    status[b] = SDB_ST_OK;
+    logz[b] = ((double)lg2(EZ) + (double)cslope * (double)n) * (double)SDB_LN2;
+  }
+  if (!marg_all) return;
+  float* mg = marg_all + (size_t)b * N1 * N1;
+  const float rz = 1.f / EZ;
+  for (int e = tid; e < N1; e += kThreads) mg[e * N1 + e] = 0.f;
+  if (single)
+    for (int cc = 1 + tid; cc <= n; cc += kThreads)
+      mg[cc] = fminf(fmaxf(W(0, cc) * CL(1, cc) * CR(cc, n) * rz, 0.f), 1.f);
+
+  // =============================================================== outside
+  for (int w = n; w >= 1; --w) {
+    float lmax = 0.f;
+    for (int a = warp; a + w <= n; a += kWarps) {
+      const int bb = a + w;
+      const int n1 = n - bb, n2 = a;
+      float sA = 0.f, sB = 0.f;
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        const int x = lane + 32 * q;
+        if (x < n1) {
+          const int j = bb + 1 + x;
+          sA = fmaf(gfo[pk(a, j, n)], CL(bb + 1, j), sA);   // split parents (a, j)
+          sB = fmaf(gcl[pk(a, j, n)], il[pk(bb, j, n)], sB);  // cl parents (a, j)
+        }
+        if (x < n2) {
+          const int i = x;
+          sA = fmaf(gcr[pk(i, bb, n)], ir[pk(i, a, n)], sA);  // cr parents (i, bb)
+          sB = fmaf(gfo[pk(i, bb, n)], CR(i, a - 1), sB);     // split parents (i, bb)
+        }
+      }
+      float vgcr = warp_dot_sum(sA), vgcl = warp_dot_sum(sB);
+      if (lane == 0) {
+        if (!single) {
+          if (a == 0 && bb == n) vgcr = rz;
+        } else {
+          if (bb == n && a >= 1) vgcr += W(0, a) * CL(1, a) * rz;
+          if (a == 1) vgcl += W(0, bb) * CR(bb, n) * rz;
+        }
+        gcr[pk(a, bb, n)] = vgcr;
+        gcl[pk(a, bb, n)] = vgcl;
+      }
+      __syncwarp();
+      float tr = 0.f, tl = 0.f;
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        const int x = lane + 32 * q;
+        const int j = bb + x;
+        if (j <= n) tr = fmaf(gcr[pk(a, j, n)], CR(bb, j), tr);
+        if (x <= a) tl = fmaf(gcl[pk(x, bb, n)], CL(x, a), tl);
+      }
+      const float gir = warp_dot_sum(tr), gil = warp_dot_sum(tl);
+      if (lane == 0) {
+        const int e = pk(a, bb, n);
+        const float vf = gil * W(bb, a) + gir * W(a, bb);
+        gfo[e] = vf;
+        const float pr = gir * ir[e], pl = gil * il[e];
+        if (!(single && a == 0)) mg[a * N1 + bb] = fminf(fmaxf(pr, 0.f), 1.f);
+        mg[bb * N1 + a] = fminf(fmaxf(pl, 0.f), 1.f);
+        lmax = fmaxf(lmax, fmaxf(fmaxf(vgcr, vgcl), vf));
+      }
+    }
+    lmax = warp_max(lmax);
+    if (lane == 0) wred[warp] = lmax;
+    __syncthreads();
+    float M = 0.f;
+#pragma unroll
+    for (int q = 0; q < kWarps; ++q) M = fmaxf(M, wred[q]);
+    if (!(M <= 3.0e38f)) {
+      if (tid == 0) status[b] = kRetry;
+      return;
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- Kuhlmann
 // fp64 max-plus over positions 0..n+1 (n+1 = end marker, heads nothing).
 // table packed strict-upper over N2 = n+2 positions; back = (k, head).
@@ -456,10 +687,16 @@ extern "C" int sdb_eisner(const float* adjacency, int64_t B, int32_t n, int32_t 
   if (!adjacency || !logz || !status) return SDB_ERR_ARG;
   if (B == 0) return SDB_OK;
   const size_t smem = eisner_smem(n);
-  if (cudaFuncSetAttribute(eisner_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+  const size_t smem_lin = (size_t)7 * (n * (n + 1) / 2) * 4;  // the seven charts only
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaFuncSetAttribute(eisner_lin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_lin) !=
+          cudaSuccess ||
+      cudaFuncSetAttribute(eisner_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return SDB_ERR_CUDA;
-  eisner_kernel<<<(unsigned)B, kThreads, smem, (cudaStream_t)stream>>>(adjacency, n, single_root ? 1 : 0, logz, marg,
-                                                                       status);
+  // exp-space first; the log-space kernel redoes only the instances it flagged
+  eisner_lin_kernel<<<(unsigned)B, kThreads, smem_lin, s>>>(adjacency, n, single_root ? 1 : 0, logz, marg, status);
+  SDB_CHECK_LAUNCH();
+  eisner_kernel<<<(unsigned)B, kThreads, smem, s>>>(adjacency, n, single_root ? 1 : 0, logz, marg, status, 1);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
 }
