@@ -98,3 +98,19 @@ def test_cle_argmax_vs_oracle(single):
     heads, st = K.cle(dev(z), single)
     for b in range(4):
         np.testing.assert_array_equal(heads[b].cpu().numpy(), O.cle_heads(z[b], single))
+
+
+@pytest.mark.parametrize("single", [False, True])
+def test_eisner_exp_space_fallback(single):
+    """Instances whose linear-space charts over/underflow (huge |theta|) are
+    recomputed by the log-space kernel; mixed batch with normal instances."""
+    need_gpu()
+    adj = batch_spanning(3200, 4, 40)
+    adj[1] *= 80.0   # ~e^{+-250} per arc: linear space must give up
+    adj[3][adj[3] > 0] *= 50.0
+    logz, marg, st = K.eisner(dev(adj), single)
+    assert (st.cpu().numpy() == 0).all()
+    for b in range(4):
+        z, mg = O.eisner_marginals(adj[b], single)
+        assert abs(logz[b].item() - z) <= RTOL * abs(z) + 1e-6
+        np.testing.assert_allclose(marg[b].cpu().numpy(), mg, rtol=RTOL, atol=2e-6)
