@@ -57,7 +57,7 @@ CONFIGS = {
     "c3": dict(workload="SpanningTreeCRF non-projective (Matrix-Tree, multi-root)", B=512, shape=dict(n=128),
                work=4_194_304, bound="fp32", argmax=False, kernel="mtt_kernel<true>"),
     "c4": dict(workload="SpanningTreeCRF projective (Eisner, multi-root) + Kuhlmann argmax", B=256,
-               shape=dict(n=128), work=2_504_320, bound="mufu", argmax=True, kernel="eisner_kernel"),
+               shape=dict(n=128), work=2_504_320, bound="mufu", argmax=True, kernel="eisner_lin_kernel"),
     "c5a": dict(workload="TreeCRF (CKY)", B=128, shape=dict(n=64, m=32), work=790_532, bound="hbm",
                 argmax=False, kernel="tree_kernel<1>"),
     "c5b": dict(workload="PCFG (CKY, NT=32, PT=32)", B=128, shape=dict(n=64, NT=32, PT=32),
