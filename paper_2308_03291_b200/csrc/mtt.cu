@@ -38,13 +38,14 @@ struct MttSmem {
   int* used;      // [kN]
 };
 
+// No shared copy of the adjacency (it is re-read from global/L2 where needed):
+// ~70 KB of shared memory and <= 64 registers let TWO instances share an SM.
 size_t mtt_smem(int n) {
-  return (size_t)(n + 1) * (n + 1) * 4 + (size_t)kN * kN * 4 + (size_t)kN * 4 * 3 + (size_t)4 * kN * 4 +
-         (size_t)kN * 8 + 256;
+  return (size_t)kN * kN * 4 + (size_t)kN * 4 * 3 + (size_t)4 * kN * 4 + (size_t)kN * 8 + 256;
 }
 
 template <bool kMarg>
-__global__ void __launch_bounds__(kThreads, 1) mtt_kernel(const float* __restrict__ adj_all, int n, int single,
+__global__ void __launch_bounds__(kThreads, 2) mtt_kernel(const float* __restrict__ adj_all, int n, int single,
                                                           double* __restrict__ logz, float* __restrict__ marg_all,
                                                           int32_t* __restrict__ status) {
   extern __shared__ __align__(16) char smraw[];
@@ -59,22 +60,19 @@ __global__ void __launch_bounds__(kThreads, 1) mtt_kernel(const float* __restric
     sm.colbuf = (float*)p; p += 2 * kN * 4;
     sm.perm = (int*)p; p += kN * 4;
     sm.used = (int*)p; p += kN * 4;
-    sm.adj = (float*)p;
   }
   __shared__ int flag_bad, flag_vac, piv_row;
   __shared__ float piv_val;
-  __shared__ double logdet;
+  __shared__ double logdet, detm;  // |det| = detm * 2^dete, logged once at the end
+  __shared__ int dete;
   __shared__ int negs;
 
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int N1 = n + 1;
   const float* A = adj_all + (size_t)b * N1 * N1;
-  if (tid == 0) { flag_bad = 0; flag_vac = 0; logdet = 0.0; negs = 0; }
-  for (int e = tid; e < N1 * N1; e += kThreads) {
-    const float x = A[e];
-    if (bad_input(x)) flag_bad = 1;
-    sm.adj[e] = x;
-  }
+  if (tid == 0) { flag_bad = 0; flag_vac = 0; logdet = 0.0; detm = 1.0; dete = 0; negs = 0; }
+  for (int e = tid; e < N1 * N1; e += kThreads)
+    if (bad_input(__ldg(A + e))) flag_bad = 1;
   for (int e = tid; e < kN; e += kThreads) { sm.used[e] = 0; sm.rowmag[e] = 0.f; }
   __syncthreads();
   // column shifts and diagonal (spanning.py:90-120); thread d handles dependent d+1
@@ -82,12 +80,12 @@ __global__ void __launch_bounds__(kThreads, 1) mtt_kernel(const float* __restric
     const int d = tid, dep = d + 1;
     float mx = ninf();
     for (int h = 0; h <= n; ++h)
-      if (h != dep) mx = fmaxf(mx, sm.adj[h * N1 + dep]);
+      if (h != dep) mx = fmaxf(mx, __ldg(A + h * N1 + dep));
     if (mx == ninf()) flag_vac = 1;
     float s = 0.f;
     if (mx != ninf())
       for (int h = single ? 1 : 0; h <= n; ++h)
-        if (h != dep) s += fexp(sm.adj[h * N1 + dep] - mx);
+        if (h != dep) s += fexp(__ldg(A + h * N1 + dep) - mx);
     sm.shift[d] = mx;
     sm.diag[d] = s;
   }
@@ -114,11 +112,11 @@ __global__ void __launch_bounds__(kThreads, 1) mtt_kernel(const float* __restric
       if (r >= n || c >= n) {
         v = (r == c) ? 1.f : 0.f;  // identity padding
       } else if (single && r == 0) {
-        v = fexp(sm.adj[c + 1] - sm.shift[c]);  // row 0 <- root weights (Koo et al.)
+        v = fexp(__ldg(A + c + 1) - sm.shift[c]);  // row 0 <- root weights (Koo et al.)
       } else if (r == c) {
         v = sm.diag[c];
       } else {
-        v = -fexp(sm.adj[(r + 1) * N1 + c + 1] - sm.shift[c]);
+        v = -fexp(__ldg(A + (r + 1) * N1 + c + 1) - sm.shift[c]);
       }
       a[ii][jj] = v;
     }
@@ -183,7 +181,11 @@ __global__ void __launch_bounds__(kThreads, 1) mtt_kernel(const float* __restric
       const float mag = fabsf(piv);
       if (!(mag > 1e-12f * fmaxf(sm.rowmag[p], 1e-30f))) singular = true, flag_vac = 1;
       if (piv < 0.f) negs++;
-      logdet += (double)log((double)mag);
+      // running product (exact fp64 scaling; one log at the end keeps the
+      // per-step critical path free of a software fp64 log)
+      int ex;
+      detm = frexp(detm * (double)mag, &ex);
+      dete += ex;
     }
     const float inv_piv = 1.f / piv;
     float cv[4];
@@ -219,6 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1) mtt_kernel(const float* __restric
       parity ^= (len + 1) & 1;  // a cycle of length L has L-1 transpositions
     }
     const int sgn = ((negs + parity) & 1) ? -1 : 1;
+    logdet = log(detm) + (double)dete * 0.6931471805599453;
     double ssum = 0.0;
     for (int d = 0; d < n; ++d) ssum += (double)sm.shift[d];
     const bool vac = flag_vac || sgn <= 0;
@@ -246,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1) mtt_kernel(const float* __restric
     float v = 0.f;
     if (!vac && dep >= 1 && h != dep) {
       const int d = dep - 1;
-      const float w = fexp(sm.adj[e] - sm.shift[d]);
+      const float w = fexp(__ldg(A + e) - sm.shift[d]);
       const float idd = sm.inv[d * kN + d];
       if (single) {
         if (h == 0) v = w * sm.inv[d * kN + 0];
