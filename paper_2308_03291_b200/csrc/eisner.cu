@@ -560,7 +560,7 @@ size_t kuhl_smem(int n) {
 
 __device__ __forceinline__ int pk2(int i, int j, int N) { return i * (N - 1) - (i * (i - 1)) / 2 + (j - i - 1); }
 
-__global__ void __launch_bounds__(kThreads, 1) kuhlmann_kernel(const float* __restrict__ adj_all, int n, int single,
+__global__ void __launch_bounds__(kThreads, 2) kuhlmann_kernel(const float* __restrict__ adj_all, int n, int single,
                                                                int32_t* __restrict__ heads_all,
                                                                double* __restrict__ score,
                                                                int32_t* __restrict__ status) {
