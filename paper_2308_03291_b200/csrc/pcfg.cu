@@ -35,6 +35,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kSpW = 8;    // spans per warp (register block); n <= 64
 constexpr int kBS = 4;     // B-slice width
 constexpr int kMaxN = 64;
+constexpr int kCP = 8;     // outside parents per shared-memory chunk
 
 struct PcfgWs {
   float* RE;    // [B][4][32 A][32 B][32 C]  exp(rules) per child-class block t, zero padded
@@ -44,7 +45,6 @@ struct PcfgWs {
   float* ou;    // [B][n][n][32]
   double* osc;  // [B][n][n]
   float* P;     // [B][n][3][32][32] per-width scratch (P in inside, Q in outside)
-  float* Q2;    // [B][n][3][32][32] transposed Q for left pushes
   float* P2;    // [B][n][3][32][32] inside pair products recomputed in the outside pass (mode 2)
   float* G;     // [B][4][32 A][32 B][32 C] expected rule counts before the exp(rule) factor (mode 2)
 };
@@ -60,7 +60,6 @@ PcfgWs pcfg_carve(void* base, int64_t B, int n, int NT, int PT, size_t* bytes, b
   w.ou = c.take<float>((size_t)B * n * n * 32);
   w.osc = c.take<double>((size_t)B * n * n);
   w.P = c.take<float>((size_t)B * n * 3 * 1024);
-  w.Q2 = c.take<float>((size_t)B * n * 3 * 1024);
   w.P2 = grad ? c.take<float>((size_t)B * n * 3 * 1024) : nullptr;
   w.G = grad ? c.take<float>((size_t)B * 4 * 32768) : nullptr;
   *bytes = c.used;
@@ -112,7 +111,6 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
   float* ou = ws.ou + (size_t)b * n * n * 32;
   double* osc = ws.osc + (size_t)b * n * n;
   float* Pw = ws.P + (size_t)b * n * 3 * 1024;
-  float* Q2 = ws.Q2 + (size_t)b * n * 3 * 1024;
   __shared__ int badsh;
   __shared__ double smax_s[kMaxN];
   __shared__ double smax2_s[kMaxN];
@@ -305,8 +303,10 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
     if (lane == 0) osc[n - 1] = (rm == ninf()) ? ninfd() : (double)rm;
   }
   __syncthreads();
-  float* REs = smf;                  // [3][32 A][kBS][32 C]
-  float* Os = smf + 3 * kBS * 1024;  // [kMaxN parents][32 A]
+  float* REs = smf;                                  // [2][3][32 A][kBS][32 C] (double buffer)
+  float* Os = REs + 2 * 3 * kBS * 1024;              // [kCP parents][32 A]
+  float* Qc = Os + kCP * 32;                         // [kCP][3][32 B][33 C] (padded rows: both push
+                                                     //  orientations read it conflict-free)
   for (int w = n; w >= 2; --w) {
     const int nsp = n - w + 1;
     const int nslot = (w == 2) ? 1 : 3;
@@ -340,95 +340,100 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
       }
       __syncthreads();
     }
-    // stage parent outside vectors (with the parent's own sticky folded into its scale)
-    for (int e = tid; e < nsp * 32; e += kThreads) {
-      const int s = e >> 5, A = e & 31;
-      Os[e] = (A < NT) ? ou[(size_t)(s * n + s + w - 1) * 32 + A] : 0.f;
-    }
-    // ---- Q-build: Q[s][slot][B][C] = sum_A o_s[A] R_t[A, B', C'] (lane = C)
-    for (int b0 = 0; b0 < 32; b0 += kBS) {
-      // REs[sl][A][bb][C]: 512 B contiguous per (sl, A)
-      for (int e = tid; e < nslot * 32 * 32; e += kThreads) {
-        const int sl = e >> 10, r = e & 1023;
-        const int A = r >> 5, q = r & 31;
-        const int t = slot_type(sl, w);
-        cpa16(REs + (sl * 32 + A) * kBS * 32 + 4 * q, RE + (((size_t)t * 32 + A) * 32 + b0) * 32 + 4 * q);
+    // Parents are processed in chunks of kCP: their Q matrices are built straight
+    // into shared memory (both orientations) and the pushes read them there --
+    // no global scratch round trip, each Q row is read from smem by every split
+    // of its parent.
+    for (int c0 = 0; c0 < nsp; c0 += kCP) {
+      const int cn = min(kCP, nsp - c0);
+      // stage the chunk's parent outside vectors
+      for (int e = tid; e < cn * 32; e += kThreads) {
+        const int pz = e >> 5, A = e & 31, s = c0 + pz;
+        Os[e] = (A < NT) ? ou[(size_t)(s * n + s + w - 1) * 32 + A] : 0.f;
       }
-      cpa_commit_wait();
-      __syncthreads();
-      for (int sl = 0; sl < nslot; ++sl) {
-        float q4[kSpW][kBS];
+      // ---- Q-build: Q[p][slot][B][C] = sum_A o_p[A] R_t[A, B', C'] (warp = parent, lane = C);
+      // R slices double-buffered through shared memory
+      auto stage = [&](int b0, float* dst) {
+        for (int e = tid; e < nslot * 32 * 32; e += kThreads) {
+          const int sl = e >> 10, r = e & 1023;
+          const int A = r >> 5, q = r & 31;
+          const int t = slot_type(sl, w);
+          cpa16(dst + (sl * 32 + A) * kBS * 32 + 4 * q, RE + (((size_t)t * 32 + A) * 32 + b0) * 32 + 4 * q);
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+      };
+      stage(0, REs);
+      for (int b0 = 0; b0 < 32; b0 += kBS) {
+        float* cur = REs + ((b0 / kBS) & 1) * 3 * kBS * 1024;
+        if (b0 + kBS < 32) {
+          stage(b0 + kBS, REs + (((b0 / kBS) + 1) & 1) * 3 * kBS * 1024);
+          asm volatile("cp.async.wait_group 1;\n" ::);
+        } else {
+          asm volatile("cp.async.wait_group 0;\n" ::);
+        }
+        __syncthreads();
+        if (warp < cn) {
+          for (int sl = 0; sl < nslot; ++sl) {
+            float q4[kBS];
 #pragma unroll
-        for (int q = 0; q < kSpW; ++q)
+            for (int bb = 0; bb < kBS; ++bb) q4[bb] = 0.f;
+            for (int A = 0; A < NT; ++A) {
+              const float o = Os[warp * 32 + A];
 #pragma unroll
-          for (int bb = 0; bb < kBS; ++bb) q4[q][bb] = 0.f;
-        for (int A = 0; A < NT; ++A) {
-          float rr[kBS];
-#pragma unroll
-          for (int bb = 0; bb < kBS; ++bb) rr[bb] = REs[((sl * 32 + A) * kBS + bb) * 32 + lane];
-#pragma unroll
-          for (int q = 0; q < kSpW; ++q) {
-            const int s = warp + q * kWarps;
-            if (s < nsp) {
-              const float o = Os[s * 32 + A];
-#pragma unroll
-              for (int bb = 0; bb < kBS; ++bb) q4[q][bb] = fmaf(o, rr[bb], q4[q][bb]);
+              for (int bb = 0; bb < kBS; ++bb) q4[bb] = fmaf(o, cur[((sl * 32 + A) * kBS + bb) * 32 + lane], q4[bb]);
             }
+#pragma unroll
+            for (int bb = 0; bb < kBS; ++bb) Qc[((warp * 3 + sl) * 32 + b0 + bb) * 33 + lane] = q4[bb];  // [B][C]
           }
         }
-#pragma unroll
-        for (int q = 0; q < kSpW; ++q) {
-          const int s = warp + q * kWarps;
-          if (s < nsp) {
-#pragma unroll
-            for (int bb = 0; bb < kBS; ++bb) {
-              Pw[(size_t)s * 3 * 1024 + sl * 1024 + (b0 + bb) * 32 + lane] = q4[q][bb];  // [B][C]
-              Q2[(size_t)s * 3 * 1024 + sl * 1024 + lane * 32 + (b0 + bb)] = q4[q][bb];  // [C][B]
-            }
-          }
-        }
+        __syncthreads();
       }
-      __syncthreads();
-    }
-    // ---- pushes; parent scale = osc + sticky (constituency.py:303)
-    for (int side = 0; side < 2; ++side) {
-      for (int s = warp; s < nsp; s += kWarps) {
-        const int i = s, j = i + w - 1;
-        const double ps = osc[i * n + j] + (double)STK(i, j);
-        if (ps == ninfd()) continue;
-        for (int k = i; k < j; ++k) {
-          const int sl = (w == 2) ? 0 : (k == i ? 1 : (k == j - 1 ? 2 : 0));
-          // side 0: left child (i,k) gets sum_C Q[B][C] u_(k+1)j[C];  side 1: right child (k+1,j)
-          const int si = side == 0 ? k + 1 : i, sj = side == 0 ? j : k;  // sibling span
-          const int ci = side == 0 ? i : k + 1, cj = side == 0 ? k : j;  // child span
-          const double sib = isc[si * n + sj];
-          if (sib == ninfd()) continue;
-          const float sv = iu[(size_t)(si * n + sj) * 32 + lane];
-          float g = 0.f;
-          const float* Qm = (side == 0 ? Q2 : Pw) + (size_t)s * 3 * 1024 + sl * 1024;  // [lane-major row][x]
+      // ---- pushes; parent scale = osc + sticky (constituency.py:303)
+      for (int side = 0; side < 2; ++side) {
+        for (int pz = warp; pz < cn; pz += kWarps) {
+          const int s = c0 + pz;
+          const int i = s, j = i + w - 1;
+          const double ps = osc[i * n + j] + (double)STK(i, j);
+          if (ps == ninfd()) continue;
+          for (int k = i; k < j; ++k) {
+            const int sl = (w == 2) ? 0 : (k == i ? 1 : (k == j - 1 ? 2 : 0));
+            // side 0: left child (i,k) gets sum_C Q[B][C] u_(k+1)j[C];  side 1: right child (k+1,j)
+            const int si = side == 0 ? k + 1 : i, sj = side == 0 ? j : k;  // sibling span
+            const int ci = side == 0 ? i : k + 1, cj = side == 0 ? k : j;  // child span
+            const double sib = isc[si * n + sj];
+            if (sib == ninfd()) continue;
+            const float sv = iu[(size_t)(si * n + sj) * 32 + lane];
+            // the child's current outside state, loaded before the dot product so
+            // the global latency overlaps it
+            const size_t co = (size_t)(ci * n + cj);
+            const double old = osc[co];
+            const float ou_old = ou[co * 32 + lane];
+            float g = 0.f;
+            const float* Qm = Qc + (size_t)(pz * 3 + sl) * 32 * 33;
+            if (side == 0) {  // lane = B: row B of Q
 #pragma unroll 8
-          for (int x = 0; x < 32; ++x) {
-            const float svx = __shfl_sync(0xffffffffu, sv, x);
-            g = fmaf(Qm[x * 32 + lane], svx, g);
+              for (int x = 0; x < 32; ++x) g = fmaf(Qm[lane * 33 + x], __shfl_sync(0xffffffffu, sv, x), g);
+            } else {          // lane = C: column C of Q
+#pragma unroll 8
+              for (int x = 0; x < 32; ++x) g = fmaf(Qm[x * 33 + lane], __shfl_sync(0xffffffffu, sv, x), g);
+            }
+            // normalise the contribution (keeps the child's vector O(1) at any depth)
+            const float gm = warp_max(g);
+            if (!(gm > 0.f)) continue;
+            g = g / gm;
+            // merge contribution (scale cs, vec g) into child
+            const double cs = ps + sib + (double)flog(gm);
+            const double M = fmax(old, cs);
+            const float a1 = (old == ninfd()) ? 0.f : fexp((float)(old - M));
+            const float a2 = fexp((float)(cs - M));
+            ou[co * 32 + lane] = ou_old * a1 + g * a2;
+            __syncwarp();
+            if (lane == 0) osc[co] = M;
+            __syncwarp();
           }
-          // normalise the contribution (keeps the child's vector O(1) at any depth)
-          const float gm = warp_max(g);
-          if (!(gm > 0.f)) continue;
-          g = g / gm;
-          // merge contribution (scale cs, vec g) into child
-          const double cs = ps + sib + (double)flog(gm);
-          const size_t co = (size_t)(ci * n + cj);
-          const double old = osc[co];
-          const double M = fmax(old, cs);
-          const float a1 = (old == ninfd()) ? 0.f : fexp((float)(old - M));
-          const float a2 = fexp((float)(cs - M));
-          ou[co * 32 + lane] = ou[co * 32 + lane] * a1 + g * a2;
-          __syncwarp();
-          if (lane == 0) osc[co] = M;
-          __syncwarp();
         }
+        __syncthreads();
       }
-      __syncthreads();
     }
   }
   // ---- span marginals (constituency.py:334-338)
@@ -667,7 +672,9 @@ template <int kMode>
 int pcfg_launch(const float* root, const float* rules, const float* emissions, const float* sticky, int64_t B, int n,
                 int NT, int PT, PcfgWs ws, double* logz, float* span_marg, PcfgGradOut gout, int32_t* status,
                 cudaStream_t s) {
-  const size_t smem = (size_t)(3 * kBS * 1024 + kMaxN * 3 * kBS * 32 + (kMode == 2 ? kMaxN * 32 : 0)) * 4;
+  const size_t smem_in = (size_t)(3 * kBS * 1024 + kMaxN * 3 * kBS * 32 + (kMode == 2 ? kMaxN * 32 : 0)) * 4;
+  const size_t smem_out = (size_t)(2 * 3 * kBS * 1024 + kCP * 32 + kCP * 3 * 32 * 33) * 4;
+  const size_t smem = kMode == 0 ? smem_in : (smem_in > smem_out ? smem_in : smem_out);
   if (cudaFuncSetAttribute(pcfg_kernel<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return SDB_ERR_CUDA;
   pcfg_kernel<kMode><<<(unsigned)B, kThreads, smem, s>>>(root, rules, emissions, sticky, n, NT, PT, ws, logz,
