@@ -11,6 +11,6 @@ run nw fb nw_mitm
 run chain fb chain_lin
 run ctc fb ctc_kernel
 run mtt fb mtt_kernel
-run eisner fb eisner_kernel
+run eisner fb eisner_lin_kernel
 run tree fb tree_kernel
 run pcfg fb pcfg_kernel
