@@ -117,9 +117,11 @@ int sdb_ctc_viterbi(const float* frame_potentials, const int32_t* targets, int64
  *
  * sdb_tree_fb replaces _tree_charts/cky_log_partition/tree_marginals
  * (constituency.py:52-110): logz [B]; marg [B,n,n,m] nullable (0 for i > j
- * and unreachable spans).  No workspace (charts live in shared memory). */
+ * and unreachable spans).  Workspace: the label-folded span chart and the
+ * per-span marginal multipliers, 2 x B n(n+1)/2 fp32. */
+size_t sdb_tree_fb_workspace(int64_t B, int32_t n, int32_t m);
 int sdb_tree_fb(const float* span_potentials, int64_t B, int32_t n, int32_t m, double* logz, float* marg,
-                int32_t* status, void* stream);
+                int32_t* status, void* workspace, size_t ws_bytes, void* stream);
 
 /* sdb_tree_viterbi replaces cky_max_score/_tree_walk/tree_argmax
  * (constituency.py:72-133): labels [B,n,n] int32 = label of each span in the

@@ -35,7 +35,8 @@ SIGNATURES = {
     "sdb_ctc_fb": (ctypes.c_int, [_c_p, _c_p, _i64, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
     "sdb_ctc_viterbi_workspace": (_sz, [_i64, _i32, _i32, _i32]),
     "sdb_ctc_viterbi": (ctypes.c_int, [_c_p, _c_p, _i64, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
-    "sdb_tree_fb": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p]),
+    "sdb_tree_fb_workspace": (_sz, [_i64, _i32, _i32]),
+    "sdb_tree_fb": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
     "sdb_tree_viterbi": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p]),
     "sdb_mtt": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p]),
     "sdb_eisner": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p]),

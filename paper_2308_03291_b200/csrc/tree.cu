@@ -23,6 +23,7 @@ namespace {
 
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
+constexpr int32_t kRetry = 5;  // scaled-linear DP could not represent this instance
 
 __device__ __forceinline__ int tri(int i, int j, int n) { return i * n - (i * (i - 1)) / 2 + (j - i); }
 
@@ -47,7 +48,10 @@ template <int kMode>  // 0 logZ, 1 logZ+marginals, 2 max-plus argmax
 __global__ void __launch_bounds__(kThreads) tree_kernel(const float* __restrict__ th_all, int n, int m,
                                                          double* __restrict__ logz, float* __restrict__ marg_all,
                                                          int32_t* __restrict__ labels_all,
-                                                         double* __restrict__ score, int32_t* __restrict__ status) {
+                                                         double* __restrict__ score, int32_t* __restrict__ status,
+                                                         int only_retry) {
+  // fallback use: redo only the instances the scaled-linear path gave up on
+  if (only_retry && status[blockIdx.x] != kRetry) return;
   extern __shared__ __align__(16) char smraw[];
   const size_t T = (size_t)n * (n + 1) / 2;
   double* ins = (double*)smraw;
@@ -304,13 +308,361 @@ __global__ void __launch_bounds__(kThreads) tree_kernel(const float* __restrict_
   }
 }
 
+// ===========================================================================
+// Scaled-linear path for log_partition + marginals (the C5a hot path).
+//
+//   tree_fold_kernel  (HBM):     fold[b][i,j] = lse_l theta[b,i,j,l], a warp per
+//                                (b, i) row: the spans j = i..n-1 of one row are
+//                                contiguous, so the row streams with coalesced
+//                                16-byte loads, m/4 lanes per span.
+//   tree_lin_kernel   (latency): one CTA per instance; inside and outside over
+//                                F = exp(fold) 2^-e in LINEAR fp32 (every tree
+//                                over a width-w span has 2w-1 nodes, so the
+//                                per-node factor 2^-e scales each width
+//                                uniformly and cancels exactly in
+//                                outside*inside/Z); split sums are dot products
+//                                of two contiguous chart rows/columns (packed
+//                                row-major and column-major copies).  Writes
+//                                K[i,j] = log(O I / Z) - fold[i,j] per span.
+//   tree_emit_kernel  (HBM):     marg[b,i,j,l] = exp(K[i,j] + theta[b,i,j,l]),
+//                                zeros for i > j; a CTA per (b, i) row.
+// Instances whose linear charts leave [2^-110, 2^110] (or hold a -inf fold)
+// are flagged kRetry and recomputed by the log-space tree_kernel.
+// ===========================================================================
+
+constexpr int kFoldWarps = 8;
+constexpr int kEmitThreads = 256;
+constexpr float kLinHi = 1.2980742e33f;   // 2^110
+constexpr float kLinLo = 7.7037198e-34f;  // 2^-110
+
+__global__ void __launch_bounds__(kFoldWarps * 32) tree_fold_kernel(const float* __restrict__ th_all, int64_t B,
+                                                                    int n, int m, float* __restrict__ fold_all) {
+  const int64_t row = (int64_t)blockIdx.x * kFoldWarps + (threadIdx.x >> 5);
+  if (row >= B * n) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t b = row / n;
+  const int i = (int)(row - b * n);
+  const int T = n * (n + 1) / 2;
+  const float* src = th_all + ((size_t)row * n + i) * m;  // theta[b, i, i, 0]
+  float* dst = fold_all + (size_t)b * T + tri(i, i, n);
+  const int ns = n - i;
+  const int q = m >> 2;
+  if ((m & 3) == 0 && q <= 32 && (32 % q) == 0 && (((uintptr_t)src) & 15) == 0) {
+    // q lanes per span, 32/q spans per pass, 4 passes (loads) in flight per lane
+    const int spp = 32 / q;
+    const int sub = lane / q, r = lane - sub * q;
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    for (int s0 = 0; s0 < ns; s0 += 4 * spp) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int sp = s0 + u * spp + sub;
+        v[u] = (sp < ns) ? __ldg(s4 + (size_t)sp * q + r) : make_float4(ninf(), ninf(), ninf(), ninf());
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int sp = s0 + u * spp + sub;
+        int bad = bad_input(v[u].x) | bad_input(v[u].y) | bad_input(v[u].z) | bad_input(v[u].w);
+        float mx = fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w));
+        for (int o = q >> 1; o > 0; o >>= 1) {
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+          bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+        }
+        float s = 0.f;
+        if (mx != ninf()) s = fexp(v[u].x - mx) + fexp(v[u].y - mx) + fexp(v[u].z - mx) + fexp(v[u].w - mx);
+        for (int o = q >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (r == 0 && sp < ns)
+          dst[sp] = bad ? __int_as_float(0x7fc00000) : ((mx == ninf()) ? ninf() : mx + flog(s));
+      }
+    }
+  } else {
+    for (int sp = lane; sp < ns; sp += 32) {
+      const float* rw = src + (size_t)sp * m;
+      Lse acc;
+      int bad = 0;
+      for (int l = 0; l < m; ++l) {
+        const float x = __ldg(rw + l);
+        bad |= bad_input(x);
+        acc.add(x);
+      }
+      dst[sp] = bad ? __int_as_float(0x7fc00000) : acc.result();
+    }
+  }
+}
+
+
+// Charts: packed row-major (R: chart[i, i..n-1] at rs(i)) and packed
+// column-major (C: chart[0..j, j] at cs(j)) copies, so the split terms of a
+// span are contiguous in both operands.  A span of width w gets G = 2^LG lanes
+// (<= 8 terms per lane); lane r takes terms r, r+G, ..., so for a fixed term
+// the G lanes of a span read G consecutive words.  The step body is
+// instantiated per LG: term offsets are immediates, loads are predicated (no
+// branches), and a step costs ~50 instructions per warp.
+constexpr int kLinThreads = 256;
+
+__device__ __forceinline__ int rs(int i, int n) { return i * n - ((i * (i - 1)) >> 1); }  // == tri(i, i, n)
+__device__ __forceinline__ int cs(int j) { return (j * (j + 1)) >> 1; }
+
+// log2(lanes per span) for L terms: <= 8 terms per lane
+__device__ __forceinline__ int group_lg(int L) {
+  const int x = (L - 1) >> 3;
+  return x > 0 ? 32 - __clz(x) : 0;
+}
+
+struct LinCharts {
+  float *base, *fl, *Fr, *Ir, *Ic, *Pr, *Pc;
+  int zi;  // index of a shared zero word (masked operands read it)
+};
+
+template <int LG>
+__device__ __forceinline__ int inside_step(const LinCharts& c, int n, int w, int tid, int bad) {
+  constexpr int G = 1 << LG;
+  const int L = w - 1, nsp = n - w + 1, r = tid & (G - 1);
+  const int wfirst = (tid & ~31) >> LG;
+  for (int base = 0; base < nsp; base += kLinThreads >> LG) {
+    if (base + wfirst >= nsp) break;  // warp-uniform
+    const int i = base + (tid >> LG), j = i + w - 1;
+    const bool ok = i < nsp;
+    // operand indices relative to c.base; masked terms read the zero slot (no branches)
+    const int p = (int)(c.Ir - c.base) + rs(i, n) + r;  // I[i, i + t]
+    const int q = (int)(c.Ic - c.base) + cs(j) + i + 1 + r;  // I[i + 1 + t, j]
+    const int lim = ok ? L - r : 0;
+    float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const bool pr = u * G < lim;
+      const float x = c.base[pr ? p + u * G : c.zi], y = c.base[pr ? q + u * G : c.zi];
+      if (u & 1) a1 = fmaf(x, y, a1); else a0 = fmaf(x, y, a0);
+    }
+    float acc = a0 + a1;
+#pragma unroll
+    for (int o = G >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (ok && r == 0) {
+      const int t = rs(i, n) + w - 1;
+      const float v = acc * c.Fr[t];
+      bad |= !(v >= kLinLo && v <= kLinHi);
+      c.Ir[t] = v;
+      c.Ic[cs(j) + i] = v;
+    }
+  }
+  return bad;
+}
+
+template <int LG>
+__device__ __forceinline__ int outside_step(const LinCharts& c, int n, int w, int tid, int bad, float lz2,
+                                            float* __restrict__ Kb) {
+  constexpr int G = 1 << LG;
+  const int L = n - w, nsp = n - w + 1, r = tid & (G - 1);
+  const int wfirst = (tid & ~31) >> LG;
+  for (int base = 0; base < nsp; base += kLinThreads >> LG) {
+    if (base + wfirst >= nsp) break;  // warp-uniform
+    const int i = base + (tid >> LG), j = i + w - 1, nr = n - 1 - j;
+    const bool ok = i < nsp;
+    // right-sibling parents (i, j+1+t), t < nr: P[i, j+1+t] (row i), I[j+1, j+1+t] (row j+1)
+    const int pa = (int)(c.Pr - c.base) + rs(i, n) + w + r;
+    const int pb = (int)(c.Ir - c.base) + rs(j + 1, n) + r;
+    // left-sibling parents (t - nr, j), t >= nr: P[t-nr, j] (column j), I[t-nr, i-1] (column i-1)
+    const int qa = (int)(c.Pc - c.base) + cs(j) - nr + r;
+    const int qb = (int)(c.Ic - c.base) + cs(i - 1) - nr + r;
+    const int lim = ok ? L - r : 0, rlim = nr - r;
+    float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const bool pr = u * G < lim, right = u * G < rlim;
+      const int xa = pr ? (right ? pa : qa) + u * G : c.zi;
+      const int xb = pr ? (right ? pb : qb) + u * G : c.zi;
+      const float x = c.base[xa], y = c.base[xb];
+      if (u & 1) a1 = fmaf(x, y, a1); else a0 = fmaf(x, y, a0);
+    }
+    float acc = a0 + a1;
+#pragma unroll
+    for (int o = G >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (ok && r == 0) {
+      const int t = rs(i, n) + w - 1;
+      bad |= !(acc >= kLinLo && acc <= kLinHi);
+      const float pv = acc * c.Fr[t];
+      c.Pr[t] = pv;
+      c.Pc[cs(j) + i] = pv;
+      Kb[t] = (lg2(acc) + lg2(c.Ir[t]) - lz2) * SDB_LN2 - c.fl[t];
+    }
+  }
+  return bad;
+}
+
+template <bool kMarg>
+__global__ void __launch_bounds__(kLinThreads) tree_lin_kernel(const float* __restrict__ fold_all, int n,
+                                                              double* __restrict__ logz, float* __restrict__ K_all,
+                                                              int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) float sml[];
+  const int T = n * (n + 1) / 2;
+  LinCharts c;
+  c.base = sml;
+  c.zi = 6 * T;
+  c.fl = sml;         // fold (log), row-major
+  c.Fr = c.fl + T;    // F' = exp(fold) 2^-e, row-major
+  c.Ir = c.Fr + T;    // inside, row-major
+  c.Ic = c.Ir + T;    // inside, column-major
+  c.Pr = c.Ic + T;    // outside * F', row-major
+  c.Pc = c.Pr + T;    // outside * F', column-major
+  __shared__ float red[2][kLinThreads / 32];
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // ---- load fold; NaN -> invalid, -inf -> retry (the log-space kernel handles
+  // -inf structure exactly)
+  const float* fsrc = fold_all + (size_t)b * T;
+  float mx = ninf();
+  int flg = 0;
+  if (tid == 0) sml[c.zi] = 0.f;
+  for (int t0 = 0; t0 < T; t0 += kLinThreads * 4) {
+    float v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = t0 + kLinThreads * u + tid;
+      v[u] = (t < T) ? fsrc[t] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = t0 + kLinThreads * u + tid;
+      if (t < T) {
+        const float f = v[u];
+        c.fl[t] = f;
+        if (f != f) flg |= 1;
+        else if (f == ninf()) flg |= 2;
+        else mx = fmaxf(mx, f);
+      }
+    }
+  }
+  mx = warp_max(mx);
+  if (lane == 0) red[0][warp] = mx;
+  flg = (__syncthreads_or(flg & 1) ? 1 : 0) | (__syncthreads_or(flg & 2) ? 2 : 0);
+  if (flg) {
+    if (tid == 0) {
+      status[b] = (flg & 1) ? SDB_ST_INVALID : kRetry;
+      logz[b] = (flg & 1) ? __longlong_as_double(0x7ff8000000000000ULL) : ninfd();
+    }
+    return;
+  }
+  mx = red[0][0];
+#pragma unroll
+  for (int k = 1; k < kLinThreads / 32; ++k) mx = fmaxf(mx, red[0][k]);
+  float s = 0.f;
+  for (int t = tid; t < T; t += kLinThreads) s += fexp(c.fl[t] - mx);
+  s = warp_sum(s);
+  if (lane == 0) red[1][warp] = s;
+  __syncthreads();
+  float st = 0.f;
+#pragma unroll
+  for (int k = 0; k < kLinThreads / 32; ++k) st += red[1][k];
+  // per-node scale: twice the mean factor (Catalan growth ~4^w over 2w-1 nodes)
+  const float e = mx * SDB_LOG2E + lg2(st / (float)T) + 1.f;
+  int bad = 0;
+  for (int t = tid; t < T; t += kLinThreads) {
+    const float f = ex2(fmaf(c.fl[t], SDB_LOG2E, -e));
+    bad |= !(f >= kLinLo && f <= kLinHi);
+    c.Fr[t] = f;
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += kLinThreads) {
+    const float f = c.Fr[rs(i, n)];
+    c.Ir[rs(i, n)] = f;
+    c.Ic[cs(i) + i] = f;
+  }
+  // ---- inside (constituency.py:57-63): I[i,j] = F'[i,j] sum_k I[i,k] I[k+1,j]
+  for (int w = 2; w <= n; ++w) {
+    __syncthreads();
+    switch (group_lg(w - 1)) {
+      case 0: bad = inside_step<0>(c, n, w, tid, bad); break;
+      case 1: bad = inside_step<1>(c, n, w, tid, bad); break;
+      case 2: bad = inside_step<2>(c, n, w, tid, bad); break;
+      case 3: bad = inside_step<3>(c, n, w, tid, bad); break;
+      default: bad = inside_step<4>(c, n, w, tid, bad); break;
+    }
+  }
+  bad = __syncthreads_or(bad);
+  const float Zs = c.Ir[rs(0, n) + n - 1];
+  if (bad) {
+    if (tid == 0) status[b] = kRetry;
+    return;
+  }
+  if (tid == 0) logz[b] = log((double)Zs) + (double)e * (double)(2 * n - 1) * 0.6931471805599453;
+  if (!kMarg) {
+    if (tid == 0) status[b] = SDB_ST_OK;
+    return;
+  }
+  // ---- outside (constituency.py:84-99) over P = O' F'; K = log(O' I' / Z') - fold
+  float* Kb = K_all + (size_t)b * T;  // row-major packed (read by tree_emit_kernel)
+  const float lz2 = lg2(Zs);
+  if (tid == 0) {
+    const int t = n - 1;  // root (0, n-1)
+    c.Pr[t] = c.Fr[t];
+    c.Pc[cs(n - 1)] = c.Fr[t];
+    Kb[t] = -c.fl[t];  // O' I' / Z' = 1 at the root
+  }
+  for (int w = n - 1; w >= 1; --w) {
+    __syncthreads();
+    switch (group_lg(n - w)) {
+      case 0: bad = outside_step<0>(c, n, w, tid, bad, lz2, Kb); break;
+      case 1: bad = outside_step<1>(c, n, w, tid, bad, lz2, Kb); break;
+      case 2: bad = outside_step<2>(c, n, w, tid, bad, lz2, Kb); break;
+      case 3: bad = outside_step<3>(c, n, w, tid, bad, lz2, Kb); break;
+      default: bad = outside_step<4>(c, n, w, tid, bad, lz2, Kb); break;
+    }
+  }
+  bad = __syncthreads_or(bad);
+  if (tid == 0) status[b] = bad ? kRetry : SDB_ST_OK;
+}
+
+__global__ void __launch_bounds__(kEmitThreads) tree_emit_kernel(const float* __restrict__ th_all, int n, int m,
+                                                                 int qshift, const float* __restrict__ K_all,
+                                                                 const int32_t* __restrict__ status,
+                                                                 float* __restrict__ marg_all) {
+  const int64_t row = blockIdx.x;
+  const int64_t b = row / n;
+  const int i = (int)(row - b * n);
+  const int st = status[b];
+  if (st == kRetry) return;  // the log-space kernel writes this instance
+  const bool live = st == SDB_ST_OK;
+  const int T = n * (n + 1) / 2;
+  const float* Kr = K_all + (size_t)b * T + tri(i, i, n) - i;  // Kr[j] = K[i, j] for j >= i
+  const float* src = th_all + (size_t)row * n * m;
+  float* dst = marg_all + (size_t)row * n * m;
+  if (qshift >= 0) {
+    const int tot = n << qshift;
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    float4* d4 = reinterpret_cast<float4*>(dst);
+    for (int x = threadIdx.x; x < tot; x += kEmitThreads) {
+      const int j = x >> qshift;
+      float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (live && j >= i) {
+        const float k = Kr[j];
+        const float4 v = __ldg(s4 + x);
+        o.x = fexp(k + v.x); o.y = fexp(k + v.y); o.z = fexp(k + v.z); o.w = fexp(k + v.w);
+      }
+      d4[x] = o;
+    }
+  } else {
+    const int tot = n * m;
+    for (int x = threadIdx.x; x < tot; x += kEmitThreads) {
+      const int j = x / m;
+      dst[x] = (live && j >= i) ? fexp(Kr[j] + __ldg(src + x)) : 0.f;
+    }
+  }
+}
+
+size_t tree_ws(int64_t B, int n) {
+  Carve c(nullptr);
+  const size_t T = (size_t)n * (n + 1) / 2;
+  c.take<float>((size_t)B * T);
+  c.take<float>((size_t)B * T);
+  return c.used;
+}
+
 template <int kMode>
 int tree_launch(const float* th, int64_t B, int n, int m, double* logz, float* marg, int32_t* labels, double* score,
-                int32_t* status, cudaStream_t s) {
+                int32_t* status, cudaStream_t s, int only_retry = 0) {
   const size_t smem = tree_smem(n);
   if (cudaFuncSetAttribute(tree_kernel<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return SDB_ERR_CUDA;
-  tree_kernel<kMode><<<(unsigned)B, kThreads, smem, s>>>(th, n, m, logz, marg, labels, score, status);
+  tree_kernel<kMode><<<(unsigned)B, kThreads, smem, s>>>(th, n, m, logz, marg, labels, score, status, only_retry);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
 }
@@ -323,15 +675,48 @@ int tree_check(int64_t B, int n, int m) {
 
 }  // namespace
 
+extern "C" size_t sdb_tree_fb_workspace(int64_t B, int32_t n, int32_t m) {
+  (void)m;
+  return (B > 0 && n > 0) ? tree_ws(B, n) : 0;
+}
+
 extern "C" int sdb_tree_fb(const float* span_potentials, int64_t B, int32_t n, int32_t m, double* logz, float* marg,
-                           int32_t* status, void* stream) {
+                           int32_t* status, void* workspace, size_t ws_bytes, void* stream) {
   int rc = tree_check(B, n, m);
   if (rc) return rc;
   if (!span_potentials || !logz || !status) return SDB_ERR_ARG;
   if (B == 0) return SDB_OK;
+  if (!workspace || ws_bytes < tree_ws(B, n)) return SDB_ERR_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
-  if (marg) return tree_launch<1>(span_potentials, B, n, m, logz, marg, nullptr, nullptr, status, s);
-  return tree_launch<0>(span_potentials, B, n, m, logz, nullptr, nullptr, nullptr, status, s);
+  Carve c(workspace);
+  const size_t T = (size_t)n * (n + 1) / 2;
+  float* fold = c.take<float>((size_t)B * T);
+  float* K = c.take<float>((size_t)B * T);
+  const size_t smem_lin = (6 * T + 1) * sizeof(float);
+  if (cudaFuncSetAttribute(tree_lin_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_lin) !=
+          cudaSuccess ||
+      cudaFuncSetAttribute(tree_lin_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_lin) !=
+          cudaSuccess)
+    return SDB_ERR_CUDA;
+  const int64_t rows = B * n;
+  tree_fold_kernel<<<(unsigned)((rows + kFoldWarps - 1) / kFoldWarps), kFoldWarps * 32, 0, s>>>(span_potentials, B,
+                                                                                               n, m, fold);
+  SDB_CHECK_LAUNCH();
+  if (marg) {
+    tree_lin_kernel<true><<<(unsigned)B, kLinThreads, smem_lin, s>>>(fold, n, logz, K, status);
+    SDB_CHECK_LAUNCH();
+    int qshift = -1;
+    if ((m & 3) == 0 && (((uintptr_t)span_potentials | (uintptr_t)marg) & 15) == 0) {
+      const int q = m >> 2;
+      if ((q & (q - 1)) == 0) qshift = __builtin_ctz(q);
+    }
+    tree_emit_kernel<<<(unsigned)rows, kEmitThreads, 0, s>>>(span_potentials, n, m, qshift, K, status, marg);
+    SDB_CHECK_LAUNCH();
+    return tree_launch<1>(span_potentials, B, n, m, logz, marg, nullptr, nullptr, status, s, 1);
+  }
+  tree_lin_kernel<false><<<(unsigned)B, kLinThreads, smem_lin, s>>>(fold, n, logz, K, status);
+  SDB_CHECK_LAUNCH();
+  return tree_launch<0>(span_potentials, B, n, m, logz, nullptr, nullptr, nullptr, status, s, 1);
 }
 
 extern "C" int sdb_tree_viterbi(const float* span_potentials, int64_t B, int32_t n, int32_t m, int32_t* labels,

@@ -177,7 +177,9 @@ def tree_fb(span_potentials, marginals: bool = True):
     logz = torch.empty(B, dtype=torch.float64, device=dev)
     status = torch.empty(B, dtype=torch.int32, device=dev)
     marg = torch.empty_like(th) if marginals else None
-    rc = lib.sdb_tree_fb(ptr(th), B, n, m, ptr(logz), ptr(marg), ptr(status), stream_ptr(dev))
+    ws = workspace(lib.sdb_tree_fb_workspace(B, n, m), dev)
+    rc = lib.sdb_tree_fb(ptr(th), B, n, m, ptr(logz), ptr(marg), ptr(status), ptr(ws), ws.numel(),
+                         stream_ptr(dev))
     _lib.check(rc, "sdb_tree_fb")
     return logz, marg, status
 

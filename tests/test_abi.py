@@ -50,6 +50,7 @@ def test_workspace_queries_are_host_only():
     lib = _lib.load()
     assert lib.sdb_chain_fb_workspace(32, 128, 32) >= 2 * 32 * 128 * 32 * 4
     assert lib.sdb_chain_viterbi_workspace(32, 128, 32) > 0
+    assert lib.sdb_tree_fb_workspace(128, 64, 32) >= 2 * 128 * (64 * 65 // 2) * 4
 
 
 def test_null_arguments_rejected_without_device():

@@ -65,3 +65,22 @@ def test_tree_status():
     th[2, 1, 2, 0] = np.inf
     logz, marg, st = K.tree_fb(dev(th))
     assert st.cpu().tolist() == [0, 1, 2]
+
+
+def test_tree_linear_fallback_mixed_batch():
+    """Instances the scaled-linear charts cannot hold (huge / very uneven
+    potentials, -inf spans) are redone in log space; the rest of the batch
+    stays on the linear path.  Every instance must match the oracle."""
+    need_gpu()
+    th = batch_tree(4100, 5, 24, 8)
+    th[1] *= 300.0               # folds spread over hundreds of nats -> linear range exceeded
+    th[3, 2, 9, :] = NEG_INF     # one forbidden span: exact -inf structure
+    th[4, :, :, 0] += 60.0       # uniform shift: still linear-representable
+    logz, marg, st = K.tree_fb(dev(th))
+    lz0, _, st0 = K.tree_fb(dev(th), marginals=False)
+    assert (st.cpu().numpy() == 0).all() and (st0.cpu().numpy() == 0).all()
+    for b in range(th.shape[0]):
+        z, mg = O.tree_marginals(th[b])
+        assert abs(logz[b].item() - z) <= RTOL * abs(z)
+        assert abs(lz0[b].item() - z) <= RTOL * abs(z)
+        np.testing.assert_allclose(marg[b].cpu().numpy(), mg, rtol=RTOL, atol=ATOL)
