@@ -145,8 +145,7 @@ def step_fn(cfg, inputs):
 
     if cfg == "c1":
         def f():
-            lz, mi, mt, st = K.chain_fb(inputs[0], inputs[1], True)
-            tags, _, _ = K.chain_viterbi(inputs[0], inputs[1])
+            (lz, mi, mt, st), (tags, _, _) = K.chain_fb_viterbi(inputs[0], inputs[1], True)
             return lz, mi, mt, tags
         return f
     if cfg == "c2a":
@@ -184,7 +183,7 @@ def kernel_fn(cfg, inputs):
 
 
 def launches_per_step(cfg):
-    return {"c1": 3, "c2a": 1, "c2b": 1, "c3": 1, "c4": 3, "c5a": 1, "c5b": 1}[cfg]
+    return {"c1": 4, "c2a": 1, "c2b": 1, "c3": 1, "c4": 3, "c5a": 4, "c5b": 1}[cfg]
 
 
 # ------------------------------------------------------------------ clocks

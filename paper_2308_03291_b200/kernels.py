@@ -85,6 +85,44 @@ def chain_viterbi(init, trans):
     return tags, score, status
 
 
+_SIDE = {}
+
+
+def _side_stream(dev) -> torch.cuda.Stream:
+    s = _SIDE.get(dev.index)
+    if s is None:
+        s = _SIDE[dev.index] = torch.cuda.Stream(dev)
+    return s
+
+
+def _concurrent(dev, main, side, keep=()):
+    """Run `side()` on a side stream concurrently with `main()` on the current
+    stream (fork/join with stream waits).  Used where both halves of one
+    request are latency-bound launches with fewer CTAs than SMs, so they share
+    the GPU instead of queueing.  `keep` tensors are read by `side`."""
+    cur = torch.cuda.current_stream(dev)
+    st = _side_stream(dev)
+    st.wait_stream(cur)
+    with torch.cuda.stream(st):
+        rs = side()
+    rm = main()
+    cur.wait_stream(st)
+    for t in list(keep) + [x for x in rs if isinstance(x, torch.Tensor)]:
+        t.record_stream(st)
+        t.record_stream(cur)
+    return rm, rs
+
+
+def chain_fb_viterbi(init, trans, marginals: bool = True):
+    """log_partition + marginals (chain.py:64-95) AND argmax (chain.py:98-114)
+    in one call: the forward-backward cluster kernel on the current stream,
+    the Viterbi kernel concurrently on a side stream (B CTAs each).
+    -> ((logz, marg_init, marg_trans, status), (tags, score, status))."""
+    init, trans = f32(init, "init"), f32(trans, "transitions")
+    return _concurrent(init.device, lambda: chain_fb(init, trans, marginals), lambda: chain_viterbi(init, trans),
+                       keep=(init, trans))
+
+
 # ------------------------------------------------------------- alignment
 
 

@@ -98,3 +98,17 @@ def test_batch_map_matches_singles():
     zs = sd.batch_map(sd.log_partition, ds)
     for d, z in zip(ds, zs):
         assert abs(z - sd.log_partition(d)) < 1e-9
+
+
+def test_chain_fb_viterbi_concurrent():
+    """The fused request (forward-backward on the current stream, Viterbi on a
+    side stream) returns exactly what the two separate calls return."""
+    need_gpu()
+    init, tr = batch_chain(300, 32, 128, 32)
+    (lz, mi, mt, st), (tags, score, st2) = K.chain_fb_viterbi(dev(init), dev(tr))
+    lz1, mi1, mt1, _ = K.chain_fb(dev(init), dev(tr))
+    tags1, score1, _ = K.chain_viterbi(dev(init), dev(tr))
+    torch.cuda.synchronize()
+    assert torch.equal(lz, lz1) and torch.equal(mt, mt1) and torch.equal(mi, mi1)
+    assert torch.equal(tags, tags1) and torch.equal(score, score1)
+    assert (st == 0).all() and (st2 == 0).all()
