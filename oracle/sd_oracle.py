@@ -563,6 +563,48 @@ def pcfg_gradients(root, rules, emis, sticky=None):
     return z, {"root": g_root, "binary_rules": g_rules, "emissions": g_emis, "sticky": span}
 
 
+def pcfg_span_marginals(root, rules, emis, sticky=None):
+    """constituency.py:292-340 restricted to what `marginals()` returns for a
+    PCFG (dist.py:125-127: the span marginals `sticky` only), in the same log
+    semiring as the reference, with the splits of a span batched: the outside
+    message of a parent span is folded once through the rules,
+    Q[B,C] = lse_A(out[A] + rules[A,B,C]) (constituency.py:321-325 summed in
+    the other order -- exact in real arithmetic, float64 here), and each split
+    k then costs one [S,S] lse.  Used as the host-CPU baseline for C5b (the
+    per-split [NT,S,S] temporaries of pcfg_gradients make it ~20x slower);
+    checked against pcfg_gradients in tests/test_oracle_golden.py.
+    Returns (logZ, span marginals [n,n])."""
+    n, pt = emis.shape
+    nt = root.shape[0]
+    S = nt + pt
+    stk = np.zeros((n, n)) if sticky is None else sticky
+    ch = pcfg_inside_chart(root, rules, emis, stk)
+    z = lse_all(root + ch[0, n - 1, :nt])
+    if z == NEG_INF:
+        return z, None
+    out = np.full((n, n, S), NEG_INF)
+    out[0, n - 1, :nt] = root
+    for w in range(n, 1, -1):
+        for i in range(0, n - w + 1):
+            j = i + w - 1
+            o = out[i, j, :nt] + stk[i, j]
+            if np.all(np.isneginf(o)):
+                continue
+            qL = lse(o[:, None, None] + rules, 0)  # [S(B), S(C)]
+            L = ch[i, i:j]                          # [w-1, S] left children (i, k)
+            R = ch[i + 1 : j + 1, j]                # [w-1, S] right children (k+1, j)
+            toL = lse(qL[None, :, :] + R[:, None, :], 2)  # [w-1, B]
+            toR = lse(qL[None, :, :] + L[:, :, None], 1)  # [w-1, C]
+            out[i, i:j] = np.logaddexp(out[i, i:j], toL)
+            out[i + 1 : j + 1, j] = np.logaddexp(out[i + 1 : j + 1, j], toR)
+    span = np.zeros((n, n))
+    tot = lse(out + ch, 2)
+    for i in range(n):
+        for j in range(i, n):
+            span[i, j] = np.exp(tot[i, j] - z) if tot[i, j] > NEG_INF else 0.0
+    return z, span
+
+
 def pcfg_argmax(root, rules, emis, sticky=None):
     """constituency.py:343-371: max-plus chart then a top-down walk picking
     the first flat argmax of rules[a] + left + right over (k, B, C).

@@ -99,6 +99,10 @@ def test_oracle_pcfg(case):
         assert grads is None
         return
     case.check_marg("sticky", grads["sticky"], rtol=1e-9, atol=1e-12)
+    # the split-batched restatement used as the C5b CPU baseline
+    z2, span = O.pcfg_span_marginals(x["root"], x["binary_rules"], x["emissions"])
+    assert _close(z2, float(case.logz))
+    case.check_marg("sticky", span, rtol=1e-9, atol=1e-12)
     if "pmarg_binary_rules" in case:
         for k in ("root", "binary_rules", "emissions"):
             np.testing.assert_allclose(grads[k], case[f"pmarg_{k}"], rtol=1e-9, atol=1e-12)
@@ -154,3 +158,18 @@ def test_oracle_closed_forms():
     adj[:, 0] = NEG_INF
     np.fill_diagonal(adj, NEG_INF)
     assert math.isclose(O.mtt_log_partition(adj), math.log(16))
+
+
+def test_oracle_pcfg_span_marginals_sticky():
+    """pcfg_span_marginals == pcfg_gradients' span marginals with a sticky
+    (bracketing) mask, the masked-inside case (constituency.py:280-289)."""
+    from golden import builders as bld
+
+    r, ru, e = bld.pcfg(11, 8, 3, 4)
+    stk = np.zeros((8, 8))
+    stk[2, 5] = NEG_INF
+    stk[0, 3] = NEG_INF
+    z1, g = O.pcfg_gradients(r, ru, e, stk)
+    z2, span = O.pcfg_span_marginals(r, ru, e, stk)
+    assert _close(z1, z2)
+    np.testing.assert_allclose(span, g["sticky"], rtol=1e-9, atol=1e-12)
