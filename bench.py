@@ -154,8 +154,7 @@ def step_fn(cfg, inputs):
         return lambda: K.mtt(inputs[0], False, True)[:2]
     if cfg == "c4":
         def f():
-            lz, mg, st = K.eisner(inputs[0], False, True)
-            heads, _, _ = K.kuhlmann(inputs[0], False)
+            (lz, mg, st), (heads, _, _) = K.eisner_kuhlmann(inputs[0], False, True)
             return lz, mg, heads
         return f
     if cfg == "c5a":

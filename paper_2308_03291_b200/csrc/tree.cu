@@ -331,6 +331,12 @@ __global__ void __launch_bounds__(kThreads) tree_kernel(const float* __restrict_
 // ===========================================================================
 
 constexpr int kFoldWarps = 8;
+
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
 constexpr int kEmitThreads = 256;
 constexpr float kLinHi = 1.2980742e33f;   // 2^110
 constexpr float kLinLo = 7.7037198e-34f;  // 2^-110
@@ -346,34 +352,30 @@ __global__ void __launch_bounds__(kFoldWarps * 32) tree_fold_kernel(const float*
   const float* src = th_all + ((size_t)row * n + i) * m;  // theta[b, i, i, 0]
   float* dst = fold_all + (size_t)b * T + tri(i, i, n);
   const int ns = n - i;
-  const int q = m >> 2;
-  if ((m & 3) == 0 && q <= 32 && (32 % q) == 0 && (((uintptr_t)src) & 15) == 0) {
-    // q lanes per span, 32/q spans per pass, 4 passes (loads) in flight per lane
-    const int spp = 32 / q;
-    const int sub = lane / q, r = lane - sub * q;
-    const float4* s4 = reinterpret_cast<const float4*>(src);
-    for (int s0 = 0; s0 < ns; s0 += 4 * spp) {
-      float4 v[4];
+  if ((m & 3) == 0 && m <= 64 && (((uintptr_t)src) & 15) == 0) {
+    // lane per span: the lane's label row is m/4 16-byte loads, all issued
+    // before the (max, sum) pass; a warp-instruction touches 32 rows but every
+    // fetched sector is consumed
+    const int q = m >> 2;
+    for (int sp = lane; sp < ns; sp += 32) {
+      const float4* r4 = reinterpret_cast<const float4*>(src + (size_t)sp * m);
+      float4 v[16];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int sp = s0 + u * spp + sub;
-        v[u] = (sp < ns) ? __ldg(s4 + (size_t)sp * q + r) : make_float4(ninf(), ninf(), ninf(), ninf());
-      }
+      for (int u = 0; u < 16; ++u)
+        if (u < q) v[u] = __ldg(r4 + u);
+      // NaN-propagating max: NaN or +inf anywhere in the row -> !(mx < +inf)
+      float mx = ninf();
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int sp = s0 + u * spp + sub;
-        int bad = bad_input(v[u].x) | bad_input(v[u].y) | bad_input(v[u].z) | bad_input(v[u].w);
-        float mx = fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w));
-        for (int o = q >> 1; o > 0; o >>= 1) {
-          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-          bad |= __shfl_xor_sync(0xffffffffu, bad, o);
-        }
-        float s = 0.f;
-        if (mx != ninf()) s = fexp(v[u].x - mx) + fexp(v[u].y - mx) + fexp(v[u].z - mx) + fexp(v[u].w - mx);
-        for (int o = q >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (r == 0 && sp < ns)
-          dst[sp] = bad ? __int_as_float(0x7fc00000) : ((mx == ninf()) ? ninf() : mx + flog(s));
+      for (int u = 0; u < 16; ++u)
+        if (u < q) mx = fmax_nan(mx, fmax_nan(fmax_nan(v[u].x, v[u].y), fmax_nan(v[u].z, v[u].w)));
+      const int bad = !(mx < __int_as_float(0x7f800000));
+      float s = 0.f;
+      if (!bad && mx != ninf()) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (u < q) s += (fexp(v[u].x - mx) + fexp(v[u].y - mx)) + (fexp(v[u].z - mx) + fexp(v[u].w - mx));
       }
+      dst[sp] = bad ? __int_as_float(0x7fc00000) : ((mx == ninf()) ? ninf() : mx + flog(s));
     }
   } else {
     for (int sp = lane; sp < ns; sp += 32) {
@@ -629,15 +631,20 @@ __global__ void __launch_bounds__(kEmitThreads) tree_emit_kernel(const float* __
     const int tot = n << qshift;
     const float4* s4 = reinterpret_cast<const float4*>(src);
     float4* d4 = reinterpret_cast<float4*>(dst);
-    for (int x = threadIdx.x; x < tot; x += kEmitThreads) {
-      const int j = x >> qshift;
-      float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (live && j >= i) {
-        const float k = Kr[j];
-        const float4 v = __ldg(s4 + x);
-        o.x = fexp(k + v.x); o.y = fexp(k + v.y); o.z = fexp(k + v.z); o.w = fexp(k + v.w);
-      }
-      d4[x] = o;
+    // two float4 per thread per pass, both loads issued before the stores
+    for (int x0 = threadIdx.x; x0 < tot; x0 += 2 * kEmitThreads) {
+      const int x1 = x0 + kEmitThreads;
+      const int j0 = x0 >> qshift, j1 = x1 >> qshift;
+      const bool l0 = live && j0 >= i, l1 = live && x1 < tot && j1 >= i;
+      float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
+      float k0 = 0.f, k1 = 0.f;
+      if (l0) { v0 = __ldg(s4 + x0); k0 = Kr[j0]; }
+      if (l1) { v1 = __ldg(s4 + x1); k1 = Kr[j1]; }
+      float4 o0 = make_float4(0.f, 0.f, 0.f, 0.f), o1 = o0;
+      if (l0) { o0.x = fexp(k0 + v0.x); o0.y = fexp(k0 + v0.y); o0.z = fexp(k0 + v0.z); o0.w = fexp(k0 + v0.w); }
+      if (l1) { o1.x = fexp(k1 + v1.x); o1.y = fexp(k1 + v1.y); o1.z = fexp(k1 + v1.z); o1.w = fexp(k1 + v1.w); }
+      d4[x0] = o0;
+      if (x1 < tot) d4[x1] = o1;
     }
   } else {
     const int tot = n * m;

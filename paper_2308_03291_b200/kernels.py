@@ -290,6 +290,17 @@ def kuhlmann(adjacency, single_root: bool = False):
     return heads, score, status
 
 
+def eisner_kuhlmann(adjacency, single_root: bool = False, marginals: bool = True):
+    """Projective log_partition + marginals (spanning.py:183-280) AND the
+    public projective argmax (Kuhlmann, spanning.py:339-402) in one call: the
+    Eisner kernels on the current stream, Kuhlmann concurrently on a side
+    stream (the Eisner grid's second wave leaves SMs idle).
+    -> ((logz, marg, status), (heads, score, status))."""
+    adj = f32(adjacency, "adjacency")
+    return _concurrent(adj.device, lambda: eisner(adj, single_root, marginals),
+                       lambda: kuhlmann(adj, single_root), keep=(adj,))
+
+
 # ------------------------------------------------------------------- PCFG
 
 

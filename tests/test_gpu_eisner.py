@@ -114,3 +114,16 @@ def test_eisner_exp_space_fallback(single):
         z, mg = O.eisner_marginals(adj[b], single)
         assert abs(logz[b].item() - z) <= RTOL * abs(z) + 1e-6
         np.testing.assert_allclose(marg[b].cpu().numpy(), mg, rtol=RTOL, atol=2e-6)
+
+
+def test_eisner_kuhlmann_concurrent():
+    """Fused request (Eisner on the current stream, Kuhlmann on a side
+    stream) == the two separate calls."""
+    need_gpu()
+    adj = dev(batch_spanning(3100, 6, 40))
+    (lz, mg, st), (heads, score, st2) = K.eisner_kuhlmann(adj)
+    lz1, mg1, _ = K.eisner(adj)
+    heads1, score1, _ = K.kuhlmann(adj)
+    torch.cuda.synchronize()
+    assert torch.equal(lz, lz1) and torch.equal(mg, mg1)
+    assert torch.equal(heads, heads1) and torch.equal(score, score1)
