@@ -393,6 +393,9 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
     for (int i0 = warp; i0 + w <= n; i0 += 2 * kWarps) {
       const int iA = i0, iB = i0 + kWarps;
       const bool hasB = iB + w <= n;
+      // arc weights first: their global-load latency overlaps the dot products
+      const float wrA = W(iA, iA + w), wlA = W(iA + w, iA);
+      const float wrB = hasB ? W(iB, iB + w) : 0.f, wlB = hasB ? W(iB + w, iB) : 0.f;
       float sA = 0.f, sB = 0.f;
 #pragma unroll
       for (int q = 0; q < kQ; ++q) {
@@ -401,8 +404,8 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
         if (hasB && kB < iB + w) sB = fmaf(CR(iB, kB), CL(kB + 1, iB + w), sB);
       }
       const float FA = warp_dot_sum(sA), FB = warp_dot_sum(sB);
-      const float virA = W(iA, iA + w) * FA, vilA = W(iA + w, iA) * FA;
-      const float virB = hasB ? W(iB, iB + w) * FB : 0.f, vilB = hasB ? W(iB + w, iB) * FB : 0.f;
+      const float virA = wrA * FA, vilA = wlA * FA;
+      const float virB = wrB * FB, vilB = wlB * FB;
       if (lane == 0) {
         ir[pk(iA, iA + w, n)] = virA; il[pk(iA, iA + w, n)] = vilA;
         if (hasB) { ir[pk(iB, iB + w, n)] = virB; il[pk(iB, iB + w, n)] = vilB; }
@@ -489,6 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
     for (int a = warp; a + w <= n; a += kWarps) {
       const int bb = a + w;
       const int n1 = n - bb, n2 = a;
+      const float wba = W(bb, a), wab = W(a, bb);  // issued before the dot products
       float sA = 0.f, sB = 0.f;
 #pragma unroll
       for (int q = 0; q < kQ; ++q) {
@@ -527,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
       const float gir = warp_dot_sum(tr), gil = warp_dot_sum(tl);
       if (lane == 0) {
         const int e = pk(a, bb, n);
-        const float vf = gil * W(bb, a) + gir * W(a, bb);
+        const float vf = gil * wba + gir * wab;
         gfo[e] = vf;
         const float pr = gir * ir[e], pl = gil * il[e];
         if (!(single && a == 0)) mg[a * N1 + bb] = fminf(fmaxf(pr, 0.f), 1.f);
