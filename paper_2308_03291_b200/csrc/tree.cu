@@ -6,9 +6,12 @@
 // Layout per instance: span_potentials [n][n][m] fp32 (only i <= j is read;
 // marginals for i > j are written as 0).
 //
-// One CTA per instance (kThreads threads, kWarps warps):
-//   1. label fold: fold[i,j] = lse_l theta[i,j,l] -- one warp per span, the
-//      32 lanes read the contiguous label row (coalesced), warp lse;
+// log_partition + marginals (sdb_tree_fb) is a chain of three kernels, see
+// the block comment above tree_fold_kernel: label fold (HBM) -> scaled-linear
+// inside/outside (one CTA per instance, latency-bound) -> marginal emission
+// (HBM).  tree_kernel below is the exact log-space path: the max-plus argmax
+// (kMode 2) and the fallback for instances the linear charts cannot hold:
+//   1. label fold: fold[i,j] = lse_l theta[i,j,l] (thread per span);
 //   2. inside by span width (constituency.py:57-63): one warp per cell of the
 //      current width, lanes over split points, warp lse; one barrier/width;
 //   3. outside by decreasing width (constituency.py:84-99): lanes over the
