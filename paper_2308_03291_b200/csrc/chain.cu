@@ -840,72 +840,108 @@ __global__ void __launch_bounds__(kThreads) chain_viterbi_kernel(
   }
 }
 
-// Viterbi fast path (m <= 32): potentials staged kD steps ahead with cp.async, 8 warps split the
-// rows (first-maximum partials in ascending row order), warp 0 merges with the (value, lower index)
-// rule -- identical tie semantics to chain.py:106 -- and keeps backpointers in shared memory.
+// Viterbi fast path (m <= 32), one CTA of 256 threads per instance and ONE
+// barrier per step.  Thread (warp w, lane l) owns next tag b = 4w + (l & 3)
+// and the predecessors a = ag + 8q (ag = l >> 2, q = 0..3, ascending, strict
+// '>' = first maximum); the 8 predecessor groups of a tag are lanes l ^ 4,
+// l ^ 8, l ^ 16, merged by three shuffles with the (value, lower index) rule
+// -- identical tie semantics to chain.py:106 and the reference's addition
+// order (score[a] + theta[a, b] in float64).  Potentials stream through a
+// (kD+1)-slot cp.async ring (rows at a 36-float pitch: the 32 lanes of a
+// warp read 32 distinct banks); the scores are double-buffered, so the barrier
+// at the top of a step both publishes the previous scores and frees the ring
+// slot refilled in this step.
+constexpr int kVP = 36;  // ring row pitch (floats)
+
 __global__ void __launch_bounds__(kThreads) chain_viterbi_small_kernel(
     const float* __restrict__ init, const float* __restrict__ trans, int n, int m, int32_t* __restrict__ tags,
     double* __restrict__ score, int32_t* __restrict__ status) {
   extern __shared__ __align__(16) float smv[];
-  const int mm = m * m;
-  float* stage = smv;                                         // [kD][mm]
-  double* sc = reinterpret_cast<double*>(stage + kD * mm);    // [32]
-  double* pv = sc + 32;                                       // [kGroups][32]
-  int* pa = reinterpret_cast<int*>(pv + kGroups * 32);        // [kGroups][32]
-  uint8_t* back = reinterpret_cast<uint8_t*>(pa + kGroups * 32);  // [n][32]
+  const int mm = m * m, slot = m * kVP;
+  float* ring = smv;                                                  // [kD+1][m][kVP]
+  double* dl = reinterpret_cast<double*>(ring + (kD + 1) * slot);     // [2][32]
+  uint8_t* back = reinterpret_cast<uint8_t*>(dl + 64);                // [n][32]
   __shared__ int redi[kThreads / 32];
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tb = 4 * warp + (lane & 3), ag = lane >> 2;
   const float* th = trans + (size_t)b * (n - 1) * mm;
-  const bool v16 = ((mm & 3) == 0);
-  int bad = 0;
+  const bool v16 = ((m & 3) == 0) && ((((uintptr_t)th) & 15) == 0);
+  // this thread's 16-byte chunk of a step (m <= 32: m*m/4 <= 256 chunks), fixed for all steps
+  const int q4 = m >> 2;
+  const int cr = q4 ? tid / q4 : 0, cc = tid - cr * q4;
+  const bool has16 = v16 && tid < m * q4;
+  const int soff = cr * m + 4 * cc, doff = cr * kVP + 4 * cc;
+  auto stage = [&](int t, int sl) {
+    float* d = ring + sl * slot;
+    const float* src = th + (size_t)t * mm;
+    if (v16) {
+      if (has16) cpa16(d + doff, src + soff);
+    } else {
+      for (int e = tid; e < mm; e += kThreads) {
+        const int r = e / m, c = e - r * m;
+        cpa4(d + r * kVP + c, src + e);
+      }
+    }
+  };
   for (int d = 0; d < kD; ++d) {
-    if (d < n - 1) stage_step(stage + d * mm, th + (size_t)d * mm, mm, v16);
+    if (d < n - 1) stage(d, d);
     cpa_commit();
   }
-  if (warp == 0) {
-    const float x = lane < m ? init[(size_t)b * m + lane] : ninf();
-    bad |= (lane < m) && bad_input(x);
-    sc[lane] = lane < m ? (double)x : ninfd();
+  int bad = 0;
+  if (tid < 32) {
+    const float x = tid < m ? init[(size_t)b * m + tid] : ninf();
+    bad |= (tid < m) && bad_input(x);
+    dl[tid] = tid < m ? (double)x : ninfd();
   }
+  const bool bok = tb < m;
+  int rsl = 0, wsl = kD;  // ring slots read / refilled this step
   for (int t = 0; t < n - 1; ++t) {
     cpa_wait_d();
     __syncthreads();
-    const float* tt = stage + (t % kD) * mm;
-    if (lane < m) {
-      double best = ninfd();
-      int arg = 0x7fffffff;
-      for (int a = warp; a < m; a += kGroups) {
-        const float x = tt[a * m + lane];
-        bad |= bad_input(x);
-        const double v = sc[a] + (double)x;
-        if (v > best || (v == best && a < arg)) { best = v; arg = a; }
-      }
-      pv[warp * 32 + lane] = best;
-      pa[warp * 32 + lane] = arg;
-    }
-    __syncthreads();
-    {
-      const int tn = t + kD;
-      if (tn < n - 1) stage_step(stage + (t % kD) * mm, th + (size_t)tn * mm, mm, v16);
-      cpa_commit();
-    }
-    if (warp == 0 && lane < m) {
-      double best = pv[lane];
-      int arg = pa[lane];
+    const double* cur = dl + (t & 1) * 32;
+    double* nxt = dl + ((t + 1) & 1) * 32;
+    const float* tt = ring + rsl * slot;
+    float x[4];
+    double d[4];
 #pragma unroll
-      for (int g = 1; g < kGroups; ++g) {
-        const double v = pv[g * 32 + lane];
-        const int a = pa[g * 32 + lane];
-        if (v > best || (v == best && a < arg)) { best = v; arg = a; }
-      }
-      sc[lane] = best;
-      back[(size_t)(t + 1) * 32 + lane] = (uint8_t)(arg == 0x7fffffff ? 0 : arg);
+    for (int q = 0; q < 4; ++q) {
+      const int a = ag + 8 * q;
+      const int ac = a < m ? a : 0;
+      x[q] = tt[ac * kVP + (bok ? tb : 0)];
+      d[q] = cur[ac];
+    }
+    if (t + kD < n - 1) stage(t + kD, wsl);
+    cpa_commit();
+    rsl = rsl == kD ? 0 : rsl + 1;
+    wsl = wsl == kD ? 0 : wsl + 1;
+    double best = ninfd();
+    int arg = 0x7fffffff;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int a = ag + 8 * q;
+      const bool live = bok && a < m;
+      bad |= live && bad_input(x[q]);
+      const double v = live ? d[q] + (double)x[q] : ninfd();
+      if (v > best) { best = v; arg = live ? a : arg; }
+    }
+#pragma unroll
+    for (int o = 4; o <= 16; o <<= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+      if (ov > best || (ov == best && oa < arg)) { best = ov; arg = oa; }
+    }
+    if (ag == 0 && bok) {
+      nxt[tb] = best;
+      back[(size_t)(t + 1) * 32 + tb] = (uint8_t)(arg == 0x7fffffff ? 0 : arg);
+    } else if (ag == 0 && tb < 32) {
+      nxt[tb] = ninfd();
     }
   }
   asm volatile("cp.async.wait_group 0;\n" ::);
-  bad = block_or(bad, redi);
+  bad = block_or(bad, redi);  // (contains the barrier that publishes the last scores)
   if (warp == 0) {
-    double best = lane < m ? sc[lane] : ninfd();
+    const double* fin = dl + ((n - 1) & 1) * 32;
+    double best = lane < m ? fin[lane] : ninfd();
     int arg = lane < m ? lane : 0x7fffffff;
     for (int o = 16; o > 0; o >>= 1) {
       const double ov = __shfl_xor_sync(0xffffffffu, best, o);
@@ -1011,7 +1047,7 @@ extern "C" int sdb_chain_viterbi(const float* init, const float* trans, int64_t 
   if (B == 0) return SDB_OK;
   if (!workspace || ws_bytes < sdb_chain_viterbi_workspace(B, n, m)) return SDB_ERR_WORKSPACE;
   if (m <= 32) {
-    const size_t smem = (size_t)kD * m * m * 4 + 32 * 8 + kGroups * 32 * 12 + (size_t)n * 32 + 64;
+    const size_t smem = (size_t)(kD + 1) * m * kVP * 4 + 64 * 8 + (size_t)n * 32 + 64;
     if (smem <= 200 * 1024) {
       if (cudaFuncSetAttribute(chain_viterbi_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
           cudaSuccess)
