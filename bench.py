@@ -64,6 +64,11 @@ CONFIGS = {
                 work=2_130_444_288, bound="fp32", argmax=False, kernel="pcfg_kernel<1>"),
 }
 HEADLINE = "c2a"
+# e2e: instance slices per request in kernels.run_host_batch (PCIe-bound configs
+# overlap H2D, kernels and D2H; tiny batches run as one slice)
+E2E_CHUNKS = {"c1": 1, "c2a": 8, "c2b": 8, "c3": 4, "c4": 4, "c5a": 4, "c5b": 1}
+if os.environ.get("SDB_E2E_CHUNKS"):
+    E2E_CHUNKS = {k: int(os.environ["SDB_E2E_CHUNKS"]) for k in E2E_CHUNKS}
 # nominal B200 compute peaks (not in MEASURED_PEAKS.json): 148 SM x 128 FMA lanes x 2 x 1.965 GHz;
 # MUFU ex2 148 x 16 x 1.965 GHz
 NOMINAL = {"fp32": (74_440.0, "GFLOP/s"), "mufu": (4_653.0, "Gop/s")}
@@ -298,19 +303,21 @@ def measure_config(cfg, device, rank, world, steps, warmup, clocks=False):
     host_out = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in probe]
     h2d = sum(t.numel() * t.element_size() for t in host_in)
     d2h = sum(o.numel() * o.element_size() for o in host_out)
+    from paper_2308_03291_b200 import kernels as K
+
     et = []
     for it in range(warmup + steps):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
         e0.record(stream)
-        dev_in = [t.to(device, non_blocking=True) for t in host_in]
-        out = [o for o in step_fn(cfg, dev_in)() if o is not None]
-        for h, o in zip(host_out, out):
-            h.copy_(o, non_blocking=True)
+        # public host-batch entry: H2D / kernels / D2H of instance slices overlapped
+        K.run_host_batch(lambda *d: step_fn(cfg, d)(), host_in, host_out, device, chunks=E2E_CHUNKS.get(cfg, 1))
         e1.record(stream)
         torch.cuda.synchronize()
         if it >= warmup:
             et.append(e0.elapsed_time(e1))
+    if os.environ.get("SDB_E2E_DEBUG"):
+        print("[bench] e2e ms per step", [round(x, 2) for x in et], file=sys.stderr)
     e2e_ms = sum(et) / len(et)
     t = torch.tensor([ms, kms, e2e_ms], dtype=torch.float64, device=device)
     if world > 1:

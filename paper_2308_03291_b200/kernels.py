@@ -635,3 +635,52 @@ def pcfg_sample(root, rules, emissions, sticky, noise, num: int):
                              num, ptr(mask), ptr(used), ptr(status), ptr(ws), ws.numel(), stream_ptr(dev))
     _lib.check(rc, "sdb_pcfg_sample")
     return mask, used, status
+
+
+# ------------------------------------------------------ host-resident batches
+
+_PIPE = {}
+
+
+def _pipe_streams(dev):
+    s = _PIPE.get(dev.index)
+    if s is None:
+        s = _PIPE[dev.index] = tuple(torch.cuda.Stream(dev) for _ in range(4))  # h2d, d2h, compute x2
+    return s
+
+
+def run_host_batch(fn, host_inputs, host_outputs, device, chunks: int = 8):
+    """Batched call on HOST-resident (pinned) tensors with the PCIe copies
+    overlapped: the batch is cut into `chunks` slices along the leading
+    (instance) axis; slice k's host->device copy, slice k-1's kernels and
+    slice k-2's device->host copy run concurrently (one copy stream per
+    direction -- PCIe is full duplex -- and two compute streams, since a
+    slice's grid is smaller than the GPU).  `fn(*device_inputs)` returns the
+    device outputs (None entries skipped) matching `host_outputs`.  The
+    current stream waits for the last copy, so an event recorded after this
+    call covers the whole request."""
+    cur = torch.cuda.current_stream(device)
+    h2d, d2h, c0, c1 = _pipe_streams(device)
+    for s in (h2d, d2h, c0, c1):
+        s.wait_stream(cur)
+    B = host_inputs[0].shape[0]
+    chunks = max(1, min(chunks, B))
+    bounds = [(B * k) // chunks for k in range(chunks + 1)]
+    for k in range(chunks):
+        lo, hi = bounds[k], bounds[k + 1]
+        comp = c0 if k % 2 == 0 else c1
+        with torch.cuda.stream(h2d):
+            dev_in = [t[lo:hi].to(device, non_blocking=True) for t in host_inputs]
+        comp.wait_stream(h2d)
+        with torch.cuda.stream(comp):
+            outs = [o for o in fn(*dev_in) if o is not None]
+        for t in dev_in:
+            t.record_stream(comp)
+        d2h.wait_stream(comp)
+        with torch.cuda.stream(d2h):
+            for h, o in zip(host_outputs, outs):
+                h[lo:hi].copy_(o, non_blocking=True)
+        for o in outs:
+            o.record_stream(d2h)
+    cur.wait_stream(d2h)
+    return host_outputs

@@ -118,3 +118,17 @@ def test_alignment_mitm_masked_and_vacuous():
         z, mg = O.nw_marginals(th[b])
         assert abs(logz[b].item() - z) <= RTOL * abs(z)
         np.testing.assert_allclose(marg[b].cpu().numpy(), mg, rtol=RTOL, atol=ATOL)
+
+
+def test_run_host_batch_matches_device_call():
+    """kernels.run_host_batch (pinned host slices, H2D / kernels / D2H
+    overlapped on separate streams) returns exactly the device call's result."""
+    need_gpu()
+    th = batch_alignment(1500, 11, 40, 24)
+    lz, mg, st = K.nw_fb(dev(th))
+    host_in = [torch.as_tensor(th, dtype=torch.float32).pin_memory()]
+    host_out = [torch.empty(tuple(lz.shape), dtype=lz.dtype).pin_memory(),
+                torch.empty(tuple(mg.shape), dtype=mg.dtype).pin_memory()]
+    K.run_host_batch(lambda t: K.nw_fb(t)[:2], host_in, host_out, torch.device("cuda", 0), chunks=4)
+    torch.cuda.synchronize()
+    assert torch.equal(host_out[0], lz.cpu()) and torch.equal(host_out[1], mg.cpu())
