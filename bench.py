@@ -262,6 +262,11 @@ def measure_config(cfg, device, rank, world, steps, warmup, clocks=False):
     for _ in range(warmup):
         step()
     torch.cuda.synchronize()
+    # Single GPU: replay the step (and the dominant launch) as CUDA graphs, so a
+    # step's host-side launch cost (ctypes, output allocation, several launches on
+    # two streams) never shows up as GPU idle time inside an event pair.
+    if world == 1:
+        step, kfn = _graphed(step, torch, device), _graphed(kfn, torch, device)
     stream = torch.cuda.current_stream(device)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     if world > 1:
@@ -325,6 +330,26 @@ def measure_config(cfg, device, rank, world, steps, warmup, clocks=False):
     ms, kms, e2e_ms = t.tolist()
     return dict(ms=ms, kms=kms, e2e_ms=e2e_ms, h2d=h2d, d2h=d2h, clocks=clk.summary() if clk else None,
                 l2="flushed between steps" if flush is not None else "inputs larger than L2")
+
+
+def _graphed(fn, torch, device):
+    """fn captured once into a CUDA graph (same kernels, same device buffers);
+    falls back to the eager callable if capture is not possible."""
+    try:
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(device)
+        s.wait_stream(torch.cuda.current_stream(device))
+        with torch.cuda.stream(s):
+            fn()  # warm the allocator on the capture stream
+        torch.cuda.current_stream(device).wait_stream(s)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            fn()
+        torch.cuda.synchronize()
+        return g.replay
+    except Exception as e:  # pragma: no cover - capture is an optimisation
+        print("[bench] graph capture failed (%s); timing eager launches" % e, file=sys.stderr)
+        return fn
 
 
 def roofline(cfg, kms):

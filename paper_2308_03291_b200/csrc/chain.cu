@@ -31,6 +31,7 @@ struct ChainWs {
   double* bcum;   // [B][n] cumulative backward normalisers
   int32_t* flags; // [B] forward status
   int32_t* need;  // [B] 1 = recompute with the exact log-space path
+  int32_t* needb; // [B] linear backward pass verdict (merged into `need` by the emission kernel)
 };
 
 __host__ ChainWs carve_chain(void* base, int64_t B, int n, int m, size_t* bytes) {
@@ -42,6 +43,7 @@ __host__ ChainWs carve_chain(void* base, int64_t B, int n, int m, size_t* bytes)
   w.bcum = c.take<double>((size_t)B * n);
   w.flags = c.take<int32_t>((size_t)B);
   w.need = c.take<int32_t>((size_t)B);
+  w.needb = c.take<int32_t>((size_t)B);
   *bytes = c.used;
   return w;
 }
@@ -382,74 +384,56 @@ __global__ void __launch_bounds__(kThreads) chain_fwd_bwd_small_kernel(
 }
 
 // ---------------------------------------------------------------------
-// Linear-space cluster kernel for m <= 32 (the C1 shape).
+// Linear-space kernel for m <= 32 (the C1 shape).
 //
-// One thread-block CLUSTER of two CTAs per instance: rank 0 runs the forward
-// recurrence, rank 1 the backward one, concurrently.  Inside a CTA:
+// Two CTAs per instance, independent: blockIdx.x & 1 == 0 runs the forward
+// recurrence, 1 the backward one, concurrently.  Inside a CTA:
 //   * warp 0 runs the recurrence in scaled LINEAR space: a step is a 32x32
 //     mat-vec of FMAs, u_x = sum_y M_t[x][y] v_y (lane x reads its row and the
 //     broadcast vector as float4), renormalised by its max (one REDUX + one
 //     MUFU.RCP), with the log scale accumulated in fp64 -- no exp/log on the
-//     critical path;
+//     critical path; every vector and its scale go to the workspace;
 //   * warps 1-7 are producers: they cp.async-stage the raw potentials two
-//     8-step blocks ahead and convert them to E_t = exp(theta_t - M_t)
-//     (M_t = the step max) one block ahead, plus per-column/row finiteness
-//     bitmasks that track exact reachability (a set bit whose linear value
-//     underflowed to 0 marks the instance for the exact log-space fallback);
-//   * the two CTAs meet in the middle (Q = transitions/2 rounded to a block):
-//     one cluster barrier, then both read the partner's boundary vector from
-//     global memory and form log Z;  after the meeting the producers also
-//     EMIT marginals for the transitions their own recurrence just passed
-//     (forward: t >= Q, backward: t < Q), e_t[a] * E_t[a][b] * f_(t+1)[b] *
-//     exp(M_t + c_t + d_(t+1) - Z), as coalesced 128-byte rows.
-// So the whole log_partition + marginals is one launch whose time is the
-// recurrence itself.  E rings are stored output-major (forward: E^T, backward:
-// E) with a 36-float pitch so the recurrence reads rows as float4.
+//     7-step blocks ahead and convert them to E_t = exp(theta_t) one block
+//     ahead (a zero / non-finite state in the recurrence flags the instance
+//     for the exact log-space fallback).
+// The marginals are NOT emitted here (they used to be, by the producers after
+// a meet-in-the-middle exchange, which made the producers the bottleneck):
+// chain_lin_marg_kernel streams them from the stored vectors with a grid over
+// (step block, instance), so this kernel's time is the recurrence itself.
+// E rings are stored output-major (forward: E^T, backward: E) with a 36-float
+// pitch so the recurrence reads rows as float4.
 constexpr int kLB = kGroups - 1;        // steps per block = producer warps (one step each)
 constexpr int kEP = 36;                // padded row pitch (16-byte aligned rows for LDS.128)
 constexpr int kERing = 3 * kLB;        // E slots: blocks k-1 (emit), k (consume), k+1 (produce)
 constexpr int kRRing = 3 * kLB;        // raw slots: blocks k+1, k+2, k+3
-constexpr int kHRing = 4 * kLB;        // recurrence-vector history slots
 
 struct LinSmem {
   float* raw;      // [kRRing][1024]
   float* E;        // [kERing][32][kEP]
   float* Mt;       // [kERing] step max (natural log)
   uint32_t* mask;  // [kERing][32] finiteness masks (fwd: per column b bits over a; bwd: per row a bits over b)
-  float* hist;     // [kERing][32] own recurrence vectors by step slot
-  double* hsc;     // [kERing] their log scales
 };
 
 size_t lin_smem_bytes() {
-  return (size_t)kRRing * 1024 * 4 + (size_t)kERing * 32 * kEP * 4 + kERing * 4 + kERing * 32 * 4 +
-         kHRing * 32 * 4 + kHRing * 8 + 256;
+  return (size_t)kRRing * 1024 * 4 + (size_t)kERing * 32 * kEP * 4 + kERing * 4 + kERing * 32 * 4 + 256;
 }
 
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     chain_lin_kernel(const float* __restrict__ init, const float* __restrict__ trans, int n, int m, ChainWs ws,
-                     double* __restrict__ logz, float* __restrict__ marg_init, float* __restrict__ marg_trans,
-                     int32_t* __restrict__ status) {
+                     double* __restrict__ logz, int32_t* __restrict__ status) {
   extern __shared__ __align__(16) char smraw[];
   LinSmem S;
   {
     char* p = smraw;
     S.raw = (float*)p; p += (size_t)kRRing * 1024 * 4;
     S.E = (float*)p; p += (size_t)kERing * 32 * kEP * 4;
-    S.hist = (float*)p; p += (size_t)kHRing * 32 * 4;
     S.mask = (uint32_t*)p; p += (size_t)kERing * 32 * 4;
-    S.Mt = (float*)p; p += kERing * 4;
-    p = (char*)(((uintptr_t)p + 7) & ~(uintptr_t)7);
-    S.hsc = (double*)p;
+    S.Mt = (float*)p;
   }
-  __shared__ double zsh;
   __shared__ int flagsh;  // bit0 invalid input, bit1 fallback needed
   __shared__ __align__(16) float vsh[32];
-  const int dir = blockIdx.x & 1;  // cluster rank: 0 forward, 1 backward
+  const int dir = blockIdx.x & 1;  // 0 forward, 1 backward
   const int b = blockIdx.x >> 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int T = n - 1;
@@ -457,15 +441,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const float* th = trans + (size_t)b * T * mm;
   float* vecs = dir == 0 ? ws.alpha + (size_t)b * n * m : ws.beta + (size_t)b * n * m;   // linear e_t / f_t
   double* scs = dir == 0 ? ws.acum + (size_t)b * n : ws.bcum + (size_t)b * n;         // their log scales
-  const float* pvecs = dir == 0 ? ws.beta + (size_t)b * n * m : ws.alpha + (size_t)b * n * m;
-  const double* pscs = dir == 0 ? ws.bcum + (size_t)b * n : ws.acum + (size_t)b * n;
   const int NB = (T + kLB - 1) / kLB;
-  const int Q = min(kLB * ((((T + 1) / 2) + kLB - 1) / kLB), T);  // meeting index (block aligned)
-  const int qmeet = Q / kLB;                                       // meeting after this many blocks
-  if (tid == 0) { flagsh = 0; zsh = ninfd(); }
+  if (tid == 0) flagsh = 0;
   // step index of processing position q
   auto tstep = [&](int q) { return dir == 0 ? q : T - 1 - q; };
-  double Z = ninfd();
   const bool v16 = ((mm & 3) == 0);
   auto issue_raw = [&](int blk) {  // producer warp w-1 stages step w-1 of block blk (own cp.async group)
     const int q = blk * kLB + (warp - 1);
@@ -520,28 +499,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     if (lane == 0) S.Mt[slot] = 0.f;
   };
-  // producers: emit the marginals of processing position q (one warp per position)
-  auto emit = [&](int q) {
-    if (q >= T) return;
-    const int t = tstep(q);
-    const int slot = q % kERing;
-    const float* E = S.E + slot * 32 * kEP;
-    const float* own = S.hist + (q % kHRing) * 32;  // fwd: e_t, bwd: f_(t+1)
-    const double osc = S.hsc[q % kHRing];
-    const int pt = dir == 0 ? t + 1 : t;            // partner: fwd needs f_(t+1), bwd needs e_t
-    const float pl = lane < m ? __ldcg(pvecs + (size_t)pt * m + lane) : 0.f;
-    const double psc = __ldcg(pscs + pt);
-    const float sf = fexp((float)((double)S.Mt[slot] + osc + psc - Z));
-    const float ol = own[lane];
-    float* out = marg_trans + ((size_t)b * T + t) * mm;
-#pragma unroll 8
-    for (int a = 0; a < 32; ++a) {
-      // element (a, lane) = e_t[a] * E_t[a][lane] * f_(t+1)[lane]
-      const float val = dir == 0 ? own[a] * E[lane * kEP + a] * pl
-                                 : __shfl_sync(0xffffffffu, pl, a) * E[a * kEP + lane] * ol;
-      if (lane < m && a < m) out[a * m + lane] = val * sf;
-    }
-  };
   // ---- prologue
   if (warp > 0) {
     issue_raw(0);
@@ -574,8 +531,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (lane == 0) scs[T] = sc;
     }
     vsh[lane] = v;
-    S.hist[lane] = v;  // slot of processing position 0 (the starting vector)
-    if (lane == 0) S.hsc[0] = sc;
   }
   __syncthreads();
   for (int blk = 0; blk < NB; ++blk) {
@@ -618,8 +573,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int tv = dir == 0 ? q + 1 : T - 1 - q;
         if (lane < m) vecs[(size_t)tv * m + lane] = v;
         if (lane == 0) scs[tv] = sc;
-        S.hist[((q + 1) % kHRing) * 32 + lane] = v;
-        if (lane == 0) S.hsc[(q + 1) % kHRing] = sc;
       }
     } else {
       // ---------------- producers: stage block blk+3, convert block blk+1, emit block blk-1
@@ -627,52 +580,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       asm volatile("cp.async.wait_group 2;\n" ::);
       __syncwarp();
       if (blk + 1 < NB) convert(blk + 1);
-      if (marg_trans && blk - 1 >= qmeet && Z != ninfd()) emit((blk - 1) * kLB + (warp - 1));
     }
     __syncthreads();
-    if (blk + 1 == qmeet) {
-      // ---------------- meet in the middle: Z = c_Q + d_Q + log sum_a e_Q[a] f_Q[a]
-      __threadfence();
-      cluster_sync_all();
-      if (warp == 0) {
-        const float e = lane < m ? __ldcg(ws.alpha + ((size_t)b * n + Q) * m + lane) : 0.f;
-        const float f = lane < m ? __ldcg(ws.beta + ((size_t)b * n + Q) * m + lane) : 0.f;
-        const float dot = warp_sum(e * f);
-        if (lane == 0) {
-          const double cq = __ldcg(ws.acum + (size_t)b * n + Q), dq = __ldcg(ws.bcum + (size_t)b * n + Q);
-          zsh = (dot > 0.f) ? cq + dq + (double)flog(dot) : ninfd();
-        }
-      }
-      __syncthreads();
-      Z = zsh;
-      // transitions processed by BOTH passes before the meeting (t in [T-Q, Q-1]) are emitted
-      // here by the forward CTA while their E slots / history are still in the rings
-      if (dir == 0 && warp > 0 && marg_trans && Z != ninfd())
-        for (int q = T - Q + (warp - 1); q < Q; q += kLB) emit(q);
-    }
   }
-  // emit the last block (its transitions are past the meeting when NB > qmeet)
-  if (warp > 0 && marg_trans && NB - 1 >= qmeet && Z != ninfd()) emit((NB - 1) * kLB + (warp - 1));
   asm volatile("cp.async.wait_group 0;\n" ::);
   __syncthreads();
-  // ---------------- outputs: status / log Z (forward CTA), p_init (backward CTA)
+  // ---------------- outputs.  Forward: log Z = c_T + log sum_a e_T[a] (beta_T = 0), status and
+  // its verdict; backward: its verdict.  Anything but a clean linear result (invalid input, a
+  // reachable state whose linear value underflowed or overflowed, vacuous) is recomputed by the
+  // exact log-space path; the emission kernel merges the two verdicts.
   const int fl = flagsh;
-  if (dir == 0 && tid == 0) {
-    // anything but a clean linear-space result (invalid input, vacuous, or a reachable state whose
-    // linear value underflowed) is recomputed by the exact log-space path for this instance
-    const bool need = (fl & 3) || Z == ninfd();
-    ws.need[b] = need ? 1 : 0;
-    ws.flags[b] = SDB_ST_OK;
-    status[b] = SDB_ST_OK;
-    logz[b] = Z;
-  }
-  if (dir == 1 && marg_init && warp == 0 && lane < m) {
-    // p_init[a] = exp(init[a] + beta_0[a] - Z), beta_0 = d_0 + log f_0
-    const float f0 = v;  // vector after the last backward step = f_0
-    const double d0 = sc;
-    float pv = 0.f;
-    if (Z != ninfd() && f0 > 0.f) pv = fexp(init[(size_t)b * m + lane] + (float)(d0 - Z)) * f0;
-    marg_init[(size_t)b * m + lane] = pv;
+  if (warp == 0) {
+    const float tot = warp_sum(lane < m ? v : 0.f);
+    if (lane == 0) {
+      if (dir == 0) {
+        const double Zf = (tot > 0.f && tot < __int_as_float(0x7f800000)) ? sc + (double)flog(tot) : ninfd();
+        ws.need[b] = ((fl & 3) || Zf == ninfd()) ? 1 : 0;
+        ws.flags[b] = SDB_ST_OK;
+        status[b] = SDB_ST_OK;
+        logz[b] = Zf;
+      } else {
+        ws.needb[b] = (fl & 3) ? 1 : 0;
+      }
+    }
   }
 }
 
@@ -726,6 +656,62 @@ __global__ void __launch_bounds__(kThreads) chain_marg_kernel(
       for (int e = threadIdx.x; e < (int)mm; e += kThreads) {
         const int a = e / m, j = e - a * m;
         out[e] = fexp(al[a] + tt[e] + be[j] + K);
+      }
+    }
+  }
+}
+
+// Marginals from the LINEAR passes (chain_lin_kernel): e_t, f_t normalised
+// vectors with log scales c_t, d_t, so
+//   p[t][a][b] = e_t[a] exp(theta_t[a][b]) f_(t+1)[b] exp(c_t + d_(t+1) - Z)
+// (chain.py:84-95).  Grid (ceil((n-1)/kStepsPerBlock), B), every element an
+// independent streaming FMUL/MUFU -- HBM-bound.  Block (0, b) also writes
+// p_init and merges the two passes' verdicts into ws.need[b]; instances that
+// need the log-space path are skipped (chain_marg_kernel writes them).
+__global__ void __launch_bounds__(kThreads) chain_lin_marg_kernel(
+    const float* __restrict__ init, const float* __restrict__ trans, int n, int m, ChainWs ws,
+    const double* __restrict__ logz, float* __restrict__ marg_init, float* __restrict__ marg_trans) {
+  const int b = blockIdx.y;
+  const int need = ws.need[b] | ws.needb[b];
+  if (blockIdx.x == 0 && threadIdx.x == 0) ws.need[b] = need;
+  if (need) return;
+  const double z = logz[b];
+  const size_t mm = (size_t)m * m;
+  const float* ev = ws.alpha + (size_t)b * n * m;
+  const float* fv = ws.beta + (size_t)b * n * m;
+  if (blockIdx.x == 0 && marg_init) {
+    // p_init[a] = exp(init[a] + d_0 - Z) f_0[a]
+    const float K = (float)(ws.bcum[(size_t)b * n] - z);
+    for (int j = threadIdx.x; j < m; j += kThreads)
+      marg_init[(size_t)b * m + j] = fexp(init[(size_t)b * m + j] + K) * fv[j];
+  }
+  if (!marg_trans) return;
+  const int t0 = blockIdx.x * kStepsPerBlock, t1 = min(t0 + kStepsPerBlock, n - 1);
+  for (int t = t0; t < t1; ++t) {
+    const float* tt = trans + ((size_t)b * (n - 1) + t) * mm;
+    float* out = marg_trans + ((size_t)b * (n - 1) + t) * mm;
+    const float* e = ev + (size_t)t * m;
+    const float* f = fv + (size_t)(t + 1) * m;
+    const float K = (float)(ws.acum[(size_t)b * n + t] + ws.bcum[(size_t)b * n + t + 1] - z);
+    if ((m & 3) == 0) {
+      const float4* t4 = reinterpret_cast<const float4*>(tt);
+      float4* o4 = reinterpret_cast<float4*>(out);
+      const int m4 = m >> 2;
+      for (int x = threadIdx.x; x < (int)(mm >> 2); x += kThreads) {
+        const int a = x / m4, j = (x - a * m4) * 4;
+        const float ea = e[a];
+        const float4 v = __ldg(t4 + x);
+        float4 r;
+        r.x = fexp(v.x + K) * ea * f[j + 0];
+        r.y = fexp(v.y + K) * ea * f[j + 1];
+        r.z = fexp(v.z + K) * ea * f[j + 2];
+        r.w = fexp(v.w + K) * ea * f[j + 3];
+        o4[x] = r;
+      }
+    } else {
+      for (int x = threadIdx.x; x < (int)mm; x += kThreads) {
+        const int a = x / m, j = x - a * m;
+        out[x] = fexp(tt[x] + K) * e[a] * f[j];
       }
     }
   }
@@ -993,8 +979,11 @@ extern "C" int sdb_chain_fb(const float* init, const float* trans, int64_t B, in
     const size_t smem = lin_smem_bytes();
     if (cudaFuncSetAttribute(chain_lin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return SDB_ERR_CUDA;
-    chain_lin_kernel<<<(unsigned)(2 * B), kThreads, smem, s>>>(init, trans, n, m, ws, logz, marg_init, marg_trans,
-                                                               status);
+    chain_lin_kernel<<<(unsigned)(2 * B), kThreads, smem, s>>>(init, trans, n, m, ws, logz, status);
+    SDB_CHECK_LAUNCH();
+    // marginals of the linear instances (also merges the two passes' verdicts into ws.need)
+    dim3 g((unsigned)((n - 1 + kStepsPerBlock - 1) / kStepsPerBlock), (unsigned)B);
+    chain_lin_marg_kernel<<<g, kThreads, 0, s>>>(init, trans, n, m, ws, logz, marg_init, marg_trans);
     SDB_CHECK_LAUNCH();
     // exact log-space recomputation of the (rare) instances the linear path flagged
     if (cudaFuncSetAttribute(chain_fwd_bwd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1004,7 +993,6 @@ extern "C" int sdb_chain_fb(const float* init, const float* trans, int64_t B, in
                                                                                   status, 1);
     SDB_CHECK_LAUNCH();
     if (marg_init || marg_trans) {
-      dim3 g((unsigned)((n - 1 + kStepsPerBlock - 1) / kStepsPerBlock), (unsigned)B);
       chain_marg_kernel<<<g, kThreads, 0, s>>>(init, trans, n, m, ws, logz, marg_init, marg_trans, 1);
       SDB_CHECK_LAUNCH();
     }
