@@ -14,17 +14,17 @@ if fam == "nw":
     th = torch.randn(B, n + 1, m + 1, 3, device="cuda", generator=g)
     th[:, 0, :, 0] = NEG_INF; th[:, 0, :, 1] = NEG_INF; th[:, :, 0, 0] = NEG_INF; th[:, :, 0, 2] = NEG_INF
     fn = {"fb": lambda: K.nw_fb(th), "logz": lambda: K.nw_fb(th, False), "vit": lambda: K.nw_viterbi(th)}[mode]
-elif fam == "chain":
+elif fam in ("chain", "chainv"):
     init = torch.randn(32, 32, device="cuda", generator=g)
     tr = torch.randn(32, 127, 32, 32, device="cuda", generator=g)
     fn = {"fb": lambda: K.chain_fb(init, tr), "lz": lambda: K.chain_fb(init, tr, False),
-          "vit": lambda: K.chain_viterbi(init, tr)}[mode]
-elif fam in ("mtt", "eisner"):
+          "vit": lambda: K.chain_viterbi(init, tr)}["vit" if fam == "chainv" else mode]
+elif fam in ("mtt", "eisner", "kuhl"):
     adj = torch.randn(512 if fam == "mtt" else 256, 129, 129, device="cuda", generator=g)
     adj[:, :, 0] = NEG_INF
     i = torch.arange(129, device="cuda")
     adj[:, i, i] = NEG_INF
-    fn = {"mtt": lambda: K.mtt(adj), "eisner": lambda: K.eisner(adj)}[fam]
+    fn = {"mtt": lambda: K.mtt(adj), "eisner": lambda: K.eisner(adj), "kuhl": lambda: K.kuhlmann(adj)}[fam]
 elif fam == "ctc":
     fp = torch.randn(256, 512, 128, device="cuda", generator=g)
     tg = torch.randint(1, 128, (256, 128), device="cuda", generator=g, dtype=torch.int32)
