@@ -619,11 +619,13 @@ __global__ void __launch_bounds__(kThreads) chain_marg_kernel(
   const size_t mm = (size_t)m * m;
   const bool ok = ws.flags[b] == SDB_ST_OK;
   const double z = logz[b];
+  // exponent arguments summed in fp64: this kernel serves the log-space path, i.e. the instances
+  // whose potentials are too large for the linear one (|theta| ~ 10^2: fp32 sums would cost 1e-4)
   if (blockIdx.x == 0 && marg_init) {
     const float* be = ws.beta + (size_t)b * n * m;
-    float K = ok ? (float)(ws.bcum[(size_t)b * n] - z) : 0.f;
+    const double K = ok ? ws.bcum[(size_t)b * n] - z : 0.0;
     for (int j = threadIdx.x; j < m; j += kThreads)
-      marg_init[(size_t)b * m + j] = ok ? fexp(init[(size_t)b * m + j] + be[j] + K) : 0.f;
+      marg_init[(size_t)b * m + j] = ok ? fexp((float)((double)init[(size_t)b * m + j] + (double)be[j] + K)) : 0.f;
   }
   if (!marg_trans) return;
   const int t1 = min(t0 + kStepsPerBlock, n - 1);
@@ -636,27 +638,10 @@ __global__ void __launch_bounds__(kThreads) chain_marg_kernel(
     }
     const float* al = ws.alpha + ((size_t)b * n + t) * m;
     const float* be = ws.beta + ((size_t)b * n + t + 1) * m;
-    const float K = (float)(ws.acum[(size_t)b * n + t] + ws.bcum[(size_t)b * n + t + 1] - z);
-    if ((m & 3) == 0) {
-      const float4* t4 = reinterpret_cast<const float4*>(tt);
-      float4* o4 = reinterpret_cast<float4*>(out);
-      const int m4 = m >> 2;
-      for (int e = threadIdx.x; e < (int)(mm >> 2); e += kThreads) {
-        const int a = e / m4, j = (e - a * m4) * 4;
-        const float x = al[a] + K;
-        float4 v = __ldg(t4 + e);
-        float4 r;
-        r.x = fexp(x + v.x + be[j + 0]);
-        r.y = fexp(x + v.y + be[j + 1]);
-        r.z = fexp(x + v.z + be[j + 2]);
-        r.w = fexp(x + v.w + be[j + 3]);
-        o4[e] = r;
-      }
-    } else {
-      for (int e = threadIdx.x; e < (int)mm; e += kThreads) {
-        const int a = e / m, j = e - a * m;
-        out[e] = fexp(al[a] + tt[e] + be[j] + K);
-      }
+    const double K = ws.acum[(size_t)b * n + t] + ws.bcum[(size_t)b * n + t + 1] - z;
+    for (int e = threadIdx.x; e < (int)mm; e += kThreads) {
+      const int a = e / m, j = e - a * m;
+      out[e] = fexp((float)(((double)al[a] + K) + ((double)tt[e] + (double)be[j])));
     }
   }
 }

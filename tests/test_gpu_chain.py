@@ -112,3 +112,22 @@ def test_chain_fb_viterbi_concurrent():
     assert torch.equal(lz, lz1) and torch.equal(mt, mt1) and torch.equal(mi, mi1)
     assert torch.equal(tags, tags1) and torch.equal(score, score1)
     assert (st == 0).all() and (st2 == 0).all()
+
+
+def test_chain_linear_fallback_mixed_batch():
+    """C1-shaped batch (linear recurrence path) where some instances cannot be
+    held in scaled linear fp32: huge potentials, and -inf structure late in
+    the chain (zero states in the BACKWARD pass only).  They are recomputed
+    by the exact log-space path; every instance must match the oracle."""
+    need_gpu()
+    init, tr = batch_chain(310, 4, 128, 32)
+    tr[1] *= 30.0                       # exp(theta) over/underflows fp32: beyond the linear range
+    tr[2, 120, :, 1:] = NEG_INF         # step 120: only tag 0 reachable -> zeros in beta
+    tr[3, 5, :, :] -= 200.0             # one very unlikely step (uniform shift)
+    logz, mi, mt, st = K.chain_fb(dev(init), dev(tr))
+    assert (st.cpu().numpy() == 0).all()
+    for b in range(4):
+        z, pi, pt = O.chain_marginals(init[b:b + 1], tr[b:b + 1])
+        assert abs(logz[b].item() - z[0]) <= RTOL * abs(z[0])
+        np.testing.assert_allclose(mi[b].cpu().numpy(), pi[0], rtol=RTOL, atol=ATOL)
+        np.testing.assert_allclose(mt[b].cpu().numpy(), pt[0], rtol=RTOL, atol=ATOL)
