@@ -170,19 +170,31 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
 #pragma unroll
         for (int q = 0; q < 32; ++q) acc[sl][q] = 0.f;
       if (sm != ninfd()) {
-        for (int k = i; k < j; ++k) {
-          const double sk = isc[i * n + k] + isc[(k + 1) * n + j];
-          if (sk == ninfd()) continue;
-          const float f = fexp((float)(sk - sm));
-          const float lv = iu[(size_t)(i * n + k) * 32 + lane];
-          const float rv = iu[(size_t)((k + 1) * n + j) * 32 + lane] * f;  // lane = C
-          const int sl = (w == 2) ? 0 : (k == i ? 1 : (k == j - 1 ? 2 : 0));
+        // four splits per pass: their (L2-resident) chart loads are all issued before the
+        // shuffle/FMA work, so one L2 latency is exposed per pass instead of per split
+        for (int k0 = i; k0 < j; k0 += 4) {
+          double sk[4];
+          float lv[4], rv[4];
 #pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            const float lb = __shfl_sync(0xffffffffu, lv, q);
-            if (sl == 0) acc[0][q] = fmaf(lb, rv, acc[0][q]);
-            else if (sl == 1) acc[1][q] = fmaf(lb, rv, acc[1][q]);
-            else acc[2][q] = fmaf(lb, rv, acc[2][q]);
+          for (int u = 0; u < 4; ++u) {
+            const int k = min(k0 + u, j - 1);
+            sk[u] = (k0 + u < j) ? isc[i * n + k] + isc[(k + 1) * n + j] : ninfd();
+            lv[u] = iu[(size_t)(i * n + k) * 32 + lane];
+            rv[u] = iu[(size_t)((k + 1) * n + j) * 32 + lane];  // lane = C
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int k = k0 + u;
+            if (sk[u] == ninfd()) continue;
+            const float rf = rv[u] * fexp((float)(sk[u] - sm));
+            const int sl = (w == 2) ? 0 : (k == i ? 1 : (k == j - 1 ? 2 : 0));
+#pragma unroll
+            for (int q = 0; q < 32; ++q) {
+              const float lb = __shfl_sync(0xffffffffu, lv[u], q);
+              if (sl == 0) acc[0][q] = fmaf(lb, rf, acc[0][q]);
+              else if (sl == 1) acc[1][q] = fmaf(lb, rf, acc[1][q]);
+              else acc[2][q] = fmaf(lb, rf, acc[2][q]);
+            }
           }
         }
       }
