@@ -407,19 +407,34 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
           const int i = s, j = i + w - 1;
           const double ps = osc[i * n + j] + (double)STK(i, j);
           if (ps == ninfd()) continue;
+          // split k's loads (sibling inside scale/vector, child outside state) are issued one
+          // split ahead, so their global latency overlaps the previous split's dot product
+          // (children and siblings of one parent's splits are all distinct spans)
+          auto span_of = [&](int k, int& si, int& sj, size_t& co) {
+            // side 0: left child (i,k) gets sum_C Q[B][C] u_(k+1)j[C];  side 1: right child (k+1,j)
+            si = side == 0 ? k + 1 : i;
+            sj = side == 0 ? j : k;  // sibling span
+            const int ci = side == 0 ? i : k + 1, cj = side == 0 ? k : j;  // child span
+            co = (size_t)(ci * n + cj);
+          };
+          int nsi, nsj;
+          size_t nco;
+          span_of(i, nsi, nsj, nco);
+          double nsib = isc[nsi * n + nsj], nold = osc[nco];
+          float nsv = iu[(size_t)(nsi * n + nsj) * 32 + lane], nou = ou[nco * 32 + lane];
           for (int k = i; k < j; ++k) {
             const int sl = (w == 2) ? 0 : (k == i ? 1 : (k == j - 1 ? 2 : 0));
-            // side 0: left child (i,k) gets sum_C Q[B][C] u_(k+1)j[C];  side 1: right child (k+1,j)
-            const int si = side == 0 ? k + 1 : i, sj = side == 0 ? j : k;  // sibling span
-            const int ci = side == 0 ? i : k + 1, cj = side == 0 ? k : j;  // child span
-            const double sib = isc[si * n + sj];
+            const double sib = nsib, old = nold;
+            const float sv = nsv, ou_old = nou;
+            const size_t co = nco;
+            if (k + 1 < j) {
+              span_of(k + 1, nsi, nsj, nco);
+              nsib = isc[nsi * n + nsj];
+              nold = osc[nco];
+              nsv = iu[(size_t)(nsi * n + nsj) * 32 + lane];
+              nou = ou[nco * 32 + lane];
+            }
             if (sib == ninfd()) continue;
-            const float sv = iu[(size_t)(si * n + sj) * 32 + lane];
-            // the child's current outside state, loaded before the dot product so
-            // the global latency overlaps it
-            const size_t co = (size_t)(ci * n + cj);
-            const double old = osc[co];
-            const float ou_old = ou[co * 32 + lane];
             float g = 0.f;
             const float* Qm = Qc + (size_t)(pz * 3 + sl) * 32 * 33;
             if (side == 0) {  // lane = B: row B of Q
