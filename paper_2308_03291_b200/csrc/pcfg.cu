@@ -384,18 +384,35 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
           asm volatile("cp.async.wait_group 0;\n" ::);
         }
         __syncthreads();
-        if (warp < cn) {
-          for (int sl = 0; sl < nslot; ++sl) {
-            float q4[kBS];
+        // register-tiled: thread = (4 parents, 3 slots) x one (bb, C) column, so every R word
+        // loaded from shared memory feeds 4 FMAs and every parent weight 3 (was 1 R load per FMA)
+        {
+          static_assert(kCP == 8 && kThreads == 256 && kBS * 32 == 128, "Q-build tiling");
+          const int pg = tid >> 7, c = tid & 127;  // parents 4pg..4pg+3 (warp-uniform), column c
+          if (4 * pg < cn) {
+            float q[4][3];
 #pragma unroll
-            for (int bb = 0; bb < kBS; ++bb) q4[bb] = 0.f;
+            for (int pp = 0; pp < 4; ++pp)
+#pragma unroll
+              for (int sl = 0; sl < 3; ++sl) q[pp][sl] = 0.f;
             for (int A = 0; A < NT; ++A) {
-              const float o = Os[warp * 32 + A];
+              float o[4], r[3];
 #pragma unroll
-              for (int bb = 0; bb < kBS; ++bb) q4[bb] = fmaf(o, cur[((sl * 32 + A) * kBS + bb) * 32 + lane], q4[bb]);
+              for (int pp = 0; pp < 4; ++pp) o[pp] = Os[(4 * pg + pp) * 32 + A];
+#pragma unroll
+              for (int sl = 0; sl < 3; ++sl) r[sl] = sl < nslot ? cur[(sl * 32 + A) * 128 + c] : 0.f;
+#pragma unroll
+              for (int pp = 0; pp < 4; ++pp)
+#pragma unroll
+                for (int sl = 0; sl < 3; ++sl) q[pp][sl] = fmaf(o[pp], r[sl], q[pp][sl]);
             }
+            const int bb = c >> 5, C = c & 31;
 #pragma unroll
-            for (int bb = 0; bb < kBS; ++bb) Qc[((warp * 3 + sl) * 32 + b0 + bb) * 33 + lane] = q4[bb];  // [B][C]
+            for (int pp = 0; pp < 4; ++pp)
+#pragma unroll
+              for (int sl = 0; sl < 3; ++sl)
+                if (4 * pg + pp < cn && sl < nslot)
+                  Qc[(((4 * pg + pp) * 3 + sl) * 32 + b0 + bb) * 33 + C] = q[pp][sl];  // [B][C]
           }
         }
         __syncthreads();
