@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
   __shared__ int badsh;
   __shared__ double smax_s[kMaxN];
   __shared__ double smax2_s[kMaxN];
+  __shared__ __align__(16) float svs[kWarps][32];  // per-warp sibling vector (push dot products)
   float* P2 = kMode == 2 ? ws.P2 + (size_t)b * n * 3 * 1024 : nullptr;
   float* G = kMode == 2 ? ws.G + (size_t)b * 4 * 32768 : nullptr;
   if (tid == 0) badsh = 0;
@@ -452,15 +453,34 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
               nou = ou[nco * 32 + lane];
             }
             if (sib == ninfd()) continue;
-            float g = 0.f;
+            float g = 0.f, g2 = 0.f;
             const float* Qm = Qc + (size_t)(pz * 3 + sl) * 32 * 33;
+            // the sibling vector goes through a per-warp shared slot and is read back as
+            // 16-byte broadcasts (8 LDS.128 instead of 32 shuffles per dot product)
+            svs[warp][lane] = sv;
+            __syncwarp();
+            const float4* s4 = reinterpret_cast<const float4*>(svs[warp]);
             if (side == 0) {  // lane = B: row B of Q
-#pragma unroll 8
-              for (int x = 0; x < 32; ++x) g = fmaf(Qm[lane * 33 + x], __shfl_sync(0xffffffffu, sv, x), g);
+#pragma unroll
+              for (int x4 = 0; x4 < 8; ++x4) {
+                const float4 v = s4[x4];
+                g = fmaf(Qm[lane * 33 + 4 * x4 + 0], v.x, g);
+                g2 = fmaf(Qm[lane * 33 + 4 * x4 + 1], v.y, g2);
+                g = fmaf(Qm[lane * 33 + 4 * x4 + 2], v.z, g);
+                g2 = fmaf(Qm[lane * 33 + 4 * x4 + 3], v.w, g2);
+              }
             } else {          // lane = C: column C of Q
-#pragma unroll 8
-              for (int x = 0; x < 32; ++x) g = fmaf(Qm[x * 33 + lane], __shfl_sync(0xffffffffu, sv, x), g);
+#pragma unroll
+              for (int x4 = 0; x4 < 8; ++x4) {
+                const float4 v = s4[x4];
+                g = fmaf(Qm[(4 * x4 + 0) * 33 + lane], v.x, g);
+                g2 = fmaf(Qm[(4 * x4 + 1) * 33 + lane], v.y, g2);
+                g = fmaf(Qm[(4 * x4 + 2) * 33 + lane], v.z, g);
+                g2 = fmaf(Qm[(4 * x4 + 3) * 33 + lane], v.w, g2);
+              }
             }
+            g += g2;
+            __syncwarp();  // the slot is rewritten by the next split
             // normalise the contribution (keeps the child's vector O(1) at any depth)
             const float gm = warp_max(g);
             if (!(gm > 0.f)) continue;
