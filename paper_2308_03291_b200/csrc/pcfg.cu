@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
   __shared__ double smax_s[kMaxN];
   __shared__ double smax2_s[kMaxN];
   __shared__ __align__(16) float svs[kWarps][32];  // per-warp sibling vector (push dot products)
+  __shared__ __align__(16) float lvs[kWarps][4][32];  // per-warp left-child vectors (P-build)
   float* P2 = kMode == 2 ? ws.P2 + (size_t)b * n * 3 * 1024 : nullptr;
   float* G = kMode == 2 ? ws.G + (size_t)b * 4 * 32768 : nullptr;
   if (tid == 0) badsh = 0;
@@ -183,20 +184,40 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
             lv[u] = iu[(size_t)(i * n + k) * 32 + lane];
             rv[u] = iu[(size_t)((k + 1) * n + j) * 32 + lane];  // lane = C
           }
+          // the left vectors go through a per-warp shared slot, read back as 16-byte broadcasts
+          // (8 LDS.128 per split instead of 32 shuffles)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) lvs[warp][u][lane] = lv[u];
+          __syncwarp();
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int k = k0 + u;
             if (sk[u] == ninfd()) continue;
             const float rf = rv[u] * fexp((float)(sk[u] - sm));
             const int sl = (w == 2) ? 0 : (k == i ? 1 : (k == j - 1 ? 2 : 0));
+            const float4* l4 = reinterpret_cast<const float4*>(lvs[warp][u]);
 #pragma unroll
-            for (int q = 0; q < 32; ++q) {
-              const float lb = __shfl_sync(0xffffffffu, lv[u], q);
-              if (sl == 0) acc[0][q] = fmaf(lb, rf, acc[0][q]);
-              else if (sl == 1) acc[1][q] = fmaf(lb, rf, acc[1][q]);
-              else acc[2][q] = fmaf(lb, rf, acc[2][q]);
+            for (int q4 = 0; q4 < 8; ++q4) {
+              const float4 lb = l4[q4];
+              if (sl == 0) {
+                acc[0][4 * q4 + 0] = fmaf(lb.x, rf, acc[0][4 * q4 + 0]);
+                acc[0][4 * q4 + 1] = fmaf(lb.y, rf, acc[0][4 * q4 + 1]);
+                acc[0][4 * q4 + 2] = fmaf(lb.z, rf, acc[0][4 * q4 + 2]);
+                acc[0][4 * q4 + 3] = fmaf(lb.w, rf, acc[0][4 * q4 + 3]);
+              } else if (sl == 1) {
+                acc[1][4 * q4 + 0] = fmaf(lb.x, rf, acc[1][4 * q4 + 0]);
+                acc[1][4 * q4 + 1] = fmaf(lb.y, rf, acc[1][4 * q4 + 1]);
+                acc[1][4 * q4 + 2] = fmaf(lb.z, rf, acc[1][4 * q4 + 2]);
+                acc[1][4 * q4 + 3] = fmaf(lb.w, rf, acc[1][4 * q4 + 3]);
+              } else {
+                acc[2][4 * q4 + 0] = fmaf(lb.x, rf, acc[2][4 * q4 + 0]);
+                acc[2][4 * q4 + 1] = fmaf(lb.y, rf, acc[2][4 * q4 + 1]);
+                acc[2][4 * q4 + 2] = fmaf(lb.z, rf, acc[2][4 * q4 + 2]);
+                acc[2][4 * q4 + 3] = fmaf(lb.w, rf, acc[2][4 * q4 + 3]);
+              }
             }
           }
+          __syncwarp();  // the slots are rewritten by the next pass
         }
       }
       float* pp = dst + (size_t)i * 3 * 1024;
