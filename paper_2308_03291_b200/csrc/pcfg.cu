@@ -75,6 +75,30 @@ __device__ __forceinline__ void cpa_commit_wait() {
   __syncthreads();
 }
 
+// inner[q] += sum_{slot, bb, C} R_t[A = lane][B'][C'] P[s_q][slot][bb][C] for the QN spans
+// s_q = warp + q kWarps of this warp (one B-slice of the inside contraction)
+template <int QN>
+__device__ __forceinline__ void contract_slice(const float* __restrict__ RTs, const float* __restrict__ Ps, int nslot,
+                                               int warp, int lane, float* inner) {
+  for (int sl = 0; sl < nslot; ++sl) {
+    for (int bb = 0; bb < kBS; ++bb) {
+#pragma unroll 4
+      for (int C = 0; C < 32; C += 4) {
+        const float r0 = RTs[((sl * kBS + bb) * 32 + C + 0) * 32 + lane];
+        const float r1 = RTs[((sl * kBS + bb) * 32 + C + 1) * 32 + lane];
+        const float r2 = RTs[((sl * kBS + bb) * 32 + C + 2) * 32 + lane];
+        const float r3 = RTs[((sl * kBS + bb) * 32 + C + 3) * 32 + lane];
+#pragma unroll
+        for (int q = 0; q < QN; ++q) {
+          const int sp = warp + q * kWarps;
+          const float4 p = *reinterpret_cast<const float4*>(&Ps[((sp * 3 + sl) * kBS + bb) * 32 + C]);
+          inner[q] = fmaf(r0, p.x, fmaf(r1, p.y, fmaf(r2, p.z, fmaf(r3, p.w, inner[q]))));
+        }
+      }
+    }
+  }
+}
+
 // child class offsets of block t: t0 = (NT,NT) t1 = (PT,NT) t2 = (NT,PT) t3 = (PT,PT)
 __device__ __forceinline__ int boff(int t, int NT) { return (t == 1 || t == 3) ? NT : 0; }
 __device__ __forceinline__ int coff(int t, int NT) { return (t == 2 || t == 3) ? NT : 0; }
@@ -257,24 +281,19 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
       }
       cpa_commit_wait();
       __syncthreads();
-      for (int sl = 0; sl < nslot; ++sl) {
-        for (int bb = 0; bb < kBS; ++bb) {
-#pragma unroll 4
-          for (int C = 0; C < 32; C += 4) {
-            const float r0 = RTs[((sl * kBS + bb) * 32 + C + 0) * 32 + lane];
-            const float r1 = RTs[((sl * kBS + bb) * 32 + C + 1) * 32 + lane];
-            const float r2 = RTs[((sl * kBS + bb) * 32 + C + 2) * 32 + lane];
-            const float r3 = RTs[((sl * kBS + bb) * 32 + C + 3) * 32 + lane];
-#pragma unroll
-            for (int q = 0; q < kSpW; ++q) {
-              const int s = warp + q * kWarps;
-              if (s < nsp) {
-                const float4 p = *reinterpret_cast<const float4*>(&Ps[((s * 3 + sl) * kBS + bb) * 32 + C]);
-                inner[q] = fmaf(r0, p.x, fmaf(r1, p.y, fmaf(r2, p.z, fmaf(r3, p.w, inner[q]))));
-              }
-            }
-          }
-        }
+      // the warp's span count qn is warp-uniform: dispatch to a body with exactly qn spans so
+      // wide widths (few spans) do not issue the idle span slots
+      const int qn = nsp > warp ? min(kSpW, (nsp - warp + kWarps - 1) / kWarps) : 0;
+      switch (qn) {
+        case 8: contract_slice<8>(RTs, Ps, nslot, warp, lane, inner); break;
+        case 7: contract_slice<7>(RTs, Ps, nslot, warp, lane, inner); break;
+        case 6: contract_slice<6>(RTs, Ps, nslot, warp, lane, inner); break;
+        case 5: contract_slice<5>(RTs, Ps, nslot, warp, lane, inner); break;
+        case 4: contract_slice<4>(RTs, Ps, nslot, warp, lane, inner); break;
+        case 3: contract_slice<3>(RTs, Ps, nslot, warp, lane, inner); break;
+        case 2: contract_slice<2>(RTs, Ps, nslot, warp, lane, inner); break;
+        case 1: contract_slice<1>(RTs, Ps, nslot, warp, lane, inner); break;
+        default: break;
       }
       __syncthreads();
     }
