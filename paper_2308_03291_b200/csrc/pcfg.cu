@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
   }
   __syncthreads();
   float* REs = smf;                                  // [2][3][32 A][kBS][32 C] (double buffer)
-  float* Os = REs + 2 * 3 * kBS * 1024;              // [kCP parents][32 A]
+  float* Os = REs + 2 * 3 * kBS * 1024;              // [32 A][kCP parents]
   float* Qc = Os + kCP * 32;                         // [kCP][3][32 B][33 C] (padded rows: both push
                                                      //  orientations read it conflict-free)
   for (int w = n; w >= 2; --w) {
@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
       // stage the chunk's parent outside vectors
       for (int e = tid; e < cn * 32; e += kThreads) {
         const int pz = e >> 5, A = e & 31, s = c0 + pz;
-        Os[e] = (A < NT) ? ou[(size_t)(s * n + s + w - 1) * 32 + A] : 0.f;
+        Os[A * kCP + pz] = (A < NT) ? ou[(size_t)(s * n + s + w - 1) * 32 + A] : 0.f;  // [A][parent]
       }
       // ---- Q-build: Q[p][slot][B][C] = sum_A o_p[A] R_t[A, B', C'] (warp = parent, lane = C);
       // R slices double-buffered through shared memory
@@ -438,8 +438,10 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
               for (int sl = 0; sl < 3; ++sl) q[pp][sl] = 0.f;
             for (int A = 0; A < NT; ++A) {
               float o[4], r[3];
-#pragma unroll
-              for (int pp = 0; pp < 4; ++pp) o[pp] = Os[(4 * pg + pp) * 32 + A];
+              {
+                const float4 o4 = *reinterpret_cast<const float4*>(&Os[A * kCP + 4 * pg]);
+                o[0] = o4.x; o[1] = o4.y; o[2] = o4.z; o[3] = o4.w;
+              }
 #pragma unroll
               for (int sl = 0; sl < 3; ++sl) r[sl] = sl < nslot ? cur[(sl * 32 + A) * 128 + c] : 0.f;
 #pragma unroll
@@ -522,7 +524,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
             g += g2;
             __syncwarp();  // the slot is rewritten by the next split
             // normalise the contribution (keeps the child's vector O(1) at any depth)
-            const float gm = warp_max(g);
+            // g >= 0: its float bits order like unsigned ints -> one REDUX instead of 5 shuffles
+          const float gm = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(g)));
             if (!(gm > 0.f)) continue;
             g = g / gm;
             // merge contribution (scale cs, vec g) into child
