@@ -534,9 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
             const float a1 = (old == ninfd()) ? 0.f : fexp((float)(old - M));
             const float a2 = fexp((float)(cs - M));
             ou[co * 32 + lane] = ou_old * a1 + g * a2;
-            __syncwarp();
-            if (lane == 0) osc[co] = M;
-            __syncwarp();
+            if (lane == 0) osc[co] = M;  // this child is not touched again in this side pass
           }
         }
         __syncthreads();
