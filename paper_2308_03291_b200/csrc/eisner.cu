@@ -624,9 +624,11 @@ __global__ void __launch_bounds__(kThreads, 2) kuhlmann_kernel(const float* __re
       double best = ninfd();
       int arg = 0x7fffffff;  // encoded order index 2*(k-i-1) + (head==j)
       for (int k = i + 1 + lane; k < j; k += 32) {
+        // arc scores first: the global (L2) loads overlap the shared-memory chart reads
+        const double s1 = S(i, k), s2 = S(j, k);
         const double base = tab[pk2(i, k, N)] + tab[pk2(k, j, N)];
         if (base == ninfd()) continue;
-        const double c1 = base + S(i, k), c2 = base + S(j, k);
+        const double c1 = base + s1, c2 = base + s2;
         const int o = 2 * (k - i - 1);
         if (c1 > best) { best = c1; arg = o; }
         if (c2 > best) { best = c2; arg = o + 1; }
