@@ -311,7 +311,10 @@ def measure_config(cfg, device, rank, world, steps, warmup, clocks=False):
     from paper_2308_03291_b200 import kernels as K
 
     et = []
-    for it in range(warmup + steps):
+    # the host path (pinned copies, launches, syncs) needs a longer warm-up than the device
+    # loop: per-step e2e times keep falling for the first ~15 iterations
+    ew = max(warmup, 20)
+    for it in range(ew + steps):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
         e0.record(stream)
@@ -319,7 +322,7 @@ def measure_config(cfg, device, rank, world, steps, warmup, clocks=False):
         K.run_host_batch(lambda *d: step_fn(cfg, d)(), host_in, host_out, device, chunks=E2E_CHUNKS.get(cfg, 1))
         e1.record(stream)
         torch.cuda.synchronize()
-        if it >= warmup:
+        if it >= ew:
             et.append(e0.elapsed_time(e1))
     if os.environ.get("SDB_E2E_DEBUG"):
         print("[bench] e2e ms per step", [round(x, 2) for x in et], file=sys.stderr)
