@@ -396,9 +396,11 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
       // arc weights first: their global-load latency overlaps the dot products
       const float wrA = W(iA, iA + w), wlA = W(iA + w, iA);
       const float wrB = hasB ? W(iB, iB + w) : 0.f, wlB = hasB ? W(iB + w, iB) : 0.f;
+      const int qi = (w + 31) >> 5;  // split terms per lane actually present at this width
       float sA = 0.f, sB = 0.f;
 #pragma unroll
       for (int q = 0; q < kQ; ++q) {
+        if (q >= qi) break;  // warp-uniform: only the 32-term slices this width needs
         const int kA = iA + lane + 32 * q, kB = iB + lane + 32 * q;
         if (kA < iA + w) sA = fmaf(CR(iA, kA), CL(kA + 1, iA + w), sA);
         if (hasB && kB < iB + w) sB = fmaf(CR(iB, kB), CL(kB + 1, iB + w), sB);
@@ -414,6 +416,7 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
       float srA = 0.f, slA = 0.f, srB = 0.f, slB = 0.f;
 #pragma unroll
       for (int q = 0; q < kQ; ++q) {
+        if (q >= qi) break;  // warp-uniform: only the 32-term slices this width needs
         const int o = lane + 32 * q;
         if (o + 1 <= w) srA = fmaf(ir[pk(iA, iA + 1 + o, n)], CR(iA + 1 + o, iA + w), srA);
         if (o < w) slA = fmaf(CL(iA, iA + o), il[pk(iA + o, iA + w, n)], slA);
@@ -493,9 +496,11 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
       const int bb = a + w;
       const int n1 = n - bb, n2 = a;
       const float wba = W(bb, a), wab = W(a, bb);  // issued before the dot products
+      const int qo1 = (max(n1, n2) + 31) >> 5, qo2 = (max(n1, a) + 32) >> 5;
       float sA = 0.f, sB = 0.f;
 #pragma unroll
       for (int q = 0; q < kQ; ++q) {
+        if (q >= qo1) break;  // warp-uniform: only the 32-term slices this width needs
         const int x = lane + 32 * q;
         if (x < n1) {
           const int j = bb + 1 + x;
@@ -523,6 +528,7 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
       float tr = 0.f, tl = 0.f;
 #pragma unroll
       for (int q = 0; q < kQ; ++q) {
+        if (q >= qo2) break;  // warp-uniform: only the 32-term slices this width needs
         const int x = lane + 32 * q;
         const int j = bb + x;
         if (j <= n) tr = fmaf(gcr[pk(a, j, n)], CR(bb, j), tr);
