@@ -655,7 +655,8 @@ def run_host_batch(fn, host_inputs, host_outputs, device, chunks: int = 8):
     (instance) axis; slice k's host->device copy, slice k-1's kernels and
     slice k-2's device->host copy run concurrently (one copy stream per
     direction -- PCIe is full duplex -- and two compute streams, since a
-    slice's grid is smaller than the GPU).  `fn(*device_inputs)` returns the
+    slice's grid is smaller than the GPU).  `chunks` is a slice count or a
+    list of slice sizes (a short last slice shortens the D2H tail).  `fn(*device_inputs)` returns the
     device outputs (None entries skipped) matching `host_outputs`.  The
     current stream waits for the last copy, so an event recorded after this
     call covers the whole request."""
@@ -664,8 +665,15 @@ def run_host_batch(fn, host_inputs, host_outputs, device, chunks: int = 8):
     for s in (h2d, d2h, c0, c1):
         s.wait_stream(cur)
     B = host_inputs[0].shape[0]
-    chunks = max(1, min(chunks, B))
-    bounds = [(B * k) // chunks for k in range(chunks + 1)]
+    if isinstance(chunks, (list, tuple)):  # explicit slice sizes (e.g. a short last slice)
+        assert sum(chunks) == B, "slice sizes must cover the batch"
+        bounds = [0]
+        for c in chunks:
+            bounds.append(bounds[-1] + int(c))
+    else:
+        nch = max(1, min(int(chunks), B))
+        bounds = [(B * k) // nch for k in range(nch + 1)]
+    chunks = len(bounds) - 1
     for k in range(chunks):
         lo, hi = bounds[k], bounds[k + 1]
         comp = c0 if k % 2 == 0 else c1
