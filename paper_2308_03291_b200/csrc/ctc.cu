@@ -155,6 +155,11 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
       if (act) wsb[(size_t)(T - 1) * S + s] = (cur[s] == ninfd()) ? ninf() : (float)(cur[s] - base);
       if (tid == 0) wsbase[T - 1] = base;
     }
+    // successor labels of this state are fixed for all frames: keep them in registers
+    const bool has1 = act && (s + 1 < S);
+    const int lab1 = has1 ? sm.lab[s + 1] : 0;
+    const int lab2 = (act && s + 2 < S) ? sm.lab[s + 2] : 0;
+    const bool sk2 = act && (s + 2 < S) && lab2 != 0 && lab2 != mylab;
     for (int t = T - 2; t >= 0; --t) {
       // frame t+1 must be resident: it was issued (T-1)-(t+1) groups ago
       cp_wait<kP - 1>();
@@ -163,9 +168,8 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
       double v = ninfd();
       if (act) {
         const double x0 = cur[s] + (double)E[mylab];
-        const double x1 = (s + 1 < S) ? cur[s + 1] + (double)E[sm.lab[s + 1]] : ninfd();
-        const bool sk2 = (s + 2 < S) && sm.lab[s + 2] != 0 && sm.lab[s + 2] != mylab;
-        const double x2 = sk2 ? cur[s + 2] + (double)E[sm.lab[s + 2]] : ninfd();
+        const double x1 = has1 ? cur[s + 1] + (double)E[lab1] : ninfd();
+        const double x2 = sk2 ? cur[s + 2] + (double)E[lab2] : ninfd();
         const double M = fmax(fmax(x0, x1), x2);
         if (M != ninfd()) {
           const float e = fexp((float)(x0 - M)) + fexp((float)(x1 - M)) + fexp((float)(x2 - M));
@@ -227,6 +231,7 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
     const double Z = zsh;
     const bool zok = Z != ninfd();
     float* marg = (kMode == 1) ? marg_all + (size_t)b * T * V : nullptr;
+    const int q_lo = (kMode == 1 && tid < V) ? sm.off[tid] : 0, q_hi = (kMode == 1 && tid < V) ? sm.off[tid + 1] : 0;
     int8_t* back = (kMode == 2) ? back_all + (size_t)b * T * S : nullptr;
     int bad = 0;
     for (int t = 0; t < T; ++t) {
@@ -285,6 +290,8 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
           float acc = 0.f;
           if (v == 0) {
             for (int w = 0; w < nwarps; ++w) acc += sm.bred[w];
+          } else if (v == tid) {  // the common case (V <= blockDim): list bounds in registers
+            for (int q = q_lo; q < q_hi; ++q) acc += sm.post[sm.lst[q]];
           } else {
             for (int q = sm.off[v]; q < sm.off[v + 1]; ++q) acc += sm.post[sm.lst[q]];
           }
