@@ -42,12 +42,12 @@ struct CtcSmem {
   double* wred;   // [2][32]
   float* bred;    // [32]
   float* bring;   // [kP][S] beta rows (phase B prefetch)
-  double* bbase;  // [kP] their bases
+  double* bbase;  // [kP][32] their per-warp bases
 };
 
 size_t ctc_smem_bytes(int S, int V, int L) {
   return (size_t)2 * (S + 2) * 8 + (size_t)kP * V * 4 + (size_t)S * 4 + (size_t)(L + 1) * 4 +
-         (size_t)(V + 1) * 4 + (size_t)S * 4 + 64 * 8 + 32 * 4 + (size_t)kP * 8 + (size_t)kP * S * 4 + 128;
+         (size_t)(V + 1) * 4 + (size_t)S * 4 + 64 * 8 + 32 * 4 + (size_t)kP * 32 * 8 + (size_t)kP * S * 4 + 128;
 }
 
 __device__ CtcSmem ctc_carve(char* p, int S, int V, int L) {
@@ -55,7 +55,7 @@ __device__ CtcSmem ctc_carve(char* p, int S, int V, int L) {
   s.a0 = (double*)p; p += (size_t)(S + 2) * 8;
   s.a1 = (double*)p; p += (size_t)(S + 2) * 8;
   s.wred = (double*)p; p += 64 * 8;
-  s.bbase = (double*)p; p += kP * 8;
+  s.bbase = (double*)p; p += kP * 32 * 8;
   s.rows = (float*)p; p += (size_t)kP * V * 4;
   s.lab = (int*)p; p += (size_t)S * 4;
   s.lst = (int*)p; p += (size_t)(L + 1) * 4;
@@ -68,17 +68,6 @@ __device__ CtcSmem ctc_carve(char* p, int S, int V, int L) {
 
 __device__ __forceinline__ void load_row(const float* __restrict__ fp, int t, int V, float* dst) {
   for (int v = threadIdx.x; v < V; v += blockDim.x) cp_async4(dst + v, fp + (size_t)t * V + v);
-}
-
-// block-wide max of one double per thread (all threads get it); one barrier
-__device__ __forceinline__ double block_maxd_after(double v, double* wred) {
-  v = warp_maxd(v);
-  if ((threadIdx.x & 31) == 0) wred[threadIdx.x >> 5] = v;
-  __syncthreads();
-  double r = wred[0];
-  const int nw = blockDim.x >> 5;
-  for (int i = 1; i < nw; ++i) r = fmax(r, wred[i]);
-  return r;
 }
 
 template <int kMode>  // 0 logZ only, 1 logZ + marginals, 2 max-plus path
@@ -132,7 +121,7 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
   }
   const int nwarps = blockDim.x >> 5;
   float* wsb = (kMode == 1) ? wsb_all + (size_t)b * T * S : nullptr;
-  double* wsbase = (kMode == 1) ? wsbase_all + (size_t)b * T : nullptr;
+  double* wsbase = (kMode == 1) ? wsbase_all + (size_t)b * T * 32 : nullptr;  // [T][32 warps]
 
   // ======================= phase A: backward (marginals only)
   if (kMode == 1) {
@@ -148,12 +137,13 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
     if (tid < S + 2 && tid >= S) cur[tid] = ninfd();  // right pads beyond S
     if (tid < 2) { sm.a0[tid] = ninfd(); sm.a1[tid] = ninfd(); }
     __syncthreads();
-    // store beta[T-1]
+    // store beta[T-1] (offsets from a per-WARP base: a warp max, no CTA reduction per frame)
     {
-      double base = block_maxd_after(act ? cur[s] : ninfd(), sm.wred);
-      if (base == ninfd()) base = 0.0;
-      if (act) wsb[(size_t)(T - 1) * S + s] = (cur[s] == ninfd()) ? ninf() : (float)(cur[s] - base);
-      if (tid == 0) wsbase[T - 1] = base;
+      const double v = act ? cur[s] : ninfd();
+      const float wm = warp_max((float)v);
+      const double base = (wm == ninf()) ? 0.0 : (double)wm;
+      if (act) wsb[(size_t)(T - 1) * S + s] = (v == ninfd()) ? ninf() : (float)(v - base);
+      if ((tid & 31) == 0) wsbase[(size_t)(T - 1) * 32 + (tid >> 5)] = base;
     }
     // successor labels of this state are fixed for all frames: keep them in registers
     const bool has1 = act && (s + 1 < S);
@@ -177,22 +167,21 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
         }
         nxt[s] = v;
       }
+      // beta[t] as fp32 offsets from its warp's max (the base only has to be close to the
+      // values it is subtracted from; one fp32 warp max, no CTA-wide reduction)
       {
-        const double wm = warp_maxd(v);
-        if ((tid & 31) == 0) sm.wred[(t & 1) * 32 + (tid >> 5)] = wm;
+        const float wm = warp_max((float)v);
+        const double base = (wm == ninf()) ? 0.0 : (double)wm;
+        if (act) wsb[(size_t)t * S + s] = (v == ninfd()) ? ninf() : (float)(v - base);
+        if ((tid & 31) == 0) wsbase[(size_t)t * 32 + (tid >> 5)] = base;
       }
-      __syncthreads();  // all reads of cur and row (t+1) done; nxt and the warp maxima complete
+      __syncthreads();  // all reads of cur and row (t+1) done; nxt complete
       // refill the ring slot of frame t+1 with frame t+1-kP
       {
         const int tn = t + 1 - kP;
         if (tn >= 0) load_row(fp, tn, V, sm.rows + (size_t)(tn % kP) * V);
         cp_commit();
       }
-      double base = sm.wred[(t & 1) * 32];
-      for (int i = 1; i < nwarps; ++i) base = fmax(base, sm.wred[(t & 1) * 32 + i]);
-      if (base == ninfd()) base = 0.0;
-      if (act) wsb[(size_t)t * S + s] = (v == ninfd()) ? ninf() : (float)(v - base);
-      if (tid == 0) wsbase[t] = base;
       double* tmp = cur; cur = nxt; nxt = tmp;
     }
     cp_wait<0>();
@@ -216,9 +205,9 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
     auto load_beta = [&](int t) {  // beta row t + its base into ring slot t % kP
       if (kMode != 1) return;
       if (act) cp_async4(sm.bring + (size_t)(t % kP) * S + s, wsb + (size_t)t * S + s);
-      if (tid == 0) {
-        unsigned sa = (unsigned)__cvta_generic_to_shared(sm.bbase + (t % kP));
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(wsbase + t));
+      if ((tid & 31) == 0) {  // this warp's base
+        unsigned sa = (unsigned)__cvta_generic_to_shared(sm.bbase + (t % kP) * 32 + (tid >> 5));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(wsbase + (size_t)t * 32 + (tid >> 5)));
       }
     };
     for (int k = 0; k < kP; ++k) {
@@ -267,7 +256,7 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
         float p = 0.f;
         if (act && zok && a != ninfd()) {
           const float bt = sm.bring[(size_t)(t % kP) * S + s];
-          const double bb = sm.bbase[t % kP];
+          const double bb = sm.bbase[(t % kP) * 32 + (tid >> 5)];
           if (bt != ninf()) p = fexp((float)(a + bb - Z) + bt);
         }
         if (act) sm.post[s] = p;
@@ -345,7 +334,7 @@ CtcWs ctc_carve_ws(void* base, int64_t B, int T, int L, int mode, size_t* bytes)
   CtcWs w{};
   if (mode == 1) {
     w.wsb = c.take<float>((size_t)B * T * S);
-    w.wsbase = c.take<double>((size_t)B * T);
+    w.wsbase = c.take<double>((size_t)B * T * 32);
   }
   if (mode == 2) w.back = c.take<int8_t>((size_t)B * T * S);
   *bytes = c.used;
