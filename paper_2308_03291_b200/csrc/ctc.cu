@@ -73,7 +73,7 @@ __device__ __forceinline__ void load_row(const float* __restrict__ fp, int t, in
 template <int kMode>  // 0 logZ only, 1 logZ + marginals, 2 max-plus path
 __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __restrict__ tg_all, int T, int V,
                            int L, float* __restrict__ wsb_all, double* __restrict__ wsbase_all,
-                           int8_t* __restrict__ back_all, double* __restrict__ logz, float* __restrict__ marg_all,
+                           int32_t* __restrict__ csr_all, int8_t* __restrict__ back_all, double* __restrict__ logz, float* __restrict__ marg_all,
                            int32_t* __restrict__ path_all, double* __restrict__ score,
                            int32_t* __restrict__ status) {
   extern __shared__ __align__(16) char smraw[];
@@ -120,7 +120,13 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
     __syncthreads();
   }
   const int nwarps = blockDim.x >> 5;
+  (void)nwarps;
   float* wsb = (kMode == 1) ? wsb_all + (size_t)b * T * S : nullptr;
+  if (kMode == 1) {  // the label CSR, for ctc_marg_kernel
+    int32_t* csr = csr_all + (size_t)b * (V + 1 + L);
+    for (int e = tid; e <= V; e += blockDim.x) csr[e] = sm.off[e];
+    for (int e = tid; e < L; e += blockDim.x) csr[V + 1 + e] = sm.lst[e];
+  }
   double* wsbase = (kMode == 1) ? wsbase_all + (size_t)b * T * 32 : nullptr;  // [T][32 warps]
 
   // ======================= phase A: backward (marginals only)
@@ -219,8 +225,6 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
     }
     const double Z = zsh;
     const bool zok = Z != ninfd();
-    float* marg = (kMode == 1) ? marg_all + (size_t)b * T * V : nullptr;
-    const int q_lo = (kMode == 1 && tid < V) ? sm.off[tid] : 0, q_hi = (kMode == 1 && tid < V) ? sm.off[tid + 1] : 0;
     int8_t* back = (kMode == 2) ? back_all + (size_t)b * T * S : nullptr;
     int bad = 0;
     for (int t = 0; t < T; ++t) {
@@ -251,21 +255,18 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
         }
         now[s] = a;
       }
-      if (kMode == 1) {
-        // posterior of state s at frame t
+      if (kMode == 1 && act) {
+        // posterior of state s at frame t, written over beta's slot (frame t of the beta ring
+        // has been consumed); ctc_marg_kernel scatter-adds the rows by label off this loop
         float p = 0.f;
-        if (act && zok && a != ninfd()) {
+        if (zok && a != ninfd()) {
           const float bt = sm.bring[(size_t)(t % kP) * S + s];
           const double bb = sm.bbase[(t % kP) * 32 + (tid >> 5)];
           if (bt != ninf()) p = fexp((float)(a + bb - Z) + bt);
         }
-        if (act) sm.post[s] = p;
-        // blank column: fixed-order butterfly over the even states of each warp
-        float pb = (act && !(s & 1)) ? p : 0.f;
-        pb = warp_sum(pb);
-        if ((tid & 31) == 0) sm.bred[tid >> 5] = pb;
+        wsb[(size_t)t * S + s] = p;
       }
-      __syncthreads();  // now[] and post[] complete; row t consumed
+      __syncthreads();  // now[] complete; row t consumed
       {
         const int tn = t + kP;
         if (tn < T) {
@@ -273,19 +274,6 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
           load_beta(tn);
         }
         cp_commit();
-      }
-      if (kMode == 1) {
-        for (int v = tid; v < V; v += blockDim.x) {
-          float acc = 0.f;
-          if (v == 0) {
-            for (int w = 0; w < nwarps; ++w) acc += sm.bred[w];
-          } else if (v == tid) {  // the common case (V <= blockDim): list bounds in registers
-            for (int q = q_lo; q < q_hi; ++q) acc += sm.post[sm.lst[q]];
-          } else {
-            for (int q = sm.off[v]; q < sm.off[v + 1]; ++q) acc += sm.post[sm.lst[q]];
-          }
-          marg[(size_t)t * V + v] = acc;
-        }
       }
       double* tmp = prv; prv = now; now = tmp;
     }
@@ -322,19 +310,72 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
   }
 }
 
+// Per-frame vocabulary marginals from the posteriors ctc_kernel<1> left in
+// the workspace (alignment.py:290-301): marg[t][v] = sum of post[t][s] over
+// the states s with label v (blank: the L+1 even states; repeated labels
+// accumulate), in increasing s -- a deterministic order.  Grid (frame blocks,
+// instances), every frame independent, so this streams at HBM rate instead of
+// sitting inside the sequential frame loop.
+constexpr int kMargFrames = 16;
+
+__global__ void __launch_bounds__(256) ctc_marg_kernel(const float* __restrict__ post_all,
+                                                       const int32_t* __restrict__ csr_all, int T, int V, int L,
+                                                       const int32_t* __restrict__ status,
+                                                       float* __restrict__ marg_all) {
+  extern __shared__ __align__(16) float cm[];
+  const int S = 2 * L + 1;
+  float* prow = cm;                                  // [S]
+  int* off = reinterpret_cast<int*>(prow + S);       // [V+1]
+  int* lst = off + V + 1;                            // [L]
+  __shared__ float bsum[8];
+  const int b = blockIdx.y, t0 = blockIdx.x * kMargFrames, tid = threadIdx.x;
+  const int t1 = min(t0 + kMargFrames, T);
+  float* mg = marg_all + (size_t)b * T * V;
+  if (status[b] != SDB_ST_OK) {  // vacuous / invalid: zero marginals (as the reference's -inf Z)
+    for (int e = tid; e < (t1 - t0) * V; e += blockDim.x) mg[(size_t)t0 * V + e] = 0.f;
+    return;
+  }
+  const int32_t* csr = csr_all + (size_t)b * (V + 1 + L);  // built by ctc_kernel<1>
+  for (int e = tid; e <= V; e += blockDim.x) off[e] = csr[e];
+  for (int e = tid; e < L; e += blockDim.x) lst[e] = csr[V + 1 + e];
+  const float* pb = post_all + (size_t)b * T * S;
+  for (int t = t0; t < t1; ++t) {
+    __syncthreads();  // CSR ready / previous row consumed
+    for (int e = tid; e < S; e += blockDim.x) prow[e] = pb[(size_t)t * S + e];
+    __syncthreads();
+    // blank: even states, fixed-order (per-warp butterflies, then warps in order)
+    float bl = 0.f;
+    for (int e = 2 * tid; e < S; e += 2 * blockDim.x) bl += prow[e];
+    bl = warp_sum(bl);
+    if ((tid & 31) == 0) bsum[tid >> 5] = bl;
+    __syncthreads();
+    for (int v = tid; v < V; v += blockDim.x) {
+      float acc = 0.f;
+      if (v == 0) {
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) acc += bsum[w];
+      } else {
+        for (int q = off[v]; q < off[v + 1]; ++q) acc += prow[lst[q]];
+      }
+      mg[(size_t)t * V + v] = acc;
+    }
+  }
+}
+
 struct CtcWs {
-  float* wsb;
-  double* wsbase;
+  float* wsb;      // [B][T][S] beta offsets, then the state posteriors
+  double* wsbase;  // [B][T][32] per-warp beta bases
+  int32_t* csr;    // [B][V+1+L] label CSR (offsets, odd states by label)
   int8_t* back;
 };
 
-CtcWs ctc_carve_ws(void* base, int64_t B, int T, int L, int mode, size_t* bytes) {
+CtcWs ctc_carve_ws(void* base, int64_t B, int T, int V, int L, int mode, size_t* bytes) {
   const int S = 2 * L + 1;
   Carve c(base);
   CtcWs w{};
   if (mode == 1) {
     w.wsb = c.take<float>((size_t)B * T * S);
     w.wsbase = c.take<double>((size_t)B * T * 32);
+    w.csr = c.take<int32_t>((size_t)B * (V + 1 + L));
   }
   if (mode == 2) w.back = c.take<int8_t>((size_t)B * T * S);
   *bytes = c.used;
@@ -356,9 +397,19 @@ int ctc_launch(const float* fp, const int32_t* tg, int64_t B, int T, int V, int 
   const size_t smem = ctc_smem_bytes(S, V, L);
   if (cudaFuncSetAttribute(ctc_kernel<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return SDB_ERR_CUDA;
-  ctc_kernel<kMode><<<(unsigned)B, threads, smem, s>>>(fp, tg, T, V, L, ws.wsb, ws.wsbase, ws.back, logz, marg,
-                                                      path, score, status);
+  ctc_kernel<kMode><<<(unsigned)B, threads, smem, s>>>(fp, tg, T, V, L, ws.wsb, ws.wsbase, ws.csr, ws.back, logz,
+                                                      marg, path, score, status);
   SDB_CHECK_LAUNCH();
+  if (kMode == 1) {
+    const int S2 = 2 * L + 1;
+    const size_t msmem = (size_t)S2 * 4 + (size_t)(V + 1 + L) * 4;
+    if (msmem > 48 * 1024 &&
+        cudaFuncSetAttribute(ctc_marg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem) != cudaSuccess)
+      return SDB_ERR_CUDA;
+    dim3 g((unsigned)((T + kMargFrames - 1) / kMargFrames), (unsigned)B);
+    ctc_marg_kernel<<<g, 256, msmem, s>>>(ws.wsb, ws.csr, T, V, L, status, marg);
+    SDB_CHECK_LAUNCH();
+  }
   return SDB_OK;
 }
 
@@ -367,7 +418,7 @@ int ctc_launch(const float* fp, const int32_t* tg, int64_t B, int T, int V, int 
 extern "C" size_t sdb_ctc_fb_workspace(int64_t B, int32_t T, int32_t V, int32_t L) {
   (void)V;
   size_t bytes = 0;
-  ctc_carve_ws(nullptr, B, T, L, 1, &bytes);
+  ctc_carve_ws(nullptr, B, T, V, L, 1, &bytes);
   return bytes;
 }
 
@@ -381,7 +432,7 @@ extern "C" int sdb_ctc_fb(const float* frame_potentials, const int32_t* targets,
   cudaStream_t s = (cudaStream_t)stream;
   if (!marg) return ctc_launch<0>(frame_potentials, targets, B, T, V, L, CtcWs{}, logz, nullptr, nullptr, nullptr, status, s);
   size_t need = 0;
-  CtcWs ws = ctc_carve_ws(workspace, B, T, L, 1, &need);
+  CtcWs ws = ctc_carve_ws(workspace, B, T, V, L, 1, &need);
   if (!workspace || ws_bytes < need) return SDB_ERR_WORKSPACE;
   return ctc_launch<1>(frame_potentials, targets, B, T, V, L, ws, logz, marg, nullptr, nullptr, status, s);
 }
@@ -389,7 +440,7 @@ extern "C" int sdb_ctc_fb(const float* frame_potentials, const int32_t* targets,
 extern "C" size_t sdb_ctc_viterbi_workspace(int64_t B, int32_t T, int32_t V, int32_t L) {
   (void)V;
   size_t bytes = 0;
-  ctc_carve_ws(nullptr, B, T, L, 2, &bytes);
+  ctc_carve_ws(nullptr, B, T, V, L, 2, &bytes);
   return bytes;
 }
 
@@ -401,7 +452,7 @@ extern "C" int sdb_ctc_viterbi(const float* frame_potentials, const int32_t* tar
   if (!frame_potentials || (L > 0 && !targets) || !labels || !score || !status) return SDB_ERR_ARG;
   if (B == 0) return SDB_OK;
   size_t need = 0;
-  CtcWs ws = ctc_carve_ws(workspace, B, T, L, 2, &need);
+  CtcWs ws = ctc_carve_ws(workspace, B, T, V, L, 2, &need);
   if (!workspace || ws_bytes < need) return SDB_ERR_WORKSPACE;
   return ctc_launch<2>(frame_potentials, targets, B, T, V, L, ws, nullptr, nullptr, labels, score, status,
                        (cudaStream_t)stream);
