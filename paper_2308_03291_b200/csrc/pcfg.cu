@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
   __shared__ int badsh;
   __shared__ double smax_s[kMaxN];
   __shared__ double smax2_s[kMaxN];
-  __shared__ __align__(16) float svs[kWarps][32];  // per-warp sibling vector (push dot products)
+  __shared__ __align__(16) float svs[kWarps][2][32];  // per-warp sibling vectors (push dot products)
   __shared__ __align__(16) float lvs[kWarps][4][32];  // per-warp left-child vectors (P-build)
   float* P2 = kMode == 2 ? ws.P2 + (size_t)b * n * 3 * 1024 : nullptr;
   float* G = kMode == 2 ? ws.G + (size_t)b * 4 * 32768 : nullptr;
@@ -477,31 +477,22 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
             const int ci = side == 0 ? i : k + 1, cj = side == 0 ? k : j;  // child span
             co = (size_t)(ci * n + cj);
           };
-          int nsi, nsj;
-          size_t nco;
-          span_of(i, nsi, nsj, nco);
-          double nsib = isc[nsi * n + nsj], nold = osc[nco];
-          float nsv = iu[(size_t)(nsi * n + nsj) * 32 + lane], nou = ou[nco * 32 + lane];
-          for (int k = i; k < j; ++k) {
-            const int sl = (w == 2) ? 0 : (k == i ? 1 : (k == j - 1 ? 2 : 0));
-            const double sib = nsib, old = nold;
-            const float sv = nsv, ou_old = nou;
-            const size_t co = nco;
-            if (k + 1 < j) {
-              span_of(k + 1, nsi, nsj, nco);
-              nsib = isc[nsi * n + nsj];
-              nold = osc[nco];
-              nsv = iu[(size_t)(nsi * n + nsj) * 32 + lane];
-              nou = ou[nco * 32 + lane];
-            }
-            if (sib == ninfd()) continue;
+          // two splits per pass (independent children: their dot products and merges
+          // interleave), the next pass's loads issued before this pass's arithmetic
+          struct Item { double sib, old; float sv, ou; size_t co; };
+          auto fetch = [&](int k, Item& x) {
+            int si, sj;
+            span_of(k, si, sj, x.co);
+            x.sib = isc[si * n + sj];
+            x.old = osc[x.co];
+            x.sv = iu[(size_t)(si * n + sj) * 32 + lane];
+            x.ou = ou[x.co * 32 + lane];
+          };
+          auto slot_of = [&](int k) { return (w == 2) ? 0 : (k == i ? 1 : (k == j - 1 ? 2 : 0)); };
+          auto dot = [&](int k, const float* sv4) {
+            const float* Qm = Qc + (size_t)(pz * 3 + slot_of(k)) * 32 * 33;
+            const float4* s4 = reinterpret_cast<const float4*>(sv4);
             float g = 0.f, g2 = 0.f;
-            const float* Qm = Qc + (size_t)(pz * 3 + sl) * 32 * 33;
-            // the sibling vector goes through a per-warp shared slot and is read back as
-            // 16-byte broadcasts (8 LDS.128 instead of 32 shuffles per dot product)
-            svs[warp][lane] = sv;
-            __syncwarp();
-            const float4* s4 = reinterpret_cast<const float4*>(svs[warp]);
             if (side == 0) {  // lane = B: row B of Q
 #pragma unroll
               for (int x4 = 0; x4 < 8; ++x4) {
@@ -521,20 +512,39 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
                 g2 = fmaf(Qm[(4 * x4 + 3) * 33 + lane], v.w, g2);
               }
             }
-            g += g2;
-            __syncwarp();  // the slot is rewritten by the next split
-            // normalise the contribution (keeps the child's vector O(1) at any depth)
+            return g + g2;
+          };
+          // merge contribution g (child scale ps + sib + log max g) into the child
+          auto merge = [&](const Item& x, float g) {
+            if (x.sib == ninfd()) return;
             // g >= 0: its float bits order like unsigned ints -> one REDUX instead of 5 shuffles
-          const float gm = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(g)));
-            if (!(gm > 0.f)) continue;
-            g = g / gm;
-            // merge contribution (scale cs, vec g) into child
-            const double cs = ps + sib + (double)flog(gm);
-            const double M = fmax(old, cs);
-            const float a1 = (old == ninfd()) ? 0.f : fexp((float)(old - M));
+            const float gm = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(g)));
+            if (!(gm > 0.f)) return;
+            const double cs = ps + x.sib + (double)flog(gm);
+            const double M = fmax(x.old, cs);
+            const float a1 = (x.old == ninfd()) ? 0.f : fexp((float)(x.old - M));
             const float a2 = fexp((float)(cs - M));
-            ou[co * 32 + lane] = ou_old * a1 + g * a2;
-            if (lane == 0) osc[co] = M;  // this child is not touched again in this side pass
+            ou[x.co * 32 + lane] = x.ou * a1 + (g / gm) * a2;
+            if (lane == 0) osc[x.co] = M;  // this child is not touched again in this side pass
+          };
+          Item A, Bv;
+          fetch(i, A);
+          if (i + 1 < j) fetch(i + 1, Bv);
+          for (int k = i; k < j; k += 2) {
+            const Item a = A, bq = Bv;
+            const bool hb = k + 1 < j;
+            if (k + 2 < j) fetch(k + 2, A);
+            if (k + 3 < j) fetch(k + 3, Bv);
+            // the sibling vectors go through per-warp shared slots and are read back as
+            // 16-byte broadcasts (8 LDS.128 instead of 32 shuffles per dot product)
+            svs[warp][0][lane] = a.sv;
+            svs[warp][1][lane] = hb ? bq.sv : 0.f;
+            __syncwarp();
+            const float ga = dot(k, svs[warp][0]);
+            const float gb = hb ? dot(k + 1, svs[warp][1]) : 0.f;
+            __syncwarp();  // the slots are rewritten by the next pass
+            merge(a, ga);
+            if (hb) merge(bq, gb);
           }
         }
         __syncthreads();
