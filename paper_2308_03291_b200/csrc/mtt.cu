@@ -36,12 +36,13 @@ struct MttSmem {
   float* colbuf;  // [2][kN]
   int* perm;      // [kN] pivot row of step k
   int* used;      // [kN]
+  double* red64;  // [8]
 };
 
 // No shared copy of the adjacency (it is re-read from global/L2 where needed):
 // ~70 KB of shared memory and <= 64 registers let TWO instances share an SM.
 size_t mtt_smem(int n) {
-  return (size_t)kN * kN * 4 + (size_t)kN * 4 * 3 + (size_t)4 * kN * 4 + (size_t)kN * 8 + 256;
+  return (size_t)kN * kN * 4 + (size_t)kN * 4 * 3 + (size_t)4 * kN * 4 + (size_t)kN * 8 + 64 + 256;
 }
 
 template <bool kMarg>
@@ -60,17 +61,17 @@ __global__ void __launch_bounds__(kThreads, 2) mtt_kernel(const float* __restric
     sm.colbuf = (float*)p; p += 2 * kN * 4;
     sm.perm = (int*)p; p += kN * 4;
     sm.used = (int*)p; p += kN * 4;
+    sm.red64 = (double*)p; p += 8 * 8;
   }
   __shared__ int flag_bad, flag_vac, piv_row;
   __shared__ float piv_val;
-  __shared__ double logdet, detm;  // |det| = detm * 2^dete, logged once at the end
-  __shared__ int dete;
+  __shared__ double logdet;
   __shared__ int negs;
 
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int N1 = n + 1;
   const float* A = adj_all + (size_t)b * N1 * N1;
-  if (tid == 0) { flag_bad = 0; flag_vac = 0; logdet = 0.0; detm = 1.0; dete = 0; negs = 0; }
+  if (tid == 0) { flag_bad = 0; flag_vac = 0; logdet = 0.0; negs = 0; }
   for (int e = tid; e < N1 * N1; e += kThreads)
     if (bad_input(__ldg(A + e))) flag_bad = 1;
   for (int e = tid; e < kN; e += kThreads) { sm.used[e] = 0; sm.rowmag[e] = 0.f; }
@@ -177,16 +178,9 @@ __global__ void __launch_bounds__(kThreads, 2) mtt_kernel(const float* __restric
     }
     __syncthreads();
     const float piv = rowbuf[k];
-    if (tid == 0) {
-      const float mag = fabsf(piv);
-      if (!(mag > 1e-12f * fmaxf(sm.rowmag[p], 1e-30f))) singular = true, flag_vac = 1;
-      if (piv < 0.f) negs++;
-      // running product (exact fp64 scaling; one log at the end keeps the
-      // per-step critical path free of a software fp64 log)
-      int ex;
-      detm = frexp(detm * (double)mag, &ex);
-      dete += ex;
-    }
+    // pivot bookkeeping (singularity test, sign, log|det|) happens after the loop, in
+    // parallel over the recorded pivots: nothing fp64 on the per-step critical path
+    if (tid == 0) sm.diag[k] = piv;  // diag is free once the Laplacian is in registers
     const float inv_piv = 1.f / piv;
     float cv[4];
 #pragma unroll
@@ -209,6 +203,32 @@ __global__ void __launch_bounds__(kThreads, 2) mtt_kernel(const float* __restric
   }
   (void)singular;
   __syncthreads();
+  // log|det| = sum log|pivot| (numerics.py:157) in fp64, singular pivots
+  // (numerics.py:143-146) and the pivot signs
+  {
+    double lg = 0.0;
+    int neg = 0, sing = 0;
+    if (tid < kN) {
+      const float pv = sm.diag[tid];
+      const float mag = fabsf(pv);
+      sing = !(mag > 1e-12f * fmaxf(sm.rowmag[sm.perm[tid]], 1e-30f));
+      lg = log((double)mag);
+      neg = pv < 0.f;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lg += __shfl_xor_sync(0xffffffffu, lg, o);
+    const int negc = __syncthreads_count(neg);
+    if (__syncthreads_or(sing) && tid == 0) flag_vac = 1;
+    if (lane == 0 && warp < kN / 32) sm.red64[warp] = lg;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w2 = 0; w2 < kN / 32; ++w2) t += sm.red64[w2];
+      logdet = t;
+      negs = negc;
+    }
+  }
+  __syncthreads();
   // sign: pivot signs x permutation parity (numerics.py:149-155)
   if (tid == 0) {
     int parity = 0;
@@ -221,7 +241,6 @@ __global__ void __launch_bounds__(kThreads, 2) mtt_kernel(const float* __restric
       parity ^= (len + 1) & 1;  // a cycle of length L has L-1 transpositions
     }
     const int sgn = ((negs + parity) & 1) ? -1 : 1;
-    logdet = log(detm) + (double)dete * 0.6931471805599453;
     double ssum = 0.0;
     for (int d = 0; d < n; ++d) ssum += (double)sm.shift[d];
     const bool vac = flag_vac || sgn <= 0;
