@@ -258,27 +258,40 @@ __global__ void __launch_bounds__(kThreads, 2) mtt_kernel(const float* __restric
   for (int ii = 0; ii < 4; ++ii) {
     const int i = r0 + ii, qi = sm.used[i];
 #pragma unroll
-    for (int jj = 0; jj < 8; ++jj) sm.inv[qi * kN + sm.perm[c0 + jj]] = a[ii][jj];
+    for (int jj = 0; jj < 8; ++jj) sm.inv[sm.perm[c0 + jj] * kN + qi] = a[ii][jj];  // transposed: inv^T[x][d]
   }
   __syncthreads();
   float* mg = marg_all + (size_t)b * N1 * N1;
   const bool vac = flag_vac;
-  for (int e = tid; e < N1 * N1; e += kThreads) {
-    const int h = e / N1, dep = e - h * N1;
-    float v = 0.f;
-    if (!vac && dep >= 1 && h != dep) {
-      const int d = dep - 1;
-      const float w = fexp(__ldg(A + e) - sm.shift[d]);
-      const float idd = sm.inv[d * kN + d];
-      if (single) {
-        if (h == 0) v = w * sm.inv[d * kN + 0];
-        else v = w * ((d != 0 ? idd : 0.f) - ((h - 1) != 0 ? sm.inv[d * kN + (h - 1)] : 0.f));
-      } else {
-        v = (h == 0) ? w * idd : w * (idd - sm.inv[d * kN + (h - 1)]);
-      }
-      v = fminf(fmaxf(v, 0.f), 1.f);  // spanning.py:175
+  // warp per head row h, lane over dependents: coalesced adjacency loads, and the transposed
+  // inverse makes inv[d][h-1] for consecutive d contiguous (no bank conflicts)
+  const float* invT = sm.inv;  // invT[x * kN + d] = A^{-1}[d][x]
+  for (int h = warp; h < N1; h += kThreads / 32) {
+    float av[5];
+#pragma unroll
+    for (int u = 0; u < 5; ++u) {
+      const int dep = lane + 32 * u;
+      av[u] = dep < N1 ? __ldg(A + (size_t)h * N1 + dep) : 0.f;
     }
-    mg[e] = v;
+#pragma unroll
+    for (int u = 0; u < 5; ++u) {
+      const int dep = lane + 32 * u;
+      if (dep >= N1) continue;
+      float v = 0.f;
+      if (!vac && dep >= 1 && h != dep) {
+        const int d = dep - 1;
+        const float w = fexp(av[u] - sm.shift[d]);
+        const float idd = invT[d * kN + d];
+        if (single) {
+          if (h == 0) v = w * invT[0 * kN + d];
+          else v = w * ((d != 0 ? idd : 0.f) - ((h - 1) != 0 ? invT[(h - 1) * kN + d] : 0.f));
+        } else {
+          v = (h == 0) ? w * idd : w * (idd - invT[(h - 1) * kN + d]);
+        }
+        v = fminf(fmaxf(v, 0.f), 1.f);  // spanning.py:175
+      }
+      mg[(size_t)h * N1 + dep] = v;
+    }
   }
 }
 
