@@ -188,16 +188,33 @@ __global__ void __launch_bounds__(kThreads, 2) mtt_kernel(const float* __restric
     float rv[8];
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj) rv[jj] = rowbuf[c0 + jj] * inv_piv;
+    if (warp == (k >> 3)) {  // the warp owning column k (warp-uniform branch)
 #pragma unroll
-    for (int ii = 0; ii < 4; ++ii) {
-      const int r = r0 + ii;
-      if (r == p) {
+      for (int ii = 0; ii < 4; ++ii) {
+        const int r = r0 + ii;
+        if (r == p) {
 #pragma unroll
-        for (int jj = 0; jj < 8; ++jj) a[ii][jj] = (c0 + jj == k) ? inv_piv : rv[jj];
-      } else {
+          for (int jj = 0; jj < 8; ++jj) a[ii][jj] = (c0 + jj == k) ? inv_piv : rv[jj];
+        } else {
+          const float f = cv[ii];
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) a[ii][jj] = (c0 + jj == k) ? -f * inv_piv : fmaf(-f, rv[jj], a[ii][jj]);
+        }
+      }
+    } else {  // plain rank-1 update; the pivot row is overwritten by its owner lane
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii) {
         const float f = cv[ii];
 #pragma unroll
-        for (int jj = 0; jj < 8; ++jj) a[ii][jj] = (c0 + jj == k) ? -f * inv_piv : fmaf(-f, rv[jj], a[ii][jj]);
+        for (int jj = 0; jj < 8; ++jj) a[ii][jj] = fmaf(-f, rv[jj], a[ii][jj]);
+      }
+      if ((p >> 2) == lane) {
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii)
+          if (ii == (p & 3)) {
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) a[ii][jj] = rv[jj];
+          }
       }
     }
   }
