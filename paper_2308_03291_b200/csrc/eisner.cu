@@ -623,28 +623,39 @@ __global__ void __launch_bounds__(kThreads, 2) kuhlmann_kernel(const float* __re
   __syncthreads();
   for (int i = tid; i + 1 < N; i += kThreads) tab[pk2(i, i + 1, N)] = 0.0;
   __syncthreads();
+  // G = 2^lg lanes per span (<= 4 split points per lane): narrow widths put
+  // many spans in a warp instead of one span with mostly idle lanes
   for (int w = 2; w < N; ++w) {
-    for (int i = warp; i + w < N; i += kWarps) {
-      const int j = i + w;
+    const int nsp = N - w, L = w - 1;
+    const int x = (L - 1) >> 2;
+    const int lg = min(5, x > 0 ? 32 - __clz(x) : 0), G = 1 << lg, r = lane & (G - 1);
+    const int wfirst = (tid & ~31) >> lg;
+    for (int base = 0; base < nsp; base += kThreads >> lg) {
+      if (base + wfirst >= nsp) break;  // warp-uniform
+      const int i0 = base + (tid >> lg);
+      const bool ok = i0 < nsp;
+      const int i = ok ? i0 : 0, j = i + w;
       // candidates in reference order: k ascending, head i then head j; strict '>'
       double best = ninfd();
       int arg = 0x7fffffff;  // encoded order index 2*(k-i-1) + (head==j)
-      for (int k = i + 1 + lane; k < j; k += 32) {
-        // arc scores first: the global (L2) loads overlap the shared-memory chart reads
-        const double s1 = S(i, k), s2 = S(j, k);
-        const double base = tab[pk2(i, k, N)] + tab[pk2(k, j, N)];
-        if (base == ninfd()) continue;
-        const double c1 = base + s1, c2 = base + s2;
-        const int o = 2 * (k - i - 1);
-        if (c1 > best) { best = c1; arg = o; }
-        if (c2 > best) { best = c2; arg = o + 1; }
+      if (ok) {
+        for (int k = i + 1 + r; k < j; k += G) {
+          // arc scores first: the global (L2) loads overlap the shared-memory chart reads
+          const double s1 = S(i, k), s2 = S(j, k);
+          const double base2 = tab[pk2(i, k, N)] + tab[pk2(k, j, N)];
+          if (base2 == ninfd()) continue;
+          const double c1 = base2 + s1, c2 = base2 + s2;
+          const int o = 2 * (k - i - 1);
+          if (c1 > best) { best = c1; arg = o; }
+          if (c2 > best) { best = c2; arg = o + 1; }
+        }
       }
-      for (int o = 16; o > 0; o >>= 1) {
+      for (int o = G >> 1; o > 0; o >>= 1) {
         const double ov = __shfl_xor_sync(0xffffffffu, best, o);
         const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
         if (ov > best || (ov == best && oa < arg)) { best = ov; arg = oa; }
       }
-      if (lane == 0) {
+      if (ok && r == 0) {
         tab[pk2(i, j, N)] = best;
         back[pk2(i, j, N)] = (arg == 0x7fffffff) ? -1 : arg;
       }
