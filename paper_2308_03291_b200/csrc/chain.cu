@@ -14,6 +14,10 @@
 // pass exp(alpha~_t[a] + theta_t[a,b] + beta~_{t+1}[b] + K_t) with
 // K_t = A_t + B_{t+1} - logZ folded in fp64.
 //
+// For m <= 32 (the C1 shape) log_partition + marginals take the scaled-LINEAR
+// path instead (chain_lin_kernel + chain_lin_marg_kernel below); this
+// log-space path serves larger m and the instances the linear path flags.
+//
 // Viterbi runs in fp64 with the reference's addition order
 // (score[a] + theta[a,b]) so argmax ties and sums are bit-identical to the
 // float64 reference on the same fp32 inputs.
