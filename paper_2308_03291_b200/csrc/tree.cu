@@ -344,6 +344,28 @@ constexpr int kEmitThreads = 256;
 constexpr float kLinHi = 1.2980742e33f;   // 2^110
 constexpr float kLinLo = 7.7037198e-34f;  // 2^-110
 
+// lse over one label row held as QV float4 in registers (QV compile-time: no
+// register array sized for the largest m, so the occupancy stays high)
+template <int QV>
+__device__ __forceinline__ float fold_row(const float4* __restrict__ r4) {
+  float4 v[QV];
+#pragma unroll
+  for (int u = 0; u < QV; ++u) v[u] = __ldg(r4 + u);
+  // NaN-propagating max: NaN or +inf anywhere in the row -> !(mx < +inf)
+  float mx = ninf();
+#pragma unroll
+  for (int u = 0; u < QV; ++u) mx = fmax_nan(mx, fmax_nan(fmax_nan(v[u].x, v[u].y), fmax_nan(v[u].z, v[u].w)));
+  const int bad = !(mx < __int_as_float(0x7f800000));
+  float s = 0.f;
+  if (!bad && mx != ninf()) {
+#pragma unroll
+    for (int u = 0; u < QV; ++u) s += (fexp(v[u].x - mx) + fexp(v[u].y - mx)) + (fexp(v[u].z - mx) + fexp(v[u].w - mx));
+  }
+  return bad ? __int_as_float(0x7fc00000) : ((mx == ninf()) ? ninf() : mx + flog(s));
+}
+
+// QV = m/4 when m is 16, 32 or 64 (16-byte rows), 0 = generic scalar path
+template <int QV>
 __global__ void __launch_bounds__(kFoldWarps * 32) tree_fold_kernel(const float* __restrict__ th_all, int64_t B,
                                                                     int n, int m, float* __restrict__ fold_all) {
   const int64_t row = (int64_t)blockIdx.x * kFoldWarps + (threadIdx.x >> 5);
@@ -355,31 +377,12 @@ __global__ void __launch_bounds__(kFoldWarps * 32) tree_fold_kernel(const float*
   const float* src = th_all + ((size_t)row * n + i) * m;  // theta[b, i, i, 0]
   float* dst = fold_all + (size_t)b * T + tri(i, i, n);
   const int ns = n - i;
-  if ((m & 3) == 0 && m <= 64 && (((uintptr_t)src) & 15) == 0) {
+  if (QV > 0) {
     // lane per span: the lane's label row is m/4 16-byte loads, all issued
     // before the (max, sum) pass; a warp-instruction touches 32 rows but every
     // fetched sector is consumed
-    const int q = m >> 2;
-    for (int sp = lane; sp < ns; sp += 32) {
-      const float4* r4 = reinterpret_cast<const float4*>(src + (size_t)sp * m);
-      float4 v[16];
-#pragma unroll
-      for (int u = 0; u < 16; ++u)
-        if (u < q) v[u] = __ldg(r4 + u);
-      // NaN-propagating max: NaN or +inf anywhere in the row -> !(mx < +inf)
-      float mx = ninf();
-#pragma unroll
-      for (int u = 0; u < 16; ++u)
-        if (u < q) mx = fmax_nan(mx, fmax_nan(fmax_nan(v[u].x, v[u].y), fmax_nan(v[u].z, v[u].w)));
-      const int bad = !(mx < __int_as_float(0x7f800000));
-      float s = 0.f;
-      if (!bad && mx != ninf()) {
-#pragma unroll
-        for (int u = 0; u < 16; ++u)
-          if (u < q) s += (fexp(v[u].x - mx) + fexp(v[u].y - mx)) + (fexp(v[u].z - mx) + fexp(v[u].w - mx));
-      }
-      dst[sp] = bad ? __int_as_float(0x7fc00000) : ((mx == ninf()) ? ninf() : mx + flog(s));
-    }
+    for (int sp = lane; sp < ns; sp += 32)
+      dst[sp] = fold_row<(QV > 0 ? QV : 1)>(reinterpret_cast<const float4*>(src + (size_t)sp * m));
   } else {
     for (int sp = lane; sp < ns; sp += 32) {
       const float* rw = src + (size_t)sp * m;
@@ -709,8 +712,14 @@ extern "C" int sdb_tree_fb(const float* span_potentials, int64_t B, int32_t n, i
           cudaSuccess)
     return SDB_ERR_CUDA;
   const int64_t rows = B * n;
-  tree_fold_kernel<<<(unsigned)((rows + kFoldWarps - 1) / kFoldWarps), kFoldWarps * 32, 0, s>>>(span_potentials, B,
-                                                                                               n, m, fold);
+  {
+    const unsigned fg = (unsigned)((rows + kFoldWarps - 1) / kFoldWarps);
+    const bool al16 = (((uintptr_t)span_potentials) & 15) == 0;
+    if (al16 && m == 32) tree_fold_kernel<8><<<fg, kFoldWarps * 32, 0, s>>>(span_potentials, B, n, m, fold);
+    else if (al16 && m == 16) tree_fold_kernel<4><<<fg, kFoldWarps * 32, 0, s>>>(span_potentials, B, n, m, fold);
+    else if (al16 && m == 64) tree_fold_kernel<16><<<fg, kFoldWarps * 32, 0, s>>>(span_potentials, B, n, m, fold);
+    else tree_fold_kernel<0><<<fg, kFoldWarps * 32, 0, s>>>(span_potentials, B, n, m, fold);
+  }
   SDB_CHECK_LAUNCH();
   if (marg) {
     tree_lin_kernel<true><<<(unsigned)B, kLinThreads, smem_lin, s>>>(fold, n, logz, K, status);
