@@ -575,16 +575,13 @@ __global__ void __launch_bounds__(kLinThreads) tree_lin_kernel(const float* __re
     c.Ic[cs(i) + i] = f;
   }
   // ---- inside (constituency.py:57-63): I[i,j] = F'[i,j] sum_k I[i,k] I[k+1,j]
-  for (int w = 2; w <= n; ++w) {
-    __syncthreads();
-    switch (group_lg(w - 1)) {
-      case 0: bad = inside_step<0>(c, n, w, tid, bad); break;
-      case 1: bad = inside_step<1>(c, n, w, tid, bad); break;
-      case 2: bad = inside_step<2>(c, n, w, tid, bad); break;
-      case 3: bad = inside_step<3>(c, n, w, tid, bad); break;
-      default: bad = inside_step<4>(c, n, w, tid, bad); break;
-    }
-  }
+  // widths with the same lane-group size are contiguous (L = w-1 <= 8 * 2^LG): one
+  // specialised loop per group size instead of a per-width indirect branch
+  for (int w = 2; w <= min(n, 9); ++w) { __syncthreads(); bad = inside_step<0>(c, n, w, tid, bad); }
+  for (int w = 10; w <= min(n, 17); ++w) { __syncthreads(); bad = inside_step<1>(c, n, w, tid, bad); }
+  for (int w = 18; w <= min(n, 33); ++w) { __syncthreads(); bad = inside_step<2>(c, n, w, tid, bad); }
+  for (int w = 34; w <= min(n, 65); ++w) { __syncthreads(); bad = inside_step<3>(c, n, w, tid, bad); }
+  for (int w = 66; w <= n; ++w) { __syncthreads(); bad = inside_step<4>(c, n, w, tid, bad); }
   bad = __syncthreads_or(bad);
   const float Zs = c.Ir[rs(0, n) + n - 1];
   if (bad) {
@@ -605,16 +602,12 @@ __global__ void __launch_bounds__(kLinThreads) tree_lin_kernel(const float* __re
     c.Pc[cs(n - 1)] = c.Fr[t];
     Kb[t] = -c.fl[t];  // O' I' / Z' = 1 at the root
   }
-  for (int w = n - 1; w >= 1; --w) {
-    __syncthreads();
-    switch (group_lg(n - w)) {
-      case 0: bad = outside_step<0>(c, n, w, tid, bad, lz2, Kb); break;
-      case 1: bad = outside_step<1>(c, n, w, tid, bad, lz2, Kb); break;
-      case 2: bad = outside_step<2>(c, n, w, tid, bad, lz2, Kb); break;
-      case 3: bad = outside_step<3>(c, n, w, tid, bad, lz2, Kb); break;
-      default: bad = outside_step<4>(c, n, w, tid, bad, lz2, Kb); break;
-    }
-  }
+  // L = n - w grows as w falls: the same contiguous group-size ranges, in reverse
+  for (int w = n - 1; w >= max(1, n - 8); --w) { __syncthreads(); bad = outside_step<0>(c, n, w, tid, bad, lz2, Kb); }
+  for (int w = n - 9; w >= max(1, n - 16); --w) { __syncthreads(); bad = outside_step<1>(c, n, w, tid, bad, lz2, Kb); }
+  for (int w = n - 17; w >= max(1, n - 32); --w) { __syncthreads(); bad = outside_step<2>(c, n, w, tid, bad, lz2, Kb); }
+  for (int w = n - 33; w >= max(1, n - 64); --w) { __syncthreads(); bad = outside_step<3>(c, n, w, tid, bad, lz2, Kb); }
+  for (int w = n - 65; w >= 1; --w) { __syncthreads(); bad = outside_step<4>(c, n, w, tid, bad, lz2, Kb); }
   bad = __syncthreads_or(bad);
   if (tid == 0) status[b] = bad ? kRetry : SDB_ST_OK;
 }
