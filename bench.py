@@ -66,7 +66,7 @@ CONFIGS = {
 HEADLINE = "c2a"
 # e2e: instance slices per request in kernels.run_host_batch (PCIe-bound configs
 # overlap H2D, kernels and D2H; tiny batches run as one slice)
-E2E_CHUNKS = {"c1": 1, "c2a": [32] * 7 + [24, 8], "c2b": [32] * 7 + [24, 8], "c3": 4, "c4": 4, "c5a": 4, "c5b": 1}
+E2E_CHUNKS = {"c1": 1, "c2a": [32] * 7 + [24, 8], "c2b": [32] * 7 + [24, 8], "c3": 8, "c4": 4, "c5a": 4, "c5b": 1}
 if os.environ.get("SDB_E2E_CHUNKS"):
     E2E_CHUNKS = {k: json.loads(os.environ["SDB_E2E_CHUNKS"]) for k in E2E_CHUNKS}
 # nominal B200 compute peaks (not in MEASURED_PEAKS.json): 148 SM x 128 FMA lanes x 2 x 1.965 GHz;

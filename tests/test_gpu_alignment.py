@@ -132,3 +132,9 @@ def test_run_host_batch_matches_device_call():
     K.run_host_batch(lambda t: K.nw_fb(t)[:2], host_in, host_out, torch.device("cuda", 0), chunks=4)
     torch.cuda.synchronize()
     assert torch.equal(host_out[0], lz.cpu()) and torch.equal(host_out[1], mg.cpu())
+    # explicit (uneven) slice sizes
+    for h in host_out:
+        h.zero_()
+    K.run_host_batch(lambda t: K.nw_fb(t)[:2], host_in, host_out, torch.device("cuda", 0), chunks=[5, 4, 2])
+    torch.cuda.synchronize()
+    assert torch.equal(host_out[0], lz.cpu()) and torch.equal(host_out[1], mg.cpu())
