@@ -28,7 +28,8 @@ def test_tree_golden(case):
     assert score == float(case.argmax_score)
 
 
-@pytest.mark.parametrize("B,n,m", [(3, 64, 32), (4, 17, 5), (2, 1, 3), (2, 128, 4), (3, 33, 33)])
+@pytest.mark.parametrize("B,n,m", [(3, 64, 32), (4, 17, 5), (2, 1, 3), (2, 128, 4), (3, 33, 33), (2, 20, 16), (2, 12, 64),
+                                   (2, 80, 8)])
 def test_tree_batched_vs_oracle(B, n, m):
     need_gpu()
     th = batch_tree(4000, B, n, m)
