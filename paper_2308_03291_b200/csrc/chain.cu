@@ -686,8 +686,9 @@ __global__ void __launch_bounds__(kThreads) chain_lin_marg_kernel(
       const float4* t4 = reinterpret_cast<const float4*>(tt);
       float4* o4 = reinterpret_cast<float4*>(out);
       const int m4 = m >> 2;
+      const int sh = ((m4 & (m4 - 1)) == 0) ? __ffs(m4) - 1 : -1;  // m4 a power of two: shift, no division
       for (int x = threadIdx.x; x < (int)(mm >> 2); x += kThreads) {
-        const int a = x / m4, j = (x - a * m4) * 4;
+        const int a = sh >= 0 ? (x >> sh) : x / m4, j = (x - a * m4) * 4;
         const float ea = e[a];
         const float4 v = __ldg(t4 + x);
         float4 r;
