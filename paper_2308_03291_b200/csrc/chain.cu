@@ -653,10 +653,12 @@ __global__ void __launch_bounds__(kThreads) chain_marg_kernel(
 // Marginals from the LINEAR passes (chain_lin_kernel): e_t, f_t normalised
 // vectors with log scales c_t, d_t, so
 //   p[t][a][b] = e_t[a] exp(theta_t[a][b]) f_(t+1)[b] exp(c_t + d_(t+1) - Z)
-// (chain.py:84-95).  Grid (ceil((n-1)/kStepsPerBlock), B), every element an
+// (chain.py:84-95).  Grid (ceil((n-1)/kLinMargSteps), B), every element an
 // independent streaming FMUL/MUFU -- HBM-bound.  Block (0, b) also writes
 // p_init and merges the two passes' verdicts into ws.need[b]; instances that
 // need the log-space path are skipped (chain_marg_kernel writes them).
+constexpr int kLinMargSteps = 2;  // steps per CTA: short dependent load chains per thread
+
 __global__ void __launch_bounds__(kThreads) chain_lin_marg_kernel(
     const float* __restrict__ init, const float* __restrict__ trans, int n, int m, ChainWs ws,
     const double* __restrict__ logz, float* __restrict__ marg_init, float* __restrict__ marg_trans) {
@@ -675,7 +677,7 @@ __global__ void __launch_bounds__(kThreads) chain_lin_marg_kernel(
       marg_init[(size_t)b * m + j] = fexp(init[(size_t)b * m + j] + K) * fv[j];
   }
   if (!marg_trans) return;
-  const int t0 = blockIdx.x * kStepsPerBlock, t1 = min(t0 + kStepsPerBlock, n - 1);
+  const int t0 = blockIdx.x * kLinMargSteps, t1 = min(t0 + kLinMargSteps, n - 1);
   for (int t = t0; t < t1; ++t) {
     const float* tt = trans + ((size_t)b * (n - 1) + t) * mm;
     float* out = marg_trans + ((size_t)b * (n - 1) + t) * mm;
@@ -972,8 +974,9 @@ extern "C" int sdb_chain_fb(const float* init, const float* trans, int64_t B, in
     chain_lin_kernel<<<(unsigned)(2 * B), kThreads, smem, s>>>(init, trans, n, m, ws, logz, status);
     SDB_CHECK_LAUNCH();
     // marginals of the linear instances (also merges the two passes' verdicts into ws.need)
+    dim3 gl((unsigned)((n - 1 + kLinMargSteps - 1) / kLinMargSteps), (unsigned)B);
+    chain_lin_marg_kernel<<<gl, kThreads, 0, s>>>(init, trans, n, m, ws, logz, marg_init, marg_trans);
     dim3 g((unsigned)((n - 1 + kStepsPerBlock - 1) / kStepsPerBlock), (unsigned)B);
-    chain_lin_marg_kernel<<<g, kThreads, 0, s>>>(init, trans, n, m, ws, logz, marg_init, marg_trans);
     SDB_CHECK_LAUNCH();
     // exact log-space recomputation of the (rare) instances the linear path flagged
     if (cudaFuncSetAttribute(chain_fwd_bwd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
