@@ -316,19 +316,24 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
 // accumulate), in increasing s -- a deterministic order.  Grid (frame blocks,
 // instances), every frame independent, so this streams at HBM rate instead of
 // sitting inside the sequential frame loop.
-constexpr int kMargFrames = 16;
+constexpr int kMargWarps = 8;       // warps per CTA, one frame per warp at a time
+constexpr int kMargFrames = 32;     // frames per CTA (4 per warp)
 
-__global__ void __launch_bounds__(256) ctc_marg_kernel(const float* __restrict__ post_all,
-                                                       const int32_t* __restrict__ csr_all, int T, int V, int L,
-                                                       const int32_t* __restrict__ status,
-                                                       float* __restrict__ marg_all) {
+// A warp owns whole frames: it stages the frame's posterior row in its own
+// shared slice and reduces it with warp primitives only, so the warps of a CTA
+// never wait on each other (the per-frame CTA barriers of a row-per-CTA layout
+// left this kernel latency-bound).
+__global__ void __launch_bounds__(kMargWarps * 32) ctc_marg_kernel(const float* __restrict__ post_all,
+                                                                  const int32_t* __restrict__ csr_all, int T, int V,
+                                                                  int L, const int32_t* __restrict__ status,
+                                                                  float* __restrict__ marg_all) {
   extern __shared__ __align__(16) float cm[];
   const int S = 2 * L + 1;
-  float* prow = cm;                                  // [S]
-  int* off = reinterpret_cast<int*>(prow + S);       // [V+1]
-  int* lst = off + V + 1;                            // [L]
-  __shared__ float bsum[8];
+  int* off = reinterpret_cast<int*>(cm);      // [V+1]
+  int* lst = off + V + 1;                     // [L]
+  float* prow_all = cm + ((V + 1 + L + 3) & ~3);  // [kMargWarps][S]
   const int b = blockIdx.y, t0 = blockIdx.x * kMargFrames, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
   const int t1 = min(t0 + kMargFrames, T);
   float* mg = marg_all + (size_t)b * T * V;
   if (status[b] != SDB_ST_OK) {  // vacuous / invalid: zero marginals (as the reference's -inf Z)
@@ -338,26 +343,27 @@ __global__ void __launch_bounds__(256) ctc_marg_kernel(const float* __restrict__
   const int32_t* csr = csr_all + (size_t)b * (V + 1 + L);  // built by ctc_kernel<1>
   for (int e = tid; e <= V; e += blockDim.x) off[e] = csr[e];
   for (int e = tid; e < L; e += blockDim.x) lst[e] = csr[V + 1 + e];
+  __syncthreads();
+  float* prow = prow_all + (size_t)warp * S;
   const float* pb = post_all + (size_t)b * T * S;
-  for (int t = t0; t < t1; ++t) {
-    __syncthreads();  // CSR ready / previous row consumed
-    for (int e = tid; e < S; e += blockDim.x) prow[e] = pb[(size_t)t * S + e];
-    __syncthreads();
-    // blank: even states, fixed-order (per-warp butterflies, then warps in order)
+  for (int t = t0 + warp; t < t1; t += kMargWarps) {
+    const float* src = pb + (size_t)t * S;
+    for (int e = lane; e < S; e += 32) prow[e] = src[e];
+    __syncwarp();
+    // blank: the even states, fixed order (lane-strided partial sums, then a butterfly)
     float bl = 0.f;
-    for (int e = 2 * tid; e < S; e += 2 * blockDim.x) bl += prow[e];
+    for (int e = 2 * lane; e < S; e += 64) bl += prow[e];
     bl = warp_sum(bl);
-    if ((tid & 31) == 0) bsum[tid >> 5] = bl;
-    __syncthreads();
-    for (int v = tid; v < V; v += blockDim.x) {
+    for (int v = lane; v < V; v += 32) {
       float acc = 0.f;
       if (v == 0) {
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) acc += bsum[w];
+        acc = bl;
       } else {
         for (int q = off[v]; q < off[v + 1]; ++q) acc += prow[lst[q]];
       }
       mg[(size_t)t * V + v] = acc;
     }
+    __syncwarp();  // the slice is rewritten for the warp's next frame
   }
 }
 
@@ -402,12 +408,12 @@ int ctc_launch(const float* fp, const int32_t* tg, int64_t B, int T, int V, int 
   SDB_CHECK_LAUNCH();
   if (kMode == 1) {
     const int S2 = 2 * L + 1;
-    const size_t msmem = (size_t)S2 * 4 + (size_t)(V + 1 + L) * 4;
+    const size_t msmem = (((size_t)(V + 1 + L) + 3) & ~(size_t)3) * 4 + (size_t)kMargWarps * S2 * 4;
     if (msmem > 48 * 1024 &&
         cudaFuncSetAttribute(ctc_marg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem) != cudaSuccess)
       return SDB_ERR_CUDA;
     dim3 g((unsigned)((T + kMargFrames - 1) / kMargFrames), (unsigned)B);
-    ctc_marg_kernel<<<g, 256, msmem, s>>>(ws.wsb, ws.csr, T, V, L, status, marg);
+    ctc_marg_kernel<<<g, kMargWarps * 32, msmem, s>>>(ws.wsb, ws.csr, T, V, L, status, marg);
     SDB_CHECK_LAUNCH();
   }
   return SDB_OK;
