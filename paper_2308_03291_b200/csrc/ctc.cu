@@ -323,6 +323,7 @@ constexpr int kMargFrames = 32;     // frames per CTA (4 per warp)
 // shared slice and reduces it with warp primitives only, so the warps of a CTA
 // never wait on each other (the per-frame CTA barriers of a row-per-CTA layout
 // left this kernel latency-bound).
+template <int kRowRegs>  // >= ceil(S / 32): the row's states per lane
 __global__ void __launch_bounds__(kMargWarps * 32) ctc_marg_kernel(const float* __restrict__ post_all,
                                                                   const int32_t* __restrict__ csr_all, int T, int V,
                                                                   int L, const int32_t* __restrict__ status,
@@ -346,9 +347,24 @@ __global__ void __launch_bounds__(kMargWarps * 32) ctc_marg_kernel(const float* 
   __syncthreads();
   float* prow = prow_all + (size_t)warp * S;
   const float* pb = post_all + (size_t)b * T * S;
-  for (int t = t0 + warp; t < t1; t += kMargWarps) {
+  // the warp's next frame is loaded into registers while the current one is reduced
+  float nxt[kRowRegs];
+  auto fetch = [&](int t) {
     const float* src = pb + (size_t)t * S;
-    for (int e = lane; e < S; e += 32) prow[e] = src[e];
+#pragma unroll
+    for (int u = 0; u < kRowRegs; ++u) {
+      const int e = lane + 32 * u;
+      if (e < S) nxt[u] = src[e];
+    }
+  };
+  if (t0 + warp < t1) fetch(t0 + warp);
+  for (int t = t0 + warp; t < t1; t += kMargWarps) {
+#pragma unroll
+    for (int u = 0; u < kRowRegs; ++u) {
+      const int e = lane + 32 * u;
+      if (e < S) prow[e] = nxt[u];
+    }
+    if (t + kMargWarps < t1) fetch(t + kMargWarps);
     __syncwarp();
     // blank: the even states, fixed order (lane-strided partial sums, then a butterfly)
     float bl = 0.f;
@@ -409,11 +425,19 @@ int ctc_launch(const float* fp, const int32_t* tg, int64_t B, int T, int V, int 
   if (kMode == 1) {
     const int S2 = 2 * L + 1;
     const size_t msmem = (((size_t)(V + 1 + L) + 3) & ~(size_t)3) * 4 + (size_t)kMargWarps * S2 * 4;
-    if (msmem > 48 * 1024 &&
-        cudaFuncSetAttribute(ctc_marg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem) != cudaSuccess)
-      return SDB_ERR_CUDA;
     dim3 g((unsigned)((T + kMargFrames - 1) / kMargFrames), (unsigned)B);
-    ctc_marg_kernel<<<g, kMargWarps * 32, msmem, s>>>(ws.wsb, ws.csr, T, V, L, status, marg);
+    const int rr = (S2 + 31) / 32;
+    if (rr <= 9) {
+      if (msmem > 48 * 1024 && cudaFuncSetAttribute(ctc_marg_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    (int)msmem) != cudaSuccess)
+        return SDB_ERR_CUDA;
+      ctc_marg_kernel<9><<<g, kMargWarps * 32, msmem, s>>>(ws.wsb, ws.csr, T, V, L, status, marg);
+    } else {
+      if (msmem > 48 * 1024 && cudaFuncSetAttribute(ctc_marg_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    (int)msmem) != cudaSuccess)
+        return SDB_ERR_CUDA;
+      ctc_marg_kernel<32><<<g, kMargWarps * 32, msmem, s>>>(ws.wsb, ws.csr, T, V, L, status, marg);
+    }
     SDB_CHECK_LAUNCH();
   }
   return SDB_OK;
