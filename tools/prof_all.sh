@@ -10,7 +10,7 @@ run() {  # fam mode regex count
 run nw fb nw_mitm
 run chain fb "chain_lin" 2
 run chainv vit chain_viterbi
-run ctc fb ctc_kernel
+run ctc fb "ctc_(kernel|marg)" 2
 run mtt fb mtt_kernel
 run eisner fb eisner_lin_kernel
 run kuhl fb kuhlmann
