@@ -515,7 +515,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   // recurrence state (warp 0): linear vector v (lane holds component lane), scale
   float v = 0.f;
   double sc = 0.0;
-  uint32_t R = 0;
   if (warp == 0) {
     if (dir == 0) {
       const float x = lane < m ? init[(size_t)b * m + lane] : ninf();
@@ -524,13 +523,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float mc = (mx == ninf()) ? 0.f : mx;
       v = lane < m ? fexp(x - mc) : 0.f;
       sc = (double)mc;
-      R = __ballot_sync(0xffffffffu, lane < m && x > ninf());
       if (lane < m) vecs[lane] = v;
       if (lane == 0) scs[0] = sc;
     } else {
       v = lane < m ? 1.f : 0.f;
       sc = 0.0;
-      R = __ballot_sync(0xffffffffu, lane < m);
       if (lane < m) vecs[(size_t)T * m + lane] = v;
       if (lane == 0) scs[T] = sc;
     }

@@ -581,11 +581,11 @@ __global__ void __launch_bounds__(kThreads, 2) kuhlmann_kernel(const float* __re
   int* back = (int*)(tab + T);  // (k << 1) | (head == j)
   __shared__ double rw_c;
   __shared__ int badsh;
-  __shared__ float fmin_s, fmax_s;
+  __shared__ float fmax_s;
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int N1 = n + 1;
   const float* th = adj_all + (size_t)b * N1 * N1;
-  if (tid == 0) { badsh = 0; fmin_s = __int_as_float(0x7f800000); fmax_s = ninf(); }
+  if (tid == 0) { badsh = 0; fmax_s = ninf(); }
   __syncthreads();
   {
     int bad = 0;
@@ -604,7 +604,6 @@ __global__ void __launch_bounds__(kThreads, 2) kuhlmann_kernel(const float* __re
     if (tid == 0) {
       float L = lo_w[0], H = hi_w[0];
       for (int q = 1; q < kWarps; ++q) { L = fminf(L, lo_w[q]); H = fmaxf(H, hi_w[q]); }
-      fmin_s = L;
       fmax_s = H;
       // spanning.py:339-350: c = n * (max - min) + 1 over the finite entries
       rw_c = (double)n * ((double)H - (double)L) + 1.0;

@@ -64,7 +64,6 @@ __global__ void __launch_bounds__(kThreads, 2) mtt_kernel(const float* __restric
     sm.red64 = (double*)p; p += 8 * 8;
   }
   __shared__ int flag_bad, flag_vac, piv_row;
-  __shared__ float piv_val;
   __shared__ double logdet;
   __shared__ int negs;
 

@@ -50,7 +50,8 @@ struct PcfgWs {
 };
 
 PcfgWs pcfg_carve(void* base, int64_t B, int n, int NT, int PT, size_t* bytes, bool grad = false) {
-  const size_t S = NT + PT;
+  (void)NT;
+  (void)PT;
   Carve c(base);
   PcfgWs w;
   w.RE = c.take<float>((size_t)B * 4 * 32768);  // REp[t][A][B][C] zero-padded per child block

@@ -411,12 +411,6 @@ constexpr int kLinThreads = 256;
 __device__ __forceinline__ int rs(int i, int n) { return i * n - ((i * (i - 1)) >> 1); }  // == tri(i, i, n)
 __device__ __forceinline__ int cs(int j) { return (j * (j + 1)) >> 1; }
 
-// log2(lanes per span) for L terms: <= 8 terms per lane
-__device__ __forceinline__ int group_lg(int L) {
-  const int x = (L - 1) >> 3;
-  return x > 0 ? 32 - __clz(x) : 0;
-}
-
 struct LinCharts {
   float *base, *fl, *Fr, *Ir, *Ic, *Pr, *Pc;
   int zi;  // index of a shared zero word (masked operands read it)
