@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(kThreads, 2) mtt_kernel(const float* __restric
   }
   __syncthreads();
 
+  uint32_t usedm = 0;  // bit ii: row r0+ii has been a pivot row
   // ---- Gauss-Jordan with implicit partial pivoting
   bool singular = false;
   for (int k = 0; k < kN; ++k) {
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(kThreads, 2) mtt_kernel(const float* __restric
         for (int q = 0; q < 8; ++q) if (q == jj) v = a[ii][q];
         colbuf[r] = v;
         const float av = fabsf(v);
-        if (!sm.used[r] && (av > bv || (av == bv && r < br))) { bv = av; br = r; }
+        if (!((usedm >> ii) & 1u) && (av > bv || (av == bv && r < br))) { bv = av; br = r; }
       }
       for (int o = 16; o > 0; o >>= 1) {
         const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
@@ -160,11 +161,11 @@ __global__ void __launch_bounds__(kThreads, 2) mtt_kernel(const float* __restric
       if (lane == 0) {
         piv_row = br;
         sm.perm[k] = br;
-        sm.used[br] = 1;
       }
     }
     __syncthreads();
     const int p = piv_row;
+    if ((p >> 2) == lane) usedm |= 1u << (p & 3);  // this lane's rows already pivoted (registers)
     // owners of row p publish it
     if ((p >> 2) == lane) {
       const int ii = p & 3;
