@@ -140,8 +140,10 @@ __global__ void __launch_bounds__(kThreads, 2) mtt_kernel(const float* __restric
     float* colbuf = sm.colbuf + kb * kN;
     if (warp == (k >> 3)) {
       const int jj = k & 7;
-      // argmax |a[r][k]| over unused rows r (first index on ties)
-      float bv = -1.f;
+      // argmax |a[r][k]| over unused rows r (first index on ties): |v| as float bits orders
+      // like an unsigned int, so the warp argmax is two REDUX ops (max key, then the lowest
+      // row holding it) instead of five shuffle rounds.  key = bits(|v|) + 1, 0 = no candidate.
+      uint32_t bk = 0;
       int br = 0x7fffffff;
 #pragma unroll
       for (int ii = 0; ii < 4; ++ii) {
@@ -150,14 +152,11 @@ __global__ void __launch_bounds__(kThreads, 2) mtt_kernel(const float* __restric
 #pragma unroll
         for (int q = 0; q < 8; ++q) if (q == jj) v = a[ii][q];
         colbuf[r] = v;
-        const float av = fabsf(v);
-        if (!((usedm >> ii) & 1u) && (av > bv || (av == bv && r < br))) { bv = av; br = r; }
+        const uint32_t key = ((usedm >> ii) & 1u) ? 0u : __float_as_uint(fabsf(v)) + 1u;
+        if (key > bk) { bk = key; br = r; }  // rows ascending: strict '>' keeps the first
       }
-      for (int o = 16; o > 0; o >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int orr = __shfl_xor_sync(0xffffffffu, br, o);
-        if (ov > bv || (ov == bv && orr < br)) { bv = ov; br = orr; }
-      }
+      const uint32_t mk = __reduce_max_sync(0xffffffffu, bk);
+      br = (int)__reduce_min_sync(0xffffffffu, (bk == mk) ? (uint32_t)br : 0x7fffffffu);
       if (lane == 0) {
         piv_row = br;
         sm.perm[k] = br;
