@@ -12,9 +12,10 @@
 // identity block).  The 128x128 Laplacian lives in REGISTERS: warp w owns
 // columns [8w, 8w+8), lane l owns rows [4l, 4l+4) -> 32 fp32 per thread.
 // In-place Gauss-Jordan with implicit partial pivoting: step k picks the
-// unused row p with max |a[p][k]| (a warp argmax inside the column's warp),
-// broadcasts row p and column k through shared memory, and every thread does
-// a register-blocked rank-1 update (32 FFMA per 12 shared loads).  Pivots
+// unused row p with max |a[p][k]| (a warp argmax inside the column's warp,
+// two REDUX ops), publishes column k through shared memory (one CTA barrier
+// per step), row p travels by shuffles inside each warp, and every thread does
+// a register-blocked rank-1 update (32 FFMA; pivot-row scaling deferred).  Pivots
 // equal the reference's LU pivots, so log|det| = sum log|pivot| (fp64) and the
 // sign comes from the pivot signs and the permutation parity.  The result is
 // the row/column-permuted inverse, scattered to shared memory as A^{-1}, from
@@ -32,10 +33,10 @@ struct MttSmem {
   float* shift;   // [kN] column max s_d
   float* diag;    // [kN]
   float* rowmag;  // [kN]
-  float* rowbuf;  // [2][kN]
+  int* prow;      // [2] pivot row of the step (double-buffered)
   float* colbuf;  // [2][kN]
   int* perm;      // [kN] pivot row of step k
-  int* used;      // [kN]
+  int* qinv;      // [kN] inverse pivot permutation
   double* red64;  // [8]
 };
 
@@ -57,23 +58,21 @@ __global__ void __launch_bounds__(kThreads, 2) mtt_kernel(const float* __restric
     sm.shift = (float*)p; p += kN * 4;
     sm.diag = (float*)p; p += kN * 4;
     sm.rowmag = (float*)p; p += kN * 4;
-    sm.rowbuf = (float*)p; p += 2 * kN * 4;
+    sm.prow = (int*)p; p += 2 * kN * 4;
     sm.colbuf = (float*)p; p += 2 * kN * 4;
     sm.perm = (int*)p; p += kN * 4;
-    sm.used = (int*)p; p += kN * 4;
+    sm.qinv = (int*)p; p += kN * 4;
     sm.red64 = (double*)p; p += 8 * 8;
   }
-  __shared__ int flag_bad, flag_vac, piv_row;
-  __shared__ double logdet;
-  __shared__ int negs;
+  __shared__ int flag_bad, flag_vac;
 
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int N1 = n + 1;
   const float* A = adj_all + (size_t)b * N1 * N1;
-  if (tid == 0) { flag_bad = 0; flag_vac = 0; logdet = 0.0; negs = 0; }
+  if (tid == 0) { flag_bad = 0; flag_vac = 0; }
   for (int e = tid; e < N1 * N1; e += kThreads)
     if (bad_input(__ldg(A + e))) flag_bad = 1;
-  for (int e = tid; e < kN; e += kThreads) { sm.used[e] = 0; sm.rowmag[e] = 0.f; }
+  for (int e = tid; e < kN; e += kThreads) sm.rowmag[e] = 0.f;
   __syncthreads();
   // column shifts and diagonal (spanning.py:90-120); thread d handles dependent d+1
   if (tid < n) {
@@ -132,11 +131,12 @@ __global__ void __launch_bounds__(kThreads, 2) mtt_kernel(const float* __restric
   __syncthreads();
 
   uint32_t usedm = 0;  // bit ii: row r0+ii has been a pivot row
-  // ---- Gauss-Jordan with implicit partial pivoting
-  bool singular = false;
+  // ---- Gauss-Jordan with implicit partial pivoting.  One CTA barrier per step: the warp
+  // owning column k publishes the column and the pivot row index; the pivot row's entries
+  // in a warp's own 8 columns live in one lane of that same warp, so they are broadcast
+  // with shuffles instead of through shared memory.
   for (int k = 0; k < kN; ++k) {
     const int kb = k & 1;
-    float* rowbuf = sm.rowbuf + kb * kN;
     float* colbuf = sm.colbuf + kb * kN;
     if (warp == (k >> 3)) {
       const int jj = k & 7;
@@ -158,69 +158,50 @@ __global__ void __launch_bounds__(kThreads, 2) mtt_kernel(const float* __restric
       const uint32_t mk = __reduce_max_sync(0xffffffffu, bk);
       br = (int)__reduce_min_sync(0xffffffffu, (bk == mk) ? (uint32_t)br : 0x7fffffffu);
       if (lane == 0) {
-        piv_row = br;
+        sm.prow[kb] = br;
         sm.perm[k] = br;
       }
     }
     __syncthreads();
-    const int p = piv_row;
-    if ((p >> 2) == lane) usedm |= 1u << (p & 3);  // this lane's rows already pivoted (registers)
-    // owners of row p publish it
-    if ((p >> 2) == lane) {
-      const int ii = p & 3;
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (q == ii) {
-#pragma unroll
-          for (int jj = 0; jj < 8; ++jj) rowbuf[c0 + jj] = a[q][jj];
-        }
-    }
-    __syncthreads();
-    const float piv = rowbuf[k];
+    const int p = sm.prow[kb];
+    const int pl = p >> 2, pi = p & 3;
+    if (pl == lane) usedm |= 1u << pi;  // this lane's rows already pivoted (registers)
+    const float piv = colbuf[p];
     // pivot bookkeeping (singularity test, sign, log|det|) happens after the loop, in
     // parallel over the recorded pivots: nothing fp64 on the per-step critical path
     if (tid == 0) sm.diag[k] = piv;  // diag is free once the Laplacian is in registers
-    const float inv_piv = 1.f / piv;
-    float cv[4];
+    float inv_piv;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv_piv) : "f"(piv));
+    // Lazy row scaling: the pivot row is NOT divided by the pivot here (multiplier 0 keeps it
+    // as is); it stays piv_k x the true row, which later rank-1 updates preserve (they are
+    // linear in the row), and the scatter below applies 1/piv_k once.  So every thread runs
+    // the same 32 FFMA with no per-lane overwrite of the pivot row.
+    float f[4];
 #pragma unroll
-    for (int ii = 0; ii < 4; ++ii) cv[ii] = colbuf[r0 + ii];
+    for (int ii = 0; ii < 4; ++ii) f[ii] = (r0 + ii == p) ? 0.f : colbuf[r0 + ii] * inv_piv;
     float rv[8];
 #pragma unroll
-    for (int jj = 0; jj < 8; ++jj) rv[jj] = rowbuf[c0 + jj] * inv_piv;
-    if (warp == (k >> 3)) {  // the warp owning column k (warp-uniform branch)
+    for (int jj = 0; jj < 8; ++jj) {
+      const float x = pi == 0 ? a[0][jj] : pi == 1 ? a[1][jj] : pi == 2 ? a[2][jj] : a[3][jj];
+      rv[jj] = __shfl_sync(0xffffffffu, x, pl);
+    }
 #pragma unroll
-      for (int ii = 0; ii < 4; ++ii) {
-        const int r = r0 + ii;
-        if (r == p) {
+    for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj) a[ii][jj] = (c0 + jj == k) ? inv_piv : rv[jj];
-        } else {
-          const float f = cv[ii];
+      for (int jj = 0; jj < 8; ++jj) a[ii][jj] = fmaf(-f[ii], rv[jj], a[ii][jj]);
+    if (warp == (k >> 3)) {  // column k: -a[r][k] / piv, and (scaled) 1 / piv on the pivot row
+      const int jk = k & 7;
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj) a[ii][jj] = (c0 + jj == k) ? -f * inv_piv : fmaf(-f, rv[jj], a[ii][jj]);
-        }
-      }
-    } else {  // plain rank-1 update; the pivot row is overwritten by its owner lane
+      for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
-      for (int ii = 0; ii < 4; ++ii) {
-        const float f = cv[ii];
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) a[ii][jj] = fmaf(-f, rv[jj], a[ii][jj]);
-      }
-      if ((p >> 2) == lane) {
-#pragma unroll
-        for (int ii = 0; ii < 4; ++ii)
-          if (ii == (p & 3)) {
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj) a[ii][jj] = rv[jj];
-          }
-      }
+        for (int jj = 0; jj < 8; ++jj)
+          if (jj == jk) a[ii][jj] = (r0 + ii == p) ? 1.f : -f[ii];
     }
   }
-  (void)singular;
   __syncthreads();
-  // log|det| = sum log|pivot| (numerics.py:157) in fp64, singular pivots
-  // (numerics.py:143-146) and the pivot signs
+  // log|det| = sum log|pivot| (numerics.py:157) in fp64, plus the column shifts; singular
+  // pivots (numerics.py:143-146); sign = pivot signs x permutation parity (numerics.py:149-155),
+  // the parity as the inversion count of k -> perm[k] mod 2 (all threads, no serial cycle walk)
   {
     double lg = 0.0;
     int neg = 0, sing = 0;
@@ -228,53 +209,45 @@ __global__ void __launch_bounds__(kThreads, 2) mtt_kernel(const float* __restric
       const float pv = sm.diag[tid];
       const float mag = fabsf(pv);
       sing = !(mag > 1e-12f * fmaxf(sm.rowmag[sm.perm[tid]], 1e-30f));
-      lg = log((double)mag);
+      lg = log((double)mag) + (tid < n ? (double)sm.shift[tid] : 0.0);
       neg = pv < 0.f;
+    }
+    int inv = 0;
+    {
+      const int i = tid & (kN - 1), j0 = (tid >> 7) * (kN / 4);
+      const int pi = sm.perm[i];
+#pragma unroll 8
+      for (int j = j0; j < j0 + kN / 4; ++j) inv += (j > i) & (sm.perm[j] < pi);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) lg += __shfl_xor_sync(0xffffffffu, lg, o);
     const int negc = __syncthreads_count(neg);
+    const int par = __syncthreads_count(inv & 1);
     if (__syncthreads_or(sing) && tid == 0) flag_vac = 1;
     if (lane == 0 && warp < kN / 32) sm.red64[warp] = lg;
     __syncthreads();
     if (tid == 0) {
       double t = 0.0;
       for (int w2 = 0; w2 < kN / 32; ++w2) t += sm.red64[w2];
-      logdet = t;
-      negs = negc;
+      const int sgn = ((negc + par) & 1) ? -1 : 1;
+      const bool vac = flag_vac || sgn <= 0;
+      flag_vac = vac;
+      logz[b] = vac ? ninfd() : t;
+      status[b] = vac ? SDB_ST_VACUOUS : SDB_ST_OK;
     }
-  }
-  __syncthreads();
-  // sign: pivot signs x permutation parity (numerics.py:149-155)
-  if (tid == 0) {
-    int parity = 0;
-    // parity of k -> perm[k]: count transpositions via cycle decomposition
-    for (int k = 0; k < kN; ++k) sm.used[k] = 0;
-    for (int k = 0; k < kN; ++k) {
-      if (sm.used[k]) continue;
-      int len = 0, x = k;
-      while (!sm.used[x]) { sm.used[x] = 1; x = sm.perm[x]; ++len; }
-      parity ^= (len + 1) & 1;  // a cycle of length L has L-1 transpositions
-    }
-    const int sgn = ((negs + parity) & 1) ? -1 : 1;
-    double ssum = 0.0;
-    for (int d = 0; d < n; ++d) ssum += (double)sm.shift[d];
-    const bool vac = flag_vac || sgn <= 0;
-    flag_vac = vac;
-    logz[b] = vac ? ninfd() : logdet + ssum;
-    status[b] = vac ? SDB_ST_VACUOUS : SDB_ST_OK;
   }
   if (!kMarg) return;
   // q = inverse permutation (q[perm[k]] = k)
   __syncthreads();
-  if (tid < kN) sm.used[sm.perm[tid]] = tid;  // reuse `used` as q
+  if (tid < kN) sm.qinv[sm.perm[tid]] = tid;
   __syncthreads();
   // A^{-1}[r][x] = M[p_r][q_x]  ->  M[i][j] goes to inv[q_i][p_j]
 #pragma unroll
   for (int ii = 0; ii < 4; ++ii) {
-    const int i = r0 + ii, qi = sm.used[i];
+    const int i = r0 + ii, qi = sm.qinv[i];
+    const float sc = 1.f / sm.diag[qi];  // the deferred pivot-row scaling
 #pragma unroll
-    for (int jj = 0; jj < 8; ++jj) sm.inv[sm.perm[c0 + jj] * kN + qi] = a[ii][jj];  // transposed: inv^T[x][d]
+    for (int jj = 0; jj < 8; ++jj) sm.inv[sm.perm[c0 + jj] * kN + qi] = a[ii][jj] * sc;  // transposed: inv^T[x][d]
   }
   __syncthreads();
   float* mg = marg_all + (size_t)b * N1 * N1;
