@@ -1108,6 +1108,44 @@ def wilson_sample(adj, single_root, rng):
     return parent
 
 
+COLBOURN_COL_TOL = 1e-6  # spanning.py:591
+
+
+def colbourn_sample(adj, single_root, rng):
+    """spanning.py:567-603 (+ 517-528): condition one dependent at a time on the
+    Matrix-Tree marginals of the partially conditioned weights; when those
+    degenerate (vacuous, singular, non-finite, or a column not summing to 1
+    within 1e-6) finish with loop-erased walks on the conditioned weights
+    (spanning.py:592-597).  Returns (heads [n+1], fell_back)."""
+    n = adj.shape[0] - 1
+    parent = np.full(n + 1, -1, dtype=np.int64)
+    adj = adj.copy()
+    if single_root:
+        marg = mtt_marginals(adj, True)
+        child = 1 + sample_log_categorical(rng, np.log(np.maximum(marg[0, 1:], 1e-300)))
+        keep = adj[0, child]
+        adj[0, :] = NEG_INF
+        adj[0, child] = keep
+        parent[child] = 0
+    for dep in [x for x in range(1, n + 1) if parent[x] < 0]:
+        try:
+            col = mtt_marginals(adj, False)[:, dep]
+            if not np.isfinite(col).all() or abs(col.sum() - 1.0) > COLBOURN_COL_TOL:
+                raise Vacuous("conditioned marginals degenerated")
+        except (Vacuous, np.linalg.LinAlgError):
+            tail = wilson_sample(adj, False, rng)
+            for dd in range(1, n + 1):
+                if parent[dd] < 0:
+                    parent[dd] = tail[dd]
+            return parent, True
+        h = sample_log_categorical(rng, np.log(np.maximum(col, 1e-300)))
+        parent[dep] = h
+        keep = adj[h, dep]
+        adj[:, dep] = NEG_INF
+        adj[h, dep] = keep
+    return parent, False
+
+
 def sm_sample(th, rng):
     """chain.py:330-344 -> segments [(start, width, prev, label)] in walk order."""
     n, s, m, _ = th.shape

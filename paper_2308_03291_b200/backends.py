@@ -443,8 +443,8 @@ class SpanningBackend(Backend):
 
     def sample(self, ds, seeds, num, algorithm=None):
         """span_sample (spanning.py:709-728): projective -> Eisner decode with
-        Gumbel picks; the non-projective samplers (Wilson, Colbourn) are not
-        on the GPU path."""
+        Gumbel picks; non-projective -> Wilson's loop-erased walks (default) or
+        Colbourn's sequential conditioning, both on the GPU."""
         d0 = ds[0]
         if not d0.projective:
             return self._sample_nonprojective(ds, seeds, num, algorithm)
@@ -469,12 +469,10 @@ class SpanningBackend(Backend):
         """span_sample non-projective (spanning.py:719-728) with Wilson's
         loop-erased walks on the GPU (spanning.py:531-558); single-root first
         draws the root's child from the GPU Matrix-Tree marginals
-        (spanning.py:517-528)."""
-        from .errors import SamplerStepLimit, UnsupportedInference
+        (spanning.py:517-528); algorithm="colbourn" -> _sample_colbourn."""
+        from .errors import SamplerStepLimit
 
-        if algorithm == "colbourn":
-            raise UnsupportedInference("the Colbourn sampler is not on the GPU path (use the default, Wilson)")
-        if algorithm not in (None, "wilson"):
+        if algorithm not in (None, "wilson", "colbourn"):
             raise InvalidProblem(f"unknown spanning-tree sampler {algorithm!r}")
         d0 = ds[0]
         single = d0.single_root_edge
@@ -487,6 +485,8 @@ class SpanningBackend(Backend):
                 raise VacuousDistribution("no spanning tree has finite score")
         streams = [K.GumbelStream(s) for s in seeds]
         mg = to_host(marg).astype(np.float64) if single else None
+        if algorithm == "colbourn":
+            return self._sample_colbourn(ds, adj, mg, streams, num)
         n = d0.n
         out = [[] for _ in ds]
         for _ in range(num):
@@ -513,6 +513,84 @@ class SpanningBackend(Backend):
                 mask[par[i, 1:], np.arange(1, n + 1)] = 1.0
                 out[i].append({"adjacency": mask})
         return out, self._prefix(d0) + "wilson"
+
+
+    # fp32 Matrix-Tree marginals: a column of a healthy conditioned problem sums to 1 within
+    # ~1e-6 relative; the reference's 1e-6 test (fp64) would flag round-off here, so the GPU
+    # path tests 1e-3 -- still far below what a degenerate (near-singular) column produces
+    COLBOURN_COL_TOL = 1e-3
+
+    def _sample_colbourn(self, ds, adj, mg, streams, num):
+        """colbourn_sample_arcs (spanning.py:573-603, root child 517-528): for
+        each dependent in order, the Matrix-Tree marginals of the partially
+        conditioned weights come from ONE batched mtt_kernel launch over all
+        instances; the head is a Gumbel-max pick from the instance's own stream
+        (numerics.py:162-168, same draws as the reference) and the column is
+        conditioned on the device.  An instance whose conditioned marginals
+        degenerate finishes with the GPU loop-erased walks on its conditioned
+        weights (spanning.py:592-597)."""
+        from .errors import SamplerStepLimit
+
+        d0 = ds[0]
+        B, n, single = len(ds), d0.n, d0.single_root_edge
+        dev = adj.device
+        bi = torch.arange(B, device=dev)
+        out = [[] for _ in ds]
+        fell = np.zeros(B, dtype=bool)
+        for _ in range(num):
+            work = adj.clone()
+            parent = np.full((B, n + 1), -1, dtype=np.int64)
+            if single:  # spanning.py:517-528
+                child = np.empty(B, dtype=np.int64)
+                for i in range(B):
+                    w = np.log(np.maximum(mg[i, 0, 1:], 1e-300))
+                    child[i] = 1 + int(np.argmax(w + streams[i].take(n)))
+                    parent[i, child[i]] = 0
+                ct = torch.as_tensor(child, device=dev)
+                keep = work[bi, 0, ct].clone()
+                work[:, 0, :] = float("-inf")
+                work[bi, 0, ct] = keep
+            fell = np.zeros(B, dtype=bool)
+            for dep in range(1, n + 1):
+                todo = [i for i in range(B) if not fell[i] and parent[i, dep] < 0]
+                if not todo:
+                    continue
+                _, marg, st = K.mtt(work, False, True)
+                col = to_host(marg[:, :, dep]).astype(np.float64)
+                st = to_host(st)
+                sel, heads = [], []
+                for i in todo:
+                    c = col[i]
+                    if st[i] != 0 or not np.isfinite(c).all() or abs(c.sum() - 1.0) > self.COLBOURN_COL_TOL:
+                        fell[i] = True
+                        continue
+                    w = np.log(np.maximum(c, 1e-300))
+                    h = int(np.argmax(w + streams[i].take(n + 1)))
+                    parent[i, dep] = h
+                    sel.append(i)
+                    heads.append(h)
+                if sel:
+                    si = torch.as_tensor(sel, device=dev)
+                    hi = torch.as_tensor(heads, device=dev)
+                    keep = work[si, hi, dep].clone()
+                    work[si, :, dep] = float("-inf")
+                    work[si, hi, dep] = keep
+            if fell.any():  # spanning.py:592-597: walks on the conditioned weights
+                idx = np.nonzero(fell)[0]
+                par, st2 = K.wilson(work[torch.as_tensor(idx, device=dev)], [streams[i] for i in idx])
+                if (to_host(st2) == 4).any():
+                    raise SamplerStepLimit("loop-erased walk exceeded its step cap; weights are near-degenerate")
+                par = to_host(par)
+                for k, i in enumerate(idx):
+                    miss = parent[i] < 0
+                    miss[0] = False
+                    parent[i, miss] = par[k, miss]
+            for i in range(B):
+                mask = np.zeros((n + 1, n + 1))
+                mask[parent[i, 1:], np.arange(1, n + 1)] = 1.0
+                out[i].append({"adjacency": mask})
+        name = "colbourn+wilson-fallback" if fell[0] else "colbourn"
+        return out, self._prefix(d0) + name
 
 
 # ------------------------------------------------------------------- PCFG

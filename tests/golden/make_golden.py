@@ -237,6 +237,29 @@ def wilson_cases(st):
             st.add("spanning", dict(seed=seed, n=n, single=single, algo=algo), **out)
 
 
+def colbourn_cases(st):
+    """Reference Colbourn samples (sequential conditioning on Matrix-Tree
+    marginals, spanning.py:567-603), num=2 from one stream; the point-mass
+    case of test_spanning.py:180-189."""
+    for single in (False, True):
+        for seed, n in enumerate([2, 5, 9, 16, 24]):
+            adj = bld.spanning(600 + seed, n, True)
+            d = sd.SpanningTreeCRF(adj, directed=True, projective=False, single_root_edge=single)
+            inds, algo = sd.sample_info(d, seed, num=2, algorithm="colbourn")
+            out = {"in_adjacency": adj}
+            for r, ind in enumerate(inds):
+                out[f"sample{r}_adjacency"] = ind["adjacency"]
+            st.add("spanning", dict(seed=seed, n=n, single=single, algo=algo), **out)
+    adj = np.full((4, 4), NEG_INF)
+    adj[0, 1] = adj[1, 2] = adj[2, 3] = 0.0
+    for seed in range(3):
+        inds, algo = sd.sample_info(sd.SpanningTreeCRF(adj, directed=True), seed, num=2, algorithm="colbourn")
+        out = {"in_adjacency": adj}
+        for r, ind in enumerate(inds):
+            out[f"sample{r}_adjacency"] = ind["adjacency"]
+        st.add("spanning", dict(seed=seed, n=3, single=False, algo=algo, kind="point_mass"), **out)
+
+
 def sample2_cases(st):
     """Reference samples for the semi-Markov CRF and the PCFG (chain.py:330-344,
     constituency.py:374-378), num=2 from one stream."""
@@ -261,6 +284,7 @@ def main():
         "chain": chain_cases, "semi_markov": semi_markov_cases, "alignment": alignment_cases,
         "ctc": ctc_cases, "tree": tree_cases, "pcfg": pcfg_cases, "spanning": spanning_cases,
         "sample": sample_cases, "wilson": wilson_cases, "sample2": sample2_cases,
+        "colbourn": colbourn_cases,
     }
     only = sys.argv[1:] or list(fams)
     for fam in only:

@@ -133,8 +133,8 @@ def test_sample_vacuous_and_unsupported():
     with pytest.raises(sd.InvalidProblem):
         sd.sample_info(sd.LinearChainCRF(np.zeros(2), np.zeros((1, 2, 2))), 0, num=0)
     adj = batch_spanning(75, 1, 5)[0]
-    with pytest.raises(sd.UnsupportedInference):
-        sd.sample_info(sd.SpanningTreeCRF(adj, projective=False), 0, algorithm="colbourn")
+    with pytest.raises(sd.InvalidProblem):
+        sd.sample_info(sd.SpanningTreeCRF(adj, projective=False), 0, algorithm="no-such-sampler")
 
 
 @pytest.mark.parametrize("case", load("wilson"), ids=lambda c: str(c.meta))
@@ -159,6 +159,62 @@ def test_wilson_vs_oracle_config_size():
     assert (st == 0).all()
     for b, s in enumerate(_seeds(B)):
         np.testing.assert_array_equal(parent[b].cpu().numpy(), O.wilson_sample(adj[b], False, np.random.default_rng(s)))
+
+
+@pytest.mark.parametrize("case", load("colbourn"), ids=lambda c: str(c.meta))
+def test_colbourn_golden(case):
+    """Colbourn's sequential conditioning (spanning.py:567-603): identical to
+    the reference for the same seed (num=2 from one stream), incl. the
+    point-mass case of test_spanning.py:180-189."""
+    need_gpu()
+    d = sd.SpanningTreeCRF(case["in_adjacency"], directed=True, projective=False,
+                           single_root_edge=bool(case.meta["single"]))
+    inds, algo = sd.sample_info(d, int(case.meta["seed"]), num=2, algorithm="colbourn")
+    assert algo == case.meta["algo"]
+    for r, ind in enumerate(inds):
+        np.testing.assert_array_equal(ind["adjacency"], case[f"sample{r}_adjacency"])
+
+
+@pytest.mark.parametrize("single", [False, True])
+def test_colbourn_batched_vs_oracle(single):
+    """Batched GPU Colbourn (one mtt launch per dependent for all instances)
+    against the oracle's per-instance restatement, n=40."""
+    from paper_2308_03291_b200.backends import SpanningBackend
+
+    need_gpu()
+    B, n = 3, 40
+    adj = batch_spanning(77, B, n)
+    ds = [sd.SpanningTreeCRF(adj[b], directed=True, projective=False, single_root_edge=single) for b in range(B)]
+    seeds = [31 + b for b in range(B)]
+    out, algo = SpanningBackend().sample(ds, seeds, 2, "colbourn")
+    assert algo == "colbourn"
+    for b in range(B):
+        rng = np.random.default_rng(seeds[b])
+        for r in range(2):
+            heads, fell = O.colbourn_sample(adj[b], single, rng)
+            assert not fell
+            mask = np.zeros((n + 1, n + 1))
+            mask[heads[1:], np.arange(1, n + 1)] = 1.0
+            np.testing.assert_array_equal(out[b][r]["adjacency"], mask)
+
+
+def test_colbourn_wilson_agree_in_distribution():
+    """Both exact samplers target the same distribution: on a 3-node problem
+    (16 trees) the empirical tree frequencies of 300 Colbourn and 300 Wilson
+    draws agree with the exact Matrix-Tree probabilities (loose tolerance)."""
+    need_gpu()
+    adj = batch_spanning(78, 1, 3)[0]
+    d = sd.SpanningTreeCRF(adj, directed=True, projective=False)
+    lz = float(sd.log_partition(d))
+    counts = {}
+    for algo in ("colbourn", "wilson"):
+        inds, _ = sd.sample_info(d, 5, num=300, algorithm=algo)
+        for ind in inds:
+            key = (algo, tuple(np.argmax(ind["adjacency"][:, 1:], axis=0)))
+            counts[key] = counts.get(key, 0) + 1
+    for (algo, heads), c in counts.items():
+        p = np.exp(sum(adj[h, dd + 1] for dd, h in enumerate(heads)) - lz)
+        assert abs(c / 300 - p) < 0.1, (algo, heads, c, p)
 
 
 @pytest.mark.parametrize("case", load("sample2"), ids=lambda c: str(c.meta))

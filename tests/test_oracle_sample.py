@@ -77,6 +77,19 @@ def test_oracle_wilson_matches_reference(case):
         np.testing.assert_array_equal(mask, case[f"sample{r}_adjacency"])
 
 
+@pytest.mark.parametrize("case", load("colbourn"), ids=lambda c: str(c.meta))
+def test_oracle_colbourn_matches_reference(case):
+    adj = inputs(case)["adjacency"]
+    single = bool(case.meta["single"])
+    rng = np.random.default_rng(int(case.meta["seed"]))
+    for r in range(2):
+        heads, fell = O.colbourn_sample(adj, single, rng)
+        assert fell == case.meta["algo"].endswith("wilson-fallback")
+        mask = np.zeros_like(adj)
+        mask[heads[1:], np.arange(1, len(heads))] = 1
+        np.testing.assert_array_equal(mask, case[f"sample{r}_adjacency"])
+
+
 @pytest.mark.parametrize("case", load("sample2"), ids=lambda c: str(c.meta))
 def test_oracle_semimarkov_pcfg_samples_match_reference(case):
     x = inputs(case)
