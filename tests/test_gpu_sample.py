@@ -198,6 +198,33 @@ def test_colbourn_batched_vs_oracle(single):
             np.testing.assert_array_equal(out[b][r]["adjacency"], mask)
 
 
+@pytest.mark.parametrize("single", [False, True])
+def test_colbourn_fallback_vs_oracle(single, monkeypatch):
+    """The degenerate-marginals branch (spanning.py:592-597): forcing the
+    column test to fail at the first dependent on both sides, the GPU path
+    must finish with Wilson walks on the same conditioned weights and the
+    same stream position as the oracle, and report the fallback name."""
+    from paper_2308_03291_b200.backends import SpanningBackend
+
+    need_gpu()
+    monkeypatch.setattr(SpanningBackend, "COLBOURN_COL_TOL", -1.0)
+    monkeypatch.setattr(O, "COLBOURN_COL_TOL", -1.0)
+    B, n = 2, 24
+    adj = batch_spanning(79, B, n)
+    ds = [sd.SpanningTreeCRF(adj[b], directed=True, projective=False, single_root_edge=single) for b in range(B)]
+    seeds = [41, 42]
+    out, algo = SpanningBackend().sample(ds, seeds, 2, "colbourn")
+    assert algo == "colbourn+wilson-fallback"
+    for b in range(B):
+        rng = np.random.default_rng(seeds[b])
+        for r in range(2):
+            heads, fell = O.colbourn_sample(adj[b], single, rng)
+            assert fell
+            mask = np.zeros((n + 1, n + 1))
+            mask[heads[1:], np.arange(1, n + 1)] = 1.0
+            np.testing.assert_array_equal(out[b][r]["adjacency"], mask)
+
+
 def test_colbourn_wilson_agree_in_distribution():
     """Both exact samplers target the same distribution: on a 3-node problem
     (16 trees) the empirical tree frequencies of 300 Colbourn and 300 Wilson
