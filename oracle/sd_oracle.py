@@ -458,7 +458,8 @@ def tree_marginals(th):
             terms = np.concatenate(parts) if parts else np.zeros(0)
             if terms.size:
                 out[i, j] = lse(terms, 0)
-    child = ins - fold
+    with np.errstate(invalid="ignore"):  # -inf - -inf on spans the mask below drops
+        child = ins - fold
     ok = np.isfinite(ins) & np.isfinite(out)
     iu, ju = np.nonzero(np.triu(ok))
     marg[iu, ju] = np.exp(out[iu, ju, None] + child[iu, ju, None] + th[iu, ju] - z)

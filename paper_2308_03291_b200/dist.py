@@ -248,7 +248,8 @@ def batch_map(op, dists, *args, ragged: bool = True, **kwargs) -> list:
     """dist.py:355-361, batched: log_partition / marginals / argmax (and
     their *_info forms) run as ONE kernel call per group.  Same-shape
     instances group directly; with `ragged`, chains, alignments, CTC
-    (same target length) and multi-root spanning trees of DIFFERENT lengths
+    (same target length), multi-root spanning trees, semi-Markov CRFs (same
+    s, m) and Tree-CRFs (same m) of DIFFERENT lengths
     share a launch through inference-neutral padding (ragged.py; the
     reference's pad_chain, chain.py:161-176) and their results are sliced
     back.  Any other op maps the same GPU-backed op per instance."""

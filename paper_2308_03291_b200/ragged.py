@@ -16,7 +16,14 @@ slices a marginal / indicator dict back to `d`'s shape:
   prefix, and the first original frame sees the same alpha;
 * SpanningTreeCRF, multi-root only: extra nodes whose ONLY arc is root -> node
   (weight exp(0) = 1; no outgoing arcs), projective-compatible since they sit
-  after position n.
+  after position n;
+* SemiMarkovCRF: width-1 identity segments appended (label kept, potential 0;
+  every other padded segment, and every original segment that would now run
+  past position n, -inf): each labelled segmentation extends uniquely;
+* TreeCRF: the padded words are single-word spans (label 0, potential 0) and
+  the only spans that cover them are the left-branching (0, j), j >= n (label
+  0, potential 0); every other span touching a padded word is -inf, so every
+  binary tree over the n words extends by exactly one tree.
 
 Host-side glue only: the padded batch runs through the same kernels.
 """
@@ -25,7 +32,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .families import CTCDist, LinearChainCRF, MonotoneAlignmentCRF, SpanningTreeCRF
+from .families import CTCDist, LinearChainCRF, MonotoneAlignmentCRF, SemiMarkovCRF, SpanningTreeCRF, TreeCRF
 
 NEG_INF = float("-inf")
 
@@ -86,6 +93,42 @@ def _span_unpad(d, x):
     return {"adjacency": x["adjacency"][: d.n + 1, : d.n + 1]}
 
 
+def _sm_pad(d, n):
+    th0 = d.segment_potentials
+    n0, s, m, _ = th0.shape
+    if n == n0:
+        return d
+    th = np.full((n, s, m, m), NEG_INF)
+    th[:n0] = th0
+    for w in range(1, s + 1):  # original segments that would now end past n0
+        th[max(n0 - w + 1, 0):n0, w - 1] = NEG_INF
+    idx = np.arange(m)
+    th[n0:, 0, idx, idx] = 0.0
+    return SemiMarkovCRF(th)
+
+
+def _sm_unpad(d, x):
+    return {"segment_potentials": x["segment_potentials"][: d.segment_potentials.shape[0]]}
+
+
+def _tree_pad(d, n):
+    th0 = d.span_potentials
+    n0, _, m = th0.shape
+    if n == n0:
+        return d
+    th = np.full((n, n, m), NEG_INF)
+    th[:n0, :n0] = th0
+    k = np.arange(n0, n)
+    th[k, k, 0] = 0.0      # padded words
+    th[0, n0:, 0] = 0.0    # (0, j), j >= n0: the original tree, then one padded word at a time
+    return TreeCRF(th)
+
+
+def _tree_unpad(d, x):
+    n0 = d.span_potentials.shape[0]
+    return {"span_potentials": x["span_potentials"][:n0, :n0]}
+
+
 # family -> (key, size, combine sizes, pad, unpad)
 RAGGED = {
     LinearChainCRF: (lambda d: (d.m,), lambda d: d.n, max, _chain_pad, _chain_unpad),
@@ -93,6 +136,10 @@ RAGGED = {
                            lambda ss: (max(s[0] for s in ss), max(s[1] for s in ss)), _nw_pad, _nw_unpad),
     CTCDist: (lambda d: (d.vocab_size, len(d.target)), lambda d: d.num_frames, max, _ctc_pad, _ctc_unpad),
     SpanningTreeCRF: (lambda d: (d.directed, d.projective), lambda d: d.n, max, _span_pad, _span_unpad),
+    SemiMarkovCRF: (lambda d: d.segment_potentials.shape[1:3], lambda d: d.segment_potentials.shape[0], max,
+                    _sm_pad, _sm_unpad),
+    TreeCRF: (lambda d: (d.span_potentials.shape[2],), lambda d: d.span_potentials.shape[0], max,
+              _tree_pad, _tree_unpad),
 }
 
 

@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 import paper_2308_03291_b200 as sd
-from golden.builders import alignment, chain, ctc, spanning
+from golden.builders import alignment, chain, ctc, semi_markov, spanning, tree
 from gpu_util import ATOL, RTOL, need_gpu
 
 pytestmark = pytest.mark.gpu
@@ -49,3 +49,19 @@ def test_ragged_ctc_and_spanning():
     for proj in (False, True):
         dists = [sd.SpanningTreeCRF(spanning(s, n, True), projective=proj) for s, n in enumerate([3, 11, 20])]
         _check(dists)
+
+
+def test_ragged_semimarkov_and_tree():
+    need_gpu()
+    dists = [sd.SemiMarkovCRF(semi_markov(s, n, 3, 4)) for s, n in enumerate([3, 11, 25, 7])]
+    _check(dists)
+    dists = [sd.TreeCRF(tree(s, n, 3)) for s, n in enumerate([1, 6, 19, 12])]
+    _check(dists)
+    for dists in ([sd.SemiMarkovCRF(semi_markov(s, n, 3, 4)) for s, n in enumerate([3, 11, 25])],
+                  [sd.TreeCRF(tree(s, n, 3)) for s, n in enumerate([2, 9, 17])]):
+        am = sd.batch_map(sd.argmax_info, dists)
+        for d, (ind, score, algo) in zip(dists, am):
+            ind0, score0, algo0 = sd.argmax_info(d)
+            for k in ind0:
+                np.testing.assert_array_equal(ind[k], ind0[k])
+            assert score == score0 and algo == algo0

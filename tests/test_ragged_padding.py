@@ -5,10 +5,11 @@ marginals unchanged after padding (chain.py:161-176, test_chain.py:58-62)."""
 import numpy as np
 import pytest
 
-from golden.builders import alignment, chain, ctc, spanning
+from golden.builders import alignment, chain, ctc, semi_markov, spanning, tree
 from oracle import sd_oracle as O
 from paper_2308_03291_b200 import ragged as rg
-from paper_2308_03291_b200.families import CTCDist, LinearChainCRF, MonotoneAlignmentCRF, SpanningTreeCRF
+from paper_2308_03291_b200.families import (CTCDist, LinearChainCRF, MonotoneAlignmentCRF, SemiMarkovCRF,
+                                             SpanningTreeCRF, TreeCRF)
 
 
 def test_chain_padding_neutral():
@@ -61,6 +62,35 @@ def test_spanning_multiroot_padding_neutral(projective):
         z1, m1 = O.mtt_log_partition(p.adjacency), O.mtt_marginals(p.adjacency)
     assert abs(z0 - z1) <= 1e-9
     np.testing.assert_allclose(rg.unpad(d, {"adjacency": m1})["adjacency"], m0, atol=1e-9)
+
+
+@pytest.mark.parametrize("n0,n", [(5, 9), (1, 4), (6, 6)])
+def test_semimarkov_padding_neutral(n0, n):
+    d = SemiMarkovCRF(semi_markov(12, n0, min(3, n0), 3))
+    p = rg._sm_pad(d, n)
+    assert p.segment_potentials.shape[0] == n
+    z0, m0 = O.sm_marginals(d.segment_potentials)
+    z1, m1 = O.sm_marginals(p.segment_potentials)
+    assert abs(z0 - z1) <= 1e-9
+    np.testing.assert_allclose(rg.unpad(d, {"segment_potentials": m1})["segment_potentials"], m0, atol=1e-12)
+    seg0, s0 = O.sm_viterbi(d.segment_potentials)
+    seg1, s1 = O.sm_viterbi(p.segment_potentials)
+    assert s0 == s1
+    assert [g for g in seg1 if g[0] < n0] == [g for g in seg0]
+
+
+@pytest.mark.parametrize("n0,n", [(5, 9), (1, 3), (7, 8)])
+def test_tree_padding_neutral(n0, n):
+    d = TreeCRF(tree(13, n0, 3))
+    p = rg._tree_pad(d, n)
+    z0, m0 = O.tree_marginals(d.span_potentials)
+    z1, m1 = O.tree_marginals(p.span_potentials)
+    assert abs(z0 - z1) <= 1e-9
+    np.testing.assert_allclose(rg.unpad(d, {"span_potentials": m1})["span_potentials"], m0, atol=1e-12)
+    lab0, s0 = O.tree_argmax(d.span_potentials)
+    lab1, s1 = O.tree_argmax(p.span_potentials)
+    assert s0 == s1
+    np.testing.assert_array_equal(lab1[:n0, :n0], lab0)
 
 
 def test_groups():
