@@ -22,7 +22,7 @@ import torch
 
 from . import backends
 from .errors import InvalidProblem, ONE_TO_ONE_REASON, UnsupportedInference, VacuousDistribution
-from .families import OneToOneMatching
+from .families import PCFG, OneToOneMatching
 
 NEG_INF = float("-inf")
 
@@ -249,7 +249,7 @@ def batch_map(op, dists, *args, ragged: bool = True, **kwargs) -> list:
     their *_info forms) run as ONE kernel call per group.  Same-shape
     instances group directly; with `ragged`, chains, alignments, CTC
     (same target length), multi-root spanning trees, semi-Markov CRFs (same
-    s, m) and Tree-CRFs (same m) of DIFFERENT lengths
+    s, m), Tree-CRFs (same m) and PCFGs (same NT, PT) of DIFFERENT lengths
     share a launch through inference-neutral padding (ragged.py; the
     reference's pad_chain, chain.py:161-176) and their results are sliced
     back.  Any other op maps the same GPU-backed op per instance."""
@@ -271,7 +271,7 @@ def batch_map(op, dists, *args, ragged: bool = True, **kwargs) -> list:
         if key[0] == "ragged":
             padded = rg.pad_group(group)
             res = _BATCHED[name](be, padded)
-            res = [_unpad_result(name, d, r) for d, r in zip(group, res)]
+            res = [_unpad_result(name, d, p, r) for d, p, r in zip(group, padded, res)]
         else:
             res = _BATCHED[name](be, group)
         for i, r in zip(idx, res):
@@ -279,17 +279,21 @@ def batch_map(op, dists, *args, ragged: bool = True, **kwargs) -> list:
     return out
 
 
-def _unpad_result(name, d, r):
+def _unpad_result(name, d, padded, r):
     from . import ragged as rg
 
-    if name.startswith("log_partition"):
-        return r
+    if name == "log_partition":
+        return r + rg.logz_shift(d, padded)
+    if name == "log_partition_info":
+        return r[0] + rg.logz_shift(d, padded), r[1]
     if name in ("marginals", "argmax"):
         return rg.unpad(d, r)
     if name == "marginals_info":
         return rg.unpad(d, r[0]), r[1]
-    # argmax_info: the score of the unpadded indicator (padding adds 0)
     ind = rg.unpad(d, r[0])
+    if isinstance(d, PCFG):  # the best derivation's score, less the padding's 1/2 factors
+        return ind, r[1] + rg.logz_shift(d, padded), r[2]
+    # argmax_info: the score of the unpadded indicator (padding adds 0)
     return ind, structure_score(d, ind), r[2]
 
 

@@ -23,7 +23,14 @@ slices a marginal / indicator dict back to `d`'s shape:
 * TreeCRF: the padded words are single-word spans (label 0, potential 0) and
   the only spans that cover them are the left-branching (0, j), j >= n (label
   0, potential 0); every other span touching a padded word is -inf, so every
-  binary tree over the n words extends by exactly one tree.
+  binary tree over the n words extends by exactly one tree;
+* PCFG: the grammar gains a nonterminal X and a preterminal P (every
+  instance of the group, so the shapes agree).  A padded word emits only P;
+  X is the new start symbol (root[X] = 0) with rules X -> X P and
+  X -> A P (A an original nonterminal, weight root[A]), each times 1/2 so
+  X's rules stay normalised; the only derivations are the original ones
+  extended left-branching over the padded words, so the span marginals are
+  unchanged and log Z drops by exactly (N - n) log 2 (`logz_shift`).
 
 Host-side glue only: the padded batch runs through the same kernels.
 """
@@ -32,7 +39,8 @@ from __future__ import annotations
 
 import numpy as np
 
-from .families import CTCDist, LinearChainCRF, MonotoneAlignmentCRF, SemiMarkovCRF, SpanningTreeCRF, TreeCRF
+from .families import (CTCDist, LinearChainCRF, MonotoneAlignmentCRF, PCFG, SemiMarkovCRF, SpanningTreeCRF,
+                       TreeCRF)
 
 NEG_INF = float("-inf")
 
@@ -129,6 +137,42 @@ def _tree_unpad(d, x):
     return {"span_potentials": x["span_potentials"][:n0, :n0]}
 
 
+LOG_HALF = -float(np.log(2.0))
+
+
+def _pcfg_pad(d, n):
+    nt0, pt0, n0 = d.num_nt, d.num_pt, d.n
+    nt, pt = nt0 + 1, pt0 + 1
+    X, P = nt0, nt + pt0  # X: new nonterminal; P: new preterminal (child index)
+    cmap = np.concatenate([np.arange(nt0), nt + np.arange(pt0)])  # original child -> new child index
+    rules = np.full((nt, nt + pt, nt + pt), NEG_INF)
+    rules[np.ix_(np.arange(nt0), cmap, cmap)] = d.binary_rules
+    rules[X, X, P] = LOG_HALF
+    rules[X, np.arange(nt0), P] = d.root + LOG_HALF
+    root = np.full(nt, NEG_INF)
+    if n > n0:
+        root[X] = 0.0
+    else:
+        root[:nt0] = d.root
+    emis = np.full((n, pt), NEG_INF)
+    emis[:n0, :pt0] = d.emissions
+    emis[n0:, pt0] = 0.0
+    sticky = np.zeros((n, n))
+    sticky[:n0, :n0] = d.sticky
+    return PCFG(root, rules, emis, sticky)
+
+
+def _pcfg_unpad(d, x):
+    return {"sticky": x["sticky"][: d.n, : d.n]}
+
+
+def logz_shift(d, padded) -> float:
+    """log Z(d) - log Z(padded) (0 except for the PCFG's 1/2 per padded word)."""
+    if isinstance(d, PCFG):
+        return (padded.n - d.n) * float(np.log(2.0))
+    return 0.0
+
+
 # family -> (key, size, combine sizes, pad, unpad)
 RAGGED = {
     LinearChainCRF: (lambda d: (d.m,), lambda d: d.n, max, _chain_pad, _chain_unpad),
@@ -140,6 +184,7 @@ RAGGED = {
                     _sm_pad, _sm_unpad),
     TreeCRF: (lambda d: (d.span_potentials.shape[2],), lambda d: d.span_potentials.shape[0], max,
               _tree_pad, _tree_unpad),
+    PCFG: (lambda d: (d.num_nt, d.num_pt), lambda d: d.n, max, _pcfg_pad, _pcfg_unpad),
 }
 
 

@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 import paper_2308_03291_b200 as sd
-from golden.builders import alignment, chain, ctc, semi_markov, spanning, tree
+from golden.builders import alignment, chain, ctc, pcfg, semi_markov, spanning, tree
 from gpu_util import ATOL, RTOL, need_gpu
 
 pytestmark = pytest.mark.gpu
@@ -65,3 +65,17 @@ def test_ragged_semimarkov_and_tree():
             for k in ind0:
                 np.testing.assert_array_equal(ind[k], ind0[k])
             assert score == score0 and algo == algo0
+
+
+def test_ragged_pcfg():
+    """PCFGs of different lengths (same NT, PT) share one launch through the
+    X -> X P / X -> A P padding grammar; log Z, span marginals and the best
+    derivation (score less the padding's log 2 per padded word) match."""
+    need_gpu()
+    dists = [sd.PCFG(*pcfg(s, n, 3, 2)) for s, n in enumerate([2, 7, 12, 5])]
+    _check(dists)
+    am = sd.batch_map(sd.argmax_info, dists)
+    for d, (ind, score, algo) in zip(dists, am):
+        ind0, score0, algo0 = sd.argmax_info(d)
+        np.testing.assert_array_equal(ind["sticky"], ind0["sticky"])
+        assert abs(score - score0) <= 1e-4 * abs(score0) and algo == algo0

@@ -5,10 +5,10 @@ marginals unchanged after padding (chain.py:161-176, test_chain.py:58-62)."""
 import numpy as np
 import pytest
 
-from golden.builders import alignment, chain, ctc, semi_markov, spanning, tree
+from golden.builders import alignment, chain, ctc, pcfg, semi_markov, spanning, tree
 from oracle import sd_oracle as O
 from paper_2308_03291_b200 import ragged as rg
-from paper_2308_03291_b200.families import (CTCDist, LinearChainCRF, MonotoneAlignmentCRF, SemiMarkovCRF,
+from paper_2308_03291_b200.families import (PCFG, CTCDist, LinearChainCRF, MonotoneAlignmentCRF, SemiMarkovCRF,
                                              SpanningTreeCRF, TreeCRF)
 
 
@@ -91,6 +91,28 @@ def test_tree_padding_neutral(n0, n):
     lab1, s1 = O.tree_argmax(p.span_potentials)
     assert s0 == s1
     np.testing.assert_array_equal(lab1[:n0, :n0], lab0)
+
+
+@pytest.mark.parametrize("n0,n", [(4, 7), (1, 3), (5, 5)])
+def test_pcfg_padding_neutral(n0, n):
+    d = PCFG(*pcfg(14, n0, 3, 2))
+    p = rg._pcfg_pad(d, n)
+    assert (p.num_nt, p.num_pt, p.n) == (4, 3, n)
+    args0 = (d.root, d.binary_rules, d.emissions, d.sticky)
+    args1 = (p.root, p.binary_rules, p.emissions, p.sticky)
+    z0, z1 = O.pcfg_log_partition(*args0), O.pcfg_log_partition(*args1)
+    if z0 == -np.inf:  # one word: no binary derivation (vacuous) on both sides
+        assert z1 == -np.inf
+        return
+    assert abs(z0 - (z1 + rg.logz_shift(d, p))) <= 1e-9
+    m0, m1 = O.pcfg_span_marginals(*args0), O.pcfg_span_marginals(*args1)
+    m0 = m0[1] if isinstance(m0, tuple) else m0
+    m1 = m1[1] if isinstance(m1, tuple) else m1
+    np.testing.assert_allclose(rg.unpad(d, {"sticky": m1})["sticky"], m0, atol=1e-12)
+    a0, s0 = O.pcfg_argmax(*args0)
+    a1, s1 = O.pcfg_argmax(*args1)
+    np.testing.assert_array_equal(np.asarray(a1)[:n0, :n0], a0)
+    assert abs(s0 - (s1 + rg.logz_shift(d, p))) <= 1e-9
 
 
 def test_groups():
