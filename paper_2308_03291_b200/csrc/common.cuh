@@ -89,7 +89,17 @@ struct LseD {
   __device__ __forceinline__ double result() const { return m == ninfd() ? ninfd() : m + (double)flog(s); }
 };
 
+// Full-warp float max as ONE redux.sync.max.u32 on order-preserving keys
+// (sign-magnitude -> unsigned order; NaN maps to key 0, so like fmaxf it only
+// wins when every lane is NaN) instead of five dependent shuffle+max rounds.
 __device__ __forceinline__ float warp_max(float v) {
+  const uint32_t u = __float_as_uint(v);
+  uint32_t key = u ^ ((uint32_t)((int32_t)u >> 31) | 0x80000000u);
+  key = (v != v) ? 0u : key;
+  const uint32_t mk = __reduce_max_sync(0xffffffffu, key);
+  return __uint_as_float(mk ^ (((mk >> 31) - 1u) | 0x80000000u));
+}
+__device__ __forceinline__ float warp_max_shfl(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
