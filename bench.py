@@ -53,7 +53,7 @@ CONFIGS = {
     "c2a": dict(workload="MonotoneAlignmentCRF", B=256, shape=dict(n=512, m=128), work=1_588_252, bound="hbm",
                 argmax=False, kernel="nw_mitm_kernel"),
     "c2b": dict(workload="CTCDist", B=256, shape=dict(T=512, V=128, L=128), work=921_088, bound="mufu",
-                argmax=False, kernel="ctc_kernel<1>"),
+                argmax=False, kernel="ctc_dir_kernel + ctc_marg_kernel<9>"),
     "c3": dict(workload="SpanningTreeCRF non-projective (Matrix-Tree, multi-root)", B=512, shape=dict(n=128),
                work=4_194_304, bound="fp32", argmax=False, kernel="mtt_kernel<true>"),
     "c4": dict(workload="SpanningTreeCRF projective (Eisner, multi-root) + Kuhlmann argmax", B=256,
@@ -185,7 +185,7 @@ def kernel_fn(cfg, inputs):
 
 
 def launches_per_step(cfg):
-    return {"c1": 4, "c2a": 1, "c2b": 1, "c3": 1, "c4": 3, "c5a": 4, "c5b": 1}[cfg]
+    return {"c1": 4, "c2a": 1, "c2b": 2, "c3": 1, "c4": 3, "c5a": 4, "c5b": 1}[cfg]
 
 
 # ------------------------------------------------------------------ clocks

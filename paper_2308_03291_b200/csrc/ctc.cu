@@ -6,17 +6,20 @@
 // _ctc_walk).  Layout per instance: frame_potentials [T][V] fp32,
 // targets [L] int32 (labels in 1..V-1), blank = 0.
 //
-// Schedule: one CTA per instance, one thread per lattice state s (S = 2L+1
-// <= 1024), frames in lockstep (one __syncthreads per frame).  Frame rows are
-// prefetched kP frames ahead into a shared ring with cp.async and each state
-// gathers its emission theta[t][lab(s)] from shared memory.
-//   phase A: beta over frames T-1..0, stored as fp32 offsets from a per-frame
-//            fp64 base (the frame max) -> workspace; Z = lse(beta[0][0..1] + E).
-//   phase B: alpha over frames 0..T-1; posterior exp(alpha + beta - Z) per
-//            state, reduced by label deterministically (blank: fixed-order warp
-//            butterflies; labels: each vocabulary thread sums its own state
-//            list in increasing s) and written as one coalesced [V] row.
-// Log values are fp64; exp/log fp32 MUFU on differences.
+// Schedule: one CTA per (instance, direction), one thread per lattice state s
+// (S = 2L+1 <= 1024), frames in lockstep (one __syncthreads per frame).  Frame
+// rows are prefetched kP frames ahead into a shared ring with cp.async and each
+// state gathers its emission theta[t][lab(s)] from shared memory.
+//   ctc_kernel<0/2>: alpha (log-sum-exp) or the max-plus alpha with
+//            first-maximum back pointers and the walk (logZ, argmax).
+//   ctc_dir_kernel (marginals, grid B x 2): the forward CTA stores alpha, the
+//            backward CTA beta, both as fp32 offsets from per-(frame, warp)
+//            bases, concurrently; the forward owns Z, the status and the label
+//            CSR.
+//   ctc_marg_kernel: posteriors exp(alpha + beta - Z) reduced by label in a
+//            fixed order (blank: lane-strided sums + butterfly; labels: the CSR
+//            state list in increasing s), a warp per frame, streaming.
+// Log values are fp64 on the recursion; exp/log fp32 MUFU on differences.
 #include "common.cuh"
 
 namespace {
@@ -32,37 +35,24 @@ template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 struct CtcSmem {
-  double* a0;     // [S+2] ping (2 leading -inf pads)
-  double* a1;     // [S+2] pong
-  float* rows;    // [kP][V]
-  int* lab;       // [S]
-  int* lst;       // [L] states grouped by label (CSR)
-  int* off;       // [V+1]
-  float* post;    // [S]
-  double* wred;   // [2][32]
-  float* bred;    // [32]
-  float* bring;   // [kP][S] beta rows (phase B prefetch)
-  double* bbase;  // [kP][32] their per-warp bases
+  double* a0;   // [S+2] ping (2 leading -inf pads)
+  double* a1;   // [S+2] pong
+  float* rows;  // [kP][V]
+  int* lab;     // [S]
 };
 
 size_t ctc_smem_bytes(int S, int V, int L) {
-  return (size_t)2 * (S + 2) * 8 + (size_t)kP * V * 4 + (size_t)S * 4 + (size_t)(L + 1) * 4 +
-         (size_t)(V + 1) * 4 + (size_t)S * 4 + 64 * 8 + 32 * 4 + (size_t)kP * 32 * 8 + (size_t)kP * S * 4 + 128;
+  (void)L;
+  return (size_t)2 * (S + 2) * 8 + (size_t)kP * V * 4 + (size_t)S * 4 + 128;
 }
 
 __device__ CtcSmem ctc_carve(char* p, int S, int V, int L) {
+  (void)L;
   CtcSmem s;
   s.a0 = (double*)p; p += (size_t)(S + 2) * 8;
   s.a1 = (double*)p; p += (size_t)(S + 2) * 8;
-  s.wred = (double*)p; p += 64 * 8;
-  s.bbase = (double*)p; p += kP * 32 * 8;
   s.rows = (float*)p; p += (size_t)kP * V * 4;
-  s.lab = (int*)p; p += (size_t)S * 4;
-  s.lst = (int*)p; p += (size_t)(L + 1) * 4;
-  s.off = (int*)p; p += (size_t)(V + 1) * 4;
-  s.post = (float*)p; p += (size_t)S * 4;
-  s.bred = (float*)p; p += 32 * 4;
-  s.bring = (float*)p;
+  s.lab = (int*)p;
   return s;
 }
 
@@ -70,31 +60,23 @@ __device__ __forceinline__ void load_row(const float* __restrict__ fp, int t, in
   for (int v = threadIdx.x; v < V; v += blockDim.x) cp_async4(dst + v, fp + (size_t)t * V + v);
 }
 
-template <int kMode>  // 0 logZ only, 1 logZ + marginals, 2 max-plus path
+template <int kMode>  // 0 logZ only, 2 max-plus path (marginals: ctc_dir_kernel)
 __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __restrict__ tg_all, int T, int V,
-                           int L, float* __restrict__ wsb_all, double* __restrict__ wsbase_all,
-                           int32_t* __restrict__ csr_all, int8_t* __restrict__ back_all, double* __restrict__ logz, float* __restrict__ marg_all,
-                           int32_t* __restrict__ path_all, double* __restrict__ score,
-                           int32_t* __restrict__ status) {
+                           int L, int8_t* __restrict__ back_all, double* __restrict__ logz,
+                           int32_t* __restrict__ path_all, double* __restrict__ score, int32_t* __restrict__ status) {
+  static_assert(kMode == 0 || kMode == 2, "ctc_kernel modes");
   extern __shared__ __align__(16) char smraw[];
   const int S = 2 * L + 1;
   CtcSmem sm = ctc_carve(smraw, S, V, L);
-  __shared__ double zsh;
   __shared__ int badsh;
   const int b = blockIdx.x, tid = threadIdx.x;
   const float* fp = fp_all + (size_t)b * T * V;
   const int32_t* tg = tg_all + (size_t)b * L;
   const int s = tid;
   const bool act = s < S;
-
-  // ---- prologue: labels, skip flags, label lists
-  if (tid == 0) {
-    badsh = 0;
-    zsh = ninfd();
-  }
+  if (tid == 0) badsh = 0;
   __syncthreads();
   int mylab = 0;
-  bool skip = false;
   if (act) {
     mylab = (s & 1) ? tg[s >> 1] : 0;
     if ((s & 1) && (mylab < 1 || mylab >= V)) {
@@ -104,63 +86,183 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
     sm.lab[s] = mylab;
   }
   __syncthreads();
-  if (act) skip = (s >= 2) && mylab != 0 && mylab != sm.lab[s - 2];
-  if (kMode == 1) {
-    if (tid == 0) {  // CSR of the odd states by label, increasing s (deterministic order)
-      for (int v = 0; v <= V; ++v) sm.off[v] = 0;
-      for (int k = 0; k < L; ++k) sm.off[sm.lab[2 * k + 1] + 1]++;
-      for (int v = 0; v < V; ++v) sm.off[v + 1] += sm.off[v];
-      for (int k = 0; k < L; ++k) sm.lst[k] = -1;
+  const bool skip = act && (s >= 2) && mylab != 0 && mylab != sm.lab[s - 2];
+  // forward (alignment.py:248-269; max-plus with first-maximum back pointers, 304-318)
+  double* prv = sm.a0 + 2;  // alpha[t-1]
+  double* now = sm.a1 + 2;
+  if (tid < 2) { sm.a0[tid] = ninfd(); sm.a1[tid] = ninfd(); }
+  for (int k = 0; k < kP; ++k) {
+    if (k < T) load_row(fp, k, V, sm.rows + (size_t)k * V);
+    cp_commit();
+  }
+  int8_t* back = (kMode == 2) ? back_all + (size_t)b * T * S : nullptr;
+  int bad = 0;
+  for (int t = 0; t < T; ++t) {
+    cp_wait<kP - 1>();
+    __syncthreads();
+    const float* E = sm.rows + (size_t)(t % kP) * V;
+    for (int v = tid; v < V; v += blockDim.x) bad |= bad_input(E[v]);
+    double a = ninfd();
+    if (act) {
+      const double e = (double)E[mylab];
+      if (t == 0) {
+        a = (s <= 1) ? e : ninfd();
+      } else if (kMode == 2) {
+        // first maximum in predecessor order [s, s-1, s-2] (alignment.py:239-245, 304-318)
+        double best = prv[s];
+        int k = 0;
+        if (s >= 1 && prv[s - 1] > best) { best = prv[s - 1]; k = 1; }
+        if (skip && prv[s - 2] > best) { best = prv[s - 2]; k = 2; }
+        a = best + e;
+        back[(size_t)t * S + s] = (int8_t)k;
+      } else {
+        const double x0 = prv[s], x1 = prv[s - 1], x2 = skip ? prv[s - 2] : ninfd();
+        const double M = fmax(fmax(x0, x1), x2);
+        if (M != ninfd()) {
+          const float sum = fexp((float)(x0 - M)) + fexp((float)(x1 - M)) + fexp((float)(x2 - M));
+          a = M + (double)flog(sum) + e;
+        }
+      }
+      now[s] = a;
+    }
+    __syncthreads();  // now[] complete; row t consumed
+    {
+      const int tn = t + kP;
+      if (tn < T) load_row(fp, tn, V, sm.rows + (size_t)(tn % kP) * V);
+      cp_commit();
+    }
+    double* tmp = prv; prv = now; now = tmp;
+  }
+  cp_wait<0>();
+  if (bad) atomicOr(&badsh, 1);
+  __syncthreads();
+  // final states (alignment.py:263-264): [S-1] or [S-1, S-2]
+  if (tid == 0) {
+    const double f1 = prv[S - 1];
+    const double f2 = (S > 1) ? prv[S - 2] : ninfd();
+    double res;
+    int fin = S - 1;
+    if (kMode == 2) {
+      res = f1;
+      if (S > 1 && f2 > f1) { res = f2; fin = S - 2; }
+    } else {
+      const double M = fmax(f1, f2);
+      res = (M == ninfd()) ? ninfd() : M + (double)flog(fexp((float)(f1 - M)) + fexp((float)(f2 - M)));
+    }
+    const int st = badsh ? SDB_ST_INVALID : (res == ninfd() ? SDB_ST_VACUOUS : SDB_ST_OK);
+    status[b] = st;
+    if (kMode == 2) {
+      score[b] = res;
+      int32_t* path = path_all + (size_t)b * T;
+      int cs = fin;
+      for (int t = T - 1; t >= 0; --t) {
+        path[t] = (st == SDB_ST_OK) ? sm.lab[cs] : 0;
+        if (t > 0 && st == SDB_ST_OK) cs -= back[(size_t)t * S + cs];
+      }
+    } else {
+      logz[b] = res;
+    }
+  }
+}
+
+// log_partition + marginals as TWO independent CTAs per instance (grid B x 2):
+// blockIdx.y = 0 runs the forward (alpha) over frames 0..T-1 and owns Z, the
+// status and the label CSR; blockIdx.y = 1 runs the backward (beta) over
+// T-1..0.  Both store their vectors as fp32 offsets from a per-(frame, warp)
+// fp64 base; ctc_marg_kernel forms exp(alpha + beta - Z).  Twice the CTAs of
+// one fwd-then-bwd CTA per instance, and each runs half the frames: the
+// per-frame latency chains of the two directions overlap across the SM
+// instead of running back to back.
+size_t ctc_dir_smem_bytes(int S, int V, int L) {
+  return (size_t)2 * (S + 2) * 8 + (size_t)kP * V * 4 + (size_t)S * 4 + (size_t)(L + 1) * 4 + (size_t)(V + 1) * 4 +
+         128;
+}
+
+__global__ void ctc_dir_kernel(const float* __restrict__ fp_all, const int32_t* __restrict__ tg_all, int T, int V,
+                               int L, float* __restrict__ wsa_all, float* __restrict__ wsabase_all,
+                               float* __restrict__ wsb_all, float* __restrict__ wsbase_all,
+                               int32_t* __restrict__ csr_all, double* __restrict__ logz,
+                               int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) char smraw[];
+  const int S = 2 * L + 1;
+  double *a0, *a1;
+  float* rows;
+  int *lab, *lst, *off;
+  {
+    char* p = smraw;
+    a0 = (double*)p; p += (size_t)(S + 2) * 8;
+    a1 = (double*)p; p += (size_t)(S + 2) * 8;
+    rows = (float*)p; p += (size_t)kP * V * 4;
+    lab = (int*)p; p += (size_t)S * 4;
+    lst = (int*)p; p += (size_t)(L + 1) * 4;
+    off = (int*)p;
+  }
+  __shared__ int badsh;
+  const int b = blockIdx.x, dir = blockIdx.y, tid = threadIdx.x, s = tid, lane = tid & 31, wq = tid >> 5;
+  const bool act = s < S;
+  const float* fp = fp_all + (size_t)b * T * V;
+  const int32_t* tg = tg_all + (size_t)b * L;
+  if (tid == 0) badsh = 0;
+  __syncthreads();
+  int mylab = 0;
+  if (act) {
+    mylab = (s & 1) ? tg[s >> 1] : 0;
+    if ((s & 1) && (mylab < 1 || mylab >= V)) {
+      atomicOr(&badsh, 1);
+      mylab = 0;
+    }
+    lab[s] = mylab;
+  }
+  __syncthreads();
+  if (dir == 0) {  // label CSR for ctc_marg_kernel: odd states by label, increasing s
+    if (tid == 0) {
+      for (int v = 0; v <= V; ++v) off[v] = 0;
+      for (int k = 0; k < L; ++k) off[lab[2 * k + 1] + 1]++;
+      for (int v = 0; v < V; ++v) off[v + 1] += off[v];
+      for (int k = 0; k < L; ++k) lst[k] = -1;
       for (int k = 0; k < L; ++k) {
-        int pos = sm.off[sm.lab[2 * k + 1]];
-        while (sm.lst[pos] >= 0) ++pos;
-        sm.lst[pos] = 2 * k + 1;
+        int pos = off[lab[2 * k + 1]];
+        while (lst[pos] >= 0) ++pos;
+        lst[pos] = 2 * k + 1;
       }
     }
     __syncthreads();
-  }
-  const int nwarps = blockDim.x >> 5;
-  (void)nwarps;
-  float* wsb = (kMode == 1) ? wsb_all + (size_t)b * T * S : nullptr;
-  if (kMode == 1) {  // the label CSR, for ctc_marg_kernel
     int32_t* csr = csr_all + (size_t)b * (V + 1 + L);
-    for (int e = tid; e <= V; e += blockDim.x) csr[e] = sm.off[e];
-    for (int e = tid; e < L; e += blockDim.x) csr[V + 1 + e] = sm.lst[e];
+    for (int e = tid; e <= V; e += blockDim.x) csr[e] = off[e];
+    for (int e = tid; e < L; e += blockDim.x) csr[V + 1 + e] = lst[e];
   }
-  double* wsbase = (kMode == 1) ? wsbase_all + (size_t)b * T * 32 : nullptr;  // [T][32 warps]
-
-  // ======================= phase A: backward (marginals only)
-  if (kMode == 1) {
-    double* cur = sm.a0 + 2;  // beta[t+1][*]
-    double* nxt = sm.a1 + 2;
-    // prefetch frames T-1 .. T-kP (we need E[t+1] while computing beta[t])
+  // vectors as fp32 offsets from a per-warp base (one REDUX max per frame, no CTA reduction);
+  // the base is an fp32 value (the warp max of the fp32-rounded vector), so it is stored as one
+  auto store = [&](float* ws, float* wsbase, int t, double v) {
+    const float wm = warp_max((float)v);
+    const float base = (wm == ninf()) ? 0.f : wm;
+    if (act) ws[(size_t)t * S + s] = (v == ninfd()) ? ninf() : (float)(v - (double)base);
+    if (lane == 0) wsbase[(size_t)t * 32 + wq] = base;
+  };
+  if (tid < 2) { a0[tid] = ninfd(); a1[tid] = ninfd(); }
+  if (dir == 1) {
+    // ======================= backward (alignment.py:272-287)
+    float* wsb = wsb_all + (size_t)b * T * S;
+    float* wsbase = wsbase_all + (size_t)b * T * 32;
+    double* cur = a0 + 2;  // beta[t+1][*]
+    double* nxt = a1 + 2;
     for (int k = 0; k < kP; ++k) {
       const int t = T - 1 - k;
-      if (t >= 0) load_row(fp, t, V, sm.rows + (size_t)(t % kP) * V);
+      if (t >= 0) load_row(fp, t, V, rows + (size_t)(t % kP) * V);
       cp_commit();
     }
     if (act) cur[s] = (s == S - 1 || s == S - 2) ? 0.0 : ninfd();
     if (tid < S + 2 && tid >= S) cur[tid] = ninfd();  // right pads beyond S
-    if (tid < 2) { sm.a0[tid] = ninfd(); sm.a1[tid] = ninfd(); }
     __syncthreads();
-    // store beta[T-1] (offsets from a per-WARP base: a warp max, no CTA reduction per frame)
-    {
-      const double v = act ? cur[s] : ninfd();
-      const float wm = warp_max((float)v);
-      const double base = (wm == ninf()) ? 0.0 : (double)wm;
-      if (act) wsb[(size_t)(T - 1) * S + s] = (v == ninfd()) ? ninf() : (float)(v - base);
-      if ((tid & 31) == 0) wsbase[(size_t)(T - 1) * 32 + (tid >> 5)] = base;
-    }
-    // successor labels of this state are fixed for all frames: keep them in registers
+    store(wsb, wsbase, T - 1, act ? cur[s] : ninfd());
     const bool has1 = act && (s + 1 < S);
-    const int lab1 = has1 ? sm.lab[s + 1] : 0;
-    const int lab2 = (act && s + 2 < S) ? sm.lab[s + 2] : 0;
+    const int lab1 = has1 ? lab[s + 1] : 0;
+    const int lab2 = (act && s + 2 < S) ? lab[s + 2] : 0;
     const bool sk2 = act && (s + 2 < S) && lab2 != 0 && lab2 != mylab;
     for (int t = T - 2; t >= 0; --t) {
-      // frame t+1 must be resident: it was issued (T-1)-(t+1) groups ago
       cp_wait<kP - 1>();
       __syncthreads();
-      const float* E = sm.rows + (size_t)((t + 1) % kP) * V;
+      const float* E = rows + (size_t)((t + 1) % kP) * V;
       double v = ninfd();
       if (act) {
         const double x0 = cur[s] + (double)E[mylab];
@@ -173,140 +275,68 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
         }
         nxt[s] = v;
       }
-      // beta[t] as fp32 offsets from its warp's max (the base only has to be close to the
-      // values it is subtracted from; one fp32 warp max, no CTA-wide reduction)
-      {
-        const float wm = warp_max((float)v);
-        const double base = (wm == ninf()) ? 0.0 : (double)wm;
-        if (act) wsb[(size_t)t * S + s] = (v == ninfd()) ? ninf() : (float)(v - base);
-        if ((tid & 31) == 0) wsbase[(size_t)t * 32 + (tid >> 5)] = base;
-      }
+      store(wsb, wsbase, t, v);
       __syncthreads();  // all reads of cur and row (t+1) done; nxt complete
-      // refill the ring slot of frame t+1 with frame t+1-kP
       {
         const int tn = t + 1 - kP;
-        if (tn >= 0) load_row(fp, tn, V, sm.rows + (size_t)(tn % kP) * V);
+        if (tn >= 0) load_row(fp, tn, V, rows + (size_t)(tn % kP) * V);
         cp_commit();
       }
       double* tmp = cur; cur = nxt; nxt = tmp;
     }
     cp_wait<0>();
-    __syncthreads();
-    // Z = lse(beta[0][0] + E0[lab0], beta[0][1] + E0[lab1])  (E0 = frame 0 still in the ring)
-    if (tid == 0) {
-      const float* E0 = sm.rows;  // frame 0 sits in slot 0
-      const double z0 = cur[0] + (double)E0[sm.lab[0]];
-      const double z1 = (S > 1) ? cur[1] + (double)E0[sm.lab[1]] : ninfd();
-      const double M = fmax(z0, z1);
-      zsh = (M == ninfd()) ? ninfd() : M + (double)flog(fexp((float)(z0 - M)) + fexp((float)(z1 - M)));
-    }
-    __syncthreads();
+    return;
   }
-
-  // ======================= phase B: forward
-  {
-    double* prv = sm.a0 + 2;  // alpha[t-1]
-    double* now = sm.a1 + 2;
-    if (tid < 2) { sm.a0[tid] = ninfd(); sm.a1[tid] = ninfd(); }
-    auto load_beta = [&](int t) {  // beta row t + its base into ring slot t % kP
-      if (kMode != 1) return;
-      if (act) cp_async4(sm.bring + (size_t)(t % kP) * S + s, wsb + (size_t)t * S + s);
-      if ((tid & 31) == 0) {  // this warp's base
-        unsigned sa = (unsigned)__cvta_generic_to_shared(sm.bbase + (t % kP) * 32 + (tid >> 5));
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(wsbase + (size_t)t * 32 + (tid >> 5)));
+  // ======================= forward (alignment.py:248-269)
+  float* wsa = wsa_all + (size_t)b * T * S;
+  float* wsabase = wsabase_all + (size_t)b * T * 32;
+  double* prv = a0 + 2;
+  double* now = a1 + 2;
+  const bool skip = act && (s >= 2) && mylab != 0 && mylab != lab[s - 2];
+  for (int k = 0; k < kP; ++k) {
+    if (k < T) load_row(fp, k, V, rows + (size_t)k * V);
+    cp_commit();
+  }
+  int bad = 0;
+  for (int t = 0; t < T; ++t) {
+    cp_wait<kP - 1>();
+    __syncthreads();
+    const float* E = rows + (size_t)(t % kP) * V;
+    for (int v = tid; v < V; v += blockDim.x) bad |= bad_input(E[v]);
+    double a = ninfd();
+    if (act) {
+      const double e = (double)E[mylab];
+      if (t == 0) {
+        a = (s <= 1) ? e : ninfd();
+      } else {
+        const double x0 = prv[s], x1 = prv[s - 1], x2 = skip ? prv[s - 2] : ninfd();
+        const double M = fmax(fmax(x0, x1), x2);
+        if (M != ninfd()) {
+          const float sum = fexp((float)(x0 - M)) + fexp((float)(x1 - M)) + fexp((float)(x2 - M));
+          a = M + (double)flog(sum) + e;
+        }
       }
-    };
-    for (int k = 0; k < kP; ++k) {
-      if (k < T) {
-        load_row(fp, k, V, sm.rows + (size_t)k * V);
-        load_beta(k);
-      }
+      now[s] = a;
+    }
+    store(wsa, wsabase, t, a);
+    __syncthreads();  // now[] complete; row t consumed
+    {
+      const int tn = t + kP;
+      if (tn < T) load_row(fp, tn, V, rows + (size_t)(tn % kP) * V);
       cp_commit();
     }
-    const double Z = zsh;
-    const bool zok = Z != ninfd();
-    int8_t* back = (kMode == 2) ? back_all + (size_t)b * T * S : nullptr;
-    int bad = 0;
-    for (int t = 0; t < T; ++t) {
-      cp_wait<kP - 1>();
-      __syncthreads();
-      const float* E = sm.rows + (size_t)(t % kP) * V;
-      for (int v = tid; v < V; v += blockDim.x) bad |= bad_input(E[v]);
-      double a = ninfd();
-      if (act) {
-        const double e = (double)E[mylab];
-        if (t == 0) {
-          a = (s <= 1) ? e : ninfd();
-        } else if (kMode == 2) {
-          // first maximum in predecessor order [s, s-1, s-2] (alignment.py:239-245, 304-318)
-          double best = prv[s];
-          int k = 0;
-          if (s >= 1 && prv[s - 1] > best) { best = prv[s - 1]; k = 1; }
-          if (skip && prv[s - 2] > best) { best = prv[s - 2]; k = 2; }
-          a = best + e;
-          back[(size_t)t * S + s] = (int8_t)k;
-        } else {
-          const double x0 = prv[s], x1 = prv[s - 1], x2 = skip ? prv[s - 2] : ninfd();
-          const double M = fmax(fmax(x0, x1), x2);
-          if (M != ninfd()) {
-            const float sum = fexp((float)(x0 - M)) + fexp((float)(x1 - M)) + fexp((float)(x2 - M));
-            a = M + (double)flog(sum) + e;
-          }
-        }
-        now[s] = a;
-      }
-      if (kMode == 1 && act) {
-        // posterior of state s at frame t, written over beta's slot (frame t of the beta ring
-        // has been consumed); ctc_marg_kernel scatter-adds the rows by label off this loop
-        float p = 0.f;
-        if (zok && a != ninfd()) {
-          const float bt = sm.bring[(size_t)(t % kP) * S + s];
-          const double bb = sm.bbase[(t % kP) * 32 + (tid >> 5)];
-          if (bt != ninf()) p = fexp((float)(a + bb - Z) + bt);
-        }
-        wsb[(size_t)t * S + s] = p;
-      }
-      __syncthreads();  // now[] complete; row t consumed
-      {
-        const int tn = t + kP;
-        if (tn < T) {
-          load_row(fp, tn, V, sm.rows + (size_t)(tn % kP) * V);
-          load_beta(tn);
-        }
-        cp_commit();
-      }
-      double* tmp = prv; prv = now; now = tmp;
-    }
-    cp_wait<0>();
-    if (bad) atomicOr(&badsh, 1);
-    __syncthreads();
-    // final states (alignment.py:263-264): [S-1] or [S-1, S-2]
-    if (tid == 0) {
-      const double f1 = prv[S - 1];
-      const double f2 = (S > 1) ? prv[S - 2] : ninfd();
-      double res;
-      int fin = S - 1;
-      if (kMode == 2) {
-        res = f1;
-        if (S > 1 && f2 > f1) { res = f2; fin = S - 2; }
-      } else {
-        const double M = fmax(f1, f2);
-        res = (M == ninfd()) ? ninfd() : M + (double)flog(fexp((float)(f1 - M)) + fexp((float)(f2 - M)));
-      }
-      const int st = badsh ? SDB_ST_INVALID : (res == ninfd() ? SDB_ST_VACUOUS : SDB_ST_OK);
-      status[b] = st;
-      if (kMode == 2) {
-        score[b] = res;
-        int32_t* path = path_all + (size_t)b * T;
-        int cs = fin;
-        for (int t = T - 1; t >= 0; --t) {
-          path[t] = (st == SDB_ST_OK) ? sm.lab[cs] : 0;
-          if (t > 0 && st == SDB_ST_OK) cs -= back[(size_t)t * S + cs];
-        }
-      } else {
-        logz[b] = res;
-      }
-    }
+    double* tmp = prv; prv = now; now = tmp;
+  }
+  cp_wait<0>();
+  if (bad) atomicOr(&badsh, 1);
+  __syncthreads();
+  if (tid == 0) {  // final states (alignment.py:263-264): [S-1] or [S-1, S-2]
+    const double f1 = prv[S - 1];
+    const double f2 = (S > 1) ? prv[S - 2] : ninfd();
+    const double M = fmax(f1, f2);
+    const double Z = (M == ninfd()) ? ninfd() : M + (double)flog(fexp((float)(f1 - M)) + fexp((float)(f2 - M)));
+    status[b] = badsh ? SDB_ST_INVALID : (Z == ninfd() ? SDB_ST_VACUOUS : SDB_ST_OK);
+    logz[b] = Z;
   }
 }
 
@@ -324,10 +354,10 @@ constexpr int kMargFrames = 32;     // frames per CTA (4 per warp)
 // never wait on each other (the per-frame CTA barriers of a row-per-CTA layout
 // left this kernel latency-bound).
 template <int kRowRegs>  // >= ceil(S / 32): the row's states per lane
-__global__ void __launch_bounds__(kMargWarps * 32) ctc_marg_kernel(const float* __restrict__ post_all,
-                                                                  const int32_t* __restrict__ csr_all, int T, int V,
-                                                                  int L, const int32_t* __restrict__ status,
-                                                                  float* __restrict__ marg_all) {
+__global__ void __launch_bounds__(kMargWarps * 32) ctc_marg_kernel(
+    const float* __restrict__ wsa_all, const float* __restrict__ wsabase_all, const float* __restrict__ wsb_all,
+    const float* __restrict__ wsbase_all, const double* __restrict__ logz, const int32_t* __restrict__ csr_all,
+    int T, int V, int L, const int32_t* __restrict__ status, float* __restrict__ marg_all) {
   extern __shared__ __align__(16) float cm[];
   const int S = 2 * L + 1;
   int* off = reinterpret_cast<int*>(cm);      // [V+1]
@@ -346,15 +376,27 @@ __global__ void __launch_bounds__(kMargWarps * 32) ctc_marg_kernel(const float* 
   for (int e = tid; e < L; e += blockDim.x) lst[e] = csr[V + 1 + e];
   __syncthreads();
   float* prow = prow_all + (size_t)warp * S;
-  const float* pb = post_all + (size_t)b * T * S;
-  // the warp's next frame is loaded into registers while the current one is reduced
-  float nxt[kRowRegs];
+  const float* pa = wsa_all + (size_t)b * T * S;
+  const float* pb = wsb_all + (size_t)b * T * S;
+  const float* ba = wsabase_all + (size_t)b * T * 32;
+  const float* bb = wsbase_all + (size_t)b * T * 32;
+  const double Z = logz[b];
+  // the warp's next frame (both offsets and the two bases of each 32-state group) is loaded into
+  // registers while the current one is reduced; the posterior of state e = 32 u + lane is
+  // exp(alpha + beta - Z): bases and Z combined in fp64, the offsets added in fp32
+  float xa[kRowRegs], xb[kRowRegs], ca[kRowRegs], cb[kRowRegs];
   auto fetch = [&](int t) {
-    const float* src = pb + (size_t)t * S;
+    const float* sa = pa + (size_t)t * S;
+    const float* sb = pb + (size_t)t * S;
 #pragma unroll
     for (int u = 0; u < kRowRegs; ++u) {
       const int e = lane + 32 * u;
-      if (e < S) nxt[u] = src[e];
+      if (e < S) {
+        xa[u] = sa[e];
+        xb[u] = sb[e];
+        ca[u] = ba[(size_t)t * 32 + u];
+        cb[u] = bb[(size_t)t * 32 + u];
+      }
     }
   };
   if (t0 + warp < t1) fetch(t0 + warp);
@@ -362,7 +404,10 @@ __global__ void __launch_bounds__(kMargWarps * 32) ctc_marg_kernel(const float* 
 #pragma unroll
     for (int u = 0; u < kRowRegs; ++u) {
       const int e = lane + 32 * u;
-      if (e < S) prow[e] = nxt[u];
+      if (e < S) {
+        const float c = (float)((double)ca[u] + (double)cb[u] - Z);
+        prow[e] = (xa[u] == ninf() || xb[u] == ninf()) ? 0.f : fexp(c + xa[u] + xb[u]);
+      }
     }
     if (t + kMargWarps < t1) fetch(t + kMargWarps);
     __syncwarp();
@@ -384,8 +429,10 @@ __global__ void __launch_bounds__(kMargWarps * 32) ctc_marg_kernel(const float* 
 }
 
 struct CtcWs {
-  float* wsb;      // [B][T][S] beta offsets, then the state posteriors
-  double* wsbase;  // [B][T][32] per-warp beta bases
+  float* wsa;      // [B][T][S] alpha offsets
+  float* wsabase;  // [B][T][32] per-warp alpha bases
+  float* wsb;      // [B][T][S] beta offsets
+  float* wsbase;   // [B][T][32] per-warp beta bases
   int32_t* csr;    // [B][V+1+L] label CSR (offsets, odd states by label)
   int8_t* back;
 };
@@ -395,8 +442,10 @@ CtcWs ctc_carve_ws(void* base, int64_t B, int T, int V, int L, int mode, size_t*
   Carve c(base);
   CtcWs w{};
   if (mode == 1) {
+    w.wsa = c.take<float>((size_t)B * T * S);
+    w.wsabase = c.take<float>((size_t)B * T * 32);
     w.wsb = c.take<float>((size_t)B * T * S);
-    w.wsbase = c.take<double>((size_t)B * T * 32);
+    w.wsbase = c.take<float>((size_t)B * T * 32);
     w.csr = c.take<int32_t>((size_t)B * (V + 1 + L));
   }
   if (mode == 2) w.back = c.take<int8_t>((size_t)B * T * S);
@@ -416,11 +465,19 @@ int ctc_launch(const float* fp, const int32_t* tg, int64_t B, int T, int V, int 
                float* marg, int32_t* path, double* score, int32_t* status, cudaStream_t s) {
   const int S = 2 * L + 1;
   const int threads = ((S + 31) / 32) * 32;
-  const size_t smem = ctc_smem_bytes(S, V, L);
-  if (cudaFuncSetAttribute(ctc_kernel<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-    return SDB_ERR_CUDA;
-  ctc_kernel<kMode><<<(unsigned)B, threads, smem, s>>>(fp, tg, T, V, L, ws.wsb, ws.wsbase, ws.csr, ws.back, logz,
-                                                      marg, path, score, status);
+  if constexpr (kMode == 1) {
+    const size_t dsmem = ctc_dir_smem_bytes(S, V, L);
+    if (dsmem > 48 * 1024 &&
+        cudaFuncSetAttribute(ctc_dir_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem) != cudaSuccess)
+      return SDB_ERR_CUDA;
+    ctc_dir_kernel<<<dim3((unsigned)B, 2), threads, dsmem, s>>>(fp, tg, T, V, L, ws.wsa, ws.wsabase, ws.wsb,
+                                                                ws.wsbase, ws.csr, logz, status);
+  } else {
+    const size_t smem = ctc_smem_bytes(S, V, L);
+    if (cudaFuncSetAttribute(ctc_kernel<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return SDB_ERR_CUDA;
+    ctc_kernel<kMode><<<(unsigned)B, threads, smem, s>>>(fp, tg, T, V, L, ws.back, logz, path, score, status);
+  }
   SDB_CHECK_LAUNCH();
   if (kMode == 1) {
     const int S2 = 2 * L + 1;
@@ -431,12 +488,14 @@ int ctc_launch(const float* fp, const int32_t* tg, int64_t B, int T, int V, int 
       if (msmem > 48 * 1024 && cudaFuncSetAttribute(ctc_marg_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     (int)msmem) != cudaSuccess)
         return SDB_ERR_CUDA;
-      ctc_marg_kernel<9><<<g, kMargWarps * 32, msmem, s>>>(ws.wsb, ws.csr, T, V, L, status, marg);
+      ctc_marg_kernel<9><<<g, kMargWarps * 32, msmem, s>>>(ws.wsa, ws.wsabase, ws.wsb, ws.wsbase, logz, ws.csr, T, V,
+                                                          L, status, marg);
     } else {
       if (msmem > 48 * 1024 && cudaFuncSetAttribute(ctc_marg_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     (int)msmem) != cudaSuccess)
         return SDB_ERR_CUDA;
-      ctc_marg_kernel<32><<<g, kMargWarps * 32, msmem, s>>>(ws.wsb, ws.csr, T, V, L, status, marg);
+      ctc_marg_kernel<32><<<g, kMargWarps * 32, msmem, s>>>(ws.wsa, ws.wsabase, ws.wsb, ws.wsbase, logz, ws.csr, T,
+                                                           V, L, status, marg);
     }
     SDB_CHECK_LAUNCH();
   }
