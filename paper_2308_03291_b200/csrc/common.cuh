@@ -99,6 +99,16 @@ __device__ __forceinline__ float warp_max(float v) {
   const uint32_t mk = __reduce_max_sync(0xffffffffu, key);
   return __uint_as_float(mk ^ (((mk >> 31) - 1u) | 0x80000000u));
 }
+// Full-warp max of doubles truncated to their high words (sign, exponent, 20
+// mantissa bits): one REDUX on the same order-preserving keys as warp_max.  The
+// result is within 2^-20 relative of the true maximum and, inside the fp32
+// exponent range, exactly representable as a float.
+__device__ __forceinline__ double warp_max_hi(double v) {
+  const uint32_t u = (uint32_t)__double2hiint(v);
+  const uint32_t key = u ^ ((uint32_t)((int32_t)u >> 31) | 0x80000000u);
+  const uint32_t mk = __reduce_max_sync(0xffffffffu, key);
+  return __hiloint2double((int)(mk ^ (((mk >> 31) - 1u) | 0x80000000u)), 0);
+}
 __device__ __forceinline__ float warp_max_shfl(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));

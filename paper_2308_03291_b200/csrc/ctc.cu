@@ -174,7 +174,7 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
 // per-frame latency chains of the two directions overlap across the SM
 // instead of running back to back.
 size_t ctc_dir_smem_bytes(int S, int V, int L) {
-  return (size_t)2 * (S + 2) * 8 + (size_t)kP * V * 4 + (size_t)S * 4 + (size_t)(L + 1) * 4 + (size_t)(V + 1) * 4 +
+  return (size_t)3 * (S + 2) * 8 + (size_t)kP * V * 4 + (size_t)S * 4 + (size_t)(L + 1) * 4 + (size_t)(V + 1) * 4 +
          128;
 }
 
@@ -185,13 +185,14 @@ __global__ void ctc_dir_kernel(const float* __restrict__ fp_all, const int32_t* 
                                int32_t* __restrict__ status) {
   extern __shared__ __align__(16) char smraw[];
   const int S = 2 * L + 1;
-  double *a0, *a1;
+  double *a0, *a1, *a2;  // three vector buffers: one barrier per frame
   float* rows;
   int *lab, *lst, *off;
   {
     char* p = smraw;
     a0 = (double*)p; p += (size_t)(S + 2) * 8;
     a1 = (double*)p; p += (size_t)(S + 2) * 8;
+    a2 = (double*)p; p += (size_t)(S + 2) * 8;
     rows = (float*)p; p += (size_t)kP * V * 4;
     lab = (int*)p; p += (size_t)S * 4;
     lst = (int*)p; p += (size_t)(L + 1) * 4;
@@ -231,58 +232,68 @@ __global__ void ctc_dir_kernel(const float* __restrict__ fp_all, const int32_t* 
     for (int e = tid; e <= V; e += blockDim.x) csr[e] = off[e];
     for (int e = tid; e < L; e += blockDim.x) csr[V + 1 + e] = lst[e];
   }
-  // vectors as fp32 offsets from a per-warp base (one REDUX max per frame, no CTA reduction);
-  // the base is an fp32 value (the warp max of the fp32-rounded vector), so it is stored as one
+  // vectors as fp32 offsets from a per-warp base (one REDUX max per frame, no CTA reduction).
+  // The base is the warp maximum truncated to its high word (20 mantissa bits), found by a REDUX
+  // on the high words' order-preserving keys: a double that is exactly an fp32 value, so it is
+  // stored as one, and one f64->f32 conversion per state (the offset) is all the store costs.
   auto store = [&](float* ws, float* wsbase, int t, double v) {
-    const float wm = warp_max((float)v);
-    const float base = (wm == ninf()) ? 0.f : wm;
-    if (act) ws[(size_t)t * S + s] = (v == ninfd()) ? ninf() : (float)(v - (double)base);
-    if (lane == 0) wsbase[(size_t)t * 32 + wq] = base;
+    const double bm = warp_max_hi(v);
+    const double base = (bm == ninfd()) ? 0.0 : bm;
+    if (act) ws[(size_t)t * S + s] = (v == ninfd()) ? ninf() : (float)(v - base);
+    if (lane == 0) wsbase[(size_t)t * 32 + wq] = (float)base;
   };
-  if (tid < 2) { a0[tid] = ninfd(); a1[tid] = ninfd(); }
+  if (tid < 2) { a0[tid] = ninfd(); a1[tid] = ninfd(); a2[tid] = ninfd(); }
+  // Frames advance with ONE barrier each: the vector written at frame t goes to the buffer
+  // last read at frame t-2 (every thread is past frame t-1 once it passes frame t's barrier),
+  // and the row slot refilled after frame t's barrier is the one frame t-1 (forward) / t+1
+  // (backward) consumed.
   if (dir == 1) {
     // ======================= backward (alignment.py:272-287)
     float* wsb = wsb_all + (size_t)b * T * S;
     float* wsbase = wsbase_all + (size_t)b * T * 32;
-    double* cur = a0 + 2;  // beta[t+1][*]
+    double* cur = a0 + 2;  // beta[t+1][*] + theta[t+1][lab(*)]
     double* nxt = a1 + 2;
+    double* spare = a2 + 2;
     for (int k = 0; k < kP; ++k) {
       const int t = T - 1 - k;
       if (t >= 0) load_row(fp, t, V, rows + (size_t)(t % kP) * V);
       cp_commit();
     }
-    if (act) cur[s] = (s == S - 1 || s == S - 2) ? 0.0 : ninfd();
-    if (tid < S + 2 && tid >= S) cur[tid] = ninfd();  // right pads beyond S
-    __syncthreads();
-    store(wsb, wsbase, T - 1, act ? cur[s] : ninfd());
+    // the ring holds beta[t+1][s] + theta[t+1][lab(s)] (the successor term every predecessor of
+    // s reads), so a state converts and adds ONE emission per frame instead of three
+    cp_wait<kP - 1>();
+    __syncthreads();  // row T-1 landed
+    if (act) {
+      const double b0 = (s == S - 1 || s == S - 2) ? 0.0 : ninfd();
+      cur[s] = b0 + (double)rows[(size_t)((T - 1) % kP) * V + mylab];
+    }
+    store(wsb, wsbase, T - 1, (act && (s == S - 1 || s == S - 2)) ? 0.0 : ninfd());
     const bool has1 = act && (s + 1 < S);
-    const int lab1 = has1 ? lab[s + 1] : 0;
     const int lab2 = (act && s + 2 < S) ? lab[s + 2] : 0;
     const bool sk2 = act && (s + 2 < S) && lab2 != 0 && lab2 != mylab;
     for (int t = T - 2; t >= 0; --t) {
-      cp_wait<kP - 1>();
-      __syncthreads();
-      const float* E = rows + (size_t)((t + 1) % kP) * V;
+      cp_wait<kP - 2>();
+      __syncthreads();  // rows t+1 (consumed into cur) and t landed; cur complete
+      {
+        const int tn = t + 1 - kP;  // into row t+1's slot: no thread reads it any more
+        if (tn >= 0) load_row(fp, tn, V, rows + (size_t)(tn % kP) * V);
+        cp_commit();
+      }
+      const float* E = rows + (size_t)(t % kP) * V;
       double v = ninfd();
       if (act) {
-        const double x0 = cur[s] + (double)E[mylab];
-        const double x1 = has1 ? cur[s + 1] + (double)E[lab1] : ninfd();
-        const double x2 = sk2 ? cur[s + 2] + (double)E[lab2] : ninfd();
+        const double x0 = cur[s];
+        const double x1 = has1 ? cur[s + 1] : ninfd();
+        const double x2 = sk2 ? cur[s + 2] : ninfd();
         const double M = fmax(fmax(x0, x1), x2);
         if (M != ninfd()) {
           const float e = fexp((float)(x0 - M)) + fexp((float)(x1 - M)) + fexp((float)(x2 - M));
           v = M + (double)flog(e);
         }
-        nxt[s] = v;
+        nxt[s] = v + (double)E[mylab];
       }
       store(wsb, wsbase, t, v);
-      __syncthreads();  // all reads of cur and row (t+1) done; nxt complete
-      {
-        const int tn = t + 1 - kP;
-        if (tn >= 0) load_row(fp, tn, V, rows + (size_t)(tn % kP) * V);
-        cp_commit();
-      }
-      double* tmp = cur; cur = nxt; nxt = tmp;
+      double* tmp = cur; cur = nxt; nxt = spare; spare = tmp;
     }
     cp_wait<0>();
     return;
@@ -292,15 +303,21 @@ __global__ void ctc_dir_kernel(const float* __restrict__ fp_all, const int32_t* 
   float* wsabase = wsabase_all + (size_t)b * T * 32;
   double* prv = a0 + 2;
   double* now = a1 + 2;
+  double* spare = a2 + 2;
   const bool skip = act && (s >= 2) && mylab != 0 && mylab != lab[s - 2];
-  for (int k = 0; k < kP; ++k) {
+  for (int k = 0; k < kP - 1; ++k) {
     if (k < T) load_row(fp, k, V, rows + (size_t)k * V);
     cp_commit();
   }
   int bad = 0;
   for (int t = 0; t < T; ++t) {
-    cp_wait<kP - 1>();
-    __syncthreads();
+    cp_wait<kP - 2>();
+    __syncthreads();  // row t landed; alpha[t-1] complete; row t-1 consumed
+    {
+      const int tn = t + kP - 1;  // into row t-1's slot
+      if (tn < T) load_row(fp, tn, V, rows + (size_t)(tn % kP) * V);
+      cp_commit();
+    }
     const float* E = rows + (size_t)(t % kP) * V;
     for (int v = tid; v < V; v += blockDim.x) bad |= bad_input(E[v]);
     double a = ninfd();
@@ -319,13 +336,7 @@ __global__ void ctc_dir_kernel(const float* __restrict__ fp_all, const int32_t* 
       now[s] = a;
     }
     store(wsa, wsabase, t, a);
-    __syncthreads();  // now[] complete; row t consumed
-    {
-      const int tn = t + kP;
-      if (tn < T) load_row(fp, tn, V, rows + (size_t)(tn % kP) * V);
-      cp_commit();
-    }
-    double* tmp = prv; prv = now; now = tmp;
+    double* tmp = prv; prv = now; now = spare; spare = tmp;
   }
   cp_wait<0>();
   if (bad) atomicOr(&badsh, 1);
