@@ -395,7 +395,9 @@ __global__ void __launch_bounds__(kMargWarps * 32) ctc_marg_kernel(
   // the warp's next frame (both offsets and the two bases of each 32-state group) is loaded into
   // registers while the current one is reduced; the posterior of state e = 32 u + lane is
   // exp(alpha + beta - Z): bases and Z combined in fp64, the offsets added in fp32
-  float xa[kRowRegs], xb[kRowRegs], ca[kRowRegs], cb[kRowRegs];
+  // Lane g loads the two bases of 32-state group g (one coalesced load each) and forms that
+  // group's fp64 combination once; the state loop takes it by shuffle.
+  float xa[kRowRegs], xb[kRowRegs], ca, cb;
   auto fetch = [&](int t) {
     const float* sa = pa + (size_t)t * S;
     const float* sb = pb + (size_t)t * S;
@@ -405,18 +407,19 @@ __global__ void __launch_bounds__(kMargWarps * 32) ctc_marg_kernel(
       if (e < S) {
         xa[u] = sa[e];
         xb[u] = sb[e];
-        ca[u] = ba[(size_t)t * 32 + u];
-        cb[u] = bb[(size_t)t * 32 + u];
       }
     }
+    ca = ba[(size_t)t * 32 + lane];
+    cb = bb[(size_t)t * 32 + lane];
   };
   if (t0 + warp < t1) fetch(t0 + warp);
   for (int t = t0 + warp; t < t1; t += kMargWarps) {
+    const float cl = (float)((double)ca + (double)cb - Z);  // group `lane` (groups >= ceil(S/32) unused)
 #pragma unroll
     for (int u = 0; u < kRowRegs; ++u) {
       const int e = lane + 32 * u;
+      const float c = __shfl_sync(0xffffffffu, cl, u);
       if (e < S) {
-        const float c = (float)((double)ca[u] + (double)cb[u] - Z);
         prow[e] = (xa[u] == ninf() || xb[u] == ninf()) ? 0.f : fexp(c + xa[u] + xb[u]);
       }
     }
