@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(kMargWarps * 32) ctc_marg_kernel(
       const int e = lane + 32 * u;
       const float c = __shfl_sync(0xffffffffu, cl, u);
       if (e < S) {
-        prow[e] = (xa[u] == ninf() || xb[u] == ninf()) ? 0.f : fexp(c + xa[u] + xb[u]);
+        prow[e] = fexp(c + xa[u] + xb[u]);  // an -inf offset gives ex2(-inf) = +0 (no +inf offsets)
       }
     }
     if (t + kMargWarps < t1) fetch(t + kMargWarps);
