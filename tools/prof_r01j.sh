@@ -11,5 +11,5 @@ python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_referen
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/launches_c2b.csv python bench.py --config c2b --steps 2 --warmup 3 --no-cpu > /dev/null 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:"ctc_(dir|marg)" -c 2 \
-  -o gpurun_out/r01k_ctc python tools/prof_one.py ctc fb > /dev/null 2>&1
+  -o gpurun_out/r01l_ctc python tools/prof_one.py ctc fb > /dev/null 2>&1
 echo done
