@@ -351,8 +351,8 @@ __global__ void ctc_dir_kernel(const float* __restrict__ fp_all, const int32_t* 
   }
 }
 
-// Per-frame vocabulary marginals from the posteriors ctc_kernel<1> left in
-// the workspace (alignment.py:290-301): marg[t][v] = sum of post[t][s] over
+// Per-frame vocabulary marginals from the alpha/beta offsets ctc_dir_kernel left
+// in the workspace (alignment.py:290-301): marg[t][v] = sum of post[t][s] over
 // the states s with label v (blank: the L+1 even states; repeated labels
 // accumulate), in increasing s -- a deterministic order.  Grid (frame blocks,
 // instances), every frame independent, so this streams at HBM rate instead of
@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(kMargWarps * 32) ctc_marg_kernel(
     for (int e = tid; e < (t1 - t0) * V; e += blockDim.x) mg[(size_t)t0 * V + e] = 0.f;
     return;
   }
-  const int32_t* csr = csr_all + (size_t)b * (V + 1 + L);  // built by ctc_kernel<1>
+  const int32_t* csr = csr_all + (size_t)b * (V + 1 + L);  // built by ctc_dir_kernel's forward CTA
   for (int e = tid; e <= V; e += blockDim.x) off[e] = csr[e];
   for (int e = tid; e < L; e += blockDim.x) lst[e] = csr[V + 1 + e];
   __syncthreads();
