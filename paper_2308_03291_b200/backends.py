@@ -596,22 +596,6 @@ class SpanningBackend(Backend):
 # ------------------------------------------------------------------- PCFG
 
 
-def is_binary_bracketing(spans, n: int) -> bool:
-    """constituency.py:147-164: `spans` is exactly the node-span set of one
-    binary tree (host-side validation of an indicator)."""
-    if len(spans) != 2 * n - 1 or (0, n - 1) not in spans or any((i, i) not in spans for i in range(n)):
-        return False
-    memo = {}
-
-    def check(i, j):
-        if i == j:
-            return True
-        if (i, j) not in memo:
-            memo[(i, j)] = any((i, k) in spans and (k + 1, j) in spans and check(i, k) and check(k + 1, j)
-                               for k in range(i, j))
-        return memo[(i, j)]
-
-    return check(0, n - 1)
 
 
 class PCFGBackend(Backend):
@@ -651,12 +635,9 @@ class PCFGBackend(Backend):
     def log_prob(self, d, ind):
         """dist.py:266-271: log-probability of a bracketing = masked inside -
         inside, both in ONE batched kernel call (the mask rides on sticky)."""
-        mask = ind["sticky"]
-        if mask.shape != (d.n, d.n):
-            raise InvalidProblem("indicator span mask must have shape [n, n]")
-        spans = {(int(i), int(j)) for i, j in np.argwhere(mask > 0)}
-        if not is_binary_bracketing(spans, d.n):
-            raise InvalidProblem("marked spans do not form a binary bracketing")
+        from .validate import pcfg_spans
+
+        spans = pcfg_spans(d, ind)
         span_mask = np.full((d.n, d.n), -np.inf)
         for i, j in spans:
             span_mask[i, j] = 0.0

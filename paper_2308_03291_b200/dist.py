@@ -23,6 +23,7 @@ import torch
 from . import backends
 from .errors import InvalidProblem, ONE_TO_ONE_REASON, UnsupportedInference, VacuousDistribution
 from .families import PCFG, OneToOneMatching
+from .validate import validate_indicator
 
 NEG_INF = float("-inf")
 
@@ -218,13 +219,11 @@ def _directed(d):
 
 
 def log_prob_info(dist, indicator):
-    """dist.py:263-276 for the score-based families."""
+    """dist.py:263-276: validate the indicator (validate.py), then score -
+    log Z on the GPU (PCFG: masked inside - inside in one launch)."""
     _reject_one_to_one(dist)
     be = _backend(dist)
-    ind = {k: np.asarray(v, dtype=np.float64) for k, v in indicator.items()}
-    for key, mask in ind.items():
-        if (~((mask == 0.0) | (mask == 1.0))).any():
-            raise InvalidProblem(f"indicator {key!r} entries must be 0 or 1")
+    ind = validate_indicator(dist, indicator)  # dist.py:224-248, per-family structural checks
     lp = be.log_prob(dist, ind)
     if lp is not None:
         return lp
@@ -264,6 +263,14 @@ def batch_map(op, dists, *args, ragged: bool = True, **kwargs) -> list:
         be = _backend(d)
         key = ("ragged",) + rg.group_key(d) if ragged and rg.raggable(d) else (type(d), be.batch_key(d))
         groups.setdefault(key, []).append(i)
+    # a ragged group whose padded shape the kernels cannot take runs as exact-shape groups
+    for key in [k for k in groups if k[0] == "ragged"]:
+        idx = groups[key]
+        grp = [dists[i] for i in idx]
+        if rg.needs_padding(grp) and not rg.pad_fits(grp):
+            del groups[key]
+            for i in idx:
+                groups.setdefault((type(dists[i]), _backend(dists[i]).batch_key(dists[i])), []).append(i)
     out = [None] * len(dists)
     for key, idx in groups.items():
         group = [dists[i] for i in idx]

@@ -14,6 +14,8 @@ import torch
 from . import _lib
 
 ST_OK, ST_VACUOUS, ST_INVALID = 0, 1, 2
+# kernel size limits (include/sdb200.h); larger problems raise NativeError(SDB_ERR_UNSUPPORTED)
+PCFG_MAX_NT, PCFG_MAX_PT = 32, 32
 
 
 def _require_cuda(t: torch.Tensor, name: str):

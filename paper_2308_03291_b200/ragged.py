@@ -198,9 +198,27 @@ def group_key(d):
     return (type(d), RAGGED[type(d)][0](d))
 
 
+def needs_padding(ds) -> bool:
+    _, size, _, _, _ = RAGGED[type(ds[0])]
+    return len({size(d) for d in ds}) > 1
+
+
+def pad_fits(ds) -> bool:
+    """Can the padded group run on the kernels?  The PCFG padding adds one
+    nonterminal and one preterminal (kernels.PCFG_MAX_NT / _PT bound them)."""
+    if isinstance(ds[0], PCFG):
+        from .kernels import PCFG_MAX_NT, PCFG_MAX_PT
+
+        return ds[0].num_nt + 1 <= PCFG_MAX_NT and ds[0].num_pt + 1 <= PCFG_MAX_PT
+    return True
+
+
 def pad_group(ds):
-    """-> padded instances (all the same shape)."""
+    """-> padded instances (all the same shape); a group whose instances
+    already share their length is returned unchanged."""
     _, size, comb, pad, _ = RAGGED[type(ds[0])]
+    if not needs_padding(ds):
+        return list(ds)
     target = comb([size(d) for d in ds])
     return [pad(d, target) for d in ds]
 

@@ -143,3 +143,51 @@ def batch_pcfg(base, B, n, nt, pt):
 
 def batch_semi_markov(base, B, n, s, m):
     return np.stack([semi_markov(base + i, n, s, m) for i in range(B)])
+
+
+# -- derived-op cases (entropy / cross-entropy / KL / log_prob) --------------
+
+
+def family_inputs(fam, seed, shape):
+    """Inputs of one instance of `fam` as the dict of the class's fields."""
+    if fam == "chain":
+        init, tr = chain(seed, shape["n"], shape["m"])
+        return {"init": init, "transitions": tr}
+    if fam == "semi_markov":
+        return {"segment_potentials": semi_markov(seed, shape["n"], shape["s"], shape["m"])}
+    if fam == "alignment":
+        return {"move_potentials": alignment(seed, shape["n"], shape["m"])}
+    if fam == "ctc":
+        fp, tg = ctc(seed, shape["T"], shape["V"], shape["L"])
+        return {"frame_potentials": fp, "target": np.array(tg)}
+    if fam == "tree":
+        return {"span_potentials": tree(seed, shape["n"], shape["m"])}
+    if fam == "pcfg":
+        r, ru, e = pcfg(seed, shape["n"], shape["nt"], shape["pt"])
+        return {"root": r, "binary_rules": ru, "emissions": e}
+    if fam == "spanning":
+        return {"adjacency": spanning(seed, shape["n"], shape.get("directed", True))}
+    raise KeyError(fam)
+
+
+def make_dist(mod, fam, inp, flags=None):
+    """Construct the distribution of `fam` from an inputs dict with the
+    classes of `mod` (the reference `structdist` or the GPU package)."""
+    flags = flags or {}
+    if fam == "chain":
+        return mod.LinearChainCRF(inp["init"], inp["transitions"])
+    if fam == "semi_markov":
+        return mod.SemiMarkovCRF(inp["segment_potentials"])
+    if fam == "alignment":
+        return mod.MonotoneAlignmentCRF(inp["move_potentials"])
+    if fam == "ctc":
+        return mod.CTCDist(inp["frame_potentials"], tuple(int(x) for x in inp["target"]))
+    if fam == "tree":
+        return mod.TreeCRF(inp["span_potentials"])
+    if fam == "pcfg":
+        return mod.PCFG(inp["root"], inp["binary_rules"], inp["emissions"])
+    if fam == "spanning":
+        return mod.SpanningTreeCRF(inp["adjacency"], directed=flags.get("directed", True),
+                                   projective=flags.get("projective", False),
+                                   single_root_edge=flags.get("single", False))
+    raise KeyError(fam)

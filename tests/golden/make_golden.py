@@ -176,6 +176,20 @@ def spanning_cases(st):
     adj = np.full((4, 4), NEG_INF)
     run(sd.SpanningTreeCRF(adj), st, "spanning", dict(kind="vacuous", n=3, directed=True, projective=False, single=False),
         dict(adjacency=adj), argmax=False)
+    # exactly singular Laplacians with every column finite: a 2-cycle cut off from the root, and
+    # (single root only) two root branches with no arc between them (numerics.py:143-146)
+    cut = bld.spanning(41, 6)
+    cut[:5, 5:] = NEG_INF
+    cut[5:, :5] = NEG_INF
+    cut[5, 6] = 0.3
+    cut[6, 5] = -0.2
+    br = np.full((5, 5), NEG_INF)
+    br[0, 1] = 0.1; br[0, 2] = -0.4; br[1, 3] = 0.7; br[2, 4] = 0.2; br[3, 1] = 0.5
+    for kind, adj in (("cutoff", cut), ("branches", br)):
+        for single in (False, True):
+            d = sd.SpanningTreeCRF(adj, directed=True, projective=False, single_root_edge=single)
+            run(d, st, "spanning", dict(kind=kind, n=adj.shape[0] - 1, directed=True, projective=False, single=single),
+                dict(adjacency=adj), argmax=False)
     for projective in (False, True):
         for single in (False, True):
             n = 128 if not projective else 64
@@ -279,12 +293,169 @@ def sample2_cases(st):
         st.add("pcfg", dict(seed=seed, n=n, nt=nt, pt=pt, algo=algo), **out)
 
 
+
+# ----------------------------------------------------------- derived ops
+
+DERIVED_SHAPES = {
+    "chain": [dict(n=1, m=3), dict(n=5, m=3), dict(n=24, m=6)],
+    "semi_markov": [dict(n=4, s=2, m=2), dict(n=9, s=3, m=3)],
+    "alignment": [dict(n=3, m=2), dict(n=12, m=9)],
+    "ctc": [dict(T=6, V=4, L=3), dict(T=20, V=7, L=6)],
+    "tree": [dict(n=1, m=2), dict(n=5, m=3), dict(n=12, m=4)],
+    "pcfg": [dict(n=3, nt=2, pt=2), dict(n=6, nt=3, pt=3)],
+    "spanning": [dict(n=n, directed=dr, projective=pr, single=sg)
+                 for n in (3, 6) for dr in (True, False) for pr in (True, False) for sg in (True, False)],
+}
+
+
+def _bad_indicators(fam, d, good):
+    """Structurally invalid indicators derived from a valid one (each must
+    raise InvalidProblem in the reference's validate_indicator)."""
+    bad = []
+    z = {k: np.zeros_like(v) for k, v in good.items()}
+    bad.append(z)                                             # marks nothing
+    k0 = next(iter(good))
+    half = {k: v.copy() for k, v in good.items()}
+    half[k0] = half[k0] * 0.5
+    bad.append(half)                                          # not 0/1
+    if fam == "chain":
+        two = {k: v.copy() for k, v in good.items()}
+        two["init"][:] = 1.0                                  # two initial tags
+        bad.append(two)
+        if d.n > 2:
+            dis = {k: v.copy() for k, v in good.items()}
+            t = dis["transitions"][1]
+            a, b = np.argwhere(t > 0)[0]
+            t[a, b] = 0.0
+            t[(a + 1) % d.m, b] = 1.0                         # disconnected at step 1
+            bad.append(dis)
+    elif fam == "semi_markov":
+        gap = {k: v.copy() for k, v in good.items()}
+        hot = np.argwhere(gap["segment_potentials"] > 0)
+        gap["segment_potentials"][tuple(hot[-1])] = 0.0       # no longer covers n
+        bad.append(gap)
+    elif fam == "alignment":
+        off = {k: v.copy() for k, v in good.items()}
+        mv = off["move_potentials"]
+        cells = np.argwhere(mv.sum(axis=2) == 0)
+        i, j = cells[len(cells) // 2]
+        mv[i, j, 0 if (i > 0 and j > 0) else (1 if i > 0 else 2)] = 1.0  # a move off the path
+        bad.append(off)
+    elif fam == "ctc":
+        blank = {k: v.copy() for k, v in good.items()}
+        blank["frame_potentials"][:] = 0.0
+        blank["frame_potentials"][:, 0] = 1.0                 # all blanks: collapses to ()
+        bad.append(blank)
+    elif fam == "tree" and d.n > 1:
+        br = {k: v.copy() for k, v in good.items()}
+        sp = br["span_potentials"]
+        sp[0, d.n - 1] = 0.0                                  # root span missing
+        sp[1, d.n - 1, 0] = 1.0 if sp[1, d.n - 1].sum() == 0 else sp[1, d.n - 1, 0]
+        bad.append(br)
+        two = {k: v.copy() for k, v in good.items()}
+        two["span_potentials"][0, 0, :] = 1.0                 # a span with several labels
+        bad.append(two)
+    elif fam == "pcfg":
+        br = {k: v.copy() for k, v in good.items()}
+        br["sticky"][0, d.n - 1] = 0.0
+        bad.append(br)
+    elif fam == "spanning":
+        adj = good["adjacency"]
+        n = d.n
+        two = {"adjacency": adj.copy()}
+        dep = int(np.argwhere(adj > 0)[0][1])
+        h = [x for x in range(n + 1) if x != dep and adj[x, dep] == 0][0]
+        two["adjacency"][h, dep] = 1.0                        # two heads
+        bad.append(two)
+        if n >= 3:
+            cyc = {"adjacency": np.zeros_like(adj)}
+            cyc["adjacency"][0, 1] = 1.0
+            for c in range(2, n + 1):
+                cyc["adjacency"][c + 1 if c < n else 2, c] = 1.0  # 2 -> n -> n-1 ... cycle
+            bad.append(cyc)
+            star = {"adjacency": np.zeros_like(adj)}
+            star["adjacency"][0, 1:] = 1.0                    # every node on the root
+            bad.append(star)                                  # invalid only with single_root_edge
+            cross = {"adjacency": np.zeros_like(adj)}
+            cross["adjacency"][0, 1] = 1.0
+            cross["adjacency"][1, 3] = 1.0
+            cross["adjacency"][3, 2] = 1.0
+            for c in range(4, n + 1):
+                cross["adjacency"][3, c] = 1.0
+            cross["adjacency"][0, 2] = 0.0
+            bad.append(cross)                                 # 1->3 and 3->2 fine; crossing below
+            cr2 = {"adjacency": np.zeros_like(adj)}
+            cr2["adjacency"][0, 2] = 1.0
+            cr2["adjacency"][2, 1] = 1.0
+            cr2["adjacency"][1, 3] = 1.0                      # 1->3 crosses 0->2
+            for c in range(4, n + 1):
+                cr2["adjacency"][3, c] = 1.0
+            bad.append(cr2)
+    shp = {k: np.zeros(tuple(s + 1 for s in v.shape)) for k, v in good.items()}
+    bad.append(shp)                                           # wrong shape
+    return bad
+
+
+def derived_cases(st):
+    """entropy / cross_entropy / kl_divergence (dist.py:306-347) and log_prob
+    with validate_indicator (dist.py:224-276) from the unmodified reference."""
+    for fam, shapes in DERIVED_SHAPES.items():
+        for si, shape in enumerate(shapes):
+            seed = 700 + 10 * si + len(st.meta)
+            p_in = bld.family_inputs(fam, seed, shape)
+            q_in = bld.family_inputs(fam, seed + 1, shape)
+            if fam == "ctc":
+                q_in["target"] = p_in["target"]
+            if fam == "spanning" and not shape["directed"]:
+                pass
+            p = bld.make_dist(sd, fam, p_in, shape)
+            q = bld.make_dist(sd, fam, q_in, shape)
+            out = {f"in_{k}": v for k, v in p_in.items()}
+            out.update({f"q_{k}": v for k, v in q_in.items()})
+            h_p, algo = sd.dist.entropy_info(p)
+            out["entropy_p"] = np.array(h_p)
+            out["cross_pq"] = np.array(sd.cross_entropy(p, q))
+            out["kl_pq"] = np.array(sd.kl_divergence(p, q))
+            good, _, _ = sd.argmax_info(p)
+            out["logprob_argmax"] = np.array(sd.log_prob(p, good))
+            smp = sd.sample(p, seed)
+            for k, v in smp.items():
+                out[f"sample_{k}"] = v
+            out["logprob_sample"] = np.array(sd.log_prob(p, smp))
+            bads = _bad_indicators(fam, p, good)
+            raises = []
+            for b, ind in enumerate(bads):
+                for k, v in ind.items():
+                    out[f"bad{b}_{k}"] = v
+                try:
+                    raises.append(float(sd.log_prob(p, ind)))
+                except sd.InvalidProblem:
+                    raises.append(np.nan)  # NaN marks "raised InvalidProblem"
+            out["bad_logprob"] = np.array(raises)
+            st.add(fam, dict(shape, seed=seed, algo=algo, nbad=len(bads)), **out)
+    # support mismatch -> +inf cross-entropy; point mass -> entropy 0 (test_dist_ops.py:144-194)
+    init, tr = bld.chain(900, 4, 3)
+    tq = tr.copy()
+    tq[1, :, 2] = NEG_INF
+    p, q = sd.LinearChainCRF(init, tr), sd.LinearChainCRF(init, tq)
+    st.add("chain", dict(kind="support", n=4, m=3, nbad=0), in_init=init, in_transitions=tr, q_init=init,
+           q_transitions=tq, entropy_p=np.array(sd.entropy(p)), cross_pq=np.array(sd.cross_entropy(p, q)),
+           kl_pq=np.array(sd.kl_divergence(p, q)))
+    tpm = np.full((3, 3, 3), NEG_INF)
+    for t in range(3):
+        tpm[t, t % 3, (t + 1) % 3] = 0.5
+    ipm = np.array([0.0, NEG_INF, NEG_INF])
+    p = sd.LinearChainCRF(ipm, tpm)
+    st.add("chain", dict(kind="point_mass", n=4, m=3, nbad=0), in_init=ipm, in_transitions=tpm, q_init=ipm,
+           q_transitions=tpm, entropy_p=np.array(sd.entropy(p)), cross_pq=np.array(sd.cross_entropy(p, p)),
+           kl_pq=np.array(sd.kl_divergence(p, p)))
+
 def main():
     fams = {
         "chain": chain_cases, "semi_markov": semi_markov_cases, "alignment": alignment_cases,
         "ctc": ctc_cases, "tree": tree_cases, "pcfg": pcfg_cases, "spanning": spanning_cases,
         "sample": sample_cases, "wilson": wilson_cases, "sample2": sample2_cases,
-        "colbourn": colbourn_cases,
+        "colbourn": colbourn_cases, "derived": derived_cases,
     }
     only = sys.argv[1:] or list(fams)
     for fam in only:

@@ -1,0 +1,76 @@
+"""GPU parity: entropy / cross_entropy / kl_divergence (dist.py:306-347)
+and log_prob (dist.py:263-276) for all seven families against goldens from
+the unmodified reference (tests/golden/golden_derived.npz).
+
+Tolerance: the derived values are differences of fp32-path quantities
+(log Z - sum_e p(e) theta(e)); the bar is rtol 1e-4 of the magnitudes that
+are subtracted (|log Z_q| + sum_e |p(e) theta_q(e)|), plus the 1e-6 floor."""
+
+import numpy as np
+import pytest
+
+import paper_2308_03291_b200 as sd
+from golden import builders as bld
+from golden_io import load
+from gpu_util import ATOL, RTOL, need_gpu
+
+pytestmark = pytest.mark.gpu
+
+CASES = load("derived")
+
+
+def _dists(case):
+    fam = case.meta["family"]
+    p = bld.make_dist(sd, fam, {k[3:]: case[k] for k in case if k.startswith("in_")}, case.meta)
+    q = bld.make_dist(sd, fam, {k[2:]: case[k] for k in case if k.startswith("q_")}, case.meta)
+    return p, q
+
+
+def _scale(p, q):
+    mp = sd.potential_marginals(p)
+    qp = q.potentials()
+    tot = abs(sd.log_partition(q))
+    for k, m in mp.items():
+        t = np.where(m > 0, qp[k], 0.0)
+        tot += float(np.sum(np.abs(m * np.where(np.isfinite(t), t, 0.0))))
+    return tot
+
+
+def _close(got, want, scale):
+    if np.isinf(want):
+        assert got == want, (got, want)
+        return
+    assert abs(got - want) <= RTOL * max(1.0, scale) + ATOL, (got, want, scale)
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c.meta['family']}-{c.meta['idx']}")
+def test_entropy_ce_kl(case):
+    need_gpu()
+    p, q = _dists(case)
+    h, algo = sd.entropy_info(p)
+    if "algo" in case.meta:
+        assert algo == case.meta["algo"]
+    sp, sq = _scale(p, p), _scale(p, q)
+    _close(h, float(case.entropy_p), sp)
+    _close(sd.cross_entropy(p, q), float(case.cross_pq), sq)
+    _close(sd.kl_divergence(p, q), float(case.kl_pq), sp + sq)
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c.meta.get("nbad")],
+                         ids=lambda c: f"{c.meta['family']}-{c.meta['idx']}")
+def test_log_prob(case):
+    need_gpu()
+    p, _ = _dists(case)
+    lz = abs(sd.log_partition(p))
+    good = sd.argmax(p)
+    _close(sd.log_prob(p, good), float(case.logprob_argmax), lz)
+    smp = {k[7:]: case[k] for k in case if k.startswith("sample_")}
+    _close(sd.log_prob(p, smp), float(case.logprob_sample), lz)
+    for b in range(case.meta["nbad"]):
+        ind = {k[len(f"bad{b}_"):]: case[k] for k in case if k.startswith(f"bad{b}_")}
+        want = float(case.bad_logprob[b])
+        if np.isnan(want):
+            with pytest.raises(sd.InvalidProblem):
+                sd.log_prob(p, ind)
+        else:
+            _close(sd.log_prob(p, ind), want, lz)

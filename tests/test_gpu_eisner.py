@@ -30,7 +30,7 @@ def test_spanning_golden_api(case):
         return
     marg, algo2 = sd.marginals_info(d)
     assert algo2 == algo
-    case.check_marg("adjacency", marg["adjacency"], RTOL, 1e-5 if m["single"] else 2e-6)
+    case.check_marg("adjacency", marg["adjacency"], RTOL, ATOL)
     if "argmax_adjacency" in case:  # Kuhlmann (projective) / Chu-Liu-Edmonds (non-projective)
         ind, score, aalgo = sd.argmax_info(d)
         np.testing.assert_array_equal(ind["adjacency"], case["argmax_adjacency"])
@@ -50,8 +50,7 @@ def test_eisner_batched_vs_oracle(B, n, single):
         z, mg = O.eisner_marginals(adj[b], single)
         assert abs(logz[b].item() - z) <= RTOL * max(1, abs(z))
         np.testing.assert_allclose(marg[b].cpu().numpy(), mg, rtol=RTOL, atol=ATOL)
-        if n <= 64 or b == 0:
-            np.testing.assert_array_equal(heads[b].cpu().numpy(), O.kuhlmann_heads(adj[b], single))
+        np.testing.assert_array_equal(heads[b].cpu().numpy(), O.kuhlmann_heads(adj[b], single))
 
 
 def test_eisner_config_invariants():
@@ -113,7 +112,7 @@ def test_eisner_exp_space_fallback(single):
     for b in range(4):
         z, mg = O.eisner_marginals(adj[b], single)
         assert abs(logz[b].item() - z) <= RTOL * abs(z) + 1e-6
-        np.testing.assert_allclose(marg[b].cpu().numpy(), mg, rtol=RTOL, atol=2e-6)
+        np.testing.assert_allclose(marg[b].cpu().numpy(), mg, rtol=RTOL, atol=ATOL)
 
 
 def test_eisner_kuhlmann_concurrent():

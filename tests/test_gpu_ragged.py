@@ -79,3 +79,18 @@ def test_ragged_pcfg():
         ind0, score0, algo0 = sd.argmax_info(d)
         np.testing.assert_array_equal(ind["sticky"], ind0["sticky"])
         assert abs(score - score0) <= 1e-4 * abs(score0) and algo == algo0
+
+
+def test_batch_map_pcfg_full_grammar():
+    """NT = PT = 32 (the C5b grammar): same-length groups run unpadded and
+    ragged groups whose padded grammar would not fit the kernel run as
+    exact-shape groups -- no NativeError."""
+    need_gpu()
+    same = [sd.PCFG(*pcfg(40 + s, 10, 32, 32)) for s in range(3)]
+    got = sd.batch_map(sd.log_partition, same)
+    for d, z in zip(same, got):
+        assert abs(z - sd.log_partition(d)) <= 1e-5 * abs(z)
+    mixed = [sd.PCFG(*pcfg(50 + s, n, 32, 32)) for s, n in enumerate([6, 9, 6])]
+    got = sd.batch_map(sd.marginals, mixed)
+    for d, m in zip(mixed, got):
+        np.testing.assert_allclose(m["sticky"], sd.marginals(d)["sticky"], rtol=1e-5, atol=1e-7)

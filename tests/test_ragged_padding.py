@@ -123,3 +123,13 @@ def test_groups():
     assert not rg.raggable(SpanningTreeCRF(spanning(1, 3, True), single_root_edge=True))
     pa, pb = rg.pad_group([a, b])
     assert pa.n == pb.n == 8
+
+
+def test_pad_group_same_length_is_identity():
+    """A group whose instances share their length is not padded (the PCFG
+    pad would otherwise add a nonterminal and a preterminal)."""
+    ds = [PCFG(*pcfg(s, 5, 3, 2)) for s in range(3)]
+    assert all(a is b for a, b in zip(rg.pad_group(ds), ds))
+    assert not rg.needs_padding(ds)
+    full = [PCFG(*pcfg(s, n, 32, 32)) for s, n in enumerate([4, 6])]
+    assert rg.needs_padding(full) and not rg.pad_fits(full)
