@@ -10,6 +10,7 @@ The public surface mirrors `structdist/__init__.py:11-80`.
 """
 
 from . import kernels  # noqa: F401  (batched device entry points)
+from . import sharding  # noqa: F401  (multi-GPU batch sharding)
 from .dist import (
     argmax,
     argmax_info,
@@ -39,6 +40,7 @@ from .errors import (
     UnsupportedInference,
     VacuousDistribution,
 )
+from .sharding import run_sharded, sharded_batch_map  # noqa: F401
 from .families import (
     FAMILIES,
     PCFG,

@@ -7,6 +7,7 @@ import os
 import sys
 
 import numpy as np
+import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -64,3 +65,60 @@ def test_gloo_world2_gather_and_max():
     ref = np.array([O.chain_log_partition(*batch_chain(100 + i, 1, 6, 3))[0] for i in range(B)])
     np.testing.assert_allclose(full, ref, rtol=1e-12)
     assert t == 2.0
+
+
+def _gpu_worker(rank, world, port, q):
+    """Both ranks on cuda:0 (independent kernels, nothing waits across ranks):
+    the product sharding entry runs the real sm_100a kernels on each shard and
+    all-gathers log Z / status over gloo."""
+    sys.path.insert(0, HERE)
+    sys.path.insert(0, os.path.dirname(HERE))
+    import paper_2308_03291_b200 as sd
+    from golden.builders import alignment, batch_alignment
+    from paper_2308_03291_b200 import kernels as K
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    B = 7
+    th = torch.from_numpy(batch_alignment(600, B, 20, 9)).float().pin_memory()
+    res = sd.run_sharded(K.nw_fb, [th])
+    torch.cuda.synchronize()
+    dists = [sd.MonotoneAlignmentCRF(alignment(700 + i, 6 + i, 5)) for i in range(5)]
+    lz = sd.sharded_batch_map(sd.log_partition, dists)
+    mg = sd.sharded_batch_map(sd.marginals, dists, gather=False)
+    if rank == 0:
+        q.put((res.logz.cpu().numpy(), res.status.cpu().numpy(), (res.start, res.stop),
+               res.local[1].cpu().numpy(), lz, [m is not None for m in mg]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gloo_world2_real_kernels():
+    import paper_2308_03291_b200 as sd
+    from golden.builders import alignment, batch_alignment
+    from paper_2308_03291_b200 import kernels as K
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = 31000 + (os.getpid() % 1000)
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    logz, status, (a, b), marg0, lz, owned = q.get()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    th = torch.from_numpy(batch_alignment(600, 7, 20, 9)).float().cuda()
+    z1, m1, st1 = K.nw_fb(th)
+    np.testing.assert_array_equal(logz, z1.cpu().numpy())  # same kernels, same shards -> identical
+    np.testing.assert_array_equal(status, st1.cpu().numpy())
+    assert (a, b) == (0, 4)
+    np.testing.assert_array_equal(marg0, m1[a:b].cpu().numpy())
+    dists = [sd.MonotoneAlignmentCRF(alignment(700 + i, 6 + i, 5)) for i in range(5)]
+    assert lz == [sd.log_partition(d) for d in dists]
+    assert owned == [True, True, True, False, False]
