@@ -23,6 +23,8 @@
 // float64 reference on the same fp32 inputs.
 #include "common.cuh"
 
+#include <cooperative_groups.h>
+
 namespace {
 
 constexpr int kThreads = 256;
@@ -250,22 +252,20 @@ __device__ __forceinline__ void stage_step(float* dst, const float* src, int mm,
   }
 }
 
-__global__ void __launch_bounds__(kThreads) chain_fwd_bwd_small_kernel(
-    const float* __restrict__ init, const float* __restrict__ trans, int n, int m, ChainWs ws,
-    double* __restrict__ logz, int32_t* __restrict__ status, int only_need) {
-  if (only_need && ws.need[blockIdx.x] == 0) return;
-  extern __shared__ __align__(16) float sm[];
+// one log-space pass (forward or backward) of instance b by the whole CTA; the marginals are
+// formed from the stored normalised vectors by marg_steps().  `sm` >= kD*m*m + (32 + 2*kGroups*32) floats.
+__device__ void small_pass(const float* __restrict__ init, const float* __restrict__ trans, int n, int m,
+                           const ChainWs& ws, double* __restrict__ logz, int32_t* __restrict__ status, int b,
+                           bool fwd, float* sm) {
   const int mm = m * m;
   float* stage = sm;                     // [kD][mm]
   float* vec = stage + kD * mm;          // [32]
   float* pm = vec + 32;                  // [kGroups][32]
   float* ps = pm + kGroups * 32;         // [kGroups][32]
   __shared__ int redi[kThreads / 32];
-  const int b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float* th = trans + (size_t)b * (n - 1) * mm;
   const bool v16 = ((mm & 3) == 0);
-  const bool fwd = blockIdx.y == 0;
   int bad = 0;
   // prologue prefetch: steps in processing order
   for (int d = 0; d < kD; ++d) {
@@ -385,6 +385,14 @@ __global__ void __launch_bounds__(kThreads) chain_fwd_bwd_small_kernel(
     }
   }
   asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
+__global__ void __launch_bounds__(kThreads) chain_fwd_bwd_small_kernel(
+    const float* __restrict__ init, const float* __restrict__ trans, int n, int m, ChainWs ws,
+    double* __restrict__ logz, int32_t* __restrict__ status, int only_need) {
+  if (only_need && ws.need[blockIdx.x] == 0) return;
+  extern __shared__ __align__(16) float sm_small[];
+  small_pass(init, trans, n, m, ws, logz, status, blockIdx.x, blockIdx.y == 0, sm_small);
 }
 
 // ---------------------------------------------------------------------
@@ -611,25 +619,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 // writes p_init.
 constexpr int kStepsPerBlock = 8;
 
-__global__ void __launch_bounds__(kThreads) chain_marg_kernel(
-    const float* __restrict__ init, const float* __restrict__ trans, int n, int m, ChainWs ws,
-    const double* __restrict__ logz, float* __restrict__ marg_init, float* __restrict__ marg_trans, int only_need) {
-  const int b = blockIdx.y;
-  if (only_need && ws.need[b] == 0) return;
-  const int t0 = blockIdx.x * kStepsPerBlock;
+// marginals of steps [t0, t1) of instance b from the log-space passes' vectors (+ p_init if asked)
+__device__ void marg_steps(const float* __restrict__ init, const float* __restrict__ trans, int n, int m,
+                           const ChainWs& ws, const double* __restrict__ logz, float* __restrict__ marg_init,
+                           float* __restrict__ marg_trans, int b, int t0, int t1, bool with_init) {
   const size_t mm = (size_t)m * m;
   const bool ok = ws.flags[b] == SDB_ST_OK;
   const double z = logz[b];
   // exponent arguments summed in fp64: this kernel serves the log-space path, i.e. the instances
   // whose potentials are too large for the linear one (|theta| ~ 10^2: fp32 sums would cost 1e-4)
-  if (blockIdx.x == 0 && marg_init) {
+  if (with_init && marg_init) {
     const float* be = ws.beta + (size_t)b * n * m;
     const double K = ok ? ws.bcum[(size_t)b * n] - z : 0.0;
     for (int j = threadIdx.x; j < m; j += kThreads)
       marg_init[(size_t)b * m + j] = ok ? fexp((float)((double)init[(size_t)b * m + j] + (double)be[j] + K)) : 0.f;
   }
   if (!marg_trans) return;
-  const int t1 = min(t0 + kStepsPerBlock, n - 1);
   for (int t = t0; t < t1; ++t) {
     const float* tt = trans + ((size_t)b * (n - 1) + t) * mm;
     float* out = marg_trans + ((size_t)b * (n - 1) + t) * mm;
@@ -645,6 +650,16 @@ __global__ void __launch_bounds__(kThreads) chain_marg_kernel(
       out[e] = fexp((float)(((double)al[a] + K) + ((double)tt[e] + (double)be[j])));
     }
   }
+}
+
+__global__ void __launch_bounds__(kThreads) chain_marg_kernel(
+    const float* __restrict__ init, const float* __restrict__ trans, int n, int m, ChainWs ws,
+    const double* __restrict__ logz, float* __restrict__ marg_init, float* __restrict__ marg_trans, int only_need) {
+  const int b = blockIdx.y;
+  if (only_need && ws.need[b] == 0) return;
+  const int t0 = blockIdx.x * kStepsPerBlock;
+  marg_steps(init, trans, n, m, ws, logz, marg_init, marg_trans, b, t0, min(t0 + kStepsPerBlock, n - 1),
+             blockIdx.x == 0);
 }
 
 // Marginals from the LINEAR passes (chain_lin_kernel): e_t, f_t normalised
@@ -939,6 +954,599 @@ __global__ void __launch_bounds__(kThreads) chain_viterbi_small_kernel(
   }
 }
 
+// ---------------------------------------------------------------------
+// Time-parallel chain scan (m <= 32): log_partition + marginals in ONE
+// cluster launch (chain.py:64-95).
+//
+// The T = n-1 transition steps are cut into kSC chunks; the kSC CTAs of a
+// thread-block cluster own one chunk each of one instance.  Linear space with
+// exact power-of-two normalisers (log scales are integers x ln2 plus the
+// per-step shifts, summed in fp64):
+//   A  stage the chunk's potentials with bulk TMA copies (cp.async.bulk, one
+//      per step, mbarrier completion), E_t = exp(theta_t - max theta_t)
+//      (swizzled 16-byte granules: row and column reads are conflict-free),
+//      and the chunk's transfer product P_c = E_t0 E_t0+1 ... (a 32x32x32
+//      FFMA product per step; each thread owns 4 rows x 1 column);
+//   B  after a cluster barrier every CTA copies the other chunks' P~ through
+//      distributed shared memory and folds them into its boundary vectors:
+//      alpha at its chunk start (warp 0) and beta at its chunk end (warp 1);
+//   C  recompute alpha / beta inside the chunk (warp 0 forward, warp 1
+//      backward -- the reverse scan, no autodiff), then emit
+//      p_t[a][b] = alpha~_t[a] E_t[a][b] beta~_t+1[b] e^K_t as float4 rows.
+// Numerical guard: a chunk whose potentials span more than 80 nats within a
+// step (exp would underflow), a zero normaliser, an out-of-range marginal
+// scale or a NaN/+inf input sends the WHOLE instance to the exact log-space
+// path, run inline by the cluster's rank-0 CTA (small_pass + marg_steps).
+#ifdef SDB_SCAN_PROF
+__device__ unsigned long long g_scan_t[1024][10];
+#define SCAN_TS(i)                                                                     \
+  do {                                                                                 \
+    if (threadIdx.x == 0 && blockIdx.x < 1024) {                                       \
+      g_scan_t[blockIdx.x][i] = clock64();                                             \
+    }                                                                                  \
+  } while (0)
+#else
+#define SCAN_TS(i) \
+  do {             \
+  } while (0)
+#endif
+constexpr int kSC = 8;                    // chunks per instance = cluster size
+constexpr int kW = kThreads / 32;
+constexpr int kSLmax = 24;                // steps per chunk (shared-memory bound)
+constexpr int kXP = 36;                   // pitch of the transposed product (conflict-free float4 stores)
+constexpr float kRange = 80.f;            // max nats inside one step before linear space gives up
+
+__device__ __forceinline__ int swz(int a, int b) { return (a << 5) + ((((b >> 2) ^ (a & 7))) << 2) + (b & 3); }
+// column b's offset inside a swizzled row whose index is congruent to q mod 8
+__device__ __forceinline__ int swc(int q, int b) { return (((b >> 2) ^ q) << 2) + (b & 3); }
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_wait(const uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+struct ScanSmem {
+  float* E;        // [L][1024] raw theta, then E (swizzled)
+  float* XT;       // [2][32][kXP] product, transposed (XT[k][r] = Y[r][k])
+  float* P;        // [1024] own normalised chunk product (swizzled; read by the other ranks)
+  float* al;       // [L+1][32] alpha~ within the chunk
+  float* be;       // [L+1][32] beta~ within the chunk
+  float* vec;      // [2][32] boundary-scan vectors (alpha, beta)
+  float* gh;       // [L] emission factor e^(K_t / 2)
+  double* la;      // [L+1] log scales of al
+  double* lb;      // [L+1] log scales of be
+  double* lpc;     // [kSC] log scale of each chunk's product
+  float* mx;       // [L] step max
+  int* pe;         // [2][kW] power-of-two exponents of the warp maxima (double-buffered)
+  uint64_t* mbar;  // [L] TMA completion
+  uint64_t* rdy;   // [L] converted tile ready (32 arrivals)
+  int* flagA;      // [kSC] phase-A verdicts pushed by every rank
+  int* flagC;      // [kSC] phase-C verdicts
+  double* misc;    // [4] logZ, ...
+};
+
+size_t scan_smem(int L) {
+  return (size_t)L * 4096 + 2 * 32 * kXP * 4 + 4096 + 2 * (L + 1) * 32 * 4 + 2 * 32 * 4 + L * 4 +
+         2 * (L + 1) * 8 + kSC * 8 + L * 4 + 2 * 8 * 4 + 2 * L * 8 + 2 * kSC * 4 + 4 * 8 + 32 * 16;
+}
+
+__device__ __forceinline__ ScanSmem scan_carve(char* p, int L) {
+  ScanSmem S;
+  auto take = [&](size_t bytes) {
+    char* r = p;
+    p += (bytes + 15) & ~(size_t)15;
+    return r;
+  };
+  S.E = (float*)take((size_t)L * 4096);
+  S.XT = (float*)take(2 * 32 * kXP * 4);
+  S.P = (float*)take(4096);
+  S.al = (float*)take((size_t)(L + 1) * 32 * 4);
+  S.be = (float*)take((size_t)(L + 1) * 32 * 4);
+  S.vec = (float*)take(2 * 32 * 4);
+  S.gh = (float*)take((size_t)L * 4);
+  S.la = (double*)take((size_t)(L + 1) * 8);
+  S.lb = (double*)take((size_t)(L + 1) * 8);
+  S.lpc = (double*)take(kSC * 8);
+  S.mx = (float*)take((size_t)L * 4);
+  S.pe = (int*)take(2 * 8 * 4);
+  S.mbar = (uint64_t*)take((size_t)L * 8);
+  S.rdy = (uint64_t*)take((size_t)L * 8);
+  S.flagA = (int*)take(kSC * 4);
+  S.flagC = (int*)take(kSC * 4);
+  S.misc = (double*)take(4 * 8);
+  return S;
+}
+
+// exponent e with 2^e <= x < 2^(e+1) for a positive normal float (0 for x == 0 / denormal)
+__device__ __forceinline__ int fexpo(float x) { return (int)((__float_as_uint(x) >> 23) & 0xff) - 127; }
+
+template <bool kFull>  // kFull: m == 32 (bulk TMA staging); else padded element loads
+__global__ void __launch_bounds__(kThreads, 2) chain_scan_kernel(
+    const float* __restrict__ init, const float* __restrict__ trans, int n, int m, ChainWs ws,
+    double* __restrict__ logz, float* __restrict__ marg_init, float* __restrict__ marg_trans,
+    int32_t* __restrict__ status) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) char smscan[];
+  const int T = n - 1, L = (T + kSC - 1) / kSC;
+  ScanSmem S = scan_carve(smscan, L);
+  const int c = (int)cluster.block_rank();
+  const int b = blockIdx.x / kSC;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int t0 = min(T, c * L), t1 = min(T, t0 + L), Lc = t1 - t0;
+  const float* th = trans + ((size_t)b * T + t0) * (size_t)(m * m);
+  const float LN2 = 0.6931471805599453f;
+
+  SCAN_TS(0);
+  // ---- A0: stage the chunk (bulk TMA per step, or padded loads) ----------------------------
+  if (tid == 0) {
+    for (int k = 0; k < Lc; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;" ::"r"(smem_u32(S.rdy + k)));
+    if (!kFull) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (kFull) {
+    if (tid == 0) {
+      for (int k = 0; k < Lc; ++k)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(S.mbar + k)));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      for (int k = 0; k < Lc; ++k) {
+        const uint32_t bar = smem_u32(S.mbar + k);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 4096;" ::"r"(bar) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 4096, [%2];"
+                     ::"r"(smem_u32(S.E + k * 1024)), "l"(th + (size_t)k * 1024), "r"(bar) : "memory");
+      }
+    }
+  } else {
+    for (int e = tid; e < Lc * 1024; e += kThreads) {
+      const int k = e >> 10, a = (e >> 5) & 31, bb = e & 31;
+      S.E[e] = (a < m && bb < m) ? __ldg(th + (size_t)k * m * m + a * m + bb) : ninf();
+    }
+  }
+  if (tid < kSC) { S.flagA[tid] = 0; S.flagC[tid] = 0; }
+  __syncthreads();
+
+  // ---- A: warps 4-7 convert tiles (E_t = exp(theta_t - mx_t), one row per lane, swizzled in
+  // place) in step order and release each through an mbarrier; warps 0-3 multiply as tiles
+  // become ready (Y_k = Y~_(k-1) E_k, a 4 x 2 output block per lane, normalised by powers of two)
+  int flag = 0;
+  int esum = 0;  // product warps: sum of normaliser exponents
+  int cur = 0;
+  if (warp >= 4) {
+    if (warp == kW - 1) {  // alpha_0 = exp(init - max init) (every rank needs it for its boundary vector)
+      const float x = lane < m ? init[(size_t)b * m + lane] : ninf();
+      const float mi = warp_max(x);
+      float lo = x == ninf() ? __int_as_float(0x7f800000) : x;
+      lo = -warp_max(-lo);
+      if (__any_sync(0xffffffffu, bad_input(x)) || mi == ninf() || mi - lo > kRange) flag = 1;
+      S.vec[lane] = lane < m ? fexp(x - (mi == ninf() ? 0.f : mi)) : 0.f;
+      if (lane == 0) S.misc[1] = (double)mi;  // log scale of alpha~_0
+    }
+    for (int k = warp - 4; k < Lc; k += 4) {
+      if (kFull) mbar_wait(S.mbar + k, 0);
+      float* tile = S.E + k * 1024;
+      float4 v[8];
+#pragma unroll
+      for (int g = 0; g < 8; ++g) v[g] = *reinterpret_cast<const float4*>(tile + lane * 32 + 4 * ((g + lane) & 7));
+      float hi = ninf(), lo = __int_as_float(0x7f800000);
+      int bad = 0;
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        const float q[4] = {v[g].x, v[g].y, v[g].z, v[g].w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          bad |= bad_input(q[u]);
+          hi = fmaxf(hi, q[u]);
+          if (q[u] != ninf()) lo = fminf(lo, q[u]);
+        }
+      }
+      const float mxk = warp_max(hi);
+      const float mnk = -warp_max(-lo);
+      if (__any_sync(0xffffffffu, bad) || mxk == ninf() || mxk - mnk > kRange) flag = 1;
+      const float sh = mxk == ninf() ? 0.f : mxk;
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        const int gl = (g + lane) & 7;  // logical granule held in v[g]
+        float4 e;
+        e.x = fexp(v[g].x - sh);
+        e.y = fexp(v[g].y - sh);
+        e.z = fexp(v[g].z - sh);
+        e.w = fexp(v[g].w - sh);
+        *reinterpret_cast<float4*>(tile + lane * 32 + 4 * (gl ^ (lane & 7))) = e;
+      }
+      if (lane == 0) S.mx[k] = mxk;
+      asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(S.rdy + k)) : "memory");
+    }
+  } else {
+    const int pt = tid;  // 0..127
+    // Y_0 = E_t0 (max 1): transposed copy
+    if (Lc > 0) mbar_wait(S.rdy, 0);
+    for (int e = pt; e < 1024; e += 128) {
+      const int r = e >> 5, j = e & 31;
+      S.XT[j * kXP + r] = Lc > 0 ? S.E[swz(r, j)] : (r == j ? 1.f : 0.f);
+    }
+    if (pt < 4) S.pe[pt] = 0;
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    SCAN_TS(1);
+    const int rb = (warp >> 1) * 16 + 4 * (lane >> 3);  // first of this lane's 4 rows
+    const int cb = (warp & 1) * 16 + 2 * (lane & 7);    // first of its 2 columns
+    int co[8];                                          // column offset inside a swizzled row, per row & 7
+#pragma unroll
+    for (int q = 0; q < 8; ++q) co[q] = swc(q, cb);
+    for (int k = 1; k < Lc; ++k) {
+      const float* X = S.XT + cur * 32 * kXP;
+      const float* Ek = S.E + k * 1024;
+      int emax = max(max(S.pe[cur * 4], S.pe[cur * 4 + 1]), max(S.pe[cur * 4 + 2], S.pe[cur * 4 + 3]));
+      mbar_wait(S.rdy + k, 0);
+      float acc[4][2] = {};
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float4 x = *reinterpret_cast<const float4*>(X + j * kXP + rb);
+        const float2 e = *reinterpret_cast<const float2*>(Ek + j * 32 + co[j & 7]);
+        acc[0][0] = fmaf(x.x, e.x, acc[0][0]);
+        acc[0][1] = fmaf(x.x, e.y, acc[0][1]);
+        acc[1][0] = fmaf(x.y, e.x, acc[1][0]);
+        acc[1][1] = fmaf(x.y, e.y, acc[1][1]);
+        acc[2][0] = fmaf(x.z, e.x, acc[2][0]);
+        acc[2][1] = fmaf(x.z, e.y, acc[2][1]);
+        acc[3][0] = fmaf(x.w, e.x, acc[3][0]);
+        acc[3][1] = fmaf(x.w, e.y, acc[3][1]);
+      }
+      const float sc = __int_as_float((127 - emax) << 23);  // 2^-emax (exact)
+      esum += emax;
+      float mxl = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[i][0] *= sc;
+        acc[i][1] *= sc;
+        mxl = fmaxf(mxl, fmaxf(acc[i][0], acc[i][1]));
+      }
+      const float wm = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(mxl)));
+      const int nx = cur ^ 1;
+      float* Xn = S.XT + nx * 32 * kXP;
+      *reinterpret_cast<float4*>(Xn + cb * kXP + rb) = make_float4(acc[0][0], acc[1][0], acc[2][0], acc[3][0]);
+      *reinterpret_cast<float4*>(Xn + (cb + 1) * kXP + rb) = make_float4(acc[0][1], acc[1][1], acc[2][1], acc[3][1]);
+      if (lane == 0) S.pe[nx * 4 + warp] = wm > 0.f ? fexpo(wm) : -1000;
+      cur = nx;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+    }
+    int emax = max(max(S.pe[cur * 4], S.pe[cur * 4 + 1]), max(S.pe[cur * 4 + 2], S.pe[cur * 4 + 3]));
+    if (emax < -120) flag = 1;  // the product underflowed
+    emax = max(emax, -120);
+    const float sc = __int_as_float((127 - emax) << 23);
+    esum += emax;
+    const float* X = S.XT + cur * 32 * kXP;
+    for (int e = pt; e < 1024; e += 128) {
+      const int r = e >> 5, j = e & 31;
+      S.P[swz(r, j)] = X[j * kXP + r] * sc;
+    }
+  }
+  __syncthreads();
+  SCAN_TS(2);
+  int sw[8];  // this lane's column inside a swizzled row, per row residue (row & 7)
+#pragma unroll
+  for (int q = 0; q < 8; ++q) sw[q] = swc(q, lane);
+  if (tid == 0) {
+    double lp = (double)esum * (double)LN2;
+    for (int k = 0; k < Lc; ++k) lp += (double)S.mx[k];
+    S.lpc[c] = lp;
+  }
+  const int anyA = __syncthreads_or(flag);
+  if (tid < kSC) *cluster.map_shared_rank(S.flagA + c, tid) = anyA;  // push the verdict to every rank
+  cluster.sync();  // #1: every chunk product, scale and verdict visible cluster-wide
+  SCAN_TS(3);
+
+  int fail = 0;
+#pragma unroll
+  for (int r = 0; r < kSC; ++r) fail |= S.flagA[r];
+  if (fail) goto fallback;
+  {
+    // ---- B: fold the other chunks' products (read in place through DSMEM) into the boundary
+    // vectors
+    if (tid < kSC && tid != c) S.lpc[tid] = *cluster.map_shared_rank(S.lpc + tid, tid);
+    __syncthreads();
+    if (warp == 0) {
+      // alpha at the chunk start: alpha~_0 P~_0 ... P~_(c-1)  (lane = column b)
+      float* v = S.vec;
+      double A = S.misc[1];
+      for (int j = 0; j < c; ++j) {
+        const float* Pj = cluster.map_shared_rank(S.P, j);
+        float pr[32];
+#pragma unroll
+        for (int a = 0; a < 32; ++a) pr[a] = Pj[a * 32 + sw[a & 7]];
+        float acc4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int a = 0; a < 32; a += 4) {
+          const float4 vv = *reinterpret_cast<const float4*>(v + a);
+          acc4[0] = fmaf(vv.x, pr[a], acc4[0]);
+          acc4[1] = fmaf(vv.y, pr[a + 1], acc4[1]);
+          acc4[2] = fmaf(vv.z, pr[a + 2], acc4[2]);
+          acc4[3] = fmaf(vv.w, pr[a + 3], acc4[3]);
+        }
+        const float acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+        const float wm = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(acc)));
+        const int ex = wm > 0.f ? fexpo(wm) : -1000;
+        if (ex < -120) flag = 1;
+        __syncwarp();
+        v[lane] = acc * __int_as_float((127 - max(ex, -120)) << 23);
+        __syncwarp();
+        A += (double)max(ex, -120) * (double)LN2 + S.lpc[j];
+      }
+      S.al[lane] = v[lane];
+      if (lane == 0) S.la[0] = A;
+    } else if (warp == 1) {
+      // beta at the chunk end: P~_(c+1) ... P~_(C-1) 1  (lane = row a)
+      float* w = S.vec + 32;
+      w[lane] = lane < m ? 1.f : 0.f;
+      __syncwarp();
+      double Bv = 0.0;
+      for (int j = kSC - 1; j > c; --j) {
+        const float* Pj = cluster.map_shared_rank(S.P, j);
+        float4 pr[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) pr[g] = *reinterpret_cast<const float4*>(Pj + lane * 32 + 4 * (g ^ (lane & 7)));
+        float acc4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          const float4 ww = *reinterpret_cast<const float4*>(w + 4 * g);
+          acc4[0] = fmaf(pr[g].x, ww.x, acc4[0]);
+          acc4[1] = fmaf(pr[g].y, ww.y, acc4[1]);
+          acc4[2] = fmaf(pr[g].z, ww.z, acc4[2]);
+          acc4[3] = fmaf(pr[g].w, ww.w, acc4[3]);
+        }
+        const float acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+        const float wm = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(acc)));
+        const int ex = wm > 0.f ? fexpo(wm) : -1000;
+        if (ex < -120) flag = 1;
+        __syncwarp();
+        w[lane] = acc * __int_as_float((127 - max(ex, -120)) << 23);
+        __syncwarp();
+        Bv += (double)max(ex, -120) * (double)LN2 + S.lpc[j];
+      }
+      S.be[Lc * 32 + lane] = w[lane];
+      if (lane == 0) S.lb[Lc] = Bv;
+    }
+    __syncthreads();
+    SCAN_TS(4);
+    // ---- C: alpha / beta inside the chunk (warp 0 forward, warp 1 backward) ----------------
+    if (warp == 0) {
+      double A = S.la[0];
+      for (int k = 0; k < Lc; ++k) {
+        const float* Ek = S.E + k * 1024;
+        const float* v = S.al + k * 32;
+        float acc4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int a = 0; a < 32; a += 4) {
+          const float4 vv = *reinterpret_cast<const float4*>(v + a);
+          acc4[0] = fmaf(vv.x, Ek[a * 32 + sw[a & 7]], acc4[0]);
+          acc4[1] = fmaf(vv.y, Ek[(a + 1) * 32 + sw[(a + 1) & 7]], acc4[1]);
+          acc4[2] = fmaf(vv.z, Ek[(a + 2) * 32 + sw[(a + 2) & 7]], acc4[2]);
+          acc4[3] = fmaf(vv.w, Ek[(a + 3) * 32 + sw[(a + 3) & 7]], acc4[3]);
+        }
+        const float acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+        const float wm = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(acc)));
+        const int ex = wm > 0.f ? fexpo(wm) : -1000;
+        if (ex < -120) flag = 1;
+        S.al[(k + 1) * 32 + lane] = acc * __int_as_float((127 - max(ex, -120)) << 23);
+        A += (double)max(ex, -120) * (double)LN2 + (double)S.mx[k];
+        if (lane == 0) S.la[k + 1] = A;
+        __syncwarp();
+      }
+#ifdef SDB_SCAN_PROF
+      if (lane == 0) g_scan_t[blockIdx.x][8] = clock64();
+#endif
+    } else if (warp == 1) {
+      double Bv = S.lb[Lc];
+      for (int k = Lc - 1; k >= 0; --k) {
+        const float* Ek = S.E + k * 1024;
+        const float* w = S.be + (k + 1) * 32;
+        float acc4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          const float4 er = *reinterpret_cast<const float4*>(Ek + lane * 32 + 4 * (g ^ (lane & 7)));
+          const float4 ww = *reinterpret_cast<const float4*>(w + 4 * g);
+          acc4[0] = fmaf(er.x, ww.x, acc4[0]);
+          acc4[1] = fmaf(er.y, ww.y, acc4[1]);
+          acc4[2] = fmaf(er.z, ww.z, acc4[2]);
+          acc4[3] = fmaf(er.w, ww.w, acc4[3]);
+        }
+        const float acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+        const float wm = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(acc)));
+        const int ex = wm > 0.f ? fexpo(wm) : -1000;
+        if (ex < -120) flag = 1;
+        S.be[k * 32 + lane] = acc * __int_as_float((127 - max(ex, -120)) << 23);
+        Bv += (double)max(ex, -120) * (double)LN2 + (double)S.mx[k];
+        if (lane == 0) S.lb[k] = Bv;
+        __syncwarp();
+      }
+#ifdef SDB_SCAN_PROF
+      if (lane == 0) g_scan_t[blockIdx.x][9] = clock64();
+#endif
+    }
+    __syncthreads();
+    SCAN_TS(5);
+    // log Z from this chunk's start: A_t0 + B_t0 + log sum_a alpha~ beta~, and the emission factors
+    if (warp == 0) {
+      const float z = S.al[lane] * S.be[lane];
+      const float zs = warp_sum(z);
+      if (!(zs > 0.f)) flag = 1;
+      const double lz = S.la[0] + S.lb[0] + (double)flog(fmaxf(zs, 1e-38f));
+      if (lane == 0) S.misc[0] = lz;
+      for (int k = lane; k < Lc; k += 32) {
+        const double K = S.la[k] + (double)S.mx[k] + S.lb[k + 1] - lz;  // p = al E be e^K
+        if (K > 170.0) flag = 1;
+        S.gh[k] = fexp((float)(0.5 * fmin(K, 170.0)));
+      }
+    }
+    const int anyC = __syncthreads_or(flag);
+    if (tid < kSC) *cluster.map_shared_rank(S.flagC + c, tid) = anyC;
+  }
+  SCAN_TS(6);
+  cluster.sync();  // #2: no rank reads another's shared memory after this
+  SCAN_TS(7);
+  {
+    int failc = 0;
+#pragma unroll
+    for (int r = 0; r < kSC; ++r) failc |= S.flagC[r];
+    if (failc) goto fallback;
+  }
+  // ---- emission: p_t[a][b] = (alpha~[a] g) E[a][b] (beta~[b] g) --------------------------
+  if (c == 0 && tid == 0) {
+    logz[b] = S.misc[0];
+    status[b] = SDB_ST_OK;
+  }
+  if (marg_init && c == 0 && tid < m) {
+    const double K = S.la[0] + S.lb[0] - S.misc[0];
+    marg_init[(size_t)b * m + tid] = (float)((double)(S.al[tid] * S.be[tid]) * exp(K));
+  }
+  if (marg_trans) {
+    float* out = marg_trans + ((size_t)b * T + t0) * (size_t)(m * m);
+    if (kFull) {
+      const int a = tid >> 3, g = tid & 7;
+      for (int k = 0; k < Lc; ++k) {
+        const float gk = S.gh[k];
+        const float ra = S.al[k * 32 + a] * gk;
+        const float4 e = *reinterpret_cast<const float4*>(S.E + k * 1024 + a * 32 + 4 * (g ^ (a & 7)));
+        const float4 bv = *reinterpret_cast<const float4*>(S.be + (k + 1) * 32 + 4 * g);
+        float4 r;
+        r.x = ra * e.x * (bv.x * gk);
+        r.y = ra * e.y * (bv.y * gk);
+        r.z = ra * e.z * (bv.z * gk);
+        r.w = ra * e.w * (bv.w * gk);
+        __stcs(reinterpret_cast<float4*>(out + (size_t)k * 1024) + tid, r);
+      }
+
+    } else {
+      for (int e = tid; e < Lc * m * m; e += kThreads) {
+        const int k = e / (m * m), r = e - k * m * m, a = r / m, bb = r - a * m;
+        const float gk = S.gh[k];
+        out[e] = (S.al[k * 32 + a] * gk) * S.E[k * 1024 + swz(a, bb)] * (S.be[(k + 1) * 32 + bb] * gk);
+      }
+    }
+  }
+  return;
+
+fallback:
+  // exact log-space path for the whole instance, by the cluster's rank-0 CTA
+  if (c != 0) return;
+  __syncthreads();
+  {
+    float* sm = reinterpret_cast<float*>(smscan);
+    small_pass(init, trans, n, m, ws, logz, status, b, true, sm);
+    __syncthreads();
+    small_pass(init, trans, n, m, ws, logz, status, b, false, sm);
+    __syncthreads();
+    marg_steps(init, trans, n, m, ws, logz, marg_init, marg_trans, b, 0, T, true);
+  }
+}
+
+// Viterbi for m <= 32 (chain.py:98-114), one 1024-thread CTA per instance:
+// warp b owns next tag b, lane a the predecessor a.  A step is one fp64
+// candidate per thread, s_t[a] + theta_t[a][b] (the reference's addition
+// order: bit-identical scores), and a warp argmax by REDUX on an
+// order-preserving 64-bit key (high word, then low word among the ties,
+// then the lowest lane: the first maximum, chain.py:106).  The winner lane
+// writes s_(t+1)[b] and the backpointer; ONE CTA barrier per step publishes
+// the new scores.  theta tiles are staged transposed (T[b][a], pitch 33) by
+// all threads with 4-byte cp.async kVD steps ahead.
+constexpr int kVT = 1024;
+constexpr int kVD = 8;
+constexpr int kVTP = 33;
+
+__device__ __forceinline__ uint64_t dkey(double v) {
+  const uint64_t u = (uint64_t)__double_as_longlong(v);
+  return u ^ ((u >> 63) ? 0xffffffffffffffffull : 0x8000000000000000ull);
+}
+
+__global__ void __launch_bounds__(kVT, 1) chain_viterbi_warp_kernel(
+    const float* __restrict__ init, const float* __restrict__ trans, int n, int m, int32_t* __restrict__ tags,
+    double* __restrict__ score, int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) float smw[];
+  float* ring = smw;                                                       // [kVD][32][kVTP]
+  double* sv = reinterpret_cast<double*>(ring + kVD * 32 * kVTP);          // [2][32]
+  uint8_t* back = reinterpret_cast<uint8_t*>(sv + 64);                     // [n][32]
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int T = n - 1, mm = m * m;
+  const float* th = trans + (size_t)b * T * mm;
+  // this thread's staged element: (row a, col c) of a step, stored transposed
+  const int sa = tid >> 5, sc = tid & 31;
+  const bool st_live = sa < m && sc < m;
+  auto stage = [&](int t) {
+    if (st_live) {
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(ring + (t % kVD) * 32 * kVTP + sc * kVTP + sa);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(th + (size_t)t * mm + sa * m + sc));
+    }
+  };
+  for (int d = 0; d < kVD; ++d) {
+    if (d < T) stage(d);
+    cpa_commit();
+  }
+  int bad = 0;
+  if (tid < 32) {
+    const float x = tid < m ? init[(size_t)b * m + tid] : ninf();
+    bad |= (tid < m) && bad_input(x);
+    sv[tid] = tid < m ? (double)x : ninfd();
+  }
+  const bool wlive = warp < m, alive = lane < m;
+  for (int t = 0; t < T; ++t) {
+    cpa_wait_d();
+    __syncthreads();  // tile t resident; s_t published
+    const double* cur = sv + (t & 1) * 32;
+    double* nxt = sv + ((t + 1) & 1) * 32;
+    const float x = ring[(t % kVD) * 32 * kVTP + warp * kVTP + lane];
+    const double sa_v = cur[lane];
+    if (t + kVD < T) stage(t + kVD);
+    cpa_commit();
+    if (wlive) {
+      bad |= alive && bad_input(x);
+      const double v = alive ? sa_v + (double)x : ninfd();
+      const uint64_t k = dkey(v);
+      const uint32_t hi = (uint32_t)(k >> 32), lo = (uint32_t)k;
+      const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
+      uint32_t cand = __ballot_sync(0xffffffffu, hi == mh);
+      if (cand & (cand - 1)) {  // several equal high words: compare the low words
+        const uint32_t ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+        cand = __ballot_sync(0xffffffffu, hi == mh && lo == ml);
+      }
+      const int win = __ffs(cand) - 1;  // lowest predecessor among the maxima
+      if (lane == win) {
+        nxt[warp] = v;
+        back[(size_t)(t + 1) * 32 + warp] = (uint8_t)win;
+      }
+    } else if (lane == 0) {
+      nxt[warp] = ninfd();
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  bad = __syncthreads_or(bad);  // also publishes the last scores
+  if (warp == 0) {
+    const double* fin = sv + (T & 1) * 32;
+    const double v = alive ? fin[lane] : ninfd();
+    const uint64_t k = dkey(v);
+    const uint32_t hi = (uint32_t)(k >> 32), lo = (uint32_t)k;
+    const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
+    uint32_t cand = __ballot_sync(0xffffffffu, hi == mh);
+    if (cand & (cand - 1)) {
+      const uint32_t ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+      cand = __ballot_sync(0xffffffffu, hi == mh && lo == ml);
+    }
+    const int win = __ffs(cand) - 1;  // final tag: first argmax (chain.py:111)
+    const double best = __shfl_sync(0xffffffffu, v, win);
+    if (lane == 0) {
+      int32_t* tg = tags + (size_t)b * n;
+      const bool vac = (best == ninfd());
+      status[b] = bad ? SDB_ST_INVALID : (vac ? SDB_ST_VACUOUS : SDB_ST_OK);
+      score[b] = best;
+      int c = vac ? 0 : win;
+      tg[n - 1] = c;
+      for (int t = n - 2; t >= 0; --t) {
+        c = vac ? 0 : back[(size_t)(t + 1) * 32 + c];
+        tg[t] = c;
+      }
+    }
+  }
+}
+
 size_t viterbi_smem(int n, int m, bool with_back) {
   size_t s = (size_t)m * 8 + (size_t)kGroups * m * 12;
   if (with_back) s += (size_t)n * m * 2;
@@ -946,6 +1554,14 @@ size_t viterbi_smem(int n, int m, bool with_back) {
 }
 
 }  // namespace
+
+#ifdef SDB_SCAN_PROF
+extern "C" int sdb_debug_scan_times(void* host, size_t bytes) {
+  return cudaMemcpyFromSymbol(host, g_scan_t, bytes < sizeof(g_scan_t) ? bytes : sizeof(g_scan_t)) == cudaSuccess
+             ? 0
+             : -1;
+}
+#endif
 
 extern "C" size_t sdb_chain_fb_workspace(int64_t B, int32_t n, int32_t m) {
   size_t bytes = 0;
@@ -962,6 +1578,30 @@ extern "C" int sdb_chain_fb(const float* init, const float* trans, int64_t B, in
   ChainWs ws = carve_chain(workspace, B, n, m, &need);
   if (!workspace || ws_bytes < need) return SDB_ERR_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
+  const int T = n - 1;
+  if (m <= 32 && T >= 2 * kSC && (T + kSC - 1) / kSC <= kSLmax) {
+    // time-parallel scan: one cluster of kSC CTAs per instance, one launch
+    const size_t smem = scan_smem((T + kSC - 1) / kSC);
+    auto kern = (m == 32) ? chain_scan_kernel<true> : chain_scan_kernel<false>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return SDB_ERR_CUDA;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(B * kSC));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kSC;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, init, trans, n, m, ws, logz, marg_init, marg_trans, status) != cudaSuccess)
+      return SDB_ERR_CUDA;
+    SDB_CHECK_LAUNCH();
+    return SDB_OK;
+  }
   const bool lin = (m <= 32) && (n - 1 >= 2 * kLB);
   const size_t small_smem = (size_t)kD * m * m * 4 + (32 + 2 * kGroups * 32) * 4;
   if (lin) {
@@ -1025,6 +1665,16 @@ extern "C" int sdb_chain_viterbi(const float* init, const float* trans, int64_t 
   if (B == 0) return SDB_OK;
   if (!workspace || ws_bytes < sdb_chain_viterbi_workspace(B, n, m)) return SDB_ERR_WORKSPACE;
   if (m <= 32) {
+    const size_t smw = (size_t)kVD * 32 * kVTP * 4 + 64 * 8 + (size_t)n * 32 + 64;
+    if (smw <= 200 * 1024) {
+      if (cudaFuncSetAttribute(chain_viterbi_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw) !=
+          cudaSuccess)
+        return SDB_ERR_CUDA;
+      chain_viterbi_warp_kernel<<<(unsigned)B, kVT, smw, (cudaStream_t)stream>>>(init, trans, n, m, tags, score,
+                                                                               status);
+      SDB_CHECK_LAUNCH();
+      return SDB_OK;
+    }
     const size_t smem = (size_t)(kD + 1) * m * kVP * 4 + 64 * 8 + (size_t)n * 32 + 64;
     if (smem <= 200 * 1024) {
       if (cudaFuncSetAttribute(chain_viterbi_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=

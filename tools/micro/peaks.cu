@@ -26,6 +26,8 @@ __global__ void __launch_bounds__(512) spin(int iters, float* out) {
       for (int c = 0; c < kChains; ++c) {
         if (kOp == 0) {
           f[c] = fmaf(f[c], 0.9999999f, 1e-7f);
+        } else if (kOp == 3) {
+          f[c] = fmaf(f[c], f[(c + 1) & (kChains - 1)], f[(c + 3) & (kChains - 1)]);
         } else if (kOp == 1) {
           d[c] = fma(d[c], 0.9999999, 1e-7);
         } else {
@@ -68,7 +70,7 @@ int main() {
   const int sms = p.multiProcessorCount;
   int clk_khz = 0;
   cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
-  double ffma = 0, dfma = 0, ex2 = 0;
+  double ffma = 0, dfma = 0, ex2 = 0, ffma3 = 0;
   for (int rep = 0; rep < 3; ++rep) {  // best of 3
     double x = run<0>(sms, 4000);
     ffma = x > ffma ? x : ffma;
@@ -76,11 +78,13 @@ int main() {
     dfma = x > dfma ? x : dfma;
     x = run<2>(sms, 2000);
     ex2 = x > ex2 ? x : ex2;
+    x = run<3>(sms, 4000);
+    ffma3 = x > ffma3 ? x : ffma3;
   }
   printf("{\"gpu\": \"%s\", \"sms\": %d, \"clock_mhz_attr\": %.0f, "
-         "\"fp32_ffma_gflops\": %.1f, \"fp64_dfma_gflops\": %.1f, \"mufu_ex2_gops\": %.1f, "
+         "\"fp32_ffma_gflops\": %.1f, \"fp32_ffma_3reg_gflops\": %.1f, \"fp64_dfma_gflops\": %.1f, \"mufu_ex2_gops\": %.1f, "
          "\"ffma_lanes_per_sm_clk\": %.2f, \"dfma_lanes_per_sm_clk\": %.2f, \"ex2_lanes_per_sm_clk\": %.2f}\n",
-         p.name, sms, clk_khz / 1e3, 2 * ffma / 1e9, 2 * dfma / 1e9, ex2 / 1e9, ffma / sms / (clk_khz * 1e3),
+         p.name, sms, clk_khz / 1e3, 2 * ffma / 1e9, 2 * ffma3 / 1e9, 2 * dfma / 1e9, ex2 / 1e9, ffma / sms / (clk_khz * 1e3),
          dfma / sms / (clk_khz * 1e3), ex2 / sms / (clk_khz * 1e3));
   return 0;
 }
