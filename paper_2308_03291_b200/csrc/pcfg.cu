@@ -4,8 +4,9 @@
 // Reference: structdist constituency.py:246-371 (_pcfg_inside, pcfg_inside,
 // pcfg_gradients, _pcfg_walk, pcfg_argmax).  Per instance: root [NT],
 // binary_rules [NT][S][S] (children: NTs 0..NT-1 then PTs NT..S-1),
-// emissions [n][PT], optional sticky [n][n] in {0,-inf}.  NT, PT <= 32,
-// n <= 64.
+// emissions [n][PT], optional sticky [n][n] in {0,-inf}.  This kernel
+// serves NT, PT <= 32, n <= 64 (the C5b shape); larger grammars / sentences
+// take the general fp64 path in pcfg_gen.cu.
 //
 // Representation: each chart cell (i,j) holds a fp64 log scale s_ij and a
 // fp32 vector u_ij[32] = exp(chart[i,j,X] - s_ij) over its symbol class (PT
@@ -27,6 +28,11 @@
 //   per parent width, so no atomics), merged into the child's scaled vector.
 // Span marginals: exp(o_s + i_s - Z) * sum_X o[X] u[X].
 #include "common.cuh"
+
+size_t pcfg_gen_workspace(int64_t B, int n, int NT, int PT, bool grad);
+int pcfg_gen_launch(int mode, const float* root, const float* rules, const float* emissions, const float* sticky,
+                    int64_t B, int n, int NT, int PT, double* logz, float* span_marg, float* groot, float* grules,
+                    float* gemis, int32_t* status, void* workspace, size_t ws_bytes, cudaStream_t s);
 
 namespace {
 
@@ -629,11 +635,13 @@ __global__ void __launch_bounds__(kThreads) pcfg_max_kernel(
     const float* __restrict__ sticky_all, int n, int NT, int PT, double* __restrict__ chart_all,
     int8_t* __restrict__ mask_all, double* __restrict__ score, int32_t* __restrict__ status,
     const double* __restrict__ noise_all = nullptr, int64_t cap = 0, int num = 1, int32_t* __restrict__ used = nullptr) {
-  extern __shared__ double pairs[];  // [S][S]
+  extern __shared__ double pairs[];  // [S][S], then the walk stack [3][2n] ints
   __shared__ ArgBest red[kWarps];
-  __shared__ int stk_i[2 * kMaxN], stk_j[2 * kMaxN], stk_a[2 * kMaxN];
   __shared__ int badsh;
   const int S = NT + PT, S2 = S * S;
+  int* stk_i = reinterpret_cast<int*>(pairs + S2);
+  int* stk_j = stk_i + 2 * n;
+  int* stk_a = stk_j + 2 * n;
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float* root = root_all + (size_t)b * NT;
   const float* rules = rules_all + (size_t)b * NT * S2;
@@ -684,24 +692,27 @@ __global__ void __launch_bounds__(kThreads) pcfg_max_kernel(
             for (int e = lane; e < S2; e += 32) m = fmax(m, (double)ra[e] + pairs[e]);
             m = warp_maxd(m);
           } else {
-            // lse over C per B (lane per B), then over B (constituency.py:263-264)
-            double vb[2] = {ninfd(), ninfd()};
-            for (int q = 0; q < 2; ++q) {
-              const int Bq = lane + 32 * q;
-              if (Bq >= S) continue;
+            // lse over C per B (lanes over B), then over B (constituency.py:263-264); the
+            // per-B values are combined with an online (max, sum) so any S works
+            double lm = ninfd(), ls = 0.0;
+            for (int Bq = lane; Bq < S; Bq += 32) {
               double mx = ninfd();
               for (int Cq = 0; Cq < S; ++Cq) mx = fmax(mx, (double)ra[Bq * S + Cq] + pairs[Bq * S + Cq]);
-              if (mx != ninfd()) {
-                double sm = 0.0;
-                for (int Cq = 0; Cq < S; ++Cq) sm += exp((double)ra[Bq * S + Cq] + pairs[Bq * S + Cq] - mx);
-                mx = log(sm) + mx;
+              if (mx == ninfd()) continue;
+              double sm = 0.0;
+              for (int Cq = 0; Cq < S; ++Cq) sm += exp((double)ra[Bq * S + Cq] + pairs[Bq * S + Cq] - mx);
+              const double vb = log(sm) + mx;
+              if (vb > lm) {
+                ls = (lm == ninfd() ? 0.0 : ls * exp(lm - vb)) + 1.0;
+                lm = vb;
+              } else {
+                ls += exp(vb - lm);
               }
-              vb[q] = mx;
             }
-            double mx = warp_maxd(fmax(vb[0], vb[1]));
+            double mx = warp_maxd(lm);
             double sm = 0.0;
             if (mx != ninfd()) {
-              for (int q = 0; q < 2; ++q) sm += (vb[q] == ninfd()) ? 0.0 : exp(vb[q] - mx);
+              sm = (lm == ninfd()) ? 0.0 : ls * exp(lm - mx);
               for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
               mx = log(sm) + mx;
             }
@@ -801,13 +812,21 @@ int pcfg_launch(const float* root, const float* rules, const float* emissions, c
 
 int pcfg_check(int64_t B, int n, int NT, int PT) {
   if (B < 0 || n < 1 || NT < 1 || PT < 1) return SDB_ERR_ARG;
-  if (n > kMaxN || NT > 32 || PT > 32) return SDB_ERR_UNSUPPORTED;
+  if (n > 1024 || NT + PT > 1024) return SDB_ERR_UNSUPPORTED;
   return SDB_OK;
+}
+
+// the register / shared-memory specialised inside-outside kernel; other shapes take pcfg_gen.cu
+bool pcfg_fast(int n, int NT, int PT) { return n <= kMaxN && NT <= 32 && PT <= 32; }
+
+size_t max_smem(int n, int NT, int PT) {
+  return (size_t)(NT + PT) * (NT + PT) * sizeof(double) + (size_t)6 * n * sizeof(int);
 }
 
 }  // namespace
 
 extern "C" size_t sdb_pcfg_fb_workspace(int64_t B, int32_t n, int32_t NT, int32_t PT) {
+  if (!pcfg_fast(n, NT, PT)) return pcfg_gen_workspace(B, n, NT, PT, false);
   size_t bytes = 0;
   pcfg_carve(nullptr, B, n, NT, PT, &bytes);
   return bytes;
@@ -820,10 +839,13 @@ extern "C" int sdb_pcfg_fb(const float* root, const float* rules, const float* e
   if (rc) return rc;
   if (!root || !rules || !emissions || !logz || !status) return SDB_ERR_ARG;
   if (B == 0) return SDB_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!pcfg_fast(n, NT, PT))
+    return pcfg_gen_launch(span_marg ? 1 : 0, root, rules, emissions, sticky, B, n, NT, PT, logz, span_marg, nullptr,
+                           nullptr, nullptr, status, workspace, ws_bytes, s);
   size_t need = 0;
   PcfgWs ws = pcfg_carve(workspace, B, n, NT, PT, &need);
   if (!workspace || ws_bytes < need) return SDB_ERR_WORKSPACE;
-  cudaStream_t s = (cudaStream_t)stream;
   return span_marg ? pcfg_launch<1>(root, rules, emissions, sticky, B, n, NT, PT, ws, logz, span_marg, PcfgGradOut{},
                                     status, s)
                    : pcfg_launch<0>(root, rules, emissions, sticky, B, n, NT, PT, ws, logz, nullptr, PcfgGradOut{},
@@ -831,6 +853,7 @@ extern "C" int sdb_pcfg_fb(const float* root, const float* rules, const float* e
 }
 
 extern "C" size_t sdb_pcfg_grad_workspace(int64_t B, int32_t n, int32_t NT, int32_t PT) {
+  if (!pcfg_fast(n, NT, PT)) return pcfg_gen_workspace(B, n, NT, PT, true);
   size_t bytes = 0;
   pcfg_carve(nullptr, B, n, NT, PT, &bytes, true);
   return bytes;
@@ -845,6 +868,9 @@ extern "C" int sdb_pcfg_grad(const float* root, const float* rules, const float*
   if (!root || !rules || !emissions || !logz || !span_marg || !grad_root || !grad_rules || !grad_emissions || !status)
     return SDB_ERR_ARG;
   if (B == 0) return SDB_OK;
+  if (!pcfg_fast(n, NT, PT))
+    return pcfg_gen_launch(2, root, rules, emissions, sticky, B, n, NT, PT, logz, span_marg, grad_root, grad_rules,
+                           grad_emissions, status, workspace, ws_bytes, (cudaStream_t)stream);
   size_t need = 0;
   PcfgWs ws = pcfg_carve(workspace, B, n, NT, PT, &need, true);
   if (!workspace || ws_bytes < need) return SDB_ERR_WORKSPACE;
@@ -864,7 +890,8 @@ extern "C" int sdb_pcfg_viterbi(const float* root, const float* rules, const flo
   if (!root || !rules || !emissions || !span_mask || !score || !status) return SDB_ERR_ARG;
   if (B == 0) return SDB_OK;
   if (!workspace || ws_bytes < sdb_pcfg_viterbi_workspace(B, n, NT, PT)) return SDB_ERR_WORKSPACE;
-  const size_t smem = (size_t)(NT + PT) * (NT + PT) * sizeof(double);
+  const size_t smem = max_smem(n, NT, PT);
+  if (smem > 220 * 1024) return SDB_ERR_UNSUPPORTED;
   if (cudaFuncSetAttribute(pcfg_max_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return SDB_ERR_CUDA;
@@ -887,7 +914,8 @@ extern "C" int sdb_pcfg_sample(const float* root, const float* rules, const floa
   if (noise_per_instance < (int64_t)num * (NT + S * S * ((int64_t)n * (n - 1) / 2))) return SDB_ERR_ARG;
   if (B == 0) return SDB_OK;
   if (!workspace || ws_bytes < sdb_pcfg_viterbi_workspace(B, n, NT, PT)) return SDB_ERR_WORKSPACE;
-  const size_t smem = (size_t)S * S * sizeof(double);
+  const size_t smem = max_smem(n, NT, PT);
+  if (smem > 220 * 1024) return SDB_ERR_UNSUPPORTED;
   if (cudaFuncSetAttribute(pcfg_max_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return SDB_ERR_CUDA;

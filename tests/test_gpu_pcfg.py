@@ -154,3 +154,45 @@ def test_pcfg_log_prob_masked_inside():
     bad["sticky"][0, 0] = 0.0
     with pytest.raises(sd.InvalidProblem):
         sd.log_prob(d, bad)
+
+
+@pytest.mark.parametrize("B,n,nt,pt", [(2, 8, 40, 36), (2, 70, 3, 2), (1, 6, 64, 96), (2, 5, 33, 1)])
+def test_pcfg_general_shapes_vs_oracle(B, n, nt, pt):
+    """Grammars / sentences outside the fast kernel's shape (n > 64 or NT, PT >
+    32: the paper's NT=64, PT=96 grammar) run on the general
+    fp64 inside-outside kernel (pcfg_gen.cu): log Z, span marginals, all four
+    gradients and the argmax against the oracle."""
+    need_gpu()
+    root, rules, emis = batch_pcfg(4300, B, n, nt, pt)
+    logz, marg, st = K.pcfg_fb(dev(root), dev(rules), dev(emis))
+    gl, g, st2 = K.pcfg_grad(dev(root), dev(rules), dev(emis))
+    assert (st.cpu().numpy() == 0).all() and (st2.cpu().numpy() == 0).all()
+    for b in range(B):
+        z, go = O.pcfg_gradients(root[b], rules[b], emis[b])
+        assert abs(logz[b].item() - z) <= RTOL * abs(z) + 1e-9
+        assert abs(gl[b].item() - z) <= RTOL * abs(z) + 1e-9
+        np.testing.assert_allclose(marg[b].cpu().numpy(), go["sticky"], rtol=RTOL, atol=ATOL)
+        for k in ("root", "binary_rules", "emissions", "sticky"):
+            np.testing.assert_allclose(g[k][b].cpu().numpy(), go[k], rtol=RTOL, atol=ATOL, err_msg=k)
+    if n <= 12:
+        mask, score, st3 = K.pcfg_viterbi(dev(root), dev(rules), dev(emis))
+        for b in range(B):
+            mo, so = O.pcfg_argmax(root[b], rules[b], emis[b])
+            np.testing.assert_array_equal(mask[b].cpu().numpy(), mo)
+            assert score[b].item() == so
+
+
+def test_pcfg_paper_grammar_api():
+    """The drop-in API at the paper's PCFG grammar size (NT=64, PT=96) with a
+    sticky span mask: log_partition / marginals / log_prob run (general path)."""
+    need_gpu()
+    root, rules, emis = batch_pcfg(4400, 1, 6, 64, 96)
+    d = sd.PCFG(root[0], rules[0], emis[0])
+    z = sd.log_partition(d)
+    zo = O.pcfg_log_partition(root[0], rules[0], emis[0])
+    assert abs(z - zo) <= RTOL * abs(zo)
+    m = sd.marginals(d)["sticky"]
+    np.testing.assert_allclose(m, O.pcfg_gradients(root[0], rules[0], emis[0])[1]["sticky"], rtol=RTOL, atol=ATOL)
+    ind = sd.argmax(d)
+    lp = sd.log_prob(d, ind)
+    assert lp <= 0.0 and np.isfinite(lp)
