@@ -1444,18 +1444,29 @@ fallback:
 // warp b owns next tag b, lane a the predecessor a.  A step is one fp64
 // candidate per thread, s_t[a] + theta_t[a][b] (the reference's addition
 // order: bit-identical scores), and a warp argmax by REDUX on an
-// order-preserving 64-bit key (high word, then low word among the ties,
+// order-preserving 64-bit key (high word, then the low word among the ties,
 // then the lowest lane: the first maximum, chain.py:106).  The winner lane
 // writes s_(t+1)[b] and the backpointer; ONE CTA barrier per step publishes
-// the new scores.  theta tiles are staged transposed (T[b][a], pitch 33) by
-// all threads with 4-byte cp.async kVD steps ahead.
+// the new scores.  theta tiles stream through a ring of kVD row-padded tiles
+// (pitch 36), one 16-byte cp.async per thread of the first 256 per step.
 constexpr int kVT = 1024;
 constexpr int kVD = 8;
-constexpr int kVTP = 33;
+constexpr int kVTP = 36;
 
 __device__ __forceinline__ uint64_t dkey(double v) {
   const uint64_t u = (uint64_t)__double_as_longlong(v);
   return u ^ ((u >> 63) ? 0xffffffffffffffffull : 0x8000000000000000ull);
+}
+// lowest lane holding the maximum key (the reference's first argmax)
+__device__ __forceinline__ int warp_argmax_key(uint64_t k) {
+  const uint32_t hi = (uint32_t)(k >> 32), lo = (uint32_t)k;
+  const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
+  uint32_t cand = __ballot_sync(0xffffffffu, hi == mh);
+  if (cand & (cand - 1)) {  // several equal high words: compare the low words
+    const uint32_t ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+    cand = __ballot_sync(0xffffffffu, hi == mh && lo == ml);
+  }
+  return __ffs(cand) - 1;
 }
 
 __global__ void __launch_bounds__(kVT, 1) chain_viterbi_warp_kernel(
@@ -1468,13 +1479,21 @@ __global__ void __launch_bounds__(kVT, 1) chain_viterbi_warp_kernel(
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int T = n - 1, mm = m * m;
   const float* th = trans + (size_t)b * T * mm;
-  // this thread's staged element: (row a, col c) of a step, stored transposed
-  const int sa = tid >> 5, sc = tid & 31;
-  const bool st_live = sa < m && sc < m;
+  const bool full = (m == 32) && ((((uintptr_t)th) & 15) == 0);
   auto stage = [&](int t) {
-    if (st_live) {
-      const unsigned dst = (unsigned)__cvta_generic_to_shared(ring + (t % kVD) * 32 * kVTP + sc * kVTP + sa);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(th + (size_t)t * mm + sa * m + sc));
+    float* tile = ring + (t % kVD) * 32 * kVTP;
+    if (full) {
+      if (tid < 256) {
+        const int r = tid >> 3, c4 = (tid & 7) * 4;
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(tile + r * kVTP + c4);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(th + (size_t)t * 1024 + r * 32 + c4));
+      }
+    } else {
+      const int r = tid >> 5, c = tid & 31;
+      if (r < m && c < m) {
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(tile + r * kVTP + c);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(th + (size_t)t * mm + r * m + c));
+      }
     }
   };
   for (int d = 0; d < kVD; ++d) {
@@ -1493,22 +1512,14 @@ __global__ void __launch_bounds__(kVT, 1) chain_viterbi_warp_kernel(
     __syncthreads();  // tile t resident; s_t published
     const double* cur = sv + (t & 1) * 32;
     double* nxt = sv + ((t + 1) & 1) * 32;
-    const float x = ring[(t % kVD) * 32 * kVTP + warp * kVTP + lane];
-    const double sa_v = cur[lane];
+    const float x = ring[(t % kVD) * 32 * kVTP + lane * kVTP + warp];
+    const double sa = cur[lane];
     if (t + kVD < T) stage(t + kVD);
     cpa_commit();
     if (wlive) {
       bad |= alive && bad_input(x);
-      const double v = alive ? sa_v + (double)x : ninfd();
-      const uint64_t k = dkey(v);
-      const uint32_t hi = (uint32_t)(k >> 32), lo = (uint32_t)k;
-      const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
-      uint32_t cand = __ballot_sync(0xffffffffu, hi == mh);
-      if (cand & (cand - 1)) {  // several equal high words: compare the low words
-        const uint32_t ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
-        cand = __ballot_sync(0xffffffffu, hi == mh && lo == ml);
-      }
-      const int win = __ffs(cand) - 1;  // lowest predecessor among the maxima
+      const double v = alive ? sa + (double)x : ninfd();
+      const int win = warp_argmax_key(dkey(v));
       if (lane == win) {
         nxt[warp] = v;
         back[(size_t)(t + 1) * 32 + warp] = (uint8_t)win;
@@ -1522,15 +1533,7 @@ __global__ void __launch_bounds__(kVT, 1) chain_viterbi_warp_kernel(
   if (warp == 0) {
     const double* fin = sv + (T & 1) * 32;
     const double v = alive ? fin[lane] : ninfd();
-    const uint64_t k = dkey(v);
-    const uint32_t hi = (uint32_t)(k >> 32), lo = (uint32_t)k;
-    const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
-    uint32_t cand = __ballot_sync(0xffffffffu, hi == mh);
-    if (cand & (cand - 1)) {
-      const uint32_t ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
-      cand = __ballot_sync(0xffffffffu, hi == mh && lo == ml);
-    }
-    const int win = __ffs(cand) - 1;  // final tag: first argmax (chain.py:111)
+    const int win = warp_argmax_key(dkey(v));  // final tag: first argmax (chain.py:111)
     const double best = __shfl_sync(0xffffffffu, v, win);
     if (lane == 0) {
       int32_t* tg = tags + (size_t)b * n;
@@ -1665,7 +1668,7 @@ extern "C" int sdb_chain_viterbi(const float* init, const float* trans, int64_t 
   if (B == 0) return SDB_OK;
   if (!workspace || ws_bytes < sdb_chain_viterbi_workspace(B, n, m)) return SDB_ERR_WORKSPACE;
   if (m <= 32) {
-    const size_t smw = (size_t)kVD * 32 * kVTP * 4 + 64 * 8 + (size_t)n * 32 + 64;
+    const size_t smw = (size_t)kVD * 32 * kVTP * 4 + 64 * 8 + (size_t)n * 32 + 64;  // ring, scores, backpointers
     if (smw <= 200 * 1024) {
       if (cudaFuncSetAttribute(chain_viterbi_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw) !=
           cudaSuccess)

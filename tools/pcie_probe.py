@@ -29,3 +29,5 @@ print("h2d||d2h    ms", t(both))
 print("kernel      ms", t(lambda: K.nw_fb(th)))
 for ch in (1, 2, 4, 8, 16):
     print("pipelined chunks=%2d ms" % ch, t(lambda: K.run_host_batch(lambda x: K.nw_fb(x)[:2], [hin], [hz, hout], dev, chunks=ch)))
+for sizes in ([16] * 16, [32] * 7 + [24, 8], [16] * 14 + [24, 8], [8] * 4 + [16] * 14):
+    print("pipelined sizes=%s ms" % (sizes[:3],), t(lambda: K.run_host_batch(lambda x: K.nw_fb(x)[:2], [hin], [hz, hout], dev, chunks=sizes)))
