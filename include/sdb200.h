@@ -285,6 +285,16 @@ int sdb_pcfg_sample(const float* root, const float* rules, const float* emission
                     int8_t* span_mask, int32_t* used, int32_t* status, void* workspace, size_t ws_bytes,
                     void* stream);
 
+/* ---- derived quantities: expected score under a potential tensor ------------
+ * Replaces dist.py:306-347's host reduction _expected_score_under (masked_dot,
+ * numerics.py:171-183) for cross_entropy / entropy / kl_divergence: out[b] +=
+ * sum_e marg[b][e] * theta[b][e] over the parts with marg > 0 (0 * -inf = 0);
+ * neginf[b] |= 1 when such a part has theta = -inf (supp p not in supp q -> the
+ * cross-entropy is +inf).  Accumulates (zero out / neginf once for several
+ * tensors).  marg, theta [B][len] fp32 device arrays. */
+int sdb_masked_dot(const float* marg, const float* theta, int64_t B, int64_t len, double* out, int32_t* neginf,
+                   void* stream);
+
 #ifdef __cplusplus
 }
 #endif

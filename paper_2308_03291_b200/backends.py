@@ -49,12 +49,13 @@ def to_host(t):
 class Result:
     """Host-side outcome of one batched log-partition / marginals call."""
 
-    def __init__(self, logz, status, marg, vacuous_msg, public_keys=None):
+    def __init__(self, logz, status, marg, vacuous_msg, public_keys=None, dev=None):
         self.logz = np.asarray(logz, dtype=np.float64)
         self.status = np.asarray(status)
         self.marg = marg  # list of dict[str, ndarray] or None
         self.msg = vacuous_msg
         self.public_keys = public_keys
+        self.dev = dev  # dict[str, device tensor [B, ...]] when run(dev=True): marginals left on the GPU
 
     def raise_vacuous(self, i):
         st = int(self.status[i])
@@ -148,10 +149,12 @@ class ChainBackend(Backend):
     def _stack(self, ds):
         return to_dev([d.init for d in ds]), to_dev([d.transitions for d in ds])
 
-    def run(self, ds, marginals=True, full=False):
+    def run(self, ds, marginals=True, full=False, dev=False):
         init, trans = self._stack(ds)
         logz, mi, mt, st = K.chain_fb(init, trans, marginals)
         marg = None
+        if marginals and dev:
+            return Result(to_host(logz), to_host(st), None, self.vacuous_msg, dev={"init": mi, "transitions": mt})
         if marginals:
             mi, mt = to_host(mi).astype(np.float64), to_host(mt).astype(np.float64)
             marg = [{"init": mi[i], "transitions": mt[i]} for i in range(len(ds))]
@@ -211,9 +214,11 @@ class AlignmentBackend(Backend):
     def argmax_algo(self, d):
         return "max-plus-needleman-wunsch"
 
-    def run(self, ds, marginals=True, full=False):
+    def run(self, ds, marginals=True, full=False, dev=False):
         th = to_dev([d.move_potentials for d in ds])
         logz, marg, st = K.nw_fb(th, marginals)
+        if marginals and dev:
+            return Result(to_host(logz), to_host(st), None, self.vacuous_msg, dev={"move_potentials": marg})
         out = None
         if marginals:
             mg = to_host(marg).astype(np.float64)
@@ -274,9 +279,11 @@ class CTCBackend(Backend):
         tg = to_dev([np.asarray(d.target, dtype=np.int64).reshape(-1) for d in ds], torch.int32)
         return to_dev([d.frame_potentials for d in ds]), tg
 
-    def run(self, ds, marginals=True, full=False):
+    def run(self, ds, marginals=True, full=False, dev=False):
         fp, tg = self._stack(ds)
         logz, marg, st = K.ctc_fb(fp, tg, marginals)
+        if marginals and dev:
+            return Result(to_host(logz), to_host(st), None, self.vacuous_msg, dev={"frame_potentials": marg})
         out = None
         if marginals:
             mg = to_host(marg).astype(np.float64)
@@ -333,9 +340,11 @@ class TreeBackend(Backend):
     def argmax_algo(self, d):
         return "max-plus-cky"
 
-    def run(self, ds, marginals=True, full=False):
+    def run(self, ds, marginals=True, full=False, dev=False):
         th = to_dev([d.span_potentials for d in ds])
         logz, marg, st = K.tree_fb(th, marginals)
+        if marginals and dev:
+            return Result(to_host(logz), to_host(st), None, self.vacuous_msg, dev={"span_potentials": marg})
         out = None
         if marginals:
             mg = to_host(marg).astype(np.float64)
@@ -406,7 +415,7 @@ class SpanningBackend(Backend):
             name = "reweighting+" + name
         return self._prefix(d) + name
 
-    def run(self, ds, marginals=True, full=False):
+    def run(self, ds, marginals=True, full=False, dev=False):
         d0 = ds[0]
         adj = to_dev([d.adjacency for d in ds])
         if d0.projective:
@@ -416,6 +425,8 @@ class SpanningBackend(Backend):
             logz, marg, st = K.mtt(adj, d0.single_root_edge, marginals)
             msg = "no spanning tree has finite score"
         out = None
+        if marginals and dev:
+            return Result(to_host(logz), to_host(st), None, msg, dev={"adjacency": marg})
         if marginals:
             mg = to_host(marg).astype(np.float64)
             out = [{"adjacency": mg[i]} for i in range(len(ds))]
@@ -617,11 +628,13 @@ class PCFGBackend(Backend):
         return (to_dev([d.root for d in ds]), to_dev([d.binary_rules for d in ds]), to_dev([d.emissions for d in ds]),
                 to_dev([d.sticky for d in ds]))
 
-    def run(self, ds, marginals=True, full=False):
+    def run(self, ds, marginals=True, full=False, dev=False):
         root, rules, emis, sticky = self._inputs(ds)
         if full:
             # potential_marginals: all four gradients of pcfg_gradients (constituency.py:292-340)
             logz, g, st = K.pcfg_grad(root, rules, emis, sticky)
+            if dev:
+                return Result(to_host(logz), to_host(st), None, self.vacuous_msg, public_keys=("sticky",), dev=dict(g))
             gh = {k: to_host(v).astype(np.float64) for k, v in g.items()}
             out = [{k: gh[k][i] for k in ("root", "binary_rules", "emissions", "sticky")} for i in range(len(ds))]
             return Result(to_host(logz), to_host(st), out, self.vacuous_msg, public_keys=("sticky",))
@@ -692,9 +705,11 @@ class SemiMarkovBackend(Backend):
     def argmax_algo(self, d):
         return "semi-markov-viterbi"
 
-    def run(self, ds, marginals=True, full=False):
+    def run(self, ds, marginals=True, full=False, dev=False):
         th = to_dev([d.segment_potentials for d in ds])
         logz, marg, st = K.semimarkov_fb(th, marginals)
+        if marginals and dev:
+            return Result(to_host(logz), to_host(st), None, self.vacuous_msg, dev={"segment_potentials": marg})
         out = None
         if marginals:
             mg = to_host(marg).astype(np.float64)

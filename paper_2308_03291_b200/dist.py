@@ -149,14 +149,35 @@ def _expected_score(marg, q_pots) -> float:
     return total
 
 
+def _expected_scores_device(be, ps, qs):
+    """sum_e p(e) theta_q(e) for a same-shape group, fused on the GPU: p's
+    full marginals (potential_marginals, dist.py:96-117) stay on the device
+    and one masked-dot reduction per potential tensor (kernels.expected_score)
+    returns B doubles (-inf where a marked part of p is -inf under q)."""
+    res = be.run(ps, marginals=True, full=True, dev=True)
+    for i in range(len(ps)):
+        res.raise_vacuous(i)
+    dev = next(iter(res.dev.values())).device
+    pairs = []
+    for key, marg in res.dev.items():
+        theta = torch.from_numpy(np.ascontiguousarray(np.stack([q.potentials()[key] for q in qs]))).to(
+            torch.float32).to(dev, non_blocking=True)
+        pairs.append((marg, theta))
+    from . import kernels as K
+
+    score, flag = K.expected_score(pairs, len(ps), dev)
+    score, flag = score.cpu().numpy(), flag.cpu().numpy()
+    return [NEG_INF if f else float(x) for x, f in zip(score, flag)]
+
+
 def cross_entropy_info(p, q):
-    """dist.py:316-325: H(p,q) = logZ_q - sum_e p(e) theta_q(e)."""
+    """dist.py:316-325: H(p,q) = logZ_q - sum_e p(e) theta_q(e); the expected
+    score is a fused device reduction over p's marginals."""
     _reject_one_to_one(p)
     _reject_one_to_one(q)
     _same_factorization(p, q)
-    marg_p = potential_marginals(p)
+    expected = _expected_scores_device(_backend(p), [p], [q])[0]
     log_zq, algo = log_partition_info(q)
-    expected = _expected_score(marg_p, q.potentials())
     if expected == NEG_INF:
         return float("inf"), algo
     return log_zq - expected, algo
@@ -245,7 +266,7 @@ _BATCHED = {}
 
 def batch_map(op, dists, *args, ragged: bool = True, **kwargs) -> list:
     """dist.py:355-361, batched: log_partition / marginals / argmax (and
-    their *_info forms) run as ONE kernel call per group.  Same-shape
+    their *_info forms) and entropy run as ONE kernel call per group.  Same-shape
     instances group directly; with `ragged`, chains, alignments, CTC
     (same target length), multi-root spanning trees, semi-Markov CRFs (same
     s, m), Tree-CRFs (same m) and PCFGs (same NT, PT) of DIFFERENT lengths
@@ -261,7 +282,8 @@ def batch_map(op, dists, *args, ragged: bool = True, **kwargs) -> list:
     groups: "OrderedDict[tuple, list[int]]" = OrderedDict()
     for i, d in enumerate(dists):
         be = _backend(d)
-        key = ("ragged",) + rg.group_key(d) if ragged and rg.raggable(d) else (type(d), be.batch_key(d))
+        pad = ragged and name not in ("entropy", "entropy_info") and rg.raggable(d)  # entropy: exact shapes only
+        key = ("ragged",) + rg.group_key(d) if pad else (type(d), be.batch_key(d))
         groups.setdefault(key, []).append(i)
     # a ragged group whose padded shape the kernels cannot take runs as exact-shape groups
     for key in [k for k in groups if k[0] == "ragged"]:
@@ -340,10 +362,23 @@ def _b_argmax(be, group):
     return [r[0] for r in _b_argmax_info(be, group)]
 
 
+def _b_entropy_info(be, group):
+    """entropy over a same-shape group: ONE marginal launch, ONE fused
+    expected-score reduction, ONE log-partition launch (dist.py:338-339)."""
+    expected = _expected_scores_device(be, group, group)
+    logz = be.run(group, marginals=False).logz
+    return [(float("inf") if e == NEG_INF else float(z) - e, be.algo(d)) for e, z, d in zip(expected, logz, group)]
+
+
+def _b_entropy(be, group):
+    return [h for h, _ in _b_entropy_info(be, group)]
+
+
 _BATCHED.update({
     "log_partition": _b_logz, "log_partition_info": _b_logz_info,
     "marginals": _b_marg, "marginals_info": _b_marg_info,
     "argmax": _b_argmax, "argmax_info": _b_argmax_info,
+    "entropy": _b_entropy, "entropy_info": _b_entropy_info,
 })
 
 

@@ -639,6 +639,29 @@ def pcfg_sample(root, rules, emissions, sticky, noise, num: int):
     return mask, used, status
 
 
+# ------------------------------------------------------ derived quantities
+
+
+def expected_score(pairs, B: int, device):
+    """sum_e p(e) theta(e) per instance over (marginals, potentials) device
+    tensor pairs with a leading batch axis (dist.py:306-347 via masked_dot,
+    numerics.py:171-183) -> (score [B] f64, neginf [B] i32: a marked part
+    is -inf).  Only B doubles leave the device."""
+    lib = _lib.load()
+    out = torch.zeros(B, dtype=torch.float64, device=device)
+    flag = torch.zeros(B, dtype=torch.int32, device=device)
+    keep = []
+    for marg, theta in pairs:
+        marg, theta = f32(marg, "marginals"), f32(theta, "potentials")
+        if marg.shape != theta.shape:
+            raise ValueError(f"marginals {tuple(marg.shape)} vs potentials {tuple(theta.shape)}")
+        keep += [marg, theta]
+        rc = lib.sdb_masked_dot(ptr(marg), ptr(theta), B, marg.numel() // max(B, 1), ptr(out), ptr(flag),
+                                stream_ptr(device))
+        _lib.check(rc, "sdb_masked_dot")
+    return out, flag
+
+
 # ------------------------------------------------------ host-resident batches
 
 _PIPE = {}

@@ -74,3 +74,14 @@ def test_log_prob(case):
                 sd.log_prob(p, ind)
         else:
             _close(sd.log_prob(p, ind), want, lz)
+
+
+def test_batched_entropy_matches_single():
+    """batch_map(entropy): one marginal launch + one fused expected-score
+    reduction per shape group == the per-instance calls."""
+    need_gpu()
+    dists = [bld.make_dist(sd, "chain", bld.family_inputs("chain", 40 + s, dict(n=9, m=4))) for s in range(5)]
+    dists += [bld.make_dist(sd, "tree", bld.family_inputs("tree", 50 + s, dict(n=6, m=3))) for s in range(3)]
+    got = sd.batch_map(sd.entropy, dists)
+    for d, h in zip(dists, got):
+        assert abs(h - sd.entropy(d)) <= 1e-9 * max(1.0, abs(h))
