@@ -11,6 +11,7 @@ The public surface mirrors `structdist/__init__.py:11-80`.
 
 from . import kernels  # noqa: F401  (batched device entry points)
 from . import sharding  # noqa: F401  (multi-GPU batch sharding)
+from . import problemfile  # noqa: F401  (problem documents, batched loader)
 from .dist import (
     argmax,
     argmax_info,

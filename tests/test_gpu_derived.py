@@ -85,3 +85,22 @@ def test_batched_entropy_matches_single():
     got = sd.batch_map(sd.entropy, dists)
     for d, h in zip(dists, got):
         assert abs(h - sd.entropy(d)) <= 1e-9 * max(1.0, abs(h))
+
+
+def test_solve_problem_files():
+    """Problem documents written by the reference, solved as one batch
+    (problemfile.solve_problems -> batch_map): log Z as the reference
+    computed it when writing the fixtures."""
+    need_gpu()
+    import glob
+    import json
+    import os
+
+    from paper_2308_03291_b200 import problemfile as pf
+
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "problems")
+    verdicts = json.load(open(os.path.join(here, "verdicts.json")))
+    names = sorted(k for k, v in verdicts.items() if v["ok"])
+    got = pf.solve_problems([os.path.join(here, k + ".json") for k in names], sd.log_partition)
+    for k, z in zip(names, got):
+        assert abs(z - verdicts[k]["logz"]) <= RTOL * max(1.0, abs(z)), k
