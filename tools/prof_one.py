@@ -18,7 +18,8 @@ elif fam in ("chain", "chainv"):
     init = torch.randn(32, 32, device="cuda", generator=g)
     tr = torch.randn(32, 127, 32, 32, device="cuda", generator=g)
     fn = {"fb": lambda: K.chain_fb(init, tr), "lz": lambda: K.chain_fb(init, tr, False),
-          "vit": lambda: K.chain_viterbi(init, tr)}["vit" if fam == "chainv" else mode]
+          "vit": lambda: K.chain_viterbi(init, tr),
+          "both": lambda: K.chain_fb_viterbi(init, tr)}["vit" if fam == "chainv" else mode]
 elif fam in ("mtt", "eisner", "kuhl"):
     adj = torch.randn(512 if fam == "mtt" else 256, 129, 129, device="cuda", generator=g)
     adj[:, :, 0] = NEG_INF
