@@ -1440,16 +1440,17 @@ fallback:
   }
 }
 
-// Viterbi for m <= 32 (chain.py:98-114), one 1024-thread CTA per instance:
-// warp b owns next tag b, lane a the predecessor a.  A step is one fp64
-// candidate per thread, s_t[a] + theta_t[a][b] (the reference's addition
+// Viterbi for m <= 32 (chain.py:98-114), one 512-thread CTA per instance:
+// warp w owns the next tags 2w, 2w+1, lane a the predecessor a.  A step is two
+// independent fp64 candidates per thread (their argmax chains interleave),
+// s_t[a] + theta_t[a][b] (the reference's addition
 // order: bit-identical scores), and a warp argmax by REDUX on an
 // order-preserving 64-bit key (high word, then the low word among the ties,
 // then the lowest lane: the first maximum, chain.py:106).  The winner lane
 // writes s_(t+1)[b] and the backpointer; ONE CTA barrier per step publishes
 // the new scores.  theta tiles stream through a ring of kVD row-padded tiles
 // (pitch 36), one 16-byte cp.async per thread of the first 256 per step.
-constexpr int kVT = 1024;
+constexpr int kVT = 512;
 constexpr int kVD = 8;
 constexpr int kVTP = 36;
 
@@ -1489,10 +1490,12 @@ __global__ void __launch_bounds__(kVT, 1) chain_viterbi_warp_kernel(
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(th + (size_t)t * 1024 + r * 32 + c4));
       }
     } else {
-      const int r = tid >> 5, c = tid & 31;
-      if (r < m && c < m) {
-        const unsigned dst = (unsigned)__cvta_generic_to_shared(tile + r * kVTP + c);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(th + (size_t)t * mm + r * m + c));
+      for (int e = tid; e < 1024; e += kVT) {
+        const int r = e >> 5, c = e & 31;
+        if (r < m && c < m) {
+          const unsigned dst = (unsigned)__cvta_generic_to_shared(tile + r * kVTP + c);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(th + (size_t)t * mm + r * m + c));
+        }
       }
     }
   };
@@ -1506,26 +1509,29 @@ __global__ void __launch_bounds__(kVT, 1) chain_viterbi_warp_kernel(
     bad |= (tid < m) && bad_input(x);
     sv[tid] = tid < m ? (double)x : ninfd();
   }
-  const bool wlive = warp < m, alive = lane < m;
+  const bool alive = lane < m;
+  const int b0 = 2 * warp;
   for (int t = 0; t < T; ++t) {
     cpa_wait_d();
     __syncthreads();  // tile t resident; s_t published
     const double* cur = sv + (t & 1) * 32;
     double* nxt = sv + ((t + 1) & 1) * 32;
-    const float x = ring[(t % kVD) * 32 * kVTP + lane * kVTP + warp];
+    const float2 x = *reinterpret_cast<const float2*>(ring + (t % kVD) * 32 * kVTP + lane * kVTP + b0);
     const double sa = cur[lane];
     if (t + kVD < T) stage(t + kVD);
     cpa_commit();
-    if (wlive) {
-      bad |= alive && bad_input(x);
-      const double v = alive ? sa + (double)x : ninfd();
-      const int win = warp_argmax_key(dkey(v));
-      if (lane == win) {
-        nxt[warp] = v;
-        back[(size_t)(t + 1) * 32 + warp] = (uint8_t)win;
-      }
-    } else if (lane == 0) {
-      nxt[warp] = ninfd();
+    bad |= alive && ((b0 < m && bad_input(x.x)) | (b0 + 1 < m && bad_input(x.y)));
+    const double v0 = (alive && b0 < m) ? sa + (double)x.x : ninfd();
+    const double v1 = (alive && b0 + 1 < m) ? sa + (double)x.y : ninfd();
+    const int w0 = warp_argmax_key(dkey(v0));
+    const int w1 = warp_argmax_key(dkey(v1));
+    if (lane == w0) {
+      nxt[b0] = v0;
+      back[(size_t)(t + 1) * 32 + b0] = (uint8_t)w0;
+    }
+    if (lane == w1) {
+      nxt[b0 + 1] = v1;
+      back[(size_t)(t + 1) * 32 + b0 + 1] = (uint8_t)w1;
     }
   }
   asm volatile("cp.async.wait_group 0;\n" ::);
