@@ -285,6 +285,18 @@ int sdb_pcfg_sample(const float* root, const float* rules, const float* emission
                     int8_t* span_mask, int32_t* used, int32_t* status, void* workspace, size_t ws_bytes,
                     void* stream);
 
+/* ---- ragged chain batches (per-instance lengths) -----------------------------
+ * Replaces batch_map over chains of different lengths (dist.py:355-361) without
+ * pad_chain (chain.py:161-176): init [B][m], trans [B][n-1][m][m] in the batch
+ * layout, instance b uses its first lengths[b] positions (1 <= lengths[b] <= n);
+ * marginals / tags past them are 0.  m <= 32 and n <= 193 (else
+ * SDB_ERR_UNSUPPORTED: pad on the host instead).  Workspace as sdb_chain_fb. */
+int sdb_chain_fb_lengths(const float* init, const float* trans, const int32_t* lengths, int64_t B, int32_t n,
+                         int32_t m, double* logz, float* marg_init, float* marg_trans, int32_t* status,
+                         void* workspace, size_t ws_bytes, void* stream);
+int sdb_chain_viterbi_lengths(const float* init, const float* trans, const int32_t* lengths, int64_t B, int32_t n,
+                              int32_t m, int32_t* tags, double* score, int32_t* status, void* stream);
+
 /* ---- derived quantities: expected score under a potential tensor ------------
  * Replaces dist.py:306-347's host reduction _expected_score_under (masked_dot,
  * numerics.py:171-183) for cross_entropy / entropy / kl_divergence: out[b] +=

@@ -73,6 +73,9 @@ SIGNATURES = {
                                              _c_p, _sz, _c_p]),
     "sdb_pcfg_sample": (ctypes.c_int, [_c_p, _c_p, _c_p, _c_p, _i64, _i32, _i32, _i32, _c_p, _i64, _i32, _c_p, _c_p,
                                        _c_p, _c_p, _sz, _c_p]),
+    "sdb_chain_fb_lengths": (ctypes.c_int, [_c_p, _c_p, _c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p, _sz,
+                                            _c_p]),
+    "sdb_chain_viterbi_lengths": (ctypes.c_int, [_c_p, _c_p, _c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p]),
     "sdb_masked_dot": (ctypes.c_int, [_c_p, _c_p, _i64, _i64, _c_p, _c_p, _c_p]),
     "sdb_semimarkov_fb": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p]),
     "sdb_semimarkov_viterbi_workspace": (_sz, [_i64, _i32, _i32, _i32]),

@@ -147,22 +147,32 @@ class ChainBackend(Backend):
         return "viterbi"
 
     def _stack(self, ds):
-        return to_dev([d.init for d in ds]), to_dev([d.transitions for d in ds])
+        """Same-length group -> ([B,m], [B,n-1,m,m], None); a ragged group (dist.batch_map
+        with per-instance lengths) -> zero-padded layout + lengths [B] for the kernels."""
+        ns = [d.n for d in ds]
+        if len(set(ns)) == 1:
+            return to_dev([d.init for d in ds]), to_dev([d.transitions for d in ds]), None
+        n, m = max(ns), ds[0].m
+        tr = np.zeros((len(ds), n - 1, m, m))
+        for i, d in enumerate(ds):
+            tr[i, : d.n - 1] = d.transitions
+        lengths = torch.as_tensor(ns, dtype=torch.int32).to(_device())
+        return to_dev([d.init for d in ds]), to_dev(list(tr)), lengths
 
     def run(self, ds, marginals=True, full=False, dev=False):
-        init, trans = self._stack(ds)
-        logz, mi, mt, st = K.chain_fb(init, trans, marginals)
+        init, trans, lengths = self._stack(ds)
+        logz, mi, mt, st = K.chain_fb(init, trans, marginals, lengths)
         marg = None
-        if marginals and dev:
+        if marginals and dev and lengths is None:
             return Result(to_host(logz), to_host(st), None, self.vacuous_msg, dev={"init": mi, "transitions": mt})
         if marginals:
             mi, mt = to_host(mi).astype(np.float64), to_host(mt).astype(np.float64)
-            marg = [{"init": mi[i], "transitions": mt[i]} for i in range(len(ds))]
+            marg = [{"init": mi[i], "transitions": mt[i, : d.n - 1]} for i, d in enumerate(ds)]
         return Result(to_host(logz), to_host(st), marg, self.vacuous_msg)
 
     def argmax(self, ds):
-        init, trans = self._stack(ds)
-        tags, score, st = K.chain_viterbi(init, trans)
+        init, trans, lengths = self._stack(ds)
+        tags, score, st = K.chain_viterbi(init, trans, lengths)
         tags = to_host(tags)
 
         def build(i):
@@ -171,13 +181,14 @@ class ChainBackend(Backend):
             ind_i[tags[i, 0]] = 1.0
             ind_t = np.zeros_like(d.transitions)
             t = np.arange(d.n - 1)
-            ind_t[t, tags[i, :-1], tags[i, 1:]] = 1.0
+            ti = tags[i, : d.n]  # (ragged groups: the tags past this instance's length are padding)
+            ind_t[t, ti[:-1], ti[1:]] = 1.0
             return {"init": ind_i, "transitions": ind_t}
 
         return ArgmaxResult(to_host(st), build, self.vacuous_msg)
 
     def sample(self, ds, seeds, num):
-        init, trans = self._stack(ds)
+        init, trans, _ = self._stack(ds)
         d0 = ds[0]
         noise = self._noise(seeds, K.stream_len("chain", dict(n=d0.n, m=d0.m)), num)
         tags, _, st = K.chain_sample(init, trans, noise, num)

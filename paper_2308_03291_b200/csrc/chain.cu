@@ -256,7 +256,9 @@ __device__ __forceinline__ void stage_step(float* dst, const float* src, int mm,
 // formed from the stored normalised vectors by marg_steps().  `sm` >= kD*m*m + (32 + 2*kGroups*32) floats.
 __device__ void small_pass(const float* __restrict__ init, const float* __restrict__ trans, int n, int m,
                            const ChainWs& ws, double* __restrict__ logz, int32_t* __restrict__ status, int b,
-                           bool fwd, float* sm) {
+                           bool fwd, float* sm, int nl = -1) {
+  // n: this instance's length; nl: the layout length of the batch (strides), >= n
+  if (nl < 0) nl = n;
   const int mm = m * m;
   float* stage = sm;                     // [kD][mm]
   float* vec = stage + kD * mm;          // [32]
@@ -264,7 +266,7 @@ __device__ void small_pass(const float* __restrict__ init, const float* __restri
   float* ps = pm + kGroups * 32;         // [kGroups][32]
   __shared__ int redi[kThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const float* th = trans + (size_t)b * (n - 1) * mm;
+  const float* th = trans + (size_t)b * (nl - 1) * mm;
   const bool v16 = ((mm & 3) == 0);
   int bad = 0;
   // prologue prefetch: steps in processing order
@@ -274,8 +276,8 @@ __device__ void small_pass(const float* __restrict__ init, const float* __restri
     cpa_commit();
   }
   if (fwd) {
-    float* al = ws.alpha + (size_t)b * n * m;
-    double* ac = ws.acum + (size_t)b * n;
+    float* al = ws.alpha + (size_t)b * nl * m;
+    double* ac = ws.acum + (size_t)b * nl;
     double A = 0.0;
     bool vac = false;
     if (warp == 0) {
@@ -346,8 +348,8 @@ __device__ void small_pass(const float* __restrict__ init, const float* __restri
       }
     }
   } else {
-    float* be = ws.beta + (size_t)b * n * m;
-    double* bc = ws.bcum + (size_t)b * n;
+    float* be = ws.beta + (size_t)b * nl * m;
+    double* bc = ws.bcum + (size_t)b * nl;
     double Bc = 0.0;
     if (warp == 0 && lane < m) {
       vec[lane] = 0.f;
@@ -1066,17 +1068,19 @@ template <bool kFull>  // kFull: m == 32 (bulk TMA staging); else padded element
 __global__ void __launch_bounds__(kThreads, 2) chain_scan_kernel(
     const float* __restrict__ init, const float* __restrict__ trans, int n, int m, ChainWs ws,
     double* __restrict__ logz, float* __restrict__ marg_init, float* __restrict__ marg_trans,
-    int32_t* __restrict__ status) {
+    int32_t* __restrict__ status, const int32_t* __restrict__ lengths) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) char smscan[];
-  const int T = n - 1, L = (T + kSC - 1) / kSC;
+  // per-instance length (ragged batches, chain.py:161-176 without padding): this instance
+  // has T = lengths[b] - 1 steps; the arrays keep the batch layout of Tl = n - 1 steps
+  const int b = blockIdx.x / kSC;
+  const int Tl = n - 1, T = lengths ? min(max(lengths[b], 1), n) - 1 : Tl, L = (T + kSC - 1) / kSC;
   ScanSmem S = scan_carve(smscan, L);
   const int c = (int)cluster.block_rank();
-  const int b = blockIdx.x / kSC;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int t0 = min(T, c * L), t1 = min(T, t0 + L), Lc = t1 - t0;
-  const float* th = trans + ((size_t)b * T + t0) * (size_t)(m * m);
+  const float* th = trans + ((size_t)b * Tl + t0) * (size_t)(m * m);
   const float LN2 = 0.6931471805599453f;
 
   SCAN_TS(0);
@@ -1400,7 +1404,11 @@ __global__ void __launch_bounds__(kThreads, 2) chain_scan_kernel(
     marg_init[(size_t)b * m + tid] = (float)((double)(S.al[tid] * S.be[tid]) * exp(K));
   }
   if (marg_trans) {
-    float* out = marg_trans + ((size_t)b * T + t0) * (size_t)(m * m);
+    // steps past this instance's length: marginal 0
+    for (size_t e = (size_t)T * m * m + (size_t)c * kThreads + tid; e < (size_t)Tl * m * m;
+         e += (size_t)kSC * kThreads)
+      marg_trans[(size_t)b * Tl * m * m + e] = 0.f;
+    float* out = marg_trans + ((size_t)b * Tl + t0) * (size_t)(m * m);
     if (kFull) {
       const int a = tid >> 3, g = tid & 7;
       for (int k = 0; k < Lc; ++k) {
@@ -1432,11 +1440,14 @@ fallback:
   __syncthreads();
   {
     float* sm = reinterpret_cast<float*>(smscan);
-    small_pass(init, trans, n, m, ws, logz, status, b, true, sm);
+    small_pass(init, trans, T + 1, m, ws, logz, status, b, true, sm, n);
     __syncthreads();
-    small_pass(init, trans, n, m, ws, logz, status, b, false, sm);
+    small_pass(init, trans, T + 1, m, ws, logz, status, b, false, sm, n);
     __syncthreads();
     marg_steps(init, trans, n, m, ws, logz, marg_init, marg_trans, b, 0, T, true);
+    if (marg_trans)
+      for (size_t e = (size_t)T * m * m + tid; e < (size_t)Tl * m * m; e += kThreads)
+        marg_trans[(size_t)b * Tl * m * m + e] = 0.f;
   }
 }
 
@@ -1472,14 +1483,16 @@ __device__ __forceinline__ int warp_argmax_key(uint64_t k) {
 
 __global__ void __launch_bounds__(kVT, 1) chain_viterbi_warp_kernel(
     const float* __restrict__ init, const float* __restrict__ trans, int n, int m, int32_t* __restrict__ tags,
-    double* __restrict__ score, int32_t* __restrict__ status) {
+    double* __restrict__ score, int32_t* __restrict__ status, const int32_t* __restrict__ lengths) {
   extern __shared__ __align__(16) float smw[];
   float* ring = smw;                                                       // [kVD][32][kVTP]
   double* sv = reinterpret_cast<double*>(ring + kVD * 32 * kVTP);          // [2][32]
   uint8_t* back = reinterpret_cast<uint8_t*>(sv + 64);                     // [n][32]
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int T = n - 1, mm = m * m;
-  const float* th = trans + (size_t)b * T * mm;
+  const int nl = n, mm = m * m;  // nl: layout length; n: this instance's length (ragged batches)
+  n = lengths ? min(max(lengths[b], 1), nl) : nl;
+  const int T = n - 1;
+  const float* th = trans + (size_t)b * (nl - 1) * mm;
   const bool full = (m == 32) && ((((uintptr_t)th) & 15) == 0);
   auto stage = [&](int t) {
     float* tile = ring + (t % kVD) * 32 * kVTP;
@@ -1541,8 +1554,9 @@ __global__ void __launch_bounds__(kVT, 1) chain_viterbi_warp_kernel(
     const double v = alive ? fin[lane] : ninfd();
     const int win = warp_argmax_key(dkey(v));  // final tag: first argmax (chain.py:111)
     const double best = __shfl_sync(0xffffffffu, v, win);
+    int32_t* tg = tags + (size_t)b * nl;
+    for (int t = n + lane; t < nl; t += 32) tg[t] = 0;  // past this instance's length
     if (lane == 0) {
-      int32_t* tg = tags + (size_t)b * n;
       const bool vac = (best == ninfd());
       status[b] = bad ? SDB_ST_INVALID : (vac ? SDB_ST_VACUOUS : SDB_ST_OK);
       score[b] = best;
@@ -1606,7 +1620,8 @@ extern "C" int sdb_chain_fb(const float* init, const float* trans, int64_t B, in
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, kern, init, trans, n, m, ws, logz, marg_init, marg_trans, status) != cudaSuccess)
+    if (cudaLaunchKernelEx(&cfg, kern, init, trans, n, m, ws, logz, marg_init, marg_trans, status,
+                           (const int32_t*)nullptr) != cudaSuccess)
       return SDB_ERR_CUDA;
     SDB_CHECK_LAUNCH();
     return SDB_OK;
@@ -1661,6 +1676,60 @@ extern "C" int sdb_chain_fb(const float* init, const float* trans, int64_t B, in
   return SDB_OK;
 }
 
+// Ragged batches (per-instance lengths, no padding compute; chain.py:161-176 semantics
+// without pad_chain): the arrays keep the batch layout of n positions, instance b uses
+// its first lengths[b] (1 <= lengths[b] <= n); marginals / tags past it are 0.
+// Served by the scan and Viterbi kernels: m <= 32, n <= kSC * kSLmax + 1.
+extern "C" int sdb_chain_fb_lengths(const float* init, const float* trans, const int32_t* lengths, int64_t B,
+                                    int32_t n, int32_t m, double* logz, float* marg_init, float* marg_trans,
+                                    int32_t* status, void* workspace, size_t ws_bytes, void* stream) {
+  if (B < 0 || n < 1 || m < 1 || !init || (n > 1 && !trans) || !lengths || !logz || !status) return SDB_ERR_ARG;
+  if (m > 32 || (n - 1 + kSC - 1) / kSC > kSLmax) return SDB_ERR_UNSUPPORTED;
+  if (B == 0) return SDB_OK;
+  size_t need = 0;
+  ChainWs ws = carve_chain(workspace, B, n, m, &need);
+  if (!workspace || ws_bytes < need) return SDB_ERR_WORKSPACE;
+  const int T = n - 1;
+  const size_t smem = scan_smem((T + kSC - 1) / kSC);
+  auto kern = (m == 32) ? chain_scan_kernel<true> : chain_scan_kernel<false>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return SDB_ERR_CUDA;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(B * kSC));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kSC;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, init, trans, n, m, ws, logz, marg_init, marg_trans, status, lengths) !=
+      cudaSuccess)
+    return SDB_ERR_CUDA;
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
+extern "C" int sdb_chain_viterbi_lengths(const float* init, const float* trans, const int32_t* lengths, int64_t B,
+                                         int32_t n, int32_t m, int32_t* tags, double* score, int32_t* status,
+                                         void* stream) {
+  if (B < 0 || n < 1 || m < 1 || !init || (n > 1 && !trans) || !lengths || !tags || !score || !status)
+    return SDB_ERR_ARG;
+  const size_t smw = (size_t)kVD * 32 * kVTP * 4 + 64 * 8 + (size_t)n * 32 + 64;
+  if (m > 32 || smw > 200 * 1024) return SDB_ERR_UNSUPPORTED;
+  if (B == 0) return SDB_OK;
+  if (cudaFuncSetAttribute(chain_viterbi_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw) !=
+      cudaSuccess)
+    return SDB_ERR_CUDA;
+  chain_viterbi_warp_kernel<<<(unsigned)B, kVT, smw, (cudaStream_t)stream>>>(init, trans, n, m, tags, score, status,
+                                                                           lengths);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
 extern "C" size_t sdb_chain_viterbi_workspace(int64_t B, int32_t n, int32_t m) {
   if (viterbi_smem(n, m, true) <= 160 * 1024) return 256;
   return (size_t)B * n * m * sizeof(uint16_t) + 256;
@@ -1680,7 +1749,7 @@ extern "C" int sdb_chain_viterbi(const float* init, const float* trans, int64_t 
           cudaSuccess)
         return SDB_ERR_CUDA;
       chain_viterbi_warp_kernel<<<(unsigned)B, kVT, smw, (cudaStream_t)stream>>>(init, trans, n, m, tags, score,
-                                                                               status);
+                                                                               status, nullptr);
       SDB_CHECK_LAUNCH();
       return SDB_OK;
     }

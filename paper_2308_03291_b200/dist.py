@@ -297,7 +297,9 @@ def batch_map(op, dists, *args, ragged: bool = True, **kwargs) -> list:
     for key, idx in groups.items():
         group = [dists[i] for i in idx]
         be = _backend(group[0])
-        if key[0] == "ragged":
+        if key[0] == "ragged" and rg.native_ragged(group):  # the kernels take per-instance lengths
+            res = _BATCHED[name](be, group)
+        elif key[0] == "ragged":
             padded = rg.pad_group(group)
             res = _BATCHED[name](be, padded)
             res = [_unpad_result(name, d, p, r) for d, p, r in zip(group, padded, res)]

@@ -50,9 +50,11 @@ def workspace(nbytes: int, device) -> torch.Tensor:
 # ----------------------------------------------------------------- chain
 
 
-def chain_fb(init, trans, marginals: bool = True):
+def chain_fb(init, trans, marginals: bool = True, lengths=None):
     """chain.py:64-95 batched: init [B,m], trans [B,n-1,m,m] ->
-    (logz [B] f64, marg_init [B,m] | None, marg_trans | None, status [B])."""
+    (logz [B] f64, marg_init [B,m] | None, marg_trans | None, status [B]).
+    `lengths` [B] int32 (optional): ragged batch, instance b uses its first
+    lengths[b] positions (sdb_chain_fb_lengths; marginals past them are 0)."""
     lib = _lib.load()
     init, trans = f32(init, "init"), f32(trans, "transitions")
     B, m = init.shape
@@ -64,14 +66,26 @@ def chain_fb(init, trans, marginals: bool = True):
     mt = torch.empty_like(trans) if marginals else None
     wsb = lib.sdb_chain_fb_workspace(B, n, m)
     ws = workspace(wsb, dev)
+    if lengths is not None:
+        lengths = i32(lengths, "lengths")
+        rc = lib.sdb_chain_fb_lengths(ptr(init), ptr(trans), ptr(lengths), B, n, m, ptr(logz), ptr(mi), ptr(mt),
+                                      ptr(status), ptr(ws), ws.numel(), stream_ptr(dev))
+        _lib.check(rc, "sdb_chain_fb_lengths")
+        return logz, mi, mt, status
     rc = lib.sdb_chain_fb(ptr(init), ptr(trans), B, n, m, ptr(logz), ptr(mi), ptr(mt), ptr(status),
                           ptr(ws), ws.numel(), stream_ptr(dev))
     _lib.check(rc, "sdb_chain_fb")
     return logz, mi, mt, status
 
 
-def chain_viterbi(init, trans):
-    """chain.py:98-114 batched -> (tags [B,n] int32, score [B] f64, status)."""
+def chain_ragged_supported(n: int, m: int) -> bool:
+    """Shapes the per-instance-length chain kernels serve (else pad on the host)."""
+    return m <= 32 and (n - 1 + 7) // 8 <= 24
+
+
+def chain_viterbi(init, trans, lengths=None):
+    """chain.py:98-114 batched -> (tags [B,n] int32, score [B] f64, status);
+    `lengths` as in chain_fb (tags past an instance's length are 0)."""
     lib = _lib.load()
     init, trans = f32(init, "init"), f32(trans, "transitions")
     B, m = init.shape
@@ -80,6 +94,12 @@ def chain_viterbi(init, trans):
     tags = torch.empty(B, n, dtype=torch.int32, device=dev)
     score = torch.empty(B, dtype=torch.float64, device=dev)
     status = torch.empty(B, dtype=torch.int32, device=dev)
+    if lengths is not None:
+        lengths = i32(lengths, "lengths")
+        rc = lib.sdb_chain_viterbi_lengths(ptr(init), ptr(trans), ptr(lengths), B, n, m, ptr(tags), ptr(score),
+                                           ptr(status), stream_ptr(dev))
+        _lib.check(rc, "sdb_chain_viterbi_lengths")
+        return tags, score, status
     ws = workspace(lib.sdb_chain_viterbi_workspace(B, n, m), dev)
     rc = lib.sdb_chain_viterbi(ptr(init), ptr(trans), B, n, m, ptr(tags), ptr(score), ptr(status),
                                ptr(ws), ws.numel(), stream_ptr(dev))

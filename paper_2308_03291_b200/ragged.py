@@ -198,6 +198,16 @@ def group_key(d):
     return (type(d), RAGGED[type(d)][0](d))
 
 
+def native_ragged(ds) -> bool:
+    """Groups the kernels serve WITHOUT padding, through per-instance lengths
+    (chains: sdb_chain_fb_lengths / sdb_chain_viterbi_lengths)."""
+    if not isinstance(ds[0], LinearChainCRF) or not needs_padding(ds):
+        return False
+    from .kernels import chain_ragged_supported
+
+    return chain_ragged_supported(max(d.n for d in ds), ds[0].m)
+
+
 def needs_padding(ds) -> bool:
     _, size, _, _, _ = RAGGED[type(ds[0])]
     return len({size(d) for d in ds}) > 1

@@ -3,6 +3,7 @@ launch per group through inference-neutral padding and match the
 per-instance results (log Z, marginals, argmax)."""
 
 import numpy as np
+import torch
 import pytest
 
 import paper_2308_03291_b200 as sd
@@ -94,3 +95,32 @@ def test_batch_map_pcfg_full_grammar():
     got = sd.batch_map(sd.marginals, mixed)
     for d, m in zip(mixed, got):
         np.testing.assert_allclose(m["sticky"], sd.marginals(d)["sticky"], rtol=1e-5, atol=1e-7)
+
+
+def test_ragged_chain_native_lengths():
+    """Chains of different lengths run through the per-instance-length kernels
+    (no padding compute): log Z, marginals and Viterbi equal the per-instance
+    calls; the kernel zeroes marginals / tags past each instance's length."""
+    need_gpu()
+    from paper_2308_03291_b200 import kernels as K
+    from paper_2308_03291_b200 import ragged as rg
+
+    dists = [sd.LinearChainCRF(*chain(70 + s, n, 5)) for s, n in enumerate([3, 40, 17, 1, 64, 2])]
+    assert rg.native_ragged(dists)
+    _check(dists)
+    am = sd.batch_map(sd.argmax_info, dists)
+    for d, (ind, score, algo) in zip(dists, am):
+        ind0, score0, algo0 = sd.argmax_info(d)
+        for k in ind0:
+            np.testing.assert_array_equal(ind[k], ind0[k])
+        assert score == score0 and algo == algo0
+    # raw kernel contract: zeros past the length
+    init = torch.stack([torch.as_tensor(d.init, dtype=torch.float32) for d in dists]).cuda()
+    tr = torch.zeros(len(dists), 63, 5, 5)
+    for i, d in enumerate(dists):
+        tr[i, : d.n - 1] = torch.as_tensor(d.transitions, dtype=torch.float32)
+    lens = torch.tensor([d.n for d in dists], dtype=torch.int32).cuda()
+    lz, mi, mt, st = K.chain_fb(init, tr.cuda(), True, lens)
+    tags, score, st2 = K.chain_viterbi(init, tr.cuda(), lens)
+    for i, d in enumerate(dists):
+        assert (mt[i, d.n - 1:] == 0).all() and (tags[i, d.n:] == 0).all()
