@@ -1111,7 +1111,7 @@ int nw_launch(const float* theta, int64_t B, int n, int m, NwWs ws, double* logz
   const int NW = (m + 1 + 31) / 32;
   const size_t smem = nw_smem_bytes(NW);
   if (kMode == 2) {
-    if (cudaFuncSetAttribute(nw_max_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (sdb_set_smem((const void*)nw_max_kernel, smem) != cudaSuccess)
       return SDB_ERR_CUDA;
     nw_max_kernel<<<(unsigned)B, 32 * NW, smem, s>>>(theta, n, m, ws.choice, score, status);
     SDB_CHECK_LAUNCH();
@@ -1121,14 +1121,14 @@ int nw_launch(const float* theta, int64_t B, int n, int m, NwWs ws, double* logz
   }
   if (kMode == 1 && ws.wsa2) {
     const size_t sm2 = mitm_smem_bytes(NW);
-    if (cudaFuncSetAttribute(nw_mitm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2) != cudaSuccess)
+    if (sdb_set_smem((const void*)nw_mitm_kernel, sm2) != cudaSuccess)
       return SDB_ERR_CUDA;
     nw_mitm_kernel<<<(unsigned)B, 64 * NW, sm2, s>>>(theta, n, m, ws.wsa2, ws.wsb2, logz, marg, status);
     SDB_CHECK_LAUNCH();
     return SDB_OK;
   }
   constexpr int M2 = kMode == 1 ? 1 : 0;
-  if (cudaFuncSetAttribute(nw_kernel<M2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+  if (sdb_set_smem((const void*)nw_kernel<M2>, smem) != cudaSuccess)
     return SDB_ERR_CUDA;
   nw_kernel<M2><<<(unsigned)B, 32 * NW, smem, s>>>(theta, n, m, ws.wsb, ws.wsk, logz, marg, status);
   SDB_CHECK_LAUNCH();

@@ -1606,7 +1606,7 @@ extern "C" int sdb_chain_fb(const float* init, const float* trans, int64_t B, in
     // time-parallel scan: one cluster of kSC CTAs per instance, one launch
     const size_t smem = scan_smem((T + kSC - 1) / kSC);
     auto kern = (m == 32) ? chain_scan_kernel<true> : chain_scan_kernel<false>;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (sdb_set_smem((const void*)kern, smem) != cudaSuccess)
       return SDB_ERR_CUDA;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(B * kSC));
@@ -1630,7 +1630,7 @@ extern "C" int sdb_chain_fb(const float* init, const float* trans, int64_t B, in
   const size_t small_smem = (size_t)kD * m * m * 4 + (32 + 2 * kGroups * 32) * 4;
   if (lin) {
     const size_t smem = lin_smem_bytes();
-    if (cudaFuncSetAttribute(chain_lin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (sdb_set_smem((const void*)chain_lin_kernel, smem) != cudaSuccess)
       return SDB_ERR_CUDA;
     chain_lin_kernel<<<(unsigned)(2 * B), kThreads, smem, s>>>(init, trans, n, m, ws, logz, status);
     SDB_CHECK_LAUNCH();
@@ -1640,8 +1640,7 @@ extern "C" int sdb_chain_fb(const float* init, const float* trans, int64_t B, in
     dim3 g((unsigned)((n - 1 + kStepsPerBlock - 1) / kStepsPerBlock), (unsigned)B);
     SDB_CHECK_LAUNCH();
     // exact log-space recomputation of the (rare) instances the linear path flagged
-    if (cudaFuncSetAttribute(chain_fwd_bwd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)small_smem) != cudaSuccess)
+    if (sdb_set_smem((const void*)chain_fwd_bwd_small_kernel, small_smem) != cudaSuccess)
       return SDB_ERR_CUDA;
     chain_fwd_bwd_small_kernel<<<dim3((unsigned)B, 2), kThreads, small_smem, s>>>(init, trans, n, m, ws, logz,
                                                                                   status, 1);
@@ -1653,15 +1652,14 @@ extern "C" int sdb_chain_fb(const float* init, const float* trans, int64_t B, in
     return SDB_OK;
   }
   if (m <= 32) {
-    if (cudaFuncSetAttribute(chain_fwd_bwd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)small_smem) != cudaSuccess)
+    if (sdb_set_smem((const void*)chain_fwd_bwd_small_kernel, small_smem) != cudaSuccess)
       return SDB_ERR_CUDA;
     chain_fwd_bwd_small_kernel<<<dim3((unsigned)B, 2), kThreads, small_smem, s>>>(init, trans, n, m, ws, logz,
                                                                                   status, 0);
   } else {
     size_t smem = (size_t)m * 4 * (1 + 2 * kGroups);
     if (smem > 48 * 1024) {
-      if (cudaFuncSetAttribute(chain_fwd_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      if (sdb_set_smem((const void*)chain_fwd_bwd_kernel, smem) !=
           cudaSuccess)
         return SDB_ERR_CUDA;
     }
@@ -1692,7 +1690,7 @@ extern "C" int sdb_chain_fb_lengths(const float* init, const float* trans, const
   const int T = n - 1;
   const size_t smem = scan_smem((T + kSC - 1) / kSC);
   auto kern = (m == 32) ? chain_scan_kernel<true> : chain_scan_kernel<false>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+  if (sdb_set_smem((const void*)kern, smem) != cudaSuccess)
     return SDB_ERR_CUDA;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(B * kSC));
@@ -1721,7 +1719,7 @@ extern "C" int sdb_chain_viterbi_lengths(const float* init, const float* trans, 
   const size_t smw = (size_t)kVD * 32 * kVTP * 4 + 64 * 8 + (size_t)n * 32 + 64;
   if (m > 32 || smw > 200 * 1024) return SDB_ERR_UNSUPPORTED;
   if (B == 0) return SDB_OK;
-  if (cudaFuncSetAttribute(chain_viterbi_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw) !=
+  if (sdb_set_smem((const void*)chain_viterbi_warp_kernel, smw) !=
       cudaSuccess)
     return SDB_ERR_CUDA;
   chain_viterbi_warp_kernel<<<(unsigned)B, kVT, smw, (cudaStream_t)stream>>>(init, trans, n, m, tags, score, status,
@@ -1745,7 +1743,7 @@ extern "C" int sdb_chain_viterbi(const float* init, const float* trans, int64_t 
   if (m <= 32) {
     const size_t smw = (size_t)kVD * 32 * kVTP * 4 + 64 * 8 + (size_t)n * 32 + 64;  // ring, scores, backpointers
     if (smw <= 200 * 1024) {
-      if (cudaFuncSetAttribute(chain_viterbi_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw) !=
+      if (sdb_set_smem((const void*)chain_viterbi_warp_kernel, smw) !=
           cudaSuccess)
         return SDB_ERR_CUDA;
       chain_viterbi_warp_kernel<<<(unsigned)B, kVT, smw, (cudaStream_t)stream>>>(init, trans, n, m, tags, score,
@@ -1755,7 +1753,7 @@ extern "C" int sdb_chain_viterbi(const float* init, const float* trans, int64_t 
     }
     const size_t smem = (size_t)(kD + 1) * m * kVP * 4 + 64 * 8 + (size_t)n * 32 + 64;
     if (smem <= 200 * 1024) {
-      if (cudaFuncSetAttribute(chain_viterbi_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      if (sdb_set_smem((const void*)chain_viterbi_small_kernel, smem) !=
           cudaSuccess)
         return SDB_ERR_CUDA;
       chain_viterbi_small_kernel<<<(unsigned)B, kThreads, smem, (cudaStream_t)stream>>>(init, trans, n, m, tags,
@@ -1767,7 +1765,7 @@ extern "C" int sdb_chain_viterbi(const float* init, const float* trans, int64_t 
   const bool in_smem = viterbi_smem(n, m, true) <= 160 * 1024;
   size_t smem = viterbi_smem(n, m, in_smem);
   if (smem > 48 * 1024) {
-    if (cudaFuncSetAttribute(chain_viterbi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (sdb_set_smem((const void*)chain_viterbi_kernel, smem) != cudaSuccess)
       return SDB_ERR_CUDA;
   }
   chain_viterbi_kernel<<<(unsigned)B, kThreads, smem, (cudaStream_t)stream>>>(

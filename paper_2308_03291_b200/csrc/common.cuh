@@ -12,6 +12,10 @@
 #include <stdint.h>
 #include <math.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "../../include/sdb200.h"
 
 #define SDB_LOG2E 1.4426950408889634f
@@ -148,6 +152,21 @@ struct Carve {
     return p ? (T*)(p + off) : nullptr;
   }
 };
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel):
+// the runtime call costs microseconds of host time on every launch otherwise
+inline cudaError_t sdb_set_smem(const void* kern, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{dev, kern}];
+  if (have >= smem) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) have = smem;
+  return e;
+}
 
 #define SDB_CHECK_LAUNCH()                       \
   do {                                           \

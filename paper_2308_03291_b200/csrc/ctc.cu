@@ -482,13 +482,13 @@ int ctc_launch(const float* fp, const int32_t* tg, int64_t B, int T, int V, int 
   if constexpr (kMode == 1) {
     const size_t dsmem = ctc_dir_smem_bytes(S, V, L);
     if (dsmem > 48 * 1024 &&
-        cudaFuncSetAttribute(ctc_dir_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem) != cudaSuccess)
+        sdb_set_smem((const void*)ctc_dir_kernel, dsmem) != cudaSuccess)
       return SDB_ERR_CUDA;
     ctc_dir_kernel<<<dim3((unsigned)B, 2), threads, dsmem, s>>>(fp, tg, T, V, L, ws.wsa, ws.wsabase, ws.wsb,
                                                                 ws.wsbase, ws.csr, logz, status);
   } else {
     const size_t smem = ctc_smem_bytes(S, V, L);
-    if (cudaFuncSetAttribute(ctc_kernel<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (sdb_set_smem((const void*)ctc_kernel<kMode>, smem) != cudaSuccess)
       return SDB_ERR_CUDA;
     ctc_kernel<kMode><<<(unsigned)B, threads, smem, s>>>(fp, tg, T, V, L, ws.back, logz, path, score, status);
   }
@@ -499,14 +499,12 @@ int ctc_launch(const float* fp, const int32_t* tg, int64_t B, int T, int V, int 
     dim3 g((unsigned)((T + kMargFrames - 1) / kMargFrames), (unsigned)B);
     const int rr = (S2 + 31) / 32;
     if (rr <= 9) {
-      if (msmem > 48 * 1024 && cudaFuncSetAttribute(ctc_marg_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                    (int)msmem) != cudaSuccess)
+      if (msmem > 48 * 1024 && sdb_set_smem((const void*)ctc_marg_kernel<9>, msmem) != cudaSuccess)
         return SDB_ERR_CUDA;
       ctc_marg_kernel<9><<<g, kMargWarps * 32, msmem, s>>>(ws.wsa, ws.wsabase, ws.wsb, ws.wsbase, logz, ws.csr, T, V,
                                                           L, status, marg);
     } else {
-      if (msmem > 48 * 1024 && cudaFuncSetAttribute(ctc_marg_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                    (int)msmem) != cudaSuccess)
+      if (msmem > 48 * 1024 && sdb_set_smem((const void*)ctc_marg_kernel<32>, msmem) != cudaSuccess)
         return SDB_ERR_CUDA;
       ctc_marg_kernel<32><<<g, kMargWarps * 32, msmem, s>>>(ws.wsa, ws.wsabase, ws.wsb, ws.wsbase, logz, ws.csr, T,
                                                            V, L, status, marg);

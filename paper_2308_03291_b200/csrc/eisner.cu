@@ -711,9 +711,9 @@ extern "C" int sdb_eisner(const float* adjacency, int64_t B, int32_t n, int32_t 
   const size_t smem = eisner_smem(n);
   const size_t smem_lin = (size_t)7 * (n * (n + 1) / 2) * 4;  // the seven charts only
   cudaStream_t s = (cudaStream_t)stream;
-  if (cudaFuncSetAttribute(eisner_lin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_lin) !=
+  if (sdb_set_smem((const void*)eisner_lin_kernel, smem_lin) !=
           cudaSuccess ||
-      cudaFuncSetAttribute(eisner_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      sdb_set_smem((const void*)eisner_kernel, smem) != cudaSuccess)
     return SDB_ERR_CUDA;
   // exp-space first; the log-space kernel redoes only the instances it flagged
   eisner_lin_kernel<<<(unsigned)B, kThreads, smem_lin, s>>>(adjacency, n, single_root ? 1 : 0, logz, marg, status);
@@ -730,7 +730,7 @@ extern "C" int sdb_kuhlmann(const float* adjacency, int64_t B, int32_t n, int32_
   if (!adjacency || !heads || !score || !status) return SDB_ERR_ARG;
   if (B == 0) return SDB_OK;
   const size_t smem = kuhl_smem(n);
-  if (cudaFuncSetAttribute(kuhlmann_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+  if (sdb_set_smem((const void*)kuhlmann_kernel, smem) != cudaSuccess)
     return SDB_ERR_CUDA;
   kuhlmann_kernel<<<(unsigned)B, kThreads, smem, (cudaStream_t)stream>>>(adjacency, n, single_root ? 1 : 0, heads,
                                                                          score, status);

@@ -509,8 +509,7 @@ template <typename T, bool kMarg, bool kPivot>
 int launch_mtt(const float* adjacency, int64_t B, int n, int sr, double* logz, float* marg, int32_t* status,
                cudaStream_t s) {
   const size_t smem = mtt_smem<T, kMarg>();
-  if (cudaFuncSetAttribute(mtt_kernel<T, kMarg, kPivot>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
+  if (sdb_set_smem((const void*)mtt_kernel<T, kMarg, kPivot>, smem) != cudaSuccess)
     return SDB_ERR_CUDA;
   mtt_kernel<T, kMarg, kPivot><<<(unsigned)B, kThreads, smem, s>>>(adjacency, n, sr, logz, marg, status);
   SDB_CHECK_LAUNCH();

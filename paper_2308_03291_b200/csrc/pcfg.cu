@@ -802,7 +802,7 @@ int pcfg_launch(const float* root, const float* rules, const float* emissions, c
   const size_t smem_in = (size_t)(3 * kBS * 1024 + kMaxN * 3 * kBS * 32 + (kMode == 2 ? kMaxN * 32 : 0)) * 4;
   const size_t smem_out = (size_t)(2 * 3 * kBS * 1024 + kCP * 32 + kCP * 3 * 32 * 33) * 4;
   const size_t smem = kMode == 0 ? smem_in : (smem_in > smem_out ? smem_in : smem_out);
-  if (cudaFuncSetAttribute(pcfg_kernel<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+  if (sdb_set_smem((const void*)pcfg_kernel<kMode>, smem) != cudaSuccess)
     return SDB_ERR_CUDA;
   pcfg_kernel<kMode><<<(unsigned)B, kThreads, smem, s>>>(root, rules, emissions, sticky, n, NT, PT, ws, logz,
                                                          span_marg, gout, status);
@@ -892,7 +892,7 @@ extern "C" int sdb_pcfg_viterbi(const float* root, const float* rules, const flo
   if (!workspace || ws_bytes < sdb_pcfg_viterbi_workspace(B, n, NT, PT)) return SDB_ERR_WORKSPACE;
   const size_t smem = max_smem(n, NT, PT);
   if (smem > 220 * 1024) return SDB_ERR_UNSUPPORTED;
-  if (cudaFuncSetAttribute(pcfg_max_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+  if (sdb_set_smem((const void*)pcfg_max_kernel<false>, smem) !=
       cudaSuccess)
     return SDB_ERR_CUDA;
   pcfg_max_kernel<false><<<(unsigned)B, kThreads, smem, (cudaStream_t)stream>>>(
@@ -916,7 +916,7 @@ extern "C" int sdb_pcfg_sample(const float* root, const float* rules, const floa
   if (!workspace || ws_bytes < sdb_pcfg_viterbi_workspace(B, n, NT, PT)) return SDB_ERR_WORKSPACE;
   const size_t smem = max_smem(n, NT, PT);
   if (smem > 220 * 1024) return SDB_ERR_UNSUPPORTED;
-  if (cudaFuncSetAttribute(pcfg_max_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+  if (sdb_set_smem((const void*)pcfg_max_kernel<true>, smem) !=
       cudaSuccess)
     return SDB_ERR_CUDA;
   pcfg_max_kernel<true><<<(unsigned)B, kThreads, smem, (cudaStream_t)stream>>>(

@@ -212,11 +212,11 @@ extern "C" int sdb_semimarkov_fb(const float* segment_potentials, int64_t B, int
   const size_t smem = sm_smem(n, m);
   cudaStream_t st = (cudaStream_t)stream;
   if (marg) {
-    if (cudaFuncSetAttribute(semimarkov_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (sdb_set_smem((const void*)semimarkov_kernel<1>, smem) != cudaSuccess)
       return SDB_ERR_CUDA;
     semimarkov_kernel<1><<<(unsigned)B, kThreads, smem, st>>>(segment_potentials, n, s, m, logz, marg, status);
   } else {
-    if (cudaFuncSetAttribute(semimarkov_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (sdb_set_smem((const void*)semimarkov_kernel<0>, smem) != cudaSuccess)
       return SDB_ERR_CUDA;
     semimarkov_kernel<0><<<(unsigned)B, kThreads, smem, st>>>(segment_potentials, n, s, m, logz, nullptr, status);
   }

@@ -660,7 +660,7 @@ template <int kMode>
 int tree_launch(const float* th, int64_t B, int n, int m, double* logz, float* marg, int32_t* labels, double* score,
                 int32_t* status, cudaStream_t s, int only_retry = 0) {
   const size_t smem = tree_smem(n);
-  if (cudaFuncSetAttribute(tree_kernel<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+  if (sdb_set_smem((const void*)tree_kernel<kMode>, smem) != cudaSuccess)
     return SDB_ERR_CUDA;
   tree_kernel<kMode><<<(unsigned)B, kThreads, smem, s>>>(th, n, m, logz, marg, labels, score, status, only_retry);
   SDB_CHECK_LAUNCH();
@@ -693,9 +693,9 @@ extern "C" int sdb_tree_fb(const float* span_potentials, int64_t B, int32_t n, i
   float* fold = c.take<float>((size_t)B * T);
   float* K = c.take<float>((size_t)B * T);
   const size_t smem_lin = (6 * T + 1) * sizeof(float);
-  if (cudaFuncSetAttribute(tree_lin_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_lin) !=
+  if (sdb_set_smem((const void*)tree_lin_kernel<true>, smem_lin) !=
           cudaSuccess ||
-      cudaFuncSetAttribute(tree_lin_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_lin) !=
+      sdb_set_smem((const void*)tree_lin_kernel<false>, smem_lin) !=
           cudaSuccess)
     return SDB_ERR_CUDA;
   const int64_t rows = B * n;

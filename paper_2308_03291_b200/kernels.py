@@ -83,9 +83,11 @@ def chain_ragged_supported(n: int, m: int) -> bool:
     return m <= 32 and (n - 1 + 7) // 8 <= 24
 
 
-def chain_viterbi(init, trans, lengths=None):
+def chain_viterbi(init, trans, lengths=None, stream=None):
     """chain.py:98-114 batched -> (tags [B,n] int32, score [B] f64, status);
-    `lengths` as in chain_fb (tags past an instance's length are 0)."""
+    `lengths` as in chain_fb (tags past an instance's length are 0).  `stream`:
+    launch there instead of the current stream (outputs are still allocated on
+    the current stream: see _concurrent)."""
     lib = _lib.load()
     init, trans = f32(init, "init"), f32(trans, "transitions")
     B, m = init.shape
@@ -97,12 +99,14 @@ def chain_viterbi(init, trans, lengths=None):
     if lengths is not None:
         lengths = i32(lengths, "lengths")
         rc = lib.sdb_chain_viterbi_lengths(ptr(init), ptr(trans), ptr(lengths), B, n, m, ptr(tags), ptr(score),
-                                           ptr(status), stream_ptr(dev))
+                                           ptr(status), stream.cuda_stream if stream else stream_ptr(dev))
         _lib.check(rc, "sdb_chain_viterbi_lengths")
         return tags, score, status
     ws = workspace(lib.sdb_chain_viterbi_workspace(B, n, m), dev)
+    if stream is not None:  # freed when this call returns: keep it out of reuse until the side work ends
+        ws.record_stream(stream)
     rc = lib.sdb_chain_viterbi(ptr(init), ptr(trans), B, n, m, ptr(tags), ptr(score), ptr(status),
-                               ptr(ws), ws.numel(), stream_ptr(dev))
+                               ptr(ws), ws.numel(), stream.cuda_stream if stream else stream_ptr(dev))
     _lib.check(rc, "sdb_chain_viterbi")
     return tags, score, status
 
@@ -117,21 +121,20 @@ def _side_stream(dev) -> torch.cuda.Stream:
     return s
 
 
-def _concurrent(dev, main, side, keep=()):
-    """Run `side()` on a side stream concurrently with `main()` on the current
-    stream (fork/join with stream waits).  Used where both halves of one
-    request are latency-bound launches with fewer CTAs than SMs, so they share
-    the GPU instead of queueing.  `keep` tensors are read by `side`."""
+def _concurrent(dev, main, side):
+    """Run `side(stream)` on a side stream concurrently with `main()` on the
+    current stream (fork/join: two stream waits).  Used where both halves of
+    one request are latency-bound launches with fewer CTAs than SMs, so they
+    share the GPU instead of queueing.  `side` allocates its outputs on the
+    CURRENT stream and only launches on the side stream; the join makes every
+    later use or free on the current stream ordered after the side work, so no
+    per-tensor record_stream bookkeeping is needed."""
     cur = torch.cuda.current_stream(dev)
     st = _side_stream(dev)
     st.wait_stream(cur)
-    with torch.cuda.stream(st):
-        rs = side()
+    rs = side(st)
     rm = main()
     cur.wait_stream(st)
-    for t in list(keep) + [x for x in rs if isinstance(x, torch.Tensor)]:
-        t.record_stream(st)
-        t.record_stream(cur)
     return rm, rs
 
 
@@ -141,8 +144,8 @@ def chain_fb_viterbi(init, trans, marginals: bool = True):
     the Viterbi kernel concurrently on a side stream (B CTAs each).
     -> ((logz, marg_init, marg_trans, status), (tags, score, status))."""
     init, trans = f32(init, "init"), f32(trans, "transitions")
-    return _concurrent(init.device, lambda: chain_fb(init, trans, marginals), lambda: chain_viterbi(init, trans),
-                       keep=(init, trans))
+    return _concurrent(init.device, lambda: chain_fb(init, trans, marginals),
+                       lambda st: chain_viterbi(init, trans, stream=st))
 
 
 # ------------------------------------------------------------- alignment
@@ -297,8 +300,9 @@ def eisner(adjacency, single_root: bool = False, marginals: bool = True):
     return logz, marg, status
 
 
-def kuhlmann(adjacency, single_root: bool = False):
-    """spanning.py:339-402 batched -> (heads [B,n+1] int32, score, status)."""
+def kuhlmann(adjacency, single_root: bool = False, stream=None):
+    """spanning.py:339-402 batched -> (heads [B,n+1] int32, score, status);
+    `stream` as in chain_viterbi."""
     lib = _lib.load()
     adj = f32(adjacency, "adjacency")
     B, n1, _ = adj.shape
@@ -307,7 +311,7 @@ def kuhlmann(adjacency, single_root: bool = False):
     score = torch.empty(B, dtype=torch.float64, device=dev)
     status = torch.empty(B, dtype=torch.int32, device=dev)
     rc = lib.sdb_kuhlmann(ptr(adj), B, n1 - 1, 1 if single_root else 0, ptr(heads), ptr(score), ptr(status),
-                          stream_ptr(dev))
+                          stream.cuda_stream if stream else stream_ptr(dev))
     _lib.check(rc, "sdb_kuhlmann")
     return heads, score, status
 
@@ -320,7 +324,7 @@ def eisner_kuhlmann(adjacency, single_root: bool = False, marginals: bool = True
     -> ((logz, marg, status), (heads, score, status))."""
     adj = f32(adjacency, "adjacency")
     return _concurrent(adj.device, lambda: eisner(adj, single_root, marginals),
-                       lambda: kuhlmann(adj, single_root), keep=(adj,))
+                       lambda st: kuhlmann(adj, single_root, stream=st))
 
 
 # ------------------------------------------------------------------- PCFG
