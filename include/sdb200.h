@@ -285,6 +285,16 @@ int sdb_pcfg_sample(const float* root, const float* rules, const float* emission
                     int8_t* span_mask, int32_t* used, int32_t* status, void* workspace, size_t ws_bytes,
                     void* stream);
 
+/* ---- Matrix-Tree for any n ----------------------------------------------------
+ * sdb_mtt serves n <= 128 (register-resident Laplacian, no workspace);
+ * sdb_mtt_ex serves any n: n <= 128 forwards to sdb_mtt, larger n runs the
+ * general fp64 Gauss-Jordan with the Laplacian and its inverse in the caller's
+ * workspace (sdb_mtt_ex_workspace bytes; 0 for n <= 128).  Same outputs,
+ * status codes and reference semantics as sdb_mtt (spanning.py:90-175). */
+size_t sdb_mtt_ex_workspace(int64_t B, int32_t n);
+int sdb_mtt_ex(const float* adjacency, int64_t B, int32_t n, int32_t single_root, double* logz, float* marg,
+               int32_t* status, void* workspace, size_t ws_bytes, void* stream);
+
 /* ---- ragged chain batches (per-instance lengths) -----------------------------
  * Replaces batch_map over chains of different lengths (dist.py:355-361) without
  * pad_chain (chain.py:161-176): init [B][m], trans [B][n-1][m][m] in the batch

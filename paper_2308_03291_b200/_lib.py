@@ -73,6 +73,8 @@ SIGNATURES = {
                                              _c_p, _sz, _c_p]),
     "sdb_pcfg_sample": (ctypes.c_int, [_c_p, _c_p, _c_p, _c_p, _i64, _i32, _i32, _i32, _c_p, _i64, _i32, _c_p, _c_p,
                                        _c_p, _c_p, _sz, _c_p]),
+    "sdb_mtt_ex_workspace": (_sz, [_i64, _i32]),
+    "sdb_mtt_ex": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
     "sdb_chain_fb_lengths": (ctypes.c_int, [_c_p, _c_p, _c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p, _sz,
                                             _c_p]),
     "sdb_chain_viterbi_lengths": (ctypes.c_int, [_c_p, _c_p, _c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p]),

@@ -499,6 +499,14 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1)
   }
 }
 
+}  // namespace
+
+size_t mtt_gen_workspace(int64_t B, int n);
+int mtt_gen_launch(const float* adjacency, int64_t B, int n, int single, double* logz, float* marg, int32_t* status,
+                   void* workspace, size_t ws_bytes, cudaStream_t s);
+
+namespace {
+
 int mtt_check(int64_t B, int n) {
   if (B < 0 || n < 1) return SDB_ERR_ARG;
   if (n > kN) return SDB_ERR_UNSUPPORTED;
@@ -534,4 +542,17 @@ extern "C" int sdb_mtt(const float* adjacency, int64_t B, int32_t n, int32_t sin
               : launch_mtt<double, true, false>(adjacency, B, n, sr, logz, marg, status, s);
   return sr ? launch_mtt<float, false, true>(adjacency, B, n, sr, logz, nullptr, status, s)
             : launch_mtt<float, false, false>(adjacency, B, n, sr, logz, nullptr, status, s);
+}
+
+// n > 128 (or any n): the general fp64 kernel (mtt_gen.cu) with a caller workspace;
+// n <= 128 takes the register-resident kernel and needs no workspace.
+extern "C" size_t sdb_mtt_ex_workspace(int64_t B, int32_t n) { return n <= kN ? 0 : mtt_gen_workspace(B, n); }
+
+extern "C" int sdb_mtt_ex(const float* adjacency, int64_t B, int32_t n, int32_t single_root, double* logz, float* marg,
+                          int32_t* status, void* workspace, size_t ws_bytes, void* stream) {
+  if (B < 0 || n < 1 || !adjacency || !logz || !status) return SDB_ERR_ARG;
+  if (n <= kN) return sdb_mtt(adjacency, B, n, single_root, logz, marg, status, stream);
+  if (B == 0) return SDB_OK;
+  return mtt_gen_launch(adjacency, B, n, single_root ? 1 : 0, logz, marg, status, workspace, ws_bytes,
+                        (cudaStream_t)stream);
 }

@@ -275,9 +275,15 @@ def mtt(adjacency, single_root: bool = False, marginals: bool = True):
     logz = torch.empty(B, dtype=torch.float64, device=dev)
     status = torch.empty(B, dtype=torch.int32, device=dev)
     marg = torch.empty_like(adj) if marginals else None
-    rc = lib.sdb_mtt(ptr(adj), B, n1 - 1, 1 if single_root else 0, ptr(logz), ptr(marg), ptr(status),
-                     stream_ptr(dev))
-    _lib.check(rc, "sdb_mtt")
+    if n1 - 1 <= 128:
+        rc = lib.sdb_mtt(ptr(adj), B, n1 - 1, 1 if single_root else 0, ptr(logz), ptr(marg), ptr(status),
+                         stream_ptr(dev))
+        _lib.check(rc, "sdb_mtt")
+        return logz, marg, status
+    ws = workspace(lib.sdb_mtt_ex_workspace(B, n1 - 1), dev)  # general fp64 path (mtt_gen.cu)
+    rc = lib.sdb_mtt_ex(ptr(adj), B, n1 - 1, 1 if single_root else 0, ptr(logz), ptr(marg), ptr(status), ptr(ws),
+                        ws.numel(), stream_ptr(dev))
+    _lib.check(rc, "sdb_mtt_ex")
     return logz, marg, status
 
 

@@ -116,3 +116,26 @@ def test_mtt_single_root_branches():
                 np.testing.assert_allclose(marg[b].cpu().numpy(), O.mtt_marginals(adj[b], single), rtol=RTOL,
                                            atol=ATOL)
     assert O.mtt_log_partition(adj[0], True) == NEG_INF
+
+
+@pytest.mark.parametrize("single", [False, True])
+@pytest.mark.parametrize("B,n", [(2, 129), (2, 160), (1, 200)])
+def test_mtt_general_n_vs_oracle(B, n, single):
+    """n > 128 (beyond the register-resident kernel): the general fp64
+    Gauss-Jordan (mtt_gen.cu) through the same entry, vs the oracle."""
+    need_gpu()
+    adj = batch_spanning(2100, B, n)
+    logz, marg, st = K.mtt(dev(adj), single)
+    assert (st.cpu().numpy() == 0).all()
+    for b in range(B):
+        z = O.mtt_log_partition(adj[b], single)
+        assert abs(logz[b].item() - z) <= RTOL * max(1, abs(z))
+        np.testing.assert_allclose(marg[b].cpu().numpy(), O.mtt_marginals(adj[b], single), rtol=RTOL, atol=ATOL)
+    cut = adj.copy()
+    cut[:, :, 5] = NEG_INF
+    cut[:, 7, 5] = 0.0  # node 5 reachable only from node 7 ...
+    cut[:, 5, 7] = 0.0
+    cut[:, :, 7] = NEG_INF
+    cut[:, 5, 7] = 0.0  # ... which is reachable only from 5: a cut-off 2-cycle
+    z2, _, st2 = K.mtt(dev(cut), single)
+    assert (st2.cpu().numpy() == 1).all() and (z2.cpu().numpy() == NEG_INF).all()
