@@ -49,6 +49,8 @@ extern "C" {
 /* Library version (major*10000 + minor*100 + patch) and status strings. */
 int sdb_version(void);
 const char* sdb_status_string(int code);
+/* CUDA runtime message of the last error an entry point returned SDB_ERR_CUDA for. */
+const char* sdb_last_cuda_error(void);
 
 /* ---------------------------------------------------------------- chain --
  * LinearChainCRF (chain.py:32-61): init [B,m], transitions [B,n-1,m,m]

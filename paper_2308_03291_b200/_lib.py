@@ -23,6 +23,7 @@ _sz = ctypes.c_size_t
 SIGNATURES = {
     "sdb_version": (ctypes.c_int, []),
     "sdb_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+    "sdb_last_cuda_error": (ctypes.c_char_p, []),
     "sdb_chain_fb_workspace": (_sz, [_i64, _i32, _i32]),
     "sdb_chain_fb": (ctypes.c_int, [_c_p, _c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
     "sdb_chain_viterbi_workspace": (_sz, [_i64, _i32, _i32]),
@@ -117,5 +118,8 @@ def load():
 
 def check(rc: int, what: str):
     if rc != 0:
-        msg = load().sdb_status_string(rc).decode()
+        lib = load()
+        msg = lib.sdb_status_string(rc).decode()
+        if rc == -3:  # SDB_ERR_CUDA: add the runtime's own message
+            msg += ": " + lib.sdb_last_cuda_error().decode()
         raise NativeError(f"{what}: {msg} (code {rc})")

@@ -13,3 +13,7 @@ extern "C" const char* sdb_status_string(int code) {
     default: return "unknown";
   }
 }
+
+// the CUDA runtime's message for the last error an entry point returned
+// SDB_ERR_CUDA for ("no error" if none)
+extern "C" const char* sdb_last_cuda_error(void) { return cudaGetErrorString((cudaError_t)sdb_last_cuda().load()); }

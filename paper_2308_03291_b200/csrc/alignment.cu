@@ -625,11 +625,12 @@ struct BState {
 template <int kPh>
 __device__ __forceinline__ void mitm_fwd(const float* __restrict__ th, int n, int m, int NW, const MShared& sh, int RF, int off,
                          int nblk, float2* __restrict__ wsa, const float2* __restrict__ wsb, float zint, float zfrac,
-                         float* __restrict__ marg, FState& st, int* bad_flag) {
+                         float* __restrict__ marg, FState& st, int* bad_flag, bool edge) {
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const int g = l >> 4, q = l & 15;
   const int j = 32 * w + l;
-  const bool col_ok = j <= m;
+  const bool col_ok = j < (edge ? m : m + 1);
+  const bool lastcol = edge & (j == m - 1);  // alpha(., m-1) is kept for every row (edge column epilogue)
   const int steps = n + 32;
   const int lo = kPh == 1 ? 0 : RF + 1, hi = kPh == 1 ? RF : n;
   const size_t rowstride = (size_t)(m + 1) * 3;
@@ -740,7 +741,7 @@ __device__ __forceinline__ void mitm_fwd(const float* __restrict__ th, int n, in
           O = On;
           cur = VO{a, On};
         }
-        if (kPh == 1 && (kS || act)) wsa_b[32 * k] = make_float2(a, On);
+        if ((kPh == 1 || lastcol) && (kS || act)) wsa_b[32 * k] = make_float2(a, On);
         if (pub & (kS || act)) bnd_out[i & (kRB - 1)] = make_float2(a, On);
       }
     };
@@ -770,12 +771,18 @@ __device__ __forceinline__ void mitm_fwd(const float* __restrict__ th, int n, in
 template <int kPh>
 __device__ __forceinline__ void mitm_bwd(const float* __restrict__ th, int n, int m, int NW, const MShared& sh, int RFu, int off,
                          int nblk, const float2* __restrict__ wsa, float2* __restrict__ wsb, float zint, float zfrac,
-                         float* __restrict__ marg, BState& st) {
+                         float* __restrict__ marg, BState& st, bool edge, const float2* __restrict__ pushR,
+                         const float2* __restrict__ pushD) {
   const int wb = (threadIdx.x >> 5) - NW, l = threadIdx.x & 31;
   const int g = l >> 4, q = l & 15;
   const int mp = 32 * NW - 1;
   const int jo = mp - (32 * wb + l);
-  const bool col_ok = jo <= m;
+  const bool col_ok = jo < (edge ? m : m + 1);
+  // edge mode: column m is not in a strip; lane 0 of warp 0 (column m-1) streams
+  // that column's pushes (precomputed by mitm_edge_prologue) into warp 0's
+  // otherwise unused boundary rings
+  const bool edge_lane = edge & (wb == 0) & (l == 0);
+  const uint32_t e0_u = smem_u32(sh.bndB0), e1_u = smem_u32(sh.bndB1);
   const int u = NW - 1 - wb, lf = 31 - l;
   const int steps = n + 32;
   const int QB = n - RFu - 1;  // flipped rows [0, QB] are original rows > RF(u)
@@ -852,6 +859,12 @@ __device__ __forceinline__ void mitm_bwd(const float* __restrict__ th, int n, in
           const bool lv = (u > 0) & (l == 0) & (sl >= 0) & (sl < steps);
           cp8p(slabL_u + (uint32_t)((sa + 1) & (kMS - 1)) * 8u, sl_b - 32 * k, lv);
         }
+        {
+          const int sp = s + kMP;
+          const bool ev = edge_lane & (kIn ? true : ((sp >= 0) & (sp <= n)));
+          cp8p(e0_u + (uint32_t)(sp & (kRB - 1)) * 8u, pushR + sp, ev);
+          cp8p(e1_u + (uint32_t)(sp & (kRB - 1)) * 8u, pushD + sp, ev);
+        }
         cp_commit();
       }
       if (kIn || ((s >= 0) & (s < steps))) {
@@ -865,7 +878,7 @@ __device__ __forceinline__ void mitm_bwd(const float* __restrict__ th, int n, in
         const bool inrow = kIn ? true : ((ip >= 0) & (ip <= n));
         {
           const float2 a = bnd0_in[b0 + k], d = bnd1_in[b0 + k];
-          const bool ok = (wb > 0) & inrow;
+          const bool ok = ((wb > 0) | edge) & inrow;
           const bool l0 = l == 0;
           rR.v = l0 ? (ok ? a.x : ninf()) : rR.v;
           rR.o = l0 ? (ok ? a.y : 0.f) : rR.o;
@@ -959,14 +972,19 @@ __device__ __forceinline__ void mitm_bwd(const float* __restrict__ th, int n, in
   st.O = O;
 }
 
-// log2 Z over the moves that cross from A into B (fp64, all threads).
+// log2 Z over the moves that cross from A into B (fp64, all threads).  In
+// edge mode column m is entirely in B: its entry moves from column m-1 (DIAG
+// into rows 1..RF(NW-1)+1, RIGHT into rows 0..RF(NW-1)) are crossings too.
 __device__ double mitm_z(const float* __restrict__ th, int n, int m, int NW, const float2* __restrict__ wsa,
-                         const float2* __restrict__ wsb, double* red) {
+                         const float2* __restrict__ wsb, double* red, bool edge, const double* __restrict__ betaM) {
   const int steps = n + 32;
   const int m1 = m + 1;
+  const int mc = edge ? m : m1;  // strip columns
+  const int RFl = mitm_rf(NW - 1, n, NW);
   // per column: DOWN and DIAG into row RF+1; per strip boundary 32w: RIGHT into
   // rows (RF(w), RF(w-1)] and DIAG into rows (RF(w)+1, RF(w-1)+1]
-  const int E = 2 * m1 + 2 * (mitm_rf(0, n, NW) - mitm_rf(NW - 1, n, NW));
+  const int Eb = 2 * mc + 2 * (mitm_rf(0, n, NW) - RFl);
+  const int E = Eb + (edge ? 2 * (RFl + 1) : 0);
   auto alpha = [&](int i, int j) {
     const float2 v = wsa[((size_t)(j >> 5) * steps + i + (j & 31)) * 32 + (j & 31)];
     return (double)v.x + (double)v.y;
@@ -979,15 +997,21 @@ __device__ double mitm_z(const float* __restrict__ th, int n, int m, int NW, con
   double mx = ninfd(), sm = 0.0;
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     double t = ninfd();
-    if (e < 2 * m1) {
-      const int j = e < m1 ? e : e - m1;
+    if (e >= Eb) {
+      const int x = e - Eb;
+      if (x <= RFl)  // RIGHT (x, m-1) -> (x, m)
+        t = alpha(x, m - 1) + theta(x, m, 2) + betaM[x];
+      else  // DIAG (i-1, m-1) -> (i, m), i = x - RFl
+        t = alpha(x - RFl - 1, m - 1) + theta(x - RFl, m, 0) + betaM[x - RFl];
+    } else if (e < 2 * mc) {
+      const int j = e < mc ? e : e - mc;
       const int R = mitm_rf(j >> 5, n, NW);
-      if (e < m1)
+      if (e < mc)
         t = alpha(R, j) + theta(R + 1, j, 1) + beta(R + 1, j);
       else if (j >= 1)
         t = alpha(R, j - 1) + theta(R + 1, j, 0) + beta(R + 1, j);
     } else {
-      int x = e - 2 * m1, w = 1;
+      int x = e - 2 * mc, w = 1;
       while (x >= 2 * (mitm_rf(w - 1, n, NW) - mitm_rf(w, n, NW))) {
         x -= 2 * (mitm_rf(w - 1, n, NW) - mitm_rf(w, n, NW));
         ++w;
@@ -1027,9 +1051,102 @@ __device__ double mitm_z(const float* __restrict__ th, int n, int m, int NW, con
   return (M == ninfd()) ? ninfd() : M + log2(S);
 }
 
-__global__ void nw_mitm_kernel(const float* __restrict__ theta, int n, int m, float2* __restrict__ wsa_all,
-                               float2* __restrict__ wsb_all, double* __restrict__ logz, float* __restrict__ marg_all,
-                               int32_t* __restrict__ status) {
+// Edge mode (m % 32 == 0): the last column m would be a strip of its own with
+// one live lane per direction.  It is not needed as one: every path that enters
+// column m only moves DOWN afterwards, so
+//   beta(i, m) = sum_{r > i} theta[r, m, DOWN]            (a suffix sum)
+// and, with e(r) the marginal of the DIAG + RIGHT moves into (r, m),
+//   p(DOWN into (i, m)) = sum_{r < i} e(r)                 (a prefix sum).
+// The backward pass consumes column m's pushes from these sums, the forward
+// pass never computes column m (alignment.py:62-118 define the same numbers
+// through the full recurrences).
+//
+// Chunked block-wide scans in fp64: thread t owns rows [t*C, t*C + C).
+__device__ double block_excl(double v, double* scratch, int t, int T, bool suffix, int bar_id) {
+  scratch[t] = v;
+  bar_dir(bar_id, T);
+  double acc = 0.0;
+  if (suffix)
+    for (int x = t + 1; x < T; ++x) acc += scratch[x];
+  else
+    for (int x = 0; x < t; ++x) acc += scratch[x];
+  bar_dir(bar_id, T);
+  return acc;
+}
+
+// backward warps (T = 32 NW threads, barrier 2): betaM[i] = beta(i, m) (log2),
+// pushR/pushD[ip] = the RIGHT / DIAG pushes of cell (n - ip, m) as (v, O).
+__device__ void mitm_edge_prologue(const float* __restrict__ th, int n, int m, int NW, double* __restrict__ betaM,
+                                   float2* __restrict__ pushR, float2* __restrict__ pushD, double* scratch,
+                                   int* bad_flag) {
+  const int T = 32 * NW, t = threadIdx.x - T;
+  const int C = (n + 1 + T - 1) / T, r0 = min(t * C, n + 1), r1 = min(r0 + C, n + 1);
+  const size_t rs = (size_t)(m + 1) * 3;
+  const float* col = th + (size_t)m * 3;
+  const double L = 1.4426950408889634;
+  double cs = 0.0;
+  bool bad = false;
+  for (int r = r0; r < r1; ++r) {
+    const float x0 = col[r * rs], x1 = col[r * rs + 1], x2 = col[r * rs + 2];
+    bad |= bad_input(x0) | bad_input(x1) | bad_input(x2);
+    if (r >= 1) cs += (double)x1 * L;
+  }
+  double b = block_excl(cs, scratch, t, T, true, 2);  // beta(r1 - 1, m)
+  auto split = [](double x) {
+    if (!(x > -1e300)) return make_float2(ninf(), 0.f);
+    const double o = rint(x);
+    return make_float2((float)(x - o), (float)o);
+  };
+  for (int r = r1 - 1; r >= r0; --r) {
+    betaM[r] = b;
+    pushR[n - r] = split((double)col[r * rs + 2] * L + b);
+    pushD[n - r] = split((double)col[r * rs] * L + b);
+    if (r >= 1) b += (double)col[r * rs + 1] * L;
+  }
+  if (bad) atomicOr(bad_flag, 1);
+}
+
+// all threads, after phase 2: column m's move marginals.
+__device__ void mitm_edge_epilogue(const float* __restrict__ th, int n, int m, int NW, const float2* __restrict__ wsa,
+                                   const double* __restrict__ betaM, double z2, float* __restrict__ marg,
+                                   double* scratch) {
+  const int T = blockDim.x, t = threadIdx.x;
+  const int C = (n + 1 + T - 1) / T, r0 = min(t * C, n + 1), r1 = min(r0 + C, n + 1);
+  const int steps = n + 32;
+  const size_t rs = (size_t)(m + 1) * 3;
+  const float* col = th + (size_t)m * 3;
+  float* mc = marg + (size_t)m * 3;
+  const double L = 1.4426950408889634;
+  const bool zok = z2 != ninfd();
+  const float2* wl = wsa + ((size_t)(NW - 1) * steps + 31) * 32 + 31;  // alpha(i, m-1) at wl[32 i]
+  auto alpha = [&](int i) { const float2 v = wl[(size_t)i * 32]; return (double)v.x + (double)v.y; };
+  auto entry = [&](int r, double& ed, double& er) {
+    ed = (zok & (r >= 1)) ? exp2(alpha(r - 1) + (double)col[r * rs] * L + betaM[r] - z2) : 0.0;
+    er = zok ? exp2(alpha(r) + (double)col[r * rs + 2] * L + betaM[r] - z2) : 0.0;
+  };
+  double cs = 0.0;
+  for (int r = r0; r < r1; ++r) {
+    double ed, er;
+    entry(r, ed, er);
+    mc[r * rs] = (float)ed;
+    mc[r * rs + 2] = (float)er;
+    cs += ed + er;
+  }
+  double run = block_excl(cs, scratch, t, T, false, 0);
+  for (int r = r0; r < r1; ++r) {
+    double ed, er;
+    entry(r, ed, er);
+    mc[r * rs + 1] = (float)run;  // 0 for r = 0
+    run += ed + er;
+  }
+}
+
+// kMaxT = 640 for NW >= 9: 18-20 warps put 5 on one SM sub-partition, whose
+// 16K registers then cap the kernel at 96 registers per thread.
+template <int kMaxT>
+__global__ void __launch_bounds__(kMaxT) nw_mitm_kernel(const float* __restrict__ theta, int n, int m, float2* __restrict__ wsa_all,
+                               float2* __restrict__ wsb_all, double* __restrict__ edge_all, double* __restrict__ logz,
+                               float* __restrict__ marg_all, int32_t* __restrict__ status) {
   extern __shared__ __align__(16) char smraw[];
   const int NW = blockDim.x >> 6;
   const int b = blockIdx.x;
@@ -1039,6 +1156,10 @@ __global__ void nw_mitm_kernel(const float* __restrict__ theta, int n, int m, fl
   const size_t wsz = (size_t)NW * (n + 32) * 32;
   float2* wsa = wsa_all + (size_t)b * wsz;
   float2* wsb = wsb_all + (size_t)b * wsz;
+  const bool edge = (m & 31) == 0;
+  double* betaM = edge_all + (size_t)b * 3 * (n + 1);  // [n+1] doubles, then pushR, pushD [n+1] float2
+  float2* pushR = (float2*)(betaM + (n + 1));
+  float2* pushD = pushR + (n + 1);
   if (threadIdx.x == 0) sh.flags[0] = 0;
   const int warp = threadIdx.x >> 5;
   const bool fwd = warp < NW;
@@ -1054,20 +1175,27 @@ __global__ void nw_mitm_kernel(const float* __restrict__ theta, int n, int m, fl
   FState fs{{ninf(), 0.f}, {ninf(), 0.f}, ninf(), 0.f};
   BState bs{{ninf(), 0.f}, {ninf(), 0.f}, {ninf(), 0.f}, {ninf(), 0.f}, 0.f};
   bar_all();
-  if (fwd)
-    mitm_fwd<1>(th, n, m, NW, sh, mitm_rf(w, n, NW), 0, G1, wsa, wsb, 0.f, ninf(), nullptr, fs, sh.flags);
-  else
-    mitm_bwd<1>(th, n, m, NW, sh, mitm_rf(NW - 1 - w, n, NW), 0, G1, wsa, wsb, 0.f, ninf(), nullptr, bs);
+  if (fwd) {
+    mitm_fwd<1>(th, n, m, NW, sh, mitm_rf(w, n, NW), 0, G1, wsa, wsb, 0.f, ninf(), nullptr, fs, sh.flags, edge);
+  } else {
+    // the backward rings are free until the first prefetch: scratch for the scan
+    if (edge) mitm_edge_prologue(th, n, m, NW, betaM, pushR, pushD, (double*)(sh.ring + (size_t)NW * kMRing), sh.flags);
+    mitm_bwd<1>(th, n, m, NW, sh, mitm_rf(NW - 1 - w, n, NW), 0, G1, wsa, wsb, 0.f, ninf(), nullptr, bs, edge, pushR,
+                pushD);
+  }
   __threadfence_block();
   bar_all();
-  const double z2 = mitm_z(th, n, m, NW, wsa, wsb, sh.red);
+  const double z2 = mitm_z(th, n, m, NW, wsa, wsb, sh.red, edge, betaM);
   const float zint = (z2 == ninfd()) ? 0.f : (float)rint(z2);
   const float zfrac = (z2 == ninfd()) ? ninf() : (float)(z2 - rint(z2));
   if (fwd)
-    mitm_fwd<2>(th, n, m, NW, sh, mitm_rf(w, n, NW), off2, G2, wsa, wsb, zint, zfrac, marg, fs, sh.flags);
+    mitm_fwd<2>(th, n, m, NW, sh, mitm_rf(w, n, NW), off2, G2, wsa, wsb, zint, zfrac, marg, fs, sh.flags, edge);
   else
-    mitm_bwd<2>(th, n, m, NW, sh, mitm_rf(NW - 1 - w, n, NW), off2, G2, wsa, wsb, zint, zfrac, marg, bs);
+    mitm_bwd<2>(th, n, m, NW, sh, mitm_rf(NW - 1 - w, n, NW), off2, G2, wsa, wsb, zint, zfrac, marg, bs, edge, pushR,
+                pushD);
+  __threadfence_block();
   bar_all();
+  if (edge) mitm_edge_epilogue(th, n, m, NW, wsa, betaM, z2, marg, (double*)sh.ring);
   if (threadIdx.x == 0) {
     const double z = (z2 == ninfd()) ? ninfd() : z2 * (double)SDB_LN2;
     status[b] = sh.flags[0] ? SDB_ST_INVALID : (z == ninfd() ? SDB_ST_VACUOUS : SDB_ST_OK);
@@ -1075,8 +1203,11 @@ __global__ void nw_mitm_kernel(const float* __restrict__ theta, int n, int m, fl
   }
 }
 
+// strips per direction: columns 0..m, or 0..m-1 when column m is an edge column
+int mitm_nw(int m) { return (m & 31) == 0 ? m / 32 : (m + 1 + 31) / 32; }
+
 int mitm_ok(int n, int m) {
-  const int NW = (m + 1 + 31) / 32;
+  const int NW = mitm_nw(m);
   return NW <= 10 && n >= 40 * (NW - 1) + 32 && mitm_smem_bytes(NW) <= 220 * 1024;
 }
 
@@ -1086,6 +1217,7 @@ struct NwWs {
   int8_t* choice;
   float2* wsa2;  // meet-in-the-middle alpha / beta (v, O)
   float2* wsb2;
+  double* edge;  // [B][3 (n+1)]: beta(., m) fp64, then the column-m pushes (edge mode)
 };
 
 NwWs nw_carve_ws(void* base, int64_t B, int n, int m, int mode, size_t* bytes) {
@@ -1094,8 +1226,10 @@ NwWs nw_carve_ws(void* base, int64_t B, int n, int m, int mode, size_t* bytes) {
   Carve c(base);
   NwWs w{};
   if (mode == 1 && mitm_ok(n, m)) {
-    w.wsa2 = c.take<float2>((size_t)B * wsz * 32);
-    w.wsb2 = c.take<float2>((size_t)B * wsz * 32);
+    const size_t wsm = (size_t)mitm_nw(m) * (n + 32);
+    w.wsa2 = c.take<float2>((size_t)B * wsm * 32);
+    w.wsb2 = c.take<float2>((size_t)B * wsm * 32);
+    w.edge = c.take<double>((m & 31) == 0 ? (size_t)B * 3 * (n + 1) : 1);
   } else if (mode == 1) {
     w.wsb = c.take<float>((size_t)B * wsz * 32);
     w.wsk = c.take<float>((size_t)B * wsz);
@@ -1120,10 +1254,12 @@ int nw_launch(const float* theta, int64_t B, int n, int m, NwWs ws, double* logz
     return SDB_OK;
   }
   if (kMode == 1 && ws.wsa2) {
-    const size_t sm2 = mitm_smem_bytes(NW);
-    if (sdb_set_smem((const void*)nw_mitm_kernel, sm2) != cudaSuccess)
+    const int NWm = mitm_nw(m);
+    const size_t sm2 = mitm_smem_bytes(NWm);
+    auto kern = NWm >= 9 ? nw_mitm_kernel<640> : nw_mitm_kernel<512>;
+    if (sdb_set_smem((const void*)kern, sm2) != cudaSuccess)
       return SDB_ERR_CUDA;
-    nw_mitm_kernel<<<(unsigned)B, 64 * NW, sm2, s>>>(theta, n, m, ws.wsa2, ws.wsb2, logz, marg, status);
+    kern<<<(unsigned)B, 64 * NWm, sm2, s>>>(theta, n, m, ws.wsa2, ws.wsb2, ws.edge, logz, marg, status);
     SDB_CHECK_LAUNCH();
     return SDB_OK;
   }

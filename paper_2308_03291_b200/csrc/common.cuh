@@ -13,6 +13,7 @@
 #include <math.h>
 
 #include <map>
+#include <atomic>
 #include <mutex>
 #include <utility>
 
@@ -153,6 +154,16 @@ struct Carve {
   }
 };
 
+// last CUDA runtime error seen by an entry point (sdb_last_cuda_error)
+inline std::atomic<int>& sdb_last_cuda() {
+  static std::atomic<int> e{0};
+  return e;
+}
+inline cudaError_t sdb_note(cudaError_t e) {
+  if (e != cudaSuccess) sdb_last_cuda().store((int)e);
+  return e;
+}
+
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel):
 // the runtime call costs microseconds of host time on every launch otherwise
 inline cudaError_t sdb_set_smem(const void* kern, size_t smem) {
@@ -165,11 +176,14 @@ inline cudaError_t sdb_set_smem(const void* kern, size_t smem) {
   if (have >= smem) return cudaSuccess;
   const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess) have = smem;
-  return e;
+  return sdb_note(e);
 }
 
 #define SDB_CHECK_LAUNCH()                       \
   do {                                           \
     cudaError_t _e = cudaGetLastError();         \
-    if (_e != cudaSuccess) return SDB_ERR_CUDA;  \
+    if (_e != cudaSuccess) {                     \
+      sdb_note(_e);                              \
+      return SDB_ERR_CUDA;                       \
+    }                                            \
   } while (0)

@@ -120,6 +120,29 @@ def test_alignment_mitm_masked_and_vacuous():
         np.testing.assert_allclose(marg[b].cpu().numpy(), mg, rtol=RTOL, atol=ATOL)
 
 
+@pytest.mark.parametrize("n,m", [(200, 64), (152, 128), (33, 32)])
+def test_alignment_mitm_edge_column(n, m):
+    """m % 32 == 0: column m is handled outside the strips (suffix sums for
+    beta, prefix sums of the entry marginals for its DOWN moves).  Masks and
+    bad values placed in that column must behave exactly as anywhere else."""
+    need_gpu()
+    th = batch_alignment(31 + n + m, 6, n, m)
+    th[1, n // 3, m, 1] = NEG_INF        # no DOWN through (n/3, m): enter below
+    th[2, n // 2, m, 1] = np.nan         # invalid
+    th[3, :n, m, 0] = NEG_INF            # enter column m only by RIGHT ...
+    th[3, :n // 2, m, 2] = NEG_INF       # ... in the lower half
+    th[4, 0, m, 0] = np.inf              # an unused move, still invalid
+    th[5, :, m, 0] = NEG_INF             # column m unreachable -> vacuous
+    th[5, :, m, 2] = NEG_INF
+    logz, marg, st = K.nw_fb(dev(th))
+    assert st.cpu().tolist() == [0, 0, 2, 0, 2, 1]
+    assert logz[5].item() == NEG_INF and float(marg[5].abs().sum()) == 0.0
+    for b in (0, 1, 3):
+        z, mg = O.nw_marginals(th[b])
+        assert abs(logz[b].item() - z) <= RTOL * abs(z)
+        np.testing.assert_allclose(marg[b].cpu().numpy(), mg, rtol=RTOL, atol=ATOL)
+
+
 def test_run_host_batch_matches_device_call():
     """kernels.run_host_batch (pinned host slices, H2D / kernels / D2H
     overlapped on separate streams) returns exactly the device call's result."""
