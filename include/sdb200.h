@@ -75,7 +75,8 @@ int sdb_chain_viterbi(const float* init, const float* trans, int64_t B, int32_t 
 /* ------------------------------------------------------------ alignment --
  * MonotoneAlignmentCRF (alignment.py:30-59): theta [B,n+1,m+1,3] with moves
  * {0 DIAG from (i-1,j-1), 1 DOWN from (i-1,j), 2 RIGHT from (i,j-1)} scored
- * on arrival.  n >= 1, 1 <= m <= 351.
+ * on arrival.  n >= 1, m >= 1 (m <= 351: strip kernels; larger m: an anti-diagonal
+ * fp64 kernel, min(n, m) < 8192).
  *
  * sdb_nw_fb replaces _nw_forward/_nw_backward/nw_log_partition/nw_marginals
  * (alignment.py:62-118): logz [B]; marg [B,n+1,m+1,3] nullable.

@@ -1271,16 +1271,29 @@ int nw_launch(const float* theta, int64_t B, int n, int m, NwWs ws, double* logz
   return SDB_OK;
 }
 
-int nw_check(int64_t B, int n, int m) {
-  if (B < 0 || n < 1 || m < 1) return SDB_ERR_ARG;
+bool nw_fast_ok(int n, int m) {
   const int NW = (m + 1 + 31) / 32;
-  if (NW > 32 || nw_smem_bytes(NW) > 220 * 1024) return SDB_ERR_UNSUPPORTED;
-  return SDB_OK;
+  return NW <= 32 && nw_smem_bytes(NW) <= 220 * 1024;
 }
 
 }  // namespace
 
+// nw_gen.cu: anti-diagonal fp64 kernels for m beyond the strip kernels
+bool nw_gen_ok(int n, int m);
+size_t nw_gen_workspace(int64_t B, int n, int m, int mode);
+int nw_gen_launch(int mode, const float* theta, int64_t B, int n, int m, void* ws, size_t ws_bytes, double* out,
+                  float* marg, int8_t* path, int32_t* status, cudaStream_t s);
+
+namespace {
+int nw_check(int64_t B, int n, int m) {
+  if (B < 0 || n < 1 || m < 1) return SDB_ERR_ARG;
+  if (!nw_fast_ok(n, m) && !nw_gen_ok(n, m)) return SDB_ERR_UNSUPPORTED;
+  return SDB_OK;
+}
+}  // namespace
+
 extern "C" size_t sdb_nw_fb_workspace(int64_t B, int32_t n, int32_t m) {
+  if (!nw_fast_ok(n, m)) return nw_gen_workspace(B, n, m, 1);
   size_t bytes = 0;
   nw_carve_ws(nullptr, B, n, m, 1, &bytes);
   return bytes;
@@ -1292,6 +1305,9 @@ extern "C" int sdb_nw_fb(const float* theta, int64_t B, int32_t n, int32_t m, do
   if (rc) return rc;
   if (!theta || !logz || !status) return SDB_ERR_ARG;
   if (B == 0) return SDB_OK;
+  if (!nw_fast_ok(n, m))
+    return nw_gen_launch(marg ? 1 : 0, theta, B, n, m, workspace, ws_bytes, logz, marg, nullptr, status,
+                         (cudaStream_t)stream);
   if (!marg) return nw_launch<0>(theta, B, n, m, NwWs{}, logz, nullptr, nullptr, nullptr, status, (cudaStream_t)stream);
   size_t need = 0;
   NwWs ws = nw_carve_ws(workspace, B, n, m, 1, &need);
@@ -1300,6 +1316,7 @@ extern "C" int sdb_nw_fb(const float* theta, int64_t B, int32_t n, int32_t m, do
 }
 
 extern "C" size_t sdb_nw_viterbi_workspace(int64_t B, int32_t n, int32_t m) {
+  if (!nw_fast_ok(n, m)) return nw_gen_workspace(B, n, m, 2);
   size_t bytes = 0;
   nw_carve_ws(nullptr, B, n, m, 2, &bytes);
   return bytes;
@@ -1311,10 +1328,14 @@ extern "C" int sdb_nw_viterbi(const float* theta, int64_t B, int32_t n, int32_t 
   if (rc) return rc;
   if (!theta || !path || !score || !status) return SDB_ERR_ARG;
   if (B == 0) return SDB_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!nw_fast_ok(n, m)) {
+    if (sdb_note(cudaMemsetAsync(path, 0xff, (size_t)B * (n + 1) * (m + 1), s)) != cudaSuccess) return SDB_ERR_CUDA;
+    return nw_gen_launch(2, theta, B, n, m, workspace, ws_bytes, score, nullptr, path, status, s);
+  }
   size_t need = 0;
   NwWs ws = nw_carve_ws(workspace, B, n, m, 2, &need);
   if (!workspace || ws_bytes < need) return SDB_ERR_WORKSPACE;
-  cudaStream_t s = (cudaStream_t)stream;
   if (cudaMemsetAsync(path, 0xff, (size_t)B * (n + 1) * (m + 1), s) != cudaSuccess) return SDB_ERR_CUDA;
   return nw_launch<2>(theta, B, n, m, ws, nullptr, nullptr, path, score, status, s);
 }

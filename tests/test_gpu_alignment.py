@@ -143,6 +143,37 @@ def test_alignment_mitm_edge_column(n, m):
         np.testing.assert_allclose(marg[b].cpu().numpy(), mg, rtol=RTOL, atol=ATOL)
 
 
+@pytest.mark.parametrize("B,n,m", [(2, 20, 400), (2, 360, 370), (3, 5, 1000)])
+def test_alignment_general_shapes(B, n, m):
+    """m > 351 runs the anti-diagonal fp64 kernel (nw_gen.cu): same results,
+    same argmax tie-breaking, same statuses as the strip kernels."""
+    need_gpu()
+    th = batch_alignment(4000 + n + m, B, n, m)
+    th[B - 1, n // 2, :, 1] = NEG_INF  # a row no path can enter by DOWN
+    logz, marg, st = K.nw_fb(dev(th))
+    lz_only, _, st0 = K.nw_fb(dev(th), marginals=False)
+    path, score, st2 = K.nw_viterbi(dev(th))
+    for b in range(B):
+        z, mg = O.nw_marginals(th[b])
+        assert st[b].item() == st0[b].item() == st2[b].item() == (0 if z > NEG_INF else 1)
+        if z == NEG_INF:
+            continue
+        assert abs(logz[b].item() - z) <= RTOL * abs(z) and abs(lz_only[b].item() - z) <= RTOL * abs(z)
+        np.testing.assert_allclose(marg[b].cpu().numpy(), mg, rtol=RTOL, atol=ATOL)
+        mask, sc = O.nw_argmax(th[b])
+        p = path[b].cpu().numpy()
+        got = np.zeros_like(mask)
+        ii, jj = np.nonzero(p >= 0)
+        got[ii, jj, p[ii, jj]] = 1
+        np.testing.assert_array_equal(got, mask)
+        assert score[b].item() == sc
+    bad = th.copy()
+    bad[0, 3, 7, 2] = np.nan
+    assert K.nw_fb(dev(bad))[2][0].item() == 2
+    d = sd.MonotoneAlignmentCRF(th[0])  # through the public API
+    assert abs(sd.log_partition(d) - O.nw_marginals(th[0])[0]) <= RTOL * abs(float(logz[0]))
+
+
 def test_run_host_batch_matches_device_call():
     """kernels.run_host_batch (pinned host slices, H2D / kernels / D2H
     overlapped on separate streams) returns exactly the device call's result."""
