@@ -467,10 +467,23 @@ CtcWs ctc_carve_ws(void* base, int64_t B, int T, int V, int L, int mode, size_t*
   return w;
 }
 
+bool ctc_fast_ok(int V, int L) {
+  const int S = 2 * L + 1;
+  return S <= 1024 && ctc_smem_bytes(S, V, L) <= 200 * 1024 && ctc_dir_smem_bytes(S, V, L) <= 200 * 1024;
+}
+
+}  // namespace
+
+// ctc_gen.cu: states strided over the threads, fp64, for larger lattices
+bool ctc_gen_ok(int L);
+size_t ctc_gen_workspace(int64_t B, int T, int L, int mode);
+int ctc_gen_launch(int mode, const float* fp, const int32_t* tg, int64_t B, int T, int V, int L, void* ws,
+                   size_t ws_bytes, double* out, float* marg, int32_t* path, int32_t* status, cudaStream_t s);
+
+namespace {
 int ctc_check(int64_t B, int T, int V, int L) {
   if (B < 0 || T < 1 || V < 1 || L < 0) return SDB_ERR_ARG;
-  const int S = 2 * L + 1;
-  if (S > 1024 || ctc_smem_bytes(S, V, L) > 200 * 1024) return SDB_ERR_UNSUPPORTED;
+  if (!ctc_fast_ok(V, L) && !ctc_gen_ok(L)) return SDB_ERR_UNSUPPORTED;
   return SDB_OK;
 }
 
@@ -517,7 +530,7 @@ int ctc_launch(const float* fp, const int32_t* tg, int64_t B, int T, int V, int 
 }  // namespace
 
 extern "C" size_t sdb_ctc_fb_workspace(int64_t B, int32_t T, int32_t V, int32_t L) {
-  (void)V;
+  if (!ctc_fast_ok(V, L)) return ctc_gen_workspace(B, T, L, 1);
   size_t bytes = 0;
   ctc_carve_ws(nullptr, B, T, V, L, 1, &bytes);
   return bytes;
@@ -531,6 +544,9 @@ extern "C" int sdb_ctc_fb(const float* frame_potentials, const int32_t* targets,
   if (!frame_potentials || (L > 0 && !targets) || !logz || !status) return SDB_ERR_ARG;
   if (B == 0) return SDB_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  if (!ctc_fast_ok(V, L))
+    return ctc_gen_launch(marg ? 1 : 0, frame_potentials, targets, B, T, V, L, workspace, ws_bytes, logz, marg,
+                          nullptr, status, s);
   if (!marg) return ctc_launch<0>(frame_potentials, targets, B, T, V, L, CtcWs{}, logz, nullptr, nullptr, nullptr, status, s);
   size_t need = 0;
   CtcWs ws = ctc_carve_ws(workspace, B, T, V, L, 1, &need);
@@ -539,7 +555,7 @@ extern "C" int sdb_ctc_fb(const float* frame_potentials, const int32_t* targets,
 }
 
 extern "C" size_t sdb_ctc_viterbi_workspace(int64_t B, int32_t T, int32_t V, int32_t L) {
-  (void)V;
+  if (!ctc_fast_ok(V, L)) return ctc_gen_workspace(B, T, L, 2);
   size_t bytes = 0;
   ctc_carve_ws(nullptr, B, T, V, L, 2, &bytes);
   return bytes;
@@ -552,6 +568,9 @@ extern "C" int sdb_ctc_viterbi(const float* frame_potentials, const int32_t* tar
   if (rc) return rc;
   if (!frame_potentials || (L > 0 && !targets) || !labels || !score || !status) return SDB_ERR_ARG;
   if (B == 0) return SDB_OK;
+  if (!ctc_fast_ok(V, L))
+    return ctc_gen_launch(2, frame_potentials, targets, B, T, V, L, workspace, ws_bytes, score, nullptr, labels,
+                          status, (cudaStream_t)stream);
   size_t need = 0;
   CtcWs ws = ctc_carve_ws(workspace, B, T, V, L, 2, &need);
   if (!workspace || ws_bytes < need) return SDB_ERR_WORKSPACE;

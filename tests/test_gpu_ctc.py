@@ -33,7 +33,9 @@ def test_ctc_golden(case):
     assert score == float(case.argmax_score)
 
 
-@pytest.mark.parametrize("B,T,V,L", [(4, 512, 128, 128), (3, 50, 7, 12), (2, 9, 3, 4), (5, 1, 4, 0), (2, 30, 40, 300)])
+# the last three run ctc_gen.cu: 2L+1 > 1024 states, a 20000-word vocabulary
+@pytest.mark.parametrize("B,T,V,L", [(4, 512, 128, 128), (3, 50, 7, 12), (2, 9, 3, 4), (5, 1, 4, 0), (2, 30, 40, 300),
+                                     (2, 1100, 30, 520), (2, 700, 6, 600), (2, 40, 20000, 10)])
 def test_ctc_batched_vs_oracle(B, T, V, L):
     need_gpu()
     fp, tg = batch_ctc(1000, B, T, V, L)
