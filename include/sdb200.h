@@ -116,7 +116,9 @@ int sdb_ctc_viterbi(const float* frame_potentials, const int32_t* targets, int64
 
 /* ------------------------------------------------------------- Tree-CRF --
  * TreeCRF (constituency.py:26-49): span_potentials [B,n,n,m] (i, j, label),
- * only i <= j read.  1 <= n <= 128.
+ * only i <= j read.  n >= 1: n <= 128 runs the shared-memory chart kernels,
+ * larger n fp64 charts in global memory (workspace 3 x B n^2 doubles;
+ * sdb_tree_viterbi allocates that scratch stream-ordered).
  *
  * sdb_tree_fb replaces _tree_charts/cky_log_partition/tree_marginals
  * (constituency.py:52-110): logz [B]; marg [B,n,n,m] nullable (0 for i > j
@@ -135,7 +137,8 @@ int sdb_tree_viterbi(const float* span_potentials, int64_t B, int32_t n, int32_t
 /* ---------------------------------------------------- Matrix-Tree (MTT) --
  * Directed non-projective SpanningTreeCRF (spanning.py:41-70):
  * adjacency [B,n+1,n+1] (head, dependent), node 0 = root, diagonal and
- * column 0 -inf.  1 <= n <= 128.  single_root != 0 selects the Koo et al.
+ * column 0 -inf.  1 <= n <= 128 (sdb_mtt_ex below: any n).  single_root != 0
+ * selects the Koo et al.
  * single-root-edge Laplacian.
  *
  * sdb_mtt replaces _shifted_exp_weights/_build_laplacian/signed_log_det/

@@ -667,16 +667,27 @@ int tree_launch(const float* th, int64_t B, int n, int m, double* logz, float* m
   return SDB_OK;
 }
 
+bool tree_fast_ok(int n) { return n <= 128 && tree_smem(n) <= 220 * 1024; }  // <= 4 terms per lane
+
+}  // namespace
+
+// tree_gen.cu: fp64 charts in global memory for longer sentences
+bool tree_gen_ok(int n);
+size_t tree_gen_workspace(int64_t B, int n);
+int tree_gen_launch(int mode, const float* sp, int64_t B, int n, int m, void* ws, size_t ws_bytes, double* out,
+                    float* marg, int32_t* labels, int32_t* status, cudaStream_t s);
+
+namespace {
 int tree_check(int64_t B, int n, int m) {
   if (B < 0 || n < 1 || m < 1) return SDB_ERR_ARG;
-  if (n > 128 || tree_smem(n) > 220 * 1024) return SDB_ERR_UNSUPPORTED;  // <= 4 terms per lane
+  if (!tree_fast_ok(n) && !tree_gen_ok(n)) return SDB_ERR_UNSUPPORTED;
   return SDB_OK;
 }
-
 }  // namespace
 
 extern "C" size_t sdb_tree_fb_workspace(int64_t B, int32_t n, int32_t m) {
   (void)m;
+  if (B > 0 && n > 0 && !tree_fast_ok(n)) return tree_gen_workspace(B, n);
   return (B > 0 && n > 0) ? tree_ws(B, n) : 0;
 }
 
@@ -686,6 +697,11 @@ extern "C" int sdb_tree_fb(const float* span_potentials, int64_t B, int32_t n, i
   if (rc) return rc;
   if (!span_potentials || !logz || !status) return SDB_ERR_ARG;
   if (B == 0) return SDB_OK;
+  if (!tree_fast_ok(n)) {
+    if (!workspace) return SDB_ERR_WORKSPACE;
+    return tree_gen_launch(marg ? 1 : 0, span_potentials, B, n, m, workspace, ws_bytes, logz, marg, nullptr, status,
+                           (cudaStream_t)stream);
+  }
   if (!workspace || ws_bytes < tree_ws(B, n)) return SDB_ERR_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
   Carve c(workspace);
@@ -731,5 +747,8 @@ extern "C" int sdb_tree_viterbi(const float* span_potentials, int64_t B, int32_t
   if (rc) return rc;
   if (!span_potentials || !labels || !score || !status) return SDB_ERR_ARG;
   if (B == 0) return SDB_OK;
+  if (!tree_fast_ok(n))
+    return tree_gen_launch(2, span_potentials, B, n, m, nullptr, 0, score, nullptr, labels, status,
+                           (cudaStream_t)stream);
   return tree_launch<2>(span_potentials, B, n, m, nullptr, nullptr, labels, score, status, (cudaStream_t)stream);
 }

@@ -29,7 +29,7 @@ def test_tree_golden(case):
 
 
 @pytest.mark.parametrize("B,n,m", [(3, 64, 32), (4, 17, 5), (2, 1, 3), (2, 128, 4), (3, 33, 33), (2, 20, 16), (2, 12, 64),
-                                   (2, 80, 8)])
+                                   (2, 80, 8), (2, 160, 6), (1, 257, 3)])  # n > 128: tree_gen.cu
 def test_tree_batched_vs_oracle(B, n, m):
     need_gpu()
     th = batch_tree(4000, B, n, m)
@@ -44,6 +44,28 @@ def test_tree_batched_vs_oracle(B, n, m):
         np.testing.assert_allclose(marg[b].cpu().numpy(), mg, rtol=RTOL, atol=ATOL)
         lab, sc = O.tree_argmax(th[b])
         np.testing.assert_array_equal(labels[b].cpu().numpy(), lab)  # bit-exact
+        assert score[b].item() == sc
+
+
+def test_tree_general_status():
+    """n > 128 (tree_gen.cu): invalid, vacuous and masked instances."""
+    need_gpu()
+    n, m = 140, 4
+    th = batch_tree(4100, 4, n, m)
+    th[0, 5, 90, 2] = np.nan            # invalid
+    th[1, 0, n - 1, :] = NEG_INF        # the root span has no label -> vacuous
+    th[2, :, :, 1:] = NEG_INF           # one label everywhere
+    th[2, 10, 50, 0] = NEG_INF          # and one span forbidden
+    logz, marg, st = K.tree_fb(dev(th))
+    labels, score, st2 = K.tree_viterbi(dev(th))
+    assert st.cpu().tolist() == [2, 1, 0, 0] and st2.cpu().tolist() == [2, 1, 0, 0]
+    assert float(marg[1].abs().sum()) == 0.0 and (labels[1] == -1).all()
+    for b in (2, 3):
+        z, mg = O.tree_marginals(th[b])
+        assert abs(logz[b].item() - z) <= RTOL * abs(z)
+        np.testing.assert_allclose(marg[b].cpu().numpy(), mg, rtol=RTOL, atol=ATOL)
+        lab, sc = O.tree_argmax(th[b])
+        np.testing.assert_array_equal(labels[b].cpu().numpy(), lab)
         assert score[b].item() == sc
 
 
