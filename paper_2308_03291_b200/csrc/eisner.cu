@@ -570,14 +570,17 @@ size_t kuhl_smem(int n) {
 
 __device__ __forceinline__ int pk2(int i, int j, int N) { return i * (N - 1) - (i * (i - 1)) / 2 + (j - i - 1); }
 
+// kGlobal: table and back pointers in global scratch (n beyond shared memory)
+template <bool kGlobal>
 __global__ void __launch_bounds__(kThreads, 2) kuhlmann_kernel(const float* __restrict__ adj_all, int n, int single,
                                                                int32_t* __restrict__ heads_all,
                                                                double* __restrict__ score,
-                                                               int32_t* __restrict__ status) {
+                                                               int32_t* __restrict__ status, char* __restrict__ gscr) {
   extern __shared__ __align__(16) char smraw[];
   const int N = n + 2;
   const int T = N * (N - 1) / 2;
-  double* tab = (double*)smraw;
+  double* tab = kGlobal ? (double*)(gscr + (size_t)blockIdx.x * (((size_t)T * 12 + 15) & ~(size_t)15))
+                       : (double*)smraw;
   int* back = (int*)(tab + T);  // (k << 1) | (head == j)
   __shared__ double rw_c;
   __shared__ int badsh;
@@ -694,13 +697,19 @@ __global__ void __launch_bounds__(kThreads, 2) kuhlmann_kernel(const float* __re
   }
 }
 
+bool eisner_fast_ok(int n) { return n <= kMaxN && eisner_smem(n) <= 227 * 1024; }
+
 int eisner_check(int64_t B, int n) {
   if (B < 0 || n < 1) return SDB_ERR_ARG;
-  if (n > kMaxN || eisner_smem(n) > 227 * 1024) return SDB_ERR_UNSUPPORTED;
+  if (n > 4096) return SDB_ERR_UNSUPPORTED;
   return SDB_OK;
 }
 
 }  // namespace
+
+// eisner_gen.cu: fp64 charts in global memory for n > 128
+int eisner_gen_launch(const float* adj, int64_t B, int n, int single, double* logz, float* marg, int32_t* status,
+                      cudaStream_t s);
 
 extern "C" int sdb_eisner(const float* adjacency, int64_t B, int32_t n, int32_t single_root, double* logz,
                           float* marg, int32_t* status, void* stream) {
@@ -708,6 +717,8 @@ extern "C" int sdb_eisner(const float* adjacency, int64_t B, int32_t n, int32_t 
   if (rc) return rc;
   if (!adjacency || !logz || !status) return SDB_ERR_ARG;
   if (B == 0) return SDB_OK;
+  if (!eisner_fast_ok(n))
+    return eisner_gen_launch(adjacency, B, n, single_root ? 1 : 0, logz, marg, status, (cudaStream_t)stream);
   const size_t smem = eisner_smem(n);
   const size_t smem_lin = (size_t)7 * (n * (n + 1) / 2) * 4;  // the seven charts only
   cudaStream_t s = (cudaStream_t)stream;
@@ -726,14 +737,25 @@ extern "C" int sdb_eisner(const float* adjacency, int64_t B, int32_t n, int32_t 
 extern "C" int sdb_kuhlmann(const float* adjacency, int64_t B, int32_t n, int32_t single_root, int32_t* heads,
                             double* score, int32_t* status, void* stream) {
   if (B < 0 || n < 1) return SDB_ERR_ARG;
-  if (kuhl_smem(n) > 227 * 1024) return SDB_ERR_UNSUPPORTED;
+  if (n > 8192) return SDB_ERR_UNSUPPORTED;
   if (!adjacency || !heads || !score || !status) return SDB_ERR_ARG;
   if (B == 0) return SDB_OK;
+  cudaStream_t s = (cudaStream_t)stream;
   const size_t smem = kuhl_smem(n);
-  if (sdb_set_smem((const void*)kuhlmann_kernel, smem) != cudaSuccess)
+  if (smem > 227 * 1024) {  // tables in stream-ordered global scratch (no workspace argument)
+    const size_t N2 = n + 2, T = N2 * (N2 - 1) / 2;
+    void* scr = nullptr;
+    if (sdb_note(cudaMallocAsync(&scr, (size_t)B * ((T * 12 + 15) & ~(size_t)15), s)) != cudaSuccess)
+      return SDB_ERR_CUDA;
+    kuhlmann_kernel<true><<<(unsigned)B, kThreads, 0, s>>>(adjacency, n, single_root ? 1 : 0, heads, score, status,
+                                                          (char*)scr);
+    SDB_CHECK_LAUNCH();
+    return sdb_note(cudaFreeAsync(scr, s)) == cudaSuccess ? SDB_OK : SDB_ERR_CUDA;
+  }
+  if (sdb_set_smem((const void*)kuhlmann_kernel<false>, smem) != cudaSuccess)
     return SDB_ERR_CUDA;
-  kuhlmann_kernel<<<(unsigned)B, kThreads, smem, (cudaStream_t)stream>>>(adjacency, n, single_root ? 1 : 0, heads,
-                                                                         score, status);
+  kuhlmann_kernel<false><<<(unsigned)B, kThreads, smem, s>>>(adjacency, n, single_root ? 1 : 0, heads, score, status,
+                                                             nullptr);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
 }

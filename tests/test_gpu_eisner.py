@@ -39,7 +39,7 @@ def test_spanning_golden_api(case):
 
 
 @pytest.mark.parametrize("single", [False, True])
-@pytest.mark.parametrize("B,n", [(4, 128), (6, 9), (3, 1), (3, 2), (2, 50)])
+@pytest.mark.parametrize("B,n", [(4, 128), (6, 9), (3, 1), (3, 2), (2, 50), (2, 160), (1, 203)])  # n > 128: eisner_gen.cu
 def test_eisner_batched_vs_oracle(B, n, single):
     need_gpu()
     adj = batch_spanning(3000, B, n)
