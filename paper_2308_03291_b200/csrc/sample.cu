@@ -321,7 +321,9 @@ __global__ void __launch_bounds__(kT) tree_sample_kernel(const float* __restrict
   const bool alive = ins[n - 1] > ninfd();
   status[b] = alive ? SDB_ST_OK : SDB_ST_VACUOUS;
   int64_t pos = 0;
-  __shared__ int si[2 * 128], sj[2 * 128];  // walk stack (n <= 128), thread 0 only
+  extern __shared__ int tstk[];  // walk stack [2][2n] (dynamic), thread 0 only
+  int* si = tstk;
+  int* sj = tstk + 2 * n;
   if (alive) {
     for (int r = 0; r < num; ++r) {
       int32_t* lab = lab_all + ((size_t)b * num + r) * n * n;
@@ -431,7 +433,10 @@ __global__ void __launch_bounds__(kT) eisner_decode_kernel(const float* __restri
   }
   const bool alive = zroot > ninfd();
   status[b] = alive ? SDB_ST_OK : SDB_ST_VACUOUS;
-  __shared__ int sk[8 * 130], si[8 * 130], sj[8 * 130];  // walk stack (n <= 128), thread 0 only
+  extern __shared__ int estk[];  // walk stack [3][8 (n+2)] (dynamic), thread 0 only
+  int* sk = estk;
+  int* si = estk + 8 * (n + 2);
+  int* sj = estk + 16 * (n + 2);
   if (alive) {
     for (int r = 0; r < num; ++r) {
       int32_t* heads = heads_all + ((size_t)b * num + r) * N;
@@ -534,12 +539,14 @@ extern "C" int sdb_tree_sample(const float* span_potentials, int64_t B, int32_t 
                                int64_t noise_per_instance, int32_t num, int32_t* labels, int32_t* used,
                                int32_t* status, void* workspace, size_t ws_bytes, void* stream) {
   if (B < 0 || n < 1 || m < 1 || num < 1) return SDB_ERR_ARG;
-  if (n > 128) return SDB_ERR_UNSUPPORTED;
+  if (n > 8192) return SDB_ERR_UNSUPPORTED;
   if (!span_potentials || !noise || !labels || !used || !status) return SDB_ERR_ARG;
   if (noise_per_instance < (int64_t)num * ((2 * n - 1) * (int64_t)m + (int64_t)n * n)) return SDB_ERR_ARG;
   if (B == 0) return SDB_OK;
   if (!workspace || ws_bytes < sdb_tree_sample_workspace(B, n, m)) return SDB_ERR_WORKSPACE;
-  tree_sample_kernel<<<(unsigned)B, kT, 0, (cudaStream_t)stream>>>(span_potentials, n, m, noise, noise_per_instance,
+  const size_t stk = (size_t)4 * n * sizeof(int);
+  if (sdb_set_smem((const void*)tree_sample_kernel, stk) != cudaSuccess) return SDB_ERR_CUDA;
+  tree_sample_kernel<<<(unsigned)B, kT, stk, (cudaStream_t)stream>>>(span_potentials, n, m, noise, noise_per_instance,
                                                                   num, (double*)workspace, labels, used, status);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
@@ -552,18 +559,22 @@ extern "C" int sdb_eisner_decode(const float* adjacency, int64_t B, int32_t n, i
                                  const double* noise, int64_t noise_per_instance, int32_t num, int32_t* heads,
                                  int32_t* used, int32_t* status, void* workspace, size_t ws_bytes, void* stream) {
   if (B < 0 || n < 1 || num < 1) return SDB_ERR_ARG;
-  if (n > 128) return SDB_ERR_UNSUPPORTED;
+  if (n > 2000) return SDB_ERR_UNSUPPORTED;
   if (!adjacency || !heads || !used || !status) return SDB_ERR_ARG;
   if (noise && noise_per_instance < (int64_t)num * (n + 4 * (int64_t)(n + 1) * (n + 1))) return SDB_ERR_ARG;
   if (B == 0) return SDB_OK;
   if (!workspace || ws_bytes < sdb_eisner_decode_workspace(B, n)) return SDB_ERR_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
+  const size_t stk = (size_t)24 * (n + 2) * sizeof(int);
+  if (sdb_set_smem(noise ? (const void*)eisner_decode_kernel<false> : (const void*)eisner_decode_kernel<true>, stk) !=
+      cudaSuccess)
+    return SDB_ERR_CUDA;
   if (noise)
-    eisner_decode_kernel<false><<<(unsigned)B, kT, 0, s>>>(adjacency, n, single_root, noise, noise_per_instance, num,
-                                                          (double*)workspace, heads, used, status);
+    eisner_decode_kernel<false><<<(unsigned)B, kT, stk, s>>>(adjacency, n, single_root, noise, noise_per_instance, num,
+                                                            (double*)workspace, heads, used, status);
   else
-    eisner_decode_kernel<true><<<(unsigned)B, kT, 0, s>>>(adjacency, n, single_root, nullptr, 0, num,
-                                                         (double*)workspace, heads, used, status);
+    eisner_decode_kernel<true><<<(unsigned)B, kT, stk, s>>>(adjacency, n, single_root, nullptr, 0, num,
+                                                           (double*)workspace, heads, used, status);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
 }

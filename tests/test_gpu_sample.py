@@ -94,9 +94,10 @@ def test_ctc_sample_vs_oracle():
             np.testing.assert_array_equal(states[b, r].cpu().numpy(), O.ctc_sample(fp[b], tg[b], rng))
 
 
-def test_tree_sample_vs_oracle():
+@pytest.mark.parametrize("n", [24, 140])  # 140: past the old 128-span walk stack
+def test_tree_sample_vs_oracle(n):
     need_gpu()
-    B, n, m, num = 3, 24, 6, 2
+    B, m, num = 3, 6, 2
     th = batch_tree(73, B, n, m)
     cnt = K.stream_len("tree", dict(n=n, m=m))
     noise = torch.stack([torch.as_tensor(np.random.default_rng(s).gumbel(size=num * cnt)) for s in _seeds(B)]).cuda()
@@ -108,10 +109,11 @@ def test_tree_sample_vs_oracle():
             np.testing.assert_array_equal(labels[b, r].cpu().numpy(), O.tree_sample(th[b], rng))
 
 
+@pytest.mark.parametrize("n", [40, 150])
 @pytest.mark.parametrize("single", [False, True])
-def test_eisner_sample_and_max_decode_vs_oracle(single):
+def test_eisner_sample_and_max_decode_vs_oracle(single, n):
     need_gpu()
-    B, n, num = 3, 40, 2
+    B, num = 3, 2
     adj = batch_spanning(74, B, n)
     cnt = K.stream_len("eisner", dict(n=n))
     noise = torch.stack([torch.as_tensor(np.random.default_rng(s).gumbel(size=num * cnt)) for s in _seeds(B)]).cuda()
