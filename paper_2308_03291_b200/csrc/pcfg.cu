@@ -197,21 +197,21 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
       for (int k = i + lane; k < j; k += 32) sm = fmax(sm, isc[i * n + k] + isc[(k + 1) * n + j]);
       sm = warp_maxd(sm);
       if (lane == 0) smx[i] = sm;
-      float acc[3][32];
+      // slot 0: the interior splits (both children wide); at w == 2 the single split (PT, PT)
+      float acc[32];
 #pragma unroll
-      for (int sl = 0; sl < 3; ++sl)
-#pragma unroll
-        for (int q = 0; q < 32; ++q) acc[sl][q] = 0.f;
+      for (int q = 0; q < 32; ++q) acc[q] = 0.f;
+      const int klo = (w == 2) ? i : i + 1, khi = (w == 2) ? j : j - 1;
       if (sm != ninfd()) {
         // four splits per pass: their (L2-resident) chart loads are all issued before the
         // shuffle/FMA work, so one L2 latency is exposed per pass instead of per split
-        for (int k0 = i; k0 < j; k0 += 4) {
+        for (int k0 = klo; k0 < khi; k0 += 4) {
           double sk[4];
           float lv[4], rv[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const int k = min(k0 + u, j - 1);
-            sk[u] = (k0 + u < j) ? isc[i * n + k] + isc[(k + 1) * n + j] : ninfd();
+            const int k = min(k0 + u, khi - 1);
+            sk[u] = (k0 + u < khi) ? isc[i * n + k] + isc[(k + 1) * n + j] : ninfd();
             lv[u] = iu[(size_t)(i * n + k) * 32 + lane];
             rv[u] = iu[(size_t)((k + 1) * n + j) * 32 + lane];  // lane = C
           }
@@ -222,30 +222,16 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
           __syncwarp();
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const int k = k0 + u;
             if (sk[u] == ninfd()) continue;
             const float rf = rv[u] * fexp((float)(sk[u] - sm));
-            const int sl = (w == 2) ? 0 : (k == i ? 1 : (k == j - 1 ? 2 : 0));
             const float4* l4 = reinterpret_cast<const float4*>(lvs[warp][u]);
 #pragma unroll
             for (int q4 = 0; q4 < 8; ++q4) {
               const float4 lb = l4[q4];
-              if (sl == 0) {
-                acc[0][4 * q4 + 0] = fmaf(lb.x, rf, acc[0][4 * q4 + 0]);
-                acc[0][4 * q4 + 1] = fmaf(lb.y, rf, acc[0][4 * q4 + 1]);
-                acc[0][4 * q4 + 2] = fmaf(lb.z, rf, acc[0][4 * q4 + 2]);
-                acc[0][4 * q4 + 3] = fmaf(lb.w, rf, acc[0][4 * q4 + 3]);
-              } else if (sl == 1) {
-                acc[1][4 * q4 + 0] = fmaf(lb.x, rf, acc[1][4 * q4 + 0]);
-                acc[1][4 * q4 + 1] = fmaf(lb.y, rf, acc[1][4 * q4 + 1]);
-                acc[1][4 * q4 + 2] = fmaf(lb.z, rf, acc[1][4 * q4 + 2]);
-                acc[1][4 * q4 + 3] = fmaf(lb.w, rf, acc[1][4 * q4 + 3]);
-              } else {
-                acc[2][4 * q4 + 0] = fmaf(lb.x, rf, acc[2][4 * q4 + 0]);
-                acc[2][4 * q4 + 1] = fmaf(lb.y, rf, acc[2][4 * q4 + 1]);
-                acc[2][4 * q4 + 2] = fmaf(lb.z, rf, acc[2][4 * q4 + 2]);
-                acc[2][4 * q4 + 3] = fmaf(lb.w, rf, acc[2][4 * q4 + 3]);
-              }
+              acc[4 * q4 + 0] = fmaf(lb.x, rf, acc[4 * q4 + 0]);
+              acc[4 * q4 + 1] = fmaf(lb.y, rf, acc[4 * q4 + 1]);
+              acc[4 * q4 + 2] = fmaf(lb.z, rf, acc[4 * q4 + 2]);
+              acc[4 * q4 + 3] = fmaf(lb.w, rf, acc[4 * q4 + 3]);
             }
           }
           __syncwarp();  // the slots are rewritten by the next pass
@@ -253,9 +239,31 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
       }
       float* pp = dst + (size_t)i * 3 * 1024;
 #pragma unroll
-      for (int sl = 0; sl < 3; ++sl)
+      for (int q = 0; q < 32; ++q) pp[q * 32 + lane] = acc[q];  // [slot 0][B][C]
+      // slots 1 (k = i: (PT, NT)) and 2 (k = j-1: (NT, PT)) hold ONE split each: rank-1
+      // outer products written directly (no accumulator registers)
+      if (w > 2) {
+#pragma unroll 1
+        for (int e = 0; e < 2; ++e) {
+          const int k = e == 0 ? i : j - 1;
+          const double skk = isc[i * n + k] + isc[(k + 1) * n + j];
+          const bool live = (sm != ninfd()) && (skk != ninfd());
+          const float rf = live ? iu[(size_t)((k + 1) * n + j) * 32 + lane] * fexp((float)(skk - sm)) : 0.f;
+          lvs[warp][0][lane] = iu[(size_t)(i * n + k) * 32 + lane];
+          __syncwarp();
+          const float4* l4 = reinterpret_cast<const float4*>(lvs[warp][0]);
+          float* pe = pp + (1 + e) * 1024;
 #pragma unroll
-        for (int q = 0; q < 32; ++q) pp[sl * 1024 + q * 32 + lane] = acc[sl][q];  // [slot][B][C]
+          for (int q4 = 0; q4 < 8; ++q4) {
+            const float4 lb = l4[q4];
+            pe[(4 * q4 + 0) * 32 + lane] = lb.x * rf;
+            pe[(4 * q4 + 1) * 32 + lane] = lb.y * rf;
+            pe[(4 * q4 + 2) * 32 + lane] = lb.z * rf;
+            pe[(4 * q4 + 3) * 32 + lane] = lb.w * rf;
+          }
+          __syncwarp();
+        }
+      }
     }
   };
 
