@@ -36,12 +36,15 @@ int pcfg_gen_launch(int mode, const float* root, const float* rules, const float
 
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 256;  // pcfg_max_kernel
 constexpr int kWarps = kThreads / 32;
-constexpr int kSpW = 8;    // spans per warp (register block); n <= 64
+constexpr int kPT = 512;       // pcfg_kernel: 16 warps (<= 128 registers) for latency hiding
+constexpr int kPWarps = kPT / 32;
+constexpr int kSpW = 4;    // spans per warp (register block); n <= 64 = kSpW * kPWarps
 constexpr int kBS = 4;     // B-slice width
 constexpr int kMaxN = 64;
 constexpr int kCP = 8;     // outside parents per shared-memory chunk
+static_assert(kPWarps == 2 * kCP && kSpW * kPWarps >= 64, "pcfg_kernel warp roles");
 
 struct PcfgWs {
   float* RE;    // [B][4][32 A][32 B][32 C]  exp(rules) per child-class block t, zero padded
@@ -83,7 +86,7 @@ __device__ __forceinline__ void cpa_commit_wait() {
 }
 
 // inner[q] += sum_{slot, bb, C} R_t[A = lane][B'][C'] P[s_q][slot][bb][C] for the QN spans
-// s_q = warp + q kWarps of this warp (one B-slice of the inside contraction)
+// s_q = warp + q kPWarps of this warp (one B-slice of the inside contraction)
 template <int QN>
 __device__ __forceinline__ void contract_slice(const float* __restrict__ RTs, const float* __restrict__ Ps, int nslot,
                                                int warp, int lane, float* inner) {
@@ -97,7 +100,7 @@ __device__ __forceinline__ void contract_slice(const float* __restrict__ RTs, co
         const float r3 = RTs[((sl * kBS + bb) * 32 + C + 3) * 32 + lane];
 #pragma unroll
         for (int q = 0; q < QN; ++q) {
-          const int sp = warp + q * kWarps;
+          const int sp = warp + q * kPWarps;
           const float4 p = *reinterpret_cast<const float4*>(&Ps[((sp * 3 + sl) * kBS + bb) * 32 + C]);
           inner[q] = fmaf(r0, p.x, fmaf(r1, p.y, fmaf(r2, p.z, fmaf(r3, p.w, inner[q]))));
         }
@@ -123,7 +126,7 @@ struct PcfgGradOut {
 // kMode: 0 = log Z, 1 = + span marginals, 2 = + rule / root / emission
 // expected counts (the full pcfg_gradients, constituency.py:292-340)
 template <int kMode>
-__global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
+__global__ void __launch_bounds__(kPT, 1) pcfg_kernel(
     const float* __restrict__ root_all, const float* __restrict__ rules_all, const float* __restrict__ emis_all,
     const float* __restrict__ sticky_all, int n, int NT, int PT, PcfgWs ws, double* __restrict__ logz,
     float* __restrict__ marg_all, PcfgGradOut gout, int32_t* __restrict__ status) {
@@ -145,8 +148,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
   __shared__ int badsh;
   __shared__ double smax_s[kMaxN];
   __shared__ double smax2_s[kMaxN];
-  __shared__ __align__(16) float svs[kWarps][2][32];  // per-warp sibling vectors (push dot products)
-  __shared__ __align__(16) float lvs[kWarps][4][32];  // per-warp left-child vectors (P-build)
+  __shared__ __align__(16) float svs[kPWarps][2][32];  // per-warp sibling vectors (push dot products)
+  __shared__ __align__(16) float lvs[kPWarps][4][32];  // per-warp left-child vectors (P-build)
   float* P2 = kMode == 2 ? ws.P2 + (size_t)b * n * 3 * 1024 : nullptr;
   float* G = kMode == 2 ? ws.G + (size_t)b * 4 * 32768 : nullptr;
   if (tid == 0) badsh = 0;
@@ -157,8 +160,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
   // input checks
   {
     int bad = 0;
-    for (int e = tid; e < NT * S * S; e += kThreads) bad |= bad_input(rules[e]);
-    for (int e = tid; e < 4 * 32768; e += kThreads) {
+    for (int e = tid; e < NT * S * S; e += kPT) bad |= bad_input(rules[e]);
+    for (int e = tid; e < 4 * 32768; e += kPT) {
       const int t = e >> 15, r = e & 32767;
       const int A = r >> 10, Bi = (r >> 5) & 31, C = r & 31;
       float v = 0.f;
@@ -167,17 +170,17 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
       RE[e] = v;                                              // [t][A][B][C]
       RT[(((size_t)t * 32 + Bi) * 32 + C) * 32 + A] = v;      // [t][B][C][A]
     }
-    for (int e = tid; e < NT; e += kThreads) bad |= bad_input(root[e]);
-    for (int e = tid; e < n * PT; e += kThreads) bad |= bad_input(emis[e]);
+    for (int e = tid; e < NT; e += kPT) bad |= bad_input(root[e]);
+    for (int e = tid; e < n * PT; e += kPT) bad |= bad_input(emis[e]);
     if (sticky)
-      for (int e = tid; e < n * n; e += kThreads) bad |= !(sticky[e] == 0.f || sticky[e] == ninf());
+      for (int e = tid; e < n * n; e += kPT) bad |= !(sticky[e] == 0.f || sticky[e] == ninf());
     if (bad) atomicOr(&badsh, 1);
     if (kMode == 2)
-      for (int e = tid; e < 4 * 32768; e += kThreads) G[e] = 0.f;
+      for (int e = tid; e < 4 * 32768; e += kPT) G[e] = 0.f;
   }
   __syncthreads();
   // ---- width 1: preterminal slots (constituency.py:257-258)
-  for (int i = warp; i < n; i += kWarps) {
+  for (int i = warp; i < n; i += kPWarps) {
     const float x = (lane < PT) ? emis[i * PT + lane] : ninf();
     const float m = warp_max(x);
     const float st = STK(i, i);
@@ -191,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
   // f_k = exp(s_ik + s_(k+1)j - Smax); Smax -> smx[i]
   auto pbuild = [&](int w, float* dst, double* smx) {
     const int nsp = n - w + 1;
-    for (int i = warp; i < nsp; i += kWarps) {
+    for (int i = warp; i < nsp; i += kPWarps) {
       const int j = i + w - 1;
       double sm = ninfd();
       for (int k = i + lane; k < j; k += 32) sm = fmax(sm, isc[i * n + k] + isc[(k + 1) * n + j]);
@@ -284,12 +287,12 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
     for (int b0 = 0; b0 < 32; b0 += kBS) {
       // stage R slice RTs[sl][bb][C][A] (4 KB contiguous per (sl, bb)) and the P slice
       // Ps[s][sl][bb][C] (512 B contiguous per (s, sl)) with 16-byte cp.async
-      for (int e = tid; e < nslot * kBS * 256; e += kThreads) {
+      for (int e = tid; e < nslot * kBS * 256; e += kPT) {
         const int sl = e / (kBS * 256), r = e - sl * (kBS * 256);
         const int t = slot_type(sl, w);
         cpa16(RTs + sl * kBS * 1024 + 4 * r, RT + ((size_t)t * 32 + b0) * 1024 + 4 * r);
       }
-      for (int e = tid; e < nsp * nslot * 32; e += kThreads) {
+      for (int e = tid; e < nsp * nslot * 32; e += kPT) {
         const int s2 = e / (nslot * 32), r = e - s2 * (nslot * 32);
         const int sl = r >> 5, q = r & 31;
         cpa16(Ps + (s2 * 3 + sl) * kBS * 32 + 4 * q, Pw + (size_t)s2 * 3 * 1024 + sl * 1024 + b0 * 32 + 4 * q);
@@ -298,7 +301,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
       __syncthreads();
       // the warp's span count qn is warp-uniform: dispatch to a body with exactly qn spans so
       // wide widths (few spans) do not issue the idle span slots
-      const int qn = nsp > warp ? min(kSpW, (nsp - warp + kWarps - 1) / kWarps) : 0;
+      const int qn = nsp > warp ? min(kSpW, (nsp - warp + kPWarps - 1) / kPWarps) : 0;
       switch (qn) {
         case 8: contract_slice<8>(RTs, Ps, nslot, warp, lane, inner); break;
         case 7: contract_slice<7>(RTs, Ps, nslot, warp, lane, inner); break;
@@ -315,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
     // ---- normalise and store the width's cells (constituency.py:264-265)
 #pragma unroll
     for (int q = 0; q < kSpW; ++q) {
-      const int i = warp + q * kWarps;
+      const int i = warp + q * kPWarps;
       if (i < nsp) {
         const int j = i + w - 1;
         const float v = (lane < NT) ? inner[q] : 0.f;
@@ -351,18 +354,18 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
   float* mg = marg_all + (size_t)b * n * n;
   const int S2 = S * S;
   if (Z == ninfd() || badsh) {
-    for (int e = tid; e < n * n; e += kThreads) mg[e] = 0.f;
+    for (int e = tid; e < n * n; e += kPT) mg[e] = 0.f;
     if (kMode == 2) {
-      for (int e = tid; e < NT; e += kThreads) gout.root[(size_t)b * NT + e] = 0.f;
-      for (int e = tid; e < NT * S2; e += kThreads) gout.rules[(size_t)b * NT * S2 + e] = 0.f;
-      for (int e = tid; e < n * PT; e += kThreads) gout.emis[(size_t)b * n * PT + e] = 0.f;
+      for (int e = tid; e < NT; e += kPT) gout.root[(size_t)b * NT + e] = 0.f;
+      for (int e = tid; e < NT * S2; e += kPT) gout.rules[(size_t)b * NT * S2 + e] = 0.f;
+      for (int e = tid; e < n * PT; e += kPT) gout.emis[(size_t)b * n * PT + e] = 0.f;
     }
     return;
   }
 
   // =============================================================== outside
-  for (int e = tid; e < n * n; e += kThreads) osc[e] = ninfd();
-  for (int e = tid; e < n * n * 32; e += kThreads) ou[e] = 0.f;
+  for (int e = tid; e < n * n; e += kPT) osc[e] = ninfd();
+  for (int e = tid; e < n * n * 32; e += kPT) ou[e] = 0.f;
   __syncthreads();
   if (warp == 0) {
     const float r = (lane < NT) ? root[lane] : ninf();
@@ -384,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
       float* Cs = smf + 3 * kBS * 1024 + kMaxN * 3 * kBS * 32;  // [nsp][32 A]
       pbuild(w, P2, smax2_s);
       __syncthreads();
-      for (int e = tid; e < nsp * 32; e += kThreads) {
+      for (int e = tid; e < nsp * 32; e += kPT) {
         const int s2 = e >> 5, A = e & 31, i = s2, j = s2 + w - 1;
         const double c = osc[i * n + j] + (double)STK(i, j) + smax2_s[s2] - Z;
         Cs[e] = (A < NT && c != ninfd()) ? (float)(exp(c) * (double)ou[(size_t)(i * n + j) * 32 + A]) : 0.f;
@@ -392,8 +395,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
       __syncthreads();
       for (int sl = 0; sl < nslot; ++sl) {
         float* Gt = G + (size_t)slot_type(sl, w) * 32768;
-        for (int r = 0; r < 4; ++r) {
-          const int bc = tid + kThreads * r;
+        for (int r = 0; r < 1024 / kPT; ++r) {
+          const int bc = tid + kPT * r;
           float acc[32];
 #pragma unroll
           for (int A = 0; A < 32; ++A) acc[A] = 0.f;
@@ -415,14 +418,14 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
     for (int c0 = 0; c0 < nsp; c0 += kCP) {
       const int cn = min(kCP, nsp - c0);
       // stage the chunk's parent outside vectors
-      for (int e = tid; e < cn * 32; e += kThreads) {
+      for (int e = tid; e < cn * 32; e += kPT) {
         const int pz = e >> 5, A = e & 31, s = c0 + pz;
         Os[A * kCP + pz] = (A < NT) ? ou[(size_t)(s * n + s + w - 1) * 32 + A] : 0.f;  // [A][parent]
       }
       // ---- Q-build: Q[p][slot][B][C] = sum_A o_p[A] R_t[A, B', C'] (warp = parent, lane = C);
       // R slices double-buffered through shared memory
       auto stage = [&](int b0, float* dst) {
-        for (int e = tid; e < nslot * 32 * 32; e += kThreads) {
+        for (int e = tid; e < nslot * 32 * 32; e += kPT) {
           const int sl = e >> 10, r = e & 1023;
           const int A = r >> 5, q = r & 31;
           const int t = slot_type(sl, w);
@@ -440,44 +443,45 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
           asm volatile("cp.async.wait_group 0;\n" ::);
         }
         __syncthreads();
-        // register-tiled: thread = (4 parents, 3 slots) x one (bb, C) column, so every R word
-        // loaded from shared memory feeds 4 FMAs and every parent weight 3 (was 1 R load per FMA)
+        // register-tiled: thread = (2 parents, 3 slots) x one (bb, C) column, so every R word
+        // loaded from shared memory feeds 2 FMAs and every parent weight 3
         {
-          static_assert(kCP == 8 && kThreads == 256 && kBS * 32 == 128, "Q-build tiling");
-          const int pg = tid >> 7, c = tid & 127;  // parents 4pg..4pg+3 (warp-uniform), column c
-          if (4 * pg < cn) {
-            float q[4][3];
+          static_assert(kCP == 8 && kPT == 512 && kBS * 32 == 128, "Q-build tiling");
+          const int pg = tid >> 7, c = tid & 127;  // parents 2pg, 2pg+1 (warp-uniform), column c
+          if (2 * pg < cn) {
+            float q[2][3];
 #pragma unroll
-            for (int pp = 0; pp < 4; ++pp)
+            for (int pp = 0; pp < 2; ++pp)
 #pragma unroll
               for (int sl = 0; sl < 3; ++sl) q[pp][sl] = 0.f;
             for (int A = 0; A < NT; ++A) {
-              float o[4], r[3];
-              {
-                const float4 o4 = *reinterpret_cast<const float4*>(&Os[A * kCP + 4 * pg]);
-                o[0] = o4.x; o[1] = o4.y; o[2] = o4.z; o[3] = o4.w;
-              }
+              float r[3];
+              const float2 o2 = *reinterpret_cast<const float2*>(&Os[A * kCP + 2 * pg]);
+              const float o[2] = {o2.x, o2.y};
 #pragma unroll
               for (int sl = 0; sl < 3; ++sl) r[sl] = sl < nslot ? cur[(sl * 32 + A) * 128 + c] : 0.f;
 #pragma unroll
-              for (int pp = 0; pp < 4; ++pp)
+              for (int pp = 0; pp < 2; ++pp)
 #pragma unroll
                 for (int sl = 0; sl < 3; ++sl) q[pp][sl] = fmaf(o[pp], r[sl], q[pp][sl]);
             }
             const int bb = c >> 5, C = c & 31;
 #pragma unroll
-            for (int pp = 0; pp < 4; ++pp)
+            for (int pp = 0; pp < 2; ++pp)
 #pragma unroll
               for (int sl = 0; sl < 3; ++sl)
-                if (4 * pg + pp < cn && sl < nslot)
-                  Qc[(((4 * pg + pp) * 3 + sl) * 32 + b0 + bb) * 33 + C] = q[pp][sl];  // [B][C]
+                if (2 * pg + pp < cn && sl < nslot)
+                  Qc[(((2 * pg + pp) * 3 + sl) * 32 + b0 + bb) * 33 + C] = q[pp][sl];  // [B][C]
           }
         }
         __syncthreads();
       }
       // ---- pushes; parent scale = osc + sticky (constituency.py:303)
       for (int side = 0; side < 2; ++side) {
-        for (int pz = warp; pz < cn; pz += kWarps) {
+        // two warps per parent (kPWarps = 2 kCP): warp half h takes the split pairs
+        // (k, k+1), k = i + 2h (mod 4) -- the children of distinct splits are distinct
+        const int half = warp / kCP;
+        for (int pz = warp % kCP; pz < cn; pz += kCP) {
           const int s = c0 + pz;
           const int i = s, j = i + w - 1;
           const double ps = osc[i * n + j] + (double)STK(i, j);
@@ -543,13 +547,14 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
             if (lane == 0) osc[x.co] = M;  // this child is not touched again in this side pass
           };
           Item A, Bv;
-          fetch(i, A);
-          if (i + 1 < j) fetch(i + 1, Bv);
-          for (int k = i; k < j; k += 2) {
+          const int kf = i + 2 * half;
+          if (kf < j) fetch(kf, A);
+          if (kf + 1 < j) fetch(kf + 1, Bv);
+          for (int k = kf; k < j; k += 4) {
             const Item a = A, bq = Bv;
             const bool hb = k + 1 < j;
-            if (k + 2 < j) fetch(k + 2, A);
-            if (k + 3 < j) fetch(k + 3, Bv);
+            if (k + 4 < j) fetch(k + 4, A);
+            if (k + 5 < j) fetch(k + 5, Bv);
             // the sibling vectors go through per-warp shared slots and are read back as
             // 16-byte broadcasts (8 LDS.128 instead of 32 shuffles per dot product)
             svs[warp][0][lane] = a.sv;
@@ -567,7 +572,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
     }
   }
   // ---- span marginals (constituency.py:334-338)
-  for (int e = warp; e < n * n; e += kWarps) {
+  for (int e = warp; e < n * n; e += kPWarps) {
     const int i = e / n, j = e - i * n;
     float v = 0.f;
     if (i <= j) {
@@ -588,14 +593,14 @@ __global__ void __launch_bounds__(kThreads, 1) pcfg_kernel(
         (si == ninfd() || !(u > 0.f)) ? 0.f : (float)(exp((double)root[lane] + si - Z) * (double)u);
   }
   // emission gradient exp(outside[i,i,PT] + sticky[i,i] + emissions - Z) (constituency.py:327-329)
-  for (int i = warp; i < n; i += kWarps) {
+  for (int i = warp; i < n; i += kPWarps) {
     const int e = i * n + i;
     const double c = osc[e] + (double)STK(i, i) + isc[e] - Z;
     const float v = ou[(size_t)e * 32 + lane] * iu[(size_t)e * 32 + lane];
     if (lane < PT) gout.emis[((size_t)b * n + i) * PT + lane] = (c == ninfd() || !(v > 0.f)) ? 0.f : (float)(exp(c) * (double)v);
   }
   // rule gradient = G_t[A][B'][C'] * exp(rules[A][B][C])
-  for (int e = tid; e < NT * S2; e += kThreads) {
+  for (int e = tid; e < NT * S2; e += kPT) {
     const int A = e / S2, r = e - A * S2, Bf = r / S, Cf = r - Bf * S;
     const int t = (Bf < NT ? 0 : 1) + (Cf < NT ? 0 : 2);
     const int Bi = Bf - boff(t, NT), Ci = Cf - coff(t, NT);
@@ -812,7 +817,7 @@ int pcfg_launch(const float* root, const float* rules, const float* emissions, c
   const size_t smem = kMode == 0 ? smem_in : (smem_in > smem_out ? smem_in : smem_out);
   if (sdb_set_smem((const void*)pcfg_kernel<kMode>, smem) != cudaSuccess)
     return SDB_ERR_CUDA;
-  pcfg_kernel<kMode><<<(unsigned)B, kThreads, smem, s>>>(root, rules, emissions, sticky, n, NT, PT, ws, logz,
+  pcfg_kernel<kMode><<<(unsigned)B, kPT, smem, s>>>(root, rules, emissions, sticky, n, NT, PT, ws, logz,
                                                          span_marg, gout, status);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
