@@ -323,6 +323,46 @@ int sdb_chain_viterbi_lengths(const float* init, const float* trans, const int32
 int sdb_masked_dot(const float* marg, const float* theta, int64_t B, int64_t len, double* out, int32_t* neginf,
                    void* stream);
 
+/* ---- exact mode: float64 potentials in, float64 results out ----------------
+ * The reference computes in float64 on float64 inputs; these entry points do
+ * the same on the GPU (fp64 lattices / charts in the workspace, one CTA per
+ * instance, the reference recurrences restated one-for-one) for callers that
+ * compare at the reference's own tolerances.  Same layouts, statuses and
+ * nullable-marginal convention as the fp32 entry points above; no size limits
+ * beyond the workspace (alignment min(n, m) < 8192, CTC 2L+1 <= 12288,
+ * MTT n <= 2048, Eisner n <= 4096).
+ *   chain.py:64-95 / 250-298, alignment.py:62-118 / 248-301,
+ *   constituency.py:52-110 / 246-340, spanning.py:90-175 / 183-280. */
+size_t sdb_chain_fb_f64_workspace(int64_t B, int32_t n, int32_t m);
+int sdb_chain_fb_f64(const double* init, const double* trans, int64_t B, int32_t n, int32_t m, double* logz,
+                     double* marg_init, double* marg_trans, int32_t* status, void* workspace, size_t ws_bytes,
+                     void* stream);
+size_t sdb_semimarkov_fb_f64_workspace(int64_t B, int32_t n, int32_t s, int32_t m);
+int sdb_semimarkov_fb_f64(const double* segment_potentials, int64_t B, int32_t n, int32_t s, int32_t m, double* logz,
+                          double* marg, int32_t* status, void* workspace, size_t ws_bytes, void* stream);
+size_t sdb_nw_fb_f64_workspace(int64_t B, int32_t n, int32_t m);
+int sdb_nw_fb_f64(const double* theta, int64_t B, int32_t n, int32_t m, double* logz, double* marg, int32_t* status,
+                  void* workspace, size_t ws_bytes, void* stream);
+size_t sdb_ctc_fb_f64_workspace(int64_t B, int32_t T, int32_t V, int32_t L);
+int sdb_ctc_fb_f64(const double* frame_potentials, const int32_t* targets, int64_t B, int32_t T, int32_t V,
+                   int32_t L, double* logz, double* marg, int32_t* status, void* workspace, size_t ws_bytes,
+                   void* stream);
+size_t sdb_tree_fb_f64_workspace(int64_t B, int32_t n, int32_t m);
+int sdb_tree_fb_f64(const double* span_potentials, int64_t B, int32_t n, int32_t m, double* logz, double* marg,
+                    int32_t* status, void* workspace, size_t ws_bytes, void* stream);
+/* span_marg NULL: log Z only; groot / grules / gemis non-NULL (with span_marg): pcfg_gradients too. */
+size_t sdb_pcfg_f64_workspace(int64_t B, int32_t n, int32_t NT, int32_t PT, int32_t grad);
+int sdb_pcfg_f64(const double* root, const double* rules, const double* emissions, const double* sticky, int64_t B,
+                 int32_t n, int32_t NT, int32_t PT, double* logz, double* span_marg, double* groot, double* grules,
+                 double* gemis, int32_t* status, void* workspace, size_t ws_bytes, void* stream);
+size_t sdb_mtt_f64_workspace(int64_t B, int32_t n);
+int sdb_mtt_f64(const double* adjacency, int64_t B, int32_t n, int32_t single_root, double* logz, double* marg,
+                int32_t* status, void* workspace, size_t ws_bytes, void* stream);
+int sdb_eisner_f64(const double* adjacency, int64_t B, int32_t n, int32_t single_root, double* logz, double* marg,
+                   int32_t* status, void* stream);
+int sdb_masked_dot_f64(const double* marg, const double* theta, int64_t B, int64_t len, double* out,
+                       int32_t* neginf, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

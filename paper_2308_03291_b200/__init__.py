@@ -34,6 +34,7 @@ from .dist import (
     sample_info,
     structure_score,
 )
+from .dist import get_precision, set_precision  # noqa: F401  (exact fp64 mode)
 from .errors import (
     InvalidProblem,
     SamplerStepLimit,

@@ -22,6 +22,23 @@ _sz = ctypes.c_size_t
 # name -> (restype, argtypes); must mirror include/sdb200.h exactly.
 SIGNATURES = {
     "sdb_version": (ctypes.c_int, []),
+    "sdb_chain_fb_f64_workspace": (_sz, [_i64, _i32, _i32]),
+    "sdb_chain_fb_f64": (ctypes.c_int, [_c_p, _c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
+    "sdb_semimarkov_fb_f64_workspace": (_sz, [_i64, _i32, _i32, _i32]),
+    "sdb_semimarkov_fb_f64": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
+    "sdb_nw_fb_f64_workspace": (_sz, [_i64, _i32, _i32]),
+    "sdb_nw_fb_f64": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
+    "sdb_ctc_fb_f64_workspace": (_sz, [_i64, _i32, _i32, _i32]),
+    "sdb_ctc_fb_f64": (ctypes.c_int, [_c_p, _c_p, _i64, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
+    "sdb_tree_fb_f64_workspace": (_sz, [_i64, _i32, _i32]),
+    "sdb_tree_fb_f64": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
+    "sdb_pcfg_f64_workspace": (_sz, [_i64, _i32, _i32, _i32, _i32]),
+    "sdb_pcfg_f64": (ctypes.c_int, [_c_p, _c_p, _c_p, _c_p, _i64, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p,
+                                    _c_p, _c_p, _sz, _c_p]),
+    "sdb_mtt_f64_workspace": (_sz, [_i64, _i32]),
+    "sdb_mtt_f64": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
+    "sdb_eisner_f64": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p]),
+    "sdb_masked_dot_f64": (ctypes.c_int, [_c_p, _c_p, _i64, _i64, _c_p, _c_p, _c_p]),
     "sdb_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "sdb_last_cuda_error": (ctypes.c_char_p, []),
     "sdb_chain_fb_workspace": (_sz, [_i64, _i32, _i32]),

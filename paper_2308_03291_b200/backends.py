@@ -34,6 +34,17 @@ def _device():
     return device()
 
 
+# Exact mode (dist.set_precision("fp64")): log_partition / marginals / derived
+# quantities take float64 potentials to the sdb_*_f64 entry points (fp64 in and
+# out, like the reference); argmax and sampling keep their fp32-input kernels
+# (their arithmetic is fp64 already).
+EXACT = False
+
+
+def pot_dtype():
+    return torch.float64 if EXACT else torch.float32
+
+
 def to_dev(arrs, dtype=torch.float32):
     """Stack host arrays -> one pinned host tensor -> one async H2D copy."""
     host = torch.from_numpy(np.ascontiguousarray(np.stack(arrs))).to(dtype)
@@ -146,12 +157,12 @@ class ChainBackend(Backend):
     def argmax_algo(self, d):
         return "viterbi"
 
-    def _stack(self, ds):
+    def _stack(self, ds, dtype=torch.float32):
         """Same-length group -> ([B,m], [B,n-1,m,m], None); a ragged group (dist.batch_map
         with per-instance lengths) -> zero-padded layout + lengths [B] for the kernels."""
         ns = [d.n for d in ds]
         if len(set(ns)) == 1:
-            return to_dev([d.init for d in ds]), to_dev([d.transitions for d in ds]), None
+            return to_dev([d.init for d in ds], dtype), to_dev([d.transitions for d in ds], dtype), None
         n, m = max(ns), ds[0].m
         tr = np.zeros((len(ds), n - 1, m, m))
         for i, d in enumerate(ds):
@@ -160,7 +171,7 @@ class ChainBackend(Backend):
         return to_dev([d.init for d in ds]), to_dev(list(tr)), lengths
 
     def run(self, ds, marginals=True, full=False, dev=False):
-        init, trans, lengths = self._stack(ds)
+        init, trans, lengths = self._stack(ds, pot_dtype())
         logz, mi, mt, st = K.chain_fb(init, trans, marginals, lengths)
         marg = None
         if marginals and dev and lengths is None:
@@ -226,7 +237,7 @@ class AlignmentBackend(Backend):
         return "max-plus-needleman-wunsch"
 
     def run(self, ds, marginals=True, full=False, dev=False):
-        th = to_dev([d.move_potentials for d in ds])
+        th = to_dev([d.move_potentials for d in ds], pot_dtype())
         logz, marg, st = K.nw_fb(th, marginals)
         if marginals and dev:
             return Result(to_host(logz), to_host(st), None, self.vacuous_msg, dev={"move_potentials": marg})
@@ -286,12 +297,12 @@ class CTCBackend(Backend):
     def argmax_algo(self, d):
         return "max-plus-ctc"
 
-    def _stack(self, ds):
+    def _stack(self, ds, dtype=torch.float32):
         tg = to_dev([np.asarray(d.target, dtype=np.int64).reshape(-1) for d in ds], torch.int32)
-        return to_dev([d.frame_potentials for d in ds]), tg
+        return to_dev([d.frame_potentials for d in ds], dtype), tg
 
     def run(self, ds, marginals=True, full=False, dev=False):
-        fp, tg = self._stack(ds)
+        fp, tg = self._stack(ds, pot_dtype())
         logz, marg, st = K.ctc_fb(fp, tg, marginals)
         if marginals and dev:
             return Result(to_host(logz), to_host(st), None, self.vacuous_msg, dev={"frame_potentials": marg})
@@ -352,7 +363,7 @@ class TreeBackend(Backend):
         return "max-plus-cky"
 
     def run(self, ds, marginals=True, full=False, dev=False):
-        th = to_dev([d.span_potentials for d in ds])
+        th = to_dev([d.span_potentials for d in ds], pot_dtype())
         logz, marg, st = K.tree_fb(th, marginals)
         if marginals and dev:
             return Result(to_host(logz), to_host(st), None, self.vacuous_msg, dev={"span_potentials": marg})
@@ -428,7 +439,7 @@ class SpanningBackend(Backend):
 
     def run(self, ds, marginals=True, full=False, dev=False):
         d0 = ds[0]
-        adj = to_dev([d.adjacency for d in ds])
+        adj = to_dev([d.adjacency for d in ds], pot_dtype())
         if d0.projective:
             logz, marg, st = K.eisner(adj, d0.single_root_edge, marginals)
             msg = "no projective tree has finite score"
@@ -635,12 +646,12 @@ class PCFGBackend(Backend):
     def argmax_algo(self, d):
         return "max-plus-pcfg"
 
-    def _inputs(self, ds):
-        return (to_dev([d.root for d in ds]), to_dev([d.binary_rules for d in ds]), to_dev([d.emissions for d in ds]),
-                to_dev([d.sticky for d in ds]))
+    def _inputs(self, ds, dtype=torch.float32):
+        return (to_dev([d.root for d in ds], dtype), to_dev([d.binary_rules for d in ds], dtype),
+                to_dev([d.emissions for d in ds], dtype), to_dev([d.sticky for d in ds], dtype))
 
     def run(self, ds, marginals=True, full=False, dev=False):
-        root, rules, emis, sticky = self._inputs(ds)
+        root, rules, emis, sticky = self._inputs(ds, pot_dtype())
         if full:
             # potential_marginals: all four gradients of pcfg_gradients (constituency.py:292-340)
             logz, g, st = K.pcfg_grad(root, rules, emis, sticky)
@@ -665,8 +676,8 @@ class PCFGBackend(Backend):
         span_mask = np.full((d.n, d.n), -np.inf)
         for i, j in spans:
             span_mask[i, j] = 0.0
-        root, rules, emis, sticky = self._inputs([d, d])
-        sticky[0] = sticky[0] + torch.as_tensor(span_mask, dtype=torch.float32, device=sticky.device)
+        root, rules, emis, sticky = self._inputs([d, d], pot_dtype())
+        sticky[0] = sticky[0] + torch.as_tensor(span_mask, dtype=sticky.dtype, device=sticky.device)
         logz, _, st = K.pcfg_fb(root, rules, emis, sticky, marginals=False)
         lz, sth = to_host(logz), to_host(st)
         if (sth == K.ST_INVALID).any():
@@ -717,7 +728,7 @@ class SemiMarkovBackend(Backend):
         return "semi-markov-viterbi"
 
     def run(self, ds, marginals=True, full=False, dev=False):
-        th = to_dev([d.segment_potentials for d in ds])
+        th = to_dev([d.segment_potentials for d in ds], pot_dtype())
         logz, marg, st = K.semimarkov_fb(th, marginals)
         if marginals and dev:
             return Result(to_host(logz), to_host(st), None, self.vacuous_msg, dev={"segment_potentials": marg})

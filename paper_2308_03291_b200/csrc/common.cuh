@@ -46,6 +46,9 @@ __device__ __forceinline__ bool is_ninfd(double x) { return x == ninfd(); }
 // Input validity (numerics.py:22-29): NaN and +inf are rejected, -inf allowed.
 // NaN or +inf (one unordered compare: !(x < +inf))
 __device__ __forceinline__ bool bad_input(float x) { return !(x < __int_as_float(0x7f800000)); }
+// NaN or +inf for either precision (the exact-mode kernels read float64 potentials)
+__device__ __forceinline__ bool bad_value(float x) { return bad_input(x); }
+__device__ __forceinline__ bool bad_value(double x) { return !(x < __longlong_as_double(0x7ff0000000000000LL)); }
 
 // (max, sum exp(x - max)) accumulator for a log-sum-exp reduction.
 struct Lse {

@@ -33,10 +33,10 @@ struct Lab {
 };
 
 // kMode 0: log Z; 1: log Z + marginals [T][V]; 2: max-plus score + labels per frame
-template <int kMode>
-__global__ void __launch_bounds__(kT) ctc_gen_kernel(const float* __restrict__ fp_all, const int32_t* __restrict__ tg_all,
+template <int kMode, typename TP, typename M>  // TP / M: potential / marginal types (float64 = exact mode)
+__global__ void __launch_bounds__(kT) ctc_gen_kernel(const TP* __restrict__ fp_all, const int32_t* __restrict__ tg_all,
                                                      int T, int V, int L, double* __restrict__ ws_all,
-                                                     double* __restrict__ out, float* __restrict__ marg_all,
+                                                     double* __restrict__ out, M* __restrict__ marg_all,
                                                      int32_t* __restrict__ path_all, int32_t* __restrict__ status) {
   extern __shared__ __align__(16) double rows[];  // [2][S]
   __shared__ int bad_s;
@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(kT) ctc_gen_kernel(const float* __restrict__ f
   __shared__ int fin_s;
   const int b = blockIdx.x, tid = threadIdx.x;
   const int S = 2 * L + 1;
-  const float* fp = fp_all + (size_t)b * T * V;
+  const TP* fp = fp_all + (size_t)b * T * V;
   const Lab lab{tg_all + (size_t)b * L, S};
   double* A = kMode ? ws_all + (size_t)b * T * S : nullptr;
   auto E = [&](int t, int s) { return (double)__ldg(fp + (size_t)t * V + lab(s)); };
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(kT) ctc_gen_kernel(const float* __restrict__ f
   __syncthreads();
   {
     int bad = 0;
-    for (size_t e = tid; e < (size_t)T * V; e += kT) bad |= bad_input(__ldg(fp + e));
+    for (size_t e = tid; e < (size_t)T * V; e += kT) bad |= bad_value(__ldg(fp + e));
     for (int x = tid; x < L; x += kT) bad |= (lab.tg[x] < 1) | (lab.tg[x] >= V);
     if (bad) bad_s = 1;
   }
@@ -107,20 +107,20 @@ __global__ void __launch_bounds__(kT) ctc_gen_kernel(const float* __restrict__ f
   if (z == ninfd()) return;  // marginals were zeroed by the launcher; labels stay 0
   if (kMode == 1) {
     // backward (alignment.py:272-290) + posteriors scattered by label (291-301)
-    float* mg = marg_all + (size_t)b * T * V;
+    M* mg = marg_all + (size_t)b * T * V;
     double* nxt = prv;  // beta[t+1]
     double* now = cur;
     // blank states (even s) share label 0: reduced per warp before the atomic
     auto emit = [&](int t, int s, double p, double& pb) {
       if (s & 1) {
-        if (p > 0.0) atomicAdd(mg + (size_t)t * V + lab(s), (float)p);
+        if (p > 0.0) atomicAdd(mg + (size_t)t * V + lab(s), (M)p);
       } else {
         pb += p;
       }
     };
     auto flush_blank = [&](int t, double pb) {
       for (int o = 16; o > 0; o >>= 1) pb += __shfl_xor_sync(0xffffffffu, pb, o);
-      if ((tid & 31) == 0 && pb > 0.0) atomicAdd(mg + (size_t)t * V, (float)pb);
+      if ((tid & 31) == 0 && pb > 0.0) atomicAdd(mg + (size_t)t * V, (M)pb);
     };
     {
       double pb = 0.0;
@@ -176,22 +176,43 @@ size_t ctc_gen_workspace(int64_t B, int T, int L, int mode) {
   return mode ? (size_t)B * T * (2 * L + 1) * sizeof(double) + 256 : 0;
 }
 
-int ctc_gen_launch(int mode, const float* fp, const int32_t* tg, int64_t B, int T, int V, int L, void* ws,
-                   size_t ws_bytes, double* out, float* marg, int32_t* path, int32_t* status, cudaStream_t s) {
+template <typename TP, typename M>
+int ctc_gen_launch_t(int mode, const TP* fp, const int32_t* tg, int64_t B, int T, int V, int L, void* ws,
+                     size_t ws_bytes, double* out, M* marg, int32_t* path, int32_t* status, cudaStream_t s) {
   if (!ctc_gen_ok(L)) return SDB_ERR_UNSUPPORTED;
   if (ws_bytes < ctc_gen_workspace(B, T, L, mode) || (mode && !ws)) return SDB_ERR_WORKSPACE;
   const size_t smem = (size_t)2 * (2 * L + 1) * sizeof(double);
-  const void* k = mode == 0 ? (const void*)ctc_gen_kernel<0> : mode == 1 ? (const void*)ctc_gen_kernel<1>
-                                                                           : (const void*)ctc_gen_kernel<2>;
+  const void* k = mode == 0 ? (const void*)ctc_gen_kernel<0, TP, M>
+                            : mode == 1 ? (const void*)ctc_gen_kernel<1, TP, M> : (const void*)ctc_gen_kernel<2, TP, M>;
   if (sdb_set_smem(k, smem) != cudaSuccess) return SDB_ERR_CUDA;
   double* w = (double*)ws;
-  if (mode == 1 && sdb_note(cudaMemsetAsync(marg, 0, (size_t)B * T * V * sizeof(float), s)) != cudaSuccess)
+  if (mode == 1 && sdb_note(cudaMemsetAsync(marg, 0, (size_t)B * T * V * sizeof(M), s)) != cudaSuccess)
     return SDB_ERR_CUDA;
   if (mode == 2 && sdb_note(cudaMemsetAsync(path, 0, (size_t)B * T * sizeof(int32_t), s)) != cudaSuccess)
     return SDB_ERR_CUDA;
-  if (mode == 0) ctc_gen_kernel<0><<<(unsigned)B, kT, smem, s>>>(fp, tg, T, V, L, w, out, marg, path, status);
-  if (mode == 1) ctc_gen_kernel<1><<<(unsigned)B, kT, smem, s>>>(fp, tg, T, V, L, w, out, marg, path, status);
-  if (mode == 2) ctc_gen_kernel<2><<<(unsigned)B, kT, smem, s>>>(fp, tg, T, V, L, w, out, marg, path, status);
+  if (mode == 0) ctc_gen_kernel<0, TP, M><<<(unsigned)B, kT, smem, s>>>(fp, tg, T, V, L, w, out, marg, path, status);
+  if (mode == 1) ctc_gen_kernel<1, TP, M><<<(unsigned)B, kT, smem, s>>>(fp, tg, T, V, L, w, out, marg, path, status);
+  if (mode == 2) ctc_gen_kernel<2, TP, M><<<(unsigned)B, kT, smem, s>>>(fp, tg, T, V, L, w, out, marg, path, status);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
+}
+
+int ctc_gen_launch(int mode, const float* fp, const int32_t* tg, int64_t B, int T, int V, int L, void* ws,
+                   size_t ws_bytes, double* out, float* marg, int32_t* path, int32_t* status, cudaStream_t s) {
+  return ctc_gen_launch_t<float, float>(mode, fp, tg, B, T, V, L, ws, ws_bytes, out, marg, path, status, s);
+}
+
+// ---- exact mode (float64 frame potentials and marginals)
+extern "C" size_t sdb_ctc_fb_f64_workspace(int64_t B, int32_t T, int32_t V, int32_t L) {
+  (void)V;
+  return (B < 0 || T < 1 || L < 0) ? 0 : ctc_gen_workspace(B, T, L, 1);
+}
+extern "C" int sdb_ctc_fb_f64(const double* frame_potentials, const int32_t* targets, int64_t B, int32_t T, int32_t V,
+                              int32_t L, double* logz, double* marg, int32_t* status, void* workspace,
+                              size_t ws_bytes, void* stream) {
+  if (B < 0 || T < 1 || V < 1 || L < 0 || !frame_potentials || (L > 0 && !targets) || !logz || !status)
+    return SDB_ERR_ARG;
+  if (B == 0) return SDB_OK;
+  return ctc_gen_launch_t<double, double>(marg ? 1 : 0, frame_potentials, targets, B, T, V, L, workspace, ws_bytes,
+                                          logz, marg, nullptr, status, (cudaStream_t)stream);
 }

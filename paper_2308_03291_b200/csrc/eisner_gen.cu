@@ -31,15 +31,16 @@ struct WLse {
   }
 };
 
-__global__ void __launch_bounds__(kT) eisner_gen_kernel(const float* __restrict__ adj_all, int n, int single,
+template <typename TP, typename M>  // potential / marginal types (float64 = exact mode)
+__global__ void __launch_bounds__(kT) eisner_gen_kernel(const TP* __restrict__ adj_all, int n, int single,
                                                         double* __restrict__ ws_all, double* __restrict__ logz,
-                                                        float* __restrict__ marg_all, int32_t* __restrict__ status) {
+                                                        M* __restrict__ marg_all, int32_t* __restrict__ status) {
   __shared__ int bad_s;
   __shared__ double z_s;
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int N = n + 1;
   const size_t NN = (size_t)N * N;
-  const float* th = adj_all + (size_t)b * NN;
+  const TP* th = adj_all + (size_t)b * NN;
   double* cr = ws_all + (size_t)b * 8 * NN;
   double* cl = cr + NN;
   double* ir = cl + NN;
@@ -55,7 +56,7 @@ __global__ void __launch_bounds__(kT) eisner_gen_kernel(const float* __restrict_
   {
     int bad = 0;
     for (size_t e = tid; e < NN; e += kT) {
-      bad |= bad_input(__ldg(th + e));
+      bad |= bad_value(__ldg(th + e));
       const bool diag = (e / N) == (e % N);
       cr[e] = diag ? 0.0 : ninfd();
       cl[e] = diag ? 0.0 : ninfd();
@@ -108,13 +109,13 @@ __global__ void __launch_bounds__(kT) eisner_gen_kernel(const float* __restrict_
   __syncthreads();
   const double z = z_s;
   if (!marg_all || bad_s || z == ninfd()) return;  // marginals zeroed by the launcher
-  float* mg = marg_all + (size_t)b * NN;
+  M* mg = marg_all + (size_t)b * NN;
   // adjoints (spanning.py:224-280)
   if (single) {
     for (int c = 1 + tid; c <= n; c += kT) {
       const double t = T(0, c) + cl[at(1, c)] + cr[at(c, n)];
       const double p = t > ninfd() ? exp(t - z) : 0.0;
-      mg[at(0, c)] = (float)fmin(fmax(p, 0.0), 1.0);
+      mg[at(0, c)] = (M)fmin(fmax(p, 0.0), 1.0);
       bcl[at(1, c)] += p;
       bcr[at(c, n)] += p;
     }
@@ -148,7 +149,7 @@ __global__ void __launch_bounds__(kT) eisner_gen_kernel(const float* __restrict_
       {  // il[i, j]: arc j -> i
         const double bb = bil[ij], c = il[ij];
         if (bb > 0.0 && c > ninfd()) {
-          if (lane == 0) mg[at(j, i)] = (float)fmin(bb, 1.0);
+          if (lane == 0) mg[at(j, i)] = (M)fmin(bb, 1.0);
           const double fold = c - T(j, i);
           for (int k = i + lane; k < j; k += 32) {
             const double wt = bb * exp(cr[at(i, k)] + cl[at(k + 1, j)] - fold);
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(kT) eisner_gen_kernel(const float* __restrict_
       {  // ir[i, j]: arc i -> j
         const double bb = bir[ij], c = ir[ij];
         if (bb > 0.0 && c > ninfd()) {
-          if (lane == 0) mg[ij] = (float)fmin(bb, 1.0);
+          if (lane == 0) mg[ij] = (M)fmin(bb, 1.0);
           const double fold = c - T(i, j);
           for (int k = i + lane; k < j; k += 32) {
             const double wt = bb * exp(cr[at(i, k)] + cl[at(k + 1, j)] - fold);
@@ -181,15 +182,30 @@ bool eisner_gen_ok(int n) { return n <= 4096; }
 size_t eisner_gen_workspace(int64_t B, int n) { return (size_t)B * 8 * (n + 1) * (n + 1) * sizeof(double) + 256; }
 
 // no workspace argument in sdb_eisner: stream-ordered scratch
-int eisner_gen_launch(const float* adj, int64_t B, int n, int single, double* logz, float* marg, int32_t* status,
-                      cudaStream_t s) {
+template <typename TP, typename M>
+int eisner_gen_launch_t(const TP* adj, int64_t B, int n, int single, double* logz, M* marg, int32_t* status,
+                        cudaStream_t s) {
   if (!eisner_gen_ok(n)) return SDB_ERR_UNSUPPORTED;
   void* ws = nullptr;
   if (sdb_note(cudaMallocAsync(&ws, eisner_gen_workspace(B, n), s)) != cudaSuccess) return SDB_ERR_CUDA;
-  if (marg && sdb_note(cudaMemsetAsync(marg, 0, (size_t)B * (n + 1) * (n + 1) * sizeof(float), s)) != cudaSuccess)
+  if (marg && sdb_note(cudaMemsetAsync(marg, 0, (size_t)B * (n + 1) * (n + 1) * sizeof(M), s)) != cudaSuccess)
     return SDB_ERR_CUDA;
-  eisner_gen_kernel<<<(unsigned)B, kT, 0, s>>>(adj, n, single, (double*)ws, logz, marg, status);
+  eisner_gen_kernel<TP, M><<<(unsigned)B, kT, 0, s>>>(adj, n, single, (double*)ws, logz, marg, status);
   SDB_CHECK_LAUNCH();
   if (sdb_note(cudaFreeAsync(ws, s)) != cudaSuccess) return SDB_ERR_CUDA;
   return SDB_OK;
+}
+
+int eisner_gen_launch(const float* adj, int64_t B, int n, int single, double* logz, float* marg, int32_t* status,
+                      cudaStream_t s) {
+  return eisner_gen_launch_t<float, float>(adj, B, n, single, logz, marg, status, s);
+}
+
+// ---- exact mode (float64 adjacency and marginals)
+extern "C" int sdb_eisner_f64(const double* adjacency, int64_t B, int32_t n, int32_t single_root, double* logz,
+                              double* marg, int32_t* status, void* stream) {
+  if (B < 0 || n < 1 || !adjacency || !logz || !status) return SDB_ERR_ARG;
+  if (B == 0) return SDB_OK;
+  return eisner_gen_launch_t<double, double>(adjacency, B, n, single_root ? 1 : 0, logz, marg, status,
+                                             (cudaStream_t)stream);
 }

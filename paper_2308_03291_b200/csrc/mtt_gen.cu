@@ -18,7 +18,8 @@ constexpr int kGT = 1024;
 constexpr int kGW = kGT / 32;
 constexpr int kMaxGen = 2048;
 
-__device__ bool reach_all(const float* __restrict__ A, int n, int src, bool skip_root, uint8_t* seen, uint8_t* front,
+template <typename TP>
+__device__ bool reach_all(const TP* __restrict__ A, int n, int src, bool skip_root, uint8_t* seen, uint8_t* front,
                           int* flag) {
   const int N1 = n + 1;
   for (int v = threadIdx.x; v < N1; v += kGT) {
@@ -32,7 +33,7 @@ __device__ bool reach_all(const float* __restrict__ A, int n, int src, bool skip
     for (int d = threadIdx.x; d < N1; d += kGT) {
       if (seen[d] || d == 0) continue;
       for (int h = skip_root ? 1 : 0; h < N1; ++h) {
-        if (front[h] && h != d && !is_ninf(__ldg(A + (size_t)h * N1 + d))) {
+        if (front[h] && h != d && !((double)__ldg(A + (size_t)h * N1 + d) == ninfd())) {
           seen[d] = 2;  // reached this round
           *flag = 1;
           break;
@@ -53,16 +54,17 @@ __device__ bool reach_all(const float* __restrict__ A, int n, int src, bool skip
   return !__syncthreads_or(miss);
 }
 
-__global__ void __launch_bounds__(kGT) mtt_gen_kernel(const float* __restrict__ adj_all, int n, int single,
+template <typename TP, typename M>  // adjacency / marginal types (float64 = exact mode)
+__global__ void __launch_bounds__(kGT) mtt_gen_kernel(const TP* __restrict__ adj_all, int n, int single,
                                                       double* __restrict__ wsL, double* __restrict__ wsI,
-                                                      double* __restrict__ logz, float* __restrict__ marg_all,
+                                                      double* __restrict__ logz, M* __restrict__ marg_all,
                                                       int32_t* __restrict__ status) {
   extern __shared__ __align__(16) double smd[];
   double* f = smd;               // [n] multipliers
   double* prow = f + n;          // [n] pivot row
   double* piv = prow + n;        // [n] pivots
   double* rowmag = piv + n;      // [n]
-  float* shift = (float*)(rowmag + n);    // [n]
+  double* shift = rowmag + n;             // [n] (column max, exact in either precision)
   int* perm = (int*)(shift + n);          // [n]
   int* qinv = perm + n;                   // [n]
   uint8_t* used = (uint8_t*)(qinv + n);   // [n]
@@ -73,20 +75,20 @@ __global__ void __launch_bounds__(kGT) mtt_gen_kernel(const float* __restrict__ 
   __shared__ int flag, bad_s, vac_s, pk_s;
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int N1 = n + 1;
-  const float* A = adj_all + (size_t)b * N1 * N1;
+  const TP* A = adj_all + (size_t)b * N1 * N1;
   double* L = wsL + (size_t)b * n * n;
   double* I = wsI + (size_t)b * n * n;
   if (tid == 0) { bad_s = 0; vac_s = 0; }
   __syncthreads();
   for (int e = tid; e < N1 * N1; e += kGT)
-    if (bad_input(__ldg(A + e))) bad_s = 1;
+    if (bad_value(__ldg(A + e))) bad_s = 1;
   // column shifts (spanning.py:90-103)
   for (int d = tid; d < n; d += kGT) {
-    float mx = ninf();
+    double mx = ninfd();
     for (int h = 0; h <= n; ++h)
-      if (h != d + 1) mx = fmaxf(mx, __ldg(A + (size_t)h * N1 + d + 1));
+      if (h != d + 1) mx = fmax(mx, (double)__ldg(A + (size_t)h * N1 + d + 1));
     shift[d] = mx;
-    if (mx == ninf()) vac_s = 1;
+    if (mx == ninfd()) vac_s = 1;
   }
   __syncthreads();
   bool feasible = !bad_s && !vac_s;
@@ -96,7 +98,7 @@ __global__ void __launch_bounds__(kGT) mtt_gen_kernel(const float* __restrict__ 
     } else {
       feasible = false;
       for (int c = 1; c <= n && !feasible; ++c) {
-        if (is_ninf(__ldg(A + c))) continue;
+        if ((double)__ldg(A + c) == ninfd()) continue;
         feasible = reach_all(A, n, c, true, seen, front, &flag);
       }
     }
@@ -107,7 +109,7 @@ __global__ void __launch_bounds__(kGT) mtt_gen_kernel(const float* __restrict__ 
       logz[b] = ninfd();
     }
     if (marg_all)
-      for (int e = tid; e < N1 * N1; e += kGT) marg_all[(size_t)b * N1 * N1 + e] = 0.f;
+      for (int e = tid; e < N1 * N1; e += kGT) marg_all[(size_t)b * N1 * N1 + e] = (M)0;
     return;
   }
   // Laplacian (spanning.py:106-120): column c = dependent c+1, row r = head r+1
@@ -210,7 +212,7 @@ __global__ void __launch_bounds__(kGT) mtt_gen_kernel(const float* __restrict__ 
     I[(size_t)perm[j] * n + qi] = L[e] / piv[qi];
   }
   __syncthreads();
-  float* mg = marg_all + (size_t)b * N1 * N1;
+  M* mg = marg_all + (size_t)b * N1 * N1;
   for (int e = tid; e < N1 * N1; e += kGT) {
     const int h = e / N1, dep = e - h * N1;
     double v = 0.0;
@@ -226,7 +228,7 @@ __global__ void __launch_bounds__(kGT) mtt_gen_kernel(const float* __restrict__ 
       }
       v = fmin(fmax(v, 0.0), 1.0);  // spanning.py:175
     }
-    mg[e] = (float)v;
+    mg[e] = (M)v;
   }
 }
 
@@ -234,15 +236,31 @@ __global__ void __launch_bounds__(kGT) mtt_gen_kernel(const float* __restrict__ 
 
 size_t mtt_gen_workspace(int64_t B, int n) { return (size_t)B * n * n * 8 * 2 + 256; }
 
-int mtt_gen_launch(const float* adjacency, int64_t B, int n, int single, double* logz, float* marg, int32_t* status,
-                   void* workspace, size_t ws_bytes, cudaStream_t s) {
+template <typename TP, typename M>
+int mtt_gen_launch_t(const TP* adjacency, int64_t B, int n, int single, double* logz, M* marg, int32_t* status,
+                     void* workspace, size_t ws_bytes, cudaStream_t s) {
   if (n > kMaxGen) return SDB_ERR_UNSUPPORTED;
   if (!workspace || ws_bytes < mtt_gen_workspace(B, n)) return SDB_ERR_WORKSPACE;
-  const size_t smem = (size_t)n * (4 * 8 + 4 + 4 + 4 + 1) + 2 * (size_t)(n + 1) + 64;
-  if (sdb_set_smem((const void*)mtt_gen_kernel, smem) != cudaSuccess) return SDB_ERR_CUDA;
+  const size_t smem = (size_t)n * (5 * 8 + 4 + 4 + 1) + 2 * (size_t)(n + 1) + 64;
+  if (sdb_set_smem((const void*)mtt_gen_kernel<TP, M>, smem) != cudaSuccess) return SDB_ERR_CUDA;
   double* L = (double*)workspace;
   double* I = L + (size_t)B * n * n;
-  mtt_gen_kernel<<<(unsigned)B, kGT, smem, s>>>(adjacency, n, single, L, I, logz, marg, status);
+  mtt_gen_kernel<TP, M><<<(unsigned)B, kGT, smem, s>>>(adjacency, n, single, L, I, logz, marg, status);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
+}
+
+int mtt_gen_launch(const float* adjacency, int64_t B, int n, int single, double* logz, float* marg, int32_t* status,
+                   void* workspace, size_t ws_bytes, cudaStream_t s) {
+  return mtt_gen_launch_t<float, float>(adjacency, B, n, single, logz, marg, status, workspace, ws_bytes, s);
+}
+
+// ---- exact mode (float64 adjacency and marginals, any n)
+extern "C" size_t sdb_mtt_f64_workspace(int64_t B, int32_t n) { return (B < 0 || n < 1) ? 0 : mtt_gen_workspace(B, n); }
+extern "C" int sdb_mtt_f64(const double* adjacency, int64_t B, int32_t n, int32_t single_root, double* logz,
+                           double* marg, int32_t* status, void* workspace, size_t ws_bytes, void* stream) {
+  if (B < 0 || n < 1 || !adjacency || !logz || !status) return SDB_ERR_ARG;
+  if (B == 0) return SDB_OK;
+  return mtt_gen_launch_t<double, double>(adjacency, B, n, single_root ? 1 : 0, logz, marg, status, workspace,
+                                          ws_bytes, (cudaStream_t)stream);
 }

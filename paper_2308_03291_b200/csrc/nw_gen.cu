@@ -27,27 +27,29 @@ struct Diag {
   __device__ int hi(int d) const { return d < n ? d : n; }
 };
 
-// kMode 0: log Z; 1: log Z + marginals; 2: max-plus score + argmax path
-template <int kMode>
-__global__ void __launch_bounds__(kT) nw_gen_kernel(const float* __restrict__ theta, int n, int m,
+// kMode 0: log Z; 1: log Z + marginals; 2: max-plus score + argmax path.
+// T / M: potential and marginal types (float: the batched fp32 contract;
+// double: the exact mode, float64 in and out like the reference)
+template <int kMode, typename T, typename M>
+__global__ void __launch_bounds__(kT) nw_gen_kernel(const T* __restrict__ theta, int n, int m,
                                                     double* __restrict__ ws_all, double* __restrict__ out,
-                                                    float* __restrict__ marg_all, int8_t* __restrict__ path_all,
+                                                    M* __restrict__ marg_all, int8_t* __restrict__ path_all,
                                                     int32_t* __restrict__ status) {
   extern __shared__ __align__(16) double dbuf[];
   __shared__ int bad_s;
   __shared__ double z_s;
   const int b = blockIdx.x, tid = threadIdx.x;
   const int n1 = n + 1, m1 = m + 1, L = min(n, m) + 1;
-  const float* th = theta + (size_t)b * n1 * m1 * 3;
+  const T* th = theta + (size_t)b * n1 * m1 * 3;
   double* A = kMode ? ws_all + (size_t)b * n1 * m1 : nullptr;
   double* dv[3] = {dbuf, dbuf + L, dbuf + 2 * L};
   const Diag D{n, m};
-  auto T = [&](int i, int j, int k) { return (double)__ldg(th + ((size_t)i * m1 + j) * 3 + k); };
+  auto Th = [&](int i, int j, int k) { return (double)__ldg(th + ((size_t)i * m1 + j) * 3 + k); };
   if (tid == 0) bad_s = 0;
   __syncthreads();
   {
     int bad = 0;
-    for (size_t e = tid; e < (size_t)n1 * m1 * 3; e += kT) bad |= bad_input(__ldg(th + e));
+    for (size_t e = tid; e < (size_t)n1 * m1 * 3; e += kT) bad |= bad_value(__ldg(th + e));
     if (bad) bad_s = 1;
   }
   // forward (alignment.py:62-76; max-plus for the argmax, alignment.py:155-167)
@@ -62,9 +64,9 @@ __global__ void __launch_bounds__(kT) nw_gen_kernel(const float* __restrict__ th
       if (d == 0) {
         a = 0.0;
       } else {
-        const double c0 = (i > 0 && j > 0) ? p2[i - 1 - lo2] + T(i, j, 0) : ninfd();
-        const double c1 = (i > 0) ? p1[i - 1 - lo1] + T(i, j, 1) : ninfd();
-        const double c2 = (j > 0) ? p1[i - lo1] + T(i, j, 2) : ninfd();
+        const double c0 = (i > 0 && j > 0) ? p2[i - 1 - lo2] + Th(i, j, 0) : ninfd();
+        const double c1 = (i > 0) ? p1[i - 1 - lo1] + Th(i, j, 1) : ninfd();
+        const double c2 = (j > 0) ? p1[i - lo1] + Th(i, j, 2) : ninfd();
         a = kMode == 2 ? fmax(c0, fmax(c1, c2)) : lse3d(c0, c1, c2);
       }
       cur[i - lo] = a;
@@ -81,7 +83,7 @@ __global__ void __launch_bounds__(kT) nw_gen_kernel(const float* __restrict__ th
     status[b] = bad ? SDB_ST_INVALID : (z == ninfd() ? SDB_ST_VACUOUS : SDB_ST_OK);
   }
   if (kMode == 1) {
-    float* mg = marg_all + (size_t)b * n1 * m1 * 3;
+    M* mg = marg_all + (size_t)b * n1 * m1 * 3;
     const bool zok = !bad && z != ninfd();
     // backward (alignment.py:79-99) with the marginals of each finished cell
     for (int d = n + m; d >= 0; --d) {
@@ -95,17 +97,17 @@ __global__ void __launch_bounds__(kT) nw_gen_kernel(const float* __restrict__ th
         if (d == n + m) {
           bt = 0.0;
         } else {
-          const double c0 = (i < n && j < m) ? T(i + 1, j + 1, 0) + q2[i + 1 - lq2] : ninfd();
-          const double c1 = (i < n) ? T(i + 1, j, 1) + q1[i + 1 - lq1] : ninfd();
-          const double c2 = (j < m) ? T(i, j + 1, 2) + q1[i - lq1] : ninfd();
+          const double c0 = (i < n && j < m) ? Th(i + 1, j + 1, 0) + q2[i + 1 - lq2] : ninfd();
+          const double c1 = (i < n) ? Th(i + 1, j, 1) + q1[i + 1 - lq1] : ninfd();
+          const double c2 = (j < m) ? Th(i, j + 1, 2) + q1[i - lq1] : ninfd();
           bt = lse3d(c0, c1, c2);
         }
         cur[i - lo] = bt;
-        float* o = mg + ((size_t)i * m1 + j) * 3;
+        M* o = mg + ((size_t)i * m1 + j) * 3;
         const double base = bt - z;
-        o[0] = (zok && i > 0 && j > 0) ? (float)exp(A[(size_t)(i - 1) * m1 + j - 1] + T(i, j, 0) + base) : 0.f;
-        o[1] = (zok && i > 0) ? (float)exp(A[(size_t)(i - 1) * m1 + j] + T(i, j, 1) + base) : 0.f;
-        o[2] = (zok && j > 0) ? (float)exp(A[(size_t)i * m1 + j - 1] + T(i, j, 2) + base) : 0.f;
+        o[0] = (M)((zok && i > 0 && j > 0) ? exp(A[(size_t)(i - 1) * m1 + j - 1] + Th(i, j, 0) + base) : 0.0);
+        o[1] = (M)((zok && i > 0) ? exp(A[(size_t)(i - 1) * m1 + j] + Th(i, j, 1) + base) : 0.0);
+        o[2] = (M)((zok && j > 0) ? exp(A[(size_t)i * m1 + j - 1] + Th(i, j, 2) + base) : 0.0);
       }
       __syncthreads();
     }
@@ -117,13 +119,13 @@ __global__ void __launch_bounds__(kT) nw_gen_kernel(const float* __restrict__ th
     while (i != 0 || j != 0) {
       int k = -1;
       double best = 0.0;
-      if (i > 0 && j > 0) { best = A[(size_t)(i - 1) * m1 + j - 1] + T(i, j, 0); k = 0; }
+      if (i > 0 && j > 0) { best = A[(size_t)(i - 1) * m1 + j - 1] + Th(i, j, 0); k = 0; }
       if (i > 0) {
-        const double c = A[(size_t)(i - 1) * m1 + j] + T(i, j, 1);
+        const double c = A[(size_t)(i - 1) * m1 + j] + Th(i, j, 1);
         if (k < 0 || c > best) { best = c; k = 1; }
       }
       if (j > 0) {
-        const double c = A[(size_t)i * m1 + j - 1] + T(i, j, 2);
+        const double c = A[(size_t)i * m1 + j - 1] + Th(i, j, 2);
         if (k < 0 || c > best) { best = c; k = 2; }
       }
       pb[(size_t)i * m1 + j] = (int8_t)k;
@@ -142,18 +144,36 @@ size_t nw_gen_workspace(int64_t B, int n, int m, int mode) {
   return mode ? (size_t)B * (n + 1) * (m + 1) * sizeof(double) + 256 : 0;
 }
 
-int nw_gen_launch(int mode, const float* theta, int64_t B, int n, int m, void* ws, size_t ws_bytes, double* out,
-                  float* marg, int8_t* path, int32_t* status, cudaStream_t s) {
+template <typename T, typename M>
+int nw_gen_launch_t(int mode, const T* theta, int64_t B, int n, int m, void* ws, size_t ws_bytes, double* out, M* marg,
+                    int8_t* path, int32_t* status, cudaStream_t s) {
   if (!nw_gen_ok(n, m)) return SDB_ERR_UNSUPPORTED;
   if (ws_bytes < nw_gen_workspace(B, n, m, mode) || (mode && !ws)) return SDB_ERR_WORKSPACE;
   const size_t smem = (size_t)3 * (min(n, m) + 1) * sizeof(double);
-  const void* k = mode == 0 ? (const void*)nw_gen_kernel<0> : mode == 1 ? (const void*)nw_gen_kernel<1>
-                                                                         : (const void*)nw_gen_kernel<2>;
+  const void* k = mode == 0 ? (const void*)nw_gen_kernel<0, T, M> : mode == 1 ? (const void*)nw_gen_kernel<1, T, M>
+                                                                               : (const void*)nw_gen_kernel<2, T, M>;
   if (sdb_set_smem(k, smem) != cudaSuccess) return SDB_ERR_CUDA;
   double* w = (double*)ws;
-  if (mode == 0) nw_gen_kernel<0><<<(unsigned)B, kT, smem, s>>>(theta, n, m, w, out, marg, path, status);
-  if (mode == 1) nw_gen_kernel<1><<<(unsigned)B, kT, smem, s>>>(theta, n, m, w, out, marg, path, status);
-  if (mode == 2) nw_gen_kernel<2><<<(unsigned)B, kT, smem, s>>>(theta, n, m, w, out, marg, path, status);
+  if (mode == 0) nw_gen_kernel<0, T, M><<<(unsigned)B, kT, smem, s>>>(theta, n, m, w, out, marg, path, status);
+  if (mode == 1) nw_gen_kernel<1, T, M><<<(unsigned)B, kT, smem, s>>>(theta, n, m, w, out, marg, path, status);
+  if (mode == 2) nw_gen_kernel<2, T, M><<<(unsigned)B, kT, smem, s>>>(theta, n, m, w, out, marg, path, status);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
+}
+
+int nw_gen_launch(int mode, const float* theta, int64_t B, int n, int m, void* ws, size_t ws_bytes, double* out,
+                  float* marg, int8_t* path, int32_t* status, cudaStream_t s) {
+  return nw_gen_launch_t<float, float>(mode, theta, B, n, m, ws, ws_bytes, out, marg, path, status, s);
+}
+
+// ---- exact mode (float64 potentials and marginals, any shape)
+extern "C" size_t sdb_nw_fb_f64_workspace(int64_t B, int32_t n, int32_t m) {
+  return (B < 0 || n < 1 || m < 1) ? 0 : nw_gen_workspace(B, n, m, 1);
+}
+extern "C" int sdb_nw_fb_f64(const double* theta, int64_t B, int32_t n, int32_t m, double* logz, double* marg,
+                             int32_t* status, void* workspace, size_t ws_bytes, void* stream) {
+  if (B < 0 || n < 1 || m < 1 || !theta || !logz || !status) return SDB_ERR_ARG;
+  if (B == 0) return SDB_OK;
+  return nw_gen_launch_t<double, double>(marg ? 1 : 0, theta, B, n, m, workspace, ws_bytes, logz, marg, nullptr,
+                                         status, (cudaStream_t)stream);
 }

@@ -94,20 +94,20 @@ __device__ double build_pairs(const double* iu, const double* is, int n, int S, 
 }
 
 // kMode: 0 log Z, 1 + span marginals, 2 + root / rule / emission gradients
-template <int kMode>
+template <int kMode, typename TP, typename M>  // TP / M: input / output types (float64 = exact mode)
 __global__ void __launch_bounds__(kGT) pcfg_gen_kernel(
-    const float* __restrict__ root_all, const float* __restrict__ rules_all, const float* __restrict__ emis_all,
-    const float* __restrict__ sticky_all, int n, int NT, int PT, GenWs ws, double* __restrict__ logz,
-    float* __restrict__ marg_all, float* __restrict__ groot_all, float* __restrict__ grules_all,
-    float* __restrict__ gemis_all, int32_t* __restrict__ status) {
+    const TP* __restrict__ root_all, const TP* __restrict__ rules_all, const TP* __restrict__ emis_all,
+    const TP* __restrict__ sticky_all, int n, int NT, int PT, GenWs ws, double* __restrict__ logz,
+    M* __restrict__ marg_all, M* __restrict__ groot_all, M* __restrict__ grules_all,
+    M* __restrict__ gemis_all, int32_t* __restrict__ status) {
   __shared__ double red[kGW];
   __shared__ int badsh;
   const int S = NT + PT, S2 = S * S;
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const float* root = root_all + (size_t)b * NT;
-  const float* rules = rules_all + (size_t)b * NT * S2;
-  const float* emis = emis_all + (size_t)b * n * PT;
-  const float* sticky = sticky_all ? sticky_all + (size_t)b * n * n : nullptr;
+  const TP* root = root_all + (size_t)b * NT;
+  const TP* rules = rules_all + (size_t)b * NT * S2;
+  const TP* emis = emis_all + (size_t)b * n * PT;
+  const TP* sticky = sticky_all ? sticky_all + (size_t)b * n * n : nullptr;
   double* Rl = ws.Rl + (size_t)b * NT * S2;
   double* iu = ws.iu + (size_t)b * n * n * S;
   double* is = ws.is + (size_t)b * n * n;
@@ -122,15 +122,15 @@ __global__ void __launch_bounds__(kGT) pcfg_gen_kernel(
   {
     int bad = 0;
     for (int e = tid; e < NT * S2; e += kGT) {
-      const float r = rules[e];
-      bad |= bad_input(r);
+      const TP r = rules[e];
+      bad |= bad_value(r);
       Rl[e] = exp((double)r);
       if (kMode == 2) G[e] = 0.0;
     }
-    for (int e = tid; e < NT; e += kGT) bad |= bad_input(root[e]);
-    for (int e = tid; e < n * PT; e += kGT) bad |= bad_input(emis[e]);
+    for (int e = tid; e < NT; e += kGT) bad |= bad_value(root[e]);
+    for (int e = tid; e < n * PT; e += kGT) bad |= bad_value(emis[e]);
     if (sticky)
-      for (int e = tid; e < n * n; e += kGT) bad |= !(sticky[e] == 0.f || sticky[e] == ninf());
+      for (int e = tid; e < n * n; e += kGT) bad |= !((double)sticky[e] == 0.0 || (double)sticky[e] == ninfd());
     if (bad) atomicOr(&badsh, 1);
   }
   // ---- inside, width 1: preterminal slots = emissions + sticky (constituency.py:255-256)
@@ -165,10 +165,10 @@ __global__ void __launch_bounds__(kGT) pcfg_gen_kernel(
         }
       }
       for (int X = NT + tid; X < S; X += kGT) u[X] = 0.0;
-      const double M = block_max_d(lane == 0 ? lmax : ninfd(), red);  // (includes the barrier)
-      const bool live = M > 0.0 && M != ninfd();
-      for (int A = tid; A < NT; A += kGT) u[A] = live ? u[A] / M : 0.0;
-      if (tid == 0) is[i * n + j] = live ? m + log(M) + STK(i, j) : ninfd();
+      const double Mx = block_max_d(lane == 0 ? lmax : ninfd(), red);  // (includes the barrier)
+      const bool live = Mx > 0.0 && Mx != ninfd();
+      for (int A = tid; A < NT; A += kGT) u[A] = live ? u[A] / Mx : 0.0;
+      if (tid == 0) is[i * n + j] = live ? m + log(Mx) + STK(i, j) : ninfd();
       __syncthreads();
     }
   }
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(kGT) pcfg_gen_kernel(
   }
   if (kMode == 0) return;
   const bool ok = !badsh && z != ninfd();
-  float* marg = marg_all + (size_t)b * n * n;
+  M* marg = marg_all + (size_t)b * n * n;
   if (!ok) {
     for (int e = tid; e < n * n; e += kGT) marg[e] = 0.f;
     if (kMode == 2) {
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(kGT) pcfg_gen_kernel(
   // ---- span marginals: exp(lse(outside + chart) - Z) (constituency.py:330-334)
   for (int c = warp; c < n * n; c += kGW) {
     const int i = c / n, j = c - i * n;
-    float val = 0.f;
+    double val = 0.0;
     if (j >= i) {
       const double t = os[c], s = is[c];
       double acc = 0.0;
@@ -287,9 +287,9 @@ __global__ void __launch_bounds__(kGT) pcfg_gen_kernel(
         for (int X = lane; X < S; X += 32) acc = fma(ou[(size_t)c * S + X], iu[(size_t)c * S + X], acc);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (acc > 0.0) val = (float)exp(log(acc) + t + s - z);
+      if (acc > 0.0) val = exp(log(acc) + t + s - z);
     }
-    if (lane == 0) marg[c] = val;
+    if (lane == 0) marg[c] = (M)val;
   }
   if (kMode != 2) return;
   // ---- gradients (constituency.py:326-329)
@@ -298,14 +298,14 @@ __global__ void __launch_bounds__(kGT) pcfg_gen_kernel(
     const double s0 = is[n - 1];
     for (int A = tid; A < NT; A += kGT)
       groot_all[(size_t)b * NT + A] =
-          (s0 == ninfd() || u[A] == 0.0) ? 0.f : (float)exp((double)root[A] + s0 + log(u[A]) - z);
-    for (int e = tid; e < NT * S2; e += kGT) grules_all[(size_t)b * NT * S2 + e] = (float)(G[e] * Rl[e]);
+          (M)((s0 == ninfd() || u[A] == 0.0) ? 0.0 : exp((double)root[A] + s0 + log(u[A]) - z));
+    for (int e = tid; e < NT * S2; e += kGT) grules_all[(size_t)b * NT * S2 + e] = (M)(G[e] * Rl[e]);
     for (int e = tid; e < n * PT; e += kGT) {
       const int i = e / PT, X = e - i * PT;
       const double t = os[i * n + i];
       const double o = ou[((size_t)i * n + i) * S + NT + X];
       const double v = (t == ninfd() || o == 0.0) ? ninfd() : log(o) + t + STK(i, i) + (double)emis[e] - z;
-      gemis_all[(size_t)b * n * PT + e] = v == ninfd() ? 0.f : (float)exp(v);
+      gemis_all[(size_t)b * n * PT + e] = (M)(v == ninfd() ? 0.0 : exp(v));
     }
   }
 }
@@ -318,21 +318,45 @@ size_t pcfg_gen_workspace(int64_t B, int n, int NT, int PT, bool grad) {
   return bytes;
 }
 
-int pcfg_gen_launch(int mode, const float* root, const float* rules, const float* emissions, const float* sticky,
-                    int64_t B, int n, int NT, int PT, double* logz, float* span_marg, float* groot, float* grules,
-                    float* gemis, int32_t* status, void* workspace, size_t ws_bytes, cudaStream_t s) {
+template <typename TP, typename M>
+int pcfg_gen_launch_t(int mode, const TP* root, const TP* rules, const TP* emissions, const TP* sticky, int64_t B,
+                      int n, int NT, int PT, double* logz, M* span_marg, M* groot, M* grules, M* gemis,
+                      int32_t* status, void* workspace, size_t ws_bytes, cudaStream_t s) {
   size_t need = 0;
   GenWs ws = gen_carve(workspace, B, n, NT, PT, mode == 2, &need);
   if (!workspace || ws_bytes < need) return SDB_ERR_WORKSPACE;
   if (mode == 0)
-    pcfg_gen_kernel<0><<<(unsigned)B, kGT, 0, s>>>(root, rules, emissions, sticky, n, NT, PT, ws, logz, nullptr,
-                                                    nullptr, nullptr, nullptr, status);
+    pcfg_gen_kernel<0, TP, M><<<(unsigned)B, kGT, 0, s>>>(root, rules, emissions, sticky, n, NT, PT, ws, logz,
+                                                           nullptr, nullptr, nullptr, nullptr, status);
   else if (mode == 1)
-    pcfg_gen_kernel<1><<<(unsigned)B, kGT, 0, s>>>(root, rules, emissions, sticky, n, NT, PT, ws, logz, span_marg,
-                                                    nullptr, nullptr, nullptr, status);
+    pcfg_gen_kernel<1, TP, M><<<(unsigned)B, kGT, 0, s>>>(root, rules, emissions, sticky, n, NT, PT, ws, logz,
+                                                           span_marg, nullptr, nullptr, nullptr, status);
   else
-    pcfg_gen_kernel<2><<<(unsigned)B, kGT, 0, s>>>(root, rules, emissions, sticky, n, NT, PT, ws, logz, span_marg,
-                                                    groot, grules, gemis, status);
+    pcfg_gen_kernel<2, TP, M><<<(unsigned)B, kGT, 0, s>>>(root, rules, emissions, sticky, n, NT, PT, ws, logz,
+                                                           span_marg, groot, grules, gemis, status);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
+}
+
+int pcfg_gen_launch(int mode, const float* root, const float* rules, const float* emissions, const float* sticky,
+                    int64_t B, int n, int NT, int PT, double* logz, float* span_marg, float* groot, float* grules,
+                    float* gemis, int32_t* status, void* workspace, size_t ws_bytes, cudaStream_t s) {
+  return pcfg_gen_launch_t<float, float>(mode, root, rules, emissions, sticky, B, n, NT, PT, logz, span_marg, groot,
+                                         grules, gemis, status, workspace, ws_bytes, s);
+}
+
+// ---- exact mode (float64 grammar / emissions / sticky in, float64 span marginals and gradients out)
+extern "C" size_t sdb_pcfg_f64_workspace(int64_t B, int32_t n, int32_t NT, int32_t PT, int32_t grad) {
+  return (B < 0 || n < 1 || NT < 1 || PT < 1) ? 0 : pcfg_gen_workspace(B, n, NT, PT, grad != 0);
+}
+// span_marg == NULL: log Z only; groot/grules/gemis non-NULL (with span_marg): the gradients too
+extern "C" int sdb_pcfg_f64(const double* root, const double* rules, const double* emissions, const double* sticky,
+                            int64_t B, int32_t n, int32_t NT, int32_t PT, double* logz, double* span_marg,
+                            double* groot, double* grules, double* gemis, int32_t* status, void* workspace,
+                            size_t ws_bytes, void* stream) {
+  if (B < 0 || n < 1 || NT < 1 || PT < 1 || !root || !rules || !emissions || !logz || !status) return SDB_ERR_ARG;
+  if (B == 0) return SDB_OK;
+  const int mode = !span_marg ? 0 : (groot && grules && gemis) ? 2 : 1;
+  return pcfg_gen_launch_t<double, double>(mode, root, rules, emissions, sticky, B, n, NT, PT, logz, span_marg, groot,
+                                           grules, gemis, status, workspace, ws_bytes, (cudaStream_t)stream);
 }

@@ -11,19 +11,20 @@ namespace {
 
 constexpr int kRT = 256;
 
-__global__ void __launch_bounds__(kRT) masked_dot_kernel(const float* __restrict__ marg,
-                                                         const float* __restrict__ theta, int64_t len,
-                                                         double* __restrict__ out, int32_t* __restrict__ neginf) {
+template <typename T>  // float: the batched path; double: the exact mode
+__global__ void __launch_bounds__(kRT) masked_dot_kernel(const T* __restrict__ marg, const T* __restrict__ theta,
+                                                         int64_t len, double* __restrict__ out,
+                                                         int32_t* __restrict__ neginf) {
   const int b = blockIdx.y;
-  const float* p = marg + (size_t)b * len;
-  const float* t = theta + (size_t)b * len;
+  const T* p = marg + (size_t)b * len;
+  const T* t = theta + (size_t)b * len;
   double acc = 0.0;
   int ninf_hit = 0;
   for (int64_t e = (int64_t)blockIdx.x * kRT + threadIdx.x; e < len; e += (int64_t)gridDim.x * kRT) {
-    const float pe = __ldg(p + e);
-    if (pe > 0.f) {
-      const float te = __ldg(t + e);
-      if (te == ninf()) ninf_hit = 1;
+    const T pe = __ldg(p + e);
+    if (pe > (T)0) {
+      const T te = __ldg(t + e);
+      if ((double)te == ninfd()) ninf_hit = 1;
       else acc = fma((double)pe, (double)te, acc);
     }
   }
@@ -60,7 +61,19 @@ extern "C" int sdb_masked_dot(const float* marg, const float* theta, int64_t B, 
   if (B == 0 || len == 0) return SDB_OK;
   const int64_t per = (len + kRT - 1) / kRT;
   const unsigned gx = (unsigned)(per < 64 ? per : 64);
-  masked_dot_kernel<<<dim3(gx, (unsigned)B), kRT, 0, (cudaStream_t)stream>>>(marg, theta, len, out, neginf);
+  masked_dot_kernel<float><<<dim3(gx, (unsigned)B), kRT, 0, (cudaStream_t)stream>>>(marg, theta, len, out, neginf);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
+// exact mode: float64 marginals and potentials
+extern "C" int sdb_masked_dot_f64(const double* marg, const double* theta, int64_t B, int64_t len, double* out,
+                                  int32_t* neginf, void* stream) {
+  if (B < 0 || len < 0 || (B > 0 && len > 0 && (!marg || !theta || !out || !neginf))) return SDB_ERR_ARG;
+  if (B == 0 || len == 0) return SDB_OK;
+  const int64_t per = (len + kRT - 1) / kRT;
+  const unsigned gx = (unsigned)(per < 64 ? per : 64);
+  masked_dot_kernel<double><<<dim3(gx, (unsigned)B), kRT, 0, (cudaStream_t)stream>>>(marg, theta, len, out, neginf);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
 }

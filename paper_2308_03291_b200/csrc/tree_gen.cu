@@ -28,16 +28,16 @@ struct WLse {  // per-lane online log-sum-exp (or max), then a warp reduction
 };
 
 // kMode 0: log Z; 1: log Z + marginals; 2: max-plus score + best tree labels
-template <int kMode>
-__global__ void __launch_bounds__(kT) tree_gen_kernel(const float* __restrict__ sp_all, int n, int m,
+template <int kMode, typename TP, typename M>  // TP / M: potential / marginal types (float64 = exact mode)
+__global__ void __launch_bounds__(kT) tree_gen_kernel(const TP* __restrict__ sp_all, int n, int m,
                                                       double* __restrict__ ws_all, double* __restrict__ out,
-                                                      float* __restrict__ marg_all, int32_t* __restrict__ lab_all,
+                                                      M* __restrict__ marg_all, int32_t* __restrict__ lab_all,
                                                       int32_t* __restrict__ status) {
   __shared__ int bad_s;
   constexpr bool kMax = kMode == 2;
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const size_t nn = (size_t)n * n;
-  const float* sp = sp_all + (size_t)b * nn * m;
+  const TP* sp = sp_all + (size_t)b * nn * m;
   double* S = ws_all + (size_t)b * 3 * nn;  // label fold
   double* I = S + nn;                       // inside
   double* O = I + nn;                       // outside (marginals) / walk stack (argmax)
@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(kT) tree_gen_kernel(const float* __restrict__ 
   __syncthreads();
   {
     int bad = 0;
-    for (size_t e = tid; e < nn * m; e += kT) bad |= bad_input(__ldg(sp + e));
+    for (size_t e = tid; e < nn * m; e += kT) bad |= bad_value(__ldg(sp + e));
     if (bad) bad_s = 1;
   }
   // label fold (constituency.py:55), one warp per span
@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(kT) tree_gen_kernel(const float* __restrict__ 
     status[b] = bad ? SDB_ST_INVALID : (z == ninfd() ? SDB_ST_VACUOUS : SDB_ST_OK);
   }
   if (kMode == 1) {
-    float* mg = marg_all + (size_t)b * nn * m;
+    M* mg = marg_all + (size_t)b * nn * m;
     const bool zok = !bad && z != ninfd();
     for (size_t e = tid; e < nn; e += kT) O[e] = ninfd();
     __syncthreads();
@@ -103,10 +103,10 @@ __global__ void __launch_bounds__(kT) tree_gen_kernel(const float* __restrict__ 
     for (size_t e = tid; e < nn * m; e += kT) {
       const size_t c = e / m;
       const int i = (int)(c / n), j = (int)(c % n);
-      float v = 0.f;
+      double v = 0.0;
       if (zok && i <= j && I[c] != ninfd() && O[c] != ninfd())
-        v = (float)exp(O[c] + (I[c] - S[c]) + (double)__ldg(sp + e) - z);
-      mg[e] = v;
+        v = exp(O[c] + (I[c] - S[c]) + (double)__ldg(sp + e) - z);
+      mg[e] = (M)v;
     }
   }
   if (kMode == 2 && tid == 0 && !bad && z != ninfd()) {
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(kT) tree_gen_kernel(const float* __restrict__ 
     stack[top++] = n - 1;  // (0, n-1) encoded as i * n + j
     while (top > 0) {
       const int c = stack[--top], i = c / n, j = c % n;
-      const float* th = sp + (size_t)c * m;
+      const TP* th = sp + (size_t)c * m;
       int bl = 0;
       for (int l = 1; l < m; ++l)
         if (th[l] > th[bl]) bl = l;
@@ -141,8 +141,9 @@ bool tree_gen_ok(int n) { return n <= 8192; }
 
 size_t tree_gen_workspace(int64_t B, int n) { return (size_t)B * 3 * n * n * sizeof(double) + 256; }
 
-int tree_gen_launch(int mode, const float* sp, int64_t B, int n, int m, void* ws, size_t ws_bytes, double* out,
-                    float* marg, int32_t* labels, int32_t* status, cudaStream_t s) {
+template <typename TP, typename M>
+int tree_gen_launch_t(int mode, const TP* sp, int64_t B, int n, int m, void* ws, size_t ws_bytes, double* out,
+                      M* marg, int32_t* labels, int32_t* status, cudaStream_t s) {
   if (!tree_gen_ok(n)) return SDB_ERR_UNSUPPORTED;
   const size_t need = tree_gen_workspace(B, n);
   bool own = false;
@@ -155,10 +156,29 @@ int tree_gen_launch(int mode, const float* sp, int64_t B, int n, int m, void* ws
   double* w = (double*)ws;
   if (mode == 2 && sdb_note(cudaMemsetAsync(labels, 0xff, (size_t)B * n * n * sizeof(int32_t), s)) != cudaSuccess)
     return SDB_ERR_CUDA;
-  if (mode == 0) tree_gen_kernel<0><<<(unsigned)B, kT, 0, s>>>(sp, n, m, w, out, marg, labels, status);
-  if (mode == 1) tree_gen_kernel<1><<<(unsigned)B, kT, 0, s>>>(sp, n, m, w, out, marg, labels, status);
-  if (mode == 2) tree_gen_kernel<2><<<(unsigned)B, kT, 0, s>>>(sp, n, m, w, out, marg, labels, status);
+  if (mode == 0) tree_gen_kernel<0, TP, M><<<(unsigned)B, kT, 0, s>>>(sp, n, m, w, out, marg, labels, status);
+  if (mode == 1) tree_gen_kernel<1, TP, M><<<(unsigned)B, kT, 0, s>>>(sp, n, m, w, out, marg, labels, status);
+  if (mode == 2) tree_gen_kernel<2, TP, M><<<(unsigned)B, kT, 0, s>>>(sp, n, m, w, out, marg, labels, status);
   SDB_CHECK_LAUNCH();
   if (own && sdb_note(cudaFreeAsync(ws, s)) != cudaSuccess) return SDB_ERR_CUDA;
   return SDB_OK;
+}
+
+int tree_gen_launch(int mode, const float* sp, int64_t B, int n, int m, void* ws, size_t ws_bytes, double* out,
+                    float* marg, int32_t* labels, int32_t* status, cudaStream_t s) {
+  return tree_gen_launch_t<float, float>(mode, sp, B, n, m, ws, ws_bytes, out, marg, labels, status, s);
+}
+
+// ---- exact mode (float64 span potentials and marginals)
+extern "C" size_t sdb_tree_fb_f64_workspace(int64_t B, int32_t n, int32_t m) {
+  (void)m;
+  return (B < 0 || n < 1) ? 0 : tree_gen_workspace(B, n);
+}
+extern "C" int sdb_tree_fb_f64(const double* span_potentials, int64_t B, int32_t n, int32_t m, double* logz,
+                               double* marg, int32_t* status, void* workspace, size_t ws_bytes, void* stream) {
+  if (B < 0 || n < 1 || m < 1 || !span_potentials || !logz || !status) return SDB_ERR_ARG;
+  if (B == 0) return SDB_OK;
+  if (!workspace) return SDB_ERR_WORKSPACE;
+  return tree_gen_launch_t<double, double>(marg ? 1 : 0, span_potentials, B, n, m, workspace, ws_bytes, logz, marg,
+                                           nullptr, status, (cudaStream_t)stream);
 }

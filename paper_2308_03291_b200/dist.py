@@ -161,7 +161,7 @@ def _expected_scores_device(be, ps, qs):
     pairs = []
     for key, marg in res.dev.items():
         theta = torch.from_numpy(np.ascontiguousarray(np.stack([q.potentials()[key] for q in qs]))).to(
-            torch.float32).to(dev, non_blocking=True)
+            marg.dtype).to(dev, non_blocking=True)
         pairs.append((marg, theta))
     from . import kernels as K
 
@@ -382,6 +382,26 @@ _BATCHED.update({
     "argmax": _b_argmax, "argmax_info": _b_argmax_info,
     "entropy": _b_entropy, "entropy_info": _b_entropy_info,
 })
+
+
+def set_precision(mode: str):
+    """"fp32" (default): potentials go to the batched fp32 kernels, results
+    within the rtol 1e-4 contract.  "fp64": the exact mode -- log_partition,
+    marginals and the derived quantities take the float64 potentials as they
+    are (sdb_*_f64: fp64 in, fp64 out, the reference's recurrences on the GPU),
+    for callers that compare at the reference's own tolerances.  argmax and
+    sampling are unchanged (fp64 arithmetic on fp32-rounded potentials)."""
+    from . import backends
+
+    if mode not in ("fp32", "fp64"):
+        raise ValueError(f"precision must be 'fp32' or 'fp64', got {mode!r}")
+    backends.EXACT = mode == "fp64"
+
+
+def get_precision() -> str:
+    from . import backends
+
+    return "fp64" if backends.EXACT else "fp32"
 
 
 def device():

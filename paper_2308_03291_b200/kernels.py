@@ -28,6 +28,17 @@ def f32(t: torch.Tensor, name: str = "tensor") -> torch.Tensor:
     return t.to(torch.float32).contiguous()
 
 
+def f64(t: torch.Tensor, name: str = "tensor") -> torch.Tensor:
+    _require_cuda(t, name)
+    return t.to(torch.float64).contiguous()
+
+
+def exact(t) -> bool:
+    """float64 potentials select the exact-mode entry points (sdb_*_f64):
+    fp64 in, fp64 out, the reference's recurrences in fp64 on the GPU."""
+    return isinstance(t, torch.Tensor) and t.dtype == torch.float64
+
+
 def i32(t: torch.Tensor, name: str = "tensor") -> torch.Tensor:
     _require_cuda(t, name)
     return t.to(torch.int32).contiguous()
@@ -54,8 +65,11 @@ def chain_fb(init, trans, marginals: bool = True, lengths=None):
     """chain.py:64-95 batched: init [B,m], trans [B,n-1,m,m] ->
     (logz [B] f64, marg_init [B,m] | None, marg_trans | None, status [B]).
     `lengths` [B] int32 (optional): ragged batch, instance b uses its first
-    lengths[b] positions (sdb_chain_fb_lengths; marginals past them are 0)."""
+    lengths[b] positions (sdb_chain_fb_lengths; marginals past them are 0).
+    float64 init/trans (no lengths): the exact mode, sdb_chain_fb_f64."""
     lib = _lib.load()
+    if exact(init) and lengths is None:
+        return _chain_fb_f64(lib, init, trans, marginals)
     init, trans = f32(init, "init"), f32(trans, "transitions")
     B, m = init.shape
     n = trans.shape[1] + 1
@@ -75,6 +89,22 @@ def chain_fb(init, trans, marginals: bool = True, lengths=None):
     rc = lib.sdb_chain_fb(ptr(init), ptr(trans), B, n, m, ptr(logz), ptr(mi), ptr(mt), ptr(status),
                           ptr(ws), ws.numel(), stream_ptr(dev))
     _lib.check(rc, "sdb_chain_fb")
+    return logz, mi, mt, status
+
+
+def _chain_fb_f64(lib, init, trans, marginals):
+    init, trans = f64(init, "init"), f64(trans, "transitions")
+    B, m = init.shape
+    n = trans.shape[1] + 1
+    dev = init.device
+    logz = torch.empty(B, dtype=torch.float64, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    mi = torch.empty_like(init) if marginals else None
+    mt = torch.empty_like(trans) if marginals else None
+    ws = workspace(lib.sdb_chain_fb_f64_workspace(B, n, m), dev)
+    rc = lib.sdb_chain_fb_f64(ptr(init), ptr(trans), B, n, m, ptr(logz), ptr(mi), ptr(mt), ptr(status), ptr(ws),
+                              ws.numel(), stream_ptr(dev))
+    _lib.check(rc, "sdb_chain_fb_f64")
     return logz, mi, mt, status
 
 
@@ -155,13 +185,20 @@ def nw_fb(theta, marginals: bool = True):
     """alignment.py:62-118 batched: theta [B,n+1,m+1,3] ->
     (logz [B] f64, marg [B,n+1,m+1,3] | None, status)."""
     lib = _lib.load()
-    theta = f32(theta, "move_potentials")
+    x64 = exact(theta)
+    theta = (f64 if x64 else f32)(theta, "move_potentials")
     B, n1, m1, _ = theta.shape
     n, m = n1 - 1, m1 - 1
     dev = theta.device
     logz = torch.empty(B, dtype=torch.float64, device=dev)
     status = torch.empty(B, dtype=torch.int32, device=dev)
     marg = torch.empty_like(theta) if marginals else None
+    if x64:
+        ws = workspace(lib.sdb_nw_fb_f64_workspace(B, n, m) if marginals else 0, dev)
+        rc = lib.sdb_nw_fb_f64(ptr(theta), B, n, m, ptr(logz), ptr(marg), ptr(status), ptr(ws), ws.numel(),
+                               stream_ptr(dev))
+        _lib.check(rc, "sdb_nw_fb_f64")
+        return logz, marg, status
     ws = workspace(lib.sdb_nw_fb_workspace(B, n, m) if marginals else 0, dev)
     rc = lib.sdb_nw_fb(ptr(theta), B, n, m, ptr(logz), ptr(marg), ptr(status), ptr(ws), ws.numel(),
                        stream_ptr(dev))
@@ -194,7 +231,8 @@ def ctc_fb(frame_potentials, targets, marginals: bool = True):
     """alignment.py:248-301 batched: frame_potentials [B,T,V], targets
     [B,L] -> (logz [B] f64, marg [B,T,V] | None, status)."""
     lib = _lib.load()
-    fp = f32(frame_potentials, "frame_potentials")
+    x64 = exact(frame_potentials)
+    fp = (f64 if x64 else f32)(frame_potentials, "frame_potentials")
     tg = i32(targets, "targets")
     B, T, V = fp.shape
     L = tg.shape[1]
@@ -202,6 +240,12 @@ def ctc_fb(frame_potentials, targets, marginals: bool = True):
     logz = torch.empty(B, dtype=torch.float64, device=dev)
     status = torch.empty(B, dtype=torch.int32, device=dev)
     marg = torch.empty_like(fp) if marginals else None
+    if x64:
+        ws = workspace(lib.sdb_ctc_fb_f64_workspace(B, T, V, L) if marginals else 0, dev)
+        rc = lib.sdb_ctc_fb_f64(ptr(fp), ptr(tg), B, T, V, L, ptr(logz), ptr(marg), ptr(status), ptr(ws),
+                                ws.numel(), stream_ptr(dev))
+        _lib.check(rc, "sdb_ctc_fb_f64")
+        return logz, marg, status
     ws = workspace(lib.sdb_ctc_fb_workspace(B, T, V, L) if marginals else 0, dev)
     rc = lib.sdb_ctc_fb(ptr(fp), ptr(tg), B, T, V, L, ptr(logz), ptr(marg), ptr(status), ptr(ws), ws.numel(),
                         stream_ptr(dev))
@@ -234,12 +278,19 @@ def tree_fb(span_potentials, marginals: bool = True):
     """constituency.py:52-110 batched: span_potentials [B,n,n,m] ->
     (logz [B] f64, marg [B,n,n,m] | None, status)."""
     lib = _lib.load()
-    th = f32(span_potentials, "span_potentials")
+    x64 = exact(span_potentials)
+    th = (f64 if x64 else f32)(span_potentials, "span_potentials")
     B, n, _, m = th.shape
     dev = th.device
     logz = torch.empty(B, dtype=torch.float64, device=dev)
     status = torch.empty(B, dtype=torch.int32, device=dev)
     marg = torch.empty_like(th) if marginals else None
+    if x64:
+        ws = workspace(lib.sdb_tree_fb_f64_workspace(B, n, m), dev)
+        rc = lib.sdb_tree_fb_f64(ptr(th), B, n, m, ptr(logz), ptr(marg), ptr(status), ptr(ws), ws.numel(),
+                                 stream_ptr(dev))
+        _lib.check(rc, "sdb_tree_fb_f64")
+        return logz, marg, status
     ws = workspace(lib.sdb_tree_fb_workspace(B, n, m), dev)
     rc = lib.sdb_tree_fb(ptr(th), B, n, m, ptr(logz), ptr(marg), ptr(status), ptr(ws), ws.numel(),
                          stream_ptr(dev))
@@ -269,12 +320,19 @@ def mtt(adjacency, single_root: bool = False, marginals: bool = True):
     """spanning.py:90-175 batched: adjacency [B,n+1,n+1] ->
     (logz [B] f64, marg [B,n+1,n+1] | None, status)."""
     lib = _lib.load()
-    adj = f32(adjacency, "adjacency")
+    x64 = exact(adjacency)
+    adj = (f64 if x64 else f32)(adjacency, "adjacency")
     B, n1, _ = adj.shape
     dev = adj.device
     logz = torch.empty(B, dtype=torch.float64, device=dev)
     status = torch.empty(B, dtype=torch.int32, device=dev)
     marg = torch.empty_like(adj) if marginals else None
+    if x64:
+        ws = workspace(lib.sdb_mtt_f64_workspace(B, n1 - 1), dev)
+        rc = lib.sdb_mtt_f64(ptr(adj), B, n1 - 1, 1 if single_root else 0, ptr(logz), ptr(marg), ptr(status),
+                             ptr(ws), ws.numel(), stream_ptr(dev))
+        _lib.check(rc, "sdb_mtt_f64")
+        return logz, marg, status
     if n1 - 1 <= 128:
         rc = lib.sdb_mtt(ptr(adj), B, n1 - 1, 1 if single_root else 0, ptr(logz), ptr(marg), ptr(status),
                          stream_ptr(dev))
@@ -294,12 +352,18 @@ def eisner(adjacency, single_root: bool = False, marginals: bool = True):
     """spanning.py:183-280 batched: adjacency [B,n+1,n+1] ->
     (logz [B] f64, marg [B,n+1,n+1] | None, status)."""
     lib = _lib.load()
-    adj = f32(adjacency, "adjacency")
+    x64 = exact(adjacency)
+    adj = (f64 if x64 else f32)(adjacency, "adjacency")
     B, n1, _ = adj.shape
     dev = adj.device
     logz = torch.empty(B, dtype=torch.float64, device=dev)
     status = torch.empty(B, dtype=torch.int32, device=dev)
     marg = torch.empty_like(adj) if marginals else None
+    if x64:
+        rc = lib.sdb_eisner_f64(ptr(adj), B, n1 - 1, 1 if single_root else 0, ptr(logz), ptr(marg), ptr(status),
+                                stream_ptr(dev))
+        _lib.check(rc, "sdb_eisner_f64")
+        return logz, marg, status
     rc = lib.sdb_eisner(ptr(adj), B, n1 - 1, 1 if single_root else 0, ptr(logz), ptr(marg), ptr(status),
                         stream_ptr(dev))
     _lib.check(rc, "sdb_eisner")
@@ -328,7 +392,8 @@ def eisner_kuhlmann(adjacency, single_root: bool = False, marginals: bool = True
     Eisner kernels on the current stream, Kuhlmann concurrently on a side
     stream (the Eisner grid's second wave leaves SMs idle).
     -> ((logz, marg, status), (heads, score, status))."""
-    adj = f32(adjacency, "adjacency")
+    _require_cuda(adjacency, "adjacency")
+    adj = adjacency.contiguous() if exact(adjacency) else f32(adjacency, "adjacency")
     return _concurrent(adj.device, lambda: eisner(adj, single_root, marginals),
                        lambda st: kuhlmann(adj, single_root, stream=st))
 
@@ -341,6 +406,9 @@ def pcfg_fb(root, rules, emissions, sticky=None, marginals: bool = True):
     emissions [B,n,PT], sticky [B,n,n] | None -> (logz [B] f64,
     span marginals [B,n,n] | None, status)."""
     lib = _lib.load()
+    if exact(rules):
+        logz, g, status = _pcfg_f64(lib, root, rules, emissions, sticky, marginals, False)
+        return logz, (g["sticky"] if g else None), status
     root = f32(root, "root")
     rules = f32(rules, "binary_rules")
     emis = f32(emissions, "emissions")
@@ -363,6 +431,8 @@ def pcfg_grad(root, rules, emissions, sticky=None):
     {"root" [B,NT], "binary_rules" [B,NT,S,S], "emissions" [B,n,PT],
     "sticky" [B,n,n]} fp32, status)."""
     lib = _lib.load()
+    if exact(rules):
+        return _pcfg_f64(lib, root, rules, emissions, sticky, True, True)
     root = f32(root, "root")
     rules = f32(rules, "binary_rules")
     emis = f32(emissions, "emissions")
@@ -379,6 +449,28 @@ def pcfg_grad(root, rules, emissions, sticky=None):
                            ptr(g["root"]), ptr(g["binary_rules"]), ptr(g["emissions"]), ptr(status), ptr(ws),
                            ws.numel(), stream_ptr(dev))
     _lib.check(rc, "sdb_pcfg_grad")
+    return logz, g, status
+
+
+def _pcfg_f64(lib, root, rules, emissions, sticky, marginals, grad):
+    root, rules, emis = f64(root, "root"), f64(rules, "binary_rules"), f64(emissions, "emissions")
+    st_in = f64(sticky, "sticky") if sticky is not None else None
+    B, NT = root.shape
+    n, PT = emis.shape[1], emis.shape[2]
+    dev = root.device
+    logz = torch.empty(B, dtype=torch.float64, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    g = None
+    if marginals:
+        g = {"sticky": torch.empty(B, n, n, dtype=torch.float64, device=dev)}
+        if grad:
+            g.update(root=torch.empty_like(root), binary_rules=torch.empty_like(rules), emissions=torch.empty_like(emis))
+    ws = workspace(lib.sdb_pcfg_f64_workspace(B, n, NT, PT, 1 if grad else 0), dev)
+    rc = lib.sdb_pcfg_f64(ptr(root), ptr(rules), ptr(emis), ptr(st_in), B, n, NT, PT, ptr(logz),
+                          ptr(g["sticky"]) if g else None, ptr(g["root"]) if grad else None,
+                          ptr(g["binary_rules"]) if grad else None, ptr(g["emissions"]) if grad else None,
+                          ptr(status), ptr(ws), ws.numel(), stream_ptr(dev))
+    _lib.check(rc, "sdb_pcfg_f64")
     return logz, g, status
 
 
@@ -409,12 +501,19 @@ def pcfg_viterbi(root, rules, emissions, sticky=None):
 def semimarkov_fb(segment_potentials, marginals: bool = True):
     """chain.py:250-298 batched: [B,n,s,m,m] -> (logz, marg | None, status)."""
     lib = _lib.load()
-    th = f32(segment_potentials, "segment_potentials")
+    x64 = exact(segment_potentials)
+    th = (f64 if x64 else f32)(segment_potentials, "segment_potentials")
     B, n, s, m, _ = th.shape
     dev = th.device
     logz = torch.empty(B, dtype=torch.float64, device=dev)
     status = torch.empty(B, dtype=torch.int32, device=dev)
     marg = torch.empty_like(th) if marginals else None
+    if x64:
+        ws = workspace(lib.sdb_semimarkov_fb_f64_workspace(B, n, s, m), dev)
+        rc = lib.sdb_semimarkov_fb_f64(ptr(th), B, n, s, m, ptr(logz), ptr(marg), ptr(status), ptr(ws), ws.numel(),
+                                       stream_ptr(dev))
+        _lib.check(rc, "sdb_semimarkov_fb_f64")
+        return logz, marg, status
     rc = lib.sdb_semimarkov_fb(ptr(th), B, n, s, m, ptr(logz), ptr(marg), ptr(status), stream_ptr(dev))
     _lib.check(rc, "sdb_semimarkov_fb")
     return logz, marg, status
@@ -439,11 +538,6 @@ def semimarkov_viterbi(segment_potentials):
 
 
 # -------------------------------------------------------------- sampling
-
-
-def f64(t: torch.Tensor, name: str = "tensor") -> torch.Tensor:
-    _require_cuda(t, name)
-    return t.to(torch.float64).contiguous()
 
 
 def stream_len(family: str, shape: dict) -> int:
@@ -682,13 +776,15 @@ def expected_score(pairs, B: int, device):
     flag = torch.zeros(B, dtype=torch.int32, device=device)
     keep = []
     for marg, theta in pairs:
-        marg, theta = f32(marg, "marginals"), f32(theta, "potentials")
+        x64 = exact(marg) or exact(theta)
+        cv = f64 if x64 else f32
+        marg, theta = cv(marg, "marginals"), cv(theta, "potentials")
         if marg.shape != theta.shape:
             raise ValueError(f"marginals {tuple(marg.shape)} vs potentials {tuple(theta.shape)}")
         keep += [marg, theta]
-        rc = lib.sdb_masked_dot(ptr(marg), ptr(theta), B, marg.numel() // max(B, 1), ptr(out), ptr(flag),
-                                stream_ptr(device))
-        _lib.check(rc, "sdb_masked_dot")
+        fn = lib.sdb_masked_dot_f64 if x64 else lib.sdb_masked_dot
+        rc = fn(ptr(marg), ptr(theta), B, marg.numel() // max(B, 1), ptr(out), ptr(flag), stream_ptr(device))
+        _lib.check(rc, "sdb_masked_dot_f64" if x64 else "sdb_masked_dot")
     return out, flag
 
 

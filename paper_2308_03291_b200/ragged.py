@@ -203,7 +203,11 @@ def native_ragged(ds) -> bool:
     (chains: sdb_chain_fb_lengths / sdb_chain_viterbi_lengths)."""
     if not isinstance(ds[0], LinearChainCRF) or not needs_padding(ds):
         return False
+    from . import backends
     from .kernels import chain_ragged_supported
+
+    if backends.EXACT:  # the exact-mode chain kernel takes same-length groups (padded instead)
+        return False
 
     return chain_ragged_supported(max(d.n for d in ds), ds[0].m)
 

@@ -73,10 +73,15 @@ def _marg(d):
     return {k: np.asarray(v, dtype=np.float64) for k, v in gd.potential_marginals(to_gpu(d)).items()}
 
 
-def install(sd):
+def install(sd, exact: bool = False):
     """Patch the reference package `sd` (the imported `structdist`); returns an
-    undo callable."""
+    undo callable.  exact=True routes log-partition / marginals through the
+    float64 entry points (gd.set_precision("fp64")) so results match the
+    reference at its own tolerances."""
     wrap = _errors_as(sd)
+    prev = gd.get_precision()
+    if exact:
+        gd.set_precision("fp64")
     ch, al, co, sp = sd.chain, sd.alignment, sd.constituency, sd.spanning
     lz = lambda d: float(gd.log_partition(to_gpu(d)))  # noqa: E731
     am = lambda d: gd.argmax(to_gpu(d))  # noqa: E731
@@ -119,4 +124,5 @@ def install(sd):
     def undo():
         for mod, name, fn in saved:
             setattr(mod, name, fn)
+        gd.set_precision(prev)
     return undo

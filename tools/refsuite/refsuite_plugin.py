@@ -16,9 +16,11 @@ import structdist  # noqa: E402  (the unmodified reference)
 
 from paper_2308_03291_b200 import refshim  # noqa: E402
 
-_undo = refshim.install(structdist)
+_EXACT = os.environ.get("SDB_REFSUITE_EXACT", "0") == "1"  # fp64 entry points (set_precision("fp64"))
+_undo = refshim.install(structdist, exact=_EXACT)
 
 
 def pytest_report_header(config):
-    return ["structdist family functions routed onto the sm_100a kernels (paper_2308_03291_b200.refshim)",
+    return ["structdist family functions routed onto the sm_100a kernels (paper_2308_03291_b200.refshim)"
+            + (" -- exact fp64 mode" if _EXACT else ""),
             f"structdist from {os.path.dirname(structdist.__file__)}"]
