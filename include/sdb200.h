@@ -355,6 +355,10 @@ size_t sdb_pcfg_f64_workspace(int64_t B, int32_t n, int32_t NT, int32_t PT, int3
 int sdb_pcfg_f64(const double* root, const double* rules, const double* emissions, const double* sticky, int64_t B,
                  int32_t n, int32_t NT, int32_t PT, double* logz, double* span_marg, double* groot, double* grules,
                  double* gemis, int32_t* status, void* workspace, size_t ws_bytes, void* stream);
+/* pcfg_max_score / pcfg_argmax on float64 grammars (workspace: sdb_pcfg_viterbi_workspace). */
+int sdb_pcfg_viterbi_f64(const double* root, const double* rules, const double* emissions, const double* sticky,
+                         int64_t B, int32_t n, int32_t NT, int32_t PT, int8_t* span_mask, double* score,
+                         int32_t* status, void* workspace, size_t ws_bytes, void* stream);
 size_t sdb_mtt_f64_workspace(int64_t B, int32_t n);
 int sdb_mtt_f64(const double* adjacency, int64_t B, int32_t n, int32_t single_root, double* logz, double* marg,
                 int32_t* status, void* workspace, size_t ws_bytes, void* stream);

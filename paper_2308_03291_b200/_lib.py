@@ -35,6 +35,8 @@ SIGNATURES = {
     "sdb_pcfg_f64_workspace": (_sz, [_i64, _i32, _i32, _i32, _i32]),
     "sdb_pcfg_f64": (ctypes.c_int, [_c_p, _c_p, _c_p, _c_p, _i64, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p,
                                     _c_p, _c_p, _sz, _c_p]),
+    "sdb_pcfg_viterbi_f64": (ctypes.c_int, [_c_p, _c_p, _c_p, _c_p, _i64, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p,
+                                            _sz, _c_p]),
     "sdb_mtt_f64_workspace": (_sz, [_i64, _i32]),
     "sdb_mtt_f64": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
     "sdb_eisner_f64": (ctypes.c_int, [_c_p, _i64, _i32, _i32, _c_p, _c_p, _c_p, _c_p]),

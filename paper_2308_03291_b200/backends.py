@@ -83,11 +83,12 @@ class Result:
 
 
 class ArgmaxResult:
-    def __init__(self, status, build, vacuous_msg, score=None):
+    def __init__(self, status, build, vacuous_msg, score=None, score_exact=False):
         self.status = np.asarray(status)
         self._build = build
         self.msg = vacuous_msg
         self._score = score
+        self._score_exact = score_exact  # the kernel read the float64 potentials themselves
 
     def raise_vacuous(self, i):
         Result.raise_vacuous(self, i)
@@ -96,7 +97,9 @@ class ArgmaxResult:
         return self._build(i)
 
     def score_of(self, i, dist, ind):
-        if self._score is not None:
+        # exact mode: the indicator's score over the float64 potentials (dist.py:162),
+        # not the kernel's sum over their fp32 rounding
+        if self._score is not None and (self._score_exact or not EXACT):
             return float(self._score[i])
         from .dist import structure_score
 
@@ -699,7 +702,7 @@ class PCFGBackend(Backend):
 
     def argmax(self, ds):
         # pcfg_argmax (constituency.py:366-371): fp64 max-plus chart + first-max walk
-        root, rules, emis, sticky = self._inputs(ds)
+        root, rules, emis, sticky = self._inputs(ds, pot_dtype())
         mask, score, st = K.pcfg_viterbi(root, rules, emis, sticky)
         mh = to_host(mask).astype(np.float64)
 
@@ -707,7 +710,7 @@ class PCFGBackend(Backend):
             return {"sticky": mh[i]}
 
         # the PCFG argmax score is pcfg_max_score (dist.py:153-154, 164-165)
-        return ArgmaxResult(to_host(st), build, self.vacuous_msg, score=to_host(score))
+        return ArgmaxResult(to_host(st), build, self.vacuous_msg, score=to_host(score), score_exact=True)
 
 
 # ------------------------------------------------------------ semi-Markov

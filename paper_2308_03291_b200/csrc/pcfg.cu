@@ -642,10 +642,10 @@ __device__ ArgBest block_argmax(ArgBest x, ArgBest* red) {
 // kLog: log-semiring chart (constituency.py:246-266 with logsumexp) and
 // Gumbel-max picks from the caller's stream (pcfg_sample, constituency.py:374-378);
 // mask [B][num][n][n], used [B].
-template <bool kLog>
+template <bool kLog, typename TP = float>  // TP = double: the exact mode (float64 grammar)
 __global__ void __launch_bounds__(kThreads) pcfg_max_kernel(
-    const float* __restrict__ root_all, const float* __restrict__ rules_all, const float* __restrict__ emis_all,
-    const float* __restrict__ sticky_all, int n, int NT, int PT, double* __restrict__ chart_all,
+    const TP* __restrict__ root_all, const TP* __restrict__ rules_all, const TP* __restrict__ emis_all,
+    const TP* __restrict__ sticky_all, int n, int NT, int PT, double* __restrict__ chart_all,
     int8_t* __restrict__ mask_all, double* __restrict__ score, int32_t* __restrict__ status,
     const double* __restrict__ noise_all = nullptr, int64_t cap = 0, int num = 1, int32_t* __restrict__ used = nullptr) {
   extern __shared__ double pairs[];  // [S][S], then the walk stack [3][2n] ints
@@ -656,10 +656,10 @@ __global__ void __launch_bounds__(kThreads) pcfg_max_kernel(
   int* stk_j = stk_i + 2 * n;
   int* stk_a = stk_j + 2 * n;
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const float* root = root_all + (size_t)b * NT;
-  const float* rules = rules_all + (size_t)b * NT * S2;
-  const float* emis = emis_all + (size_t)b * n * PT;
-  const float* sticky = sticky_all ? sticky_all + (size_t)b * n * n : nullptr;
+  const TP* root = root_all + (size_t)b * NT;
+  const TP* rules = rules_all + (size_t)b * NT * S2;
+  const TP* emis = emis_all + (size_t)b * n * PT;
+  const TP* sticky = sticky_all ? sticky_all + (size_t)b * n * n : nullptr;
   double* chart = chart_all + (size_t)b * n * n * S;
   int8_t* mask = mask_all + (size_t)b * num * n * n;
   const double* g = kLog ? noise_all + (size_t)b * cap : nullptr;
@@ -669,11 +669,11 @@ __global__ void __launch_bounds__(kThreads) pcfg_max_kernel(
   __syncthreads();
   {
     int bad = 0;
-    for (int e = tid; e < NT * S2; e += kThreads) bad |= bad_input(rules[e]);
-    for (int e = tid; e < NT; e += kThreads) bad |= bad_input(root[e]);
-    for (int e = tid; e < n * PT; e += kThreads) bad |= bad_input(emis[e]);
+    for (int e = tid; e < NT * S2; e += kThreads) bad |= bad_value(rules[e]);
+    for (int e = tid; e < NT; e += kThreads) bad |= bad_value(root[e]);
+    for (int e = tid; e < n * PT; e += kThreads) bad |= bad_value(emis[e]);
     if (sticky)
-      for (int e = tid; e < n * n; e += kThreads) bad |= !(sticky[e] == 0.f || sticky[e] == ninf());
+      for (int e = tid; e < n * n; e += kThreads) bad |= !((double)sticky[e] == 0.0 || (double)sticky[e] == ninfd());
     if (bad) atomicOr(&badsh, 1);
     for (int e = tid; e < num * n * n; e += kThreads) mask[e] = 0;
   }
@@ -700,7 +700,7 @@ __global__ void __launch_bounds__(kThreads) pcfg_max_kernel(
       for (int A = warp; A < S; A += kWarps) {
         double m = ninfd();
         if (A < NT) {
-          const float* ra = rules + (size_t)A * S2;
+          const TP* ra = rules + (size_t)A * S2;
           if (!kLog) {
             for (int e = lane; e < S2; e += 32) m = fmax(m, (double)ra[e] + pairs[e]);
             m = warp_maxd(m);
@@ -777,7 +777,7 @@ __global__ void __launch_bounds__(kThreads) pcfg_max_kernel(
     if (tid == 0) maskr[i * n + j] = 1;
     if (i == j) continue;
     const int width = j - i;
-    const float* ra = rules + (size_t)a * S2;
+    const TP* ra = rules + (size_t)a * S2;
     ArgBest y{ninfd(), 1 << 30};
     for (int e = tid; e < width * S2; e += kThreads) {
       const int ko = e / S2, r = e - ko * S2, Bq = r / S, Cq = r - Bq * S;
@@ -909,6 +909,26 @@ extern "C" int sdb_pcfg_viterbi(const float* root, const float* rules, const flo
       cudaSuccess)
     return SDB_ERR_CUDA;
   pcfg_max_kernel<false><<<(unsigned)B, kThreads, smem, (cudaStream_t)stream>>>(
+      root, rules, emissions, sticky, n, NT, PT, (double*)workspace, span_mask, score, status);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
+// exact mode: the same max-plus chart and walk on float64 grammars (the score is
+// _pcfg_best_derivation_score, dist.py:157, exactly)
+extern "C" int sdb_pcfg_viterbi_f64(const double* root, const double* rules, const double* emissions,
+                                    const double* sticky, int64_t B, int32_t n, int32_t NT, int32_t PT,
+                                    int8_t* span_mask, double* score, int32_t* status, void* workspace,
+                                    size_t ws_bytes, void* stream) {
+  int rc = pcfg_check(B, n, NT, PT);
+  if (rc) return rc;
+  if (!root || !rules || !emissions || !span_mask || !score || !status) return SDB_ERR_ARG;
+  if (B == 0) return SDB_OK;
+  if (!workspace || ws_bytes < sdb_pcfg_viterbi_workspace(B, n, NT, PT)) return SDB_ERR_WORKSPACE;
+  const size_t smem = max_smem(n, NT, PT);
+  if (smem > 220 * 1024) return SDB_ERR_UNSUPPORTED;
+  if (sdb_set_smem((const void*)pcfg_max_kernel<false, double>, smem) != cudaSuccess) return SDB_ERR_CUDA;
+  pcfg_max_kernel<false, double><<<(unsigned)B, kThreads, smem, (cudaStream_t)stream>>>(
       root, rules, emissions, sticky, n, NT, PT, (double*)workspace, span_mask, score, status);
   SDB_CHECK_LAUNCH();
   return SDB_OK;

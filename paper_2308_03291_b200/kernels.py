@@ -476,12 +476,14 @@ def _pcfg_f64(lib, root, rules, emissions, sticky, marginals, grad):
 
 def pcfg_viterbi(root, rules, emissions, sticky=None):
     """constituency.py:275-277, 343-371 batched -> (span_mask [B,n,n] int8,
-    score [B] f64 = pcfg_max_score, status)."""
+    score [B] f64 = pcfg_max_score, status); float64 inputs: sdb_pcfg_viterbi_f64."""
     lib = _lib.load()
-    root = f32(root, "root")
-    rules = f32(rules, "binary_rules")
-    emis = f32(emissions, "emissions")
-    st_in = f32(sticky, "sticky") if sticky is not None else None
+    x64 = exact(rules)
+    cv = f64 if x64 else f32
+    root = cv(root, "root")
+    rules = cv(rules, "binary_rules")
+    emis = cv(emissions, "emissions")
+    st_in = cv(sticky, "sticky") if sticky is not None else None
     B, NT = root.shape
     n, PT = emis.shape[1], emis.shape[2]
     dev = root.device
@@ -489,9 +491,10 @@ def pcfg_viterbi(root, rules, emissions, sticky=None):
     score = torch.empty(B, dtype=torch.float64, device=dev)
     status = torch.empty(B, dtype=torch.int32, device=dev)
     ws = workspace(lib.sdb_pcfg_viterbi_workspace(B, n, NT, PT), dev)
-    rc = lib.sdb_pcfg_viterbi(ptr(root), ptr(rules), ptr(emis), ptr(st_in), B, n, NT, PT, ptr(mask), ptr(score),
-                              ptr(status), ptr(ws), ws.numel(), stream_ptr(dev))
-    _lib.check(rc, "sdb_pcfg_viterbi")
+    fn = lib.sdb_pcfg_viterbi_f64 if x64 else lib.sdb_pcfg_viterbi
+    rc = fn(ptr(root), ptr(rules), ptr(emis), ptr(st_in), B, n, NT, PT, ptr(mask), ptr(score), ptr(status), ptr(ws),
+            ws.numel(), stream_ptr(dev))
+    _lib.check(rc, "sdb_pcfg_viterbi_f64" if x64 else "sdb_pcfg_viterbi")
     return mask, score, status
 
 
