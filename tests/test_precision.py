@@ -1,0 +1,64 @@
+"""Host logic of the exact mode (no GPU): the precision switch, what it
+routes, and that the refshim restores the previous mode on undo."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2308_03291_b200 as sd
+from paper_2308_03291_b200 import backends, kernels as K, ragged
+
+
+@pytest.fixture(autouse=True)
+def restore():
+    yield
+    sd.set_precision("fp32")
+
+
+def test_switch_values():
+    assert sd.get_precision() == "fp32"
+    sd.set_precision("fp64")
+    assert sd.get_precision() == "fp64" and backends.pot_dtype() == torch.float64
+    sd.set_precision("fp32")
+    assert backends.pot_dtype() == torch.float32
+    with pytest.raises(ValueError):
+        sd.set_precision("fp16")
+
+
+def test_exact_dispatch_is_by_dtype():
+    assert K.exact(torch.zeros(2, dtype=torch.float64))
+    assert not K.exact(torch.zeros(2, dtype=torch.float32))
+    assert not K.exact(np.zeros(2))
+
+
+def test_exact_mode_pads_ragged_chains():
+    ds = [sd.LinearChainCRF(np.zeros(3), np.zeros((n - 1, 3, 3))) for n in (4, 6)]
+    sd.set_precision("fp64")
+    assert not ragged.native_ragged(ds)  # the fp64 chain kernel takes same-length groups
+
+
+def test_refshim_restores_precision():
+    from paper_2308_03291_b200 import refshim
+
+    class _Mod:  # the attributes install() replaces, on stand-in modules
+        pass
+
+    fake = _Mod()
+    fake.errors = type("E", (), {"VacuousDistribution": ValueError, "InvalidProblem": TypeError,
+                                 "UnsupportedInference": KeyError})
+    names = {"chain": ["forward_log_partition", "chain_marginals", "chain_argmax", "semi_markov_log_partition",
+                       "semi_markov_marginals", "semi_markov_argmax"],
+             "alignment": ["nw_log_partition", "nw_marginals", "nw_argmax", "ctc_log_partition", "ctc_marginals",
+                           "ctc_argmax"],
+             "constituency": ["cky_log_partition", "tree_marginals", "tree_argmax", "pcfg_inside", "pcfg_gradients",
+                              "pcfg_argmax", "pcfg_max_score"],
+             "spanning": ["span_log_partition", "span_marginals", "span_argmax"]}
+    for mod, fns in names.items():
+        m = _Mod()
+        for f in fns:
+            setattr(m, f, None)
+        setattr(fake, mod, m)
+    undo = refshim.install(fake, exact=True)
+    assert sd.get_precision() == "fp64"
+    undo()
+    assert sd.get_precision() == "fp32" and fake.chain.chain_marginals is None
