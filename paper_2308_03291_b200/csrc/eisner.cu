@@ -32,6 +32,7 @@ namespace {
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxN = 128;
+static_assert(kMaxN <= 8 * kWarps, "per-width arc-weight prefetch: <= 8 spans per warp (16 lanes)");
 constexpr int kQ = (kMaxN + 1 + 31) / 32;  // max split terms per lane
 
 // packed strict-upper index over positions 0..n (i < j)
@@ -389,13 +390,20 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
   // ================================================================ inside
   for (int w = 1; w <= n; ++w) {
     float lmax = 0.f;
+    // the arc weights of ALL this warp's spans of the width (<= 8 spans for n <= 128):
+    // lane 2q / 2q+1 loads the right / left arc of span warp + q kWarps, so one L2
+    // latency per width is exposed instead of one per span pair
+    float wpre;
+    {
+      const int q = lane >> 1, i = warp + q * kWarps;
+      wpre = (i + w <= n) ? ((lane & 1) ? W(i + w, i) : W(i, i + w)) : 0.f;
+    }
     // two spans per warp iteration: their reductions are independent (ILP)
-    for (int i0 = warp; i0 + w <= n; i0 += 2 * kWarps) {
+    for (int i0 = warp, it = 0; i0 + w <= n; i0 += 2 * kWarps, ++it) {
       const int iA = i0, iB = i0 + kWarps;
       const bool hasB = iB + w <= n;
-      // arc weights first: their global-load latency overlaps the dot products
-      const float wrA = W(iA, iA + w), wlA = W(iA + w, iA);
-      const float wrB = hasB ? W(iB, iB + w) : 0.f, wlB = hasB ? W(iB + w, iB) : 0.f;
+      const float wrA = __shfl_sync(0xffffffffu, wpre, 4 * it), wlA = __shfl_sync(0xffffffffu, wpre, 4 * it + 1);
+      const float wrB = __shfl_sync(0xffffffffu, wpre, 4 * it + 2), wlB = __shfl_sync(0xffffffffu, wpre, 4 * it + 3);
       const int qi = (w + 31) >> 5;  // split terms per lane actually present at this width
       float sA = 0.f, sB = 0.f;
 #pragma unroll
@@ -492,10 +500,15 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
   // =============================================================== outside
   for (int w = n; w >= 1; --w) {
     float lmax = 0.f;
-    for (int a = warp; a + w <= n; a += kWarps) {
+    float wpre;  // this warp's arc weights of the width, as in the inside pass
+    {
+      const int q = lane >> 1, a = warp + q * kWarps;
+      wpre = (a + w <= n) ? ((lane & 1) ? W(a, a + w) : W(a + w, a)) : 0.f;
+    }
+    for (int a = warp, it = 0; a + w <= n; a += kWarps, ++it) {
       const int bb = a + w;
       const int n1 = n - bb, n2 = a;
-      const float wba = W(bb, a), wab = W(a, bb);  // issued before the dot products
+      const float wba = __shfl_sync(0xffffffffu, wpre, 2 * it), wab = __shfl_sync(0xffffffffu, wpre, 2 * it + 1);
       const int qo1 = (max(n1, n2) + 31) >> 5, qo2 = (max(n1, a) + 32) >> 5;
       float sA = 0.f, sB = 0.f;
 #pragma unroll
