@@ -398,6 +398,50 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
       const int q = lane >> 1, i = warp + q * kWarps;
       wpre = (i + w <= n) ? ((lane & 1) ? W(i + w, i) : W(i, i + w)) : 0.f;
     }
+    if (w <= 64) {
+      // narrow widths: G = 2^lg lanes per span (<= 4 split terms per lane), 32 / G spans of
+      // this warp per pass, reductions over lg shuffle levels inside each lane group
+      const int lg = w <= 4 ? 0 : w <= 8 ? 1 : w <= 16 ? 2 : w <= 32 ? 3 : 4;
+      const int G = 1 << lg, r = lane & (G - 1), qg = lane >> lg;
+      for (int q0 = 0; warp + q0 * kWarps + w <= n; q0 += 32 >> lg) {
+        const int q = q0 + qg, i = warp + q * kWarps, j = i + w;
+        const bool ok = j <= n;
+        const int src = 2 * min(q, 15);
+        const float wr = __shfl_sync(0xffffffffu, wpre, src), wl = __shfl_sync(0xffffffffu, wpre, src + 1);
+        float sf = 0.f;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int k = i + r + G * t;
+          if (ok && k < j) sf = fmaf(CR(i, k), CL(k + 1, j), sf);
+        }
+        for (int o = G >> 1; o > 0; o >>= 1) sf += __shfl_xor_sync(0xffffffffu, sf, o);
+        const float vir = wr * sf, vil = wl * sf;
+        if (ok && r == 0) {
+          ir[pk(i, j, n)] = vir;
+          il[pk(i, j, n)] = vil;
+        }
+        __syncwarp();
+        float sr = 0.f, sl = 0.f;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int o = r + G * t;
+          if (ok && o < w) {
+            sr = fmaf(ir[pk(i, i + 1 + o, n)], CR(i + 1 + o, j), sr);
+            sl = fmaf(CL(i, i + o), il[pk(i + o, j, n)], sl);
+          }
+        }
+        for (int o = G >> 1; o > 0; o >>= 1) {
+          sr += __shfl_xor_sync(0xffffffffu, sr, o);
+          sl += __shfl_xor_sync(0xffffffffu, sl, o);
+        }
+        if (ok && r == 0) {
+          cr[pk(i, j, n)] = sr;
+          cl[pk(i, j, n)] = sl;
+        }
+        if (ok) lmax = fmaxf(lmax, fmaxf(fmaxf(vir, vil), fmaxf(sr, sl)));
+      }
+      lmax = warp_max(lmax);
+    } else
     // two spans per warp iteration: their reductions are independent (ILP)
     for (int i0 = warp, it = 0; i0 + w <= n; i0 += 2 * kWarps, ++it) {
       const int iA = i0, iB = i0 + kWarps;
