@@ -62,3 +62,26 @@ print("D2H only      %.3f ms" % timed(d2h_only))
 print("whole both    %.3f ms" % timed(whole))
 print("chunked 32x8  %.3f ms" % timed(chunked([32] * 8)))
 print("chunked 8x32  %.3f ms" % timed(chunked([8] * 32)))
+
+s3, s4 = torch.cuda.Stream(), torch.cuda.Stream()
+
+
+def chunked2(c):
+    """two copy streams per direction, chunks alternating"""
+    def f():
+        cur = torch.cuda.current_stream()
+        s3.wait_stream(cur); s4.wait_stream(cur)
+        lo = 0
+        for k, sz in enumerate(c):
+            hi = lo + sz
+            with torch.cuda.stream(s1 if k % 2 == 0 else s3):
+                dx[lo:hi].copy_(x[lo:hi], non_blocking=True)
+            with torch.cuda.stream(s2 if k % 2 == 0 else s4):
+                y[lo:hi].copy_(dy[lo:hi], non_blocking=True)
+            lo = hi
+        cur.wait_stream(s3); cur.wait_stream(s4)
+    return f
+
+
+print("chunked2 32x8 %.3f ms" % timed(chunked2([32] * 8)))
+print("chunked2 16x16 %.3f ms" % timed(chunked2([16] * 16)))
