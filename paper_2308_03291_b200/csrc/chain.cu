@@ -1452,16 +1452,16 @@ fallback:
 }
 
 // Viterbi for m <= 32 (chain.py:98-114), one 512-thread CTA per instance:
-// warp w owns the next tags 2w, 2w+1, lane a the predecessor a.  A step is two
-// independent fp64 candidates per thread (their argmax chains interleave),
-// s_t[a] + theta_t[a][b] (the reference's addition
+// warp w owns the next tag w (kTPW = 1; kTPW = 2 packs tags 2w, 2w+1 into 16
+// warps and measured 59 vs 50 us at B=32 n=128), lane a the predecessor a: the
+// candidate s_t[a] + theta_t[a][b] (the reference's addition
 // order: bit-identical scores), and a warp argmax by REDUX on an
 // order-preserving 64-bit key (high word, then the low word among the ties,
 // then the lowest lane: the first maximum, chain.py:106).  The winner lane
 // writes s_(t+1)[b] and the backpointer; ONE CTA barrier per step publishes
 // the new scores.  theta tiles stream through a ring of kVD row-padded tiles
 // (pitch 36), one 16-byte cp.async per thread of the first 256 per step.
-constexpr int kVT = 512;
+constexpr int kVT = 1024;  // one warp per next tag (kTPW = 1)
 constexpr int kVD = 8;
 constexpr int kVTP = 36;
 
@@ -1481,7 +1481,9 @@ __device__ __forceinline__ int warp_argmax_key(uint64_t k) {
   return __ffs(cand) - 1;
 }
 
-__global__ void __launch_bounds__(kVT, 1) chain_viterbi_warp_kernel(
+// kTPW next tags per warp: 2 (512 threads) or 1 (1024 threads)
+template <int kTPW>
+__global__ void __launch_bounds__(32 * 32 / kTPW, 1) chain_viterbi_warp_kernel(
     const float* __restrict__ init, const float* __restrict__ trans, int n, int m, int32_t* __restrict__ tags,
     double* __restrict__ score, int32_t* __restrict__ status, const int32_t* __restrict__ lengths) {
   extern __shared__ __align__(16) float smw[];
@@ -1503,7 +1505,7 @@ __global__ void __launch_bounds__(kVT, 1) chain_viterbi_warp_kernel(
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(th + (size_t)t * 1024 + r * 32 + c4));
       }
     } else {
-      for (int e = tid; e < 1024; e += kVT) {
+      for (int e = tid; e < 1024; e += 32 * 32 / kTPW) {
         const int r = e >> 5, c = e & 31;
         if (r < m && c < m) {
           const unsigned dst = (unsigned)__cvta_generic_to_shared(tile + r * kVTP + c);
@@ -1512,7 +1514,9 @@ __global__ void __launch_bounds__(kVT, 1) chain_viterbi_warp_kernel(
       }
     }
   };
-  for (int d = 0; d < kVD; ++d) {
+  // tile t goes into ring slot t % kVD; the refill at step t is tile t + kVD - 1 into
+  // the slot every thread finished reading at step t - 1 (behind this step's barrier)
+  for (int d = 0; d < kVD - 1; ++d) {
     if (d < T) stage(d);
     cpa_commit();
   }
@@ -1523,28 +1527,26 @@ __global__ void __launch_bounds__(kVT, 1) chain_viterbi_warp_kernel(
     sv[tid] = tid < m ? (double)x : ninfd();
   }
   const bool alive = lane < m;
-  const int b0 = 2 * warp;
+  const int b0 = kTPW * warp;
   for (int t = 0; t < T; ++t) {
-    cpa_wait_d();
-    __syncthreads();  // tile t resident; s_t published
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(kVD - 2));
+    __syncthreads();  // tile t resident; s_t published; slot (t - 1) % kVD free
     const double* cur = sv + (t & 1) * 32;
     double* nxt = sv + ((t + 1) & 1) * 32;
-    const float2 x = *reinterpret_cast<const float2*>(ring + (t % kVD) * 32 * kVTP + lane * kVTP + b0);
+    const float* xr = ring + (t % kVD) * 32 * kVTP + lane * kVTP + b0;
     const double sa = cur[lane];
-    if (t + kVD < T) stage(t + kVD);
+    if (t + kVD - 1 < T) stage(t + kVD - 1);
     cpa_commit();
-    bad |= alive && ((b0 < m && bad_input(x.x)) | (b0 + 1 < m && bad_input(x.y)));
-    const double v0 = (alive && b0 < m) ? sa + (double)x.x : ninfd();
-    const double v1 = (alive && b0 + 1 < m) ? sa + (double)x.y : ninfd();
-    const int w0 = warp_argmax_key(dkey(v0));
-    const int w1 = warp_argmax_key(dkey(v1));
-    if (lane == w0) {
-      nxt[b0] = v0;
-      back[(size_t)(t + 1) * 32 + b0] = (uint8_t)w0;
-    }
-    if (lane == w1) {
-      nxt[b0 + 1] = v1;
-      back[(size_t)(t + 1) * 32 + b0 + 1] = (uint8_t)w1;
+#pragma unroll
+    for (int k = 0; k < kTPW; ++k) {
+      const float x = xr[k];
+      bad |= alive && b0 + k < m && bad_input(x);
+      const double v = (alive && b0 + k < m) ? sa + (double)x : ninfd();
+      const int w = warp_argmax_key(dkey(v));
+      if (lane == w) {
+        nxt[b0 + k] = v;
+        back[(size_t)(t + 1) * 32 + b0 + k] = (uint8_t)w;
+      }
     }
   }
   asm volatile("cp.async.wait_group 0;\n" ::);
@@ -1719,11 +1721,9 @@ extern "C" int sdb_chain_viterbi_lengths(const float* init, const float* trans, 
   const size_t smw = (size_t)kVD * 32 * kVTP * 4 + 64 * 8 + (size_t)n * 32 + 64;
   if (m > 32 || smw > 200 * 1024) return SDB_ERR_UNSUPPORTED;
   if (B == 0) return SDB_OK;
-  if (sdb_set_smem((const void*)chain_viterbi_warp_kernel, smw) !=
-      cudaSuccess)
-    return SDB_ERR_CUDA;
-  chain_viterbi_warp_kernel<<<(unsigned)B, kVT, smw, (cudaStream_t)stream>>>(init, trans, n, m, tags, score, status,
-                                                                           lengths);
+  if (sdb_set_smem((const void*)chain_viterbi_warp_kernel<1>, smw) != cudaSuccess) return SDB_ERR_CUDA;
+  chain_viterbi_warp_kernel<1><<<(unsigned)B, kVT, smw, (cudaStream_t)stream>>>(init, trans, n, m, tags, score,
+                                                                              status, lengths);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
 }
@@ -1743,11 +1743,9 @@ extern "C" int sdb_chain_viterbi(const float* init, const float* trans, int64_t 
   if (m <= 32) {
     const size_t smw = (size_t)kVD * 32 * kVTP * 4 + 64 * 8 + (size_t)n * 32 + 64;  // ring, scores, backpointers
     if (smw <= 200 * 1024) {
-      if (sdb_set_smem((const void*)chain_viterbi_warp_kernel, smw) !=
-          cudaSuccess)
-        return SDB_ERR_CUDA;
-      chain_viterbi_warp_kernel<<<(unsigned)B, kVT, smw, (cudaStream_t)stream>>>(init, trans, n, m, tags, score,
-                                                                               status, nullptr);
+      if (sdb_set_smem((const void*)chain_viterbi_warp_kernel<1>, smw) != cudaSuccess) return SDB_ERR_CUDA;
+      chain_viterbi_warp_kernel<1><<<(unsigned)B, kVT, smw, (cudaStream_t)stream>>>(init, trans, n, m, tags, score,
+                                                                                  status, nullptr);
       SDB_CHECK_LAUNCH();
       return SDB_OK;
     }
