@@ -550,6 +550,12 @@ __global__ void nw_walk_kernel(const int8_t* __restrict__ choice_all, int n, int
 // the warps in flight.  Delay lines are split into two 16-lane halves
 // (rows s-l for lanes 0-15 and 16-31 are 16 steps apart), which halves their
 // shared memory so that two CTAs fit on an SM.
+#ifndef SDB_MITM_BLK
+#define SDB_MITM_BLK 8
+#endif
+constexpr int kMBlk = SDB_MITM_BLK;          // steps per barrier block
+constexpr int kMLag = kMBlk == 4 ? 36 : kMBlk == 8 ? 40 : 48;  // >= 32 + kMBlk - 1, a multiple of kMBlk; kMLag + kMBlk < 96 (ring)
+static_assert(kMLag >= 31 + kMBlk && kMLag % kMBlk == 0 && kMLag + kMBlk < 96 && kRB % kMBlk == 0, "mitm lag");
 constexpr int kMP = 4;                       // potentials prefetch distance (steps)
 constexpr int kMRh = 20;                     // delay-line rows per half-warp (>= 16 + kMP)
 constexpr int kMGrp = kMRh * 48 + 16;        // floats per half-warp ring incl. 16-word bank pad
@@ -592,7 +598,7 @@ __device__ MShared mitm_carve(char* base, int NW) {
   return s;
 }
 
-__device__ __forceinline__ int mitm_rf(int w, int n, int NW) { return (40 * (NW - 1 - 2 * w) + n - 1) >> 1; }
+__device__ __forceinline__ int mitm_rf(int w, int n, int NW) { return (kMLag * (NW - 1 - 2 * w) + n - 1) >> 1; }
 __device__ __forceinline__ int wrapr(int x) { return x >= kMRh ? x - kMRh : x; }
 __device__ __forceinline__ void cp8p(uint32_t saddr, const void* gmem, bool pred) {
   asm volatile(
@@ -620,7 +626,7 @@ struct BState {
   float O;
 };
 
-// Blocks of one pass: s0 = -kBlk - kLag*w + kBlk*(blk + off); consumption of
+// Blocks of one pass: s0 = -kMBlk - kMLag*w + kMBlk*(blk + off); consumption of
 // row s-l by lane l at step s, exactly like nw_forward.
 template <int kPh>
 __device__ __forceinline__ void mitm_fwd(const float* __restrict__ th, int n, int m, int NW, const MShared& sh, int RF, int off,
@@ -646,13 +652,13 @@ __device__ __forceinline__ void mitm_fwd(const float* __restrict__ th, int n, in
   float2* bnd_out = sh.bndF + (w + 1) * kRB;
   const bool pub = (l == 31) & (w + 1 < NW);
   const bool zok = zfrac != ninf();
-  const int s_lo = max(lo, 1) + 32, s_hi = min(hi, n - 1) - (kBlk - 1) - kMP;
+  const int s_lo = max(lo, 1) + 32, s_hi = min(hi, n - 1) - (kMBlk - 1) - kMP;
   bool bad = false;
   VO cur = st.cur, lprev = st.lprev;
   float av = st.av, O = st.O;
   for (int blk = 0; blk < nblk; ++blk) {
-    const int s0 = -kBlk - w * kLag + (blk + off) * kBlk;
-    if ((s0 + kBlk - 1 + kMP < max(lo, 0)) | (s0 > hi + 32 + (kPh == 2 ? 1 : 0))) {
+    const int s0 = -kMBlk - w * kMLag + (blk + off) * kMBlk;
+    if ((s0 + kMBlk - 1 + kMP < max(lo, 0)) | (s0 > hi + 32 + (kPh == 2 ? 1 : 0))) {
       bar_dir(1, 32 * NW);
       continue;
     }
@@ -693,7 +699,7 @@ __device__ __forceinline__ void mitm_fwd(const float* __restrict__ th, int n, in
         if (kPh == 2) {
           const int sp = s + kMP;
           const bool bv = kIn ? true : ((sp >= 0) & (sp < steps));
-          cp8p(slab_u + (uint32_t)((k + kMP) & (kMS - 1)) * 256u, wsb_b + 32 * k, bv);
+          cp8p(slab_u + (uint32_t)((s + kMP) & (kMS - 1)) * 256u, wsb_b + 32 * k, bv);
         }
         cp_commit();
       }
@@ -721,7 +727,7 @@ __device__ __forceinline__ void mitm_fwd(const float* __restrict__ th, int n, in
         const L3 r = lse3r(t0, t1, t2);
         const bool origin = kIn ? false : ((i == 0) & (j == 0));
         if (kPh == 2) {
-          const float2 bt = slab_w[((k)&(kMS - 1)) * 32 + l];
+          const float2 bt = slab_w[(s & (kMS - 1)) * 32 + l];
           const float e = ex2((r.Mc + bt.x) + ((O + bt.y - zint) - zfrac));
           const float F = (zok & act) ? e : 0.f;
           slot[0] = r.e0 * F;
@@ -747,13 +753,13 @@ __device__ __forceinline__ void mitm_fwd(const float* __restrict__ th, int n, in
     };
     if ((s0 >= s_lo) & (s0 <= s_hi)) {
 #pragma unroll
-      for (int k = 0; k < kBlk; ++k) step(IntC<1>{}, k);
-    } else if ((s0 >= 32) & (s0 + kBlk - 1 + kMP <= n - 1)) {
+      for (int k = 0; k < kMBlk; ++k) step(IntC<1>{}, k);
+    } else if ((s0 >= 32) & (s0 + kMBlk - 1 + kMP <= n - 1)) {
 #pragma unroll 1
-      for (int k = 0; k < kBlk; ++k) step(IntC<2>{}, k);
+      for (int k = 0; k < kMBlk; ++k) step(IntC<2>{}, k);
     } else {
 #pragma unroll 1
-      for (int k = 0; k < kBlk; ++k) step(IntC<0>{}, k);
+      for (int k = 0; k < kMBlk; ++k) step(IntC<0>{}, k);
     }
     bar_dir(1, 32 * NW);
   }
@@ -805,13 +811,13 @@ __device__ __forceinline__ void mitm_bwd(const float* __restrict__ th, int n, in
   float2* bnd1_out = sh.bndB1 + (wb + 1) * kRB;
   const bool pub = (l == 31) & (wb + 1 < NW);
   const bool zok = zfrac != ninf();
-  const int s_lo = max(lo, 1) + 32, s_hi = min(hi, n - 1) - (kBlk - 1) - kMP;
+  const int s_lo = max(lo, 1) + 32, s_hi = min(hi, n - 1) - (kMBlk - 1) - kMP;
   VO pDn = st.pDn, pR = st.pR, pD = st.pD, savedD = st.savedD;
   float O = st.O;
   float2 c1 = make_float2(ninf(), 0.f), c2 = make_float2(ninf(), 0.f);  // phase 2 alpha carries
   for (int blk = 0; blk < nblk; ++blk) {
-    const int s0 = -kBlk - wb * kLag + (blk + off) * kBlk;
-    if ((s0 + kBlk - 1 + kMP < max(lo, 0)) | (s0 > hi + 32 + (kPh == 2 ? 1 : 0))) {
+    const int s0 = -kMBlk - wb * kMLag + (blk + off) * kMBlk;
+    if ((s0 + kMBlk - 1 + kMP < max(lo, 0)) | (s0 > hi + 32 + (kPh == 2 ? 1 : 0))) {
       bar_dir(2, 32 * NW);
       continue;
     }
@@ -954,13 +960,13 @@ __device__ __forceinline__ void mitm_bwd(const float* __restrict__ th, int n, in
     };
     if ((s0 >= s_lo) & (s0 <= s_hi)) {
 #pragma unroll
-      for (int k = 0; k < kBlk; ++k) step(IntC<1>{}, k);
-    } else if ((s0 >= 32) & (s0 + kBlk - 1 + kMP <= n - 1)) {
+      for (int k = 0; k < kMBlk; ++k) step(IntC<1>{}, k);
+    } else if ((s0 >= 32) & (s0 + kMBlk - 1 + kMP <= n - 1)) {
 #pragma unroll 1
-      for (int k = 0; k < kBlk; ++k) step(IntC<2>{}, k);
+      for (int k = 0; k < kMBlk; ++k) step(IntC<2>{}, k);
     } else {
 #pragma unroll 1
-      for (int k = 0; k < kBlk; ++k) step(IntC<0>{}, k);
+      for (int k = 0; k < kMBlk; ++k) step(IntC<0>{}, k);
     }
     bar_dir(2, 32 * NW);
   }
@@ -1168,10 +1174,10 @@ __global__ void __launch_bounds__(kMaxT) nw_mitm_kernel(const float* __restrict_
   int G1 = 0, off2 = 1 << 30, G2 = 0;
   for (int x = 0; x < NW; ++x) {
     const int RF = mitm_rf(x, n, NW), QB = n - mitm_rf(NW - 1 - x, n, NW) - 1;
-    G1 = max(G1, max((RF + 31 + kBlk + kLag * x) / kBlk, (QB + 31 + kBlk + kLag * x) / kBlk) + 1);
-    off2 = min(off2, min((RF + 1 + kLag * x) / kBlk, (QB + 1 + kLag * x) / kBlk));
+    G1 = max(G1, max((RF + 31 + kMBlk + kMLag * x) / kMBlk, (QB + 31 + kMBlk + kMLag * x) / kMBlk) + 1);
+    off2 = min(off2, min((RF + 1 + kMLag * x) / kMBlk, (QB + 1 + kMLag * x) / kMBlk));
   }
-  for (int x = 0; x < NW; ++x) G2 = max(G2, (n + 33 + kBlk + kLag * x) / kBlk - off2 + 1);
+  for (int x = 0; x < NW; ++x) G2 = max(G2, (n + 33 + kMBlk + kMLag * x) / kMBlk - off2 + 1);
   FState fs{{ninf(), 0.f}, {ninf(), 0.f}, ninf(), 0.f};
   BState bs{{ninf(), 0.f}, {ninf(), 0.f}, {ninf(), 0.f}, {ninf(), 0.f}, 0.f};
   bar_all();
@@ -1208,7 +1214,7 @@ int mitm_nw(int m) { return (m & 31) == 0 ? m / 32 : (m + 1 + 31) / 32; }
 
 int mitm_ok(int n, int m) {
   const int NW = mitm_nw(m);
-  return NW <= 10 && n >= 40 * (NW - 1) + 32 && mitm_smem_bytes(NW) <= 220 * 1024;
+  return NW <= 10 && n >= kMLag * (NW - 1) + 32 && mitm_smem_bytes(NW) <= 220 * 1024;
 }
 
 struct NwWs {
