@@ -12,14 +12,15 @@
 // state gathers its emission theta[t][lab(s)] from shared memory.
 //   ctc_kernel<0/2>: alpha (log-sum-exp) or the max-plus alpha with
 //            first-maximum back pointers and the walk (logZ, argmax).
-//   ctc_dir_kernel (marginals, grid B x 2): the forward CTA stores alpha, the
-//            backward CTA beta, both as fp32 offsets from per-(frame, warp)
-//            bases, concurrently; the forward owns Z, the status and the label
-//            CSR.
+//   ctc_dir_kernel (marginals, grid B x 2): a thread per (blank, label) state
+//            pair; the forward CTA stores alpha, the backward CTA beta, both as
+//            fp32 offsets from per-(frame, warp) bases, concurrently; the
+//            forward owns Z, the status and the label CSR.
 //   ctc_marg_kernel: posteriors exp(alpha + beta - Z) reduced by label in a
 //            fixed order (blank: lane-strided sums + butterfly; labels: the CSR
 //            state list in increasing s), a warp per frame, streaming.
-// Log values are fp64 on the recursion; exp/log fp32 MUFU on differences.
+// Log values: fp64 in ctc_kernel (logZ, exact max-plus argmax); fp32 (value,
+// integer offset) pairs in log2 units in ctc_dir_kernel, MUFU exp2/log2.
 #include "common.cuh"
 
 namespace {
@@ -168,15 +169,67 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
 // log_partition + marginals as TWO independent CTAs per instance (grid B x 2):
 // blockIdx.y = 0 runs the forward (alpha) over frames 0..T-1 and owns Z, the
 // status and the label CSR; blockIdx.y = 1 runs the backward (beta) over
-// T-1..0.  Both store their vectors as fp32 offsets from a per-(frame, warp)
-// fp64 base; ctc_marg_kernel forms exp(alpha + beta - Z).  Twice the CTAs of
-// one fwd-then-bwd CTA per instance, and each runs half the frames: the
-// per-frame latency chains of the two directions overlap across the SM
-// instead of running back to back.
-size_t ctc_dir_smem_bytes(int S, int V, int L) {
-  return (size_t)3 * (S + 2) * 8 + (size_t)kP * V * 4 + (size_t)S * 4 + (size_t)(L + 1) * 4 + (size_t)(V + 1) * 4 +
-         128;
+// T-1..0, concurrently.  The recursion is fp32 in log2 units carried as
+// (v, O): value = v + O with O an integer-valued float re-chosen every frame
+// (the alignment kernel's representation).  A state combines its three
+// predecessors in the frame of the largest offset (exact integer
+// differences), so no fp64 and no f32<->f64 conversion is on the per-frame
+// chain; offsets stay exact while |value| < 2^24 (|log Z| < 1.1e7).  Dead
+// (-inf) states carry O = kNoO, which is never the largest live offset.  Both
+// directions store their vectors as fp32 offsets from the per-(frame, warp)
+// maximum O; ctc_marg_kernel forms exp2(alpha + beta - Z).
+constexpr float kNoO = -1.0e30f;
+
+__device__ __forceinline__ float2 vo_dead() { return make_float2(ninf(), kNoO); }
+
+// log2-sum-exp2 of two / three (v, O) terms plus e (log2 units), renormalised to
+// |v| <= 1/2.  Branch-free on dead terms: a dead result has v = -inf and an
+// offset <= kNoO (r, r2 clamp to kNoO, so offsets stay finite for any practical
+// T), which is never the largest offset of a term with a live one.
+__device__ __forceinline__ float2 vo_fin(float oref, float r, float v) {
+  const float r2 = rintf(fmaxf(v, kNoO));
+  return make_float2(v - r2, (oref + r) + r2);
 }
+__device__ __forceinline__ float2 vo_lse2(float2 x0, float2 x1, float e) {
+  const float oref = fmaxf(x0.y, x1.y);
+  const float t0 = x0.x + (x0.y - oref), t1 = x1.x + (x1.y - oref);
+  const float r = rintf(fmaxf(fmaxf(t0, t1), kNoO));
+  return vo_fin(oref, r, lg2(ex2(t0 - r) + ex2(t1 - r)) + e);
+}
+__device__ __forceinline__ float2 vo_lse3(float2 x0, float2 x1, float2 x2, float e) {
+  const float oref = fmaxf(fmaxf(x0.y, x1.y), x2.y);
+  const float t0 = x0.x + (x0.y - oref), t1 = x1.x + (x1.y - oref), t2 = x2.x + (x2.y - oref);
+  const float r = rintf(fmaxf(fmaxf(fmaxf(t0, t1), t2), kNoO));
+  return vo_fin(oref, r, lg2(ex2(t0 - r) + ex2(t1 - r) + ex2(t2 - r)) + e);
+}
+// (v, O) + e, renormalised
+__device__ __forceinline__ float2 vo_add(float2 x, float e) { return vo_fin(x.y, 0.f, x.x + e); }
+
+// Warp maximum of integer-valued offsets: clamped to >= -2^22 and shifted by
+// 1.5 * 2^23, every offset is a positive float whose bit pattern orders like its
+// value, so one unsigned REDUX finds the maximum.  Live offsets are exact above
+// -2^22 (|log Z| < 2.9e6); dead ones clamp to the floor.
+__device__ __forceinline__ float warp_max_off(float o) {
+  constexpr float kMagic = 12582912.f;
+  const uint32_t k = __float_as_uint(fmaxf(o, -4194304.f) + kMagic);
+  return __uint_as_float(__reduce_max_sync(0xffffffffu, k)) - kMagic;
+}
+
+// Thread i owns the state pair (2i, 2i+1) -- blank 2i, label i -- for
+// i = 0..L-1, and thread L-1 also owns the final blank 2L (L = 0: thread 0
+// owns state 0), so S = 2L+1 <= 1024 takes L <= 512 threads.  A thread's
+// previous values stay in registers; the one neighbour term crosses through
+// shared memory: forward, alpha(2i-1) from thread i-1 (a blank has
+// predecessors {2i, 2i-1}, a label {2i+1, 2i, 2i-1 if skip}); backward, c(2i+2),
+// c(2i+3) from thread i+1 (a blank has successors {2i, 2i+1}, a label {2i+1,
+// 2i+2, 2i+3 if skip}; the final blank only itself).  Workspace rows have the
+// even pitch Sp = 2L+2 (one 8-byte store per pair), bases per 64-state warp.
+size_t ctc_dir_smem_bytes(int S, int V, int L) {
+  (void)S;
+  return (size_t)3 * (L + 3) * 16 + (size_t)kP * V * 4 + (size_t)(2 * L + 1) * 4 + (size_t)(L + 1) * 4 +
+         (size_t)(V + 1) * 4 + 128;
+}
+int ctc_dir_threads(int L) { return ((max(L, 1) + 31) / 32) * 32; }
 
 __global__ void ctc_dir_kernel(const float* __restrict__ fp_all, const int32_t* __restrict__ tg_all, int T, int V,
                                int L, float* __restrict__ wsa_all, float* __restrict__ wsabase_all,
@@ -184,35 +237,45 @@ __global__ void ctc_dir_kernel(const float* __restrict__ fp_all, const int32_t* 
                                int32_t* __restrict__ csr_all, double* __restrict__ logz,
                                int32_t* __restrict__ status) {
   extern __shared__ __align__(16) char smraw[];
-  const int S = 2 * L + 1;
-  double *a0, *a1, *a2;  // three vector buffers: one barrier per frame
+  const int S = 2 * L + 1, Sp = 2 * L + 2;
+  float4 *q0, *q1, *q2;  // three pair buffers [L+3] (one dead pad each side): one barrier per frame
   float* rows;
   int *lab, *lst, *off;
   {
     char* p = smraw;
-    a0 = (double*)p; p += (size_t)(S + 2) * 8;
-    a1 = (double*)p; p += (size_t)(S + 2) * 8;
-    a2 = (double*)p; p += (size_t)(S + 2) * 8;
+    q0 = (float4*)p; p += (size_t)(L + 3) * 16;
+    q1 = (float4*)p; p += (size_t)(L + 3) * 16;
+    q2 = (float4*)p; p += (size_t)(L + 3) * 16;
     rows = (float*)p; p += (size_t)kP * V * 4;
     lab = (int*)p; p += (size_t)S * 4;
     lst = (int*)p; p += (size_t)(L + 1) * 4;
     off = (int*)p;
   }
   __shared__ int badsh;
-  const int b = blockIdx.x, dir = blockIdx.y, tid = threadIdx.x, s = tid, lane = tid & 31, wq = tid >> 5;
-  const bool act = s < S;
+  const int b = blockIdx.x, dir = blockIdx.y, tid = threadIdx.x, i = tid, lane = tid & 31, wq = tid >> 5;
+  const bool act = i < max(L, 1), has1 = i < L, ext = (L >= 1) && (i == L - 1);
+  const int ia = act ? i : 0;  // shared-memory neighbour reads of idle lanes stay in bounds
   const float* fp = fp_all + (size_t)b * T * V;
   const int32_t* tg = tg_all + (size_t)b * L;
-  if (tid == 0) badsh = 0;
-  __syncthreads();
-  int mylab = 0;
-  if (act) {
-    mylab = (s & 1) ? tg[s >> 1] : 0;
-    if ((s & 1) && (mylab < 1 || mylab >= V)) {
+  const float4 dead4 = make_float4(ninf(), kNoO, ninf(), kNoO);
+  if (tid == 0) {
+    badsh = 0;
+    q0[0] = q1[0] = q2[0] = dead4;
+    q0[L + 1] = q1[L + 1] = q2[L + 1] = dead4;
+    q0[L + 2] = q1[L + 2] = q2[L + 2] = dead4;
+  }
+  int mylab = 0;  // label of state 2i+1
+  if (has1) {
+    mylab = tg[i];
+    if (mylab < 1 || mylab >= V) {
       atomicOr(&badsh, 1);
       mylab = 0;
     }
-    lab[s] = mylab;
+  }
+  if (act) {
+    lab[2 * i] = 0;
+    if (has1) lab[2 * i + 1] = mylab;
+    if (ext) lab[2 * L] = 0;
   }
   __syncthreads();
   if (dir == 0) {  // label CSR for ctc_marg_kernel: odd states by label, increasing s
@@ -232,45 +295,51 @@ __global__ void ctc_dir_kernel(const float* __restrict__ fp_all, const int32_t* 
     for (int e = tid; e <= V; e += blockDim.x) csr[e] = off[e];
     for (int e = tid; e < L; e += blockDim.x) csr[V + 1 + e] = lst[e];
   }
-  // vectors as fp32 offsets from a per-warp base (one REDUX max per frame, no CTA reduction).
-  // The base is the warp maximum truncated to its high word (20 mantissa bits), found by a REDUX
-  // on the high words' order-preserving keys: a double that is exactly an fp32 value, so it is
-  // stored as one, and one f64->f32 conversion per state (the offset) is all the store costs.
-  auto store = [&](float* ws, float* wsbase, int t, double v) {
-    const double bm = warp_max_hi(v);
-    const double base = (bm == ninfd()) ? 0.0 : bm;
-    if (act) ws[(size_t)t * S + s] = (v == ninfd()) ? ninf() : (float)(v - base);
-    if (lane == 0) wsbase[(size_t)t * 32 + wq] = (float)base;
+  // a frame's states -> workspace: v + (O - base), base = the warp's largest offset (dead
+  // states store -inf)
+  auto store = [&](float* wrow, float* brow, float2 x0, float2 x1, float2 x2) {
+    const float base = warp_max_off(act ? fmaxf(fmaxf(x0.y, x1.y), x2.y) : kNoO);
+    if (act) *reinterpret_cast<float2*>(wrow + 2 * i) = make_float2(x0.x + (x0.y - base), x1.x + (x1.y - base));
+    if (lane == 0) brow[wq] = base;
+    if (ext) {
+      wrow[2 * L] = x2.x + (x2.y - base);
+      brow[L >> 5] = base;  // state 2L's 64-state group: this warp's, or (L % 32 == 0) an unused slot
+    }
   };
-  if (tid < 2) { a0[tid] = ninfd(); a1[tid] = ninfd(); a2[tid] = ninfd(); }
-  // Frames advance with ONE barrier each: the vector written at frame t goes to the buffer
+  // Frames advance with ONE barrier each: the pair written at frame t goes to the buffer
   // last read at frame t-2 (every thread is past frame t-1 once it passes frame t's barrier),
   // and the row slot refilled after frame t's barrier is the one frame t-1 (forward) / t+1
   // (backward) consumed.
   if (dir == 1) {
     // ======================= backward (alignment.py:272-287)
-    float* wsb = wsb_all + (size_t)b * T * S;
-    float* wsbase = wsbase_all + (size_t)b * T * 32;
-    double* cur = a0 + 2;  // beta[t+1][*] + theta[t+1][lab(*)]
-    double* nxt = a1 + 2;
-    double* spare = a2 + 2;
+    float* wrow = wsb_all + (size_t)b * T * Sp + (size_t)(T - 1) * Sp;
+    float* brow = wsbase_all + (size_t)b * T * 32 + (size_t)(T - 1) * 32;
+    float4* cur = q0 + 1;  // c = beta[t+1] + theta[t+1][lab], per pair
+    float4* nxt = q1 + 1;
+    float4* spare = q2 + 1;
     for (int k = 0; k < kP; ++k) {
       const int t = T - 1 - k;
       if (t >= 0) load_row(fp, t, V, rows + (size_t)(t % kP) * V);
       cp_commit();
     }
-    // the ring holds beta[t+1][s] + theta[t+1][lab(s)] (the successor term every predecessor of
-    // s reads), so a state converts and adds ONE emission per frame instead of three
     cp_wait<kP - 1>();
     __syncthreads();  // row T-1 landed
-    if (act) {
-      const double b0 = (s == S - 1 || s == S - 2) ? 0.0 : ninfd();
-      cur[s] = b0 + (double)rows[(size_t)((T - 1) % kP) * V + mylab];
+    // beta[T-1] = 0 on the final states 2L and 2L-1 (both thread L-1's; L = 0: thread 0's state 0)
+    const bool f0 = (L == 0) && (i == 0);
+    const float2 zero = make_float2(0.f, 0.f);
+    float2 c0 = vo_dead(), c1 = vo_dead(), c2 = vo_dead();
+    {
+      const float* E = rows + (size_t)((T - 1) % kP) * V;
+      if (f0) c0 = vo_add(zero, E[0] * SDB_LOG2E);
+      if (ext) {
+        c1 = vo_add(zero, E[mylab] * SDB_LOG2E);
+        c2 = vo_add(zero, E[0] * SDB_LOG2E);
+      }
+      if (act) cur[i] = make_float4(c0.x, c0.y, c1.x, c1.y);
     }
-    store(wsb, wsbase, T - 1, (act && (s == S - 1 || s == S - 2)) ? 0.0 : ninfd());
-    const bool has1 = act && (s + 1 < S);
-    const int lab2 = (act && s + 2 < S) ? lab[s + 2] : 0;
-    const bool sk2 = act && (s + 2 < S) && lab2 != 0 && lab2 != mylab;
+    store(wrow, brow, f0 ? zero : vo_dead(), ext ? zero : vo_dead(), ext ? zero : vo_dead());
+    const int lab3 = (i + 1 < L) ? tg[i + 1] : 0;  // label of state 2i+3
+    const bool sk = (i + 1 < L) && lab3 != mylab;
     for (int t = T - 2; t >= 0; --t) {
       cp_wait<kP - 2>();
       __syncthreads();  // rows t+1 (consumed into cur) and t landed; cur complete
@@ -279,37 +348,39 @@ __global__ void ctc_dir_kernel(const float* __restrict__ fp_all, const int32_t* 
         if (tn >= 0) load_row(fp, tn, V, rows + (size_t)(tn % kP) * V);
         cp_commit();
       }
+      wrow -= Sp;
+      brow -= 32;
       const float* E = rows + (size_t)(t % kP) * V;
-      double v = ninfd();
-      if (act) {
-        const double x0 = cur[s];
-        const double x1 = has1 ? cur[s + 1] : ninfd();
-        const double x2 = sk2 ? cur[s + 2] : ninfd();
-        const double M = fmax(fmax(x0, x1), x2);
-        if (M != ninfd()) {
-          const float e = fexp((float)(x0 - M)) + fexp((float)(x1 - M)) + fexp((float)(x2 - M));
-          v = M + (double)flog(e);
-        }
-        nxt[s] = v + (double)E[mylab];
-      }
-      store(wsb, wsbase, t, v);
-      double* tmp = cur; cur = nxt; nxt = spare; spare = tmp;
+      const float eb = E[0] * SDB_LOG2E, el = E[mylab] * SDB_LOG2E;
+      const float4 rn = cur[ia + 1];  // c(2i+2), c(2i+3) (dead pad past the end)
+      const float2 s2 = ext ? c2 : make_float2(rn.x, rn.y);
+      const float2 b0 = vo_lse2(c0, c1, 0.f);
+      const float2 b1 = vo_lse3(c1, s2, sk ? make_float2(rn.z, rn.w) : vo_dead(), 0.f);
+      const float2 b2 = c2;  // the final blank's only successor is itself
+      c0 = vo_add(b0, eb);
+      c1 = vo_add(b1, el);
+      c2 = vo_add(b2, eb);
+      if (act) nxt[i] = make_float4(c0.x, c0.y, c1.x, c1.y);
+      store(wrow, brow, b0, b1, b2);
+      float4* tmp = cur; cur = nxt; nxt = spare; spare = tmp;
     }
     cp_wait<0>();
     return;
   }
   // ======================= forward (alignment.py:248-269)
-  float* wsa = wsa_all + (size_t)b * T * S;
-  float* wsabase = wsabase_all + (size_t)b * T * 32;
-  double* prv = a0 + 2;
-  double* now = a1 + 2;
-  double* spare = a2 + 2;
-  const bool skip = act && (s >= 2) && mylab != 0 && mylab != lab[s - 2];
+  float* wrow = wsa_all + (size_t)b * T * Sp;
+  float* brow = wsabase_all + (size_t)b * T * 32;
+  float4* prv = q0 + 1;
+  float4* now = q1 + 1;
+  float4* spare = q2 + 1;
+  const int labm = (i >= 1 && has1) ? tg[i - 1] : 0;  // label of state 2i-1
+  const bool skip = has1 && i >= 1 && labm != mylab;
   for (int k = 0; k < kP - 1; ++k) {
     if (k < T) load_row(fp, k, V, rows + (size_t)k * V);
     cp_commit();
   }
   int bad = 0;
+  float2 a0 = vo_dead(), a1 = vo_dead(), a2 = vo_dead();
   for (int t = 0; t < T; ++t) {
     cp_wait<kP - 2>();
     __syncthreads();  // row t landed; alpha[t-1] complete; row t-1 consumed
@@ -320,32 +391,39 @@ __global__ void ctc_dir_kernel(const float* __restrict__ fp_all, const int32_t* 
     }
     const float* E = rows + (size_t)(t % kP) * V;
     for (int v = tid; v < V; v += blockDim.x) bad |= bad_input(E[v]);
-    double a = ninfd();
-    if (act) {
-      const double e = (double)E[mylab];
-      if (t == 0) {
-        a = (s <= 1) ? e : ninfd();
-      } else {
-        const double x0 = prv[s], x1 = prv[s - 1], x2 = skip ? prv[s - 2] : ninfd();
-        const double M = fmax(fmax(x0, x1), x2);
-        if (M != ninfd()) {
-          const float sum = fexp((float)(x0 - M)) + fexp((float)(x1 - M)) + fexp((float)(x2 - M));
-          a = M + (double)flog(sum) + e;
-        }
-      }
-      now[s] = a;
+    const float eb = E[0] * SDB_LOG2E, el = E[mylab] * SDB_LOG2E;
+    if (t == 0) {
+      a0 = (i == 0) ? vo_add(make_float2(0.f, 0.f), eb) : vo_dead();
+      a1 = (i == 0 && has1) ? vo_add(make_float2(0.f, 0.f), el) : vo_dead();
+    } else {
+      const float4 lf = prv[ia - 1];  // alpha(2i-2), alpha(2i-1) (dead pad before 0)
+      const float2 am = make_float2(lf.z, lf.w);
+      const float2 n0 = vo_lse2(a0, am, eb);
+      const float2 n2 = vo_lse2(a2, a1, eb);  // the final blank 2L: {2L, 2L-1}
+      a1 = vo_lse3(a1, a0, skip ? am : vo_dead(), el);
+      a0 = n0;
+      a2 = ext ? n2 : vo_dead();
+      if (!has1) a1 = vo_dead();
     }
-    store(wsa, wsabase, t, a);
-    double* tmp = prv; prv = now; now = spare; spare = tmp;
+    if (act) now[i] = make_float4(a0.x, a0.y, a1.x, a1.y);
+    if (ext) now[L] = make_float4(a2.x, a2.y, ninf(), kNoO);
+    store(wrow, brow, a0, a1, a2);
+    wrow += Sp;
+    brow += 32;
+    float4* tmp = prv; prv = now; now = spare; spare = tmp;
   }
   cp_wait<0>();
   if (bad) atomicOr(&badsh, 1);
   __syncthreads();
-  if (tid == 0) {  // final states (alignment.py:263-264): [S-1] or [S-1, S-2]
-    const double f1 = prv[S - 1];
-    const double f2 = (S > 1) ? prv[S - 2] : ninfd();
-    const double M = fmax(f1, f2);
-    const double Z = (M == ninfd()) ? ninfd() : M + (double)flog(fexp((float)(f1 - M)) + fexp((float)(f2 - M)));
+  if (tid == 0) {  // final states (alignment.py:263-264): 2L and 2L-1
+    const float4 pl = (L >= 1) ? prv[L] : prv[0];
+    const float2 f1 = make_float2(pl.x, pl.y);
+    const float2 f2 = (L >= 1) ? make_float2(prv[L - 1].z, prv[L - 1].w) : vo_dead();
+    const double d1 = (f1.x == ninf()) ? ninfd() : (double)f1.x + (double)f1.y;
+    const double d2 = (f2.x == ninf()) ? ninfd() : (double)f2.x + (double)f2.y;
+    const double M = fmax(d1, d2);
+    const double Z2 = (M == ninfd()) ? ninfd() : M + log2(exp2(d1 - M) + exp2(d2 - M));
+    const double Z = Z2 * (double)SDB_LN2;
     status[b] = badsh ? SDB_ST_INVALID : (Z == ninfd() ? SDB_ST_VACUOUS : SDB_ST_OK);
     logz[b] = Z;
   }
@@ -387,20 +465,21 @@ __global__ void __launch_bounds__(kMargWarps * 32) ctc_marg_kernel(
   for (int e = tid; e < L; e += blockDim.x) lst[e] = csr[V + 1 + e];
   __syncthreads();
   float* prow = prow_all + (size_t)warp * S;
-  const float* pa = wsa_all + (size_t)b * T * S;
-  const float* pb = wsb_all + (size_t)b * T * S;
+  const int Sp = S + 1;  // ctc_dir_kernel's even row pitch
+  const float* pa = wsa_all + (size_t)b * T * Sp;
+  const float* pb = wsb_all + (size_t)b * T * Sp;
   const float* ba = wsabase_all + (size_t)b * T * 32;
   const float* bb = wsbase_all + (size_t)b * T * 32;
-  const double Z = logz[b];
+  const double Z2 = logz[b] * 1.4426950408889634;  // offsets and bases are log2 units
   // the warp's next frame (both offsets and the two bases of each 32-state group) is loaded into
   // registers while the current one is reduced; the posterior of state e = 32 u + lane is
-  // exp(alpha + beta - Z): bases and Z combined in fp64, the offsets added in fp32
-  // Lane g loads the two bases of 32-state group g (one coalesced load each) and forms that
+  // exp2(alpha + beta - Z): bases and Z combined in fp64, the offsets added in fp32
+  // Lane g loads the two bases of 64-state group g (one coalesced load each) and forms that
   // group's fp64 combination once; the state loop takes it by shuffle.
   float xa[kRowRegs], xb[kRowRegs], ca, cb;
   auto fetch = [&](int t) {
-    const float* sa = pa + (size_t)t * S;
-    const float* sb = pb + (size_t)t * S;
+    const float* sa = pa + (size_t)t * Sp;
+    const float* sb = pb + (size_t)t * Sp;
 #pragma unroll
     for (int u = 0; u < kRowRegs; ++u) {
       const int e = lane + 32 * u;
@@ -414,13 +493,13 @@ __global__ void __launch_bounds__(kMargWarps * 32) ctc_marg_kernel(
   };
   if (t0 + warp < t1) fetch(t0 + warp);
   for (int t = t0 + warp; t < t1; t += kMargWarps) {
-    const float cl = (float)((double)ca + (double)cb - Z);  // group `lane` (groups >= ceil(S/32) unused)
+    const float cl = (float)((double)ca + (double)cb - Z2);  // 64-state group `lane` (>= ceil(S/64) unused)
 #pragma unroll
     for (int u = 0; u < kRowRegs; ++u) {
       const int e = lane + 32 * u;
-      const float c = __shfl_sync(0xffffffffu, cl, u);
+      const float c = __shfl_sync(0xffffffffu, cl, u >> 1);
       if (e < S) {
-        prow[e] = fexp(c + xa[u] + xb[u]);  // an -inf offset gives ex2(-inf) = +0 (no +inf offsets)
+        prow[e] = ex2(c + xa[u] + xb[u]);  // an -inf offset gives ex2(-inf) = +0 (no +inf offsets)
       }
     }
     if (t + kMargWarps < t1) fetch(t + kMargWarps);
@@ -443,10 +522,10 @@ __global__ void __launch_bounds__(kMargWarps * 32) ctc_marg_kernel(
 }
 
 struct CtcWs {
-  float* wsa;      // [B][T][S] alpha offsets
-  float* wsabase;  // [B][T][32] per-warp alpha bases
-  float* wsb;      // [B][T][S] beta offsets
-  float* wsbase;   // [B][T][32] per-warp beta bases
+  float* wsa;      // [B][T][S+1] alpha offsets
+  float* wsabase;  // [B][T][32] per-warp (64-state) alpha bases
+  float* wsb;      // [B][T][S+1] beta offsets
+  float* wsbase;   // [B][T][32] per-warp (64-state) beta bases
   int32_t* csr;    // [B][V+1+L] label CSR (offsets, odd states by label)
   int8_t* back;
 };
@@ -456,9 +535,9 @@ CtcWs ctc_carve_ws(void* base, int64_t B, int T, int V, int L, int mode, size_t*
   Carve c(base);
   CtcWs w{};
   if (mode == 1) {
-    w.wsa = c.take<float>((size_t)B * T * S);
+    w.wsa = c.take<float>((size_t)B * T * (S + 1));
     w.wsabase = c.take<float>((size_t)B * T * 32);
-    w.wsb = c.take<float>((size_t)B * T * S);
+    w.wsb = c.take<float>((size_t)B * T * (S + 1));
     w.wsbase = c.take<float>((size_t)B * T * 32);
     w.csr = c.take<int32_t>((size_t)B * (V + 1 + L));
   }
@@ -497,7 +576,7 @@ int ctc_launch(const float* fp, const int32_t* tg, int64_t B, int T, int V, int 
     if (dsmem > 48 * 1024 &&
         sdb_set_smem((const void*)ctc_dir_kernel, dsmem) != cudaSuccess)
       return SDB_ERR_CUDA;
-    ctc_dir_kernel<<<dim3((unsigned)B, 2), threads, dsmem, s>>>(fp, tg, T, V, L, ws.wsa, ws.wsabase, ws.wsb,
+    ctc_dir_kernel<<<dim3((unsigned)B, 2), ctc_dir_threads(L), dsmem, s>>>(fp, tg, T, V, L, ws.wsa, ws.wsabase, ws.wsb,
                                                                 ws.wsbase, ws.csr, logz, status);
   } else {
     const size_t smem = ctc_smem_bytes(S, V, L);
