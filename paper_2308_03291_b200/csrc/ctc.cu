@@ -6,14 +6,14 @@
 // _ctc_walk).  Layout per instance: frame_potentials [T][V] fp32,
 // targets [L] int32 (labels in 1..V-1), blank = 0.
 //
-// Schedule: one CTA per (instance, direction), one thread per lattice state s
-// (S = 2L+1 <= 1024), frames in lockstep (one __syncthreads per frame).  Frame
-// rows are prefetched kP frames ahead into a shared ring with cp.async and each
-// state gathers its emission theta[t][lab(s)] from shared memory.
-//   ctc_kernel<0/2>: alpha (log-sum-exp) or the max-plus alpha with
-//            first-maximum back pointers and the walk (logZ, argmax).
-//   ctc_dir_kernel (marginals, grid B x 2): a thread per (blank, label) state
-//            pair; the forward CTA stores alpha, the backward CTA beta, both as
+// Schedule: one CTA per (instance, direction), frames in lockstep (one
+// __syncthreads per frame).  Frame rows are prefetched kP frames ahead into a
+// shared ring with cp.async and each state gathers its emission
+// theta[t][lab(s)] from shared memory.
+//   ctc_kernel<2>: fp64 max-plus alpha, a thread per state (S = 2L+1 <= 1024),
+//            first-maximum back pointers and the walk (argmax).
+//   ctc_dir_kernel<kMarg> (log Z: grid B x 1; marginals: grid B x 2): a thread
+//            per (blank, label) state pair; the forward CTA stores alpha, the backward CTA beta, both as
 //            fp32 offsets from per-(frame, warp) bases, concurrently; the
 //            forward owns Z, the status and the label CSR.
 //   ctc_marg_kernel: posteriors exp(alpha + beta - Z) reduced by label in a
@@ -61,11 +61,11 @@ __device__ __forceinline__ void load_row(const float* __restrict__ fp, int t, in
   for (int v = threadIdx.x; v < V; v += blockDim.x) cp_async4(dst + v, fp + (size_t)t * V + v);
 }
 
-template <int kMode>  // 0 logZ only, 2 max-plus path (marginals: ctc_dir_kernel)
+template <int kMode>  // 2: max-plus path (log Z and marginals: ctc_dir_kernel)
 __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __restrict__ tg_all, int T, int V,
-                           int L, int8_t* __restrict__ back_all, double* __restrict__ logz,
+                           int L, int8_t* __restrict__ back_all, double* __restrict__ /*logz*/,
                            int32_t* __restrict__ path_all, double* __restrict__ score, int32_t* __restrict__ status) {
-  static_assert(kMode == 0 || kMode == 2, "ctc_kernel modes");
+  static_assert(kMode == 2, "ctc_kernel modes");
   extern __shared__ __align__(16) char smraw[];
   const int S = 2 * L + 1;
   CtcSmem sm = ctc_carve(smraw, S, V, L);
@@ -96,7 +96,7 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
     if (k < T) load_row(fp, k, V, sm.rows + (size_t)k * V);
     cp_commit();
   }
-  int8_t* back = (kMode == 2) ? back_all + (size_t)b * T * S : nullptr;
+  int8_t* back = back_all + (size_t)b * T * S;
   int bad = 0;
   for (int t = 0; t < T; ++t) {
     cp_wait<kP - 1>();
@@ -108,7 +108,7 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
       const double e = (double)E[mylab];
       if (t == 0) {
         a = (s <= 1) ? e : ninfd();
-      } else if (kMode == 2) {
+      } else {
         // first maximum in predecessor order [s, s-1, s-2] (alignment.py:239-245, 304-318)
         double best = prv[s];
         int k = 0;
@@ -116,13 +116,6 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
         if (skip && prv[s - 2] > best) { best = prv[s - 2]; k = 2; }
         a = best + e;
         back[(size_t)t * S + s] = (int8_t)k;
-      } else {
-        const double x0 = prv[s], x1 = prv[s - 1], x2 = skip ? prv[s - 2] : ninfd();
-        const double M = fmax(fmax(x0, x1), x2);
-        if (M != ninfd()) {
-          const float sum = fexp((float)(x0 - M)) + fexp((float)(x1 - M)) + fexp((float)(x2 - M));
-          a = M + (double)flog(sum) + e;
-        }
       }
       now[s] = a;
     }
@@ -141,27 +134,17 @@ __global__ void ctc_kernel(const float* __restrict__ fp_all, const int32_t* __re
   if (tid == 0) {
     const double f1 = prv[S - 1];
     const double f2 = (S > 1) ? prv[S - 2] : ninfd();
-    double res;
+    double res = f1;
     int fin = S - 1;
-    if (kMode == 2) {
-      res = f1;
-      if (S > 1 && f2 > f1) { res = f2; fin = S - 2; }
-    } else {
-      const double M = fmax(f1, f2);
-      res = (M == ninfd()) ? ninfd() : M + (double)flog(fexp((float)(f1 - M)) + fexp((float)(f2 - M)));
-    }
+    if (S > 1 && f2 > f1) { res = f2; fin = S - 2; }
     const int st = badsh ? SDB_ST_INVALID : (res == ninfd() ? SDB_ST_VACUOUS : SDB_ST_OK);
     status[b] = st;
-    if (kMode == 2) {
-      score[b] = res;
-      int32_t* path = path_all + (size_t)b * T;
-      int cs = fin;
-      for (int t = T - 1; t >= 0; --t) {
-        path[t] = (st == SDB_ST_OK) ? sm.lab[cs] : 0;
-        if (t > 0 && st == SDB_ST_OK) cs -= back[(size_t)t * S + cs];
-      }
-    } else {
-      logz[b] = res;
+    score[b] = res;
+    int32_t* path = path_all + (size_t)b * T;
+    int cs = fin;
+    for (int t = T - 1; t >= 0; --t) {
+      path[t] = (st == SDB_ST_OK) ? sm.lab[cs] : 0;
+      if (t > 0 && st == SDB_ST_OK) cs -= back[(size_t)t * S + cs];
     }
   }
 }
@@ -231,6 +214,8 @@ size_t ctc_dir_smem_bytes(int S, int V, int L) {
 }
 int ctc_dir_threads(int L) { return ((max(L, 1) + 31) / 32) * 32; }
 
+// kMarg = false: the forward CTA alone (grid B x 1), no workspace -- the log-partition path
+template <bool kMarg>
 __global__ void ctc_dir_kernel(const float* __restrict__ fp_all, const int32_t* __restrict__ tg_all, int T, int V,
                                int L, float* __restrict__ wsa_all, float* __restrict__ wsabase_all,
                                float* __restrict__ wsb_all, float* __restrict__ wsbase_all,
@@ -278,7 +263,7 @@ __global__ void ctc_dir_kernel(const float* __restrict__ fp_all, const int32_t* 
     if (ext) lab[2 * L] = 0;
   }
   __syncthreads();
-  if (dir == 0) {  // label CSR for ctc_marg_kernel: odd states by label, increasing s
+  if (kMarg && dir == 0) {  // label CSR for ctc_marg_kernel: odd states by label, increasing s
     if (tid == 0) {
       for (int v = 0; v <= V; ++v) off[v] = 0;
       for (int k = 0; k < L; ++k) off[lab[2 * k + 1] + 1]++;
@@ -298,6 +283,7 @@ __global__ void ctc_dir_kernel(const float* __restrict__ fp_all, const int32_t* 
   // a frame's states -> workspace: v + (O - base), base = the warp's largest offset (dead
   // states store -inf)
   auto store = [&](float* wrow, float* brow, float2 x0, float2 x1, float2 x2) {
+    if constexpr (!kMarg) return;
     const float base = warp_max_off(act ? fmaxf(fmaxf(x0.y, x1.y), x2.y) : kNoO);
     if (act) *reinterpret_cast<float2*>(wrow + 2 * i) = make_float2(x0.x + (x0.y - base), x1.x + (x1.y - base));
     if (lane == 0) brow[wq] = base;
@@ -310,7 +296,7 @@ __global__ void ctc_dir_kernel(const float* __restrict__ fp_all, const int32_t* 
   // last read at frame t-2 (every thread is past frame t-1 once it passes frame t's barrier),
   // and the row slot refilled after frame t's barrier is the one frame t-1 (forward) / t+1
   // (backward) consumed.
-  if (dir == 1) {
+  if (kMarg && dir == 1) {
     // ======================= backward (alignment.py:272-287)
     float* wrow = wsb_all + (size_t)b * T * Sp + (size_t)(T - 1) * Sp;
     float* brow = wsbase_all + (size_t)b * T * 32 + (size_t)(T - 1) * 32;
@@ -571,12 +557,18 @@ int ctc_launch(const float* fp, const int32_t* tg, int64_t B, int T, int V, int 
                float* marg, int32_t* path, double* score, int32_t* status, cudaStream_t s) {
   const int S = 2 * L + 1;
   const int threads = ((S + 31) / 32) * 32;
-  if constexpr (kMode == 1) {
+  if constexpr (kMode == 0) {  // log Z: the forward direction of the marginal kernel
+    const size_t dsmem = ctc_dir_smem_bytes(S, V, L);
+    if (dsmem > 48 * 1024 && sdb_set_smem((const void*)ctc_dir_kernel<false>, dsmem) != cudaSuccess)
+      return SDB_ERR_CUDA;
+    ctc_dir_kernel<false><<<dim3((unsigned)B, 1), ctc_dir_threads(L), dsmem, s>>>(
+        fp, tg, T, V, L, nullptr, nullptr, nullptr, nullptr, nullptr, logz, status);
+  } else if constexpr (kMode == 1) {
     const size_t dsmem = ctc_dir_smem_bytes(S, V, L);
     if (dsmem > 48 * 1024 &&
-        sdb_set_smem((const void*)ctc_dir_kernel, dsmem) != cudaSuccess)
+        sdb_set_smem((const void*)ctc_dir_kernel<true>, dsmem) != cudaSuccess)
       return SDB_ERR_CUDA;
-    ctc_dir_kernel<<<dim3((unsigned)B, 2), ctc_dir_threads(L), dsmem, s>>>(fp, tg, T, V, L, ws.wsa, ws.wsabase, ws.wsb,
+    ctc_dir_kernel<true><<<dim3((unsigned)B, 2), ctc_dir_threads(L), dsmem, s>>>(fp, tg, T, V, L, ws.wsa, ws.wsabase, ws.wsb,
                                                                 ws.wsbase, ws.csr, logz, status);
   } else {
     const size_t smem = ctc_smem_bytes(S, V, L);
