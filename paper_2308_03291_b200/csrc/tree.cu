@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32) tree_fold_kernel(const float*
 // the G lanes of a span read G consecutive words.  The step body is
 // instantiated per LG: term offsets are immediates, loads are predicated (no
 // branches), and a step costs ~50 instructions per warp.
-constexpr int kLinThreads = 256;
+constexpr int kLinThreads = 512;
 
 __device__ __forceinline__ int rs(int i, int n) { return i * n - ((i * (i - 1)) >> 1); }  // == tri(i, i, n)
 __device__ __forceinline__ int cs(int j) { return (j * (j + 1)) >> 1; }
