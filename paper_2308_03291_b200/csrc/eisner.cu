@@ -336,6 +336,28 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_kernel(const float* __rest
 constexpr int32_t kRetry = 5;
 
 __device__ __forceinline__ float warp_dot_sum(float s) { return warp_sum(s); }
+// Two warp sums in 5 shuffles (instead of 10): the xor-16 level exchanges the value the
+// partner half keeps.  Lanes 0-15 end with sum(a), lanes 16-31 with sum(b).
+__device__ __forceinline__ float warp_sum2(float a, float b, int lane) {
+  const bool hi = lane & 16;
+  float k = (hi ? b : a) + __shfl_xor_sync(0xffffffffu, hi ? a : b, 16);
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+  return k;
+}
+// Four warp sums in 6 shuffles: lanes 0-7 end with sum(a), 8-15 sum(b), 16-23 sum(c),
+// 24-31 sum(d).
+__device__ __forceinline__ float warp_sum4(float a, float b, float c, float d, int lane) {
+  const bool h16 = lane & 16, h8 = lane & 8;
+  const float k0 = (h16 ? c : a) + __shfl_xor_sync(0xffffffffu, h16 ? a : c, 16);
+  const float k1 = (h16 ? d : b) + __shfl_xor_sync(0xffffffffu, h16 ? b : d, 16);
+  float k = (h8 ? k1 : k0) + __shfl_xor_sync(0xffffffffu, h8 ? k0 : k1, 8);
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+  return k;
+}
+// packed-row offset: chart[pk(x, c, n)] == chart[prow(x, n) + c]
+__device__ __forceinline__ int prow(int x, int n) { return x * n - ((x * (x - 1)) >> 1) - x - 1; }
 
 __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __restrict__ adj_all, int n, int single,
                                                                  double* __restrict__ logz, float* __restrict__ marg_all,
@@ -457,13 +479,13 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
         if (kA < iA + w) sA = fmaf(CR(iA, kA), CL(kA + 1, iA + w), sA);
         if (hasB && kB < iB + w) sB = fmaf(CR(iB, kB), CL(kB + 1, iB + w), sB);
       }
-      const float FA = warp_dot_sum(sA), FB = warp_dot_sum(sB);
-      const float virA = wrA * FA, vilA = wlA * FA;
-      const float virB = wrB * FB, vilB = wlB * FB;
-      if (lane == 0) {
-        ir[pk(iA, iA + w, n)] = virA; il[pk(iA, iA + w, n)] = vilA;
-        if (hasB) { ir[pk(iB, iB + w, n)] = virB; il[pk(iB, iB + w, n)] = vilB; }
-      }
+      // lanes 0-15 hold F(A), lanes 16-31 F(B); lane 0 / lane 16 store span A / B
+      const float F = warp_sum2(sA, sB, lane);
+      const bool hiB = lane & 16;
+      const float vir = (hiB ? wrB : wrA) * F, vil = (hiB ? wlB : wlA) * F;
+      if (lane == 0) { ir[pk(iA, iA + w, n)] = vir; il[pk(iA, iA + w, n)] = vil; }
+      if (lane == 16 && hasB) { ir[pk(iB, iB + w, n)] = vir; il[pk(iB, iB + w, n)] = vil; }
+      lmax = fmaxf(lmax, fmaxf(vir, vil));
       __syncwarp();
       float srA = 0.f, slA = 0.f, srB = 0.f, slB = 0.f;
 #pragma unroll
@@ -477,14 +499,13 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
           if (o < w) slB = fmaf(CL(iB, iB + o), il[pk(iB + o, iB + w, n)], slB);
         }
       }
-      const float vcrA = warp_dot_sum(srA), vclA = warp_dot_sum(slA);
-      const float vcrB = warp_dot_sum(srB), vclB = warp_dot_sum(slB);
-      if (lane == 0) {
-        cr[pk(iA, iA + w, n)] = vcrA; cl[pk(iA, iA + w, n)] = vclA;
-        if (hasB) { cr[pk(iB, iB + w, n)] = vcrB; cl[pk(iB, iB + w, n)] = vclB; }
-      }
-      lmax = fmaxf(lmax, fmaxf(fmaxf(virA, vilA), fmaxf(vcrA, vclA)));
-      lmax = fmaxf(lmax, fmaxf(fmaxf(virB, vilB), fmaxf(vcrB, vclB)));
+      // lanes 0 / 8 / 16 / 24 hold cr(A) / cl(A) / cr(B) / cl(B)
+      const float v4 = warp_sum4(srA, slA, srB, slB, lane);
+      if (lane == 0) cr[pk(iA, iA + w, n)] = v4;
+      if (lane == 8) cl[pk(iA, iA + w, n)] = v4;
+      if (hasB && lane == 16) cr[pk(iB, iB + w, n)] = v4;
+      if (hasB && lane == 24) cl[pk(iB, iB + w, n)] = v4;
+      lmax = fmaxf(lmax, v4);
     }
     if (lane == 0) wred[warp] = lmax;
     __syncthreads();
@@ -542,6 +563,10 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
       mg[cc] = fminf(fmaxf(W(0, cc) * CL(1, cc) * CR(cc, n) * rz, 0.f), 1.f);
 
   // =============================================================== outside
+  // column reads chart[pk(x, c)] for x = lane + 32 q: per-lane packed-row offsets
+  int Rq[kQ];
+#pragma unroll
+  for (int q = 0; q < kQ; ++q) Rq[q] = prow(lane + 32 * q, n);
   for (int w = n; w >= 1; --w) {
     float lmax = 0.f;
     float wpre;  // this warp's arc weights of the width, as in the inside pass
@@ -549,57 +574,103 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
       const int q = lane >> 1, a = warp + q * kWarps;
       wpre = (a + w <= n) ? ((lane & 1) ? W(a, a + w) : W(a + w, a)) : 0.f;
     }
-    for (int a = warp, it = 0; a + w <= n; a += kWarps, ++it) {
-      const int bb = a + w;
-      const int n1 = n - bb, n2 = a;
-      const float wba = __shfl_sync(0xffffffffu, wpre, 2 * it), wab = __shfl_sync(0xffffffffu, wpre, 2 * it + 1);
-      const int qo1 = (max(n1, n2) + 31) >> 5, qo2 = (max(n1, a) + 32) >> 5;
-      float sA = 0.f, sB = 0.f;
+    // two spans per warp iteration (A = a, B = a + kWarps): independent chains in flight
+    for (int a = warp, it = 0; a + w <= n; a += 2 * kWarps, it += 2) {
+      const bool hasB = a + kWarps + w <= n;
+      float sv[2][2], wv[2][2];
+      int bq[2], rA[2], rB[2], rB1[2], n1q[2], n2q[2];
+      int qo1 = 0, qo2 = 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int aa = a + h * kWarps, bb = aa + w;
+        const bool live = h == 0 || hasB;
+        bq[h] = bb;
+        n1q[h] = live ? n - bb : 0;
+        n2q[h] = live ? aa : 0;
+        rA[h] = prow(aa, n);
+        rB[h] = prow(bb, n);
+        rB1[h] = prow(bb + 1, n);
+        wv[h][0] = __shfl_sync(0xffffffffu, wpre, 2 * (it + h));      // W(bb, aa)
+        wv[h][1] = __shfl_sync(0xffffffffu, wpre, 2 * (it + h) + 1);  // W(aa, bb)
+        sv[h][0] = sv[h][1] = 0.f;
+        if (live) {
+          qo1 = max(qo1, (max(n1q[h], n2q[h]) + 31) >> 5);
+          qo2 = max(qo2, (max(n1q[h], aa) + 32) >> 5);
+        }
+      }
 #pragma unroll
       for (int q = 0; q < kQ; ++q) {
         if (q >= qo1) break;  // warp-uniform: only the 32-term slices this width needs
         const int x = lane + 32 * q;
-        if (x < n1) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int aa = a + h * kWarps, bb = bq[h];
+          const bool pr = x < n1q[h], pl = x < n2q[h];
           const int j = bb + 1 + x;
-          sA = fmaf(gfo[pk(a, j, n)], CL(bb + 1, j), sA);   // split parents (a, j)
-          sB = fmaf(gcl[pk(a, j, n)], il[pk(bb, j, n)], sB);  // cl parents (a, j)
-        }
-        if (x < n2) {
-          const int i = x;
-          sA = fmaf(gcr[pk(i, bb, n)], ir[pk(i, a, n)], sA);  // cr parents (i, bb)
-          sB = fmaf(gfo[pk(i, bb, n)], CR(i, a - 1), sB);     // split parents (i, bb)
+          // right parents (aa, j): split (gfo) with CL(bb+1, j) (1 at j = bb+1), cl parents with il(bb, j)
+          const float g1 = pr ? gfo[rA[h] + j] : 0.f, c1 = (pr && x > 0) ? cl[rB1[h] + j] : 1.f;
+          const float g2 = pr ? gcl[rA[h] + j] : 0.f, c2 = pr ? il[rB[h] + j] : 0.f;
+          // left parents (x, bb): cr parents with ir(x, aa), split (gfo) with CR(x, aa-1) (1 at x = aa-1)
+          const float g3 = pl ? gcr[Rq[q] + bb] : 0.f, c3 = pl ? ir[Rq[q] + aa] : 0.f;
+          const float g4 = pl ? gfo[Rq[q] + bb] : 0.f, c4 = (pl && x != aa - 1) ? cr[Rq[q] + aa - 1] : 1.f;
+          sv[h][0] = fmaf(g1, c1, fmaf(g3, c3, sv[h][0]));
+          sv[h][1] = fmaf(g2, c2, fmaf(g4, c4, sv[h][1]));
         }
       }
-      float vgcr = warp_dot_sum(sA), vgcl = warp_dot_sum(sB);
-      if (lane == 0) {
-        if (!single) {
-          if (a == 0 && bb == n) vgcr = rz;
-        } else {
-          if (bb == n && a >= 1) vgcr += W(0, a) * CL(1, a) * rz;
-          if (a == 1) vgcl += W(0, bb) * CR(bb, n) * rz;
+      // lanes 0 / 8 / 16 / 24: cr adjoint of A / cl adjoint of A / cr of B / cl of B
+      {
+        const float vg = warp_sum4(sv[0][0], sv[0][1], sv[1][0], sv[1][1], lane);
+        const int h = lane >> 4, aa = a + h * kWarps, bb = aa + w;
+        if ((lane & 15) == 0 && (h == 0 || hasB)) {
+          float v = vg;
+          if (!single) {
+            if (aa == 0 && bb == n) v = rz;
+          } else {
+            if (bb == n && aa >= 1) v += W(0, aa) * CL(1, aa) * rz;
+          }
+          gcr[pk(aa, bb, n)] = v;
+          lmax = fmaxf(lmax, v);
         }
-        gcr[pk(a, bb, n)] = vgcr;
-        gcl[pk(a, bb, n)] = vgcl;
+        if ((lane & 15) == 8 && (h == 0 || hasB)) {
+          float v = vg;
+          if (single && aa == 1) v += W(0, bb) * CR(bb, n) * rz;
+          gcl[pk(aa, bb, n)] = v;
+          lmax = fmaxf(lmax, v);
+        }
       }
       __syncwarp();
-      float tr = 0.f, tl = 0.f;
+      float tv[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
 #pragma unroll
       for (int q = 0; q < kQ; ++q) {
         if (q >= qo2) break;  // warp-uniform: only the 32-term slices this width needs
         const int x = lane + 32 * q;
-        const int j = bb + x;
-        if (j <= n) tr = fmaf(gcr[pk(a, j, n)], CR(bb, j), tr);
-        if (x <= a) tl = fmaf(gcl[pk(x, bb, n)], CL(x, a), tl);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int aa = a + h * kWarps, bb = bq[h];
+          const bool live = h == 0 || hasB;
+          const int j = bb + x;
+          const bool pr = live && j <= n, pl = live && x <= aa;
+          const float g1 = pr ? gcr[rA[h] + j] : 0.f, c1 = (pr && x > 0) ? cr[rB[h] + j] : 1.f;  // CR(bb, j)
+          const float g2 = pl ? gcl[Rq[q] + bb] : 0.f, c2 = (pl && x != aa) ? cl[Rq[q] + aa] : 1.f;  // CL(x, aa)
+          tv[h][0] = fmaf(g1, c1, tv[h][0]);
+          tv[h][1] = fmaf(g2, c2, tv[h][1]);
+        }
       }
-      const float gir = warp_dot_sum(tr), gil = warp_dot_sum(tl);
-      if (lane == 0) {
-        const int e = pk(a, bb, n);
-        const float vf = gil * wba + gir * wab;
-        gfo[e] = vf;
-        const float pr = gir * ir[e], pl = gil * il[e];
-        if (!(single && a == 0)) mg[a * N1 + bb] = fminf(fmaxf(pr, 0.f), 1.f);
-        mg[bb * N1 + a] = fminf(fmaxf(pl, 0.f), 1.f);
-        lmax = fmaxf(lmax, fmaxf(fmaxf(vgcr, vgcl), vf));
+      // lanes 0 / 8 / 16 / 24: ir adjoint of A / il of A / ir of B / il of B
+      const float gt = warp_sum4(tv[0][0], tv[0][1], tv[1][0], tv[1][1], lane);
+      const float gl8 = __shfl_down_sync(0xffffffffu, gt, 8);
+      {
+        const int h = lane >> 4, aa = a + h * kWarps, bb = aa + w;
+        if ((lane & 15) == 0 && (h == 0 || hasB)) {
+          const int e = pk(aa, bb, n);
+          const float gir = gt, gil = gl8;
+          const float vf = gil * (h ? wv[1][0] : wv[0][0]) + gir * (h ? wv[1][1] : wv[0][1]);
+          gfo[e] = vf;
+          const float pr = gir * ir[e], pl = gil * il[e];
+          if (!(single && aa == 0)) mg[aa * N1 + bb] = fminf(fmaxf(pr, 0.f), 1.f);
+          mg[bb * N1 + aa] = fminf(fmaxf(pl, 0.f), 1.f);
+          lmax = fmaxf(lmax, vf);
+        }
       }
     }
     lmax = warp_max(lmax);
