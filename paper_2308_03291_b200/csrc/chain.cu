@@ -1451,17 +1451,9 @@ fallback:
   }
 }
 
-// Viterbi for m <= 32 (chain.py:98-114), one 512-thread CTA per instance:
-// warp w owns the next tag w (kTPW = 1; kTPW = 2 packs tags 2w, 2w+1 into 16
-// warps and measured 59 vs 50 us at B=32 n=128), lane a the predecessor a: the
-// candidate s_t[a] + theta_t[a][b] (the reference's addition
-// order: bit-identical scores), and a warp argmax by REDUX on an
-// order-preserving 64-bit key (high word, then the low word among the ties,
-// then the lowest lane: the first maximum, chain.py:106).  The winner lane
-// writes s_(t+1)[b] and the backpointer; ONE CTA barrier per step publishes
-// the new scores.  theta tiles stream through a ring of kVD row-padded tiles
-// (pitch 36), one 16-byte cp.async per thread of the first 256 per step.
-constexpr int kVT = 1024;  // one warp per next tag (kTPW = 1)
+// Viterbi for m <= 32 (chain.py:98-114), one CTA per instance; theta tiles stream
+// through a ring of kVD row-padded tiles (pitch 36), one 16-byte cp.async per thread
+// per step; ONE CTA barrier per step publishes the new scores.
 constexpr int kVD = 8;
 constexpr int kVTP = 36;
 
@@ -1481,9 +1473,18 @@ __device__ __forceinline__ int warp_argmax_key(uint64_t k) {
   return __ffs(cand) - 1;
 }
 
-// kTPW next tags per warp: 2 (512 threads) or 1 (1024 threads)
-template <int kTPW>
-__global__ void __launch_bounds__(32 * 32 / kTPW, 1) chain_viterbi_warp_kernel(
+// Grouped Viterbi (m <= 32): kGP lanes per next tag, 256 threads.  Lane q of
+// tag b's group scans the predecessors a = q, q + 8, q + 16, q + 24 with the
+// reference's fp64 sums s_t[a] + theta_t[a][b] and a strict '>' (first maximum
+// of its phase), then the group combines (value, a) pairs over three xor
+// shuffles, ties to the lower a: the first maximum over all predecessors
+// (chain.py:106).  With the tile pitch 36 the eight phases of four tags read
+// 32 distinct banks.  (One warp per tag with a REDUX argmax: 49.4 vs 47.2 us at
+// B=32 n=128; comparing on 64-bit integer keys instead of fp64: 55.4 us.)
+constexpr int kGP = 8;
+constexpr int kGT = 32 * kGP;
+
+__global__ void __launch_bounds__(kGT, 1) chain_viterbi_grp_kernel(
     const float* __restrict__ init, const float* __restrict__ trans, int n, int m, int32_t* __restrict__ tags,
     double* __restrict__ score, int32_t* __restrict__ status, const int32_t* __restrict__ lengths) {
   extern __shared__ __align__(16) float smw[];
@@ -1491,6 +1492,7 @@ __global__ void __launch_bounds__(32 * 32 / kTPW, 1) chain_viterbi_warp_kernel(
   double* sv = reinterpret_cast<double*>(ring + kVD * 32 * kVTP);          // [2][32]
   uint8_t* back = reinterpret_cast<uint8_t*>(sv + 64);                     // [n][32]
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nb = tid / kGP, q = tid % kGP;  // next tag, predecessor phase
   const int nl = n, mm = m * m;  // nl: layout length; n: this instance's length (ragged batches)
   n = lengths ? min(max(lengths[b], 1), nl) : nl;
   const int T = n - 1;
@@ -1499,13 +1501,11 @@ __global__ void __launch_bounds__(32 * 32 / kTPW, 1) chain_viterbi_warp_kernel(
   auto stage = [&](int t) {
     float* tile = ring + (t % kVD) * 32 * kVTP;
     if (full) {
-      if (tid < 256) {
-        const int r = tid >> 3, c4 = (tid & 7) * 4;
-        const unsigned dst = (unsigned)__cvta_generic_to_shared(tile + r * kVTP + c4);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(th + (size_t)t * 1024 + r * 32 + c4));
-      }
+      const int r = tid >> 3, c4 = (tid & 7) * 4;
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(tile + r * kVTP + c4);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(th + (size_t)t * 1024 + r * 32 + c4));
     } else {
-      for (int e = tid; e < 1024; e += 32 * 32 / kTPW) {
+      for (int e = tid; e < 1024; e += kGT) {
         const int r = e >> 5, c = e & 31;
         if (r < m && c < m) {
           const unsigned dst = (unsigned)__cvta_generic_to_shared(tile + r * kVTP + c);
@@ -1526,42 +1526,51 @@ __global__ void __launch_bounds__(32 * 32 / kTPW, 1) chain_viterbi_warp_kernel(
     bad |= (tid < m) && bad_input(x);
     sv[tid] = tid < m ? (double)x : ninfd();
   }
-  const bool alive = lane < m;
-  const int b0 = kTPW * warp;
+  const bool live = nb < m;
   for (int t = 0; t < T; ++t) {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(kVD - 2));
     __syncthreads();  // tile t resident; s_t published; slot (t - 1) % kVD free
     const double* cur = sv + (t & 1) * 32;
     double* nxt = sv + ((t + 1) & 1) * 32;
-    const float* xr = ring + (t % kVD) * 32 * kVTP + lane * kVTP + b0;
-    const double sa = cur[lane];
+    const float* col = ring + (t % kVD) * 32 * kVTP + nb;  // theta_t[a][nb] at col[a * kVTP]
     if (t + kVD - 1 < T) stage(t + kVD - 1);
     cpa_commit();
+    double best = ninfd();
+    int arg = q;
 #pragma unroll
-    for (int k = 0; k < kTPW; ++k) {
-      const float x = xr[k];
-      bad |= alive && b0 + k < m && bad_input(x);
-      const double v = (alive && b0 + k < m) ? sa + (double)x : ninfd();
-      const int w = warp_argmax_key(dkey(v));
-      if (lane == w) {
-        nxt[b0 + k] = v;
-        back[(size_t)(t + 1) * 32 + b0 + k] = (uint8_t)w;
-      }
+    for (int i = 0; i < 32 / kGP; ++i) {
+      const int a = q + kGP * i;
+      const float x = col[a * kVTP];
+      const bool ok = live && a < m;
+      bad |= ok && bad_input(x);
+      const double v = ok ? cur[a] + (double)x : ninfd();
+      if (v > best) { best = v; arg = a; }
+    }
+#pragma unroll
+    for (int o = 1; o < kGP; o <<= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+      if (ob > best || (ob == best && oa < arg)) { best = ob; arg = oa; }
+    }
+    if (q == 0 && live) {
+      nxt[nb] = best;
+      back[(size_t)(t + 1) * 32 + nb] = (uint8_t)arg;
     }
   }
   asm volatile("cp.async.wait_group 0;\n" ::);
   bad = __syncthreads_or(bad);  // also publishes the last scores
   if (warp == 0) {
+    const bool alive = lane < m;
     const double* fin = sv + (T & 1) * 32;
     const double v = alive ? fin[lane] : ninfd();
     const int win = warp_argmax_key(dkey(v));  // final tag: first argmax (chain.py:111)
-    const double best = __shfl_sync(0xffffffffu, v, win);
+    const double bestf = __shfl_sync(0xffffffffu, v, win);
     int32_t* tg = tags + (size_t)b * nl;
     for (int t = n + lane; t < nl; t += 32) tg[t] = 0;  // past this instance's length
     if (lane == 0) {
-      const bool vac = (best == ninfd());
+      const bool vac = (bestf == ninfd());
       status[b] = bad ? SDB_ST_INVALID : (vac ? SDB_ST_VACUOUS : SDB_ST_OK);
-      score[b] = best;
+      score[b] = bestf;
       int c = vac ? 0 : win;
       tg[n - 1] = c;
       for (int t = n - 2; t >= 0; --t) {
@@ -1721,9 +1730,9 @@ extern "C" int sdb_chain_viterbi_lengths(const float* init, const float* trans, 
   const size_t smw = (size_t)kVD * 32 * kVTP * 4 + 64 * 8 + (size_t)n * 32 + 64;
   if (m > 32 || smw > 200 * 1024) return SDB_ERR_UNSUPPORTED;
   if (B == 0) return SDB_OK;
-  if (sdb_set_smem((const void*)chain_viterbi_warp_kernel<1>, smw) != cudaSuccess) return SDB_ERR_CUDA;
-  chain_viterbi_warp_kernel<1><<<(unsigned)B, kVT, smw, (cudaStream_t)stream>>>(init, trans, n, m, tags, score,
-                                                                              status, lengths);
+  if (sdb_set_smem((const void*)chain_viterbi_grp_kernel, smw) != cudaSuccess) return SDB_ERR_CUDA;
+  chain_viterbi_grp_kernel<<<(unsigned)B, kGT, smw, (cudaStream_t)stream>>>(init, trans, n, m, tags, score, status,
+                                                                            lengths);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
 }
@@ -1743,9 +1752,9 @@ extern "C" int sdb_chain_viterbi(const float* init, const float* trans, int64_t 
   if (m <= 32) {
     const size_t smw = (size_t)kVD * 32 * kVTP * 4 + 64 * 8 + (size_t)n * 32 + 64;  // ring, scores, backpointers
     if (smw <= 200 * 1024) {
-      if (sdb_set_smem((const void*)chain_viterbi_warp_kernel<1>, smw) != cudaSuccess) return SDB_ERR_CUDA;
-      chain_viterbi_warp_kernel<1><<<(unsigned)B, kVT, smw, (cudaStream_t)stream>>>(init, trans, n, m, tags, score,
-                                                                                  status, nullptr);
+      if (sdb_set_smem((const void*)chain_viterbi_grp_kernel, smw) != cudaSuccess) return SDB_ERR_CUDA;
+      chain_viterbi_grp_kernel<<<(unsigned)B, kGT, smw, (cudaStream_t)stream>>>(init, trans, n, m, tags, score,
+                                                                                status, nullptr);
       SDB_CHECK_LAUNCH();
       return SDB_OK;
     }
