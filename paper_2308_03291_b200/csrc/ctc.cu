@@ -428,7 +428,10 @@ constexpr int kMargFrames = 32;     // frames per CTA (4 per warp)
 // shared slice and reduces it with warp primitives only, so the warps of a CTA
 // never wait on each other (the per-frame CTA barriers of a row-per-CTA layout
 // left this kernel latency-bound).
-template <int kRowRegs>  // >= ceil(S / 32): the row's states per lane
+// kVR > 0 (V <= 32 kVR): lane-owned labels v = lane + 32 k with their first two
+// states cached in registers (the CSR fallback only for a label repeated three or
+// more times); kVR = 0: every label through the CSR lists.
+template <int kRowRegs, int kVR>  // kRowRegs >= ceil(S / 32): the row's states per lane
 __global__ void __launch_bounds__(kMargWarps * 32) ctc_marg_kernel(
     const float* __restrict__ wsa_all, const float* __restrict__ wsabase_all, const float* __restrict__ wsb_all,
     const float* __restrict__ wsbase_all, const double* __restrict__ logz, const int32_t* __restrict__ csr_all,
@@ -450,6 +453,17 @@ __global__ void __launch_bounds__(kMargWarps * 32) ctc_marg_kernel(
   for (int e = tid; e <= V; e += blockDim.x) off[e] = csr[e];
   for (int e = tid; e < L; e += blockDim.x) lst[e] = csr[V + 1 + e];
   __syncthreads();
+  // label v's states in increasing s: the first two in registers (-1: none), `many` beyond
+  int s1[kVR > 0 ? kVR : 1], s2[kVR > 0 ? kVR : 1];
+  bool many[kVR > 0 ? kVR : 1];
+#pragma unroll
+  for (int k = 0; k < kVR; ++k) {
+    const int v = lane + 32 * k;
+    const int o0 = (v >= 1 && v < V) ? off[v] : 0, o1 = (v >= 1 && v < V) ? off[v + 1] : 0;
+    s1[k] = (o1 > o0) ? lst[o0] : -1;
+    s2[k] = (o1 > o0 + 1) ? lst[o0 + 1] : -1;
+    many[k] = o1 > o0 + 2;
+  }
   float* prow = prow_all + (size_t)warp * S;
   const int Sp = S + 1;  // ctc_dir_kernel's even row pitch
   const float* pa = wsa_all + (size_t)b * T * Sp;
@@ -457,9 +471,9 @@ __global__ void __launch_bounds__(kMargWarps * 32) ctc_marg_kernel(
   const float* ba = wsabase_all + (size_t)b * T * 32;
   const float* bb = wsbase_all + (size_t)b * T * 32;
   const double Z2 = logz[b] * 1.4426950408889634;  // offsets and bases are log2 units
-  // the warp's next frame (both offsets and the two bases of each 32-state group) is loaded into
+  // the warp's next frame (both offsets and the two bases of each 64-state group) is loaded into
   // registers while the current one is reduced; the posterior of state e = 32 u + lane is
-  // exp2(alpha + beta - Z): bases and Z combined in fp64, the offsets added in fp32
+  // exp2(alpha + beta - Z): bases and Z combined in fp64, the offsets added in fp32.
   // Lane g loads the two bases of 64-state group g (one coalesced load each) and forms that
   // group's fp64 combination once; the state loop takes it by shuffle.
   float xa[kRowRegs], xb[kRowRegs], ca, cb;
@@ -480,28 +494,45 @@ __global__ void __launch_bounds__(kMargWarps * 32) ctc_marg_kernel(
   if (t0 + warp < t1) fetch(t0 + warp);
   for (int t = t0 + warp; t < t1; t += kMargWarps) {
     const float cl = (float)((double)ca + (double)cb - Z2);  // 64-state group `lane` (>= ceil(S/64) unused)
+    // blank: the even states are exactly the even lanes' (e = lane + 32 u keeps the lane's parity)
+    float bl = 0.f;
 #pragma unroll
     for (int u = 0; u < kRowRegs; ++u) {
       const int e = lane + 32 * u;
       const float c = __shfl_sync(0xffffffffu, cl, u >> 1);
       if (e < S) {
-        prow[e] = ex2(c + xa[u] + xb[u]);  // an -inf offset gives ex2(-inf) = +0 (no +inf offsets)
+        const float p = ex2(c + xa[u] + xb[u]);  // an -inf offset gives ex2(-inf) = +0 (no +inf offsets)
+        prow[e] = p;
+        bl += p;
       }
     }
     if (t + kMargWarps < t1) fetch(t + kMargWarps);
+    bl = warp_sum((lane & 1) ? 0.f : bl);
     __syncwarp();
-    // blank: the even states, fixed order (lane-strided partial sums, then a butterfly)
-    float bl = 0.f;
-    for (int e = 2 * lane; e < S; e += 64) bl += prow[e];
-    bl = warp_sum(bl);
-    for (int v = lane; v < V; v += 32) {
-      float acc = 0.f;
-      if (v == 0) {
-        acc = bl;
-      } else {
-        for (int q = off[v]; q < off[v + 1]; ++q) acc += prow[lst[q]];
+    float* mrow = mg + (size_t)t * V;
+    if constexpr (kVR > 0) {
+#pragma unroll
+      for (int k = 0; k < kVR; ++k) {
+        const int v = lane + 32 * k;
+        if (v < V) {
+          float acc = 0.f;
+          if (s1[k] >= 0) acc += prow[s1[k]];
+          if (s2[k] >= 0) acc += prow[s2[k]];
+          if (many[k])
+            for (int q = off[v] + 2; q < off[v + 1]; ++q) acc += prow[lst[q]];
+          mrow[v] = (v == 0) ? bl : acc;
+        }
       }
-      mg[(size_t)t * V + v] = acc;
+    } else {
+      for (int v = lane; v < V; v += 32) {
+        float acc = 0.f;
+        if (v == 0) {
+          acc = bl;
+        } else {
+          for (int q = off[v]; q < off[v + 1]; ++q) acc += prow[lst[q]];
+        }
+        mrow[v] = acc;
+      }
     }
     __syncwarp();  // the slice is rewritten for the warp's next frame
   }
@@ -582,17 +613,22 @@ int ctc_launch(const float* fp, const int32_t* tg, int64_t B, int T, int V, int 
     const size_t msmem = (((size_t)(V + 1 + L) + 3) & ~(size_t)3) * 4 + (size_t)kMargWarps * S2 * 4;
     dim3 g((unsigned)((T + kMargFrames - 1) / kMargFrames), (unsigned)B);
     const int rr = (S2 + 31) / 32;
-    if (rr <= 9) {
-      if (msmem > 48 * 1024 && sdb_set_smem((const void*)ctc_marg_kernel<9>, msmem) != cudaSuccess)
-        return SDB_ERR_CUDA;
-      ctc_marg_kernel<9><<<g, kMargWarps * 32, msmem, s>>>(ws.wsa, ws.wsabase, ws.wsb, ws.wsbase, logz, ws.csr, T, V,
-                                                          L, status, marg);
-    } else {
-      if (msmem > 48 * 1024 && sdb_set_smem((const void*)ctc_marg_kernel<32>, msmem) != cudaSuccess)
-        return SDB_ERR_CUDA;
-      ctc_marg_kernel<32><<<g, kMargWarps * 32, msmem, s>>>(ws.wsa, ws.wsabase, ws.wsb, ws.wsbase, logz, ws.csr, T,
-                                                           V, L, status, marg);
-    }
+    const bool vr = V <= 128;
+    const void* kf = rr <= 9 ? (vr ? (const void*)ctc_marg_kernel<9, 4> : (const void*)ctc_marg_kernel<9, 0>)
+                             : (vr ? (const void*)ctc_marg_kernel<32, 4> : (const void*)ctc_marg_kernel<32, 0>);
+    if (msmem > 48 * 1024 && sdb_set_smem(kf, msmem) != cudaSuccess) return SDB_ERR_CUDA;
+    if (rr <= 9 && vr)
+      ctc_marg_kernel<9, 4><<<g, kMargWarps * 32, msmem, s>>>(ws.wsa, ws.wsabase, ws.wsb, ws.wsbase, logz, ws.csr, T,
+                                                             V, L, status, marg);
+    else if (rr <= 9)
+      ctc_marg_kernel<9, 0><<<g, kMargWarps * 32, msmem, s>>>(ws.wsa, ws.wsabase, ws.wsb, ws.wsbase, logz, ws.csr, T,
+                                                             V, L, status, marg);
+    else if (vr)
+      ctc_marg_kernel<32, 4><<<g, kMargWarps * 32, msmem, s>>>(ws.wsa, ws.wsabase, ws.wsb, ws.wsbase, logz, ws.csr,
+                                                              T, V, L, status, marg);
+    else
+      ctc_marg_kernel<32, 0><<<g, kMargWarps * 32, msmem, s>>>(ws.wsa, ws.wsabase, ws.wsb, ws.wsbase, logz, ws.csr,
+                                                              T, V, L, status, marg);
     SDB_CHECK_LAUNCH();
   }
   return SDB_OK;
