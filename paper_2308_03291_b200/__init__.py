@@ -35,6 +35,7 @@ from .dist import (
     structure_score,
 )
 from .dist import get_precision, set_precision  # noqa: F401  (exact fp64 mode)
+from .dist import warmup  # noqa: F401  (one-time CUDA context / module bring-up)
 from .errors import (
     InvalidProblem,
     SamplerStepLimit,

@@ -411,8 +411,20 @@ def device():
     return torch.device("cuda", torch.cuda.current_device())
 
 
+def warmup():
+    """Bring up the CUDA context on the current device, load `_sdb200.so` and run
+    one tiny log-partition in the current precision, so that a caller's first
+    real call does not pay the one-time context / module initialisation
+    (~1 s in a fresh process)."""
+    from .families import LinearChainCRF
+
+    device()
+    log_partition(LinearChainCRF(np.zeros(2), np.zeros((1, 2, 2))))
+    torch.cuda.synchronize()
+
+
 __all__ = [
-    "log_partition", "log_partition_info", "marginals", "marginals_info", "potential_marginals",
+    "warmup", "log_partition", "log_partition_info", "marginals", "marginals_info", "potential_marginals",
     "argmax", "argmax_info", "structure_score", "masked_dot", "entropy", "entropy_info",
     "cross_entropy", "cross_entropy_info", "kl_divergence", "kl_divergence_info",
     "log_prob", "log_prob_info", "batch_map", "VacuousDistribution",

@@ -73,15 +73,19 @@ def _marg(d):
     return {k: np.asarray(v, dtype=np.float64) for k, v in gd.potential_marginals(to_gpu(d)).items()}
 
 
-def install(sd, exact: bool = False):
+def install(sd, exact: bool = False, warm: bool = True):
     """Patch the reference package `sd` (the imported `structdist`); returns an
     undo callable.  exact=True routes log-partition / marginals through the
     float64 entry points (gd.set_precision("fp64")) so results match the
-    reference at its own tolerances."""
+    reference at its own tolerances.  warm=True brings the device up at install
+    (dist.warmup), so the first patched call does not pay the CUDA context /
+    module initialisation."""
     wrap = _errors_as(sd)
     prev = gd.get_precision()
     if exact:
         gd.set_precision("fp64")
+    if warm:
+        gd.warmup()  # the device comes up at install, not inside the first patched call
     ch, al, co, sp = sd.chain, sd.alignment, sd.constituency, sd.spanning
     lz = lambda d: float(gd.log_partition(to_gpu(d)))  # noqa: E731
     am = lambda d: gd.argmax(to_gpu(d))  # noqa: E731

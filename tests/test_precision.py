@@ -58,7 +58,7 @@ def test_refshim_restores_precision():
         for f in fns:
             setattr(m, f, None)
         setattr(fake, mod, m)
-    undo = refshim.install(fake, exact=True)
+    undo = refshim.install(fake, exact=True, warm=False)  # host logic only: no device bring-up
     assert sd.get_precision() == "fp64"
     undo()
     assert sd.get_precision() == "fp32" and fake.chain.chain_marginals is None
