@@ -359,9 +359,13 @@ __device__ __forceinline__ float warp_sum4(float a, float b, float c, float d, i
 // packed-row offset: chart[pk(x, c, n)] == chart[prow(x, n) + c]
 __device__ __forceinline__ int prow(int x, int n) { return x * n - ((x * (x - 1)) >> 1) - x - 1; }
 
-__global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __restrict__ adj_all, int n, int single,
+// 24 warps: 1.74 ms at C4 vs 1.82 (16 warps, 103 registers) and 1.86 (32 warps, 64 registers)
+constexpr int kLinT = 768;
+template <int kLT>
+__global__ void __launch_bounds__(kLT, 1) eisner_lin_kernel(const float* __restrict__ adj_all, int n, int single,
                                                                  double* __restrict__ logz, float* __restrict__ marg_all,
                                                                  int32_t* __restrict__ status) {
+  constexpr int kLW = kLT / 32;
   extern __shared__ __align__(16) char smraw[];
   const int T = n * (n + 1) / 2;
   float *cr, *cl, *ir, *il, *gcr, *gcl, *gfo;
@@ -370,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
     cr = p; p += T; cl = p; p += T; ir = p; p += T; il = p; p += T;
     gcr = p; p += T; gcl = p; p += T; gfo = p; p += T;
   }
-  __shared__ float wred[kWarps], wred2[kWarps];
+  __shared__ float wred[kLW], wred2[kLW];
   __shared__ float cslope, zv;
   __shared__ int badsh, failsh;
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -384,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
   {
     int bad = 0;
     float sum = 0.f, cnt = 0.f;
-    for (int e = tid; e < N1 * N1; e += kThreads) {
+    for (int e = tid; e < N1 * N1; e += kLT) {
       const float x = th[e];
       bad |= bad_input(x);
       const int d = e % N1;
@@ -397,14 +401,14 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
     __syncthreads();
     if (tid == 0) {
       float S = 0.f, C = 0.f;
-      for (int q = 0; q < kWarps; ++q) { S += wred[q]; C += wred2[q]; }
+      for (int q = 0; q < kLW; ++q) { S += wred[q]; C += wred2[q]; }
       cslope = (C > 0.f) ? rintf(S / C) : 0.f;
     }
     __syncthreads();
   }
   if (badsh) {  // status INVALID, zero marginals (as eisner_kernel)
     if (tid == 0) { status[b] = SDB_ST_INVALID; logz[b] = ninfd(); }
-    if (marg_all) for (int e = tid; e < N1 * N1; e += kThreads) marg_all[(size_t)b * N1 * N1 + e] = 0.f;
+    if (marg_all) for (int e = tid; e < N1 * N1; e += kLT) marg_all[(size_t)b * N1 * N1 + e] = 0.f;
     return;
   }
   auto W = [&](int h, int d) { return ex2(__ldg(th + h * N1 + d) * SDB_LOG2E - cslope); };
@@ -413,11 +417,11 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
   for (int w = 1; w <= n; ++w) {
     float lmax = 0.f;
     // the arc weights of ALL this warp's spans of the width (<= 8 spans for n <= 128):
-    // lane 2q / 2q+1 loads the right / left arc of span warp + q kWarps, so one L2
+    // lane 2q / 2q+1 loads the right / left arc of span warp + q kLW, so one L2
     // latency per width is exposed instead of one per span pair
     float wpre;
     {
-      const int q = lane >> 1, i = warp + q * kWarps;
+      const int q = lane >> 1, i = warp + q * kLW;
       wpre = (i + w <= n) ? ((lane & 1) ? W(i + w, i) : W(i, i + w)) : 0.f;
     }
     if (w <= 64) {
@@ -425,8 +429,8 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
       // this warp per pass, reductions over lg shuffle levels inside each lane group
       const int lg = w <= 4 ? 0 : w <= 8 ? 1 : w <= 16 ? 2 : w <= 32 ? 3 : 4;
       const int G = 1 << lg, r = lane & (G - 1), qg = lane >> lg;
-      for (int q0 = 0; warp + q0 * kWarps + w <= n; q0 += 32 >> lg) {
-        const int q = q0 + qg, i = warp + q * kWarps, j = i + w;
+      for (int q0 = 0; warp + q0 * kLW + w <= n; q0 += 32 >> lg) {
+        const int q = q0 + qg, i = warp + q * kLW, j = i + w;
         const bool ok = j <= n;
         const int src = 2 * min(q, 15);
         const float wr = __shfl_sync(0xffffffffu, wpre, src), wl = __shfl_sync(0xffffffffu, wpre, src + 1);
@@ -465,8 +469,8 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
       lmax = warp_max(lmax);
     } else
     // two spans per warp iteration: their reductions are independent (ILP)
-    for (int i0 = warp, it = 0; i0 + w <= n; i0 += 2 * kWarps, ++it) {
-      const int iA = i0, iB = i0 + kWarps;
+    for (int i0 = warp, it = 0; i0 + w <= n; i0 += 2 * kLW, ++it) {
+      const int iA = i0, iB = i0 + kLW;
       const bool hasB = iB + w <= n;
       const float wrA = __shfl_sync(0xffffffffu, wpre, 4 * it), wlA = __shfl_sync(0xffffffffu, wpre, 4 * it + 1);
       const float wrB = __shfl_sync(0xffffffffu, wpre, 4 * it + 2), wlB = __shfl_sync(0xffffffffu, wpre, 4 * it + 3);
@@ -511,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
     __syncthreads();
     float M = 0.f;
 #pragma unroll
-    for (int q = 0; q < kWarps; ++q) M = fmaxf(M, wred[q]);
+    for (int q = 0; q < kLW; ++q) M = fmaxf(M, wred[q]);
     if (!(M <= 3.0e38f)) {  // inf / NaN: give up on linear space
       if (tid == 0) failsh = 1;
       break;
@@ -519,7 +523,7 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
     if (M > 0.f && (M > 16777216.f || M < 5.9604645e-8f)) {
       // absorb the growth: c += delta, every stored width v scaled by 2^(-delta v)
       const float delta = lg2(M) / (float)w;
-      for (int e = tid; e < T; e += kThreads) {
+      for (int e = tid; e < T; e += kLT) {
         // decode width of packed (i, j): row i holds j = i+1..n
         int i = 0, r = e;
         while (r >= n - i) { r -= n - i; ++i; }
@@ -557,9 +561,9 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
   if (!marg_all) return;
   float* mg = marg_all + (size_t)b * N1 * N1;
   const float rz = 1.f / EZ;
-  for (int e = tid; e < N1; e += kThreads) mg[e * N1 + e] = 0.f;
+  for (int e = tid; e < N1; e += kLT) mg[e * N1 + e] = 0.f;
   if (single)
-    for (int cc = 1 + tid; cc <= n; cc += kThreads)
+    for (int cc = 1 + tid; cc <= n; cc += kLT)
       mg[cc] = fminf(fmaxf(W(0, cc) * CL(1, cc) * CR(cc, n) * rz, 0.f), 1.f);
 
   // =============================================================== outside
@@ -571,18 +575,18 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
     float lmax = 0.f;
     float wpre;  // this warp's arc weights of the width, as in the inside pass
     {
-      const int q = lane >> 1, a = warp + q * kWarps;
+      const int q = lane >> 1, a = warp + q * kLW;
       wpre = (a + w <= n) ? ((lane & 1) ? W(a, a + w) : W(a + w, a)) : 0.f;
     }
-    // two spans per warp iteration (A = a, B = a + kWarps): independent chains in flight
-    for (int a = warp, it = 0; a + w <= n; a += 2 * kWarps, it += 2) {
-      const bool hasB = a + kWarps + w <= n;
+    // two spans per warp iteration (A = a, B = a + kLW): independent chains in flight
+    for (int a = warp, it = 0; a + w <= n; a += 2 * kLW, it += 2) {
+      const bool hasB = a + kLW + w <= n;
       float sv[2][2], wv[2][2];
       int bq[2], rA[2], rB[2], rB1[2], n1q[2], n2q[2];
       int qo1 = 0, qo2 = 0;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int aa = a + h * kWarps, bb = aa + w;
+        const int aa = a + h * kLW, bb = aa + w;
         const bool live = h == 0 || hasB;
         bq[h] = bb;
         n1q[h] = live ? n - bb : 0;
@@ -604,7 +608,7 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
         const int x = lane + 32 * q;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int aa = a + h * kWarps, bb = bq[h];
+          const int aa = a + h * kLW, bb = bq[h];
           const bool pr = x < n1q[h], pl = x < n2q[h];
           const int j = bb + 1 + x;
           // right parents (aa, j): split (gfo) with CL(bb+1, j) (1 at j = bb+1), cl parents with il(bb, j)
@@ -620,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
       // lanes 0 / 8 / 16 / 24: cr adjoint of A / cl adjoint of A / cr of B / cl of B
       {
         const float vg = warp_sum4(sv[0][0], sv[0][1], sv[1][0], sv[1][1], lane);
-        const int h = lane >> 4, aa = a + h * kWarps, bb = aa + w;
+        const int h = lane >> 4, aa = a + h * kLW, bb = aa + w;
         if ((lane & 15) == 0 && (h == 0 || hasB)) {
           float v = vg;
           if (!single) {
@@ -646,7 +650,7 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
         const int x = lane + 32 * q;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int aa = a + h * kWarps, bb = bq[h];
+          const int aa = a + h * kLW, bb = bq[h];
           const bool live = h == 0 || hasB;
           const int j = bb + x;
           const bool pr = live && j <= n, pl = live && x <= aa;
@@ -660,7 +664,7 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
       const float gt = warp_sum4(tv[0][0], tv[0][1], tv[1][0], tv[1][1], lane);
       const float gl8 = __shfl_down_sync(0xffffffffu, gt, 8);
       {
-        const int h = lane >> 4, aa = a + h * kWarps, bb = aa + w;
+        const int h = lane >> 4, aa = a + h * kLW, bb = aa + w;
         if ((lane & 15) == 0 && (h == 0 || hasB)) {
           const int e = pk(aa, bb, n);
           const float gir = gt, gil = gl8;
@@ -678,7 +682,7 @@ __global__ void __launch_bounds__(kThreads, 1) eisner_lin_kernel(const float* __
     __syncthreads();
     float M = 0.f;
 #pragma unroll
-    for (int q = 0; q < kWarps; ++q) M = fmaxf(M, wred[q]);
+    for (int q = 0; q < kLW; ++q) M = fmaxf(M, wred[q]);
     if (!(M <= 3.0e38f)) {
       if (tid == 0) status[b] = kRetry;
       return;
@@ -850,12 +854,11 @@ extern "C" int sdb_eisner(const float* adjacency, int64_t B, int32_t n, int32_t 
   const size_t smem = eisner_smem(n);
   const size_t smem_lin = (size_t)7 * (n * (n + 1) / 2) * 4;  // the seven charts only
   cudaStream_t s = (cudaStream_t)stream;
-  if (sdb_set_smem((const void*)eisner_lin_kernel, smem_lin) !=
-          cudaSuccess ||
+  if (sdb_set_smem((const void*)eisner_lin_kernel<kLinT>, smem_lin) != cudaSuccess ||
       sdb_set_smem((const void*)eisner_kernel, smem) != cudaSuccess)
     return SDB_ERR_CUDA;
   // exp-space first; the log-space kernel redoes only the instances it flagged
-  eisner_lin_kernel<<<(unsigned)B, kThreads, smem_lin, s>>>(adjacency, n, single_root ? 1 : 0, logz, marg, status);
+  eisner_lin_kernel<kLinT><<<(unsigned)B, kLinT, smem_lin, s>>>(adjacency, n, single_root ? 1 : 0, logz, marg, status);
   SDB_CHECK_LAUNCH();
   eisner_kernel<<<(unsigned)B, kThreads, smem, s>>>(adjacency, n, single_root ? 1 : 0, logz, marg, status, 1);
   SDB_CHECK_LAUNCH();
