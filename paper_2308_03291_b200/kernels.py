@@ -802,27 +802,28 @@ def expected_score(pairs, B: int, device):
 _PIPE = {}
 
 
-def _pipe_streams(dev):
-    s = _PIPE.get(dev.index)
-    if s is None:
-        s = _PIPE[dev.index] = tuple(torch.cuda.Stream(dev) for _ in range(4))  # h2d, d2h, compute x2
+def _pipe_streams(dev, ncomp: int = 2):
+    s = _PIPE.get((dev.index, ncomp))
+    if s is None:  # h2d, d2h, then ncomp compute streams
+        s = _PIPE[(dev.index, ncomp)] = tuple(torch.cuda.Stream(dev) for _ in range(2 + ncomp))
     return s
 
 
-def run_host_batch(fn, host_inputs, host_outputs, device, chunks: int = 8):
+def run_host_batch(fn, host_inputs, host_outputs, device, chunks: int = 8, compute_streams: int = 2):
     """Batched call on HOST-resident (pinned) tensors with the PCIe copies
     overlapped: the batch is cut into `chunks` slices along the leading
     (instance) axis; slice k's host->device copy, slice k-1's kernels and
     slice k-2's device->host copy run concurrently (one copy stream per
-    direction -- PCIe is full duplex -- and two compute streams, since a
-    slice's grid is smaller than the GPU).  `chunks` is a slice count or a
+    direction -- PCIe is full duplex -- and `compute_streams` compute
+    streams, since a slice's grid is smaller than the GPU and latency-bound
+    slice kernels overlap).  `chunks` is a slice count or a
     list of slice sizes (a short last slice shortens the D2H tail).  `fn(*device_inputs)` returns the
     device outputs (None entries skipped) matching `host_outputs`.  The
     current stream waits for the last copy, so an event recorded after this
     call covers the whole request."""
     cur = torch.cuda.current_stream(device)
-    h2d, d2h, c0, c1 = _pipe_streams(device)
-    for s in (h2d, d2h, c0, c1):
+    h2d, d2h, *comps = _pipe_streams(device, max(1, int(compute_streams)))
+    for s in (h2d, d2h, *comps):
         s.wait_stream(cur)
     B = host_inputs[0].shape[0]
     if isinstance(chunks, (list, tuple)):  # explicit slice sizes (e.g. a short last slice)
@@ -836,7 +837,7 @@ def run_host_batch(fn, host_inputs, host_outputs, device, chunks: int = 8):
     chunks = len(bounds) - 1
     for k in range(chunks):
         lo, hi = bounds[k], bounds[k + 1]
-        comp = c0 if k % 2 == 0 else c1
+        comp = comps[k % len(comps)]
         with torch.cuda.stream(h2d):
             dev_in = [t[lo:hi].to(device, non_blocking=True) for t in host_inputs]
         comp.wait_stream(h2d)
