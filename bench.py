@@ -76,7 +76,7 @@ CONFIGS = {
 HEADLINE = "c2a"
 # e2e: instance slices per request in kernels.run_host_batch (PCIe-bound configs
 # overlap H2D, kernels and D2H; tiny batches run as one slice)
-E2E_CHUNKS = {"c1": 2, "c2a": [32] * 7 + [24, 8], "c2b": 8, "c3": 4, "c4": 2, "c5a": 4, "c5b": 1}  # tools/e2e_sweep_cfg.py
+E2E_CHUNKS = {"c1": 1, "c2a": [32] * 7 + [24, 8], "c2b": 8, "c3": 4, "c4": 2, "c5a": 4, "c5b": 1}  # tools/e2e_sweep_cfg.py
 # the unmodified reference takes ~170 s per C5b instance: its arm uses the port there
 REF_TOO_SLOW = {"c5b": "reference PCFG marginals take ~170 s per instance (SURVEY.md §6)"}
 
