@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(kMargWarps * 32) ctc_marg_kernel(
   const int S = 2 * L + 1;
   int* off = reinterpret_cast<int*>(cm);      // [V+1]
   int* lst = off + V + 1;                     // [L]
-  float* prow_all = cm + ((V + 1 + L + 3) & ~3);  // [kMargWarps][S]
+  float* prow_all = cm + ((V + 1 + L + 3) & ~3);  // [kMargWarps][S + 1]
   const int b = blockIdx.y, t0 = blockIdx.x * kMargFrames, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int t1 = min(t0 + kMargFrames, T);
@@ -464,28 +464,29 @@ __global__ void __launch_bounds__(kMargWarps * 32) ctc_marg_kernel(
     s2[k] = (o1 > o0 + 1) ? lst[o0 + 1] : -1;
     many[k] = o1 > o0 + 2;
   }
-  float* prow = prow_all + (size_t)warp * S;
+  float* prow = prow_all + (size_t)warp * (S + 1);  // even slice pitch: float2 stores
   const int Sp = S + 1;  // ctc_dir_kernel's even row pitch
   const float* pa = wsa_all + (size_t)b * T * Sp;
   const float* pb = wsb_all + (size_t)b * T * Sp;
   const float* ba = wsabase_all + (size_t)b * T * 32;
   const float* bb = wsbase_all + (size_t)b * T * 32;
   const double Z2 = logz[b] * 1.4426950408889634;  // offsets and bases are log2 units
-  // the warp's next frame (both offsets and the two bases of each 64-state group) is loaded into
-  // registers while the current one is reduced; the posterior of state e = 32 u + lane is
-  // exp2(alpha + beta - Z): bases and Z combined in fp64, the offsets added in fp32.
-  // Lane g loads the two bases of 64-state group g (one coalesced load each) and forms that
-  // group's fp64 combination once; the state loop takes it by shuffle.
-  float xa[kRowRegs], xb[kRowRegs], ca, cb;
+  // the warp's next frame is loaded into registers while the current one is reduced: lane l
+  // holds the (blank, label) state pairs j = l + 32 u of both offset rows as float2 (the
+  // direction kernel's pair layout); pair j's base group is j >> 5 = u.  Lane g loads the two
+  // bases of group g and forms their fp64 combination with Z once; the pair loop shuffles it.
+  constexpr int kPR = (kRowRegs + 1) / 2;  // pairs per lane
+  float2 xa[kPR], xb[kPR];
+  float ca, cb;
   auto fetch = [&](int t) {
-    const float* sa = pa + (size_t)t * Sp;
-    const float* sb = pb + (size_t)t * Sp;
+    const float2* sa = reinterpret_cast<const float2*>(pa + (size_t)t * Sp);
+    const float2* sb = reinterpret_cast<const float2*>(pb + (size_t)t * Sp);
 #pragma unroll
-    for (int u = 0; u < kRowRegs; ++u) {
-      const int e = lane + 32 * u;
-      if (e < S) {
-        xa[u] = sa[e];
-        xb[u] = sb[e];
+    for (int u = 0; u < kPR; ++u) {
+      const int j = lane + 32 * u;
+      if (j <= L) {
+        xa[u] = sa[j];
+        xb[u] = sb[j];
       }
     }
     ca = ba[(size_t)t * 32 + lane];
@@ -493,21 +494,22 @@ __global__ void __launch_bounds__(kMargWarps * 32) ctc_marg_kernel(
   };
   if (t0 + warp < t1) fetch(t0 + warp);
   for (int t = t0 + warp; t < t1; t += kMargWarps) {
-    const float cl = (float)((double)ca + (double)cb - Z2);  // 64-state group `lane` (>= ceil(S/64) unused)
-    // blank: the even states are exactly the even lanes' (e = lane + 32 u keeps the lane's parity)
-    float bl = 0.f;
+    const float cl = (float)((double)ca + (double)cb - Z2);  // base group `lane` (>= ceil((L+1)/32) unused)
+    float bl = 0.f;  // blank: the even state of every pair
 #pragma unroll
-    for (int u = 0; u < kRowRegs; ++u) {
-      const int e = lane + 32 * u;
-      const float c = __shfl_sync(0xffffffffu, cl, u >> 1);
-      if (e < S) {
-        const float p = ex2(c + xa[u] + xb[u]);  // an -inf offset gives ex2(-inf) = +0 (no +inf offsets)
-        prow[e] = p;
-        bl += p;
+    for (int u = 0; u < kPR; ++u) {
+      const int j = lane + 32 * u;
+      const float c = __shfl_sync(0xffffffffu, cl, u);
+      if (j <= L) {
+        // an -inf offset gives ex2(-inf) = +0 (no +inf offsets); state 2L+1 does not exist
+        const float p0 = ex2(c + xa[u].x + xb[u].x);
+        const float p1 = (j < L) ? ex2(c + xa[u].y + xb[u].y) : 0.f;
+        *reinterpret_cast<float2*>(prow + 2 * j) = make_float2(p0, p1);
+        bl += p0;
       }
     }
     if (t + kMargWarps < t1) fetch(t + kMargWarps);
-    bl = warp_sum((lane & 1) ? 0.f : bl);
+    bl = warp_sum(bl);
     __syncwarp();
     float* mrow = mg + (size_t)t * V;
     if constexpr (kVR > 0) {
@@ -610,7 +612,7 @@ int ctc_launch(const float* fp, const int32_t* tg, int64_t B, int T, int V, int 
   SDB_CHECK_LAUNCH();
   if (kMode == 1) {
     const int S2 = 2 * L + 1;
-    const size_t msmem = (((size_t)(V + 1 + L) + 3) & ~(size_t)3) * 4 + (size_t)kMargWarps * S2 * 4;
+    const size_t msmem = (((size_t)(V + 1 + L) + 3) & ~(size_t)3) * 4 + (size_t)kMargWarps * (S2 + 1) * 4;
     dim3 g((unsigned)((T + kMargFrames - 1) / kMargFrames), (unsigned)B);
     const int rr = (S2 + 31) / 32;
     const bool vr = V <= 128;
