@@ -192,3 +192,19 @@ def test_run_host_batch_matches_device_call():
     K.run_host_batch(lambda t: K.nw_fb(t)[:2], host_in, host_out, torch.device("cuda", 0), chunks=[5, 4, 2])
     torch.cuda.synchronize()
     assert torch.equal(host_out[0], lz.cpu()) and torch.equal(host_out[1], mg.cpu())
+
+
+@pytest.mark.parametrize("scale,exact", [(25.0, False), (400.0, True)])
+def test_alignment_large_magnitudes(scale, exact):
+    """Move log-potentials scaled to |theta| ~ 25 nats (|log Z| ~ 1e4) through the
+    meet-in-the-middle kernel: integer offsets keep fp32 at the parity bar.  Per-step
+    rounding grows like |theta| 2^-24; at ~400 nats float64 potentials take the exact
+    kernels."""
+    need_gpu()
+    th = (batch_alignment(2100, 2, 200, 64) * scale).astype(np.float32).astype(np.float64)
+    x = torch.as_tensor(th, dtype=torch.float64 if exact else torch.float32, device="cuda")
+    logz, marg, st = K.nw_fb(x)
+    for b in range(2):
+        z, mg = O.nw_marginals(th[b])
+        np.testing.assert_allclose(logz[b].item(), z, rtol=RTOL)
+        np.testing.assert_allclose(marg[b].cpu().numpy(), mg, rtol=RTOL, atol=ATOL)

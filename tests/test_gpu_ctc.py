@@ -76,3 +76,22 @@ def test_ctc_status():
     fp[2, 0, 1] = np.nan
     logz, _, st = K.ctc_fb(dev(fp), dev(tg, torch.int32))
     assert st.cpu().tolist() == [0, 1, 2]
+
+
+@pytest.mark.parametrize("scale,exact", [(25.0, False), (400.0, True)])
+def test_ctc_large_magnitudes(scale, exact):
+    """Emission log-potentials scaled to |theta| ~ 25 nats per frame (|log Z| ~ 1e4): the
+    fp32 (value, integer offset) recursion keeps the parity bar, every stored value being
+    renormalised to |v| <= 1/2 around an exact integer offset.  Its per-step rounding grows
+    like |theta| 2^-24, so at |theta| ~ 400 nats over 300 frames (|log Z| ~ 2e5) fp32
+    drifts past 1e-4 and float64 potentials take the exact kernels instead."""
+    need_gpu()
+    fp, tg = batch_ctc(2000, 3, 300, 40, 60)
+    fp = (fp * scale).astype(np.float32).astype(np.float64)  # the oracle sees the kernel's inputs
+    x = torch.as_tensor(fp, dtype=torch.float64 if exact else torch.float32, device="cuda")
+    logz, marg, st = K.ctc_fb(x, dev(tg, torch.int32))
+    z, mg = O.ctc_marginals(fp, tg)
+    ok = ~np.isneginf(z)
+    assert ok.any()
+    np.testing.assert_allclose(logz.cpu().numpy()[ok], z[ok], rtol=RTOL)
+    np.testing.assert_allclose(marg.cpu().numpy(), mg, rtol=RTOL, atol=ATOL)
