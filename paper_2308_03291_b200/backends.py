@@ -45,12 +45,32 @@ def pot_dtype():
     return torch.float64 if EXACT else torch.float32
 
 
+# dist._run's magnitude probe: while armed, to_dev records each uploaded tensor's largest
+# finite |x| as a device scalar (read once, after the call's results are back on the host)
+_PROBE = None
+
+
+def track_magnitude(on: bool):
+    global _PROBE
+    _PROBE = [] if on else None
+
+
+def tracked_max() -> float:
+    if not _PROBE:
+        return 0.0
+    return float(torch.stack(_PROBE).max().item())
+
+
 def to_dev(arrs, dtype=torch.float32):
     """Stack host arrays -> one pinned host tensor -> one async H2D copy."""
     host = torch.from_numpy(np.ascontiguousarray(np.stack(arrs))).to(dtype)
     if host.numel() and torch.cuda.is_available():
         host = host.pin_memory()
-    return host.to(_device(), non_blocking=True)
+    t = host.to(_device(), non_blocking=True)
+    if _PROBE is not None and t.numel() and t.is_floating_point():
+        _PROBE.append(torch.where(torch.isfinite(t), t.abs(), torch.zeros((), dtype=t.dtype, device=t.device))
+                      .max().to(torch.float64))
+    return t
 
 
 def to_host(t):

@@ -33,6 +33,43 @@ def _reject_one_to_one(dist):
         raise UnsupportedInference(ONE_TO_ONE_REASON)
 
 
+# fp32 kernels round a term of size |theta| every step: past this many nats
+# per potential a call takes the exact fp64 kernels automatically, so the drop-in keeps
+# the reference's results at any magnitude (the batched fp32 device entry points in
+# kernels.py stay fp32: their caller chose the dtype)
+AUTO_EXACT_NATS = 40.0
+
+
+def _large(group) -> bool:
+    """Host-side version of the probe (ragged chain grouping decides before any upload)."""
+    for d in group:
+        for x in d.potentials().values():
+            a = np.asarray(x, dtype=np.float64)
+            if a.size and np.nanmax(np.abs(np.where(np.isfinite(a), a, 0.0))) > AUTO_EXACT_NATS:
+                return True
+    return False
+
+
+def _run(be, group, **kw):
+    """be.run(group, **kw); rerun in the exact mode when the uploaded potentials turn out
+    large (a device-side max over the inputs, read after the results: no host pass)."""
+    if backends.EXACT:
+        return be.run(group, **kw)
+    backends.track_magnitude(True)
+    try:
+        res = be.run(group, **kw)
+        big = backends.tracked_max() > AUTO_EXACT_NATS
+    finally:
+        backends.track_magnitude(False)
+    if not big:
+        return res
+    backends.EXACT = True
+    try:
+        return be.run(group, **kw)
+    finally:
+        backends.EXACT = False
+
+
 def _backend(dist):
     _reject_one_to_one(dist)
     be = backends.for_dist(dist)
@@ -47,7 +84,7 @@ def _backend(dist):
 def log_partition_info(dist) -> tuple[float, str]:
     """dist.py:68-84."""
     be = _backend(dist)
-    res = be.run([dist], marginals=False)
+    res = _run(be, [dist], marginals=False)
     return float(res.logz[0]), be.algo(dist)
 
 
@@ -61,7 +98,7 @@ def log_partition(dist) -> float:
 def potential_marginals(dist) -> dict[str, np.ndarray]:
     """dist.py:96-117: gradient of log Z w.r.t. every potential tensor."""
     be = _backend(dist)
-    res = be.run([dist], marginals=True, full=True)
+    res = _run(be, [dist], marginals=True, full=True)
     res.raise_vacuous(0)
     return res.marg[0]
 
@@ -69,7 +106,7 @@ def potential_marginals(dist) -> dict[str, np.ndarray]:
 def marginals_info(dist) -> tuple[dict[str, np.ndarray], str]:
     """dist.py:120-129 (one GPU call; no redundant log-partition pass)."""
     be = _backend(dist)
-    res = be.run([dist], marginals=True)
+    res = _run(be, [dist], marginals=True)
     res.raise_vacuous(0)
     return res.public_marg(0), be.algo(dist)
 
@@ -154,7 +191,7 @@ def _expected_scores_device(be, ps, qs):
     full marginals (potential_marginals, dist.py:96-117) stay on the device
     and one masked-dot reduction per potential tensor (kernels.expected_score)
     returns B doubles (-inf where a marked part of p is -inf under q)."""
-    res = be.run(ps, marginals=True, full=True, dev=True)
+    res = _run(be, ps, marginals=True, full=True, dev=True)
     for i in range(len(ps)):
         res.raise_vacuous(i)
     dev = next(iter(res.dev.values())).device
@@ -329,16 +366,16 @@ def _unpad_result(name, d, padded, r):
 
 
 def _b_logz(be, group):
-    return [float(z) for z in be.run(group, marginals=False).logz]
+    return [float(z) for z in _run(be, group, marginals=False).logz]
 
 
 def _b_logz_info(be, group):
-    res = be.run(group, marginals=False)
+    res = _run(be, group, marginals=False)
     return [(float(z), be.algo(d)) for z, d in zip(res.logz, group)]
 
 
 def _b_marg(be, group):
-    res = be.run(group, marginals=True)
+    res = _run(be, group, marginals=True)
     out = []
     for i in range(len(group)):
         res.raise_vacuous(i)
@@ -368,7 +405,7 @@ def _b_entropy_info(be, group):
     """entropy over a same-shape group: ONE marginal launch, ONE fused
     expected-score reduction, ONE log-partition launch (dist.py:338-339)."""
     expected = _expected_scores_device(be, group, group)
-    logz = be.run(group, marginals=False).logz
+    logz = _run(be, group, marginals=False).logz
     return [(float("inf") if e == NEG_INF else float(z) - e, be.algo(d)) for e, z, d in zip(expected, logz, group)]
 
 

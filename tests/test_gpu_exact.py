@@ -132,3 +132,30 @@ def test_exact_entropy_and_statuses():
     assert sd.log_partition(make_dist(sd, "chain", bad)) == -np.inf
     with pytest.raises(sd.VacuousDistribution):
         sd.marginals(make_dist(sd, "chain", bad))
+
+
+@pytest.mark.parametrize("family,dims", [("alignment", dict(n=40, m=30)), ("ctc", dict(T=60, V=8, L=10)),
+                                         ("chain", dict(n=50, m=6))])
+def test_auto_exact_large_magnitudes(family, dims):
+    """fp32 mode (the default), potentials ~400 nats: the API routes the call to the exact
+    kernels by itself (dist.AUTO_EXACT_NATS), so the results keep the reference's
+    tolerances where the fp32 kernels would drift past 1e-4."""
+    need_gpu()
+    sd.set_precision("fp32")
+    inp = family_inputs(family, 19, dims)
+    inp = {k: (np.asarray(v) * 400.0 if np.asarray(v).dtype.kind == "f" else v) for k, v in inp.items()}
+    d = make_dist(sd, family, inp)
+    if family == "alignment":
+        z, mg = O.nw_marginals(inp["move_potentials"])
+        key = "move_potentials"
+    elif family == "ctc":
+        z, mg = O.ctc_marginals(inp["frame_potentials"][None], np.asarray(inp["target"])[None])
+        z, mg = z[0], mg[0]
+        key = "frame_potentials"
+    else:
+        z, pi, pt = O.chain_marginals(inp["init"][None], inp["transitions"][None])
+        z, mg = z[0], pt[0]
+        key = "transitions"
+    _close(sd.log_partition(d), z)
+    _close(sd.marginals(d)[key], mg)
+    assert sd.get_precision() == "fp32"  # the switch is scoped to the call

@@ -62,3 +62,17 @@ def test_refshim_restores_precision():
     assert sd.get_precision() == "fp64"
     undo()
     assert sd.get_precision() == "fp32" and fake.chain.chain_marginals is None
+
+
+def test_auto_exact_detection():
+    """dist._large: potentials past AUTO_EXACT_NATS (finite entries only) send a call to the
+    exact kernels; -inf structure zeros do not."""
+    from paper_2308_03291_b200 import dist as gd
+
+    small = sd.LinearChainCRF(np.zeros(3), np.full((2, 3, 3), -5.0))
+    th = np.full((2, 3, 3), -np.inf)
+    th[:, 0, 0] = 1.0
+    masked = sd.LinearChainCRF(np.zeros(3), th)
+    big = sd.LinearChainCRF(np.zeros(3), np.full((2, 3, 3), -2.0 * gd.AUTO_EXACT_NATS))
+    assert not gd._large([small]) and not gd._large([masked])
+    assert gd._large([small, big])
