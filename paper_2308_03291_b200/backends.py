@@ -119,10 +119,12 @@ class ArgmaxResult:
     def score_of(self, i, dist, ind):
         # exact mode: the indicator's score over the float64 potentials (dist.py:162),
         # not the kernel's sum over their fp32 rounding
-        if self._score is not None and (self._score_exact or not EXACT):
-            return float(self._score[i])
-        from .dist import structure_score
+        from .dist import _tiny, structure_score
 
+        # tiny instances score over the float64 potentials as in the exact mode
+        # (dist.AUTO_EXACT_SIZE)
+        if self._score is not None and (self._score_exact or not (EXACT or _tiny([dist]))):
+            return float(self._score[i])
         return structure_score(dist, ind)
 
 

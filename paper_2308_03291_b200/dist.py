@@ -38,6 +38,14 @@ def _reject_one_to_one(dist):
 # the reference's results at any magnitude (the batched fp32 device entry points in
 # kernels.py stay fp32: their caller chose the dtype)
 AUTO_EXACT_NATS = 40.0
+# ... and instances this small (potential entries per instance) run exactly as well: the
+# fp32 kernels exist for throughput on large batched problems; a tiny problem costs the
+# same either way and then matches the reference at its own tolerances
+AUTO_EXACT_SIZE = 4096
+
+
+def _tiny(group) -> bool:
+    return all(sum(np.size(x) for x in d.potentials().values()) <= AUTO_EXACT_SIZE for d in group)
 
 
 def _large(group) -> bool:
@@ -50,11 +58,28 @@ def _large(group) -> bool:
     return False
 
 
+def _argmax(be, group):
+    """be.argmax(group); tiny groups in the exact mode (scores over the float64 potentials)."""
+    if backends.EXACT or not _tiny(group):
+        return be.argmax(group)
+    backends.EXACT = True
+    try:
+        return be.argmax(group)
+    finally:
+        backends.EXACT = False
+
+
 def _run(be, group, **kw):
     """be.run(group, **kw); rerun in the exact mode when the uploaded potentials turn out
     large (a device-side max over the inputs, read after the results: no host pass)."""
     if backends.EXACT:
         return be.run(group, **kw)
+    if _tiny(group):
+        backends.EXACT = True
+        try:
+            return be.run(group, **kw)
+        finally:
+            backends.EXACT = False
     backends.track_magnitude(True)
     try:
         res = be.run(group, **kw)
@@ -147,7 +172,7 @@ def argmax_info(dist):
     if isinstance(dist, OneToOneMatching):
         raise UnsupportedInference("one-to-one argmax (Jonker-Volgenant) is outside the GPU hot path")
     be = _backend(dist)
-    res = be.argmax([dist])
+    res = _argmax(be, [dist])
     res.raise_vacuous(0)
     ind = res.indicator(0)
     score = res.score_of(0, dist, ind)
@@ -388,7 +413,7 @@ def _b_marg_info(be, group):
 
 
 def _b_argmax_info(be, group):
-    res = be.argmax(group)
+    res = _argmax(be, group)
     out = []
     for i, d in enumerate(group):
         res.raise_vacuous(i)

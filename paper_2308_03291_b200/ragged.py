@@ -208,9 +208,9 @@ def native_ragged(ds) -> bool:
 
     if backends.EXACT:  # the exact-mode chain kernel takes same-length groups (padded instead)
         return False
-    from .dist import _large
+    from .dist import _large, _tiny
 
-    if _large(ds):  # such a group runs in the exact mode (dist._run): padded as well
+    if _large(ds) or _tiny(ds):  # such a group runs in the exact mode (dist._run): padded as well
         return False
 
     return chain_ragged_supported(max(d.n for d in ds), ds[0].m)

@@ -105,7 +105,8 @@ def test_ragged_chain_native_lengths():
     from paper_2308_03291_b200 import kernels as K
     from paper_2308_03291_b200 import ragged as rg
 
-    dists = [sd.LinearChainCRF(*chain(70 + s, n, 5)) for s, n in enumerate([3, 40, 17, 1, 64, 2])]
+    # m = 12: not every instance is below dist.AUTO_EXACT_SIZE, so the group stays on the fp32 ragged kernels
+    dists = [sd.LinearChainCRF(*chain(70 + s, n, 12)) for s, n in enumerate([3, 40, 17, 1, 64, 2])]
     assert rg.native_ragged(dists)
     _check(dists)
     am = sd.batch_map(sd.argmax_info, dists)
@@ -116,7 +117,7 @@ def test_ragged_chain_native_lengths():
         assert score == score0 and algo == algo0
     # raw kernel contract: zeros past the length
     init = torch.stack([torch.as_tensor(d.init, dtype=torch.float32) for d in dists]).cuda()
-    tr = torch.zeros(len(dists), 63, 5, 5)
+    tr = torch.zeros(len(dists), 63, 12, 12)
     for i, d in enumerate(dists):
         tr[i, : d.n - 1] = torch.as_tensor(d.transitions, dtype=torch.float32)
     lens = torch.tensor([d.n for d in dists], dtype=torch.int32).cuda()
