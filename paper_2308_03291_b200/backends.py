@@ -10,6 +10,9 @@ indicators).
 
 from __future__ import annotations
 
+import contextlib
+import threading
+
 import numpy as np
 import torch
 
@@ -39,26 +42,41 @@ def _device():
 # out, like the reference); argmax and sampling keep their fp32-input kernels
 # (their arithmetic is fp64 already).
 EXACT = False
+# per-thread scoped override (dist._run / dist._argmax route a call to the exact kernels
+# without touching the process default) and the per-thread magnitude probe
+_TL = threading.local()
+
+
+def exact_now() -> bool:
+    return EXACT or getattr(_TL, "exact", False)
+
+
+@contextlib.contextmanager
+def exact_scope():
+    prev = getattr(_TL, "exact", False)
+    _TL.exact = True
+    try:
+        yield
+    finally:
+        _TL.exact = prev
 
 
 def pot_dtype():
-    return torch.float64 if EXACT else torch.float32
+    return torch.float64 if exact_now() else torch.float32
 
 
-# dist._run's magnitude probe: while armed, to_dev records each uploaded tensor's largest
-# finite |x| as a device scalar (read once, after the call's results are back on the host)
-_PROBE = None
-
-
+# dist._run's magnitude probe: while armed (per thread), to_dev records each uploaded
+# tensor's largest finite |x| as a device scalar (read once, after the call's results are
+# back on the host)
 def track_magnitude(on: bool):
-    global _PROBE
-    _PROBE = [] if on else None
+    _TL.probe = [] if on else None
 
 
 def tracked_max() -> float:
-    if not _PROBE:
+    pr = getattr(_TL, "probe", None)
+    if not pr:
         return 0.0
-    return float(torch.stack(_PROBE).max().item())
+    return float(torch.stack(pr).max().item())
 
 
 def to_dev(arrs, dtype=torch.float32):
@@ -67,8 +85,9 @@ def to_dev(arrs, dtype=torch.float32):
     if host.numel() and torch.cuda.is_available():
         host = host.pin_memory()
     t = host.to(_device(), non_blocking=True)
-    if _PROBE is not None and t.numel() and t.is_floating_point():
-        _PROBE.append(torch.where(torch.isfinite(t), t.abs(), torch.zeros((), dtype=t.dtype, device=t.device))
+    pr = getattr(_TL, "probe", None)
+    if pr is not None and t.numel() and t.is_floating_point():
+        pr.append(torch.where(torch.isfinite(t), t.abs(), torch.zeros((), dtype=t.dtype, device=t.device))
                       .max().to(torch.float64))
     return t
 
@@ -123,7 +142,7 @@ class ArgmaxResult:
 
         # tiny instances score over the float64 potentials as in the exact mode
         # (dist.AUTO_EXACT_SIZE)
-        if self._score is not None and (self._score_exact or not (EXACT or _tiny([dist]))):
+        if self._score is not None and (self._score_exact or not (exact_now() or _tiny([dist]))):
             return float(self._score[i])
         return structure_score(dist, ind)
 

@@ -60,26 +60,21 @@ def _large(group) -> bool:
 
 def _argmax(be, group):
     """be.argmax(group); tiny groups in the exact mode (scores over the float64 potentials)."""
-    if backends.EXACT or not _tiny(group):
+    if backends.exact_now() or not _tiny(group):
         return be.argmax(group)
-    backends.EXACT = True
-    try:
+    with backends.exact_scope():
         return be.argmax(group)
-    finally:
-        backends.EXACT = False
 
 
 def _run(be, group, **kw):
-    """be.run(group, **kw); rerun in the exact mode when the uploaded potentials turn out
-    large (a device-side max over the inputs, read after the results: no host pass)."""
-    if backends.EXACT:
+    """be.run(group, **kw); tiny groups in the exact mode, and a rerun in the exact mode
+    when the uploaded potentials turn out large (a device-side max over the inputs, read
+    after the results: no host pass).  The switch is scoped to this call and thread."""
+    if backends.exact_now():
         return be.run(group, **kw)
     if _tiny(group):
-        backends.EXACT = True
-        try:
+        with backends.exact_scope():
             return be.run(group, **kw)
-        finally:
-            backends.EXACT = False
     backends.track_magnitude(True)
     try:
         res = be.run(group, **kw)
@@ -88,11 +83,8 @@ def _run(be, group, **kw):
         backends.track_magnitude(False)
     if not big:
         return res
-    backends.EXACT = True
-    try:
+    with backends.exact_scope():
         return be.run(group, **kw)
-    finally:
-        backends.EXACT = False
 
 
 def _backend(dist):

@@ -206,7 +206,7 @@ def native_ragged(ds) -> bool:
     from . import backends
     from .kernels import chain_ragged_supported
 
-    if backends.EXACT:  # the exact-mode chain kernel takes same-length groups (padded instead)
+    if backends.exact_now():  # the exact-mode chain kernel takes same-length groups (padded instead)
         return False
     from .dist import _large, _tiny
 
