@@ -76,3 +76,21 @@ def test_auto_exact_detection():
     big = sd.LinearChainCRF(np.zeros(3), np.full((2, 3, 3), -2.0 * gd.AUTO_EXACT_NATS))
     assert not gd._large([small]) and not gd._large([masked])
     assert gd._large([small, big])
+
+
+def test_exact_scope_is_per_thread():
+    """dist._run / _argmax switch to the exact kernels through a per-thread scope: another
+    thread (and the process default) keeps its precision."""
+    import threading
+
+    seen = {}
+
+    def other():
+        seen["other"] = backends.exact_now()
+
+    with backends.exact_scope():
+        assert backends.exact_now() and sd.get_precision() == "fp32"
+        t = threading.Thread(target=other)
+        t.start()
+        t.join()
+    assert seen["other"] is False and not backends.exact_now()
